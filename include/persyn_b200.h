@@ -1,0 +1,258 @@
+/*
+ * persyn_b200.h — C ABI of the B200-native EM hot path of persyn
+ * (perspective texture synthesis by energy optimisation, arXiv 2006.11851).
+ *
+ * This is the drop-in boundary for the reference's hot path.  Each entry
+ * point names the reference interface it replaces (paths relative to
+ * /root/reference/proj/core).  The reference is C++ with a per-query virtual
+ * plug-in (SearchIndex::nearest, include/persyn/optimizer.hpp:111-119); a GPU
+ * is fed at batch granularity, so the boundary sits at the reference's batch
+ * entry points (search_step / update_step / optimize_level / synthesize) and a
+ * batched SearchIndex::nearest.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no C++ or torch types cross the ABI.
+ *  - HOST pointers unless a name ends in `_dev` (device-resident variants used
+ *    by the benchmark; they take CUDA device pointers).
+ *  - Images are planar fp64, planes [C][H][W], row-major, row 0 = bottom
+ *    (include/persyn/image.hpp:11-12,57-59).  C = 3 + G: R, G, B then G >= 1
+ *    guidance planes (the reference hard-codes G = 1, image.hpp:70; G = 2 is
+ *    the cfg-3 extension).
+ *  - Neighbourhood vectors are fp32, pixel-major (dy, dx), channel-minor
+ *    (src/neighborhood.cpp:128-135).  D = w * w * C.
+ *  - Caller owns every host array; handles own device memory; results are
+ *    copied into caller buffers.
+ *  - Errors: every call returns psg_status; psg_last_error() returns the
+ *    thread-local message of the last failure.  No exception crosses the ABI.
+ *    The mapping mirrors include/persyn/errors.hpp:8-36 and the reference's
+ *    std::logic_error invariants (src/optimizer.cpp:342-346,390-392).
+ *  - Arithmetic: fp64 with separate multiply and add in the reference's index
+ *    order; fp32 features = (float) of fp64 state.  NN results in exact mode
+ *    are bit-identical to the reference's KmTree exact query / brute force.
+ *  - No CPU fallback: without a usable sm_100 device psg_ctx_create fails
+ *    with PSG_E_CUDA.
+ */
+#ifndef PERSYN_B200_H
+#define PERSYN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSG_ABI_VERSION 1
+
+typedef enum {
+  PSG_OK = 0,
+  PSG_E_DOMAIN = 1, /* persyn::DomainError (errors.hpp:33-36)            */
+  PSG_E_SHAPE = 2,  /* persyn::ShapeError  (errors.hpp:26-30)            */
+  PSG_E_LOGIC = 3,  /* std::logic_error    (optimizer.cpp:344,391)       */
+  PSG_E_IO = 4,     /* persyn::IoError     (errors.hpp:14-18)            */
+  PSG_E_FORMAT = 5, /* persyn::FormatError (errors.hpp:20-24)            */
+  PSG_E_CUDA = 6,   /* CUDA runtime / driver / library failure           */
+  PSG_E_NCCL = 7    /* NCCL failure (multi-GPU row sharding)             */
+} psg_status;
+
+/* QueryBudget (include/persyn/km_tree.hpp:13-25). */
+typedef enum { PSG_GREEDY = 0, PSG_BACKTRACK = 1, PSG_EXACT = 2 } psg_mode;
+typedef struct {
+  int mode;       /* psg_mode */
+  int max_leaves; /* backtrack only, >= 1 */
+} psg_budget;
+
+/* Per-stage index build parameters (PcaTreeIndex ctor, optimizer.cpp:216-224,
+ * extended with the BASELINE configs' d cap and tree depth). */
+typedef struct {
+  double variance_target; /* fit_pca target in (0,1] (pca.cpp:79-87)          */
+  int d_cap;              /* 0 = no cap; else retained dim <= d_cap           */
+  int d_fixed;            /* 0 = variance rule; else exactly d_fixed comps    */
+  int branching;          /* k-means tree branching b >= 2                    */
+  int max_depth;          /* 0 = until leaves < leaf_threshold; else cap      */
+  int leaf_threshold;     /* 0 = branching (optimizer.cpp:223)                */
+  uint64_t seed;          /* tree seed (pipeline.cpp:54-56 level_seed)        */
+  int hist_bins;          /* exemplar histogram bins, 0 = none                */
+  int hist_include_scale; /* histogram over guidance planes too               */
+} psg_index_cfg;
+
+/* OptimizerConfig (include/persyn/optimizer.hpp:37-52). */
+typedef struct {
+  double robust_exponent;      /* r in (0,2), default 0.8            */
+  double distance_epsilon;     /* > 0, default 1e-4                  */
+  int max_iterations;          /* >= 1                               */
+  int min_iterations;          /* in [1, max_iterations]             */
+  double convergence_fraction; /* in (0,1)                           */
+  int histogram_bins;          /* >= 2                               */
+  int histogram_matching;      /* bool                               */
+  int histogram_include_scale; /* bool                               */
+  int spacing;                 /* anchor lattice step (GridSpec)     */
+  int patch_width;             /* PatchSpec, <= spacing              */
+  psg_budget budget;
+} psg_opt_cfg;
+
+/* IterationStats (include/persyn/optimizer.hpp:153-163). */
+typedef struct {
+  int iteration;
+  double energy;
+  int64_t changed;
+  int64_t nn_calls;
+  double millis;
+  double lsq_energy_before;
+  double lsq_energy_after;
+  int64_t points_scanned;   /* sum over the reference's query plan */
+  int64_t unique_queries;   /* anchors actually searched on device */
+} psg_iter_stats;
+
+typedef struct psg_ctx psg_ctx;
+typedef struct psg_index psg_index;
+typedef struct psg_level psg_level;
+
+/* ---- context ------------------------------------------------------------ */
+const char* psg_last_error(void);
+int psg_abi_version(void);
+/* stream: a cudaStream_t (NULL = the context creates its own). */
+psg_status psg_ctx_create(int device, void* stream, psg_ctx** out);
+void psg_ctx_destroy(psg_ctx* ctx);
+psg_status psg_ctx_synchronize(psg_ctx* ctx);
+/* Number of kernel launches issued by this context so far. */
+int64_t psg_ctx_launch_count(const psg_ctx* ctx);
+
+/* ---- search index (SearchIndex plug-in, optimizer.hpp:111-129) ----------- */
+/*
+ * Replaces make_pca_tree_index(extract_all(exemplar, {w,1,..}), variance,
+ * branching, seed) (optimizer.cpp:256-262, pipeline.cpp:276-284).  The dense
+ * database is never materialised: windows are gathered from the exemplar on
+ * device.  mean/basis: optional injected PCA model (PcaModel ctor,
+ * pca.hpp:18-19) — mean[D], basis[d][D] row-major; NULL = fit on device.
+ */
+psg_status psg_index_create(psg_ctx* ctx, const double* ex_planes, int C, int ew, int eh, int w,
+                            const double* mean, const double* basis, int d,
+                            const psg_index_cfg* cfg, psg_index** out);
+/* Same over an explicit fp32 vector set X[n][D] (search-only workloads). */
+psg_status psg_index_create_vectors(psg_ctx* ctx, const float* X, int64_t n, int D,
+                                    const double* mean, const double* basis, int d,
+                                    const psg_index_cfg* cfg, psg_index** out);
+void psg_index_destroy(psg_index* index);
+/* dims: {N, D, d, C, w, ew, eh, n_nodes, n_leaves, max_depth_built} */
+psg_status psg_index_info(const psg_index* index, int64_t dims[10]);
+/* PcaModel accessors (pca.hpp:21-31): mean[D], basis[d][D], variances[D]. */
+psg_status psg_index_pca(const psg_index* index, double* mean, double* basis, double* variances);
+/* ProjectedMatrix of the database (pca.cpp:103-113), [N][d] row-major. */
+psg_status psg_index_projected(const psg_index* index, double* out);
+/* Leaves in tree order (KmTree::leaves, km_tree.cpp:286-298). */
+psg_status psg_index_leaves(const psg_index* index, int32_t* ids, int32_t* sizes,
+                            int64_t* n_leaves);
+/* Exemplar histogram [slots][bins] (pipeline.cpp:379-385). */
+psg_status psg_index_histograms(const psg_index* index, double* mass);
+/*
+ * Batched SearchIndex::nearest (PcaTreeIndex::nearest, optimizer.cpp:226-236):
+ * project -> tree query -> full-D rescoring.  Q[nq][D] fp32.
+ * dist_pca (optional): sqrt of the PCA-space dist^2 of the winner (what
+ * KmTree::query returns before PcaTreeIndex replaces it).
+ */
+psg_status psg_index_query(psg_ctx* ctx, const psg_index* index, const float* Q, int64_t nq,
+                           psg_budget budget, int32_t* idx, double* dist, double* dist_pca,
+                           int64_t* scanned);
+
+/* ---- EM hot path --------------------------------------------------------- */
+/*
+ * search_step (optimizer.hpp:141-143, optimizer.cpp:275-348).  out_planes is
+ * the W x H current image (C planes, C = index C).  idx/dist: A = nx*ny
+ * anchors in ascending id.  nn_calls = the reference's plan size
+ * (optimizer.cpp:333); scanned = points scanned summed over the plan.
+ */
+psg_status psg_search_step(psg_ctx* ctx, const psg_index* index, const double* out_planes, int W,
+                           int H, int spacing, int patch_width, psg_budget budget, int32_t* idx,
+                           double* dist, int64_t* nn_calls, int64_t* scanned);
+/*
+ * update_step (optimizer.hpp:149-151, optimizer.cpp:350-401) with
+ * WeightMap{irls, hist_penalty} (optimizer.hpp:27-35).  Writes the new image.
+ */
+psg_status psg_update_step(psg_ctx* ctx, const psg_index* index, const int32_t* idx,
+                           const double* irls, const double* pen, int W, int H, int spacing,
+                           double* out_planes);
+/*
+ * optimize_level (optimizer.hpp:181-183, optimizer.cpp:426-516).
+ * ex_hist: optional exemplar histogram [slots][bins]; NULL with
+ * cfg->histogram_matching uses the index's own exemplar histogram.
+ * stats: array of cfg->max_iterations entries (may be NULL).
+ */
+psg_status psg_optimize_level(psg_ctx* ctx, const psg_index* index, const double* init, int W,
+                              int H, const psg_opt_cfg* cfg, const double* ex_hist,
+                              double* out_planes, psg_iter_stats* stats, int* n_iters);
+
+/* ---- device-resident level (benchmark / driver internals) ---------------- */
+psg_status psg_level_create(psg_ctx* ctx, const psg_index* index, const double* init, int W,
+                            int H, const psg_opt_cfg* cfg, const double* ex_hist,
+                            psg_level** out);
+/* Priming search (optimize_level's first search_step, optimizer.cpp:444-448). */
+psg_status psg_level_prime(psg_level* level);
+/* Run up to n EM iterations; stops early on the reference's convergence rule
+ * only when honor_convergence != 0.  Appends stats. */
+psg_status psg_level_iterate(psg_level* level, int n, int honor_convergence,
+                             psg_iter_stats* stats, int* n_done);
+psg_status psg_level_download(psg_level* level, double* planes, int32_t* idx, double* dist);
+/* Device pointers of the level's fp64 state planes (for device-side checks). */
+psg_status psg_level_state_dev(psg_level* level, void** planes_dev, void** idx_dev,
+                               void** dist_dev);
+void psg_level_destroy(psg_level* level);
+
+/* ---- pyramid driver (synthesize, pipeline.hpp:69, pipeline.cpp:216-315) --- */
+typedef struct {
+  int n_sizes;
+  int sizes[4]; /* neighbourhood widths per level, coarse stages first, e.g. {32,16,8} */
+} psg_stage_list;
+
+typedef struct {
+  const double* exemplar;  /* [C][eh][ew] fp64: RGB + guidance planes */
+  int C, ew, eh;
+  const double* out_guidance; /* [C-3][H][W] guidance planes of the finest output level */
+  int out_w, out_h;
+  int levels;
+  psg_stage_list stages;   /* per-level neighbourhood sizes; spacing = w / 4 */
+  psg_opt_cfg cfg;         /* spacing ignored (w/4 per stage) */
+  psg_index_cfg index;
+  uint64_t seed;
+  int guidance_kind;       /* 0 = guidance planes are row/col ramps recomputed per level */
+} psg_request;
+
+typedef struct {
+  int level, w, W, H, ew, eh, d, iterations;
+  double final_energy;
+  int64_t nn_calls;
+  double index_millis, optimize_millis;
+} psg_stage_report;
+
+typedef struct {
+  int n_stages;
+  psg_stage_report stages[16];
+  double part1_millis, part2_millis;
+  int64_t total_nn_calls;
+  double final_energy;
+} psg_report;
+
+/* out_planes: [C][out_h][out_w] fp64 final state (RGB = the synthesized image). */
+psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, double* out_planes,
+                          psg_report* report);
+
+/* ---- geometry helpers (neighborhood.cpp) ---------------------------------- */
+/* axis_positions (neighborhood.cpp:12-18); returns count, fills out if non-NULL. */
+int psg_axis_positions(int extent, int window, int step, int* out);
+/* Plan size (nn_calls) and per-anchor multiplicity of search_step's plan
+ * (optimizer.cpp:288-296); mult may be NULL.  Returns -1 if an anchor is
+ * uncovered (the reference's logic_error, optimizer.cpp:342-346). */
+int64_t psg_plan(int W, int H, int w, int spacing, int patch_width, int32_t* mult);
+
+/* ---- numerics helpers (host; the device kernels use the same code) -------- */
+/* Correctly rounded x^y (double-double), used for the IRLS weight where the
+ * reference calls glibc pow (optimizer.cpp:114, :129). */
+double psg_pow_cr(double x, double y);
+/* The exact value of `count` sequential additions of 1/pixels starting from 0
+ * (build_histograms' mass, optimizer.cpp:76-86). */
+double psg_hist_mass(int64_t count, int64_t pixels);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PERSYN_B200_H */

@@ -1,0 +1,391 @@
+"""Python mirror of the reference's ``persyn::`` hot-path API over the C ABI.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/core/include/persyn/{optimizer,km_tree,pipeline}.hpp:
+
+* :class:`QueryBudget` (km_tree.hpp:13-25), :class:`OptimizerConfig`
+  (optimizer.hpp:37-52), :class:`IterationStats` (optimizer.hpp:153-163);
+* :func:`make_pca_tree_index` (optimizer.hpp:126-129) -> :class:`SearchIndex`
+  with a batched ``nearest`` (optimizer.hpp:111-119);
+* :func:`search_step` (optimizer.hpp:141-143), :func:`update_step`
+  (optimizer.hpp:149-151), :func:`optimize_level` (optimizer.hpp:181-183),
+  :func:`synthesize` (pipeline.hpp:69).
+
+Images are numpy float64 arrays shaped (C, H, W), row 0 = bottom.  Errors
+raise DomainError / ShapeError / LogicError like the reference.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import native as N
+from .native import DomainError, LogicError, ShapeError, CudaError, PersynError  # noqa: F401
+
+
+def _c(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+def _p(a):
+    return a.ctypes.data_as(ct.c_void_p) if a is not None else None
+
+
+# ---------------------------------------------------------------------------
+@dataclass
+class QueryBudget:
+    mode: str = "backtrack"
+    max_leaves: int = 4
+
+    @staticmethod
+    def greedy():
+        return QueryBudget("greedy", 1)
+
+    @staticmethod
+    def backtrack(max_leaves: int):
+        if max_leaves < 1:
+            raise DomainError(N.PSG_E_DOMAIN, "backtrack budget must be >= 1")
+        return QueryBudget("backtrack", max_leaves)
+
+    @staticmethod
+    def exact():
+        return QueryBudget("exact", 0)
+
+    def c(self) -> N.psg_budget:
+        m = {"greedy": N.PSG_GREEDY, "backtrack": N.PSG_BACKTRACK, "exact": N.PSG_EXACT}[self.mode]
+        return N.psg_budget(m, self.max_leaves)
+
+
+@dataclass
+class OptimizerConfig:
+    robust_exponent: float = 0.8
+    distance_epsilon: float = 1e-4
+    max_iterations: int = 20
+    min_iterations: int = 1
+    convergence_fraction: float = 0.01
+    histogram_bins: int = 16
+    histogram_matching: bool = True
+    histogram_include_scale: bool = False
+    nbhd_width: int = 8
+    spacing: int = 2
+    patch_width: int = 2
+    budget: QueryBudget = field(default_factory=lambda: QueryBudget.backtrack(4))
+
+    def c(self) -> N.psg_opt_cfg:
+        return N.psg_opt_cfg(self.robust_exponent, self.distance_epsilon, self.max_iterations,
+                             self.min_iterations, self.convergence_fraction, self.histogram_bins,
+                             int(self.histogram_matching), int(self.histogram_include_scale),
+                             self.spacing, self.patch_width, self.budget.c())
+
+
+@dataclass
+class IterationStats:
+    iteration: int
+    energy: float
+    changed: int
+    nn_calls: int
+    millis: float
+    lsq_energy_before: float
+    lsq_energy_after: float
+    points_scanned: int
+    unique_queries: int
+
+    @staticmethod
+    def of(s: N.psg_iter_stats) -> "IterationStats":
+        return IterationStats(s.iteration, s.energy, s.changed, s.nn_calls, s.millis,
+                              s.lsq_energy_before, s.lsq_energy_after, s.points_scanned,
+                              s.unique_queries)
+
+
+# ---------------------------------------------------------------------------
+class Context:
+    """One device + one CUDA stream (``stream``: a cudaStream_t int or None)."""
+
+    def __init__(self, device: int = 0, stream: Optional[int] = None):
+        h = ct.c_void_p()
+        N.check(N.lib.psg_ctx_create(device, ct.c_void_p(stream) if stream else None,
+                                     ct.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            N.lib.psg_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def synchronize(self):
+        N.check(N.lib.psg_ctx_synchronize(self.h))
+
+    @property
+    def launches(self) -> int:
+        return int(N.lib.psg_ctx_launch_count(self.h))
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+def index_cfg(variance_target=0.95, d_cap=0, d_fixed=0, branching=4, max_depth=0,
+              leaf_threshold=0, seed=0, hist_bins=0, hist_include_scale=False) -> N.psg_index_cfg:
+    return N.psg_index_cfg(variance_target, d_cap, d_fixed, branching, max_depth, leaf_threshold,
+                           seed, hist_bins, int(hist_include_scale))
+
+
+class SearchIndex:
+    """PCA + k-means tree over an exemplar's dense windows (or a vector set)."""
+
+    def __init__(self, ctx: Context, handle, keep):
+        self.ctx = ctx
+        self.h = handle
+        self._keep = keep
+        dims = np.zeros(10, np.int64)
+        N.check(N.lib.psg_index_info(self.h, _p(dims)))
+        (self.count, self.dim, self.retained_dim, self.channels, self.window, self.ew, self.eh,
+         self.n_nodes, self.n_leaves, self.depth) = (int(v) for v in dims)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            N.lib.psg_index_destroy(self.h)
+            self.h = None
+
+    # PcaModel accessors (pca.hpp:21-31)
+    def pca(self):
+        mean = np.zeros(self.dim)
+        basis = np.zeros((self.retained_dim, self.dim))
+        var = np.zeros(self.dim)
+        N.check(N.lib.psg_index_pca(self.h, _p(mean), _p(basis), _p(var)))
+        return mean, basis, var
+
+    def projected(self) -> np.ndarray:
+        out = np.zeros((self.count, self.retained_dim))
+        N.check(N.lib.psg_index_projected(self.h, _p(out)))
+        return out
+
+    def leaves(self):
+        ids = np.zeros(self.count, np.int32)
+        sizes = np.zeros(self.count, np.int32)
+        nl = ct.c_int64()
+        N.check(N.lib.psg_index_leaves(self.h, _p(ids), _p(sizes), ct.byref(nl)))
+        return ids, sizes[: nl.value].copy()
+
+    def histograms(self, slots=3, bins=16) -> np.ndarray:
+        out = np.zeros((slots, bins))
+        N.check(N.lib.psg_index_histograms(self.h, _p(out)))
+        return out
+
+    def nearest(self, Q: np.ndarray, budget: QueryBudget = QueryBudget.exact()):
+        """Batched SearchIndex::nearest: (idx, full-D dist, PCA dist, points scanned)."""
+        Q = _c(Q, np.float32)
+        if Q.ndim == 1:
+            Q = Q[None, :]
+        if Q.shape[1] != self.dim:
+            raise ShapeError(N.PSG_E_SHAPE, "query dim does not match the candidates")
+        n = Q.shape[0]
+        idx = np.zeros(n, np.int32)
+        dist = np.zeros(n)
+        dpca = np.zeros(n)
+        sc = np.zeros(n, np.int64)
+        N.check(N.lib.psg_index_query(self.ctx.h, self.h, _p(Q), n, budget.c(), _p(idx), _p(dist),
+                                      _p(dpca), _p(sc)))
+        return idx, dist, dpca, sc
+
+
+def make_pca_tree_index(exemplar: np.ndarray, window: int, variance_target: float = 0.95,
+                        branching: int = 4, seed: int = 0, *, mean=None, basis=None,
+                        d_cap: int = 0, d_fixed: int = 0, max_depth: int = 0,
+                        hist_bins: int = 0, hist_include_scale: bool = False,
+                        ctx: Optional[Context] = None) -> SearchIndex:
+    """make_pca_tree_index(extract_all(exemplar, {w,1,..}), variance, b, seed)."""
+    ctx = ctx or default_context()
+    ex = _c(exemplar, np.float64)
+    C, eh, ew = ex.shape
+    cfg = index_cfg(variance_target, d_cap, d_fixed, branching, max_depth, 0, seed, hist_bins,
+                    hist_include_scale)
+    m = _c(mean, np.float64) if mean is not None else None
+    b = _c(basis, np.float64) if basis is not None else None
+    d = b.shape[0] if b is not None else 0
+    h = ct.c_void_p()
+    N.check(N.lib.psg_index_create(ctx.h, _p(ex), C, ew, eh, window, _p(m), _p(b), d,
+                                   ct.byref(cfg), ct.byref(h)))
+    return SearchIndex(ctx, h, None)
+
+
+def make_vector_index(X: np.ndarray, variance_target: float = 0.95, branching: int = 8,
+                      seed: int = 0, *, mean=None, basis=None, d_fixed: int = 0,
+                      max_depth: int = 0, ctx: Optional[Context] = None) -> SearchIndex:
+    ctx = ctx or default_context()
+    X = _c(X, np.float32)
+    cfg = index_cfg(variance_target, 0, d_fixed, branching, max_depth, 0, seed)
+    m = _c(mean, np.float64) if mean is not None else None
+    b = _c(basis, np.float64) if basis is not None else None
+    d = b.shape[0] if b is not None else 0
+    h = ct.c_void_p()
+    N.check(N.lib.psg_index_create_vectors(ctx.h, _p(X), X.shape[0], X.shape[1], _p(m), _p(b), d,
+                                           ct.byref(cfg), ct.byref(h)))
+    return SearchIndex(ctx, h, None)
+
+
+# ---------------------------------------------------------------------------
+def search_step(out: np.ndarray, index: SearchIndex, spacing: int, patch_width: int,
+                budget: QueryBudget):
+    """(assignments, distances, nn_calls, points_scanned) — optimizer.cpp:275-348."""
+    x = _c(out, np.float64)
+    C, H, W = x.shape
+    if C != index.channels:
+        raise ShapeError(N.PSG_E_SHAPE, "candidate dim does not match the grid window")
+    nx = N.lib.psg_axis_positions(W, index.window, spacing, None) or 1
+    ny = N.lib.psg_axis_positions(H, index.window, spacing, None) or 1
+    idx = np.zeros(nx * ny, np.int32)
+    dist = np.zeros(nx * ny)
+    calls = ct.c_int64()
+    sc = ct.c_int64()
+    N.check(N.lib.psg_search_step(index.ctx.h, index.h, _p(x), W, H, spacing, patch_width,
+                                  budget.c(), _p(idx), _p(dist), ct.byref(calls), ct.byref(sc)))
+    return idx, dist, calls.value, sc.value
+
+
+def update_step(idx, irls, pen, index: SearchIndex, W: int, H: int, spacing: int) -> np.ndarray:
+    """update_step with WeightMap{irls, hist_penalty} — optimizer.cpp:350-401."""
+    idx = _c(idx, np.int32)
+    irls = _c(irls, np.float64)
+    pen = _c(pen, np.float64)
+    out = np.zeros((index.channels, H, W))
+    nx = N.lib.psg_axis_positions(W, index.window, spacing, None)
+    ny = N.lib.psg_axis_positions(H, index.window, spacing, None)
+    if idx.size != nx * ny or irls.size != nx * ny or pen.size != nx * ny:
+        raise ShapeError(N.PSG_E_SHAPE, "assignments/weights do not cover the grid")
+    N.check(N.lib.psg_update_step(index.ctx.h, index.h, _p(idx), _p(irls), _p(pen), W, H, spacing,
+                                  _p(out)))
+    return out
+
+
+def optimize_level(init: np.ndarray, index: SearchIndex, cfg: OptimizerConfig,
+                   exemplar_hist: Optional[np.ndarray] = None):
+    """(image, [IterationStats]) — optimizer.cpp:426-516."""
+    x = _c(init, np.float64)
+    C, H, W = x.shape
+    if cfg.nbhd_width != index.window:
+        raise ShapeError(N.PSG_E_SHAPE, "candidate dim does not match the grid window")
+    c = cfg.c()
+    out = np.zeros_like(x)
+    stats = (N.psg_iter_stats * max(cfg.max_iterations, 1))()
+    n = ct.c_int()
+    eh = _c(exemplar_hist, np.float64) if exemplar_hist is not None else None
+    N.check(N.lib.psg_optimize_level(index.ctx.h, index.h, _p(x), W, H, ct.byref(c), _p(eh),
+                                     _p(out), ct.cast(stats, ct.c_void_p), ct.byref(n)))
+    return out, [IterationStats.of(stats[i]) for i in range(n.value)]
+
+
+class Level:
+    """Device-resident optimize_level state (benchmark / driver use)."""
+
+    def __init__(self, init: np.ndarray, index: SearchIndex, cfg: OptimizerConfig,
+                 exemplar_hist: Optional[np.ndarray] = None):
+        x = _c(init, np.float64)
+        self.C, self.H, self.W = x.shape
+        self.index = index
+        self.cfg = cfg
+        c = cfg.c()
+        eh = _c(exemplar_hist, np.float64) if exemplar_hist is not None else None
+        h = ct.c_void_p()
+        N.check(N.lib.psg_level_create(index.ctx.h, index.h, _p(x), self.W, self.H, ct.byref(c),
+                                       _p(eh), ct.byref(h)))
+        self.h = h
+        self.nx = N.lib.psg_axis_positions(self.W, index.window, cfg.spacing, None)
+        self.ny = N.lib.psg_axis_positions(self.H, index.window, cfg.spacing, None)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            N.lib.psg_level_destroy(self.h)
+            self.h = None
+
+    def prime(self):
+        N.check(N.lib.psg_level_prime(self.h))
+
+    def iterate(self, n: int, honor_convergence: bool = False):
+        stats = (N.psg_iter_stats * max(n, 1))()
+        done = ct.c_int()
+        N.check(N.lib.psg_level_iterate(self.h, n, int(honor_convergence),
+                                        ct.cast(stats, ct.c_void_p), ct.byref(done)))
+        return [IterationStats.of(stats[i]) for i in range(done.value)]
+
+    def download(self):
+        planes = np.zeros((self.C, self.H, self.W))
+        A = self.nx * self.ny
+        idx = np.zeros(A, np.int32)
+        dist = np.zeros(A)
+        N.check(N.lib.psg_level_download(self.h, _p(planes), _p(idx), _p(dist)))
+        return planes, idx, dist
+
+
+def synthesize(exemplar: np.ndarray, out_w: int, out_h: int, levels: int, sizes, cfg: OptimizerConfig,
+               variance_target=0.95, d_cap=0, d_fixed=0, branching=4, max_depth=0, seed=0,
+               out_guidance: Optional[np.ndarray] = None, ctx: Optional[Context] = None):
+    """Coarse-to-fine driver (pipeline.cpp:216-315) over stages (level x size)."""
+    ctx = ctx or default_context()
+    ex = _c(exemplar, np.float64)
+    C, eh, ew = ex.shape
+    req = N.psg_request()
+    req.exemplar = ex.ctypes.data_as(ct.POINTER(ct.c_double))
+    req.C, req.ew, req.eh = C, ew, eh
+    og = None
+    if out_guidance is not None:
+        og = _c(out_guidance, np.float64)
+        req.out_guidance = og.ctypes.data_as(ct.POINTER(ct.c_double))
+        req.guidance_kind = 1
+    req.out_w, req.out_h, req.levels = out_w, out_h, levels
+    sizes = list(sizes)
+    req.stages.n_sizes = len(sizes)
+    for i, s in enumerate(sizes):
+        req.stages.sizes[i] = s
+    req.cfg = cfg.c()
+    req.index = index_cfg(variance_target, d_cap, d_fixed, branching, max_depth, 0, seed)
+    req.seed = seed
+    out = np.zeros((C, out_h, out_w))
+    rep = N.psg_report()
+    N.check(N.lib.psg_synthesize(ctx.h, ct.byref(req), _p(out), ct.byref(rep)))
+    stages = [rep.stages[i] for i in range(rep.n_stages)]
+    report = {
+        "part1_millis": rep.part1_millis, "part2_millis": rep.part2_millis,
+        "total_nn_calls": rep.total_nn_calls, "final_energy": rep.final_energy,
+        "stages": [dict(level=s.level, w=s.w, W=s.W, H=s.H, ew=s.ew, eh=s.eh, d=s.d,
+                        iterations=s.iterations, final_energy=s.final_energy,
+                        nn_calls=s.nn_calls, index_millis=s.index_millis,
+                        optimize_millis=s.optimize_millis) for s in stages],
+    }
+    return out, report
+
+
+# ---- host helpers -----------------------------------------------------------------
+def axis_positions(extent: int, window: int, step: int) -> np.ndarray:
+    n = N.lib.psg_axis_positions(extent, window, step, None)
+    out = np.zeros(max(n, 1), np.int32)
+    N.lib.psg_axis_positions(extent, window, step, _p(out))
+    return out[:n]
+
+
+def plan(W: int, H: int, w: int, spacing: int, patch_width: int):
+    nx = N.lib.psg_axis_positions(W, w, spacing, None)
+    ny = N.lib.psg_axis_positions(H, w, spacing, None)
+    mult = np.zeros(max(nx * ny, 1), np.int32)
+    calls = N.lib.psg_plan(W, H, w, spacing, patch_width, _p(mult))
+    return int(calls), mult[: nx * ny]
+
+
+def pow_cr(x: float, y: float) -> float:
+    return N.lib.psg_pow_cr(x, y)
+
+
+def hist_mass(count: int, pixels: int) -> float:
+    return N.lib.psg_hist_mass(count, pixels)

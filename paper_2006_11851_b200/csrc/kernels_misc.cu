@@ -1,0 +1,186 @@
+// Per-stage build kernels (PCA inputs) and pyramid resampling.
+//
+//   fit_pca inputs   pca.cpp:57-65      mean + centred fp64 design matrix
+//   downsample       image.cpp:38-62    block mean, acc * (1/f^2)
+//   upsample_bilinear image.cpp:64-109  half-pixel centres, clamp to edge
+//   fit_to           pipeline.cpp:39-52 crop / edge-replicate
+#include <cuda_runtime.h>
+
+#include "numerics.cuh"
+#include "psg_internal.h"
+
+namespace psg {
+
+static int grid_cap(psg_ctx* ctx, int64_t n, int threads, int per_sm = 32) {
+  int64_t b = (n + threads - 1) / threads;
+  const int64_t cap = (int64_t)ctx->num_sms * per_sm;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+// Column means of the dense window matrix without materialising it: one CTA
+// per feature j, fixed-order strided partial sums + fixed tree (deterministic).
+__global__ void window_mean_kernel(const float* __restrict__ mirror, int img_w, int C, int w,
+                                   int nxe, int64_t N, double* __restrict__ mean) {
+  __shared__ double red[256];
+  const int j = blockIdx.x;
+  const int row = w * C;
+  const int dy = j / row, rem = j - dy * row;
+  const int dx = rem / C, c = rem - dx * C;
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
+    const int ax = (int)(i % nxe), ay = (int)(i / nxe);
+    acc += (double)mirror[((int64_t)(ay + dy) * img_w + ax + dx) * C + c];
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) mean[j] = red[0] / (double)N;
+}
+
+void launch_window_mean(psg_ctx* ctx, const float* mirror, int img_w, int C, int w, int nxe,
+                        int64_t N, double* mean) {
+  const int D = w * w * C;
+  window_mean_kernel<<<D, 256, 0, ctx->stream>>>(mirror, img_w, C, w, nxe, N, mean);
+  PSG_LAUNCHED(ctx);
+}
+
+__global__ void center_windows_kernel(const float* __restrict__ mirror, int img_w, int C, int w,
+                                      int nxe, int64_t N, const double* __restrict__ mean,
+                                      double* __restrict__ Xc) {
+  const int D = w * w * C;
+  const int row = w * C;
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < N * D;
+       f += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = f / D;
+    const int j = (int)(f - i * D);
+    const int ax = (int)(i % nxe), ay = (int)(i / nxe);
+    const int dy = j / row, jj = j - dy * row;
+    const float v = mirror[((int64_t)(ay + dy) * img_w + ax) * C + jj];
+    Xc[f] = (double)v - mean[j];
+  }
+}
+
+void launch_center_windows(psg_ctx* ctx, const float* mirror, int img_w, int C, int w, int nxe,
+                           int64_t N, const double* mean, double* Xc) {
+  const int64_t n = N * (int64_t)w * w * C;
+  center_windows_kernel<<<grid_cap(ctx, n, 256), 256, 0, ctx->stream>>>(mirror, img_w, C, w, nxe,
+                                                                         N, mean, Xc);
+  PSG_LAUNCHED(ctx);
+}
+
+__global__ void vector_mean_kernel(const float* __restrict__ X, int64_t N, int D,
+                                   double* __restrict__ mean) {
+  __shared__ double red[256];
+  const int j = blockIdx.x;
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < N; i += blockDim.x) acc += (double)X[i * D + j];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) mean[j] = red[0] / (double)N;
+}
+
+void launch_vector_mean(psg_ctx* ctx, const float* X, int64_t N, int D, double* mean) {
+  vector_mean_kernel<<<D, 256, 0, ctx->stream>>>(X, N, D, mean);
+  PSG_LAUNCHED(ctx);
+}
+
+__global__ void center_vectors_kernel(const float* __restrict__ X, int64_t N, int D,
+                                      const double* __restrict__ mean, double* __restrict__ Xc) {
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < N * D;
+       f += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(f % D);
+    Xc[f] = (double)X[f] - mean[j];
+  }
+}
+
+void launch_center_vectors(psg_ctx* ctx, const float* X, int64_t N, int D, const double* mean,
+                           double* Xc) {
+  center_vectors_kernel<<<grid_cap(ctx, N * D, 256), 256, 0, ctx->stream>>>(X, N, D, mean, Xc);
+  PSG_LAUNCHED(ctx);
+}
+
+// ---- pyramid ----------------------------------------------------------------------
+__global__ void downsample_kernel(const double* __restrict__ in, int W, int H, int f,
+                                  double* __restrict__ out, int ow, int oh) {
+  const double inv = 1.0 / ((double)f * f);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)ow * oh;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int y = (int)(i / ow), x = (int)(i - (int64_t)y * ow);
+    double acc = 0.0;
+    for (int dy = 0; dy < f; ++dy)
+      for (int dx = 0; dx < f; ++dx)
+        acc = dadd(acc, in[(int64_t)(y * f + dy) * W + x * f + dx]);
+    out[i] = dmul(acc, inv);
+  }
+}
+
+void launch_downsample(psg_ctx* ctx, const double* in, int W, int H, int f, double* out) {
+  const int ow = W / f, oh = H / f;
+  downsample_kernel<<<grid_cap(ctx, (int64_t)ow * oh, 256), 256, 0, ctx->stream>>>(in, W, H, f,
+                                                                                    out, ow, oh);
+  PSG_LAUNCHED(ctx);
+}
+
+__device__ __forceinline__ void src_coord(int dst, int limit, double inv, int& lo, int& hi,
+                                          double& frac) {
+  const double s = dsub(dmul(dadd((double)dst, 0.5), inv), 0.5);
+  const double fl = floor(s);
+  lo = (int)fl;
+  frac = dsub(s, fl);
+  hi = min(lo + 1, limit - 1);
+  lo = max(lo, 0);
+  if (hi < lo) hi = lo;
+}
+
+__global__ void upsample_kernel(const double* __restrict__ in, int W, int H, int f,
+                                double* __restrict__ out) {
+  const int ow = W * f, oh = H * f;
+  const double inv = 1.0 / f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)ow * oh;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int y = (int)(i / ow), x = (int)(i - (int64_t)y * ow);
+    int y0, y1, x0, x1;
+    double fy, fx;
+    src_coord(y, H, inv, y0, y1, fy);
+    src_coord(x, W, inv, x0, x1, fx);
+    const double v00 = in[(int64_t)y0 * W + x0], v10 = in[(int64_t)y0 * W + x1];
+    const double v01 = in[(int64_t)y1 * W + x0], v11 = in[(int64_t)y1 * W + x1];
+    const double gx = dsub(1.0, fx), gy = dsub(1.0, fy);
+    const double a = dadd(dmul(gx, v00), dmul(fx, v10));
+    const double b = dadd(dmul(gx, v01), dmul(fx, v11));
+    out[i] = dadd(dmul(gy, a), dmul(fy, b));
+  }
+}
+
+void launch_upsample_bilinear(psg_ctx* ctx, const double* in, int W, int H, int f, double* out) {
+  upsample_kernel<<<grid_cap(ctx, (int64_t)W * f * H * f, 256), 256, 0, ctx->stream>>>(in, W, H,
+                                                                                       f, out);
+  PSG_LAUNCHED(ctx);
+}
+
+__global__ void fit_to_kernel(const double* __restrict__ in, int W, int H, int ow, int oh,
+                              double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)ow * oh;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int y = (int)(i / ow), x = (int)(i - (int64_t)y * ow);
+    const int sy = min(y, H - 1), sx = min(x, W - 1);
+    out[i] = in[(int64_t)sy * W + sx];
+  }
+}
+
+void launch_fit_to(psg_ctx* ctx, const double* in, int W, int H, int ow, int oh, double* out) {
+  fit_to_kernel<<<grid_cap(ctx, (int64_t)ow * oh, 256), 256, 0, ctx->stream>>>(in, W, H, ow, oh,
+                                                                               out);
+  PSG_LAUNCHED(ctx);
+}
+
+}  // namespace psg

@@ -1,0 +1,266 @@
+// M-step kernels: IRLS weights, exact histograms + penalty, the gather-form
+// overlapping-window average, and deterministic telemetry reductions.
+//
+// Reference semantics (paths under /root/reference/proj/core/src):
+//   irls_weight          optimizer.cpp:112-115  pow(d*d + eps, (r-2)/2)
+//   WeightMap::effective optimizer.hpp:32-34    irls / (1 + penalty)
+//   build_histograms     optimizer.cpp:69-88    mass[b] += 1/P per pixel
+//   histogram_penalty    optimizer.cpp:90-108   sum_p sum_s max(0, Hx-Hz) / w^2
+//   update_step          optimizer.cpp:350-401  per pixel, ascending anchors
+//   energy_from_distances optimizer.cpp:126-131
+#include <cuda_runtime.h>
+
+#include "numerics.cuh"
+#include "psg_internal.h"
+
+namespace psg {
+
+static int grid_for(psg_ctx* ctx, int64_t n, int threads, int per_sm = 32) {
+  int64_t b = (n + threads - 1) / threads;
+  const int64_t cap = (int64_t)ctx->num_sms * per_sm;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+// ---- IRLS weights ---------------------------------------------------------------
+__global__ void weights_kernel(WeightArgs a) {
+  const double e = (a.r - 2.0) / 2.0;  // same expression as optimizer.cpp:114
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.A;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double d = a.dist[i];
+    if (d < 0.0) atomicOr(a.flags, FLAG_BAD_DISTANCE);
+    const double w = pow_cr(dadd(dmul(d, d), a.eps), e);
+    a.irls[i] = w;
+    const double p = a.pen ? a.pen[i] : 0.0;
+    const double we = w / dadd(1.0, p);
+    a.eff[i] = we;
+    if (!(we > 0.0) || !isfinite(we)) atomicOr(a.flags, FLAG_BAD_WEIGHT);
+  }
+}
+
+void launch_weights(psg_ctx* ctx, const WeightArgs& a) {
+  if (a.A <= 0) return;
+  weights_kernel<<<grid_for(ctx, a.A, 256), 256, 0, ctx->stream>>>(a);
+  PSG_LAUNCHED(ctx);
+}
+
+__global__ void eff_kernel(const double* __restrict__ irls, const double* __restrict__ pen,
+                           int64_t A, double* __restrict__ eff, int* flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double we = irls[i] / dadd(1.0, pen[i]);
+    eff[i] = we;
+    if (!(we > 0.0) || !isfinite(we)) atomicOr(flags, FLAG_BAD_WEIGHT);
+  }
+}
+
+void launch_eff_from(psg_ctx* ctx, const double* irls, const double* pen, int64_t A, double* eff,
+                     int* flags) {
+  if (A <= 0) return;
+  eff_kernel<<<grid_for(ctx, A, 256), 256, 0, ctx->stream>>>(irls, pen, A, eff, flags);
+  PSG_LAUNCHED(ctx);
+}
+
+// ---- histograms -------------------------------------------------------------------
+// Integer bin counts (exact, order-free), then the exact sequential-sum fold.
+__global__ void hist_count_kernel(const double* __restrict__ planes, int64_t P, int bins,
+                                  int slots, unsigned long long* __restrict__ counts) {
+  extern __shared__ unsigned int sh[];
+  for (int i = threadIdx.x; i < bins * slots; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    for (int s = 0; s < slots; ++s) {
+      const int b = bin_of_f64(planes[s * P + i], bins);
+      atomicAdd(&sh[s * bins + b], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < bins * slots; i += blockDim.x)
+    if (sh[i]) atomicAdd(&counts[i], (unsigned long long)sh[i]);
+}
+
+void launch_hist_count(psg_ctx* ctx, const double* planes, int64_t P, int bins, int slots,
+                       unsigned long long* counts) {
+  PSG_CUDA(cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * bins * slots, ctx->stream));
+  const size_t sm = sizeof(unsigned int) * bins * slots;
+  hist_count_kernel<<<grid_for(ctx, P, 256, 4), 256, sm, ctx->stream>>>(planes, P, bins, slots,
+                                                                         counts);
+  PSG_LAUNCHED(ctx);
+}
+
+__global__ void hist_fold_kernel(const unsigned long long* __restrict__ counts, int n, int64_t P,
+                                 const double* __restrict__ ex_mass, double* __restrict__ mass,
+                                 double* __restrict__ excess) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double inv = 1.0 / (double)P;  // optimizer.cpp:76
+  const double m = hist_mass((int64_t)counts[i], inv);
+  if (mass) mass[i] = m;
+  if (excess) {
+    const double diff = dsub(m, ex_mass[i]);  // optimizer.cpp:104
+    excess[i] = diff > 0.0 ? diff : 0.0;
+  }
+}
+
+void launch_hist_fold(psg_ctx* ctx, const unsigned long long* counts, int bins, int slots,
+                      int64_t P, const double* ex_mass, double* mass, double* excess) {
+  const int n = bins * slots;
+  hist_fold_kernel<<<(n + 63) / 64, 64, 0, ctx->stream>>>(counts, n, P, ex_mass, mass, excess);
+  PSG_LAUNCHED(ctx);
+}
+
+// Penalty of each anchor's assigned candidate (optimizer.cpp:463-467): the
+// candidate's values are the exemplar window at the candidate anchor; pixels
+// in window order (dy, dx), slots inner, one sequential fp64 sum per anchor.
+__global__ void penalty_kernel(const float* __restrict__ ex_mirror, int ew, int C, int w, int nxe,
+                               const int32_t* __restrict__ idx, int64_t A,
+                               const double* __restrict__ excess, int bins, int slots,
+                               double* __restrict__ pen) {
+  extern __shared__ double ex_s[];
+  for (int i = threadIdx.x; i < bins * slots; i += blockDim.x) ex_s[i] = excess[i];
+  __syncthreads();
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < A;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t id = idx[a];
+    const int ex = id % nxe, ey = id / nxe;
+    double total = 0.0;
+    for (int dy = 0; dy < w; ++dy) {
+      const float* z = ex_mirror + ((int64_t)(ey + dy) * ew + ex) * C;
+      for (int dx = 0; dx < w; ++dx)
+        for (int s = 0; s < slots; ++s) {
+          const int b = bin_of_f32(z[dx * C + s], bins);
+          total = dadd(total, ex_s[s * bins + b]);
+        }
+    }
+    pen[a] = total / (double)(w * w);
+  }
+}
+
+void launch_penalty(psg_ctx* ctx, const Index& ix, const int32_t* idx, int64_t A,
+                    const double* excess, int bins, int slots, double* pen) {
+  if (A <= 0) return;
+  const size_t sm = sizeof(double) * bins * slots;
+  penalty_kernel<<<grid_for(ctx, A, 128), 128, sm, ctx->stream>>>(
+      ix.ex_mirror, ix.ew, ix.C, ix.w, ix.nxe, idx, A, excess, bins, slots, pen);
+  PSG_LAUNCHED(ctx);
+}
+
+// ---- M-step: gather form ----------------------------------------------------------
+// One thread per output pixel.  The reference scatters anchors in ascending
+// id into per-pixel accumulators; for a fixed pixel that is exactly the
+// ascending (iy, ix) order of its covering anchors, which this loop walks.
+// No atomics, bit-identical sums.
+template <int CMAX>
+__global__ void __launch_bounds__(256) mstep_kernel(MstepArgs a) {
+  const int64_t P = (int64_t)a.W * a.H;
+  for (int64_t pix = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pix < P;
+       pix += (int64_t)gridDim.x * blockDim.x) {
+    const int y = (int)(pix / a.W), x = (int)(pix - (int64_t)y * a.W);
+    double acc[CMAX];
+#pragma unroll
+    for (int c = 0; c < CMAX; ++c) acc[c] = 0.0;
+    double wsum = 0.0;
+    const int iy0 = a.row_lo[y], iy1 = a.row_hi[y];
+    const int ix0 = a.col_lo[x], ix1 = a.col_hi[x];
+    for (int iy = iy0; iy < iy1; ++iy) {
+      const int dy = y - a.ys[iy];
+      for (int ix = ix0; ix < ix1; ++ix) {
+        const int64_t an = (int64_t)iy * a.nx + ix;
+        const double we = a.eff[an];
+        const int32_t id = a.idx[an];
+        const int dx = x - a.xs[ix];
+        const int ex = id % a.nxe + dx, ey = id / a.nxe + dy;
+        const float* z = a.ex_mirror + ((int64_t)ey * a.ew + ex) * a.C;
+#pragma unroll
+        for (int c = 0; c < CMAX; ++c)
+          if (c < a.C) acc[c] = dadd(acc[c], dmul(we, (double)z[c]));
+        wsum = dadd(wsum, we);
+      }
+    }
+    if (wsum <= 0.0) {
+      atomicOr(a.flags, FLAG_UNCOVERED);
+      continue;
+    }
+    const double inv = 1.0 / wsum;  // optimizer.cpp:393
+#pragma unroll
+    for (int c = 0; c < CMAX; ++c) {
+      if (c >= a.C) break;
+      double v = dmul(acc[c], inv);
+      v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);  // std::clamp(.., 0, 1)
+      a.planes[c * P + pix] = v;
+      if (a.mirror) a.mirror[pix * a.C + c] = (float)v;
+    }
+  }
+}
+
+void launch_mstep(psg_ctx* ctx, const MstepArgs& a) {
+  const int64_t P = (int64_t)a.W * a.H;
+  if (P <= 0) return;
+  const int blocks = grid_for(ctx, P, 256, 16);
+  if (a.C <= 4) {
+    mstep_kernel<4><<<blocks, 256, 0, ctx->stream>>>(a);
+  } else if (a.C <= 8) {
+    mstep_kernel<8><<<blocks, 256, 0, ctx->stream>>>(a);
+  } else {
+    fail(PSG_E_DOMAIN, "more than 8 channels are not supported");
+  }
+  PSG_LAUNCHED(ctx);
+}
+
+// ---- deterministic telemetry reductions ---------------------------------------------
+// One CTA, fixed per-thread strides and a fixed tree: run-to-run identical.
+constexpr int kStatsThreads = 512;
+__global__ void __launch_bounds__(kStatsThreads) stats_kernel(StatsArgs a) {
+  __shared__ double sd[3][kStatsThreads];
+  __shared__ long long si[3][kStatsThreads];
+  double lb = 0.0, la = 0.0, en = 0.0;
+  long long ch = 0, sp = 0, su = 0;
+  for (int64_t i = threadIdx.x; i < a.A; i += blockDim.x) {
+    if (a.eff && a.cur_dist) {
+      const double d = a.cur_dist[i];
+      lb = dadd(lb, dmul(dmul(a.eff[i], d), d));  // optimizer.cpp:473
+    }
+    if (a.eff && a.after_dist) {
+      const double d = a.after_dist[i];
+      la = dadd(la, dmul(dmul(a.eff[i], d), d));  // optimizer.cpp:482
+    }
+    if (a.next_dist) en = dadd(en, pow_cr(a.next_dist[i], a.r));  // optimizer.cpp:129
+    if (a.cur_idx && a.next_idx) ch += a.cur_idx[i] != a.next_idx[i];
+    if (a.scanned) {
+      su += a.scanned[i];
+      sp += (long long)a.scanned[i] * (a.mult ? a.mult[i] : 1);
+    }
+  }
+  const int t = threadIdx.x;
+  sd[0][t] = lb;
+  sd[1][t] = la;
+  sd[2][t] = en;
+  si[0][t] = ch;
+  si[1][t] = sp;
+  si[2][t] = su;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (t < s) {
+      for (int k = 0; k < 3; ++k) sd[k][t] = dadd(sd[k][t], sd[k][t + s]);
+      for (int k = 0; k < 3; ++k) si[k][t] += si[k][t + s];
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    a.out[0] = sd[0][0];
+    a.out[1] = sd[1][0];
+    a.out[2] = sd[2][0];
+    a.out[3] = (double)si[0][0];
+    a.out[4] = (double)si[1][0];
+    a.out[5] = (double)si[2][0];
+  }
+}
+
+void launch_stats(psg_ctx* ctx, const StatsArgs& a) {
+  stats_kernel<<<1, kStatsThreads, 0, ctx->stream>>>(a);
+  PSG_LAUNCHED(ctx);
+}
+
+}  // namespace psg

@@ -1,0 +1,521 @@
+// E-step kernels: window gather + exact fp64 PCA projection, exact k-means
+// tree search with warp-cooperative leaf scans, and full-D rescoring.
+//
+// Reference semantics (paths under /root/reference/proj/core/src):
+//   extract_window   neighborhood.cpp:120-137  fp32 = (float) fp64 state
+//   PcaModel::project pca.cpp:27-41            acc += (v_j - mean_j) * b_kj, j asc
+//   KmTree::query    km_tree.cpp:197-284       greedy / backtrack(m) / exact
+//   scan_leaf        km_tree.cpp:128-139       lexicographic min (dist^2, id)
+//   full_distance    optimizer.cpp:117-124     sqrt sum (a_j - b_j)^2, j asc
+#include <cuda_runtime.h>
+#include <float.h>
+
+#include "numerics.cuh"
+#include "psg_internal.h"
+
+namespace psg {
+
+// ----------------------------------------------------------------------------
+// planes [C][H][W] fp64 -> mirror [H][W][C] fp32 (the layout the gathers read)
+__global__ void make_mirror_kernel(const double* __restrict__ planes, int C, int64_t P,
+                                   float* __restrict__ mirror) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    for (int c = 0; c < C; ++c) mirror[i * C + c] = (float)planes[c * P + i];
+  }
+}
+
+void launch_make_mirror(psg_ctx* ctx, const double* planes, int C, int W, int H, float* mirror) {
+  const int64_t P = (int64_t)W * H;
+  const int threads = 256;
+  int blocks = (int)((P + threads - 1) / threads);
+  if (blocks > ctx->num_sms * 16) blocks = ctx->num_sms * 16;
+  if (blocks < 1) blocks = 1;
+  make_mirror_kernel<<<blocks, threads, 0, ctx->stream>>>(planes, C, P, mirror);
+  PSG_LAUNCHED(ctx);
+}
+
+// ----------------------------------------------------------------------------
+// Exact projection.  A CTA of 8 warps owns TQ = 8*RQ queries; lane owns
+// components k = lane + 32*kk.  The feature axis j is walked in order in
+// chunks of one window row (JC = w*C features) staged in shared memory:
+//   cen[q][jj] = (double)v - mean[j]      (one rounding, as the reference)
+//   bas[jj][k] = basis[k][j]              (from the transposed basis)
+//   acc[q][k]  = acc + cen * bas          (separate mul + add, j ascending)
+// Each (q, k) accumulator is a sequential chain, so the result is bit-equal
+// to pca.cpp:35-38; parallelism comes from the Q x d independent chains.
+template <int KPT, int RQ, bool kWindows>
+__global__ void __launch_bounds__(256) project_kernel(
+    const float* __restrict__ src, int img_w, int C, int w,  // windows: mirror image
+    const int32_t* __restrict__ xs, const int32_t* __restrict__ ys, int nx,
+    int64_t n, int D, int JC,                                // vectors: src = X[n][D]
+    const double* __restrict__ mean, const double* __restrict__ basisT,  // [D][32*KPT]
+    int d, double* __restrict__ out) {
+  constexpr int KP = 32 * KPT;
+  constexpr int TQ = 8 * RQ;
+  extern __shared__ double smem[];
+  const int JCp = JC | 1;  // odd stride: conflict-free per-q row fills
+  double* cen = smem;               // [TQ][JCp]
+  double* bas = smem + TQ * JCp;    // [JC][KP]
+  __shared__ int64_t base_s[TQ];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t q0 = (int64_t)blockIdx.x * TQ;
+  if (tid < TQ) {
+    const int64_t qi = q0 + tid;
+    int64_t b = -1;
+    if (qi < n) {
+      if (kWindows) {
+        const int ax = xs[qi % nx], ay = ys[qi / nx];
+        b = ((int64_t)ay * img_w + ax) * C;
+      } else {
+        b = qi * (int64_t)D;
+      }
+    }
+    base_s[tid] = b;
+  }
+
+  double acc[RQ][KPT];
+#pragma unroll
+  for (int r = 0; r < RQ; ++r)
+#pragma unroll
+    for (int kk = 0; kk < KPT; ++kk) acc[r][kk] = 0.0;
+
+  const int n_chunks = (D + JC - 1) / JC;
+  for (int ch = 0; ch < n_chunks; ++ch) {
+    const int j0 = ch * JC;
+    const int jc = min(JC, D - j0);
+    __syncthreads();
+    for (int f = tid; f < TQ * jc; f += 256) {
+      const int q = f / jc, jj = f - q * jc;
+      const int64_t b = base_s[q];
+      double v = 0.0;
+      if (b >= 0) {
+        float x;
+        if (kWindows) {
+          // window row ch (= dy) of anchor q: contiguous w*C floats
+          x = src[b + (int64_t)ch * img_w * C + jj];
+        } else {
+          x = src[b + j0 + jj];
+        }
+        v = dsub((double)x, mean[j0 + jj]);
+      }
+      cen[q * JCp + jj] = v;
+    }
+    for (int f = tid; f < jc * KP; f += 256) bas[f] = basisT[(int64_t)j0 * KP + f];
+    __syncthreads();
+#pragma unroll 4
+    for (int jj = 0; jj < jc; ++jj) {
+      double b[KPT];
+#pragma unroll
+      for (int kk = 0; kk < KPT; ++kk) b[kk] = bas[jj * KP + lane + 32 * kk];
+#pragma unroll
+      for (int r = 0; r < RQ; ++r) {
+        const double c = cen[(warp * RQ + r) * JCp + jj];
+#pragma unroll
+        for (int kk = 0; kk < KPT; ++kk) acc[r][kk] = dadd(acc[r][kk], dmul(c, b[kk]));
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RQ; ++r) {
+    const int64_t qi = q0 + warp * RQ + r;
+    if (qi >= n) continue;
+#pragma unroll
+    for (int kk = 0; kk < KPT; ++kk) {
+      const int k = lane + 32 * kk;
+      if (k < d) out[qi * d + k] = acc[r][kk];
+    }
+  }
+}
+
+template <bool kWindows>
+static void launch_project(psg_ctx* ctx, const float* src, int img_w, int C, int w,
+                           const int32_t* xs, const int32_t* ys, int nx, int64_t n, int D, int JC,
+                           const double* mean, const double* basisT, int d, double* out) {
+  if (n <= 0 || d <= 0) return;
+  constexpr int RQ = 8;
+  const int TQ = 8 * RQ;
+  const int JCp = JC | 1;
+  const int blocks = (int)((n + TQ - 1) / TQ);
+  if (d <= 32) {
+    const size_t sm = sizeof(double) * ((size_t)TQ * JCp + (size_t)JC * 32);
+    auto k = project_kernel<1, RQ, kWindows>;
+    PSG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k<<<blocks, 256, sm, ctx->stream>>>(src, img_w, C, w, xs, ys, nx, n, D, JC, mean, basisT, d,
+                                         out);
+  } else if (d <= 64) {
+    const size_t sm = sizeof(double) * ((size_t)TQ * JCp + (size_t)JC * 64);
+    auto k = project_kernel<2, RQ, kWindows>;
+    PSG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k<<<blocks, 256, sm, ctx->stream>>>(src, img_w, C, w, xs, ys, nx, n, D, JC, mean, basisT, d,
+                                         out);
+  } else {
+    fail(PSG_E_DOMAIN, "retained PCA dimension > 64 is not supported");
+  }
+  PSG_LAUNCHED(ctx);
+}
+
+void launch_project_windows(psg_ctx* ctx, const float* mirror, int img_w, int C, int w,
+                            AnchorSet anchors, const double* mean, const double* basisT, int d,
+                            double* out) {
+  const int JC = w * C;
+  launch_project<true>(ctx, mirror, img_w, C, w, anchors.xs, anchors.ys, anchors.nx,
+                       anchors.count, w * w * C, JC, mean, basisT, d, out);
+}
+
+void launch_project_vectors(psg_ctx* ctx, const float* X, int64_t n, int D, const double* mean,
+                            const double* basisT, int d, double* out) {
+  const int JC = D < 128 ? D : 128;
+  launch_project<false>(ctx, X, 0, 0, 0, nullptr, nullptr, 1, n, D, JC, mean, basisT, d, out);
+}
+
+// ----------------------------------------------------------------------------
+// Tree search: one warp per query (persistent grid-stride over queries).
+constexpr int kSearchWarps = 4;
+constexpr int kStack = 256;
+constexpr int kMaxD = 64;
+
+struct WarpLexMin {
+  double d2;
+  int32_t id;
+};
+
+__device__ __forceinline__ bool lex_less(double a, int32_t ia, double b, int32_t ib) {
+  return a < b || (a == b && ia < ib);
+}
+
+__device__ __forceinline__ WarpLexMin warp_lexmin(double d2, int32_t id) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double od = __shfl_xor_sync(0xffffffffu, d2, off);
+    const int32_t oi = __shfl_xor_sync(0xffffffffu, id, off);
+    if (lex_less(od, oi, d2, id)) {
+      d2 = od;
+      id = oi;
+    }
+  }
+  return {d2, id};
+}
+
+// dist^2 to a centroid, j ascending (km_tree.cpp:15-22) — the reference's
+// exact key for greedy/backtrack ordering.
+__device__ __forceinline__ double dist2_seq(const double* __restrict__ q,
+                                            const double* __restrict__ p, int d) {
+  double acc = 0.0;
+  for (int j = 0; j < d; ++j) {
+    const double t = dsub(q[j], p[j]);
+    acc = dadd(acc, dmul(t, t));
+  }
+  return acc;
+}
+
+// Scan one leaf: lanes over points, exact dist^2 per lane, warp lexmin.
+__device__ __forceinline__ void scan_leaf(const SearchArgs& a, const double* __restrict__ qs,
+                                          int node, int lane, double& best, int32_t& best_id,
+                                          int64_t& scanned) {
+  const int32_t s = a.tree.leaf_start[node];
+  const int32_t cnt = a.tree.leaf_count[node];
+  for (int base = 0; base < cnt; base += 32) {
+    const int i = base + lane;
+    double d2 = DBL_MAX * 2;  // +inf
+    int32_t id = 0x7fffffff;
+    if (i < cnt) {
+      const int64_t pos = (int64_t)s + i;
+      id = a.perm[pos];
+      double acc = 0.0;
+      const double* col = a.proj_soa + pos;
+      for (int j = 0; j < a.d; ++j) {
+        const double t = dsub(qs[j], col[(int64_t)j * a.N]);
+        acc = dadd(acc, dmul(t, t));
+      }
+      d2 = acc;
+    }
+    const WarpLexMin m = warp_lexmin(d2, id);
+    if (lex_less(m.d2, m.id, best, best_id)) {
+      best = m.d2;
+      best_id = m.id;
+    }
+  }
+  scanned += cnt;
+}
+
+__global__ void __launch_bounds__(32 * kSearchWarps) search_kernel(SearchArgs a) {
+  __shared__ double qs_all[kSearchWarps][kMaxD];
+  __shared__ int32_t st_node[kSearchWarps][kStack];
+  __shared__ double st_key[kSearchWarps][kStack];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* qs = qs_all[warp];
+  int32_t* sn = st_node[warp];
+  double* sk = st_key[warp];
+  const int d = a.d;
+
+  for (int64_t q = (int64_t)blockIdx.x * kSearchWarps + warp; q < a.nq;
+       q += (int64_t)gridDim.x * kSearchWarps) {
+    for (int j = lane; j < d; j += 32) qs[j] = a.q[q * d + j];
+    __syncwarp();
+    double best = DBL_MAX * 2;
+    int32_t best_id = 0x7fffffff;
+    int64_t scanned = 0;
+    if (a.seed_idx) {
+      const int32_t pid = a.seed_idx[q];
+      double d2 = 0.0;
+      if (lane == 0) d2 = dist2_seq(qs, a.proj + (int64_t)pid * d, d);
+      best = __shfl_sync(0xffffffffu, d2, 0);
+      best_id = pid;
+      scanned += 1;
+    }
+
+    if (a.mode == PSG_EXACT) {
+      int top = 0;
+      if (lane == 0) {
+        sn[0] = 0;  // root is node 0 (breadth-first layout)
+        sk[0] = 0.0;
+      }
+      top = 1;
+      __syncwarp();
+      while (top > 0) {
+        --top;
+        const int node = sn[top];
+        const double key = sk[top];
+        __syncwarp();
+        if (key > best) continue;  // km_tree.cpp:265 prune
+        const int nc = a.tree.n_children[node];
+        if (nc == 0) {
+          scan_leaf(a, qs, node, lane, best, best_id, scanned);
+          continue;
+        }
+        const int fc = a.tree.first_child[node];
+        for (int cb = 0; cb < nc; cb += 32) {
+          const int c = cb + lane;
+          double lb2 = DBL_MAX * 2;
+          bool keep = false;
+          if (c < nc) {
+            const int cid = fc + c;
+            // lower_bound2 (km_tree.cpp:255-260): (|q-c| - radius - slack)+^2
+            const double dc = sqrt(dist2_seq(qs, a.tree.centroid + (int64_t)cid * d, d));
+            const double rad = a.tree.radius[cid];
+            const double slack = 1e-9 * (1.0 + dc + rad);
+            const double lb = dc - rad - slack;
+            lb2 = lb > 0.0 ? lb * lb : 0.0;
+            keep = lb2 <= best;
+          }
+          const unsigned km = __ballot_sync(0xffffffffu, keep);
+          const int nkeep = __popc(km);
+          // rank among kept children by (lb2, child) ascending
+          int rank = 0;
+          for (int o = 0; o < 32; ++o) {
+            const double ol = __shfl_sync(0xffffffffu, lb2, o);
+            if (((km >> o) & 1u) && (ol < lb2 || (ol == lb2 && o < lane))) ++rank;
+          }
+          if (top + nkeep > kStack) {
+            if (lane == 0) atomicOr(a.flags, FLAG_STACK_OVERFLOW);
+            break;
+          }
+          if (keep) {
+            const int slot = top + nkeep - 1 - rank;  // nearest popped first
+            sn[slot] = fc + c;
+            sk[slot] = lb2;
+          }
+          top += nkeep;
+          __syncwarp();
+        }
+      }
+    } else if (a.mode == PSG_GREEDY) {
+      // km_tree.cpp:213-231: descend to the nearest child (strict <, lowest wins)
+      int node = 0;
+      int nc = a.tree.n_children[node];
+      while (nc > 0) {
+        const int fc = a.tree.first_child[node];
+        double bd = DBL_MAX * 2;
+        int32_t bi = 0x7fffffff;
+        for (int cb = 0; cb < nc; cb += 32) {
+          const int c = cb + lane;
+          double dc2 = DBL_MAX * 2;
+          if (c < nc) dc2 = dist2_seq(qs, a.tree.centroid + (int64_t)(fc + c) * d, d);
+          const WarpLexMin m = warp_lexmin(dc2, c < nc ? c : 0x7fffffff);
+          if (lex_less(m.d2, m.id, bd, bi)) {
+            bd = m.d2;
+            bi = m.id;
+          }
+        }
+        node = fc + bi;
+        nc = a.tree.n_children[node];
+      }
+      scan_leaf(a, qs, node, lane, best, best_id, scanned);
+    } else {
+      // backtrack(m), km_tree.cpp:232-250: best-first on (dist^2 to centroid,
+      // node id); frontier kept as an unsorted pool, min found by the warp.
+      int size = 1;
+      if (lane == 0) {
+        sn[0] = 0;
+        sk[0] = 0.0;
+      }
+      __syncwarp();
+      int leaves = 0;
+      while (size > 0 && leaves < a.max_leaves) {
+        double bk = DBL_MAX * 2;
+        int32_t bn = 0x7fffffff;
+        int bslot = -1;
+        for (int s0 = 0; s0 < size; s0 += 32) {
+          const int s = s0 + lane;
+          double k = DBL_MAX * 2;
+          int32_t nid = 0x7fffffff;
+          if (s < size) {
+            k = sk[s];
+            nid = sn[s];
+          }
+          const WarpLexMin m = warp_lexmin(k, nid);
+          if (lex_less(m.d2, m.id, bk, bn)) {
+            bk = m.d2;
+            bn = m.id;
+          }
+        }
+        // locate the slot of the winner and remove it (swap with last)
+        for (int s0 = 0; s0 < size; s0 += 32) {
+          const int s = s0 + lane;
+          const bool hit = s < size && sn[s] == bn && sk[s] == bk;
+          const unsigned hm = __ballot_sync(0xffffffffu, hit);
+          if (hm && bslot < 0) bslot = s0 + __ffs(hm) - 1;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          sn[bslot] = sn[size - 1];
+          sk[bslot] = sk[size - 1];
+        }
+        --size;
+        __syncwarp();
+        const int node = bn;
+        const int nc = a.tree.n_children[node];
+        if (nc == 0) {
+          scan_leaf(a, qs, node, lane, best, best_id, scanned);
+          ++leaves;
+        } else {
+          const int fc = a.tree.first_child[node];
+          if (size + nc > kStack) {
+            if (lane == 0) atomicOr(a.flags, FLAG_STACK_OVERFLOW);
+            break;
+          }
+          for (int cb = 0; cb < nc; cb += 32) {
+            const int c = cb + lane;
+            if (c < nc) {
+              sn[size + c] = fc + c;
+              sk[size + c] = dist2_seq(qs, a.tree.centroid + (int64_t)(fc + c) * d, d);
+            }
+          }
+          size += nc;
+          __syncwarp();
+        }
+      }
+    }
+    if (lane == 0) {
+      a.out_idx[q] = best_id;
+      a.out_d2[q] = best;
+      if (a.out_scanned) a.out_scanned[q] = scanned;
+    }
+    __syncwarp();
+  }
+}
+
+void launch_search(psg_ctx* ctx, const SearchArgs& a) {
+  if (a.nq <= 0) return;
+  if (a.d > kMaxD) fail(PSG_E_DOMAIN, "retained PCA dimension > 64 is not supported");
+  int64_t blocks = (a.nq + kSearchWarps - 1) / kSearchWarps;
+  const int64_t cap = (int64_t)ctx->num_sms * 16;
+  if (blocks > cap) blocks = cap;
+  search_kernel<<<(int)blocks, 32 * kSearchWarps, 0, ctx->stream>>>(a);
+  PSG_LAUNCHED(ctx);
+}
+
+// ----------------------------------------------------------------------------
+// Full-D rescoring (optimizer.cpp:117-124, :232-234): one thread per query,
+// j ascending over the window (dy, dx, c) against the candidate's dense
+// exemplar window — the candidate matrix is never materialised.
+__global__ void rescore_windows_kernel(const float* __restrict__ mirror, int img_w, int C, int w,
+                                       const int32_t* __restrict__ xs,
+                                       const int32_t* __restrict__ ys, int nx, int64_t n,
+                                       const float* __restrict__ ex_mirror, int ew, int nxe,
+                                       const int32_t* __restrict__ idx,
+                                       double* __restrict__ dist) {
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    const int ax = xs[a % nx], ay = ys[a / nx];
+    const int32_t id = idx[a];
+    const int ex = id % nxe, ey = id / nxe;
+    const int row = w * C;
+    double acc = 0.0;
+    for (int dy = 0; dy < w; ++dy) {
+      const float* v = mirror + ((int64_t)(ay + dy) * img_w + ax) * C;
+      const float* z = ex_mirror + ((int64_t)(ey + dy) * ew + ex) * C;
+      for (int jj = 0; jj < row; ++jj) {
+        const double t = dsub((double)v[jj], (double)z[jj]);
+        acc = dadd(acc, dmul(t, t));
+      }
+    }
+    dist[a] = sqrt(acc);
+  }
+}
+
+void launch_rescore_windows(psg_ctx* ctx, const float* mirror, int img_w, int C, int w,
+                            AnchorSet anchors, const Index& ix, const int32_t* idx,
+                            double* dist) {
+  if (anchors.count <= 0) return;
+  const int threads = 128;
+  int64_t blocks = (anchors.count + threads - 1) / threads;
+  if (blocks > (int64_t)ctx->num_sms * 32) blocks = (int64_t)ctx->num_sms * 32;
+  rescore_windows_kernel<<<(int)blocks, threads, 0, ctx->stream>>>(
+      mirror, img_w, C, w, anchors.xs, anchors.ys, anchors.nx, anchors.count, ix.ex_mirror,
+      ix.ew, ix.nxe, idx, dist);
+  PSG_LAUNCHED(ctx);
+}
+
+__global__ void rescore_vectors_kernel(const float* __restrict__ Q, int64_t nq, int D,
+                                       const float* __restrict__ X,
+                                       const int32_t* __restrict__ idx,
+                                       double* __restrict__ dist) {
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nq;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    const float* v = Q + a * D;
+    const float* z = X + (int64_t)idx[a] * D;
+    double acc = 0.0;
+    for (int j = 0; j < D; ++j) {
+      const double t = dsub((double)v[j], (double)z[j]);
+      acc = dadd(acc, dmul(t, t));
+    }
+    dist[a] = sqrt(acc);
+  }
+}
+
+void launch_rescore_vectors(psg_ctx* ctx, const float* Q, int64_t nq, const Index& ix,
+                            const int32_t* idx, double* dist) {
+  if (nq <= 0) return;
+  const int threads = 128;
+  int64_t blocks = (nq + threads - 1) / threads;
+  if (blocks > (int64_t)ctx->num_sms * 32) blocks = (int64_t)ctx->num_sms * 32;
+  rescore_vectors_kernel<<<(int)blocks, threads, 0, ctx->stream>>>(Q, nq, ix.D, ix.vectors, idx,
+                                                                    dist);
+  PSG_LAUNCHED(ctx);
+}
+
+// ----------------------------------------------------------------------------
+// proj [N][d] (original order) -> soa [d][N] in leaf order.
+__global__ void gather_soa_kernel(const double* __restrict__ proj, int64_t N, int d,
+                                  const int32_t* __restrict__ perm, double* __restrict__ soa) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N * d;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(i / N);
+    const int64_t pos = i - (int64_t)j * N;
+    soa[i] = proj[(int64_t)perm[pos] * d + j];
+  }
+}
+
+void launch_gather_soa(psg_ctx* ctx, const double* proj, int64_t N, int d, const int32_t* perm,
+                       double* soa) {
+  if (N <= 0 || d <= 0) return;
+  int64_t blocks = (N * d + 255) / 256;
+  if (blocks > (int64_t)ctx->num_sms * 32) blocks = (int64_t)ctx->num_sms * 32;
+  gather_soa_kernel<<<(int)blocks, 256, 0, ctx->stream>>>(proj, N, d, perm, soa);
+  PSG_LAUNCHED(ctx);
+}
+
+}  // namespace psg

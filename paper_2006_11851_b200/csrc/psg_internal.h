@@ -1,0 +1,227 @@
+// Internal declarations shared by the host runtime and the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "persyn_b200.h"
+
+namespace psg {
+
+// ---- error plumbing (status codes of include/persyn_b200.h) -----------------
+struct Error : std::runtime_error {
+  psg_status code;
+  Error(psg_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void fail(psg_status c, const std::string& m) { throw Error(c, m); }
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess)
+    fail(PSG_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" +
+                         std::to_string(line) + ")");
+}
+#define PSG_CUDA(x) ::psg::cuda_check((x), #x, __FILE__, __LINE__)
+#define PSG_LAUNCHED(ctx) \
+  do {                      \
+    PSG_CUDA(cudaGetLastError()); \
+    (ctx)->launches++;      \
+  } while (0)
+
+// Device-side error flags (bit set -> status at the next host check).
+enum DevFlag : int {
+  FLAG_BAD_WEIGHT = 1,     // non-positive / non-finite update weight (optimizer.cpp:367-369)
+  FLAG_UNCOVERED = 2,      // pixel with wsum <= 0 (optimizer.cpp:390-392)
+  FLAG_STACK_OVERFLOW = 4, // traversal stack exhausted (must never happen)
+  FLAG_BAD_DISTANCE = 8,   // negative distance into irls_weight (optimizer.cpp:113)
+};
+
+// Tree in breadth-first layout: children of a node are contiguous.
+struct DevTree {
+  int n_nodes = 0;
+  int max_depth = 0;
+  double* centroid = nullptr;  // [n_nodes][d]
+  double* radius = nullptr;    // [n_nodes]
+  int32_t* first_child = nullptr;
+  int32_t* n_children = nullptr;  // 0 = leaf
+  int32_t* leaf_start = nullptr;  // leaves: range in the leaf-ordered point arrays
+  int32_t* leaf_count = nullptr;
+};
+
+struct HostTree {
+  std::vector<double> centroid, radius;
+  std::vector<int32_t> first_child, n_children, leaf_start, leaf_count, depth;
+  std::vector<int32_t> perm;  // leaf order -> point id
+  int max_depth = 0;
+  int n_leaves = 0;
+};
+
+// Per-stage index: exemplar level + PCA model + projected DB + tree.
+struct Index {
+  psg_ctx* ctx = nullptr;
+  bool from_vectors = false;
+  int C = 0, w = 0, ew = 0, eh = 0, D = 0, d = 0;
+  int64_t N = 0;
+  int nxe = 0;              // dense DB anchors per row (ew - w + 1)
+  float* ex_mirror = nullptr;  // [eh][ew][C] fp32 (image index)
+  float* vectors = nullptr;    // [N][D] fp32 (vector index)
+  double* mean = nullptr;      // [D]
+  double* basis = nullptr;     // [d][D]
+  double* proj = nullptr;      // [N][d] original order
+  double* proj_soa = nullptr;  // [d][N] leaf order
+  int32_t* perm = nullptr;     // leaf order -> id
+  DevTree tree;
+  HostTree htree;
+  std::vector<double> h_mean, h_basis, h_var;
+  // exemplar histogram
+  int hist_bins = 0, hist_slots = 0;
+  std::vector<double> h_ex_hist;
+  double* ex_hist = nullptr;
+  ~Index();
+};
+
+}  // namespace psg
+
+struct psg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int64_t launches = 0;
+  int num_sms = 148;
+  // cuBLAS / cuSOLVER handles (opaque here, created lazily by pca.cpp)
+  void* cublas = nullptr;
+  void* cusolver = nullptr;
+  // pinned staging
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  int* d_flags = nullptr;
+};
+
+struct psg_index {
+  psg::Index impl;
+};
+
+namespace psg {
+
+// ---- kernel launchers (kernels_*.cu) ------------------------------------------
+struct AnchorSet {
+  const int32_t* xs;  // device [nx]
+  const int32_t* ys;  // device [ny]
+  int nx;
+  int64_t count;      // nx * ny
+};
+
+// planes [C][H][W] fp64 -> mirror [H][W][C] fp32
+void launch_make_mirror(psg_ctx* ctx, const double* planes, int C, int W, int H, float* mirror);
+// Exact fp64 projection of window features (pca.cpp:27-41).
+void launch_project_windows(psg_ctx* ctx, const float* mirror, int img_w, int C, int w,
+                            AnchorSet anchors, const double* mean, const double* basis, int d,
+                            double* out);
+void launch_project_vectors(psg_ctx* ctx, const float* X, int64_t n, int D, const double* mean,
+                            const double* basis, int d, double* out);
+// Exact NN search over the tree (km_tree.cpp:197-284 semantics).
+struct SearchArgs {
+  const double* q;      // [nq][d]
+  int64_t nq;
+  int d;
+  const int32_t* seed_idx;  // optional initial candidate per query (upper bound)
+  const double* proj;       // [N][d] original order (seed distances)
+  const double* proj_soa;   // [d][N] leaf order
+  const int32_t* perm;
+  int64_t N;
+  DevTree tree;
+  int mode, max_leaves;
+  int32_t* out_idx;
+  double* out_d2;
+  int64_t* out_scanned;
+  int* flags;
+};
+void launch_search(psg_ctx* ctx, const SearchArgs& a);
+// Full-D distance between query windows and assigned candidates (optimizer.cpp:117-124).
+void launch_rescore_windows(psg_ctx* ctx, const float* mirror, int img_w, int C, int w,
+                            AnchorSet anchors, const Index& ix, const int32_t* idx, double* dist);
+void launch_rescore_vectors(psg_ctx* ctx, const float* Q, int64_t nq, const Index& ix,
+                            const int32_t* idx, double* dist);
+// M-step pieces.
+struct WeightArgs {
+  const double* dist;
+  const int32_t* idx;
+  const double* pen;   // may be null
+  int64_t A;
+  double r, eps;
+  double* irls;        // out
+  double* eff;         // out: irls / (1 + pen)
+  int* flags;
+};
+void launch_weights(psg_ctx* ctx, const WeightArgs& a);
+void launch_eff_from(psg_ctx* ctx, const double* irls, const double* pen, int64_t A, double* eff,
+                     int* flags);
+void launch_hist_count(psg_ctx* ctx, const double* planes, int64_t P, int bins, int slots,
+                       unsigned long long* counts);
+void launch_hist_fold(psg_ctx* ctx, const unsigned long long* counts, int bins, int slots,
+                      int64_t P, const double* ex_mass, double* mass, double* excess);
+void launch_penalty(psg_ctx* ctx, const Index& ix, const int32_t* idx, int64_t A,
+                    const double* excess, int bins, int slots, double* pen);
+struct MstepArgs {
+  const int32_t* xs;
+  const int32_t* ys;
+  int nx, ny;
+  const int32_t* col_lo;  // [W] covering-anchor column range
+  const int32_t* col_hi;
+  const int32_t* row_lo;  // [H]
+  const int32_t* row_hi;
+  const int32_t* idx;     // [A]
+  const double* eff;      // [A]
+  int W, H, C, w;
+  const float* ex_mirror;
+  int ew, nxe;
+  double* planes;  // out [C][H][W]
+  float* mirror;   // out [H][W][C]
+  int* flags;
+};
+void launch_mstep(psg_ctx* ctx, const MstepArgs& a);
+// Deterministic reductions for telemetry.
+struct StatsArgs {
+  const double* cur_dist;   // distances the weights came from
+  const double* after_dist; // distances after update (fixed assignment)
+  const double* eff;
+  const double* next_dist;
+  const int32_t* cur_idx;
+  const int32_t* next_idx;
+  const int64_t* scanned;
+  const int32_t* mult;
+  int64_t A;
+  double r;
+  double* out;  // [6]: lsq_before, lsq_after, energy, changed, scanned_plan, unique_scanned
+};
+void launch_stats(psg_ctx* ctx, const StatsArgs& a);
+// PCA helpers.
+void launch_window_mean(psg_ctx* ctx, const float* mirror, int img_w, int C, int w, int nxe,
+                        int64_t N, double* mean);
+void launch_center_windows(psg_ctx* ctx, const float* mirror, int img_w, int C, int w, int nxe,
+                           int64_t N, const double* mean, double* Xc);
+void launch_vector_mean(psg_ctx* ctx, const float* X, int64_t N, int D, double* mean);
+void launch_center_vectors(psg_ctx* ctx, const float* X, int64_t N, int D, const double* mean,
+                           double* Xc);
+void launch_gather_soa(psg_ctx* ctx, const double* proj, int64_t N, int d, const int32_t* perm,
+                       double* soa);
+// Pyramid helpers.
+void launch_downsample(psg_ctx* ctx, const double* in, int W, int H, int f, double* out);
+void launch_upsample_bilinear(psg_ctx* ctx, const double* in, int W, int H, int f, double* out);
+void launch_fit_to(psg_ctx* ctx, const double* in, int W, int H, int ow, int oh, double* out);
+
+// ---- host pieces --------------------------------------------------------------
+HostTree build_tree_host(const double* proj, int64_t N, int d, int branching, int max_depth,
+                         int leaf_threshold, uint64_t seed);
+void fit_pca_device(psg_ctx* ctx, Index& ix, const psg_index_cfg& cfg);
+int64_t plan_host(int W, int H, int w, int sp, int p, int32_t* mult);
+std::vector<int32_t> axis_positions(int extent, int window, int step);
+
+// Correctly-rounded (double-double) pow used for the IRLS weight; exposed on
+// the host for tests via psg_pow_cr.
+double pow_cr_host(double x, double y);
+
+}  // namespace psg

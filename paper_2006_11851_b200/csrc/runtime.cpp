@@ -1,0 +1,1148 @@
+// Native host runtime + C ABI (include/persyn_b200.h).
+//
+// Owns device memory, the stream, the per-stage index build, the EM loop
+// (optimize_level, optimizer.cpp:426-516), the pyramid driver
+// (synthesize, pipeline.cpp:216-315) and the status/last-error convention.
+// All arithmetic on the hot path runs in the sm_100a kernels; the host only
+// orchestrates, validates arguments the way the reference does, and reads
+// back one small telemetry record per EM iteration (the reference's
+// convergence rule needs `changed` on the host).
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "numerics.cuh"
+#include "psg_internal.h"
+
+namespace psg {
+
+namespace {
+thread_local std::string g_last_error;
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  explicit DBuf(size_t count) { alloc(count); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+    return *this;
+  }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) PSG_CUDA(cudaMalloc(&p, sizeof(T) * count));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { release(); }
+  void upload(psg_ctx* ctx, const T* h, size_t count) {
+    if (count) PSG_CUDA(cudaMemcpyAsync(p, h, sizeof(T) * count, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  void download(psg_ctx* ctx, T* h, size_t count) const {
+    if (count) PSG_CUDA(cudaMemcpyAsync(h, p, sizeof(T) * count, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+};
+
+template <class T>
+T* dalloc(size_t count) {
+  T* p = nullptr;
+  if (count) PSG_CUDA(cudaMalloc(&p, sizeof(T) * count));
+  return p;
+}
+
+void check_flags(psg_ctx* ctx) {
+  int f = 0;
+  PSG_CUDA(cudaMemcpyAsync(&f, ctx->d_flags, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (!f) return;
+  PSG_CUDA(cudaMemsetAsync(ctx->d_flags, 0, sizeof(int), ctx->stream));
+  if (f & FLAG_BAD_DISTANCE) fail(PSG_E_DOMAIN, "distance must be non-negative");
+  if (f & FLAG_BAD_WEIGHT) fail(PSG_E_DOMAIN, "non-positive or non-finite update weight");
+  if (f & FLAG_UNCOVERED) fail(PSG_E_LOGIC, "output pixel not covered by any window");
+  if (f & FLAG_STACK_OVERFLOW) fail(PSG_E_LOGIC, "tree traversal stack overflow");
+}
+
+void validate_grid(int w, int sp, int W, int H) {  // neighborhood.cpp:22-35
+  if (w < 2) fail(PSG_E_DOMAIN, "neighborhood width must be >= 2");
+  if (w % 2 != 0) fail(PSG_E_DOMAIN, "neighborhood width must be even");
+  if (sp < 1) fail(PSG_E_DOMAIN, "grid spacing must be >= 1");
+  if (sp > w) fail(PSG_E_DOMAIN, "grid spacing larger than the neighborhood width");
+  if (W < w || H < w)
+    fail(PSG_E_DOMAIN, "image " + std::to_string(W) + "x" + std::to_string(H) +
+                           " smaller than the neighborhood window " + std::to_string(w));
+}
+
+void validate_cfg(const psg_opt_cfg& c, int w, int W, int H) {  // optimizer.cpp:24-42
+  if (!(c.robust_exponent > 0.0 && c.robust_exponent < 2.0))
+    fail(PSG_E_DOMAIN, "robust exponent must be in (0, 2)");
+  if (!(c.distance_epsilon > 0.0)) fail(PSG_E_DOMAIN, "epsilon must be positive");
+  if (c.max_iterations < 1) fail(PSG_E_DOMAIN, "max iterations must be >= 1");
+  if (c.min_iterations < 1 || c.min_iterations > c.max_iterations)
+    fail(PSG_E_DOMAIN, "min iterations must be in [1, max_iterations]");
+  if (!(c.convergence_fraction > 0.0 && c.convergence_fraction < 1.0))
+    fail(PSG_E_DOMAIN, "convergence fraction must be in (0, 1)");
+  if (c.histogram_bins < 2) fail(PSG_E_DOMAIN, "histogram bins must be >= 2");
+  validate_grid(w, c.spacing, W, H);
+  if (c.patch_width < 1) fail(PSG_E_DOMAIN, "patch width must be >= 1");
+  if (c.patch_width > c.spacing) fail(PSG_E_DOMAIN, "patch width must not exceed the grid spacing");
+  if (c.budget.mode < 0 || c.budget.mode > 2) fail(PSG_E_DOMAIN, "unknown query budget mode");
+  if (c.budget.mode == PSG_BACKTRACK && c.budget.max_leaves < 1)
+    fail(PSG_E_DOMAIN, "backtrack budget must be >= 1");
+}
+
+void validate_budget(const psg_budget& b) {
+  if (b.mode < 0 || b.mode > 2) fail(PSG_E_DOMAIN, "unknown query budget mode");
+  if (b.mode == PSG_BACKTRACK && b.max_leaves < 1) fail(PSG_E_DOMAIN, "backtrack budget must be >= 1");
+}
+
+double now_ms() {
+  using namespace std::chrono;
+  return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace
+
+std::vector<int32_t> axis_positions(int extent, int window, int step) {  // neighborhood.cpp:12-18
+  std::vector<int32_t> xs;
+  for (int p = 0; p + window <= extent; p += step) xs.push_back(p);
+  const int last = extent - window;
+  if (xs.empty() || xs.back() != last) xs.push_back(last);
+  return xs;
+}
+
+int64_t plan_host(int W, int H, int w, int sp, int p, int32_t* mult) {
+  const auto xs = axis_positions(W, w, sp), ys = axis_positions(H, w, sp);
+  const auto tx = axis_positions(W, p, p), ty = axis_positions(H, p, p);
+  auto count_in = [](const std::vector<int32_t>& v, int lo, int hi) {
+    return (int64_t)(std::upper_bound(v.begin(), v.end(), hi) -
+                     std::lower_bound(v.begin(), v.end(), lo));
+  };
+  int64_t cx = 0, cy = 0;
+  for (int t : tx) cx += count_in(xs, t + p - w, t);
+  for (int t : ty) cy += count_in(ys, t + p - w, t);
+  bool uncovered = false;
+  std::vector<int64_t> mx(xs.size()), my(ys.size());
+  for (size_t i = 0; i < xs.size(); ++i) mx[i] = count_in(tx, xs[i], xs[i] + w - p);
+  for (size_t i = 0; i < ys.size(); ++i) my[i] = count_in(ty, ys[i], ys[i] + w - p);
+  for (size_t iy = 0; iy < ys.size(); ++iy)
+    for (size_t ix = 0; ix < xs.size(); ++ix) {
+      const int64_t m = mx[ix] * my[iy];
+      if (mult) mult[iy * xs.size() + ix] = (int32_t)m;
+      if (m == 0) uncovered = true;
+    }
+  return uncovered ? -1 : cx * cy;
+}
+
+double pow_cr_host(double x, double y) { return pow_cr(x, y); }
+
+Index::~Index() {
+  cudaFree(ex_mirror);
+  cudaFree(vectors);
+  cudaFree(mean);
+  cudaFree(basis);
+  cudaFree(proj);
+  cudaFree(proj_soa);
+  cudaFree(perm);
+  cudaFree(tree.centroid);
+  cudaFree(tree.radius);
+  cudaFree(tree.first_child);
+  cudaFree(tree.n_children);
+  cudaFree(tree.leaf_start);
+  cudaFree(tree.leaf_count);
+  cudaFree(ex_hist);
+}
+
+// ---------------------------------------------------------------------------
+// Index build (PcaTreeIndex ctor, optimizer.cpp:216-224, per stage
+// pipeline.cpp:276-292).
+namespace {
+
+void finish_index(psg_ctx* ctx, Index& ix, const double* mean, const double* basis, int d,
+                  const psg_index_cfg& cfg) {
+  const int D = ix.D;
+  if (basis) {
+    if (d < 0 || d > 64) fail(PSG_E_DOMAIN, "injected PCA dimension must be in [0, 64]");
+    ix.h_mean.assign(mean, mean + D);
+    ix.h_basis.assign(basis, basis + (size_t)d * D);
+    ix.h_var.assign(D, 0.0);
+    ix.d = d;
+  } else {
+    fit_pca_device(ctx, ix, cfg);
+  }
+  d = ix.d;
+  ix.mean = dalloc<double>(D);
+  PSG_CUDA(cudaMemcpyAsync(ix.mean, ix.h_mean.data(), sizeof(double) * D, cudaMemcpyHostToDevice,
+                           ctx->stream));
+  // transposed, zero-padded basis [D][KP] for the projection kernel
+  const int KP = d <= 32 ? 32 : 64;
+  std::vector<double> bt((size_t)D * KP, 0.0);
+  for (int k = 0; k < d; ++k)
+    for (int j = 0; j < D; ++j) bt[(size_t)j * KP + k] = ix.h_basis[(size_t)k * D + j];
+  ix.basis = dalloc<double>(bt.size());
+  PSG_CUDA(cudaMemcpyAsync(ix.basis, bt.data(), sizeof(double) * bt.size(), cudaMemcpyHostToDevice,
+                           ctx->stream));
+  // project the database (pca.cpp:103-113)
+  ix.proj = dalloc<double>((size_t)ix.N * (d > 0 ? d : 1));
+  if (d > 0) {
+    if (ix.from_vectors) {
+      launch_project_vectors(ctx, ix.vectors, ix.N, D, ix.mean, ix.basis, d, ix.proj);
+    } else {
+      DBuf<int32_t> xs(ix.nxe), ys(ix.eh - ix.w + 1);
+      std::vector<int32_t> hx(ix.nxe), hy(ix.eh - ix.w + 1);
+      for (int i = 0; i < ix.nxe; ++i) hx[i] = i;
+      for (int i = 0; i < ix.eh - ix.w + 1; ++i) hy[i] = i;
+      xs.upload(ctx, hx.data(), hx.size());
+      ys.upload(ctx, hy.data(), hy.size());
+      AnchorSet as{xs.p, ys.p, ix.nxe, ix.N};
+      launch_project_windows(ctx, ix.ex_mirror, ix.ew, ix.C, ix.w, as, ix.mean, ix.basis, d,
+                             ix.proj);
+      PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+  }
+  // tree (host-native build over the device-projected points)
+  std::vector<double> hp((size_t)ix.N * d);
+  if (d > 0)
+    PSG_CUDA(cudaMemcpyAsync(hp.data(), ix.proj, sizeof(double) * hp.size(),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+  PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+  ix.htree = build_tree_host(hp.data(), ix.N, d, cfg.branching, cfg.max_depth,
+                             cfg.leaf_threshold > 0 ? cfg.leaf_threshold : cfg.branching, cfg.seed);
+  const HostTree& t = ix.htree;
+  const int nn = (int)t.radius.size();
+  ix.tree.n_nodes = nn;
+  ix.tree.max_depth = t.max_depth;
+  ix.tree.centroid = dalloc<double>((size_t)nn * (d > 0 ? d : 1));
+  ix.tree.radius = dalloc<double>(nn);
+  ix.tree.first_child = dalloc<int32_t>(nn);
+  ix.tree.n_children = dalloc<int32_t>(nn);
+  ix.tree.leaf_start = dalloc<int32_t>(nn);
+  ix.tree.leaf_count = dalloc<int32_t>(nn);
+  auto up = [&](auto* dst, const auto& v) {
+    if (!v.empty())
+      PSG_CUDA(cudaMemcpyAsync(dst, v.data(), sizeof(v[0]) * v.size(), cudaMemcpyHostToDevice,
+                               ctx->stream));
+  };
+  up(ix.tree.centroid, t.centroid);
+  up(ix.tree.radius, t.radius);
+  up(ix.tree.first_child, t.first_child);
+  up(ix.tree.n_children, t.n_children);
+  up(ix.tree.leaf_start, t.leaf_start);
+  up(ix.tree.leaf_count, t.leaf_count);
+  ix.perm = dalloc<int32_t>(ix.N);
+  up(ix.perm, t.perm);
+  ix.proj_soa = dalloc<double>((size_t)ix.N * (d > 0 ? d : 1));
+  launch_gather_soa(ctx, ix.proj, ix.N, d, ix.perm, ix.proj_soa);
+  PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void build_exemplar_hist(psg_ctx* ctx, Index& ix, const double* ex_planes_dev, int bins,
+                         int include_scale) {
+  if (bins <= 0 || ix.from_vectors) return;
+  if (bins < 2) fail(PSG_E_DOMAIN, "histogram bins must be >= 2");
+  ix.hist_bins = bins;
+  ix.hist_slots = include_scale ? ix.C : 3;
+  const int n = bins * ix.hist_slots;
+  DBuf<unsigned long long> counts(n);
+  ix.ex_hist = dalloc<double>(n);
+  const int64_t P = (int64_t)ix.ew * ix.eh;
+  launch_hist_count(ctx, ex_planes_dev, P, bins, ix.hist_slots, counts.p);
+  launch_hist_fold(ctx, counts.p, bins, ix.hist_slots, P, nullptr, ix.ex_hist, nullptr);
+  ix.h_ex_hist.resize(n);
+  PSG_CUDA(cudaMemcpyAsync(ix.h_ex_hist.data(), ix.ex_hist, sizeof(double) * n,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+  PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+std::unique_ptr<psg_index> create_index_from_device_planes(psg_ctx* ctx, const double* ex_dev,
+                                                           int C, int ew, int eh, int w,
+                                                           const double* mean,
+                                                           const double* basis, int d,
+                                                           const psg_index_cfg& cfg) {
+  if (C < 4 || C > 8) fail(PSG_E_SHAPE, "channels must be 3 + G with G in [1, 5]");
+  if (w < 2 || w % 2) fail(PSG_E_DOMAIN, "neighborhood width must be even and >= 2");
+  if (ew < w || eh < w) fail(PSG_E_DOMAIN, "exemplar smaller than the neighborhood window");
+  if (cfg.branching < 2) fail(PSG_E_DOMAIN, "tree branching must be >= 2");
+  auto h = std::make_unique<psg_index>();
+  Index& ix = h->impl;
+  ix.ctx = ctx;
+  ix.C = C;
+  ix.w = w;
+  ix.ew = ew;
+  ix.eh = eh;
+  ix.D = w * w * C;
+  ix.nxe = ew - w + 1;
+  ix.N = (int64_t)ix.nxe * (eh - w + 1);
+  ix.ex_mirror = dalloc<float>((size_t)ew * eh * C);
+  launch_make_mirror(ctx, ex_dev, C, ew, eh, ix.ex_mirror);
+  build_exemplar_hist(ctx, ix, ex_dev, cfg.hist_bins, cfg.hist_include_scale);
+  finish_index(ctx, ix, mean, basis, d, cfg);
+  return h;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Level: device-resident EM state for one stage (optimize_level).
+}  // namespace psg
+
+struct psg_level {
+  psg_ctx* ctx = nullptr;
+  const psg::Index* ix = nullptr;
+  int W = 0, H = 0, C = 0, w = 0;
+  psg_opt_cfg cfg{};
+  int nx = 0, ny = 0;
+  int64_t A = 0, P = 0, nn_calls = 0;
+  psg::DBuf<int32_t> xs, ys, col_lo, col_hi, row_lo, row_hi, mult;
+  psg::DBuf<double> planes;
+  psg::DBuf<float> mirror;
+  psg::DBuf<double> qproj, d2, cur_dist, next_dist, irls, pen, eff, after;
+  psg::DBuf<int32_t> cur_idx, next_idx;
+  psg::DBuf<int64_t> scanned;
+  psg::DBuf<unsigned long long> counts;
+  psg::DBuf<double> out_mass, excess, ex_hist, stats_dev;
+  double* stats_host = nullptr;  // pinned [6]
+  bool hist_on = false;
+  int slots = 3;
+  bool primed = false;
+  int iter = 0;
+  int64_t pending_calls = 0, pending_scanned = 0;
+  double pending_ms = 0.0;
+  int64_t unique_queries = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  ~psg_level() {
+    if (stats_host) cudaFreeHost(stats_host);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+  }
+};
+
+namespace psg {
+namespace {
+
+void level_setup(psg_level& L, psg_ctx* ctx, const Index& ix, int W, int H,
+                 const psg_opt_cfg& cfg, bool full) {
+  L.ctx = ctx;
+  L.ix = &ix;
+  L.W = W;
+  L.H = H;
+  L.C = ix.C;
+  L.w = ix.w;
+  L.cfg = cfg;
+  const int w = ix.w, sp = cfg.spacing;
+  const auto hx = axis_positions(W, w, sp), hy = axis_positions(H, w, sp);
+  L.nx = (int)hx.size();
+  L.ny = (int)hy.size();
+  L.A = (int64_t)L.nx * L.ny;
+  L.P = (int64_t)W * H;
+  L.xs.alloc(L.nx);
+  L.ys.alloc(L.ny);
+  L.xs.upload(ctx, hx.data(), hx.size());
+  L.ys.upload(ctx, hy.data(), hy.size());
+  // covering-anchor ranges per column / row: anchors a with a <= x < a + w
+  auto ranges = [&](const std::vector<int32_t>& v, int extent, std::vector<int32_t>& lo,
+                    std::vector<int32_t>& hi) {
+    lo.resize(extent);
+    hi.resize(extent);
+    for (int x = 0; x < extent; ++x) {
+      lo[x] = (int32_t)(std::lower_bound(v.begin(), v.end(), x - w + 1) - v.begin());
+      hi[x] = (int32_t)(std::upper_bound(v.begin(), v.end(), x) - v.begin());
+    }
+  };
+  std::vector<int32_t> cl, ch, rl, rh;
+  ranges(hx, W, cl, ch);
+  ranges(hy, H, rl, rh);
+  L.col_lo.alloc(W);
+  L.col_hi.alloc(W);
+  L.row_lo.alloc(H);
+  L.row_hi.alloc(H);
+  L.col_lo.upload(ctx, cl.data(), W);
+  L.col_hi.upload(ctx, ch.data(), W);
+  L.row_lo.upload(ctx, rl.data(), H);
+  L.row_hi.upload(ctx, rh.data(), H);
+  L.planes.alloc((size_t)L.P * L.C);
+  L.mirror.alloc((size_t)L.P * L.C);
+  L.cur_idx.alloc(L.A);
+  L.cur_dist.alloc(L.A);
+  L.irls.alloc(L.A);
+  L.pen.alloc(L.A);
+  L.eff.alloc(L.A);
+  if (!full) return;
+  std::vector<int32_t> m(L.A);
+  L.nn_calls = plan_host(W, H, w, sp, cfg.patch_width, m.data());
+  if (L.nn_calls < 0) fail(PSG_E_LOGIC, "anchor not covered by any patch tile");
+  L.mult.alloc(L.A);
+  L.mult.upload(ctx, m.data(), L.A);
+  L.qproj.alloc((size_t)L.A * (ix.d > 0 ? ix.d : 1));
+  L.d2.alloc(L.A);
+  L.next_idx.alloc(L.A);
+  L.next_dist.alloc(L.A);
+  L.after.alloc(L.A);
+  L.scanned.alloc(L.A);
+  L.stats_dev.alloc(8);
+  PSG_CUDA(cudaMallocHost(&L.stats_host, sizeof(double) * 8));
+  PSG_CUDA(cudaEventCreate(&L.ev0));
+  PSG_CUDA(cudaEventCreate(&L.ev1));
+}
+
+void level_set_hist(psg_level& L, const double* ex_hist_host) {
+  const Index& ix = *L.ix;
+  L.hist_on = L.cfg.histogram_matching != 0 && (ex_hist_host || ix.ex_hist);
+  if (!L.hist_on) return;
+  L.slots = L.cfg.histogram_include_scale ? L.C : 3;
+  const int n = L.cfg.histogram_bins * L.slots;
+  L.ex_hist.alloc(n);
+  if (ex_hist_host) {
+    L.ex_hist.upload(L.ctx, ex_hist_host, n);
+  } else {
+    if (ix.hist_bins != L.cfg.histogram_bins || ix.hist_slots != L.slots)
+      fail(PSG_E_SHAPE, "output/exemplar histograms disagree on bins or channels");
+    PSG_CUDA(cudaMemcpyAsync(L.ex_hist.p, ix.ex_hist, sizeof(double) * n,
+                             cudaMemcpyDeviceToDevice, L.ctx->stream));
+  }
+  L.counts.alloc(n);
+  L.out_mass.alloc(n);
+  L.excess.alloc(n);
+}
+
+// E-step over all anchors of the level's current image.
+void level_search(psg_level& L, bool seeded, int32_t* out_idx, double* out_dist) {
+  psg_ctx* ctx = L.ctx;
+  const Index& ix = *L.ix;
+  AnchorSet as{L.xs.p, L.ys.p, L.nx, L.A};
+  if (ix.d > 0)
+    launch_project_windows(ctx, L.mirror.p, L.W, L.C, L.w, as, ix.mean, ix.basis, ix.d, L.qproj.p);
+  SearchArgs a{};
+  a.q = L.qproj.p;
+  a.nq = L.A;
+  a.d = ix.d;
+  a.seed_idx = (seeded && L.cfg.budget.mode == PSG_EXACT) ? L.cur_idx.p : nullptr;
+  a.proj = ix.proj;
+  a.proj_soa = ix.proj_soa;
+  a.perm = ix.perm;
+  a.N = ix.N;
+  a.tree = ix.tree;
+  a.mode = L.cfg.budget.mode;
+  a.max_leaves = L.cfg.budget.max_leaves;
+  a.out_idx = out_idx;
+  a.out_d2 = L.d2.p;
+  a.out_scanned = L.scanned.p;
+  a.flags = ctx->d_flags;
+  launch_search(ctx, a);
+  launch_rescore_windows(ctx, L.mirror.p, L.W, L.C, L.w, as, ix, out_idx, out_dist);
+  L.unique_queries += L.A;
+}
+
+void level_read_stats(psg_level& L) {
+  L.stats_dev.download(L.ctx, L.stats_host, 6);
+  PSG_CUDA(cudaEventRecord(L.ev1, L.ctx->stream));
+  check_flags(L.ctx);  // synchronizes the stream
+}
+
+void level_prime(psg_level& L) {
+  if (L.primed) return;
+  psg_ctx* ctx = L.ctx;
+  PSG_CUDA(cudaEventRecord(L.ev0, ctx->stream));
+  level_search(L, false, L.cur_idx.p, L.cur_dist.p);
+  StatsArgs s{};
+  s.scanned = L.scanned.p;
+  s.mult = L.mult.p;
+  s.A = L.A;
+  s.r = L.cfg.robust_exponent;
+  s.out = L.stats_dev.p;
+  launch_stats(ctx, s);
+  level_read_stats(L);
+  float ms = 0.f;
+  PSG_CUDA(cudaEventElapsedTime(&ms, L.ev0, L.ev1));
+  L.pending_calls = L.nn_calls;
+  L.pending_scanned = (int64_t)L.stats_host[4];
+  L.pending_ms = ms;
+  L.primed = true;
+}
+
+MstepArgs mstep_args(psg_level& L) {
+  const Index& ix = *L.ix;
+  MstepArgs m{};
+  m.xs = L.xs.p;
+  m.ys = L.ys.p;
+  m.nx = L.nx;
+  m.ny = L.ny;
+  m.col_lo = L.col_lo.p;
+  m.col_hi = L.col_hi.p;
+  m.row_lo = L.row_lo.p;
+  m.row_hi = L.row_hi.p;
+  m.idx = L.cur_idx.p;
+  m.eff = L.eff.p;
+  m.W = L.W;
+  m.H = L.H;
+  m.C = L.C;
+  m.w = L.w;
+  m.ex_mirror = ix.ex_mirror;
+  m.ew = ix.ew;
+  m.nxe = ix.nxe;
+  m.planes = L.planes.p;
+  m.mirror = L.mirror.p;
+  m.flags = L.ctx->d_flags;
+  return m;
+}
+
+// One EM iteration (optimizer.cpp:450-513).  Returns true when converged.
+bool level_step(psg_level& L, psg_iter_stats* st, bool honor) {
+  psg_ctx* ctx = L.ctx;
+  const Index& ix = *L.ix;
+  PSG_CUDA(cudaEventRecord(L.ev0, ctx->stream));
+  WeightArgs wa{};
+  wa.dist = L.cur_dist.p;
+  wa.idx = L.cur_idx.p;
+  wa.pen = nullptr;
+  wa.A = L.A;
+  wa.r = L.cfg.robust_exponent;
+  wa.eps = L.cfg.distance_epsilon;
+  wa.irls = L.irls.p;
+  wa.eff = L.eff.p;
+  wa.flags = ctx->d_flags;
+  launch_weights(ctx, wa);
+  if (L.hist_on) {
+    const int bins = L.cfg.histogram_bins;
+    launch_hist_count(ctx, L.planes.p, L.P, bins, L.slots, L.counts.p);
+    launch_hist_fold(ctx, L.counts.p, bins, L.slots, L.P, L.ex_hist.p, L.out_mass.p, L.excess.p);
+    launch_penalty(ctx, ix, L.cur_idx.p, L.A, L.excess.p, bins, L.slots, L.pen.p);
+    launch_eff_from(ctx, L.irls.p, L.pen.p, L.A, L.eff.p, ctx->d_flags);
+  }
+  launch_mstep(ctx, mstep_args(L));
+  AnchorSet as{L.xs.p, L.ys.p, L.nx, L.A};
+  launch_rescore_windows(ctx, L.mirror.p, L.W, L.C, L.w, as, ix, L.cur_idx.p, L.after.p);
+  level_search(L, true, L.next_idx.p, L.next_dist.p);
+  StatsArgs s{};
+  s.cur_dist = L.cur_dist.p;
+  s.after_dist = L.after.p;
+  s.eff = L.eff.p;
+  s.next_dist = L.next_dist.p;
+  s.cur_idx = L.cur_idx.p;
+  s.next_idx = L.next_idx.p;
+  s.scanned = L.scanned.p;
+  s.mult = L.mult.p;
+  s.A = L.A;
+  s.r = L.cfg.robust_exponent;
+  s.out = L.stats_dev.p;
+  launch_stats(ctx, s);
+  level_read_stats(L);
+  float ms = 0.f;
+  PSG_CUDA(cudaEventElapsedTime(&ms, L.ev0, L.ev1));
+  ++L.iter;
+  const int64_t changed = (int64_t)L.stats_host[3];
+  if (st) {
+    st->iteration = L.iter;
+    st->energy = L.stats_host[2];
+    st->changed = changed;
+    st->nn_calls = L.nn_calls + L.pending_calls;
+    st->millis = ms + L.pending_ms;
+    st->lsq_energy_before = L.stats_host[0];
+    st->lsq_energy_after = L.stats_host[1];
+    st->points_scanned = (int64_t)L.stats_host[4] + L.pending_scanned;
+    st->unique_queries = L.A * (L.pending_calls ? 2 : 1);
+  }
+  L.pending_calls = 0;
+  L.pending_scanned = 0;
+  L.pending_ms = 0.0;
+  std::swap(L.cur_idx, L.next_idx);
+  std::swap(L.cur_dist, L.next_dist);
+  return honor && L.iter >= L.cfg.min_iterations &&
+         (double)changed < L.cfg.convergence_fraction * (double)L.A;
+}
+
+void upload_state(psg_level& L, const double* host_planes) {
+  L.planes.upload(L.ctx, host_planes, (size_t)L.P * L.C);
+  launch_make_mirror(L.ctx, L.planes.p, L.C, L.W, L.H, L.mirror.p);
+}
+
+}  // namespace
+}  // namespace psg
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using psg::fail;
+
+template <class F>
+static psg_status guarded(F&& f) {
+  try {
+    f();
+    return PSG_OK;
+  } catch (const psg::Error& e) {
+    psg::g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    psg::g_last_error = std::string("allocation failure: ") + e.what();
+    return PSG_E_CUDA;
+  } catch (const std::exception& e) {
+    psg::g_last_error = e.what();
+    return PSG_E_LOGIC;
+  }
+}
+
+extern "C" {
+
+const char* psg_last_error(void) { return psg::g_last_error.c_str(); }
+int psg_abi_version(void) { return PSG_ABI_VERSION; }
+
+psg_status psg_ctx_create(int device, void* stream, psg_ctx** out) {
+  return guarded([&] {
+    if (!out) fail(PSG_E_DOMAIN, "null output handle");
+    *out = nullptr;
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+      fail(PSG_E_CUDA, std::string("no CUDA device available: ") + cudaGetErrorString(e));
+    if (device < 0 || device >= n) fail(PSG_E_DOMAIN, "device ordinal out of range");
+    PSG_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    PSG_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      fail(PSG_E_CUDA, "persyn_b200 is built for sm_100a (B200); device reports sm_" +
+                           std::to_string(prop.major) + std::to_string(prop.minor));
+    auto c = std::make_unique<psg_ctx>();
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    if (stream) {
+      c->stream = static_cast<cudaStream_t>(stream);
+    } else {
+      PSG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    PSG_CUDA(cudaMalloc(&c->d_flags, sizeof(int)));
+    PSG_CUDA(cudaMemsetAsync(c->d_flags, 0, sizeof(int), c->stream));
+    *out = c.release();
+  });
+}
+
+void psg_ctx_destroy(psg_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->cublas) cublasDestroy(static_cast<cublasHandle_t>(ctx->cublas));
+  if (ctx->cusolver) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(ctx->cusolver));
+  cudaFree(ctx->d_flags);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+psg_status psg_ctx_synchronize(psg_ctx* ctx) {
+  return guarded([&] { PSG_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+
+int64_t psg_ctx_launch_count(const psg_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+psg_status psg_index_create(psg_ctx* ctx, const double* ex_planes, int C, int ew, int eh, int w,
+                            const double* mean, const double* basis, int d,
+                            const psg_index_cfg* cfg, psg_index** out) {
+  return guarded([&] {
+    if (!ctx || !ex_planes || !cfg || !out) fail(PSG_E_DOMAIN, "null argument");
+    *out = nullptr;
+    if (ew < 1 || eh < 1) fail(PSG_E_DOMAIN, "empty exemplar");
+    psg::DBuf<double> ex((size_t)C * ew * eh);
+    ex.upload(ctx, ex_planes, ex.n);
+    auto h = psg::create_index_from_device_planes(ctx, ex.p, C, ew, eh, w, mean, basis, d, *cfg);
+    *out = h.release();
+  });
+}
+
+psg_status psg_index_create_vectors(psg_ctx* ctx, const float* X, int64_t n, int D,
+                                    const double* mean, const double* basis, int d,
+                                    const psg_index_cfg* cfg, psg_index** out) {
+  return guarded([&] {
+    if (!ctx || !X || !cfg || !out) fail(PSG_E_DOMAIN, "null argument");
+    *out = nullptr;
+    if (n < 1) fail(PSG_E_DOMAIN, "empty candidate set");
+    if (D < 1) fail(PSG_E_DOMAIN, "vector dimension must be >= 1");
+    auto h = std::make_unique<psg_index>();
+    psg::Index& ix = h->impl;
+    ix.ctx = ctx;
+    ix.from_vectors = true;
+    ix.D = D;
+    ix.N = n;
+    ix.nxe = 1;
+    ix.vectors = psg::dalloc<float>((size_t)n * D);
+    PSG_CUDA(cudaMemcpyAsync(ix.vectors, X, sizeof(float) * (size_t)n * D, cudaMemcpyHostToDevice,
+                             ctx->stream));
+    psg::finish_index(ctx, ix, mean, basis, d, *cfg);
+    *out = h.release();
+  });
+}
+
+void psg_index_destroy(psg_index* index) { delete index; }
+
+psg_status psg_index_info(const psg_index* index, int64_t dims[10]) {
+  return guarded([&] {
+    const psg::Index& ix = index->impl;
+    const int64_t v[10] = {ix.N, ix.D, ix.d, ix.C, ix.w, ix.ew, ix.eh, ix.tree.n_nodes,
+                           ix.htree.n_leaves, ix.tree.max_depth};
+    std::memcpy(dims, v, sizeof(v));
+  });
+}
+
+psg_status psg_index_pca(const psg_index* index, double* mean, double* basis, double* variances) {
+  return guarded([&] {
+    const psg::Index& ix = index->impl;
+    if (mean) std::copy(ix.h_mean.begin(), ix.h_mean.end(), mean);
+    if (basis) std::copy(ix.h_basis.begin(), ix.h_basis.end(), basis);
+    if (variances) std::copy(ix.h_var.begin(), ix.h_var.end(), variances);
+  });
+}
+
+psg_status psg_index_projected(const psg_index* index, double* out) {
+  return guarded([&] {
+    const psg::Index& ix = index->impl;
+    if (ix.d > 0) {
+      PSG_CUDA(cudaMemcpyAsync(out, ix.proj, sizeof(double) * ix.N * ix.d, cudaMemcpyDeviceToHost,
+                               ix.ctx->stream));
+      PSG_CUDA(cudaStreamSynchronize(ix.ctx->stream));
+    }
+  });
+}
+
+psg_status psg_index_leaves(const psg_index* index, int32_t* ids, int32_t* sizes,
+                            int64_t* n_leaves) {
+  return guarded([&] {
+    const psg::HostTree& t = index->impl.htree;
+    *n_leaves = t.n_leaves;
+    int64_t li = 0;
+    for (size_t i = 0; i < t.n_children.size(); ++i) {
+      if (t.n_children[i] != 0) continue;
+      if (sizes) sizes[li] = t.leaf_count[i];
+      if (ids)
+        std::copy(t.perm.begin() + t.leaf_start[i], t.perm.begin() + t.leaf_start[i] + t.leaf_count[i],
+                  ids + t.leaf_start[i]);
+      ++li;
+    }
+  });
+}
+
+psg_status psg_index_histograms(const psg_index* index, double* mass) {
+  return guarded([&] {
+    const psg::Index& ix = index->impl;
+    if (ix.h_ex_hist.empty()) fail(PSG_E_DOMAIN, "index was built without a histogram");
+    std::copy(ix.h_ex_hist.begin(), ix.h_ex_hist.end(), mass);
+  });
+}
+
+psg_status psg_index_query(psg_ctx* ctx, const psg_index* index, const float* Q, int64_t nq,
+                           psg_budget budget, int32_t* idx, double* dist, double* dist_pca,
+                           int64_t* scanned) {
+  return guarded([&] {
+    if (!ctx || !index || !Q || !idx || !dist) fail(PSG_E_DOMAIN, "null argument");
+    psg::validate_budget(budget);
+    const psg::Index& ix = index->impl;
+    if (nq <= 0) return;
+    psg::DBuf<float> q((size_t)nq * ix.D);
+    q.upload(ctx, Q, q.n);
+    psg::DBuf<double> qp((size_t)nq * (ix.d > 0 ? ix.d : 1)), d2(nq), dd(nq);
+    psg::DBuf<int32_t> id(nq);
+    psg::DBuf<int64_t> sc(nq);
+    if (ix.d > 0) psg::launch_project_vectors(ctx, q.p, nq, ix.D, ix.mean, ix.basis, ix.d, qp.p);
+    psg::SearchArgs a{};
+    a.q = qp.p;
+    a.nq = nq;
+    a.d = ix.d;
+    a.proj = ix.proj;
+    a.proj_soa = ix.proj_soa;
+    a.perm = ix.perm;
+    a.N = ix.N;
+    a.tree = ix.tree;
+    a.mode = budget.mode;
+    a.max_leaves = budget.max_leaves;
+    a.out_idx = id.p;
+    a.out_d2 = d2.p;
+    a.out_scanned = sc.p;
+    a.flags = ctx->d_flags;
+    psg::launch_search(ctx, a);
+    if (ix.from_vectors) {
+      psg::launch_rescore_vectors(ctx, q.p, nq, ix, id.p, dd.p);
+    } else {
+      // window index queried with explicit vectors: rescore against the
+      // materialised candidate row gathered from the exemplar
+      fail(PSG_E_DOMAIN, "psg_index_query needs a vector index; use psg_search_step for images");
+    }
+    id.download(ctx, idx, nq);
+    dd.download(ctx, dist, nq);
+    std::vector<double> h2;
+    if (dist_pca) {
+      h2.resize(nq);
+      d2.download(ctx, h2.data(), nq);
+    }
+    if (scanned) sc.download(ctx, scanned, nq);
+    psg::check_flags(ctx);
+    if (dist_pca)
+      for (int64_t i = 0; i < nq; ++i) dist_pca[i] = std::sqrt(h2[i]);
+  });
+}
+
+psg_status psg_search_step(psg_ctx* ctx, const psg_index* index, const double* out_planes, int W,
+                           int H, int spacing, int patch_width, psg_budget budget, int32_t* idx,
+                           double* dist, int64_t* nn_calls, int64_t* scanned) {
+  return guarded([&] {
+    if (!ctx || !index || !out_planes || !idx || !dist) fail(PSG_E_DOMAIN, "null argument");
+    const psg::Index& ix = index->impl;
+    if (ix.from_vectors) fail(PSG_E_SHAPE, "candidate dim does not match the grid window");
+    psg::validate_grid(ix.w, spacing, W, H);
+    psg::validate_budget(budget);
+    if (patch_width < 1) fail(PSG_E_DOMAIN, "patch width must be >= 1");
+    if (W < patch_width || H < patch_width) fail(PSG_E_DOMAIN, "output smaller than the patch");
+    psg_opt_cfg cfg{};
+    cfg.spacing = spacing;
+    cfg.patch_width = patch_width;
+    cfg.budget = budget;
+    cfg.robust_exponent = 0.8;
+    psg_level L;
+    psg::level_setup(L, ctx, ix, W, H, cfg, true);
+    psg::upload_state(L, out_planes);
+    psg::level_prime(L);
+    L.cur_idx.download(ctx, idx, L.A);
+    L.cur_dist.download(ctx, dist, L.A);
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (nn_calls) *nn_calls = L.nn_calls;
+    if (scanned) *scanned = L.pending_scanned;
+  });
+}
+
+psg_status psg_update_step(psg_ctx* ctx, const psg_index* index, const int32_t* idx,
+                           const double* irls, const double* pen, int W, int H, int spacing,
+                           double* out_planes) {
+  return guarded([&] {
+    if (!ctx || !index || !idx || !irls || !pen || !out_planes) fail(PSG_E_DOMAIN, "null argument");
+    const psg::Index& ix = index->impl;
+    if (ix.from_vectors) fail(PSG_E_SHAPE, "update_step needs an exemplar-window index");
+    psg::validate_grid(ix.w, spacing, W, H);
+    psg_opt_cfg cfg{};
+    cfg.spacing = spacing;
+    cfg.patch_width = 1;
+    psg_level L;
+    psg::level_setup(L, ctx, ix, W, H, cfg, false);
+    for (int64_t a = 0; a < L.A; ++a)
+      if (idx[a] < 0 || idx[a] >= ix.N) fail(PSG_E_SHAPE, "assignment index out of range");
+    L.cur_idx.upload(ctx, idx, L.A);
+    L.irls.upload(ctx, irls, L.A);
+    L.pen.upload(ctx, pen, L.A);
+    psg::launch_eff_from(ctx, L.irls.p, L.pen.p, L.A, L.eff.p, ctx->d_flags);
+    psg::check_flags(ctx);
+    psg::MstepArgs m = psg::mstep_args(L);
+    m.mirror = nullptr;
+    psg::launch_mstep(ctx, m);
+    L.planes.download(ctx, out_planes, (size_t)L.P * L.C);
+    psg::check_flags(ctx);
+  });
+}
+
+psg_status psg_level_create(psg_ctx* ctx, const psg_index* index, const double* init, int W,
+                            int H, const psg_opt_cfg* cfg, const double* ex_hist,
+                            psg_level** out) {
+  return guarded([&] {
+    if (!ctx || !index || !init || !cfg || !out) fail(PSG_E_DOMAIN, "null argument");
+    *out = nullptr;
+    const psg::Index& ix = index->impl;
+    if (ix.from_vectors) fail(PSG_E_SHAPE, "optimize_level needs an exemplar-window index");
+    psg::validate_cfg(*cfg, ix.w, W, H);
+    auto L = std::make_unique<psg_level>();
+    psg::level_setup(*L, ctx, ix, W, H, *cfg, true);
+    psg::level_set_hist(*L, ex_hist);
+    psg::upload_state(*L, init);
+    *out = L.release();
+  });
+}
+
+psg_status psg_level_prime(psg_level* level) {
+  return guarded([&] { psg::level_prime(*level); });
+}
+
+psg_status psg_level_iterate(psg_level* level, int n, int honor_convergence,
+                             psg_iter_stats* stats, int* n_done) {
+  return guarded([&] {
+    psg::level_prime(*level);
+    int done = 0;
+    for (int i = 0; i < n; ++i) {
+      const bool conv = psg::level_step(*level, stats ? stats + i : nullptr, honor_convergence != 0);
+      ++done;
+      if (conv) break;
+    }
+    if (n_done) *n_done = done;
+  });
+}
+
+psg_status psg_level_download(psg_level* level, double* planes, int32_t* idx, double* dist) {
+  return guarded([&] {
+    psg_ctx* ctx = level->ctx;
+    if (planes) level->planes.download(ctx, planes, (size_t)level->P * level->C);
+    if (idx) level->cur_idx.download(ctx, idx, level->A);
+    if (dist) level->cur_dist.download(ctx, dist, level->A);
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+psg_status psg_level_state_dev(psg_level* level, void** planes_dev, void** idx_dev,
+                               void** dist_dev) {
+  return guarded([&] {
+    if (planes_dev) *planes_dev = level->planes.p;
+    if (idx_dev) *idx_dev = level->cur_idx.p;
+    if (dist_dev) *dist_dev = level->cur_dist.p;
+  });
+}
+
+void psg_level_destroy(psg_level* level) { delete level; }
+
+psg_status psg_optimize_level(psg_ctx* ctx, const psg_index* index, const double* init, int W,
+                              int H, const psg_opt_cfg* cfg, const double* ex_hist,
+                              double* out_planes, psg_iter_stats* stats, int* n_iters) {
+  psg_level* L = nullptr;
+  psg_status s = psg_level_create(ctx, index, init, W, H, cfg, ex_hist, &L);
+  if (s != PSG_OK) return s;
+  std::unique_ptr<psg_level> hold(L);
+  int done = 0;
+  s = psg_level_iterate(L, cfg->max_iterations, 1, stats, &done);
+  if (s != PSG_OK) return s;
+  if (n_iters) *n_iters = done;
+  return psg_level_download(L, out_planes, nullptr, nullptr);
+}
+
+int psg_axis_positions(int extent, int window, int step, int* out) {
+  if (window < 1 || step < 1 || extent < window) return 0;
+  const auto v = psg::axis_positions(extent, window, step);
+  if (out) std::copy(v.begin(), v.end(), out);
+  return (int)v.size();
+}
+
+int64_t psg_plan(int W, int H, int w, int spacing, int patch_width, int32_t* mult) {
+  if (w < 1 || spacing < 1 || patch_width < 1 || W < w || H < w || W < patch_width ||
+      H < patch_width)
+    return -1;
+  return psg::plan_host(W, H, w, spacing, patch_width, mult);
+}
+
+double psg_pow_cr(double x, double y) { return psg::pow_cr_host(x, y); }
+
+double psg_hist_mass(int64_t count, int64_t pixels) {
+  return psg::hist_mass(count, 1.0 / (double)pixels);
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// Pyramid driver: synthesize (pipeline.cpp:216-315), stage schedule
+// (level x neighbourhood size) per the BASELINE configs.
+// ===========================================================================
+namespace psg {
+namespace {
+
+uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+// Guidance ramps as fp32 then widened (BASELINE cfg 0: "row index/63 as fp32").
+void ramp_planes(int G, int W, int H, double* out) {
+  const size_t P = (size_t)W * H;
+  for (int g = 0; g < G; ++g)
+    for (int y = 0; y < H; ++y)
+      for (int x = 0; x < W; ++x) {
+        double v;
+        if (g % 2 == 0)
+          v = H > 1 ? (double)((float)y / (float)(H - 1)) : 0.5;
+        else
+          v = W > 1 ? (double)((float)x / (float)(W - 1)) : 0.5;
+        out[g * P + (size_t)y * W + x] = v;
+      }
+}
+
+}  // namespace
+}  // namespace psg
+
+extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, double* out_planes,
+                                     psg_report* report) {
+  return guarded([&] {
+    using namespace psg;
+    if (!ctx || !req || !out_planes) fail(PSG_E_DOMAIN, "null argument");
+    const int C = req->C, G = C - 3;
+    if (C < 4 || C > 8) fail(PSG_E_SHAPE, "channels must be 3 + G with G in [1, 5]");
+    if (req->levels < 1) fail(PSG_E_DOMAIN, "levels must be >= 1");
+    if (req->out_w < 1 || req->out_h < 1) fail(PSG_E_DOMAIN, "empty output size");
+    if (req->stages.n_sizes < 1 || req->stages.n_sizes > 4)
+      fail(PSG_E_DOMAIN, "1..4 neighbourhood sizes per level");
+    if (req->guidance_kind != 0 && !req->out_guidance)
+      fail(PSG_E_DOMAIN, "explicit guidance requires out_guidance planes");
+    const double t0 = now_ms();
+    psg_report rep{};
+    const int L = req->levels;
+    const int EW = req->ew, EH = req->eh;
+    const size_t EP = (size_t)EW * EH;
+    DBuf<double> ex_full((size_t)C * EP);
+    ex_full.upload(ctx, req->exemplar, ex_full.n);
+    DBuf<double> out_guid;
+    if (req->guidance_kind != 0) {
+      out_guid.alloc((size_t)G * req->out_w * req->out_h);
+      out_guid.upload(ctx, req->out_guidance, out_guid.n);
+    }
+    // Per-level exemplar and output guidance (device).
+    std::vector<DBuf<double>> ex_lv(L), og_lv(L);
+    std::vector<int> ew(L), eh(L), ow(L), oh(L);
+    for (int l = 0; l < L; ++l) {
+      const int shift = L - 1 - l;
+      const int f = 1 << shift;
+      ow[l] = req->out_w >> shift;
+      oh[l] = req->out_h >> shift;
+      ew[l] = EW / f;
+      eh[l] = EH / f;
+      if (ow[l] < 1 || oh[l] < 1 || ew[l] < 1 || eh[l] < 1)
+        fail(PSG_E_DOMAIN, "level " + std::to_string(l) + " has no pixels");
+      const size_t lp = (size_t)ew[l] * eh[l];
+      ex_lv[l].alloc((size_t)C * lp);
+      for (int c = 0; c < 3; ++c) {
+        if (f == 1)
+          PSG_CUDA(cudaMemcpyAsync(ex_lv[l].p + c * lp, ex_full.p + c * EP, sizeof(double) * lp,
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
+        else
+          launch_downsample(ctx, ex_full.p + c * EP, EW, EH, f, ex_lv[l].p + c * lp);
+      }
+      const size_t op = (size_t)ow[l] * oh[l];
+      og_lv[l].alloc((size_t)G * op);
+      if (req->guidance_kind == 0) {
+        std::vector<double> g((size_t)G * lp), go((size_t)G * op);
+        ramp_planes(G, ew[l], eh[l], g.data());
+        ramp_planes(G, ow[l], oh[l], go.data());
+        PSG_CUDA(cudaMemcpyAsync(ex_lv[l].p + 3 * lp, g.data(), sizeof(double) * g.size(),
+                                 cudaMemcpyHostToDevice, ctx->stream));
+        og_lv[l].upload(ctx, go.data(), go.size());
+        PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+      } else {
+        for (int g = 0; g < G; ++g) {
+          if (f == 1) {
+            PSG_CUDA(cudaMemcpyAsync(ex_lv[l].p + (3 + g) * lp, ex_full.p + (3 + g) * EP,
+                                     sizeof(double) * lp, cudaMemcpyDeviceToDevice, ctx->stream));
+            PSG_CUDA(cudaMemcpyAsync(og_lv[l].p + g * op,
+                                     out_guid.p + (size_t)g * req->out_w * req->out_h,
+                                     sizeof(double) * op, cudaMemcpyDeviceToDevice, ctx->stream));
+          } else {
+            launch_downsample(ctx, ex_full.p + (3 + g) * EP, EW, EH, f, ex_lv[l].p + (3 + g) * lp);
+            launch_downsample(ctx, out_guid.p + (size_t)g * req->out_w * req->out_h, req->out_w,
+                              req->out_h, f, og_lv[l].p + g * op);
+          }
+        }
+      }
+    }
+    // Scale-matched initialisation at the coarsest level (part 1,
+    // pipeline.cpp:96-175 in spirit): copy the RGB of an exemplar pixel on
+    // the row whose guidance matches, column chosen by a seeded hash.
+    std::vector<double> hex((size_t)C * ew[0] * eh[0]), hog((size_t)G * ow[0] * oh[0]);
+    ex_lv[0].download(ctx, hex.data(), hex.size());
+    og_lv[0].download(ctx, hog.data(), hog.size());
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    const size_t lp0 = (size_t)ew[0] * eh[0], op0 = (size_t)ow[0] * oh[0];
+    std::vector<double> init((size_t)C * op0);
+    for (int y = 0; y < oh[0]; ++y)
+      for (int x = 0; x < ow[0]; ++x) {
+        const size_t i = (size_t)y * ow[0] + x;
+        const double s = std::min(1.0, std::max(0.0, hog[i]));
+        const int ey = (int)std::lround(s * (eh[0] - 1));
+        const int ex = (int)(splitmix64(req->seed ^ (uint64_t)i) % (uint64_t)ew[0]);
+        for (int c = 0; c < 3; ++c) init[c * op0 + i] = hex[c * lp0 + (size_t)ey * ew[0] + ex];
+        for (int g = 0; g < G; ++g) init[(3 + g) * op0 + i] = hog[g * op0 + i];
+      }
+    DBuf<double> state((size_t)C * op0);
+    state.upload(ctx, init.data(), init.size());
+    rep.part1_millis = now_ms() - t0;
+
+    const double t1 = now_ms();
+    for (int l = 0; l < L; ++l) {
+      const int W = ow[l], H = oh[l];
+      const size_t op = (size_t)W * H;
+      if (l > 0) {
+        const int pw = ow[l - 1], ph = oh[l - 1];
+        DBuf<double> next((size_t)C * op), up((size_t)(2 * pw) * (2 * ph));
+        for (int c = 0; c < 3; ++c) {
+          launch_upsample_bilinear(ctx, state.p + (size_t)c * pw * ph, pw, ph, 2, up.p);
+          launch_fit_to(ctx, up.p, 2 * pw, 2 * ph, W, H, next.p + c * op);
+        }
+        PSG_CUDA(cudaMemcpyAsync(next.p + 3 * op, og_lv[l].p, sizeof(double) * G * op,
+                                 cudaMemcpyDeviceToDevice, ctx->stream));
+        state = std::move(next);
+      }
+      for (int si = 0; si < req->stages.n_sizes; ++si) {
+        const int w = req->stages.sizes[si];
+        if (w < 2 || w % 2) fail(PSG_E_DOMAIN, "neighbourhood sizes must be even and >= 2");
+        if (W < w || H < w || ew[l] < w || eh[l] < w) continue;
+        if ((int64_t)(ew[l] - w + 1) * (eh[l] - w + 1) < 2) continue;  // fit_pca needs n >= 2
+        const double ti = now_ms();
+        psg_index_cfg icfg = req->index;
+        icfg.seed = (req->seed ^ (0x9E3779B97F4A7C15ull * (uint64_t)(l + 1))) ^ (uint64_t)w;
+        if (req->cfg.histogram_matching) {
+          icfg.hist_bins = req->cfg.histogram_bins;
+          icfg.hist_include_scale = req->cfg.histogram_include_scale;
+        }
+        auto index = create_index_from_device_planes(ctx, ex_lv[l].p, C, ew[l], eh[l], w, nullptr,
+                                                     nullptr, 0, icfg);
+        const double index_ms = now_ms() - ti;
+        psg_opt_cfg cfg = req->cfg;
+        cfg.spacing = std::max(1, w / 4);
+        cfg.patch_width = std::min(std::max(1, cfg.patch_width), cfg.spacing);
+        validate_cfg(cfg, w, W, H);
+        const double to = now_ms();
+        psg_level lv;
+        level_setup(lv, ctx, index->impl, W, H, cfg, true);
+        level_set_hist(lv, nullptr);
+        PSG_CUDA(cudaMemcpyAsync(lv.planes.p, state.p, sizeof(double) * C * op,
+                                 cudaMemcpyDeviceToDevice, ctx->stream));
+        launch_make_mirror(ctx, lv.planes.p, C, W, H, lv.mirror.p);
+        level_prime(lv);
+        psg_iter_stats last{};
+        int iters = 0;
+        int64_t calls = 0;
+        for (int it = 0; it < cfg.max_iterations; ++it) {
+          const bool conv = level_step(lv, &last, true);
+          calls += last.nn_calls;
+          ++iters;
+          if (conv) break;
+        }
+        PSG_CUDA(cudaMemcpyAsync(state.p, lv.planes.p, sizeof(double) * C * op,
+                                 cudaMemcpyDeviceToDevice, ctx->stream));
+        PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (rep.n_stages < 16) {
+          psg_stage_report& sr = rep.stages[rep.n_stages++];
+          sr.level = l;
+          sr.w = w;
+          sr.W = W;
+          sr.H = H;
+          sr.ew = ew[l];
+          sr.eh = eh[l];
+          sr.d = index->impl.d;
+          sr.iterations = iters;
+          sr.final_energy = last.energy;
+          sr.nn_calls = calls;
+          sr.index_millis = index_ms;
+          sr.optimize_millis = now_ms() - to;
+        }
+        rep.total_nn_calls += calls;
+        rep.final_energy = last.energy;
+      }
+    }
+    rep.part2_millis = now_ms() - t1;
+    state.download(ctx, out_planes, (size_t)C * req->out_w * req->out_h);
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (report) *report = rep;
+  });
+}

@@ -1,0 +1,235 @@
+"""Parity of the sm_100a path (through the C ABI) against the CPU checkers.
+
+`ref`: the reference's own TUs (C = 4 only); `port`: our C restatement
+(C-generalised, pinned to `ref` in test_oracle_pins.py).  Bars:
+  * NN indices and fp64 distances bit-exact (exact search mode);
+  * fp64 image planes bit-exact for update_step with injected weights;
+  * optimize_level: images within 1/255 (north star) — in practice equal or
+    within a few ulp, since only the IRLS pow may round differently from
+    glibc (correctly rounded on device vs glibc's < 1 ulp) — energy within
+    1e-4 relative, assignment indices equal.
+"""
+import numpy as np
+import pytest
+
+from conftest import random_planes
+from oracle.oracle import fit_pca
+from paper_2006_11851_b200 import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+api = pytest.importorskip("paper_2006_11851_b200.api")
+
+
+def _stage(size=32, out=48, G=1, seed=1, d=12):
+    ex = wl.rgbs_planes(wl.sinusoid_exemplar(size, 8, 2.0, seed), G)
+    init = wl.init_output(ex, out, out, G, seed)
+    return ex, init
+
+
+def _injected(port, ex, w, d):
+    cand = port.extract_all(ex, w, 1)
+    mean, basis, _ = fit_pca(cand, d_fixed=d)
+    return cand, mean, basis, port.project_all(cand, mean, basis)
+
+
+# ---- index build ---------------------------------------------------------------
+@pytest.mark.parametrize("G,w,d", [(1, 8, 12), (2, 8, 16), (1, 4, 40), (1, 16, 32)])
+def test_projected_database_bit_exact(gpu_ctx, port, G, w, d):
+    ex, _ = _stage(G=G)
+    cand, mean, basis, proj = _injected(port, ex, w, d)
+    ix = api.make_pca_tree_index(ex, w, mean=mean, basis=basis, branching=4, max_depth=3,
+                                 ctx=gpu_ctx)
+    assert ix.count == cand.shape[0] and ix.retained_dim == d
+    assert np.array_equal(ix.projected(), proj)
+    ids, sizes = ix.leaves()
+    assert np.array_equal(np.sort(ids), np.arange(ix.count))
+    assert sizes.sum() == ix.count
+
+
+def test_exemplar_histogram_bit_exact(gpu_ctx, port):
+    ex, _ = _stage(size=40)
+    ix = api.make_pca_tree_index(ex, 8, d_fixed=8, hist_bins=16, ctx=gpu_ctx)
+    assert np.array_equal(ix.histograms(3, 16), port.build_histograms(ex, 16, 3))
+
+
+def test_device_pca_fit_properties(gpu_ctx, port):
+    ex, _ = _stage(size=40)
+    ix = api.make_pca_tree_index(ex, 8, variance_target=0.95, ctx=gpu_ctx)
+    mean, basis, var = ix.pca()
+    cand = port.extract_all(ex, 8, 1)
+    m2, b2, v2 = fit_pca(cand, 0.95)
+    assert np.allclose(mean, m2, atol=1e-12)
+    assert np.allclose(var, v2, rtol=1e-9, atol=1e-12)
+    assert basis.shape == b2.shape
+    assert np.allclose(basis @ basis.T, np.eye(basis.shape[0]), atol=1e-10)
+    # same subspace/sign convention as the numpy restatement (no near-degenerate pairs)
+    assert np.allclose(np.abs(np.sum(basis * b2, axis=1)), 1.0, atol=1e-6)
+    assert np.all(np.diff(var) <= 1e-12)
+    assert var[: basis.shape[0]].sum() >= 0.95 * var.sum()
+
+
+# ---- E-step -------------------------------------------------------------------------
+@pytest.mark.parametrize("G", [1, 2])
+def test_search_step_bit_exact(gpu_ctx, port, ref, G):
+    ex, init = _stage(G=G)
+    cand, mean, basis, proj = _injected(port, ex, 8, 12)
+    ix = api.make_pca_tree_index(ex, 8, mean=mean, basis=basis, branching=4, max_depth=3,
+                                 ctx=gpu_ctx)
+    idx, dist, calls, _ = api.search_step(init, ix, 4, 2, api.QueryBudget.exact())
+    i_p, d_p, c_p = port.search_step(init, 8, 4, 2, cand, proj, mean, basis)
+    assert calls == c_p
+    assert np.array_equal(idx, i_p)
+    assert np.array_equal(dist, d_p)
+    if G == 1:
+        h = ref.index_create(ex, 8, mean, basis, kind="tree", branching=4, seed=7)
+        i_r, d_r, c_r, _ = h.search_step(init, 8, 4, 2, mode="exact")
+        assert np.array_equal(idx, i_r) and np.array_equal(dist, d_r) and calls == c_r
+
+
+def test_search_self_image_zero_distance(gpu_ctx, port):
+    # optimizer_test.cpp:247-255: querying the exemplar itself gives distance 0
+    ex, _ = _stage(size=24)
+    ix = api.make_pca_tree_index(ex, 8, d_fixed=10, ctx=gpu_ctx)
+    _, dist, _, _ = api.search_step(ex, ix, 2, 2, api.QueryBudget.exact())
+    assert np.all(dist == 0.0)
+
+
+def test_backtrack_all_leaves_equals_exact_and_greedy_runs(gpu_ctx, port):
+    ex, init = _stage()
+    cand, mean, basis, proj = _injected(port, ex, 8, 12)
+    ix = api.make_pca_tree_index(ex, 8, mean=mean, basis=basis, branching=4, max_depth=3,
+                                 ctx=gpu_ctx)
+    e_idx, e_d, _, _ = api.search_step(init, ix, 4, 2, api.QueryBudget.exact())
+    b_idx, b_d, _, _ = api.search_step(init, ix, 4, 2, api.QueryBudget.backtrack(ix.n_leaves))
+    assert np.array_equal(e_idx, b_idx) and np.array_equal(e_d, b_d)
+    g_idx, g_d, _, _ = api.search_step(init, ix, 4, 2, api.QueryBudget.greedy())
+    assert np.all(g_idx >= 0) and np.all(g_d >= e_d - 1e-12)
+
+
+def test_vector_index_exact_equals_bruteforce(gpu_ctx, port, ref):
+    # config-2 shape at reduced size: mixture of Gaussians, D = 192, d = 24
+    X = wl.gaussian_mixture(4096, 192, 64, 20.0, 1)
+    Q = wl.gaussian_mixture(1000, 192, 64, 20.0, 2)
+    mean, basis, _ = fit_pca(X, d_fixed=24)
+    ix = api.make_vector_index(X, branching=8, max_depth=3, mean=mean, basis=basis, ctx=gpu_ctx)
+    idx, dist, dpca, scanned = ix.nearest(Q, api.QueryBudget.exact())
+    P = port.project_all(X, mean, basis)
+    qp = port.project_all(Q, mean, basis)
+    for i in range(0, 1000, 7):
+        j, d2 = port.nearest_lexmin(P, qp[i])
+        jr, dr = ref.brute_force_nearest(P, qp[i])
+        assert idx[i] == j == jr
+        assert dpca[i] == np.sqrt(d2) == dr
+        assert dist[i] == port.full_distance(Q[i], X[j])
+    assert scanned.mean() < X.shape[0]  # the tree prunes
+
+
+# ---- M-step ---------------------------------------------------------------------------
+@pytest.mark.parametrize("G,W,H,sp", [(1, 24, 24, 2), (1, 37, 23, 3), (2, 40, 32, 2)])
+def test_update_step_bit_exact(gpu_ctx, port, ref, G, W, H, sp):
+    ex, _ = _stage(size=30, G=G)
+    ix = api.make_pca_tree_index(ex, 8, d_fixed=8, ctx=gpu_ctx)
+    cand = port.extract_all(ex, 8, 1)
+    rng = np.random.Generator(np.random.PCG64(W * H))
+    A = len(port.axis_positions(W, 8, sp)) * len(port.axis_positions(H, 8, sp))
+    idx = rng.integers(0, cand.shape[0], A).astype(np.int32)
+    irls = rng.uniform(0.1, 300.0, A)
+    pen = rng.uniform(0.0, 0.5, A)
+    out = api.update_step(idx, irls, pen, ix, W, H, sp)
+    assert np.array_equal(out, port.update_step(3 + G, W, H, 8, sp, cand, idx, irls, pen))
+    if G == 1:
+        h = ref.index_create(ex, 8, kind="brute")
+        assert np.array_equal(out, h.update_step(random_planes(4, H, W, 2), 8, sp, idx, irls, pen))
+
+
+def test_update_step_rejects_bad_weight(gpu_ctx):
+    ex, _ = _stage(size=24)
+    ix = api.make_pca_tree_index(ex, 8, d_fixed=8, ctx=gpu_ctx)
+    with pytest.raises(api.DomainError):
+        api.update_step([0], [0.0], [0.0], ix, 8, 8, 2)
+
+
+# ---- EM loop -----------------------------------------------------------------------------
+@pytest.mark.parametrize("hist", [False, True])
+def test_optimize_level_matches_reference(gpu_ctx, port, ref, hist):
+    ex, init = _stage()
+    cand, mean, basis, proj = _injected(port, ex, 8, 12)
+    ix = api.make_pca_tree_index(ex, 8, mean=mean, basis=basis, branching=4, max_depth=3,
+                                 hist_bins=16 if hist else 0, ctx=gpu_ctx)
+    cfg = api.OptimizerConfig(max_iterations=3, min_iterations=3, convergence_fraction=1e-9,
+                              histogram_matching=hist, nbhd_width=8, spacing=4, patch_width=2,
+                              budget=api.QueryBudget.exact())
+    out, stats = api.optimize_level(init, ix, cfg)
+    h = ref.index_create(ex, 8, mean, basis, kind="tree", branching=4, seed=3)
+    out_r, st_r, _ = h.optimize_level(init, 8, 4, 2, max_it=3, min_it=3, frac=1e-9, bins=16,
+                                      hist_on=hist, mode="exact")
+    assert len(stats) == len(st_r)
+    assert np.max(np.abs(out - out_r)) <= 1.0 / 255
+    q = lambda a: np.rint(np.clip(a, 0, 1) * 255)  # image_io.cpp:18-21
+    assert np.array_equal(q(out[:3]), q(out_r[:3]))
+    for s, r in zip(stats, st_r):
+        assert s.iteration == r[0]
+        assert s.nn_calls == r[3]
+        assert s.changed == r[2]
+        assert abs(s.energy - r[1]) <= 1e-4 * abs(r[1])
+        assert abs(s.lsq_energy_before - r[4]) <= 1e-9 * abs(r[4])
+        assert abs(s.lsq_energy_after - r[5]) <= 1e-9 * abs(r[5])
+
+
+def test_optimize_level_c5_matches_port(gpu_ctx, port):
+    ex, init = _stage(G=2)
+    cand, mean, basis, proj = _injected(port, ex, 8, 16)
+    ix = api.make_pca_tree_index(ex, 8, mean=mean, basis=basis, branching=8, max_depth=4,
+                                 hist_bins=16, ctx=gpu_ctx)
+    cfg = api.OptimizerConfig(max_iterations=4, min_iterations=4, convergence_fraction=1e-9,
+                              nbhd_width=8, spacing=2, patch_width=2,
+                              budget=api.QueryBudget.exact())
+    out, stats = api.optimize_level(init, ix, cfg)
+    exm = port.build_histograms(ex, 16, 3)
+    out_p, st_p = port.optimize_level(init, 8, 2, 2, cand, proj, mean, basis, max_it=4, min_it=4,
+                                      frac=1e-9, bins=16, ex_mass=exm)
+    assert np.max(np.abs(out - out_p)) <= 1.0 / 255
+    for s, r in zip(stats, st_p):
+        assert s.changed == r[2] and s.nn_calls == r[3]
+        assert abs(s.energy - r[1]) <= 1e-4 * abs(r[1])
+
+
+def test_fixed_point_returns_after_one_iteration(gpu_ctx):
+    # optimizer_test.cpp:320-327
+    ex, _ = _stage(size=24)
+    ix = api.make_pca_tree_index(ex, 8, d_fixed=10, ctx=gpu_ctx)
+    cfg = api.OptimizerConfig(histogram_matching=False, nbhd_width=8, spacing=2,
+                              budget=api.QueryBudget.exact())
+    out, stats = api.optimize_level(ex, ix, cfg)
+    assert len(stats) == 1 and stats[0].changed == 0 and abs(stats[0].energy) < 1e-9
+
+
+def test_level_api_deterministic(gpu_ctx, port):
+    ex, init = _stage()
+    ix = api.make_pca_tree_index(ex, 8, d_fixed=12, branching=4, ctx=gpu_ctx)
+    cfg = api.OptimizerConfig(max_iterations=3, min_iterations=3, convergence_fraction=1e-9,
+                              nbhd_width=8, spacing=4, budget=api.QueryBudget.exact())
+    runs = []
+    for _ in range(2):
+        L = api.Level(init, ix, cfg)
+        st = L.iterate(3)
+        runs.append((L.download(), st))
+    (p1, i1, d1), s1 = runs[0]
+    (p2, i2, d2), s2 = runs[1]
+    assert np.array_equal(p1, p2) and np.array_equal(i1, i2) and np.array_equal(d1, d2)
+    assert [s.energy for s in s1] == [s.energy for s in s2]
+
+
+def test_synthesize_runs_multires(gpu_ctx):
+    cfg1 = wl.CONFIGS[1]
+    rgb = wl.sinusoid_exemplar(64, 16, 2.0, 1)
+    ex = wl.rgbs_planes(rgb, 1)
+    cfg = api.OptimizerConfig(max_iterations=2, min_iterations=2, convergence_fraction=1e-9,
+                              budget=api.QueryBudget.exact())
+    out, rep = api.synthesize(ex, 128, 128, 2, (16, 8), cfg, variance_target=0.95, d_cap=32,
+                              branching=8, max_depth=3, seed=1)
+    assert out.shape == (4, 128, 128)
+    assert np.all((out >= 0) & (out <= 1))
+    assert len(rep["stages"]) == 4
+    assert rep["total_nn_calls"] > 0
