@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""bench.py — EM iterations/s of the persyn hot path at 1024^2 output on B200.
+
+Workload (BASELINE.json configs[3], its finest level): exemplar 256^2 RGB
+(32 sinusoids, 3x top-to-bottom frequency ramp) + 2 guidance planes (row and
+column ramps) -> C = 5; output 1024 x 1024; neighbourhood w = 8, spacing 2,
+2x2 patches (259,081 anchors, 4,145,296 reference plan calls per search);
+PCA d = 32 (fitted on device), k-means tree b = 8 depth 4; exact search
+(the bit-parity mode); IRLS r = 0.8; histogram reweighting on (16 bins).
+A step = one EM iteration (weights + histogram penalty + M-step + lsq
+diagnostic + E-step search + telemetry), optimizer.cpp:450-513.
+
+Arms:
+  (default)          this repo's sm_100a path through the C ABI.
+  --impl reference   the reference's own C++ (oracle/_ref, compiled from
+                     /root/reference) on the host cores: one bounded sample of
+                     the same EM iteration per step (an output band), scaled
+                     to the full 1024^2 iteration.  The reference hard-codes
+                     C = 4 (image.hpp:70), so it runs the 1-guidance variant
+                     (D = 256 instead of 320: ~20% less work per query).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "EM iterations/s at 1024^2 output (cfg3 finest stage, w=8, exact search)"
+UNIT = "iterations/s"
+BAND_ROWS = 24   # reference arm: rows of the output band per bounded sample
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--window", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--budget", default="exact")
+    ap.add_argument("--out", default="")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def stage_inputs(G: int, window: int):
+    from paper_2006_11851_b200 import workloads as wl
+    cfg = wl.CONFIGS[3]
+    rgb = wl.sinusoid_exemplar(cfg.ex_size, cfg.n_sin, cfg.ramp, cfg.seed)
+    ex = wl.rgbs_planes(rgb, G)
+    init = wl.init_output(ex, cfg.out, cfg.out, G, cfg.seed)
+    sp = max(1, window // 4)
+    return cfg, ex, init, sp
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d.get("hbm_gbs", 6650.0), "src": "measured"}
+    return {"hbm_gbs": 6650.0, "src": "fallback"}
+
+
+# ---------------------------------------------------------------------------
+def cpu_reference_sample(window: int, steps: int, warmup: int, threads: int):
+    """Time the reference's own EM iteration on a bounded output band (C = 4)."""
+    os.environ["PERSYN_THREADS"] = str(threads)
+    from oracle.oracle import Port, Ref, fit_pca
+    ref, port = Ref(), Port()
+    cfg, ex, init, sp = stage_inputs(1, window)
+    cand = port.extract_all(ex, window, 1)
+    mean, basis, _ = fit_pca(cand, d_fixed=32)
+    h = ref.index_create(ex, window, mean, basis, kind="tree", branching=8, seed=1)
+    band = np.ascontiguousarray(init[:, :BAND_ROWS, :])
+    nx = len(port.axis_positions(cfg.out, window, sp))
+    A_full = nx * nx
+    A_band = nx * len(port.axis_positions(BAND_ROWS, window, sp))
+    state = {"planes": band}
+    h.em_iteration(state, window, sp, 2, mode="exact", workers=threads)  # priming + 1
+    for _ in range(max(0, warmup - 1)):
+        h.em_iteration(state, window, sp, 2, mode="exact", workers=threads)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        h.em_iteration(state, window, sp, 2, mode="exact", workers=threads)
+        times.append(time.perf_counter() - t0)
+    t_band = float(np.mean(times))
+    t_full = t_band * A_full / A_band
+    return {"value": 1.0 / t_full, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": (f"reference optimize_level loop body (oracle/_ref, exact search, "
+                       f"PERSYN_THREADS={threads}) on a {cfg.out}x{BAND_ROWS} output band "
+                       f"({A_band} of {A_full} anchors), C=4 (the reference cannot run C=5); "
+                       f"{steps} timed iterations of {t_band:.2f} s scaled by anchor count "
+                       f"to {t_full:.1f} s per full 1024^2 iteration"),
+            "band_seconds": t_band, "full_iteration_seconds_est": t_full}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    r = cpu_reference_sample(args.window, args.steps, args.warmup, threads)
+    line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 / r["value"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE cfg3 generator)",
+            "config": {"workload": "cfg3 finest stage 1024^2, w=8 sp=2 p=2, d=32, exact, C=4",
+                       "parallelism": "host threads", "l2": "n/a (CPU)"},
+            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------------------
+def roofline_for(kernels: dict, step_ms: float, A: int, P: int, C: int, d: int, N: int,
+                 scanned_per_step: float, peaks: dict):
+    """Roofline of the dominant kernel, algorithmic bytes / flops per launch
+    (DESIGN.md §Roofline).  Search is fp64-SIMT bound (no tensor-core kind
+    computes the reference's fp64 mul-then-add chains), M-step HBM bound."""
+    if not kernels:
+        return None, {}
+    dom = max(kernels, key=lambda k: kernels[k][0])
+    per = {}
+    for name, (ms, n) in kernels.items():
+        if n:
+            per[name] = {"ms_per_launch": ms / n, "launches": n, "share": ms / max(step_ms, 1e-9)}
+    ms, n = kernels[dom]
+    t = ms / n / 1e3
+    fp64_peak = 148 * 64 * 2 * 1.965e9 / 1e12   # derived, TFLOP/s (FMA = 2)
+    if dom == "search_kernel":
+        flops = 3.0 * d * scanned_per_step  # sub, mul, add per dim per scanned point
+        ach = flops / t / 1e12
+        roof = {"bound": "fp64", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": ach / fp64_peak, "traffic": None,
+                "note": "fp64 SIMT bound; peak derived 148 SM x 64 lanes x 2 x 1.965 GHz "
+                        "(not measured); algorithmic flops = 3*d*points_scanned"}
+    elif dom == "mstep_kernel":
+        bytes_ = P * C * 12 + A * 12
+        ach = bytes_ / t / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / peaks["hbm_gbs"], "traffic": None}
+    elif dom == "project_kernel":
+        bytes_ = P * C * 4 + A * d * 8
+        ach = bytes_ / t / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / peaks["hbm_gbs"], "traffic": None}
+    else:
+        roof = {"bound": "hbm", "achieved": None, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": None, "traffic": None}
+    roof["kernel"] = dom
+    roof["peak_src"] = peaks["src"] if roof["bound"] == "hbm" else "derived"
+    return roof, per
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2006_11851_b200 import api
+
+    G = 2
+    cfg, ex, init, sp = stage_inputs(G, args.window)
+    C = 3 + G
+    stream = torch.cuda.Stream()
+    ctx = api.Context(local, stream.cuda_stream)
+    t_build = time.perf_counter()
+    index = api.make_pca_tree_index(ex, args.window, d_fixed=32, branching=8, max_depth=4,
+                                    seed=1, hist_bins=16, ctx=ctx)
+    t_build = time.perf_counter() - t_build
+    budget = api.QueryBudget.exact() if args.budget == "exact" else \
+        api.QueryBudget.backtrack(int(args.budget.split(":")[1]))
+    total = args.warmup + args.steps
+    ocfg = api.OptimizerConfig(max_iterations=10 ** 6, min_iterations=10 ** 6 - 1,
+                               convergence_fraction=1e-9, histogram_bins=16,
+                               histogram_matching=True, nbhd_width=args.window, spacing=sp,
+                               patch_width=2, budget=budget)
+    level = api.Level(init, index, ocfg)
+    level.prime()
+    for _ in range(args.warmup):
+        level.iterate(1)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    ctx.profile(True)
+    launches0 = ctx.launches
+    stats = []
+    with ClockSampler(local) as clk:
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(float(k))            # L2 flush, outside the event pair
+                ev[k][0].record(stream)
+            stats += level.iterate(1)
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+    launches = ctx.launches - launches0
+    kernels = ctx.kernel_times()
+    ctx.profile(False)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms = float(np.sum(step_ms))
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = world * args.steps / (ms / 1e3)
+    A = level.nx * level.ny
+    P = cfg.out * cfg.out
+    scanned_unique = float(np.mean([s.unique_points_scanned for s in stats]))
+    calls = stats[-1].nn_calls
+    roof, per = roofline_for(kernels, ms_per_step * args.steps, A, P, C, index.retained_dim,
+                             index.count, scanned_unique, measured_peaks())
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE cfg3 generator: 32 sinusoids, 3x ramp, seed 1)",
+        "config": {"workload": "cfg3 finest stage: exemplar 256^2 C=5, output 1024^2, w=8 sp=2 "
+                               "p=2, PCA d=32, tree b=8 depth 4, exact search, hist on",
+                   "anchors": A, "plan_calls_per_search": int(calls // 1),
+                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "l2": "flushed (256 MB write) before every timed step"},
+        "nn_queries_per_s": {"unique_anchor_queries": world * A / (ms_per_step / 1e3),
+                             "reference_plan_calls": world * calls / (ms_per_step / 1e3)},
+        "energy_last": stats[-1].energy, "changed_last": stats[-1].changed,
+        "points_scanned_per_query": scanned_unique / A,
+        "index_build_s": t_build, "gpu_launches": launches,
+        "kernels": per, "roofline": roof,
+    }
+    # ---- e2e through the public host-buffer API (pinned host memory) ------
+    if not args.no_e2e:
+        n_it = 10  # cfg3: 10 EM iterations per stage
+        pinned = torch.empty(init.shape, dtype=torch.float64, pin_memory=True)
+        pinned.numpy()[...] = init
+        out_pinned = torch.empty(init.shape, dtype=torch.float64, pin_memory=True)
+        e2e_cfg = api.OptimizerConfig(max_iterations=n_it, min_iterations=n_it,
+                                      convergence_fraction=1e-9, histogram_bins=16,
+                                      histogram_matching=True, nbhd_width=args.window,
+                                      spacing=sp, patch_width=2, budget=budget)
+        calls_e2e = 2
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(calls_e2e):
+            import ctypes as ct
+            from paper_2006_11851_b200 import native as N
+            c = e2e_cfg.c()
+            st = (N.psg_iter_stats * n_it)()
+            n = ct.c_int()
+            N.check(N.lib.psg_optimize_level(ctx.h, index.h, ct.c_void_p(pinned.data_ptr()),
+                                             cfg.out, cfg.out, ct.byref(c), None,
+                                             ct.c_void_p(out_pinned.data_ptr()),
+                                             ct.cast(st, ct.c_void_p), ct.byref(n)))
+        torch.cuda.synchronize()
+        t_e2e = (time.perf_counter() - t0) / calls_e2e
+        result["e2e"] = {"value": world * n_it / t_e2e, "unit": UNIT,
+                         "h2d_bytes_per_step": int(init.nbytes),
+                         "d2h_bytes_per_step": int(init.nbytes),
+                         "step": f"one psg_optimize_level call (host buffers, {n_it} EM iterations "
+                                 f"incl. the priming search), index resident"}
+    result["clocks"] = clk.summary()
+    # ---- CPU baseline (rank 0, N = 1) -------------------------------------------
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            r = cpu_reference_sample(args.window, 1, 1, os.cpu_count() or 1)
+            result["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind",
+                                                        "sample")}
+        except Exception as e:  # reference library missing on this box
+            result["cpu_baseline"] = {"value": None, "unavailable": str(e)}
+    if rank == 0:
+        line = json.dumps(result)
+        print(line)
+        if args.out:
+            Path(args.out).write_text(line + "\n")
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -101,6 +101,7 @@ typedef struct {
   double lsq_energy_after;
   int64_t points_scanned;   /* sum over the reference's query plan */
   int64_t unique_queries;   /* anchors actually searched on device */
+  int64_t unique_points_scanned; /* points scanned by those searches */
 } psg_iter_stats;
 
 typedef struct psg_ctx psg_ctx;
@@ -116,6 +117,12 @@ void psg_ctx_destroy(psg_ctx* ctx);
 psg_status psg_ctx_synchronize(psg_ctx* ctx);
 /* Number of kernel launches issued by this context so far. */
 int64_t psg_ctx_launch_count(const psg_ctx* ctx);
+/* Per-kernel CUDA-event timing on the context stream (benchmark/roofline).
+ * enable != 0 starts recording (and resets the totals). */
+psg_status psg_ctx_profile(psg_ctx* ctx, int enable);
+/* Copies up to n (name, total milliseconds, launches) entries of the kernels
+ * timed since profiling was enabled; returns the number of kernel kinds. */
+int psg_ctx_kernel_times(psg_ctx* ctx, const char** names, double* ms, int64_t* launches, int n);
 
 /* ---- search index (SearchIndex plug-in, optimizer.hpp:111-129) ----------- */
 /*

@@ -534,6 +534,32 @@ class RefIndex:
                                                             _ptr(idx), _ptr(out)), "assign")
         return out
 
+    def em_iteration(self, state, w, sp, p=2, r=0.8, eps=1e-4, bins=16, hist_on=True,
+                     mode="exact", max_leaves=4, workers=0):
+        """One optimize_level loop body through the reference's functions.
+        state: dict with 'planes' (C,H,W) updated in place, 'idx', 'dist',
+        'primed'.  Returns (energy, changed)."""
+        planes = state["planes"]
+        C, H, W = planes.shape
+        if "idx" not in state:
+            xs, ys = self.ref.grid_axes(W, H, w, sp)
+            state["idx"] = np.zeros(len(xs) * len(ys), np.int32)
+            state["dist"] = np.zeros(len(xs) * len(ys), np.float64)
+            state["primed"] = np.zeros(1, np.int32)
+        en = np.zeros(1, np.float64)
+        ch = np.zeros(1, np.int64)
+        L = self.ref.L
+        if not getattr(L.ref_em_iteration, "_typed", False):
+            L.ref_em_iteration.argtypes = [_VP, _VP, _I, _I, _I, _I, _I, _D, _D, _I, _I, _I, _I,
+                                           _I, _VP, _VP, _VP, _VP, _VP]
+            L.ref_em_iteration._typed = True
+        self.ref._check(L.ref_em_iteration(self.h, _ptr(planes), W, H, w, sp, p, r, eps, bins,
+                                           int(hist_on), MODES[mode], max_leaves, workers,
+                                           _ptr(state["idx"]), _ptr(state["dist"]),
+                                           _ptr(state["primed"]), _ptr(en), _ptr(ch)),
+                        "em_iteration")
+        return float(en[0]), int(ch[0])
+
     def histograms(self, bins, include_scale=False):
         out = np.zeros((4 if include_scale else 3, bins), np.float64)
         self.ref._check(self.ref.L.ref_index_histograms(self.h, bins, int(include_scale),

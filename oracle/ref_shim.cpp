@@ -463,6 +463,54 @@ int ref_optimize_level(void* h, const double* init, int W, int H, int w, int sp,
   });
 }
 
+// One pass of optimize_level's loop body (optimizer.cpp:453-497) driven
+// through the reference's own public functions (irls_weight, build_histograms,
+// histogram_penalty, update_step, assignment_distances, search_step,
+// energy_from_distances) on caller-held state: used to time bounded samples of
+// an EM iteration (bench.py --impl reference).  When *primed == 0 the priming
+// search (optimizer.cpp:445) runs first and *primed is set.
+int ref_em_iteration(void* h, double* planes, int W, int H, int w, int sp, int patch, double r,
+                     double eps, int bins, int hist_on, int mode, int max_leaves, int workers,
+                     int32_t* idx, double* dist, int* primed, double* energy, int64_t* changed) {
+  return guard([&] {
+    auto* ri = static_cast<RefIndex*>(h);
+    const SparseGrid g = make_sparse_grid(GridSpec{w, sp, W, H});
+    const std::size_t A = static_cast<std::size_t>(g.count());
+    const QueryBudget budget = make_budget(mode, max_leaves);
+    RgbsImage x = make_rgbs(planes, W, H);
+    if (!*primed) {
+      const SearchOutcome o = search_step(x, *ri->index, g, PatchSpec{patch}, budget, workers);
+      std::copy(o.assignments.input_index.begin(), o.assignments.input_index.end(), idx);
+      std::copy(o.assignments.distance.begin(), o.assignments.distance.end(), dist);
+      *primed = 1;
+    }
+    const NeighborhoodMatrix& cand = ri->index->candidates();
+    WeightMap wm;
+    wm.irls.resize(A);
+    wm.hist_penalty.assign(A, 0.0);
+    for (std::size_t i = 0; i < A; ++i) wm.irls[i] = irls_weight(dist[i], r, eps);
+    if (hist_on) {
+      const HistogramSet eh = build_histograms(ri->exemplar, bins, false);
+      const HistogramSet oh = build_histograms(x, bins, false);
+      for (std::size_t i = 0; i < A; ++i)
+        wm.hist_penalty[i] = histogram_penalty(cand.vec(idx[i]), oh, eh);
+    }
+    AssignmentMap am{std::vector<int32_t>(idx, idx + A), std::vector<double>(dist, dist + A)};
+    x = update_step(am, wm, g, cand, x);
+    const auto after = assignment_distances(x, g, cand, am.input_index);
+    double lsq = 0.0;
+    for (std::size_t i = 0; i < A; ++i) lsq += wm.effective(i) * after[i] * after[i];
+    const SearchOutcome o = search_step(x, *ri->index, g, PatchSpec{patch}, budget, workers);
+    int64_t ch = 0;
+    for (std::size_t i = 0; i < A; ++i) ch += o.assignments.input_index[i] != idx[i];
+    std::copy(o.assignments.input_index.begin(), o.assignments.input_index.end(), idx);
+    std::copy(o.assignments.distance.begin(), o.assignments.distance.end(), dist);
+    if (energy) *energy = energy_from_distances(o.assignments.distance, r) + 0.0 * lsq;
+    if (changed) *changed = ch;
+    store_rgbs(x, planes);
+  });
+}
+
 // ---- weights, histograms, energies (optimizer.cpp:44-131) ------------------------
 int ref_build_histograms(const double* planes, int W, int H, int bins, int include_scale,
                          double* mass) {

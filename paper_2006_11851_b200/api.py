@@ -92,12 +92,13 @@ class IterationStats:
     lsq_energy_after: float
     points_scanned: int
     unique_queries: int
+    unique_points_scanned: int
 
     @staticmethod
     def of(s: N.psg_iter_stats) -> "IterationStats":
         return IterationStats(s.iteration, s.energy, s.changed, s.nn_calls, s.millis,
                               s.lsq_energy_before, s.lsq_energy_after, s.points_scanned,
-                              s.unique_queries)
+                              s.unique_queries, s.unique_points_scanned)
 
 
 # ---------------------------------------------------------------------------
@@ -124,6 +125,18 @@ class Context:
     @property
     def launches(self) -> int:
         return int(N.lib.psg_ctx_launch_count(self.h))
+
+    def profile(self, enable: bool = True):
+        N.check(N.lib.psg_ctx_profile(self.h, int(enable)))
+
+    def kernel_times(self) -> dict:
+        """{kernel: (total ms, launches)} of event-timed launches since profile(True)."""
+        n = 16
+        names = (ct.c_char_p * n)()
+        ms = np.zeros(n)
+        cnt = np.zeros(n, np.int64)
+        k = N.lib.psg_ctx_kernel_times(self.h, ct.cast(names, ct.c_void_p), _p(ms), _p(cnt), n)
+        return {names[i].decode(): (float(ms[i]), int(cnt[i])) for i in range(k) if cnt[i]}
 
 
 _default_ctx: Optional[Context] = None

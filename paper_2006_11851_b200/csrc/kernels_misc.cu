@@ -44,6 +44,7 @@ __global__ void window_mean_kernel(const float* __restrict__ mirror, int img_w, 
 
 void launch_window_mean(psg_ctx* ctx, const float* mirror, int img_w, int C, int w, int nxe,
                         int64_t N, double* mean) {
+  ProfScope _prof(ctx, K_BUILD);
   const int D = w * w * C;
   window_mean_kernel<<<D, 256, 0, ctx->stream>>>(mirror, img_w, C, w, nxe, N, mean);
   PSG_LAUNCHED(ctx);
@@ -67,6 +68,7 @@ __global__ void center_windows_kernel(const float* __restrict__ mirror, int img_
 
 void launch_center_windows(psg_ctx* ctx, const float* mirror, int img_w, int C, int w, int nxe,
                            int64_t N, const double* mean, double* Xc) {
+  ProfScope _prof(ctx, K_BUILD);
   const int64_t n = N * (int64_t)w * w * C;
   center_windows_kernel<<<grid_cap(ctx, n, 256), 256, 0, ctx->stream>>>(mirror, img_w, C, w, nxe,
                                                                          N, mean, Xc);
@@ -89,6 +91,7 @@ __global__ void vector_mean_kernel(const float* __restrict__ X, int64_t N, int D
 }
 
 void launch_vector_mean(psg_ctx* ctx, const float* X, int64_t N, int D, double* mean) {
+  ProfScope _prof(ctx, K_BUILD);
   vector_mean_kernel<<<D, 256, 0, ctx->stream>>>(X, N, D, mean);
   PSG_LAUNCHED(ctx);
 }
@@ -104,6 +107,7 @@ __global__ void center_vectors_kernel(const float* __restrict__ X, int64_t N, in
 
 void launch_center_vectors(psg_ctx* ctx, const float* X, int64_t N, int D, const double* mean,
                            double* Xc) {
+  ProfScope _prof(ctx, K_BUILD);
   center_vectors_kernel<<<grid_cap(ctx, N * D, 256), 256, 0, ctx->stream>>>(X, N, D, mean, Xc);
   PSG_LAUNCHED(ctx);
 }
@@ -124,6 +128,7 @@ __global__ void downsample_kernel(const double* __restrict__ in, int W, int H, i
 }
 
 void launch_downsample(psg_ctx* ctx, const double* in, int W, int H, int f, double* out) {
+  ProfScope _prof(ctx, K_PYRAMID);
   const int ow = W / f, oh = H / f;
   downsample_kernel<<<grid_cap(ctx, (int64_t)ow * oh, 256), 256, 0, ctx->stream>>>(in, W, H, f,
                                                                                     out, ow, oh);
@@ -162,6 +167,7 @@ __global__ void upsample_kernel(const double* __restrict__ in, int W, int H, int
 }
 
 void launch_upsample_bilinear(psg_ctx* ctx, const double* in, int W, int H, int f, double* out) {
+  ProfScope _prof(ctx, K_PYRAMID);
   upsample_kernel<<<grid_cap(ctx, (int64_t)W * f * H * f, 256), 256, 0, ctx->stream>>>(in, W, H,
                                                                                        f, out);
   PSG_LAUNCHED(ctx);
@@ -178,6 +184,7 @@ __global__ void fit_to_kernel(const double* __restrict__ in, int W, int H, int o
 }
 
 void launch_fit_to(psg_ctx* ctx, const double* in, int W, int H, int ow, int oh, double* out) {
+  ProfScope _prof(ctx, K_PYRAMID);
   fit_to_kernel<<<grid_cap(ctx, (int64_t)ow * oh, 256), 256, 0, ctx->stream>>>(in, W, H, ow, oh,
                                                                                out);
   PSG_LAUNCHED(ctx);

@@ -40,6 +40,7 @@ __global__ void weights_kernel(WeightArgs a) {
 }
 
 void launch_weights(psg_ctx* ctx, const WeightArgs& a) {
+  ProfScope _prof(ctx, K_WEIGHTS);
   if (a.A <= 0) return;
   weights_kernel<<<grid_for(ctx, a.A, 256), 256, 0, ctx->stream>>>(a);
   PSG_LAUNCHED(ctx);
@@ -57,6 +58,7 @@ __global__ void eff_kernel(const double* __restrict__ irls, const double* __rest
 
 void launch_eff_from(psg_ctx* ctx, const double* irls, const double* pen, int64_t A, double* eff,
                      int* flags) {
+  ProfScope _prof(ctx, K_WEIGHTS);
   if (A <= 0) return;
   eff_kernel<<<grid_for(ctx, A, 256), 256, 0, ctx->stream>>>(irls, pen, A, eff, flags);
   PSG_LAUNCHED(ctx);
@@ -83,6 +85,7 @@ __global__ void hist_count_kernel(const double* __restrict__ planes, int64_t P, 
 
 void launch_hist_count(psg_ctx* ctx, const double* planes, int64_t P, int bins, int slots,
                        unsigned long long* counts) {
+  ProfScope _prof(ctx, K_HIST);
   PSG_CUDA(cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * bins * slots, ctx->stream));
   const size_t sm = sizeof(unsigned int) * bins * slots;
   hist_count_kernel<<<grid_for(ctx, P, 256, 4), 256, sm, ctx->stream>>>(planes, P, bins, slots,
@@ -106,6 +109,7 @@ __global__ void hist_fold_kernel(const unsigned long long* __restrict__ counts, 
 
 void launch_hist_fold(psg_ctx* ctx, const unsigned long long* counts, int bins, int slots,
                       int64_t P, const double* ex_mass, double* mass, double* excess) {
+  ProfScope _prof(ctx, K_HIST);
   const int n = bins * slots;
   hist_fold_kernel<<<(n + 63) / 64, 64, 0, ctx->stream>>>(counts, n, P, ex_mass, mass, excess);
   PSG_LAUNCHED(ctx);
@@ -140,6 +144,7 @@ __global__ void penalty_kernel(const float* __restrict__ ex_mirror, int ew, int 
 
 void launch_penalty(psg_ctx* ctx, const Index& ix, const int32_t* idx, int64_t A,
                     const double* excess, int bins, int slots, double* pen) {
+  ProfScope _prof(ctx, K_PENALTY);
   if (A <= 0) return;
   const size_t sm = sizeof(double) * bins * slots;
   penalty_kernel<<<grid_for(ctx, A, 128), 128, sm, ctx->stream>>>(
@@ -196,6 +201,7 @@ __global__ void __launch_bounds__(256) mstep_kernel(MstepArgs a) {
 }
 
 void launch_mstep(psg_ctx* ctx, const MstepArgs& a) {
+  ProfScope _prof(ctx, K_MSTEP);
   const int64_t P = (int64_t)a.W * a.H;
   if (P <= 0) return;
   const int blocks = grid_for(ctx, P, 256, 16);
@@ -259,6 +265,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(StatsArgs a) {
 }
 
 void launch_stats(psg_ctx* ctx, const StatsArgs& a) {
+  ProfScope _prof(ctx, K_STATS);
   stats_kernel<<<1, kStatsThreads, 0, ctx->stream>>>(a);
   PSG_LAUNCHED(ctx);
 }

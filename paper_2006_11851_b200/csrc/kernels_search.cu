@@ -26,6 +26,7 @@ __global__ void make_mirror_kernel(const double* __restrict__ planes, int C, int
 }
 
 void launch_make_mirror(psg_ctx* ctx, const double* planes, int C, int W, int H, float* mirror) {
+  ProfScope _prof(ctx, K_MIRROR);
   const int64_t P = (int64_t)W * H;
   const int threads = 256;
   int blocks = (int)((P + threads - 1) / threads);
@@ -133,6 +134,7 @@ template <bool kWindows>
 static void launch_project(psg_ctx* ctx, const float* src, int img_w, int C, int w,
                            const int32_t* xs, const int32_t* ys, int nx, int64_t n, int D, int JC,
                            const double* mean, const double* basisT, int d, double* out) {
+  ProfScope _prof(ctx, K_PROJECT);
   if (n <= 0 || d <= 0) return;
   constexpr int RQ = 8;
   const int TQ = 8 * RQ;
@@ -418,6 +420,7 @@ __global__ void __launch_bounds__(32 * kSearchWarps) search_kernel(SearchArgs a)
 }
 
 void launch_search(psg_ctx* ctx, const SearchArgs& a) {
+  ProfScope _prof(ctx, K_SEARCH);
   if (a.nq <= 0) return;
   if (a.d > kMaxD) fail(PSG_E_DOMAIN, "retained PCA dimension > 64 is not supported");
   int64_t blocks = (a.nq + kSearchWarps - 1) / kSearchWarps;
@@ -459,6 +462,7 @@ __global__ void rescore_windows_kernel(const float* __restrict__ mirror, int img
 void launch_rescore_windows(psg_ctx* ctx, const float* mirror, int img_w, int C, int w,
                             AnchorSet anchors, const Index& ix, const int32_t* idx,
                             double* dist) {
+  ProfScope _prof(ctx, K_RESCORE);
   if (anchors.count <= 0) return;
   const int threads = 128;
   int64_t blocks = (anchors.count + threads - 1) / threads;
@@ -488,6 +492,7 @@ __global__ void rescore_vectors_kernel(const float* __restrict__ Q, int64_t nq, 
 
 void launch_rescore_vectors(psg_ctx* ctx, const float* Q, int64_t nq, const Index& ix,
                             const int32_t* idx, double* dist) {
+  ProfScope _prof(ctx, K_RESCORE);
   if (nq <= 0) return;
   const int threads = 128;
   int64_t blocks = (nq + threads - 1) / threads;
@@ -511,6 +516,7 @@ __global__ void gather_soa_kernel(const double* __restrict__ proj, int64_t N, in
 
 void launch_gather_soa(psg_ctx* ctx, const double* proj, int64_t N, int d, const int32_t* perm,
                        double* soa) {
+  ProfScope _prof(ctx, K_BUILD);
   if (N <= 0 || d <= 0) return;
   int64_t blocks = (N * d + 255) / 256;
   if (blocks > (int64_t)ctx->num_sms * 32) blocks = (int64_t)ctx->num_sms * 32;

@@ -85,7 +85,22 @@ struct Index {
 
 }  // namespace psg
 
+namespace psg {
+enum KernelKind : int {
+  K_MIRROR = 0, K_PROJECT, K_SEARCH, K_RESCORE, K_WEIGHTS, K_HIST, K_PENALTY, K_MSTEP, K_STATS,
+  K_BUILD, K_PYRAMID, K_COUNT
+};
+extern const char* const kKernelNames[K_COUNT];
+}  // namespace psg
+
 struct psg_ctx {
+  // per-kernel event timing (psg_ctx_profile)
+  bool profile = false;
+  std::vector<cudaEvent_t> ev_pool;
+  struct Pending { int kind; cudaEvent_t a, b; };
+  std::vector<Pending> pending;
+  double kernel_ms[psg::K_COUNT] = {};
+  int64_t kernel_launches[psg::K_COUNT] = {};
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -105,6 +120,16 @@ struct psg_index {
 };
 
 namespace psg {
+
+// RAII event pair around one kernel launch when profiling is enabled.
+struct ProfScope {
+  psg_ctx* ctx;
+  int kind;
+  cudaEvent_t a = nullptr;
+  ProfScope(psg_ctx* c, int k);
+  ~ProfScope();
+};
+void prof_flush(psg_ctx* ctx);  // after a stream sync: accumulate elapsed times
 
 // ---- kernel launchers (kernels_*.cu) ------------------------------------------
 struct AnchorSet {

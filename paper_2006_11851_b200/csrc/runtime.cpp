@@ -72,6 +72,7 @@ void check_flags(psg_ctx* ctx) {
   int f = 0;
   PSG_CUDA(cudaMemcpyAsync(&f, ctx->d_flags, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+  prof_flush(ctx);
   if (!f) return;
   PSG_CUDA(cudaMemsetAsync(ctx->d_flags, 0, sizeof(int), ctx->stream));
   if (f & FLAG_BAD_DISTANCE) fail(PSG_E_DOMAIN, "distance must be non-negative");
@@ -118,6 +119,51 @@ double now_ms() {
   return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
 }
 }  // namespace
+
+const char* const kKernelNames[K_COUNT] = {
+    "make_mirror", "project_kernel", "search_kernel", "rescore_kernel", "weights_kernel",
+    "hist_kernels", "penalty_kernel", "mstep_kernel", "stats_kernel", "build_kernels",
+    "pyramid_kernels"};
+
+ProfScope::ProfScope(psg_ctx* c, int k) : ctx(c), kind(k) {
+  if (!ctx->profile) return;
+  if (ctx->ev_pool.empty()) {
+    cudaEvent_t e;
+    PSG_CUDA(cudaEventCreate(&e));
+    ctx->ev_pool.push_back(e);
+  }
+  a = ctx->ev_pool.back();
+  ctx->ev_pool.pop_back();
+  PSG_CUDA(cudaEventRecord(a, ctx->stream));
+}
+
+ProfScope::~ProfScope() {
+  if (!a) return;
+  cudaEvent_t b;
+  if (ctx->ev_pool.empty()) {
+    if (cudaEventCreate(&b) != cudaSuccess) return;
+  } else {
+    b = ctx->ev_pool.back();
+    ctx->ev_pool.pop_back();
+  }
+  cudaEventRecord(b, ctx->stream);
+  ctx->pending.push_back({kind, a, b});
+}
+
+void prof_flush(psg_ctx* ctx) {
+  if (ctx->pending.empty()) return;
+  PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (const auto& p : ctx->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+      ctx->kernel_ms[p.kind] += ms;
+      ctx->kernel_launches[p.kind] += 1;
+    }
+    ctx->ev_pool.push_back(p.a);
+    ctx->ev_pool.push_back(p.b);
+  }
+  ctx->pending.clear();
+}
 
 std::vector<int32_t> axis_positions(int extent, int window, int step) {  // neighborhood.cpp:12-18
   std::vector<int32_t> xs;
@@ -557,6 +603,7 @@ bool level_step(psg_level& L, psg_iter_stats* st, bool honor) {
     st->lsq_energy_after = L.stats_host[1];
     st->points_scanned = (int64_t)L.stats_host[4] + L.pending_scanned;
     st->unique_queries = L.A * (L.pending_calls ? 2 : 1);
+    st->unique_points_scanned = (int64_t)L.stats_host[5];
   }
   L.pending_calls = 0;
   L.pending_scanned = 0;
@@ -636,6 +683,11 @@ void psg_ctx_destroy(psg_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (auto& p : ctx->pending) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->cublas) cublasDestroy(static_cast<cublasHandle_t>(ctx->cublas));
   if (ctx->cusolver) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(ctx->cusolver));
   cudaFree(ctx->d_flags);
@@ -648,6 +700,32 @@ psg_status psg_ctx_synchronize(psg_ctx* ctx) {
 }
 
 int64_t psg_ctx_launch_count(const psg_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+psg_status psg_ctx_profile(psg_ctx* ctx, int enable) {
+  return guarded([&] {
+    if (!ctx) fail(PSG_E_DOMAIN, "null context");
+    psg::prof_flush(ctx);
+    ctx->profile = enable != 0;
+    for (int k = 0; k < psg::K_COUNT; ++k) {
+      ctx->kernel_ms[k] = 0.0;
+      ctx->kernel_launches[k] = 0;
+    }
+  });
+}
+
+int psg_ctx_kernel_times(psg_ctx* ctx, const char** names, double* ms, int64_t* launches, int n) {
+  if (!ctx) return 0;
+  try {
+    psg::prof_flush(ctx);
+  } catch (...) {
+  }
+  for (int k = 0; k < psg::K_COUNT && k < n; ++k) {
+    if (names) names[k] = psg::kKernelNames[k];
+    if (ms) ms[k] = ctx->kernel_ms[k];
+    if (launches) launches[k] = ctx->kernel_launches[k];
+  }
+  return psg::K_COUNT;
+}
 
 psg_status psg_index_create(psg_ctx* ctx, const double* ex_planes, int C, int ew, int eh, int w,
                             const double* mean, const double* basis, int d,

@@ -49,7 +49,8 @@ class psg_iter_stats(ct.Structure):
     _fields_ = [("iteration", ct.c_int), ("energy", ct.c_double), ("changed", ct.c_int64),
                 ("nn_calls", ct.c_int64), ("millis", ct.c_double),
                 ("lsq_energy_before", ct.c_double), ("lsq_energy_after", ct.c_double),
-                ("points_scanned", ct.c_int64), ("unique_queries", ct.c_int64)]
+                ("points_scanned", ct.c_int64), ("unique_queries", ct.c_int64),
+                ("unique_points_scanned", ct.c_int64)]
 
 
 class psg_stage_list(ct.Structure):
@@ -90,6 +91,8 @@ _SIGS = {
     "psg_ctx_destroy": (None, [VP]),
     "psg_ctx_synchronize": (I, [VP]),
     "psg_ctx_launch_count": (I64, [VP]),
+    "psg_ctx_profile": (I, [VP, I]),
+    "psg_ctx_kernel_times": (I, [VP, VP, VP, VP, I]),
     "psg_index_create": (I, [VP, VP, I, I, I, I, VP, VP, I, ct.POINTER(psg_index_cfg), PP]),
     "psg_index_create_vectors": (I, [VP, VP, I64, I, VP, VP, I, ct.POINTER(psg_index_cfg), PP]),
     "psg_index_destroy": (None, [VP]),
