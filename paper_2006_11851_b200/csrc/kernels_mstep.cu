@@ -10,6 +10,8 @@
 //   energy_from_distances optimizer.cpp:126-131
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "numerics.cuh"
 #include "psg_internal.h"
 
@@ -216,14 +218,21 @@ void launch_mstep(psg_ctx* ctx, const MstepArgs& a) {
 }
 
 // ---- deterministic telemetry reductions ---------------------------------------------
-// One CTA, fixed per-thread strides and a fixed tree: run-to-run identical.
-constexpr int kStatsThreads = 512;
-__global__ void __launch_bounds__(kStatsThreads) stats_kernel(StatsArgs a) {
+// Two passes with a fixed partition and fixed trees (run-to-run identical):
+// kStatsBlocks CTAs reduce contiguous anchor ranges, one CTA folds the partials.
+constexpr int kStatsThreads = 256;
+constexpr int kStatsBlocks = 296;
+
+__global__ void __launch_bounds__(kStatsThreads) stats_partial_kernel(StatsArgs a,
+                                                                      double* __restrict__ part) {
   __shared__ double sd[3][kStatsThreads];
   __shared__ long long si[3][kStatsThreads];
+  const int64_t chunk = (a.A + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = blockIdx.x * chunk;
+  const int64_t hi = min(a.A, lo + chunk);
   double lb = 0.0, la = 0.0, en = 0.0;
   long long ch = 0, sp = 0, su = 0;
-  for (int64_t i = threadIdx.x; i < a.A; i += blockDim.x) {
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     if (a.eff && a.cur_dist) {
       const double d = a.cur_dist[i];
       lb = dadd(lb, dmul(dmul(a.eff[i], d), d));  // optimizer.cpp:473
@@ -255,19 +264,38 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(StatsArgs a) {
     __syncthreads();
   }
   if (t == 0) {
-    a.out[0] = sd[0][0];
-    a.out[1] = sd[1][0];
-    a.out[2] = sd[2][0];
-    a.out[3] = (double)si[0][0];
-    a.out[4] = (double)si[1][0];
-    a.out[5] = (double)si[2][0];
+    double* o = part + blockIdx.x * 6;
+    o[0] = sd[0][0];
+    o[1] = sd[1][0];
+    o[2] = sd[2][0];
+    o[3] = (double)si[0][0];
+    o[4] = (double)si[1][0];
+    o[5] = (double)si[2][0];
+  }
+}
+
+__global__ void stats_final_kernel(const double* __restrict__ part, int nb,
+                                   double* __restrict__ out) {
+  const int k = threadIdx.x;
+  if (k >= 6) return;
+  if (k < 3) {
+    double acc = 0.0;
+    for (int b = 0; b < nb; ++b) acc = dadd(acc, part[b * 6 + k]);
+    out[k] = acc;
+  } else {
+    long long acc = 0;
+    for (int b = 0; b < nb; ++b) acc += (long long)part[b * 6 + k];
+    out[k] = (double)acc;
   }
 }
 
 void launch_stats(psg_ctx* ctx, const StatsArgs& a) {
   ProfScope _prof(ctx, K_STATS);
-  stats_kernel<<<1, kStatsThreads, 0, ctx->stream>>>(a);
+  const int nb = (int)std::min<int64_t>(kStatsBlocks, std::max<int64_t>(1, (a.A + 255) / 256));
+  stats_partial_kernel<<<nb, kStatsThreads, 0, ctx->stream>>>(a, a.out + 8);
+  stats_final_kernel<<<1, 32, 0, ctx->stream>>>(a.out + 8, nb, a.out);
   PSG_LAUNCHED(ctx);
+  ctx->launches++;
 }
 
 }  // namespace psg

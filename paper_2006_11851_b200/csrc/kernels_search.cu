@@ -419,14 +419,304 @@ __global__ void __launch_bounds__(32 * kSearchWarps) search_kernel(SearchArgs a)
   }
 }
 
+// ----------------------------------------------------------------------------
+// Exact search (the bit-parity mode, km_tree.cpp:251-278 semantics: the
+// lexicographic minimum of (fp64 dist^2, id) over ALL database points).
+//
+//  * upper bound first: the query's previous assignment and its four lattice
+//    neighbours' assignments shifted by the anchor offset (texture coherence)
+//    are evaluated exactly; the smallest is the starting (best, best_id);
+//  * traversal: depth-first, nearest child first, one warp per query.  Child
+//    bounds max(ball, box) are computed in fp32 from outward-rounded data with
+//    a slack dominating every fp32 rounding term, so a bound never exceeds the
+//    true distance and pruning stays exact;
+//  * leaves: consecutive leaf entries on the stack are scanned together (up to
+//    32 points per warp pass); each lane evaluates an fp32 dist^2 with a
+//    rigorous error bound and only points that can still be <= best are
+//    re-evaluated with the reference's exact fp64 j-sequential chain; ties go
+//    to the lowest id (km_tree.cpp:134).
+template <int DP>
+__global__ void __launch_bounds__(256) search_exact_kernel(SearchArgs a) {
+  constexpr int W = 8;
+  __shared__ double qs_all[W][DP];
+  __shared__ __align__(16) float q32_all[W][DP];
+  __shared__ int32_t st_node[W][kStack];
+  __shared__ float st_key[W][kStack];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* qs = qs_all[warp];
+  float* q32 = q32_all[warp];
+  int32_t* sn = st_node[warp];
+  float* sk = st_key[warp];
+  const int d = a.d;
+  const int N = (int)a.N;
+  const int nn = a.tree.n_nodes;
+  const int KB = d < kBoxDims ? d : kBoxDims;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+
+  for (int64_t q = (int64_t)blockIdx.x * W + warp; q < a.nq; q += (int64_t)gridDim.x * W) {
+    double qn2 = 0.0;
+    for (int j = lane; j < DP; j += 32) {
+      const double v = j < d ? a.q[q * d + j] : 0.0;
+      qs[j] = v;
+      q32[j] = (float)v;
+      qn2 += v * v;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) qn2 += __shfl_xor_sync(0xffffffffu, qn2, off);
+    const float qn = __double2float_ru(sqrt(qn2) * (1.0 + 1e-12));
+    __syncwarp();
+    double best = kInf;
+    int32_t best_id = 0x7fffffff;
+    int64_t scanned = 0, exact_evals = 0;
+
+    // ---- coherence seeds: exact dist^2 of up to 5 candidates, one per lane ----
+    if (a.seed_idx) {
+      int32_t cand = -1;
+      if (lane == 0) {
+        cand = a.seed_idx[q];
+      } else if (lane <= 4 && a.qxs) {
+        const int qix = (int)(q % a.qnx), qiy = (int)(q / a.qnx);
+        const int qny = (int)(a.nq / a.qnx);
+        const int nix = qix + (lane == 1 ? -1 : lane == 2 ? 1 : 0);
+        const int niy = qiy + (lane == 3 ? -1 : lane == 4 ? 1 : 0);
+        if (nix >= 0 && nix < a.qnx && niy >= 0 && niy < qny) {
+          const int32_t e = a.seed_idx[(int64_t)niy * a.qnx + nix];
+          const int ex = e % a.nxe + (a.qxs[qix] - a.qxs[nix]);
+          const int ey = e / a.nxe + (a.qys[qiy] - a.qys[niy]);
+          if (ex >= 0 && ex < a.nxe && ey >= 0 && ey < a.nye) cand = ey * a.nxe + ex;
+        }
+      }
+      double d2 = kInf;
+      if (cand >= 0) d2 = dist2_seq(qs, a.proj + (int64_t)cand * d, d);
+      const WarpLexMin m = warp_lexmin(d2, cand >= 0 ? cand : 0x7fffffff);
+      best = m.d2;
+      best_id = m.id;
+      const int ns = __popc(__ballot_sync(0xffffffffu, cand >= 0));
+      scanned += ns;
+      exact_evals += ns;
+    }
+    if (lane == 0) {
+      sn[0] = 0;
+      sk[0] = 0.f;
+    }
+    int top = 1;
+    __syncwarp();
+    while (top > 0) {
+      // ---- gather a batch of leaves from the stack top (warp-uniform) ----------
+      int bnode[4], bcnt[4];
+      int nb = 0, tot = 0;
+      int node = -1;
+      while (top > 0) {
+        const int nd = sn[top - 1];
+        const float key = sk[top - 1];
+        if ((double)key > best) {  // km_tree.cpp:265 prune
+          --top;
+          continue;
+        }
+        if (a.tree.n_children[nd] != 0) {
+          if (nb == 0) {
+            node = nd;
+            --top;
+          }
+          break;
+        }
+        const int cnt = a.tree.leaf_count[nd];
+        if (nb > 0 && (tot + cnt > 32 || nb == 4)) break;
+        --top;
+        bnode[nb] = nd;
+        bcnt[nb] = cnt;
+        ++nb;
+        tot += cnt;
+        if (tot >= 32) break;
+      }
+      __syncwarp();
+      if (nb > 0) {
+        for (int b = 0; b < nb; ++b) scanned += bcnt[b];
+        int bstart[4];
+        for (int b = 0; b < nb; ++b) bstart[b] = a.tree.leaf_start[bnode[b]];
+        const int chunks = (tot + 31) / 32;
+        for (int ck = 0; ck < chunks; ++ck) {
+          int i = ck * 32 + lane;
+          int pos = -1;
+          if (i < tot) {
+            int b = 0;
+#pragma unroll
+            for (int t = 0; t < 3; ++t)
+              if (b < nb - 1 && i >= bcnt[b]) i -= bcnt[b++];
+            pos = bstart[b] + i;
+          }
+          float s = 0.f, eps = 0.f;
+          if (pos >= 0) {
+            const float4* row = reinterpret_cast<const float4*>(a.proj32_aos + (int64_t)pos * DP);
+            float4 p[DP / 4];
+#pragma unroll
+            for (int k = 0; k < DP / 4; ++k) p[k] = (4 * k < d) ? __ldg(row + k) : make_float4(0, 0, 0, 0);
+            const float4* qv = reinterpret_cast<const float4*>(q32);
+#pragma unroll
+            for (int k = 0; k < DP / 4; ++k) {
+              const float4 qq = qv[k];
+              float t = qq.x - p[k].x;
+              s = fmaf(t, t, s);
+              t = qq.y - p[k].y;
+              s = fmaf(t, t, s);
+              t = qq.z - p[k].z;
+              s = fmaf(t, t, s);
+              t = qq.w - p[k].w;
+              s = fmaf(t, t, s);
+            }
+            const float pn = a.pnorm32[pos];
+            eps = 2.5e-7f * (float)(d + 4) * s + 1.0e-6f * (qn + pn) * (sqrtf(s) + 1e-3f) + 1e-30f;
+          }
+          const bool surv = pos >= 0 && (double)s - (double)eps <= best;
+          const unsigned smask = __ballot_sync(0xffffffffu, surv);
+          if (!smask) continue;
+          double d2 = kInf;
+          int32_t id = 0x7fffffff;
+          if (surv) {
+            id = a.perm[pos];
+            const double* col = a.proj_soa + pos;
+            double acc = 0.0;
+#pragma unroll
+            for (int j0 = 0; j0 < DP; j0 += 16) {
+              if (j0 < d) {
+                double p[16];
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) p[jj] = (j0 + jj < d) ? col[(int64_t)(j0 + jj) * N] : 0.0;
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) {
+                  if (j0 + jj < d) {
+                    const double t = dsub(qs[j0 + jj], p[jj]);
+                    acc = dadd(acc, dmul(t, t));
+                  }
+                }
+              }
+            }
+            d2 = acc;
+          }
+          exact_evals += __popc(smask);
+          const WarpLexMin m = warp_lexmin(d2, id);
+          if (lex_less(m.d2, m.id, best, best_id)) {
+            best = m.d2;
+            best_id = m.id;
+          }
+        }
+        continue;
+      }
+      if (node < 0) break;
+      // ---- expand an internal node: lanes (child, dim-group) -------------------
+      const int nc = a.tree.n_children[node];
+      const int fc = a.tree.first_child[node];
+      for (int cb = 0; cb < nc; cb += 32) {
+        const int ncb = min(32, nc - cb);
+        // lanes per child: largest power of two with ncp * lpc <= 32
+        const int ncp = ncb <= 1 ? 1 : ncb <= 2 ? 2 : ncb <= 4 ? 4 : ncb <= 8 ? 8 : ncb <= 16 ? 16 : 32;
+        const int lpc = 32 / ncp;
+        const int c = lane % ncp, g = lane / ncp;
+        const bool valid = c < ncb;
+        const int cid = fc + cb + (valid ? c : 0);
+        float s = 0.f, bx = 0.f;
+        for (int j = g; j < d; j += lpc) {
+          const float t = q32[j] - a.tree.centroid32T[(int64_t)j * nn + cid];
+          s = fmaf(t, t, s);
+        }
+        for (int j = g; j < KB; j += lpc) {
+          const float qj = q32[j];
+          const float lo = a.tree.boxlo[(int64_t)j * nn + cid];
+          const float hi = a.tree.boxhi[(int64_t)j * nn + cid];
+          float gap = fmaxf(lo - qj, qj - hi) - 2.4e-7f * (fabsf(qj) + fabsf(lo) + fabsf(hi));
+          gap = fmaxf(gap, 0.f);
+          bx = fmaf(gap, gap, bx);
+        }
+        for (int off = ncp; off < 32; off <<= 1) {
+          s += __shfl_xor_sync(0xffffffffu, s, off);
+          bx += __shfl_xor_sync(0xffffffffu, bx, off);
+        }
+        float lb2 = __int_as_float(0x7f800000);
+        bool keep = false;
+        if (valid) {
+          const float dc = sqrtf(s);
+          const float rad = a.tree.radius32[cid];
+          const float slack = 2e-5f * (1.f + dc + rad + qn + a.tree.cnorm32[cid]);
+          const float lb = dc - rad - slack;
+          lb2 = lb > 0.f ? lb * lb * (1.f - 1e-6f) : 0.f;
+          lb2 = fmaxf(lb2, bx * (1.f - 1e-5f));
+          keep = (double)lb2 <= best;
+        }
+        // one representative lane (g == 0) per child
+        const unsigned km = __ballot_sync(0xffffffffu, keep && g == 0);
+        const int nkeep = __popc(km);
+        int rank = 0;
+        for (int o = 0; o < ncb; ++o) {
+          const float ol = __shfl_sync(0xffffffffu, lb2, o);
+          if (((km >> o) & 1u) && (ol < lb2 || (ol == lb2 && o < c))) ++rank;
+        }
+        if (top + nkeep > kStack) {
+          if (lane == 0) atomicOr(a.flags, FLAG_STACK_OVERFLOW);
+          break;
+        }
+        if (keep && g == 0) {
+          const int slot = top + nkeep - 1 - rank;  // nearest child popped first
+          sn[slot] = cid;
+          sk[slot] = lb2;
+        }
+        top += nkeep;
+        __syncwarp();
+      }
+    }
+    if (lane == 0) {
+      a.out_idx[q] = best_id;
+      a.out_d2[q] = best;
+      if (a.out_scanned) a.out_scanned[q] = scanned;
+      if (a.out_exact) a.out_exact[q] = exact_evals;
+    }
+    __syncwarp();
+  }
+}
+
 void launch_search(psg_ctx* ctx, const SearchArgs& a) {
   ProfScope _prof(ctx, K_SEARCH);
   if (a.nq <= 0) return;
   if (a.d > kMaxD) fail(PSG_E_DOMAIN, "retained PCA dimension > 64 is not supported");
+  if (a.mode == PSG_EXACT && a.proj32_aos && a.tree.centroid32T) {
+    int64_t blocks = (a.nq + 7) / 8;
+    const int64_t cap = (int64_t)ctx->num_sms * 8;
+    if (blocks > cap) blocks = cap;
+    if (a.d <= 32)
+      search_exact_kernel<32><<<(int)blocks, 256, 0, ctx->stream>>>(a);
+    else
+      search_exact_kernel<64><<<(int)blocks, 256, 0, ctx->stream>>>(a);
+    PSG_LAUNCHED(ctx);
+    return;
+  }
   int64_t blocks = (a.nq + kSearchWarps - 1) / kSearchWarps;
   const int64_t cap = (int64_t)ctx->num_sms * 16;
   if (blocks > cap) blocks = cap;
   search_kernel<<<(int)blocks, 32 * kSearchWarps, 0, ctx->stream>>>(a);
+  PSG_LAUNCHED(ctx);
+}
+
+// fp32 filter copies in leaf order: aos32[pos][dp] = (float) soa[j][pos], |p| rounded up.
+__global__ void make_fp32_copies_kernel(const double* __restrict__ soa, int64_t N, int d, int dp,
+                                        float* __restrict__ aos32, float* __restrict__ pn) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double n2 = 0.0;
+    for (int j = 0; j < dp; ++j) {
+      const double v = j < d ? soa[(int64_t)j * N + i] : 0.0;
+      aos32[i * dp + j] = (float)v;
+      n2 += v * v;
+    }
+    pn[i] = __double2float_ru(sqrt(n2) * (1.0 + 1e-12));
+  }
+}
+
+void launch_make_fp32_copies(psg_ctx* ctx, const double* soa, int64_t N, int d, int dp,
+                             float* aos32, float* pn) {
+  ProfScope _prof(ctx, K_BUILD);
+  if (N <= 0) return;
+  int64_t blocks = (N + 255) / 256;
+  if (blocks > (int64_t)ctx->num_sms * 32) blocks = (int64_t)ctx->num_sms * 32;
+  make_fp32_copies_kernel<<<(int)blocks, 256, 0, ctx->stream>>>(soa, N, d, dp, aos32, pn);
   PSG_LAUNCHED(ctx);
 }
 

@@ -49,12 +49,21 @@ struct DevTree {
   int32_t* n_children = nullptr;  // 0 = leaf
   int32_t* leaf_start = nullptr;  // leaves: range in the leaf-ordered point arrays
   int32_t* leaf_count = nullptr;
+  // fp32 bound data (conservative: radius and norms rounded up, boxes outward)
+  float* centroid32 = nullptr;  // [n_nodes][d]
+  float* centroid32T = nullptr; // [d][n_nodes]: children of a node are contiguous per dim
+  float* radius32 = nullptr;
+  float* cnorm32 = nullptr;     // |centroid|
+  float* boxlo = nullptr;       // [kBoxDims][n_nodes] per-dim minimum over the subtree
+  float* boxhi = nullptr;       // [kBoxDims][n_nodes]
 };
+constexpr int kBoxDims = 8;     // leading PCA dims carrying bounding boxes
 
 struct HostTree {
   std::vector<double> centroid, radius;
   std::vector<int32_t> first_child, n_children, leaf_start, leaf_count, depth;
   std::vector<int32_t> perm;  // leaf order -> point id
+  std::vector<double> boxlo, boxhi;  // [n_nodes][kBoxDims]
   int max_depth = 0;
   int n_leaves = 0;
 };
@@ -72,6 +81,9 @@ struct Index {
   double* basis = nullptr;     // [d][D]
   double* proj = nullptr;      // [N][d] original order
   double* proj_soa = nullptr;  // [d][N] leaf order
+  float* proj32_aos = nullptr; // [N][dp] leaf order, fp32 filter copy (dp = 32 or 64)
+  int dp = 32;
+  float* pnorm32 = nullptr;    // [N] leaf order, |p| rounded up
   int32_t* perm = nullptr;     // leaf order -> id
   DevTree tree;
   HostTree htree;
@@ -155,16 +167,26 @@ struct SearchArgs {
   const int32_t* seed_idx;  // optional initial candidate per query (upper bound)
   const double* proj;       // [N][d] original order (seed distances)
   const double* proj_soa;   // [d][N] leaf order
+  const float* proj32_aos;  // [N][dp] leaf order (fp32 filter)
+  const float* pnorm32;     // [N] leaf order
   const int32_t* perm;
   int64_t N;
+  // coherence seeds (image index only): query anchor lattice + DB lattice
+  const int32_t* qxs;       // [qnx] query anchor x positions (null: no neighbour seeds)
+  const int32_t* qys;
+  int qnx;
+  int nxe, nye;             // dense DB anchors per row / column
   DevTree tree;
   int mode, max_leaves;
   int32_t* out_idx;
   double* out_d2;
   int64_t* out_scanned;
+  int64_t* out_exact;       // optional: points evaluated in exact fp64
   int* flags;
 };
 void launch_search(psg_ctx* ctx, const SearchArgs& a);
+void launch_make_fp32_copies(psg_ctx* ctx, const double* soa, int64_t N, int d, int dp,
+                             float* aos32, float* pn);
 // Full-D distance between query windows and assigned candidates (optimizer.cpp:117-124).
 void launch_rescore_windows(psg_ctx* ctx, const float* mirror, int img_w, int C, int w,
                             AnchorSet anchors, const Index& ix, const int32_t* idx, double* dist);

@@ -212,6 +212,14 @@ Index::~Index() {
   cudaFree(tree.n_children);
   cudaFree(tree.leaf_start);
   cudaFree(tree.leaf_count);
+  cudaFree(tree.centroid32);
+  cudaFree(tree.radius32);
+  cudaFree(tree.cnorm32);
+  cudaFree(proj32_aos);
+  cudaFree(tree.centroid32T);
+  cudaFree(tree.boxlo);
+  cudaFree(tree.boxhi);
+  cudaFree(pnorm32);
   cudaFree(ex_hist);
 }
 
@@ -295,6 +303,43 @@ void finish_index(psg_ctx* ctx, Index& ix, const double* mean, const double* bas
   up(ix.perm, t.perm);
   ix.proj_soa = dalloc<double>((size_t)ix.N * (d > 0 ? d : 1));
   launch_gather_soa(ctx, ix.proj, ix.N, d, ix.perm, ix.proj_soa);
+  // fp32 bound/filter copies (conservative rounding, see search_exact_kernel)
+  ix.dp = d <= 32 ? 32 : 64;
+  ix.proj32_aos = dalloc<float>((size_t)ix.N * ix.dp);
+  ix.pnorm32 = dalloc<float>(ix.N);
+  launch_make_fp32_copies(ctx, ix.proj_soa, ix.N, d, ix.dp, ix.proj32_aos, ix.pnorm32);
+  {
+    std::vector<float> c32(t.centroid.size()), c32t(t.centroid.size()), r32(nn), n32(nn);
+    std::vector<float> blo((size_t)kBoxDims * nn, 0.f), bhi((size_t)kBoxDims * nn, 0.f);
+    for (int i = 0; i < nn; ++i)
+      for (int j = 0; j < d; ++j) {
+        c32[(size_t)i * d + j] = (float)t.centroid[(size_t)i * d + j];
+        c32t[(size_t)j * nn + i] = (float)t.centroid[(size_t)i * d + j];
+      }
+    for (int i = 0; i < nn; ++i)
+      for (int j = 0; j < std::min(d, kBoxDims); ++j) {
+        blo[(size_t)j * nn + i] = std::nextafter((float)t.boxlo[(size_t)i * kBoxDims + j], -INFINITY);
+        bhi[(size_t)j * nn + i] = std::nextafter((float)t.boxhi[(size_t)i * kBoxDims + j], INFINITY);
+      }
+    ix.tree.centroid32T = dalloc<float>(c32t.empty() ? 1 : c32t.size());
+    ix.tree.boxlo = dalloc<float>(blo.size());
+    ix.tree.boxhi = dalloc<float>(bhi.size());
+    up(ix.tree.centroid32T, c32t);
+    up(ix.tree.boxlo, blo);
+    up(ix.tree.boxhi, bhi);
+    for (int i = 0; i < nn; ++i) {
+      r32[i] = std::nextafter((float)t.radius[i], INFINITY);
+      double n2 = 0.0;
+      for (int j = 0; j < d; ++j) n2 += t.centroid[(size_t)i * d + j] * t.centroid[(size_t)i * d + j];
+      n32[i] = std::nextafter((float)(std::sqrt(n2) * (1.0 + 1e-12)), INFINITY);
+    }
+    ix.tree.centroid32 = dalloc<float>(c32.empty() ? 1 : c32.size());
+    ix.tree.radius32 = dalloc<float>(nn);
+    ix.tree.cnorm32 = dalloc<float>(nn);
+    up(ix.tree.centroid32, c32);
+    up(ix.tree.radius32, r32);
+    up(ix.tree.cnorm32, n32);
+  }
   PSG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
@@ -441,7 +486,7 @@ void level_setup(psg_level& L, psg_ctx* ctx, const Index& ix, int W, int H,
   L.next_dist.alloc(L.A);
   L.after.alloc(L.A);
   L.scanned.alloc(L.A);
-  L.stats_dev.alloc(8);
+  L.stats_dev.alloc(8 + 6 * 296);
   PSG_CUDA(cudaMallocHost(&L.stats_host, sizeof(double) * 8));
   PSG_CUDA(cudaEventCreate(&L.ev0));
   PSG_CUDA(cudaEventCreate(&L.ev1));
@@ -481,7 +526,14 @@ void level_search(psg_level& L, bool seeded, int32_t* out_idx, double* out_dist)
   a.seed_idx = (seeded && L.cfg.budget.mode == PSG_EXACT) ? L.cur_idx.p : nullptr;
   a.proj = ix.proj;
   a.proj_soa = ix.proj_soa;
+  a.proj32_aos = ix.proj32_aos;
+  a.pnorm32 = ix.pnorm32;
   a.perm = ix.perm;
+  a.qxs = L.xs.p;
+  a.qys = L.ys.p;
+  a.qnx = L.nx;
+  a.nxe = ix.nxe;
+  a.nye = ix.eh - ix.w + 1;
   a.N = ix.N;
   a.tree = ix.tree;
   a.mode = L.cfg.budget.mode;
@@ -840,6 +892,8 @@ psg_status psg_index_query(psg_ctx* ctx, const psg_index* index, const float* Q,
     a.d = ix.d;
     a.proj = ix.proj;
     a.proj_soa = ix.proj_soa;
+    a.proj32_aos = ix.proj32_aos;
+    a.pnorm32 = ix.pnorm32;
     a.perm = ix.perm;
     a.N = ix.N;
     a.tree = ix.tree;

@@ -159,6 +159,8 @@ HostTree build_tree_host(const double* P, int64_t N, int d, int branching, int m
     const size_t L = level.size();
     std::vector<std::vector<std::vector<int32_t>>> splits(L);
     std::vector<double> cent(L * (size_t)d), rad(L);
+    const int KB = std::min(d, kBoxDims);
+    std::vector<double> blo(L * kBoxDims, 0.0), bhi(L * kBoxDims, 0.0);
     auto work = [&](size_t lo, size_t hi) {
       for (size_t i = lo; i < hi; ++i) {
         const auto& ids = level[i].ids;
@@ -170,6 +172,15 @@ HostTree build_tree_host(const double* P, int64_t N, int d, int branching, int m
         double r = 0.0;
         for (int32_t id : ids) r = std::max(r, std::sqrt(dist2(P + (size_t)id * d, c, d)));
         rad[i] = r;
+        for (int j = 0; j < KB; ++j) {
+          double mn = P[(size_t)ids[0] * d + j], mx = mn;
+          for (int32_t id : ids) {
+            mn = std::min(mn, P[(size_t)id * d + j]);
+            mx = std::max(mx, P[(size_t)id * d + j]);
+          }
+          blo[i * kBoxDims + j] = mn;
+          bhi[i * kBoxDims + j] = mx;
+        }
         const bool can = (int64_t)ids.size() >= leaf_threshold && d > 0 &&
                          (max_depth <= 0 || level[i].depth < max_depth);
         if (can) {
@@ -202,6 +213,8 @@ HostTree build_tree_host(const double* P, int64_t N, int d, int branching, int m
     for (size_t i = 0; i < L; ++i) {
       t.centroid.insert(t.centroid.end(), cent.begin() + i * d, cent.begin() + (i + 1) * d);
       t.radius.push_back(rad[i]);
+      t.boxlo.insert(t.boxlo.end(), blo.begin() + i * kBoxDims, blo.begin() + (i + 1) * kBoxDims);
+      t.boxhi.insert(t.boxhi.end(), bhi.begin() + i * kBoxDims, bhi.begin() + (i + 1) * kBoxDims);
       t.depth.push_back(level[i].depth);
       t.max_depth = std::max(t.max_depth, level[i].depth);
       if (!splits[i].empty()) {

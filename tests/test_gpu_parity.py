@@ -235,3 +235,44 @@ def test_synthesize_runs_multires(gpu_ctx):
     assert np.all((out >= 0) & (out <= 1))
     assert len(rep["stages"]) == 4
     assert rep["total_nn_calls"] > 0
+
+
+@pytest.mark.parametrize("size,out,G,d,b,depth", [(128, 256, 2, 32, 8, 4), (256, 1024, 2, 32, 8, 4),
+                                                  (96, 192, 1, 48, 16, 3)])
+def test_exact_search_full_size_sampled(gpu_ctx, port, size, out, G, d, b, depth):
+    """Larger stages (cfg3-like): every anchor's search runs on device, a seeded
+    sample of anchors is re-searched by the oracle (exhaustive lexmin)."""
+    ex = wl.rgbs_planes(wl.sinusoid_exemplar(size, 32, 3.0, 1), G)
+    init = wl.init_output(ex, out, out, G, 1)
+    cand, mean, basis, proj = _injected(port, ex, 8, d)
+    ix = api.make_pca_tree_index(ex, 8, mean=mean, basis=basis, branching=b, max_depth=depth,
+                                 ctx=gpu_ctx)
+    idx, dist, calls, _ = api.search_step(init, ix, 2, 2, api.QueryBudget.exact())
+    A = idx.size
+    rng = np.random.Generator(np.random.PCG64(out))
+    only = np.sort(rng.choice(A, size=min(A, 400), replace=False)).astype(np.int32)
+    i_p, d_p, c_p = port.search_step(init, 8, 2, 2, cand, proj, mean, basis, only=only)
+    assert calls == c_p
+    assert np.array_equal(idx[only], i_p)
+    assert np.array_equal(dist[only], d_p)
+
+
+def test_exact_search_ties_and_duplicates(gpu_ctx, port):
+    """Exemplar with exactly repeated windows: many exact dist^2 ties, which must
+    resolve to the lowest candidate index (km_tree.cpp:134, ann_test.cpp:338-342)."""
+    tile = wl.sinusoid_exemplar(8, 4, 1.0, 3)
+    rgb = np.tile(tile, (1, 5, 5))  # 40x40, period 8 -> every window appears ~25 times
+    ex = wl.rgbs_planes(rgb, 1)
+    ex[3] = 0.5  # constant guidance keeps the repeats exact
+    init = wl.init_output(ex, 48, 48, 1, 5)
+    init[3] = 0.5
+    cand, mean, basis, proj = _injected(port, ex, 8, 10)
+    ix = api.make_pca_tree_index(ex, 8, mean=mean, basis=basis, branching=4, max_depth=3,
+                                 ctx=gpu_ctx)
+    idx, dist, calls, _ = api.search_step(init, ix, 2, 2, api.QueryBudget.exact())
+    i_p, d_p, c_p = port.search_step(init, 8, 2, 2, cand, proj, mean, basis)
+    assert np.array_equal(idx, i_p) and np.array_equal(dist, d_p)
+    # querying the exemplar itself: distance 0 and the FIRST occurrence of each window
+    idx2, dist2, _, _ = api.search_step(ex, ix, 2, 2, api.QueryBudget.exact())
+    i2, d2, _ = port.search_step(ex, 8, 2, 2, cand, proj, mean, basis)
+    assert np.all(dist2 == 0.0) and np.array_equal(idx2, i2)
