@@ -202,6 +202,10 @@ psg_status psg_level_download(psg_level* level, double* planes, int32_t* idx, do
 /* Device pointers of the level's fp64 state planes (for device-side checks). */
 psg_status psg_level_state_dev(psg_level* level, void** planes_dev, void** idx_dev,
                                void** dist_dev);
+/* Per-anchor QueryStats of the level's last search (km_tree.hpp:27-30):
+ * points scanned, points evaluated in exact fp64, tree nodes visited. */
+psg_status psg_level_query_stats(psg_level* level, int64_t* scanned, int64_t* exact_evals,
+                                 int32_t* nodes_visited);
 void psg_level_destroy(psg_level* level);
 
 /* ---- pyramid driver (synthesize, pipeline.hpp:69, pipeline.cpp:216-315) --- */

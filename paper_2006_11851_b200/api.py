@@ -333,6 +333,15 @@ class Level:
                                         ct.cast(stats, ct.c_void_p), ct.byref(done)))
         return [IterationStats.of(stats[i]) for i in range(done.value)]
 
+    def query_stats(self):
+        """Per-anchor (points_scanned, exact fp64 evaluations, nodes_visited) of the last search."""
+        A = self.nx * self.ny
+        sc = np.zeros(A, np.int64)
+        ex = np.zeros(A, np.int64)
+        vi = np.zeros(A, np.int32)
+        N.check(N.lib.psg_level_query_stats(self.h, _p(sc), _p(ex), _p(vi)))
+        return sc, ex, vi
+
     def download(self):
         planes = np.zeros((self.C, self.H, self.W))
         A = self.nx * self.ny

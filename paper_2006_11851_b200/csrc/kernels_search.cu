@@ -440,12 +440,12 @@ __global__ void __launch_bounds__(256) search_exact_kernel(SearchArgs a) {
   constexpr int W = 8;
   __shared__ double qs_all[W][DP];
   __shared__ __align__(16) float q32_all[W][DP];
-  __shared__ int32_t st_node[W][kStack];
+  __shared__ int2 st_meta[W][kStack];   // node meta: {first child | leaf start, -children | count}
   __shared__ float st_key[W][kStack];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* qs = qs_all[warp];
   float* q32 = q32_all[warp];
-  int32_t* sn = st_node[warp];
+  int2* sm_ = st_meta[warp];
   float* sk = st_key[warp];
   const int d = a.d;
   const int N = (int)a.N;
@@ -468,6 +468,7 @@ __global__ void __launch_bounds__(256) search_exact_kernel(SearchArgs a) {
     double best = kInf;
     int32_t best_id = 0x7fffffff;
     int64_t scanned = 0, exact_evals = 0;
+    int32_t visited = 0;
 
     // ---- coherence seeds: exact dist^2 of up to 5 candidates, one per lane ----
     if (a.seed_idx) {
@@ -496,34 +497,34 @@ __global__ void __launch_bounds__(256) search_exact_kernel(SearchArgs a) {
       exact_evals += ns;
     }
     if (lane == 0) {
-      sn[0] = 0;
+      sm_[0] = a.tree.meta[0];
       sk[0] = 0.f;
     }
     int top = 1;
     __syncwarp();
     while (top > 0) {
       // ---- gather a batch of leaves from the stack top (warp-uniform) ----------
-      int bnode[4], bcnt[4];
+      int bstart[4], bcnt[4];
       int nb = 0, tot = 0;
-      int node = -1;
+      int2 node = make_int2(0, 0);
       while (top > 0) {
-        const int nd = sn[top - 1];
+        const int2 md = sm_[top - 1];
         const float key = sk[top - 1];
         if ((double)key > best) {  // km_tree.cpp:265 prune
           --top;
           continue;
         }
-        if (a.tree.n_children[nd] != 0) {
+        if (md.y < 0) {
           if (nb == 0) {
-            node = nd;
+            node = md;
             --top;
           }
           break;
         }
-        const int cnt = a.tree.leaf_count[nd];
+        const int cnt = md.y;
         if (nb > 0 && (tot + cnt > 32 || nb == 4)) break;
         --top;
-        bnode[nb] = nd;
+        bstart[nb] = md.x;
         bcnt[nb] = cnt;
         ++nb;
         tot += cnt;
@@ -532,8 +533,7 @@ __global__ void __launch_bounds__(256) search_exact_kernel(SearchArgs a) {
       __syncwarp();
       if (nb > 0) {
         for (int b = 0; b < nb; ++b) scanned += bcnt[b];
-        int bstart[4];
-        for (int b = 0; b < nb; ++b) bstart[b] = a.tree.leaf_start[bnode[b]];
+        visited += nb;
         const int chunks = (tot + 31) / 32;
         for (int ck = 0; ck < chunks; ++ck) {
           int i = ck * 32 + lane;
@@ -547,10 +547,12 @@ __global__ void __launch_bounds__(256) search_exact_kernel(SearchArgs a) {
           }
           float s = 0.f, eps = 0.f;
           if (pos >= 0) {
-            const float4* row = reinterpret_cast<const float4*>(a.proj32_aos + (int64_t)pos * DP);
+            // [dp/4][N] float4 groups: lanes read consecutive points -> coalesced
+            const float4* col = reinterpret_cast<const float4*>(a.proj32_q4) + pos;
             float4 p[DP / 4];
 #pragma unroll
-            for (int k = 0; k < DP / 4; ++k) p[k] = (4 * k < d) ? __ldg(row + k) : make_float4(0, 0, 0, 0);
+            for (int k = 0; k < DP / 4; ++k)
+              p[k] = (4 * k < d) ? __ldg(col + (int64_t)k * N) : make_float4(0, 0, 0, 0);
             const float4* qv = reinterpret_cast<const float4*>(q32);
 #pragma unroll
             for (int k = 0; k < DP / 4; ++k) {
@@ -602,10 +604,11 @@ __global__ void __launch_bounds__(256) search_exact_kernel(SearchArgs a) {
         }
         continue;
       }
-      if (node < 0) break;
+      if (node.y >= 0) break;
       // ---- expand an internal node: lanes (child, dim-group) -------------------
-      const int nc = a.tree.n_children[node];
-      const int fc = a.tree.first_child[node];
+      const int nc = -node.y;
+      ++visited;
+      const int fc = node.x;
       for (int cb = 0; cb < nc; cb += 32) {
         const int ncb = min(32, nc - cb);
         // lanes per child: largest power of two with ncp * lpc <= 32
@@ -614,18 +617,42 @@ __global__ void __launch_bounds__(256) search_exact_kernel(SearchArgs a) {
         const int c = lane % ncp, g = lane / ncp;
         const bool valid = c < ncb;
         const int cid = fc + cb + (valid ? c : 0);
+        const int2 cm = (valid && g == 0) ? a.tree.meta[cid] : make_int2(0, 0);
         float s = 0.f, bx = 0.f;
-        for (int j = g; j < d; j += lpc) {
-          const float t = q32[j] - a.tree.centroid32T[(int64_t)j * nn + cid];
-          s = fmaf(t, t, s);
+        // all loads of a block issued before use: one L2 round trip per 8 dims
+        for (int j0 = g; j0 < d; j0 += 8 * lpc) {
+          float cv[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int j = j0 + k * lpc;
+            cv[k] = j < d ? __ldg(a.tree.centroid32T + (int64_t)j * nn + cid) : 0.f;
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int j = j0 + k * lpc;
+            const float t = (j < d ? q32[j] : 0.f) - cv[k];
+            s = fmaf(t, t, s);
+          }
         }
-        for (int j = g; j < KB; j += lpc) {
-          const float qj = q32[j];
-          const float lo = a.tree.boxlo[(int64_t)j * nn + cid];
-          const float hi = a.tree.boxhi[(int64_t)j * nn + cid];
-          float gap = fmaxf(lo - qj, qj - hi) - 2.4e-7f * (fabsf(qj) + fabsf(lo) + fabsf(hi));
-          gap = fmaxf(gap, 0.f);
-          bx = fmaf(gap, gap, bx);
+        {
+          float lov[kBoxDims], hiv[kBoxDims];
+#pragma unroll
+          for (int k = 0; k < kBoxDims; ++k) {
+            const int j = g + k * lpc;
+            lov[k] = j < KB ? __ldg(a.tree.boxlo + (int64_t)j * nn + cid) : 0.f;
+            hiv[k] = j < KB ? __ldg(a.tree.boxhi + (int64_t)j * nn + cid) : 0.f;
+          }
+#pragma unroll
+          for (int k = 0; k < kBoxDims; ++k) {
+            const int j = g + k * lpc;
+            if (j < KB) {
+              const float qj = q32[j];
+              float gap = fmaxf(lov[k] - qj, qj - hiv[k]) -
+                          2.4e-7f * (fabsf(qj) + fabsf(lov[k]) + fabsf(hiv[k]));
+              gap = fmaxf(gap, 0.f);
+              bx = fmaf(gap, gap, bx);
+            }
+          }
         }
         for (int off = ncp; off < 32; off <<= 1) {
           s += __shfl_xor_sync(0xffffffffu, s, off);
@@ -656,7 +683,7 @@ __global__ void __launch_bounds__(256) search_exact_kernel(SearchArgs a) {
         }
         if (keep && g == 0) {
           const int slot = top + nkeep - 1 - rank;  // nearest child popped first
-          sn[slot] = cid;
+          sm_[slot] = cm;
           sk[slot] = lb2;
         }
         top += nkeep;
@@ -668,6 +695,7 @@ __global__ void __launch_bounds__(256) search_exact_kernel(SearchArgs a) {
       a.out_d2[q] = best;
       if (a.out_scanned) a.out_scanned[q] = scanned;
       if (a.out_exact) a.out_exact[q] = exact_evals;
+      if (a.out_visited) a.out_visited[q] = visited;
     }
     __syncwarp();
   }
@@ -677,7 +705,7 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
   ProfScope _prof(ctx, K_SEARCH);
   if (a.nq <= 0) return;
   if (a.d > kMaxD) fail(PSG_E_DOMAIN, "retained PCA dimension > 64 is not supported");
-  if (a.mode == PSG_EXACT && a.proj32_aos && a.tree.centroid32T) {
+  if (a.mode == PSG_EXACT && a.proj32_q4 && a.tree.centroid32T) {
     int64_t blocks = (a.nq + 7) / 8;
     const int64_t cap = (int64_t)ctx->num_sms * 8;
     if (blocks > cap) blocks = cap;
@@ -695,15 +723,15 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
   PSG_LAUNCHED(ctx);
 }
 
-// fp32 filter copies in leaf order: aos32[pos][dp] = (float) soa[j][pos], |p| rounded up.
+// fp32 filter copies in leaf order: q4[j/4][pos][j%4] = (float) soa[j][pos], |p| rounded up.
 __global__ void make_fp32_copies_kernel(const double* __restrict__ soa, int64_t N, int d, int dp,
-                                        float* __restrict__ aos32, float* __restrict__ pn) {
+                                        float* __restrict__ q4, float* __restrict__ pn) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
        i += (int64_t)gridDim.x * blockDim.x) {
     double n2 = 0.0;
     for (int j = 0; j < dp; ++j) {
       const double v = j < d ? soa[(int64_t)j * N + i] : 0.0;
-      aos32[i * dp + j] = (float)v;
+      q4[((int64_t)(j / 4) * N + i) * 4 + (j % 4)] = (float)v;
       n2 += v * v;
     }
     pn[i] = __double2float_ru(sqrt(n2) * (1.0 + 1e-12));

@@ -56,6 +56,7 @@ struct DevTree {
   float* cnorm32 = nullptr;     // |centroid|
   float* boxlo = nullptr;       // [kBoxDims][n_nodes] per-dim minimum over the subtree
   float* boxhi = nullptr;       // [kBoxDims][n_nodes]
+  int2* meta = nullptr;         // {first_child, -n_children} or {leaf_start, leaf_count}
 };
 constexpr int kBoxDims = 8;     // leading PCA dims carrying bounding boxes
 
@@ -81,7 +82,7 @@ struct Index {
   double* basis = nullptr;     // [d][D]
   double* proj = nullptr;      // [N][d] original order
   double* proj_soa = nullptr;  // [d][N] leaf order
-  float* proj32_aos = nullptr; // [N][dp] leaf order, fp32 filter copy (dp = 32 or 64)
+  float* proj32_q4 = nullptr;  // [dp/4][N] float4 groups, leaf order, fp32 filter copy
   int dp = 32;
   float* pnorm32 = nullptr;    // [N] leaf order, |p| rounded up
   int32_t* perm = nullptr;     // leaf order -> id
@@ -167,7 +168,7 @@ struct SearchArgs {
   const int32_t* seed_idx;  // optional initial candidate per query (upper bound)
   const double* proj;       // [N][d] original order (seed distances)
   const double* proj_soa;   // [d][N] leaf order
-  const float* proj32_aos;  // [N][dp] leaf order (fp32 filter)
+  const float* proj32_q4;   // [dp/4][N] float4 groups, leaf order (fp32 filter)
   const float* pnorm32;     // [N] leaf order
   const int32_t* perm;
   int64_t N;
@@ -182,6 +183,7 @@ struct SearchArgs {
   double* out_d2;
   int64_t* out_scanned;
   int64_t* out_exact;       // optional: points evaluated in exact fp64
+  int32_t* out_visited;     // optional: nodes visited (QueryStats, km_tree.hpp:27-30)
   int* flags;
 };
 void launch_search(psg_ctx* ctx, const SearchArgs& a);

@@ -215,10 +215,11 @@ Index::~Index() {
   cudaFree(tree.centroid32);
   cudaFree(tree.radius32);
   cudaFree(tree.cnorm32);
-  cudaFree(proj32_aos);
+  cudaFree(proj32_q4);
   cudaFree(tree.centroid32T);
   cudaFree(tree.boxlo);
   cudaFree(tree.boxhi);
+  cudaFree(tree.meta);
   cudaFree(pnorm32);
   cudaFree(ex_hist);
 }
@@ -305,9 +306,9 @@ void finish_index(psg_ctx* ctx, Index& ix, const double* mean, const double* bas
   launch_gather_soa(ctx, ix.proj, ix.N, d, ix.perm, ix.proj_soa);
   // fp32 bound/filter copies (conservative rounding, see search_exact_kernel)
   ix.dp = d <= 32 ? 32 : 64;
-  ix.proj32_aos = dalloc<float>((size_t)ix.N * ix.dp);
+  ix.proj32_q4 = dalloc<float>((size_t)ix.N * ix.dp);
   ix.pnorm32 = dalloc<float>(ix.N);
-  launch_make_fp32_copies(ctx, ix.proj_soa, ix.N, d, ix.dp, ix.proj32_aos, ix.pnorm32);
+  launch_make_fp32_copies(ctx, ix.proj_soa, ix.N, d, ix.dp, ix.proj32_q4, ix.pnorm32);
   {
     std::vector<float> c32(t.centroid.size()), c32t(t.centroid.size()), r32(nn), n32(nn);
     std::vector<float> blo((size_t)kBoxDims * nn, 0.f), bhi((size_t)kBoxDims * nn, 0.f);
@@ -327,6 +328,12 @@ void finish_index(psg_ctx* ctx, Index& ix, const double* mean, const double* bas
     up(ix.tree.centroid32T, c32t);
     up(ix.tree.boxlo, blo);
     up(ix.tree.boxhi, bhi);
+    std::vector<int2> meta(nn);
+    for (int i = 0; i < nn; ++i)
+      meta[i] = t.n_children[i] > 0 ? make_int2(t.first_child[i], -t.n_children[i])
+                                    : make_int2(t.leaf_start[i], t.leaf_count[i]);
+    ix.tree.meta = dalloc<int2>(nn);
+    up(ix.tree.meta, meta);
     for (int i = 0; i < nn; ++i) {
       r32[i] = std::nextafter((float)t.radius[i], INFINITY);
       double n2 = 0.0;
@@ -405,7 +412,8 @@ struct psg_level {
   psg::DBuf<float> mirror;
   psg::DBuf<double> qproj, d2, cur_dist, next_dist, irls, pen, eff, after;
   psg::DBuf<int32_t> cur_idx, next_idx;
-  psg::DBuf<int64_t> scanned;
+  psg::DBuf<int64_t> scanned, exact_evals;
+  psg::DBuf<int32_t> visited;
   psg::DBuf<unsigned long long> counts;
   psg::DBuf<double> out_mass, excess, ex_hist, stats_dev;
   double* stats_host = nullptr;  // pinned [6]
@@ -486,6 +494,8 @@ void level_setup(psg_level& L, psg_ctx* ctx, const Index& ix, int W, int H,
   L.next_dist.alloc(L.A);
   L.after.alloc(L.A);
   L.scanned.alloc(L.A);
+  L.exact_evals.alloc(L.A);
+  L.visited.alloc(L.A);
   L.stats_dev.alloc(8 + 6 * 296);
   PSG_CUDA(cudaMallocHost(&L.stats_host, sizeof(double) * 8));
   PSG_CUDA(cudaEventCreate(&L.ev0));
@@ -526,7 +536,7 @@ void level_search(psg_level& L, bool seeded, int32_t* out_idx, double* out_dist)
   a.seed_idx = (seeded && L.cfg.budget.mode == PSG_EXACT) ? L.cur_idx.p : nullptr;
   a.proj = ix.proj;
   a.proj_soa = ix.proj_soa;
-  a.proj32_aos = ix.proj32_aos;
+  a.proj32_q4 = ix.proj32_q4;
   a.pnorm32 = ix.pnorm32;
   a.perm = ix.perm;
   a.qxs = L.xs.p;
@@ -541,6 +551,8 @@ void level_search(psg_level& L, bool seeded, int32_t* out_idx, double* out_dist)
   a.out_idx = out_idx;
   a.out_d2 = L.d2.p;
   a.out_scanned = L.scanned.p;
+  a.out_exact = L.exact_evals.p;
+  a.out_visited = L.visited.p;
   a.flags = ctx->d_flags;
   launch_search(ctx, a);
   launch_rescore_windows(ctx, L.mirror.p, L.W, L.C, L.w, as, ix, out_idx, out_dist);
@@ -892,7 +904,7 @@ psg_status psg_index_query(psg_ctx* ctx, const psg_index* index, const float* Q,
     a.d = ix.d;
     a.proj = ix.proj;
     a.proj_soa = ix.proj_soa;
-    a.proj32_aos = ix.proj32_aos;
+    a.proj32_q4 = ix.proj32_q4;
     a.pnorm32 = ix.pnorm32;
     a.perm = ix.perm;
     a.N = ix.N;
@@ -1032,6 +1044,17 @@ psg_status psg_level_state_dev(psg_level* level, void** planes_dev, void** idx_d
     if (planes_dev) *planes_dev = level->planes.p;
     if (idx_dev) *idx_dev = level->cur_idx.p;
     if (dist_dev) *dist_dev = level->cur_dist.p;
+  });
+}
+
+psg_status psg_level_query_stats(psg_level* level, int64_t* scanned, int64_t* exact_evals,
+                                 int32_t* nodes_visited) {
+  return guarded([&] {
+    psg_ctx* ctx = level->ctx;
+    if (scanned) level->scanned.download(ctx, scanned, level->A);
+    if (exact_evals) level->exact_evals.download(ctx, exact_evals, level->A);
+    if (nodes_visited) level->visited.download(ctx, nodes_visited, level->A);
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
 

@@ -110,6 +110,7 @@ _SIGS = {
     "psg_level_iterate": (I, [VP, I, I, VP, VP]),
     "psg_level_download": (I, [VP, VP, VP, VP]),
     "psg_level_state_dev": (I, [VP, PP, PP, PP]),
+    "psg_level_query_stats": (I, [VP, VP, VP, VP]),
     "psg_level_destroy": (None, [VP]),
     "psg_synthesize": (I, [VP, ct.POINTER(psg_request), VP, ct.POINTER(psg_report)]),
     "psg_axis_positions": (I, [I, I, I, VP]),
