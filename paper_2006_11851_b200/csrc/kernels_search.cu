@@ -212,6 +212,18 @@ __device__ __forceinline__ double dist2_seq(const double* __restrict__ q,
   return acc;
 }
 
+// Out-of-line copy for rarely executed call sites (seeds, filter survivors):
+// keeps the hot loops of the tile kernel small enough for the I-cache.
+__device__ __noinline__ double dist2_seq_cold(const double* __restrict__ q,
+                                             const double* __restrict__ p, int d) {
+  double acc = 0.0;
+  for (int j = 0; j < d; ++j) {
+    const double t = dsub(q[j], p[j]);
+    acc = dadd(acc, dmul(t, t));
+  }
+  return acc;
+}
+
 // Scan one leaf: lanes over points, exact dist^2 per lane, warp lexmin.
 __device__ __forceinline__ void scan_leaf(const SearchArgs& a, const double* __restrict__ qs,
                                           int node, int lane, double& best, int32_t& best_id,
@@ -701,10 +713,322 @@ __global__ void __launch_bounds__(256) search_exact_kernel(SearchArgs a) {
   }
 }
 
+// ----------------------------------------------------------------------------
+// Tile search (exact mode, default): one warp owns 32 consecutive queries,
+// one query per lane, and the 32 queries share ONE depth-first traversal.
+// A node is expanded / a leaf scanned when at least one lane's conservative
+// bound is <= that lane's own best; every lane then evaluates its own query
+// against the node's children or the leaf's points, which are staged once in
+// shared memory and read as broadcasts.  This turns the irregular per-query
+// traversal into dense, divergence-free fp32 work (lanes = queries, like a
+// GEMM tile of queries x points), while each lane keeps its own exact
+// lexicographic (fp64 dist^2, id) minimum.  Spatially consecutive anchors have
+// overlapping windows and hence overlapping candidate sets, so the shared
+// traversal visits little more than each query alone.
+constexpr int kTileStack = 48;
+constexpr int kTileMaxB = 16;
+
+template <int DP, int kTileWarps>
+__global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs a) {
+  constexpr int RS = DP + 4;  // padded staging row (floats): conflict-free 16 B accesses
+  __shared__ int2 st_meta[kTileWarps][kTileStack];
+  __shared__ float st_lb[kTileWarps][kTileStack][32];
+  __shared__ __align__(16) float stage_all[kTileWarps][32 * RS];
+  __shared__ float aux_all[kTileWarps][2][32];
+  __shared__ int2 cmeta_all[kTileWarps][kTileMaxB];
+  __shared__ float box_all[kTileWarps][kTileMaxB][2 * kBoxDims];
+  __shared__ int32_t pid_all[kTileWarps][32];
+  __shared__ float tlb_all[kTileWarps][kTileMaxB][32];
+  __shared__ unsigned tkey_all[kTileWarps][kTileMaxB];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int2* sm_ = st_meta[warp];
+  float(*slb)[32] = st_lb[warp];
+  float* stage = stage_all[warp];
+  float* aux0 = aux_all[warp][0];
+  float* aux1 = aux_all[warp][1];
+  int2* cmeta = cmeta_all[warp];
+  float(*boxs)[2 * kBoxDims] = box_all[warp];
+  int32_t* pid = pid_all[warp];
+  float(*tlb)[32] = tlb_all[warp];
+  unsigned* tkey = tkey_all[warp];
+  const int d = a.d;
+  const int N = (int)a.N;
+  const int nn = a.tree.n_nodes;
+  const int KB = d < kBoxDims ? d : kBoxDims;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  const float kInfF = __int_as_float(0x7f800000);
+  // image queries: 8 x 4 anchor tiles (overlapping windows share candidates);
+  // vector queries: 32 consecutive rows
+  const int qny = a.qxs ? (int)(a.nq / a.qnx) : 0;
+  const int tnx = a.qxs ? (a.qnx + 7) / 8 : 0;
+  const int64_t n_tiles = a.qxs ? (int64_t)tnx * ((qny + 3) / 4) : (a.nq + 31) / 32;
+
+  for (int64_t t = (int64_t)blockIdx.x * kTileWarps + warp; t < n_tiles;
+       t += (int64_t)gridDim.x * kTileWarps) {
+    int64_t q;
+    bool valid;
+    if (a.qxs) {
+      const int tx = (int)(t % tnx), ty = (int)(t / tnx);
+      const int ix = tx * 8 + (lane & 7), iy = ty * 4 + (lane >> 3);
+      valid = ix < a.qnx && iy < qny;
+      q = valid ? (int64_t)iy * a.qnx + ix : 0;
+    } else {
+      q = t * 32 + lane;
+      valid = q < a.nq;
+    }
+    const double* qrow = a.q + (valid ? q : 0) * d;
+    float q32[DP];
+    double qn2 = 0.0;
+#pragma unroll
+    for (int j = 0; j < DP; ++j) {
+      const double v = (valid && j < d) ? qrow[j] : 0.0;
+      q32[j] = (float)v;
+      qn2 += v * v;
+    }
+    const float qn = __double2float_ru(sqrt(qn2) * (1.0 + 1e-12));
+    // invalid lanes hold best = -1: every bound (>= 0) prunes them
+    double best = valid ? kInf : -1.0;
+    int32_t best_id = 0x7fffffff;
+    int64_t scanned = 0, exact_evals = 0;
+    int32_t visited = 0;
+
+    // ---- coherence seeds (exact fp64), per lane ------------------------------------
+    if (a.seed_idx && valid) {
+      const int qix = a.qxs ? (int)(q % a.qnx) : 0, qiy = a.qxs ? (int)(q / a.qnx) : 0;
+#pragma unroll 1
+      for (int k = 0; k < 5; ++k) {
+        int32_t cand = -1;
+        if (k == 0) {
+          cand = a.seed_idx[q];
+        } else if (a.qxs) {
+          const int nix = qix + (k == 1 ? -1 : k == 2 ? 1 : 0);
+          const int niy = qiy + (k == 3 ? -1 : k == 4 ? 1 : 0);
+          if (nix >= 0 && nix < a.qnx && niy >= 0 && niy < qny) {
+            const int32_t e = a.seed_idx[(int64_t)niy * a.qnx + nix];
+            const int ex = e % a.nxe + (a.qxs[qix] - a.qxs[nix]);
+            const int ey = e / a.nxe + (a.qys[qiy] - a.qys[niy]);
+            if (ex >= 0 && ex < a.nxe && ey >= 0 && ey < a.nye) cand = ey * a.nxe + ex;
+          }
+        }
+        if (cand < 0) continue;
+        const double d2 = dist2_seq_cold(qrow, a.proj + (int64_t)cand * d, d);
+        ++scanned;
+        ++exact_evals;
+        if (lex_less(d2, cand, best, best_id)) {
+          best = d2;
+          best_id = cand;
+        }
+      }
+    }
+
+    if (lane == 0) sm_[0] = a.tree.meta[0];
+    slb[0][lane] = 0.f;
+    int top = 1;
+    __syncwarp();
+    while (top > 0) {
+      // ---- pop: drop entries no lane still wants; batch consecutive leaves ------
+      int bstart[4], bcnt[4];
+      int nb = 0, tot = 0;
+      int2 node = make_int2(0, 0);
+      while (top > 0) {
+        const int2 md = sm_[top - 1];
+        const bool want = (double)slb[top - 1][lane] <= best;
+        if (!__any_sync(0xffffffffu, want)) {  // km_tree.cpp:265 prune, per lane
+          --top;
+          continue;
+        }
+        if (md.y < 0) {
+          if (nb == 0) {
+            node = md;
+            --top;
+          }
+          break;
+        }
+        if (nb > 0 && (tot + md.y > 32 || nb == 4)) break;
+        --top;
+        bstart[nb] = md.x;
+        bcnt[nb] = md.y;
+        ++nb;
+        tot += md.y;
+        if (tot >= 32) break;
+      }
+      if (nb > 0) {
+        visited += nb;
+        scanned += tot;
+        for (int c0 = 0; c0 < tot; c0 += 32) {
+          const int cn = min(32, tot - c0);
+          // stage <= 32 points: lane i loads point c0 + i (coalesced float4 groups)
+          __syncwarp();
+          if (lane < cn) {
+            int i = c0 + lane, b = 0;
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+              if (b < nb - 1 && i >= bcnt[b]) i -= bcnt[b++];
+            const int pos = bstart[b] + i;
+            const float4* col = reinterpret_cast<const float4*>(a.proj32_q4) + pos;
+            float4* dst = reinterpret_cast<float4*>(stage + lane * RS);
+#pragma unroll
+            for (int k = 0; k < DP / 4; ++k)
+              dst[k] = (4 * k < d) ? __ldg(col + (int64_t)k * N) : make_float4(0.f, 0.f, 0.f, 0.f);
+            aux0[lane] = a.pnorm32[pos];
+            pid[lane] = a.perm[pos];
+          }
+          __syncwarp();
+          // best rounded up to float: a float compare can only keep more points
+          float best_up = __double2float_ru(best);
+          for (int i = 0; i < cn; ++i) {
+            const float4* pr = reinterpret_cast<const float4*>(stage + i * RS);
+            // 4 independent partial sums (any order: the filter bound covers it)
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+            for (int k = 0; k < DP / 4; ++k) {
+              const float4 p = pr[k];
+              const float u0 = q32[4 * k] - p.x, u1 = q32[4 * k + 1] - p.y;
+              const float u2 = q32[4 * k + 2] - p.z, u3 = q32[4 * k + 3] - p.w;
+              s0 = fmaf(u0, u0, s0);
+              s1 = fmaf(u1, u1, s1);
+              s2 = fmaf(u2, u2, s2);
+              s3 = fmaf(u3, u3, s3);
+            }
+            const float s = (s0 + s1) + (s2 + s3);
+            const float eps =
+                2.5e-7f * (float)(d + 4) * s + 1.0e-6f * (qn + aux0[i]) * (sqrtf(s) + 1e-3f) + 1e-30f;
+            const bool surv = s - eps <= best_up;
+            if (__any_sync(0xffffffffu, surv)) {
+              if (surv) {
+                const int32_t id = pid[i];
+                const double d2 = dist2_seq_cold(qrow, a.proj + (int64_t)id * d, d);
+                ++exact_evals;
+                if (lex_less(d2, id, best, best_id)) {
+                  best = d2;
+                  best_id = id;
+                  best_up = __double2float_ru(best);
+                }
+              }
+            }
+          }
+        }
+        continue;
+      }
+      if (node.y >= 0) break;
+      // ---- expand an internal node: stage children, every lane bounds them -----------
+      ++visited;
+      const int nc = -node.y;
+      const int fc = node.x;
+      __syncwarp();
+      for (int f = lane; f < nc * DP; f += 32) {
+        const int c = f / DP, j = f - c * DP;
+        stage[c * RS + j] = j < d ? __ldg(a.tree.centroid32 + (int64_t)(fc + c) * d + j) : 0.f;
+      }
+      if (lane < nc) {
+        aux0[lane] = a.tree.radius32[fc + lane];
+        aux1[lane] = a.tree.cnorm32[fc + lane];
+        cmeta[lane] = a.tree.meta[fc + lane];
+      }
+      for (int f = lane; f < nc * KB; f += 32) {
+        const int c = f % nc, j = f / nc;
+        boxs[c][2 * j] = __ldg(a.tree.boxlo + (int64_t)j * nn + fc + c);
+        boxs[c][2 * j + 1] = __ldg(a.tree.boxhi + (int64_t)j * nn + fc + c);
+      }
+      __syncwarp();
+      // per-child bounds: rolled loop (keeps the kernel inside the I-cache);
+      // per-lane bounds go to shared scratch, warp-min keys to a uniform array
+#pragma unroll 1
+      for (int c = 0; c < nc; ++c) {
+        const float4* cr = reinterpret_cast<const float4*>(stage + c * RS);
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+        for (int k = 0; k < DP / 4; ++k) {
+          const float4 p = cr[k];
+          const float u0 = q32[4 * k] - p.x, u1 = q32[4 * k + 1] - p.y;
+          const float u2 = q32[4 * k + 2] - p.z, u3 = q32[4 * k + 3] - p.w;
+          s0 = fmaf(u0, u0, s0);
+          s1 = fmaf(u1, u1, s1);
+          s2 = fmaf(u2, u2, s2);
+          s3 = fmaf(u3, u3, s3);
+        }
+        const float s = (s0 + s1) + (s2 + s3);
+        float bx = 0.f;
+#pragma unroll
+        for (int j = 0; j < kBoxDims; ++j) {
+          if (j < KB) {
+            const float lo = boxs[c][2 * j], hi = boxs[c][2 * j + 1];
+            const float qj = q32[j];
+            float gap = fmaxf(lo - qj, qj - hi) - 2.4e-7f * (fabsf(qj) + fabsf(lo) + fabsf(hi));
+            gap = fmaxf(gap, 0.f);
+            bx = fmaf(gap, gap, bx);
+          }
+        }
+        const float dc = sqrtf(s);
+        const float rad = aux0[c];
+        const float slack = 2e-5f * (1.f + dc + rad + qn + aux1[c]);
+        const float lb = dc - rad - slack;
+        float lb2 = lb > 0.f ? lb * lb * (1.f - 1e-6f) : 0.f;
+        lb2 = fmaxf(lb2, bx * (1.f - 1e-5f));
+        tlb[c][lane] = lb2;
+        const bool want = (double)lb2 <= best;
+        // non-negative floats order like their bit patterns
+        const unsigned key = __reduce_min_sync(0xffffffffu, want ? __float_as_uint(lb2) : 0xffffffffu);
+        if (lane == 0) tkey[c] = key;
+      }
+      __syncwarp();
+      const unsigned mykey = lane < nc ? tkey[lane] : 0xffffffffu;
+      const bool kept = mykey != 0xffffffffu;
+      const unsigned keepmask = __ballot_sync(0xffffffffu, kept);
+      const int nkeep = __popc(keepmask);
+      if (top + nkeep > kTileStack) {
+        if (lane == 0) atomicOr(a.flags, FLAG_STACK_OVERFLOW);
+        break;
+      }
+      // lane c ranks child c among the kept ones (nearest popped first)
+      int myslot = -1;
+      if (kept) {
+        int rank = 0;
+        for (int o = 0; o < nc; ++o) {
+          const unsigned ko = tkey[o];
+          if (ko != 0xffffffffu && (ko < mykey || (ko == mykey && o < lane))) ++rank;
+        }
+        myslot = top + nkeep - 1 - rank;
+        sm_[myslot] = cmeta[lane];
+      }
+#pragma unroll 1
+      for (int c = 0; c < nc; ++c) {
+        const int slot = __shfl_sync(0xffffffffu, myslot, c);
+        if (slot >= 0) slb[slot][lane] = tlb[c][lane];
+      }
+      top += nkeep;
+      __syncwarp();
+    }
+    if (valid) {
+      a.out_idx[q] = best_id;
+      a.out_d2[q] = best;
+      if (a.out_scanned) a.out_scanned[q] = scanned;
+      if (a.out_exact) a.out_exact[q] = exact_evals;
+      if (a.out_visited) a.out_visited[q] = visited;
+    }
+    __syncwarp();
+  }
+}
+
 void launch_search(psg_ctx* ctx, const SearchArgs& a) {
   ProfScope _prof(ctx, K_SEARCH);
   if (a.nq <= 0) return;
   if (a.d > kMaxD) fail(PSG_E_DOMAIN, "retained PCA dimension > 64 is not supported");
+  const bool tile_ok = a.tree.max_children <= kTileMaxB &&
+                       1 + a.tree.max_depth * (a.tree.max_children - 1) <= kTileStack;
+  if (a.mode == PSG_EXACT && a.proj32_q4 && a.tree.centroid32 && tile_ok && !ctx->legacy_search) {
+    const int64_t tiles = (a.nq + 31) / 32;
+    const int wpb = a.d <= 32 ? 3 : 2;  // static smem <= 48 KB per CTA
+    int64_t blocks = (tiles + wpb - 1) / wpb;
+    const int64_t cap = (int64_t)ctx->num_sms * 24;
+    if (blocks > cap) blocks = cap;
+    if (a.d <= 32)
+      search_tile_kernel<32, 3><<<(int)blocks, 32 * 3, 0, ctx->stream>>>(a);
+    else
+      search_tile_kernel<64, 2><<<(int)blocks, 32 * 2, 0, ctx->stream>>>(a);
+    PSG_LAUNCHED(ctx);
+    return;
+  }
   if (a.mode == PSG_EXACT && a.proj32_q4 && a.tree.centroid32T) {
     int64_t blocks = (a.nq + 7) / 8;
     const int64_t cap = (int64_t)ctx->num_sms * 8;

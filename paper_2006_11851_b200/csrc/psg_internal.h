@@ -43,6 +43,7 @@ enum DevFlag : int {
 struct DevTree {
   int n_nodes = 0;
   int max_depth = 0;
+  int max_children = 0;
   double* centroid = nullptr;  // [n_nodes][d]
   double* radius = nullptr;    // [n_nodes]
   int32_t* first_child = nullptr;
@@ -126,6 +127,7 @@ struct psg_ctx {
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
   int* d_flags = nullptr;
+  bool legacy_search = false;  // PERSYN_SEARCH=warp: per-query warp kernel instead of tiles
 };
 
 struct psg_index {

@@ -15,6 +15,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -283,6 +284,7 @@ void finish_index(psg_ctx* ctx, Index& ix, const double* mean, const double* bas
   const int nn = (int)t.radius.size();
   ix.tree.n_nodes = nn;
   ix.tree.max_depth = t.max_depth;
+  ix.tree.max_children = t.n_children.empty() ? 0 : *std::max_element(t.n_children.begin(), t.n_children.end());
   ix.tree.centroid = dalloc<double>((size_t)nn * (d > 0 ? d : 1));
   ix.tree.radius = dalloc<double>(nn);
   ix.tree.first_child = dalloc<int32_t>(nn);
@@ -731,6 +733,7 @@ psg_status psg_ctx_create(int device, void* stream, psg_ctx** out) {
     auto c = std::make_unique<psg_ctx>();
     c->device = device;
     c->num_sms = prop.multiProcessorCount;
+    if (const char* e = std::getenv("PERSYN_SEARCH")) c->legacy_search = std::string(e) == "warp";
     if (stream) {
       c->stream = static_cast<cudaStream_t>(stream);
     } else {
