@@ -194,14 +194,18 @@ def roofline_for(kernels: dict, step_ms: float, A: int, P: int, C: int, d: int, 
             per[name] = {"ms_per_launch": ms / n, "launches": n, "share": ms / max(step_ms, 1e-9)}
     ms, n = kernels[dom]
     t = ms / n / 1e3
-    fp64_peak = 148 * 64 * 2 * 1.965e9 / 1e12   # derived, TFLOP/s (FMA = 2)
+    fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12   # derived, TFLOP/s (FMA = 2)
     if dom == "search_kernel":
-        flops = 3.0 * d * scanned_per_step  # sub, mul, add per dim per scanned point
+        # exact search = fp32 filter over (query, candidate) pairs + rare exact
+        # fp64 rechecks: algorithmic flops = 3*d per pair (sub, mul, add)
+        flops = 3.0 * d * scanned_per_step
         ach = flops / t / 1e12
-        roof = {"bound": "fp64", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
-                "frac": ach / fp64_peak, "traffic": None,
-                "note": "fp64 SIMT bound; peak derived 148 SM x 64 lanes x 2 x 1.965 GHz "
-                        "(not measured); algorithmic flops = 3*d*points_scanned"}
+        roof = {"bound": "fp32", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s",
+                "frac": ach / fp32_peak, "traffic": None,
+                "note": "irregular tree search: SIMT fp32 filter + fp64 exact recheck; neither "
+                        "HBM (working set L2-resident) nor tensor cores bind. Peak derived "
+                        "148 SM x 128 FP32 lanes x 2 x 1.965 GHz (not measured); flops = "
+                        "3*d*(query, point) pairs evaluated"}
     elif dom == "mstep_kernel":
         bytes_ = P * C * 12 + A * 12
         ach = bytes_ / t / 1e9

@@ -785,6 +785,9 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
       q32[j] = (float)v;
       qn2 += v * v;
     }
+    float2 q2[DP / 2];
+#pragma unroll
+    for (int j = 0; j < DP / 2; ++j) q2[j] = make_float2(q32[2 * j], q32[2 * j + 1]);
     const float qn = __double2float_ru(sqrt(qn2) * (1.0 + 1e-12));
     // invalid lanes hold best = -1: every bound (>= 0) prunes them
     double best = valid ? kInf : -1.0;
@@ -868,8 +871,10 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
             const float4* col = reinterpret_cast<const float4*>(a.proj32_q4) + pos;
             float4* dst = reinterpret_cast<float4*>(stage + lane * RS);
 #pragma unroll
-            for (int k = 0; k < DP / 4; ++k)
-              dst[k] = (4 * k < d) ? __ldg(col + (int64_t)k * N) : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int k = 0; k < DP / 4; ++k) {  // staged negated: u = q + (-p) with FADD2
+              const float4 v = (4 * k < d) ? __ldg(col + (int64_t)k * N) : make_float4(0.f, 0.f, 0.f, 0.f);
+              dst[k] = make_float4(-v.x, -v.y, -v.z, -v.w);
+            }
             aux0[lane] = a.pnorm32[pos];
             pid[lane] = a.perm[pos];
           }
@@ -878,19 +883,18 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
           float best_up = __double2float_ru(best);
           for (int i = 0; i < cn; ++i) {
             const float4* pr = reinterpret_cast<const float4*>(stage + i * RS);
-            // 4 independent partial sums (any order: the filter bound covers it)
-            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+            // packed fp32x2 (FADD2/FFMA2); partial sums in any order: the filter
+            // bound covers it
+            float2 sa = make_float2(0.f, 0.f), sb = make_float2(0.f, 0.f);
 #pragma unroll
             for (int k = 0; k < DP / 4; ++k) {
               const float4 p = pr[k];
-              const float u0 = q32[4 * k] - p.x, u1 = q32[4 * k + 1] - p.y;
-              const float u2 = q32[4 * k + 2] - p.z, u3 = q32[4 * k + 3] - p.w;
-              s0 = fmaf(u0, u0, s0);
-              s1 = fmaf(u1, u1, s1);
-              s2 = fmaf(u2, u2, s2);
-              s3 = fmaf(u3, u3, s3);
+              const float2 u0 = __fadd2_rn(q2[2 * k], make_float2(p.x, p.y));
+              const float2 u1 = __fadd2_rn(q2[2 * k + 1], make_float2(p.z, p.w));
+              sa = __ffma2_rn(u0, u0, sa);
+              sb = __ffma2_rn(u1, u1, sb);
             }
-            const float s = (s0 + s1) + (s2 + s3);
+            const float s = (sa.x + sa.y) + (sb.x + sb.y);
             const float eps =
                 2.5e-7f * (float)(d + 4) * s + 1.0e-6f * (qn + aux0[i]) * (sqrtf(s) + 1e-3f) + 1e-30f;
             const bool surv = s - eps <= best_up;
@@ -918,7 +922,7 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
       __syncwarp();
       for (int f = lane; f < nc * DP; f += 32) {
         const int c = f / DP, j = f - c * DP;
-        stage[c * RS + j] = j < d ? __ldg(a.tree.centroid32 + (int64_t)(fc + c) * d + j) : 0.f;
+        stage[c * RS + j] = j < d ? -__ldg(a.tree.centroid32 + (int64_t)(fc + c) * d + j) : 0.f;
       }
       if (lane < nc) {
         aux0[lane] = a.tree.radius32[fc + lane];
@@ -936,18 +940,16 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
 #pragma unroll 1
       for (int c = 0; c < nc; ++c) {
         const float4* cr = reinterpret_cast<const float4*>(stage + c * RS);
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        float2 sa = make_float2(0.f, 0.f), sb = make_float2(0.f, 0.f);
 #pragma unroll
         for (int k = 0; k < DP / 4; ++k) {
           const float4 p = cr[k];
-          const float u0 = q32[4 * k] - p.x, u1 = q32[4 * k + 1] - p.y;
-          const float u2 = q32[4 * k + 2] - p.z, u3 = q32[4 * k + 3] - p.w;
-          s0 = fmaf(u0, u0, s0);
-          s1 = fmaf(u1, u1, s1);
-          s2 = fmaf(u2, u2, s2);
-          s3 = fmaf(u3, u3, s3);
+          const float2 u0 = __fadd2_rn(q2[2 * k], make_float2(p.x, p.y));
+          const float2 u1 = __fadd2_rn(q2[2 * k + 1], make_float2(p.z, p.w));
+          sa = __ffma2_rn(u0, u0, sa);
+          sb = __ffma2_rn(u1, u1, sb);
         }
-        const float s = (s0 + s1) + (s2 + s3);
+        const float s = (sa.x + sa.y) + (sb.x + sb.y);
         float bx = 0.f;
 #pragma unroll
         for (int j = 0; j < kBoxDims; ++j) {
