@@ -28,28 +28,40 @@ namespace psg {
 
 namespace {
 thread_local std::string g_last_error;
+// Stream of the API call in flight: per-call buffers come from the device's
+// stream-ordered memory pool (cudaMallocAsync), which keeps freed blocks, so
+// repeated optimize_level / search_step calls do not pay cudaMalloc.
+thread_local cudaStream_t t_stream = nullptr;
+struct StreamScope {
+  cudaStream_t prev;
+  explicit StreamScope(cudaStream_t s) : prev(t_stream) { t_stream = s; }
+  ~StreamScope() { t_stream = prev; }
+};
 
 template <class T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
+  cudaStream_t s = nullptr;
   DBuf() = default;
   explicit DBuf(size_t count) { alloc(count); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr, o.n = 0; }
   DBuf& operator=(DBuf&& o) noexcept {
     std::swap(p, o.p);
     std::swap(n, o.n);
+    std::swap(s, o.s);
     return *this;
   }
   void alloc(size_t count) {
     release();
     n = count;
-    if (count) PSG_CUDA(cudaMalloc(&p, sizeof(T) * count));
+    s = t_stream;
+    if (count) PSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, s));
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, s);
     p = nullptr;
     n = 0;
   }
@@ -740,6 +752,12 @@ psg_status psg_ctx_create(int device, void* stream, psg_ctx** out) {
       PSG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
       c->own_stream = true;
     }
+    {
+      cudaMemPool_t pool;
+      PSG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+      uint64_t keep = UINT64_MAX;
+      PSG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     PSG_CUDA(cudaMalloc(&c->d_flags, sizeof(int)));
     PSG_CUDA(cudaMemsetAsync(c->d_flags, 0, sizeof(int), c->stream));
     *out = c.release();
@@ -770,6 +788,7 @@ int64_t psg_ctx_launch_count(const psg_ctx* ctx) { return ctx ? ctx->launches : 
 
 psg_status psg_ctx_profile(psg_ctx* ctx, int enable) {
   return guarded([&] {
+    psg::StreamScope _ss(ctx ? ctx->stream : nullptr);
     if (!ctx) fail(PSG_E_DOMAIN, "null context");
     psg::prof_flush(ctx);
     ctx->profile = enable != 0;
@@ -798,6 +817,7 @@ psg_status psg_index_create(psg_ctx* ctx, const double* ex_planes, int C, int ew
                             const double* mean, const double* basis, int d,
                             const psg_index_cfg* cfg, psg_index** out) {
   return guarded([&] {
+    psg::StreamScope _ss(ctx ? ctx->stream : nullptr);
     if (!ctx || !ex_planes || !cfg || !out) fail(PSG_E_DOMAIN, "null argument");
     *out = nullptr;
     if (ew < 1 || eh < 1) fail(PSG_E_DOMAIN, "empty exemplar");
@@ -812,6 +832,7 @@ psg_status psg_index_create_vectors(psg_ctx* ctx, const float* X, int64_t n, int
                                     const double* mean, const double* basis, int d,
                                     const psg_index_cfg* cfg, psg_index** out) {
   return guarded([&] {
+    psg::StreamScope _ss(ctx ? ctx->stream : nullptr);
     if (!ctx || !X || !cfg || !out) fail(PSG_E_DOMAIN, "null argument");
     *out = nullptr;
     if (n < 1) fail(PSG_E_DOMAIN, "empty candidate set");
@@ -891,6 +912,7 @@ psg_status psg_index_query(psg_ctx* ctx, const psg_index* index, const float* Q,
                            psg_budget budget, int32_t* idx, double* dist, double* dist_pca,
                            int64_t* scanned) {
   return guarded([&] {
+    psg::StreamScope _ss(ctx ? ctx->stream : nullptr);
     if (!ctx || !index || !Q || !idx || !dist) fail(PSG_E_DOMAIN, "null argument");
     psg::validate_budget(budget);
     const psg::Index& ix = index->impl;
@@ -944,6 +966,7 @@ psg_status psg_search_step(psg_ctx* ctx, const psg_index* index, const double* o
                            int H, int spacing, int patch_width, psg_budget budget, int32_t* idx,
                            double* dist, int64_t* nn_calls, int64_t* scanned) {
   return guarded([&] {
+    psg::StreamScope _ss(ctx ? ctx->stream : nullptr);
     if (!ctx || !index || !out_planes || !idx || !dist) fail(PSG_E_DOMAIN, "null argument");
     const psg::Index& ix = index->impl;
     if (ix.from_vectors) fail(PSG_E_SHAPE, "candidate dim does not match the grid window");
@@ -972,6 +995,7 @@ psg_status psg_update_step(psg_ctx* ctx, const psg_index* index, const int32_t* 
                            const double* irls, const double* pen, int W, int H, int spacing,
                            double* out_planes) {
   return guarded([&] {
+    psg::StreamScope _ss(ctx ? ctx->stream : nullptr);
     if (!ctx || !index || !idx || !irls || !pen || !out_planes) fail(PSG_E_DOMAIN, "null argument");
     const psg::Index& ix = index->impl;
     if (ix.from_vectors) fail(PSG_E_SHAPE, "update_step needs an exemplar-window index");
@@ -1000,6 +1024,7 @@ psg_status psg_level_create(psg_ctx* ctx, const psg_index* index, const double* 
                             int H, const psg_opt_cfg* cfg, const double* ex_hist,
                             psg_level** out) {
   return guarded([&] {
+    psg::StreamScope _ss(ctx ? ctx->stream : nullptr);
     if (!ctx || !index || !init || !cfg || !out) fail(PSG_E_DOMAIN, "null argument");
     *out = nullptr;
     const psg::Index& ix = index->impl;
@@ -1020,6 +1045,7 @@ psg_status psg_level_prime(psg_level* level) {
 psg_status psg_level_iterate(psg_level* level, int n, int honor_convergence,
                              psg_iter_stats* stats, int* n_done) {
   return guarded([&] {
+    psg::StreamScope _ss(level->ctx->stream);
     psg::level_prime(*level);
     int done = 0;
     for (int i = 0; i < n; ++i) {
@@ -1033,6 +1059,7 @@ psg_status psg_level_iterate(psg_level* level, int n, int honor_convergence,
 
 psg_status psg_level_download(psg_level* level, double* planes, int32_t* idx, double* dist) {
   return guarded([&] {
+    psg::StreamScope _ss(level->ctx->stream);
     psg_ctx* ctx = level->ctx;
     if (planes) level->planes.download(ctx, planes, (size_t)level->P * level->C);
     if (idx) level->cur_idx.download(ctx, idx, level->A);
@@ -1044,6 +1071,7 @@ psg_status psg_level_download(psg_level* level, double* planes, int32_t* idx, do
 psg_status psg_level_state_dev(psg_level* level, void** planes_dev, void** idx_dev,
                                void** dist_dev) {
   return guarded([&] {
+    psg::StreamScope _ss(level->ctx->stream);
     if (planes_dev) *planes_dev = level->planes.p;
     if (idx_dev) *idx_dev = level->cur_idx.p;
     if (dist_dev) *dist_dev = level->cur_dist.p;
@@ -1053,6 +1081,7 @@ psg_status psg_level_state_dev(psg_level* level, void** planes_dev, void** idx_d
 psg_status psg_level_query_stats(psg_level* level, int64_t* scanned, int64_t* exact_evals,
                                  int32_t* nodes_visited) {
   return guarded([&] {
+    psg::StreamScope _ss(level->ctx->stream);
     psg_ctx* ctx = level->ctx;
     if (scanned) level->scanned.download(ctx, scanned, level->A);
     if (exact_evals) level->exact_evals.download(ctx, exact_evals, level->A);
@@ -1134,6 +1163,7 @@ void ramp_planes(int G, int W, int H, double* out) {
 extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, double* out_planes,
                                      psg_report* report) {
   return guarded([&] {
+    psg::StreamScope _ss(ctx ? ctx->stream : nullptr);
     using namespace psg;
     if (!ctx || !req || !out_planes) fail(PSG_E_DOMAIN, "null argument");
     const int C = req->C, G = C - 3;
