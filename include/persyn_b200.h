@@ -208,6 +208,44 @@ psg_status psg_level_query_stats(psg_level* level, int64_t* scanned, int64_t* ex
                                  int32_t* nodes_visited);
 void psg_level_destroy(psg_level* level);
 
+/* ---- row-sharded multi-GPU ---------------------------------- */
+/* Rank `rank` of `world` owns anchor rows [a0, a1) and pixel rows [p0, p1) of
+ * the W x H output; its windows read rows [p0, e1) (halo rows [p1, e1) come
+ * from rank+1) and its pixels are also covered by anchor rows [hlo, a0) of
+ * rank-1, accumulated in ascending anchor id: bit-identical to one device. */
+typedef struct {
+  int W, H, w, spacing, rank, world;
+  int p0, p1, e1;
+  int hlo, a0, a1;
+  int nx, ny; /* anchors per row, anchor rows of the whole image */
+} psg_band;
+psg_status psg_shard_plan(int W, int H, int w, int spacing, int rank, int world, psg_band* out);
+/* rows: host [C][e1-p0][W], the band's local rows of the initial image. */
+psg_status psg_band_create(psg_ctx* ctx, const psg_index* index, const double* rows,
+                           const psg_band* band, const psg_opt_cfg* cfg, const double* ex_hist,
+                           psg_level** out);
+/* One EM iteration = phase1..4 + commit; exchanges happen in between:
+ *  phase1: IRLS weights; owned-row histogram counts -> counts_dev (u64 [slots*bins], device)
+ *  [all-reduce(sum) of the counts]
+ *  phase2: fold global counts, penalties, weights; pack {eff[n] (f64), idx[n] (i32)} of owned
+ *          anchor rows [send_row0, a1) into send_dev (device) for rank+1
+ *  [send to rank+1 / receive rank-1's rows [hlo, a0) in the same format]
+ *  phase3: M-step of owned pixel rows; copy owned mirror rows [p0, p0+n_send_rows) (f32
+ *          [rows][W][C]) into send_rows_dev for rank-1
+ *  [send to rank-1 / receive rows [p1, e1) from rank+1]
+ *  phase4: halo rows in; lsq diagnostic, E-step; partials[9] = {lsq_before, lsq_after, energy,
+ *          changed, points_scanned, unique points scanned, nn_calls, priming nn_calls,
+ *          unique queries} of this rank
+ *  [sum the partials over ranks in rank order]
+ *  commit: record global stats (sums over ranks) and advance. */
+psg_status psg_band_phase1(psg_level* level, unsigned long long* counts_dev);
+psg_status psg_band_phase2(psg_level* level, const unsigned long long* global_counts_dev,
+                           int send_row0, void* send_dev);
+psg_status psg_band_phase3(psg_level* level, const void* recv_dev, int n_send_rows,
+                           float* send_rows_dev);
+psg_status psg_band_phase4(psg_level* level, const float* recv_rows_dev, double* partials);
+psg_status psg_band_commit(psg_level* level, const double* global_partials, psg_iter_stats* st);
+
 /* ---- pyramid driver (synthesize, pipeline.hpp:69, pipeline.cpp:216-315) --- */
 typedef struct {
   int n_sizes;

@@ -68,15 +68,15 @@ void launch_eff_from(psg_ctx* ctx, const double* irls, const double* pen, int64_
 
 // ---- histograms -------------------------------------------------------------------
 // Integer bin counts (exact, order-free), then the exact sequential-sum fold.
-__global__ void hist_count_kernel(const double* __restrict__ planes, int64_t P, int bins,
-                                  int slots, unsigned long long* __restrict__ counts) {
+__global__ void hist_count_kernel(const double* __restrict__ planes, int64_t P, int64_t stride,
+                                  int bins, int slots, unsigned long long* __restrict__ counts) {
   extern __shared__ unsigned int sh[];
   for (int i = threadIdx.x; i < bins * slots; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
        i += (int64_t)gridDim.x * blockDim.x) {
     for (int s = 0; s < slots; ++s) {
-      const int b = bin_of_f64(planes[s * P + i], bins);
+      const int b = bin_of_f64(planes[s * stride + i], bins);
       atomicAdd(&sh[s * bins + b], 1u);
     }
   }
@@ -85,13 +85,13 @@ __global__ void hist_count_kernel(const double* __restrict__ planes, int64_t P, 
     if (sh[i]) atomicAdd(&counts[i], (unsigned long long)sh[i]);
 }
 
-void launch_hist_count(psg_ctx* ctx, const double* planes, int64_t P, int bins, int slots,
-                       unsigned long long* counts) {
+void launch_hist_count(psg_ctx* ctx, const double* planes, int64_t P, int64_t stride, int bins,
+                       int slots, unsigned long long* counts) {
   ProfScope _prof(ctx, K_HIST);
   PSG_CUDA(cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * bins * slots, ctx->stream));
   const size_t sm = sizeof(unsigned int) * bins * slots;
-  hist_count_kernel<<<grid_for(ctx, P, 256, 4), 256, sm, ctx->stream>>>(planes, P, bins, slots,
-                                                                         counts);
+  hist_count_kernel<<<grid_for(ctx, P, 256, 4), 256, sm, ctx->stream>>>(planes, P, stride, bins,
+                                                                         slots, counts);
   PSG_LAUNCHED(ctx);
 }
 
@@ -162,6 +162,7 @@ void launch_penalty(psg_ctx* ctx, const Index& ix, const int32_t* idx, int64_t A
 template <int CMAX>
 __global__ void __launch_bounds__(256) mstep_kernel(MstepArgs a) {
   const int64_t P = (int64_t)a.W * a.H;
+  const int64_t PS = (int64_t)a.W * a.plane_rows;  // plane stride (band: rows >= H)
   for (int64_t pix = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pix < P;
        pix += (int64_t)gridDim.x * blockDim.x) {
     const int y = (int)(pix / a.W), x = (int)(pix - (int64_t)y * a.W);
@@ -196,7 +197,7 @@ __global__ void __launch_bounds__(256) mstep_kernel(MstepArgs a) {
       if (c >= a.C) break;
       double v = dmul(acc[c], inv);
       v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);  // std::clamp(.., 0, 1)
-      a.planes[c * P + pix] = v;
+      a.planes[c * PS + pix] = v;
       if (a.mirror) a.mirror[pix * a.C + c] = (float)v;
     }
   }

@@ -777,17 +777,15 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
       valid = q < a.nq;
     }
     const double* qrow = a.q + (valid ? q : 0) * d;
-    float q32[DP];
+    float2 q2[DP / 2];
     double qn2 = 0.0;
 #pragma unroll
-    for (int j = 0; j < DP; ++j) {
-      const double v = (valid && j < d) ? qrow[j] : 0.0;
-      q32[j] = (float)v;
-      qn2 += v * v;
+    for (int j = 0; j < DP / 2; ++j) {
+      const double v0 = (valid && 2 * j < d) ? qrow[2 * j] : 0.0;
+      const double v1 = (valid && 2 * j + 1 < d) ? qrow[2 * j + 1] : 0.0;
+      q2[j] = make_float2((float)v0, (float)v1);
+      qn2 += v0 * v0 + v1 * v1;
     }
-    float2 q2[DP / 2];
-#pragma unroll
-    for (int j = 0; j < DP / 2; ++j) q2[j] = make_float2(q32[2 * j], q32[2 * j + 1]);
     const float qn = __double2float_ru(sqrt(qn2) * (1.0 + 1e-12));
     // invalid lanes hold best = -1: every bound (>= 0) prunes them
     double best = valid ? kInf : -1.0;
@@ -879,8 +877,12 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
             pid[lane] = a.perm[pos];
           }
           __syncwarp();
-          // best rounded up to float: a float compare can only keep more points
+          // best rounded up to float: a float compare can only keep more points.
+          // thr >= s for every point that can pass the precise test below
+          // (eps is increasing in s and |p| <= pnorm_max)
           float best_up = __double2float_ru(best);
+          float thr = best_up * (1.f + 1e-4f) +
+                      1.01e-6f * (qn + a.pnorm_max) * (sqrtf(2.f * best_up + 1.f) + 1e-3f) + 1e-30f;
           for (int i = 0; i < cn; ++i) {
             const float4* pr = reinterpret_cast<const float4*>(stage + i * RS);
             // packed fp32x2 (FADD2/FFMA2); partial sums in any order: the filter
@@ -895,9 +897,12 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
               sb = __ffma2_rn(u1, u1, sb);
             }
             const float s = (sa.x + sa.y) + (sb.x + sb.y);
-            const float eps =
-                2.5e-7f * (float)(d + 4) * s + 1.0e-6f * (qn + aux0[i]) * (sqrtf(s) + 1e-3f) + 1e-30f;
-            const bool surv = s - eps <= best_up;
+            bool surv = s <= thr;
+            if (surv) {
+              const float eps = 2.5e-7f * (float)(d + 4) * s +
+                                1.0e-6f * (qn + aux0[i]) * (sqrtf(s) + 1e-3f) + 1e-30f;
+              surv = s - eps <= best_up;
+            }
             if (__any_sync(0xffffffffu, surv)) {
               if (surv) {
                 const int32_t id = pid[i];
@@ -907,6 +912,8 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
                   best = d2;
                   best_id = id;
                   best_up = __double2float_ru(best);
+                  thr = best_up * (1.f + 1e-4f) +
+                        1.01e-6f * (qn + a.pnorm_max) * (sqrtf(2.f * best_up + 1.f) + 1e-3f) + 1e-30f;
                 }
               }
             }
@@ -955,7 +962,7 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
         for (int j = 0; j < kBoxDims; ++j) {
           if (j < KB) {
             const float lo = boxs[c][2 * j], hi = boxs[c][2 * j + 1];
-            const float qj = q32[j];
+            const float qj = (j & 1) ? q2[j >> 1].y : q2[j >> 1].x;
             float gap = fmaxf(lo - qj, qj - hi) - 2.4e-7f * (fabsf(qj) + fabsf(lo) + fabsf(hi));
             gap = fmaxf(gap, 0.f);
             bx = fmaf(gap, gap, bx);

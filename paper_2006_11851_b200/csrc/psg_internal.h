@@ -86,6 +86,7 @@ struct Index {
   float* proj32_q4 = nullptr;  // [dp/4][N] float4 groups, leaf order, fp32 filter copy
   int dp = 32;
   float* pnorm32 = nullptr;    // [N] leaf order, |p| rounded up
+  float pnorm_max = 0.f;
   int32_t* perm = nullptr;     // leaf order -> id
   DevTree tree;
   HostTree htree;
@@ -172,6 +173,7 @@ struct SearchArgs {
   const double* proj_soa;   // [d][N] leaf order
   const float* proj32_q4;   // [dp/4][N] float4 groups, leaf order (fp32 filter)
   const float* pnorm32;     // [N] leaf order
+  float pnorm_max;          // max of pnorm32 (rounded up)
   const int32_t* perm;
   int64_t N;
   // coherence seeds (image index only): query anchor lattice + DB lattice
@@ -210,8 +212,8 @@ struct WeightArgs {
 void launch_weights(psg_ctx* ctx, const WeightArgs& a);
 void launch_eff_from(psg_ctx* ctx, const double* irls, const double* pen, int64_t A, double* eff,
                      int* flags);
-void launch_hist_count(psg_ctx* ctx, const double* planes, int64_t P, int bins, int slots,
-                       unsigned long long* counts);
+void launch_hist_count(psg_ctx* ctx, const double* planes, int64_t P, int64_t stride, int bins,
+                       int slots, unsigned long long* counts);
 void launch_hist_fold(psg_ctx* ctx, const unsigned long long* counts, int bins, int slots,
                       int64_t P, const double* ex_mass, double* mass, double* excess);
 void launch_penalty(psg_ctx* ctx, const Index& ix, const int32_t* idx, int64_t A,
@@ -226,10 +228,11 @@ struct MstepArgs {
   const int32_t* row_hi;
   const int32_t* idx;     // [A]
   const double* eff;      // [A]
-  int W, H, C, w;
+  int W, H, C, w;     // H = rows written (a band writes its owned rows only)
+  int plane_rows;     // rows allocated per plane (plane stride = W * plane_rows)
   const float* ex_mirror;
   int ew, nxe;
-  double* planes;  // out [C][H][W]
+  double* planes;  // out [C][plane_rows][W]
   float* mirror;   // out [H][W][C]
   int* flags;
 };

@@ -324,6 +324,15 @@ void finish_index(psg_ctx* ctx, Index& ix, const double* mean, const double* bas
   ix.pnorm32 = dalloc<float>(ix.N);
   launch_make_fp32_copies(ctx, ix.proj_soa, ix.N, d, ix.dp, ix.proj32_q4, ix.pnorm32);
   {
+    std::vector<float> pn(ix.N);
+    PSG_CUDA(cudaMemcpyAsync(pn.data(), ix.pnorm32, sizeof(float) * ix.N, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    float mx = 0.f;
+    for (float v : pn) mx = std::max(mx, v);
+    ix.pnorm_max = std::nextafter(mx, INFINITY);
+  }
+  {
     std::vector<float> c32(t.centroid.size()), c32t(t.centroid.size()), r32(nn), n32(nn);
     std::vector<float> blo((size_t)kBoxDims * nn, 0.f), bhi((size_t)kBoxDims * nn, 0.f);
     for (int i = 0; i < nn; ++i)
@@ -374,7 +383,7 @@ void build_exemplar_hist(psg_ctx* ctx, Index& ix, const double* ex_planes_dev, i
   DBuf<unsigned long long> counts(n);
   ix.ex_hist = dalloc<double>(n);
   const int64_t P = (int64_t)ix.ew * ix.eh;
-  launch_hist_count(ctx, ex_planes_dev, P, bins, ix.hist_slots, counts.p);
+  launch_hist_count(ctx, ex_planes_dev, P, P, bins, ix.hist_slots, counts.p);
   launch_hist_fold(ctx, counts.p, bins, ix.hist_slots, P, nullptr, ix.ex_hist, nullptr);
   ix.h_ex_hist.resize(n);
   PSG_CUDA(cudaMemcpyAsync(ix.h_ex_hist.data(), ix.ex_hist, sizeof(double) * n,
@@ -417,10 +426,13 @@ std::unique_ptr<psg_index> create_index_from_device_planes(psg_ctx* ctx, const d
 struct psg_level {
   psg_ctx* ctx = nullptr;
   const psg::Index* ix = nullptr;
-  int W = 0, H = 0, C = 0, w = 0;
+  int W = 0, H = 0, C = 0, w = 0;  // H: global image height
   psg_opt_cfg cfg{};
-  int nx = 0, ny = 0;
-  int64_t A = 0, P = 0, nn_calls = 0;
+  psg_band band{};                 // owned rows / anchors (world = 1: everything)
+  int Hl = 0, Hu = 0;              // local rows [p0, e1) allocated, owned rows [p0, p1)
+  int nx = 0, ny = 0, nh = 0;      // local anchor rows (halo rows first), halo rows
+  int64_t A = 0, Ao = 0, off = 0;  // local anchors, owned anchors, first owned anchor
+  int64_t P = 0, nn_calls = 0;     // plane stride W*Hl, reference plan calls of owned anchors
   psg::DBuf<int32_t> xs, ys, col_lo, col_hi, row_lo, row_hi, mult;
   psg::DBuf<double> planes;
   psg::DBuf<float> mirror;
@@ -430,7 +442,7 @@ struct psg_level {
   psg::DBuf<int32_t> visited;
   psg::DBuf<unsigned long long> counts;
   psg::DBuf<double> out_mass, excess, ex_hist, stats_dev;
-  double* stats_host = nullptr;  // pinned [6]
+  double* stats_host = nullptr;  // pinned [8]
   bool hist_on = false;
   int slots = 3;
   bool primed = false;
@@ -447,28 +459,73 @@ struct psg_level {
 };
 
 namespace psg {
+
+// Row-band partition of the output.  Rank g owns anchor rows
+// [a0, a1) and pixel rows [p0, p1); its windows read rows up to e1 (halo rows
+// [p1, e1) come from rank g+1), and its pixels are also covered by anchor rows
+// [hlo, a0) of rank g-1.  Accumulating those in ascending anchor id keeps the
+// M-step bit-identical to one device.
+psg_band shard_plan(int W, int H, int w, int sp, int rank, int world) {
+  if (world < 1 || rank < 0 || rank >= world) fail(PSG_E_DOMAIN, "bad rank / world size");
+  validate_grid(w, sp, W, H);
+  const auto ys = axis_positions(H, w, sp);
+  const int ny = (int)ys.size();
+  if (world > ny) fail(PSG_E_DOMAIN, "more ranks than anchor rows");
+  auto a0_of = [&](int g) { return (int)((int64_t)g * ny / world); };
+  auto p0_of = [&](int g) { return g == 0 ? 0 : ys[a0_of(g)]; };
+  psg_band b{};
+  b.W = W;
+  b.H = H;
+  b.w = w;
+  b.spacing = sp;
+  b.rank = rank;
+  b.world = world;
+  b.a0 = a0_of(rank);
+  b.a1 = a0_of(rank + 1);
+  b.p0 = p0_of(rank);
+  b.p1 = rank == world - 1 ? H : p0_of(rank + 1);
+  b.e1 = std::min(H, ys[b.a1 - 1] + w);
+  b.hlo = (int)(std::lower_bound(ys.begin(), ys.end(), b.p0 - w + 1) - ys.begin());
+  b.nx = (int)axis_positions(W, w, sp).size();
+  b.ny = ny;
+  if (rank > 0 && b.hlo < a0_of(rank - 1))
+    fail(PSG_E_DOMAIN, "row band thinner than the window: halo anchors span two ranks");
+  if (rank < world - 1 && b.e1 > (rank + 2 == world ? H : p0_of(rank + 2)))
+    fail(PSG_E_DOMAIN, "row band thinner than the window: halo rows span two ranks");
+  return b;
+}
+
 namespace {
 
-void level_setup(psg_level& L, psg_ctx* ctx, const Index& ix, int W, int H,
-                 const psg_opt_cfg& cfg, bool full) {
+void level_setup_band(psg_level& L, psg_ctx* ctx, const Index& ix, const psg_band& b,
+                      const psg_opt_cfg& cfg, bool full) {
   L.ctx = ctx;
   L.ix = &ix;
-  L.W = W;
-  L.H = H;
+  L.W = b.W;
+  L.H = b.H;
   L.C = ix.C;
   L.w = ix.w;
   L.cfg = cfg;
-  const int w = ix.w, sp = cfg.spacing;
-  const auto hx = axis_positions(W, w, sp), hy = axis_positions(H, w, sp);
+  L.band = b;
+  const int W = b.W, w = ix.w, sp = cfg.spacing;
+  if (sp != b.spacing || w != b.w) fail(PSG_E_SHAPE, "band plan does not match the level");
+  L.Hl = b.e1 - b.p0;
+  L.Hu = b.p1 - b.p0;
+  const auto hx = axis_positions(W, w, sp), hyg = axis_positions(b.H, w, sp);
+  std::vector<int32_t> hy;  // local anchor rows [hlo, a1), y relative to p0 (halo < 0)
+  for (int iy = b.hlo; iy < b.a1; ++iy) hy.push_back(hyg[iy] - b.p0);
   L.nx = (int)hx.size();
   L.ny = (int)hy.size();
+  L.nh = b.a0 - b.hlo;
   L.A = (int64_t)L.nx * L.ny;
-  L.P = (int64_t)W * H;
+  L.off = (int64_t)L.nh * L.nx;
+  L.Ao = L.A - L.off;
+  L.P = (int64_t)W * L.Hl;
   L.xs.alloc(L.nx);
   L.ys.alloc(L.ny);
   L.xs.upload(ctx, hx.data(), hx.size());
   L.ys.upload(ctx, hy.data(), hy.size());
-  // covering-anchor ranges per column / row: anchors a with a <= x < a + w
+  // covering-anchor ranges: anchors a with a <= x < a + w (local coordinates)
   auto ranges = [&](const std::vector<int32_t>& v, int extent, std::vector<int32_t>& lo,
                     std::vector<int32_t>& hi) {
     lo.resize(extent);
@@ -480,15 +537,15 @@ void level_setup(psg_level& L, psg_ctx* ctx, const Index& ix, int W, int H,
   };
   std::vector<int32_t> cl, ch, rl, rh;
   ranges(hx, W, cl, ch);
-  ranges(hy, H, rl, rh);
+  ranges(hy, L.Hu, rl, rh);
   L.col_lo.alloc(W);
   L.col_hi.alloc(W);
-  L.row_lo.alloc(H);
-  L.row_hi.alloc(H);
+  L.row_lo.alloc(L.Hu);
+  L.row_hi.alloc(L.Hu);
   L.col_lo.upload(ctx, cl.data(), W);
   L.col_hi.upload(ctx, ch.data(), W);
-  L.row_lo.upload(ctx, rl.data(), H);
-  L.row_hi.upload(ctx, rh.data(), H);
+  L.row_lo.upload(ctx, rl.data(), L.Hu);
+  L.row_hi.upload(ctx, rh.data(), L.Hu);
   L.planes.alloc((size_t)L.P * L.C);
   L.mirror.alloc((size_t)L.P * L.C);
   L.cur_idx.alloc(L.A);
@@ -497,23 +554,31 @@ void level_setup(psg_level& L, psg_ctx* ctx, const Index& ix, int W, int H,
   L.pen.alloc(L.A);
   L.eff.alloc(L.A);
   if (!full) return;
-  std::vector<int32_t> m(L.A);
-  L.nn_calls = plan_host(W, H, w, sp, cfg.patch_width, m.data());
-  if (L.nn_calls < 0) fail(PSG_E_LOGIC, "anchor not covered by any patch tile");
-  L.mult.alloc(L.A);
-  L.mult.upload(ctx, m.data(), L.A);
-  L.qproj.alloc((size_t)L.A * (ix.d > 0 ? ix.d : 1));
-  L.d2.alloc(L.A);
+  std::vector<int32_t> m((size_t)L.nx * b.ny);
+  const int64_t calls = plan_host(W, b.H, w, sp, cfg.patch_width, m.data());
+  if (calls < 0) fail(PSG_E_LOGIC, "anchor not covered by any patch tile");
+  std::vector<int32_t> mo(m.begin() + (size_t)b.a0 * L.nx, m.begin() + (size_t)b.a1 * L.nx);
+  L.nn_calls = 0;
+  for (int32_t v : mo) L.nn_calls += v;
+  L.mult.alloc(L.Ao);
+  L.mult.upload(ctx, mo.data(), L.Ao);
+  L.qproj.alloc((size_t)L.Ao * (ix.d > 0 ? ix.d : 1));
+  L.d2.alloc(L.Ao);
   L.next_idx.alloc(L.A);
   L.next_dist.alloc(L.A);
   L.after.alloc(L.A);
-  L.scanned.alloc(L.A);
-  L.exact_evals.alloc(L.A);
-  L.visited.alloc(L.A);
+  L.scanned.alloc(L.Ao);
+  L.exact_evals.alloc(L.Ao);
+  L.visited.alloc(L.Ao);
   L.stats_dev.alloc(8 + 6 * 296);
   PSG_CUDA(cudaMallocHost(&L.stats_host, sizeof(double) * 8));
   PSG_CUDA(cudaEventCreate(&L.ev0));
   PSG_CUDA(cudaEventCreate(&L.ev1));
+}
+
+void level_setup(psg_level& L, psg_ctx* ctx, const Index& ix, int W, int H,
+                 const psg_opt_cfg& cfg, bool full) {
+  level_setup_band(L, ctx, ix, shard_plan(W, H, ix.w, cfg.spacing, 0, 1), cfg, full);
 }
 
 void level_set_hist(psg_level& L, const double* ex_hist_host) {
@@ -536,25 +601,28 @@ void level_set_hist(psg_level& L, const double* ex_hist_host) {
   L.excess.alloc(n);
 }
 
-// E-step over all anchors of the level's current image.
+AnchorSet owned_anchors(psg_level& L) { return AnchorSet{L.xs.p, L.ys.p + L.nh, L.nx, L.Ao}; }
+
+// E-step over the owned anchors of the level's current (local) image.
 void level_search(psg_level& L, bool seeded, int32_t* out_idx, double* out_dist) {
   psg_ctx* ctx = L.ctx;
   const Index& ix = *L.ix;
-  AnchorSet as{L.xs.p, L.ys.p, L.nx, L.A};
+  const AnchorSet as = owned_anchors(L);
   if (ix.d > 0)
     launch_project_windows(ctx, L.mirror.p, L.W, L.C, L.w, as, ix.mean, ix.basis, ix.d, L.qproj.p);
   SearchArgs a{};
   a.q = L.qproj.p;
-  a.nq = L.A;
+  a.nq = L.Ao;
   a.d = ix.d;
-  a.seed_idx = (seeded && L.cfg.budget.mode == PSG_EXACT) ? L.cur_idx.p : nullptr;
+  a.seed_idx = (seeded && L.cfg.budget.mode == PSG_EXACT) ? L.cur_idx.p + L.off : nullptr;
   a.proj = ix.proj;
   a.proj_soa = ix.proj_soa;
   a.proj32_q4 = ix.proj32_q4;
   a.pnorm32 = ix.pnorm32;
+  a.pnorm_max = ix.pnorm_max;
   a.perm = ix.perm;
   a.qxs = L.xs.p;
-  a.qys = L.ys.p;
+  a.qys = L.ys.p + L.nh;
   a.qnx = L.nx;
   a.nxe = ix.nxe;
   a.nye = ix.eh - ix.w + 1;
@@ -562,15 +630,16 @@ void level_search(psg_level& L, bool seeded, int32_t* out_idx, double* out_dist)
   a.tree = ix.tree;
   a.mode = L.cfg.budget.mode;
   a.max_leaves = L.cfg.budget.max_leaves;
-  a.out_idx = out_idx;
+  a.out_idx = out_idx + L.off;
   a.out_d2 = L.d2.p;
   a.out_scanned = L.scanned.p;
   a.out_exact = L.exact_evals.p;
   a.out_visited = L.visited.p;
   a.flags = ctx->d_flags;
   launch_search(ctx, a);
-  launch_rescore_windows(ctx, L.mirror.p, L.W, L.C, L.w, as, ix, out_idx, out_dist);
-  L.unique_queries += L.A;
+  launch_rescore_windows(ctx, L.mirror.p, L.W, L.C, L.w, as, ix, out_idx + L.off,
+                         out_dist + L.off);
+  L.unique_queries += L.Ao;
 }
 
 void level_read_stats(psg_level& L) {
@@ -587,7 +656,7 @@ void level_prime(psg_level& L) {
   StatsArgs s{};
   s.scanned = L.scanned.p;
   s.mult = L.mult.p;
-  s.A = L.A;
+  s.A = L.Ao;
   s.r = L.cfg.robust_exponent;
   s.out = L.stats_dev.p;
   launch_stats(ctx, s);
@@ -614,7 +683,8 @@ MstepArgs mstep_args(psg_level& L) {
   m.idx = L.cur_idx.p;
   m.eff = L.eff.p;
   m.W = L.W;
-  m.H = L.H;
+  m.H = L.Hu;
+  m.plane_rows = L.Hl;
   m.C = L.C;
   m.w = L.w;
   m.ex_mirror = ix.ex_mirror;
@@ -626,75 +696,123 @@ MstepArgs mstep_args(psg_level& L) {
   return m;
 }
 
-// One EM iteration (optimizer.cpp:450-513).  Returns true when converged.
-bool level_step(psg_level& L, psg_iter_stats* st, bool honor) {
+// ---- one EM iteration in four phases (optimizer.cpp:453-497); the exchanges
+// of a row-sharded run happen between them (paper_2006_11851_b200/sharding.py).
+
+// Phase 1: IRLS weights of the owned anchors; local histogram counts of the
+// owned pixel rows (the caller sums them over ranks: exact integers).
+void phase_weights(psg_level& L) {
   psg_ctx* ctx = L.ctx;
-  const Index& ix = *L.ix;
   PSG_CUDA(cudaEventRecord(L.ev0, ctx->stream));
   WeightArgs wa{};
-  wa.dist = L.cur_dist.p;
-  wa.idx = L.cur_idx.p;
+  wa.dist = L.cur_dist.p + L.off;
+  wa.idx = L.cur_idx.p + L.off;
   wa.pen = nullptr;
-  wa.A = L.A;
+  wa.A = L.Ao;
   wa.r = L.cfg.robust_exponent;
   wa.eps = L.cfg.distance_epsilon;
-  wa.irls = L.irls.p;
-  wa.eff = L.eff.p;
+  wa.irls = L.irls.p + L.off;
+  wa.eff = L.eff.p + L.off;
   wa.flags = ctx->d_flags;
   launch_weights(ctx, wa);
-  if (L.hist_on) {
-    const int bins = L.cfg.histogram_bins;
-    launch_hist_count(ctx, L.planes.p, L.P, bins, L.slots, L.counts.p);
-    launch_hist_fold(ctx, L.counts.p, bins, L.slots, L.P, L.ex_hist.p, L.out_mass.p, L.excess.p);
-    launch_penalty(ctx, ix, L.cur_idx.p, L.A, L.excess.p, bins, L.slots, L.pen.p);
-    launch_eff_from(ctx, L.irls.p, L.pen.p, L.A, L.eff.p, ctx->d_flags);
-  }
-  launch_mstep(ctx, mstep_args(L));
-  AnchorSet as{L.xs.p, L.ys.p, L.nx, L.A};
-  launch_rescore_windows(ctx, L.mirror.p, L.W, L.C, L.w, as, ix, L.cur_idx.p, L.after.p);
+  if (L.hist_on)
+    launch_hist_count(ctx, L.planes.p, (int64_t)L.W * L.Hu, L.P, L.cfg.histogram_bins, L.slots,
+                      L.counts.p);
+}
+
+// Phase 2: fold the global counts (1/P over the WHOLE image), penalties and
+// effective weights of the owned anchors.
+void phase_penalty(psg_level& L, const unsigned long long* global_counts) {
+  if (!L.hist_on) return;
+  psg_ctx* ctx = L.ctx;
+  const int bins = L.cfg.histogram_bins;
+  launch_hist_fold(ctx, global_counts, bins, L.slots, (int64_t)L.W * L.H, L.ex_hist.p,
+                   L.out_mass.p, L.excess.p);
+  launch_penalty(ctx, *L.ix, L.cur_idx.p + L.off, L.Ao, L.excess.p, bins, L.slots,
+                 L.pen.p + L.off);
+  launch_eff_from(ctx, L.irls.p + L.off, L.pen.p + L.off, L.Ao, L.eff.p + L.off, ctx->d_flags);
+}
+
+// Phase 3: M-step of the owned pixel rows (halo anchor rows must be filled).
+void phase_update(psg_level& L) { launch_mstep(L.ctx, mstep_args(L)); }
+
+// Phase 4: lsq diagnostic, E-step, telemetry partials of the owned anchors.
+void phase_search(psg_level& L) {
+  psg_ctx* ctx = L.ctx;
+  launch_rescore_windows(ctx, L.mirror.p, L.W, L.C, L.w, owned_anchors(L), *L.ix,
+                         L.cur_idx.p + L.off, L.after.p + L.off);
   level_search(L, true, L.next_idx.p, L.next_dist.p);
   StatsArgs s{};
-  s.cur_dist = L.cur_dist.p;
-  s.after_dist = L.after.p;
-  s.eff = L.eff.p;
-  s.next_dist = L.next_dist.p;
-  s.cur_idx = L.cur_idx.p;
-  s.next_idx = L.next_idx.p;
+  s.cur_dist = L.cur_dist.p + L.off;
+  s.after_dist = L.after.p + L.off;
+  s.eff = L.eff.p + L.off;
+  s.next_dist = L.next_dist.p + L.off;
+  s.cur_idx = L.cur_idx.p + L.off;
+  s.next_idx = L.next_idx.p + L.off;
   s.scanned = L.scanned.p;
   s.mult = L.mult.p;
-  s.A = L.A;
+  s.A = L.Ao;
   s.r = L.cfg.robust_exponent;
   s.out = L.stats_dev.p;
   launch_stats(ctx, s);
   level_read_stats(L);
+}
+
+// Closes the iteration: stats record, swap current/next assignments.
+// stats_host holds this rank's partials; `global` (may alias) the summed ones.
+void phase_commit(psg_level& L, const double* global, psg_iter_stats* st) {
   float ms = 0.f;
   PSG_CUDA(cudaEventElapsedTime(&ms, L.ev0, L.ev1));
   ++L.iter;
-  const int64_t changed = (int64_t)L.stats_host[3];
   if (st) {
     st->iteration = L.iter;
-    st->energy = L.stats_host[2];
-    st->changed = changed;
-    st->nn_calls = L.nn_calls + L.pending_calls;
+    st->energy = global[2];
+    st->changed = (int64_t)global[3];
+    st->nn_calls = (int64_t)global[6] + (int64_t)global[7];
     st->millis = ms + L.pending_ms;
-    st->lsq_energy_before = L.stats_host[0];
-    st->lsq_energy_after = L.stats_host[1];
-    st->points_scanned = (int64_t)L.stats_host[4] + L.pending_scanned;
-    st->unique_queries = L.A * (L.pending_calls ? 2 : 1);
-    st->unique_points_scanned = (int64_t)L.stats_host[5];
+    st->lsq_energy_before = global[0];
+    st->lsq_energy_after = global[1];
+    st->points_scanned = (int64_t)global[4];
+    st->unique_queries = (int64_t)global[8];
+    st->unique_points_scanned = (int64_t)global[5];
   }
   L.pending_calls = 0;
   L.pending_scanned = 0;
   L.pending_ms = 0.0;
   std::swap(L.cur_idx, L.next_idx);
   std::swap(L.cur_dist, L.next_dist);
-  return honor && L.iter >= L.cfg.min_iterations &&
-         (double)changed < L.cfg.convergence_fraction * (double)L.A;
 }
 
+// This rank's telemetry partials {lsq_before, lsq_after, energy, changed,
+// points_scanned (plan-weighted, incl. priming), unique points scanned,
+// nn_calls, pending priming nn_calls, unique queries}.
+void phase_partials(psg_level& L, double out[9]) {
+  for (int k = 0; k < 6; ++k) out[k] = L.stats_host[k];
+  out[4] += (double)L.pending_scanned;
+  out[6] = (double)L.nn_calls;
+  out[7] = (double)L.pending_calls;
+  out[8] = (double)(L.Ao * (L.pending_calls ? 2 : 1));
+}
+
+// One EM iteration on a single device (optimizer.cpp:450-513).  Returns true
+// when converged under the reference's rule.
+bool level_step(psg_level& L, psg_iter_stats* st, bool honor) {
+  phase_weights(L);
+  phase_penalty(L, L.counts.p);
+  phase_update(L);
+  phase_search(L);
+  double g[9];
+  phase_partials(L, g);
+  phase_commit(L, g, st);
+  const int64_t changed = (int64_t)g[3];
+  return honor && L.iter >= L.cfg.min_iterations &&
+         (double)changed < L.cfg.convergence_fraction * (double)L.Ao;
+}
+
+// Host rows [p0, e1) of the global image (planes [C][Hl][W]).
 void upload_state(psg_level& L, const double* host_planes) {
   L.planes.upload(L.ctx, host_planes, (size_t)L.P * L.C);
-  launch_make_mirror(L.ctx, L.planes.p, L.C, L.W, L.H, L.mirror.p);
+  launch_make_mirror(L.ctx, L.planes.p, L.C, L.W, L.Hl, L.mirror.p);
 }
 
 }  // namespace
@@ -931,6 +1049,7 @@ psg_status psg_index_query(psg_ctx* ctx, const psg_index* index, const float* Q,
     a.proj_soa = ix.proj_soa;
     a.proj32_q4 = ix.proj32_q4;
     a.pnorm32 = ix.pnorm32;
+    a.pnorm_max = ix.pnorm_max;
     a.perm = ix.perm;
     a.N = ix.N;
     a.tree = ix.tree;
@@ -1035,6 +1154,120 @@ psg_status psg_level_create(psg_ctx* ctx, const psg_index* index, const double* 
     psg::level_set_hist(*L, ex_hist);
     psg::upload_state(*L, init);
     *out = L.release();
+  });
+}
+
+psg_status psg_shard_plan(int W, int H, int w, int spacing, int rank, int world, psg_band* out) {
+  return guarded([&] {
+    if (!out) fail(PSG_E_DOMAIN, "null output");
+    *out = psg::shard_plan(W, H, w, spacing, rank, world);
+  });
+}
+
+psg_status psg_band_create(psg_ctx* ctx, const psg_index* index, const double* rows,
+                           const psg_band* band, const psg_opt_cfg* cfg, const double* ex_hist,
+                           psg_level** out) {
+  return guarded([&] {
+    psg::StreamScope _ss(ctx ? ctx->stream : nullptr);
+    if (!ctx || !index || !rows || !band || !cfg || !out) fail(PSG_E_DOMAIN, "null argument");
+    *out = nullptr;
+    const psg::Index& ix = index->impl;
+    if (ix.from_vectors) fail(PSG_E_SHAPE, "optimize_level needs an exemplar-window index");
+    psg::validate_cfg(*cfg, ix.w, band->W, band->H);
+    const psg_band chk = psg::shard_plan(band->W, band->H, ix.w, cfg->spacing, band->rank,
+                                         band->world);
+    if (std::memcmp(&chk, band, sizeof(psg_band)) != 0) fail(PSG_E_SHAPE, "inconsistent band plan");
+    auto L = std::make_unique<psg_level>();
+    psg::level_setup_band(*L, ctx, ix, *band, *cfg, true);
+    psg::level_set_hist(*L, ex_hist);
+    psg::upload_state(*L, rows);
+    *out = L.release();
+  });
+}
+
+psg_status psg_band_phase1(psg_level* level, unsigned long long* counts_dev) {
+  return guarded([&] {
+    psg::StreamScope _ss(level->ctx->stream);
+    psg::level_prime(*level);
+    psg::phase_weights(*level);
+    if (level->hist_on && counts_dev)
+      PSG_CUDA(cudaMemcpyAsync(counts_dev, level->counts.p,
+                               sizeof(unsigned long long) * level->counts.n,
+                               cudaMemcpyDeviceToDevice, level->ctx->stream));
+    PSG_CUDA(cudaStreamSynchronize(level->ctx->stream));
+  });
+}
+
+psg_status psg_band_phase2(psg_level* level, const unsigned long long* global_counts_dev,
+                           int send_row0, void* send_dev) {
+  return guarded([&] {
+    psg_level& L = *level;
+    psg::StreamScope _ss(L.ctx->stream);
+    psg::phase_penalty(L, global_counts_dev ? global_counts_dev : L.counts.p);
+    if (send_dev && send_row0 < L.band.a1) {
+      if (send_row0 < L.band.a0) fail(PSG_E_DOMAIN, "send rows start below the owned rows");
+      const int64_t first = (int64_t)(send_row0 - L.band.hlo) * L.nx;
+      const int64_t n = (int64_t)(L.band.a1 - send_row0) * L.nx;
+      char* dst = static_cast<char*>(send_dev);
+      PSG_CUDA(cudaMemcpyAsync(dst, L.eff.p + first, sizeof(double) * n,
+                               cudaMemcpyDeviceToDevice, L.ctx->stream));
+      PSG_CUDA(cudaMemcpyAsync(dst + sizeof(double) * n, L.cur_idx.p + first, sizeof(int32_t) * n,
+                               cudaMemcpyDeviceToDevice, L.ctx->stream));
+    }
+    psg::check_flags(L.ctx);
+  });
+}
+
+psg_status psg_band_phase3(psg_level* level, const void* recv_dev, int n_send_rows,
+                           float* send_rows_dev) {
+  return guarded([&] {
+    psg_level& L = *level;
+    psg::StreamScope _ss(L.ctx->stream);
+    if (L.nh > 0) {
+      if (!recv_dev) fail(PSG_E_DOMAIN, "halo anchors required");
+      const int64_t n = L.off;
+      const char* src = static_cast<const char*>(recv_dev);
+      PSG_CUDA(cudaMemcpyAsync(L.eff.p, src, sizeof(double) * n, cudaMemcpyDeviceToDevice,
+                               L.ctx->stream));
+      PSG_CUDA(cudaMemcpyAsync(L.cur_idx.p, src + sizeof(double) * n, sizeof(int32_t) * n,
+                               cudaMemcpyDeviceToDevice, L.ctx->stream));
+    }
+    psg::phase_update(L);
+    if (n_send_rows > 0 && send_rows_dev) {
+      if (n_send_rows > L.Hu) fail(PSG_E_DOMAIN, "more halo rows requested than owned");
+      PSG_CUDA(cudaMemcpyAsync(send_rows_dev, L.mirror.p,
+                               sizeof(float) * (size_t)n_send_rows * L.W * L.C,
+                               cudaMemcpyDeviceToDevice, L.ctx->stream));
+    }
+    psg::check_flags(L.ctx);
+  });
+}
+
+psg_status psg_band_phase4(psg_level* level, const float* recv_rows_dev, double* partials) {
+  return guarded([&] {
+    psg_level& L = *level;
+    psg::StreamScope _ss(L.ctx->stream);
+    if (L.Hl > L.Hu) {
+      if (!recv_rows_dev) fail(PSG_E_DOMAIN, "halo rows required");
+      PSG_CUDA(cudaMemcpyAsync(L.mirror.p + (size_t)L.Hu * L.W * L.C, recv_rows_dev,
+                               sizeof(float) * (size_t)(L.Hl - L.Hu) * L.W * L.C,
+                               cudaMemcpyDeviceToDevice, L.ctx->stream));
+    }
+    psg::phase_search(L);
+    if (partials) psg::phase_partials(L, partials);
+  });
+}
+
+psg_status psg_band_commit(psg_level* level, const double* global_partials, psg_iter_stats* st) {
+  return guarded([&] {
+    psg::StreamScope _ss(level->ctx->stream);
+    double g[9];
+    if (global_partials) {
+      std::memcpy(g, global_partials, sizeof(g));
+    } else {
+      psg::phase_partials(*level, g);
+    }
+    psg::phase_commit(*level, g, st);
   });
 }
 

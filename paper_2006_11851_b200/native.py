@@ -53,6 +53,11 @@ class psg_iter_stats(ct.Structure):
                 ("unique_points_scanned", ct.c_int64)]
 
 
+class psg_band(ct.Structure):
+    _fields_ = [(n, ct.c_int) for n in ("W", "H", "w", "spacing", "rank", "world", "p0", "p1",
+                                        "e1", "hlo", "a0", "a1", "nx", "ny")]
+
+
 class psg_stage_list(ct.Structure):
     _fields_ = [("n_sizes", ct.c_int), ("sizes", ct.c_int * 4)]
 
@@ -113,6 +118,13 @@ _SIGS = {
     "psg_level_query_stats": (I, [VP, VP, VP, VP]),
     "psg_level_destroy": (None, [VP]),
     "psg_synthesize": (I, [VP, ct.POINTER(psg_request), VP, ct.POINTER(psg_report)]),
+    "psg_shard_plan": (I, [I, I, I, I, I, I, ct.POINTER(psg_band)]),
+    "psg_band_create": (I, [VP, VP, VP, ct.POINTER(psg_band), ct.POINTER(psg_opt_cfg), VP, PP]),
+    "psg_band_phase1": (I, [VP, VP]),
+    "psg_band_phase2": (I, [VP, VP, I, VP]),
+    "psg_band_phase3": (I, [VP, VP, I, VP]),
+    "psg_band_phase4": (I, [VP, VP, VP]),
+    "psg_band_commit": (I, [VP, VP, VP]),
     "psg_axis_positions": (I, [I, I, I, VP]),
     "psg_plan": (I64, [I, I, I, I, I, VP]),
     "psg_pow_cr": (D, [D, D]),
