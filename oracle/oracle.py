@@ -75,6 +75,7 @@ class Port:
             L.or_plan.restype = _I64
             L.or_plan.argtypes = [_I, _I, _I, _I, _I, _VP]
             L.or_project.argtypes = [_VP, _I64, _VP, _VP, _I, _VP]
+            L.or_extract_window.argtypes = [_VP, _I, _I, _I, _I, _I, _I, _VP]
             L.or_project_all.argtypes = [_VP, _I64, _I64, _VP, _VP, _I, _VP]
             L.or_dist2.restype = _D
             L.or_nearest_lexmin.restype = ct.c_int32
@@ -126,6 +127,19 @@ class Port:
         n = self.L.or_extract_all(_ptr(planes), C, W, H, w, sp, None)
         out = np.zeros((n, w * w * C), np.float32)
         self.L.or_extract_all(_ptr(planes), C, W, H, w, sp, _ptr(out))
+        return out
+
+    def extract_window(self, planes, ax, ay, w):
+        """neighborhood.cpp:120-137 on a (C, H, W) image (C-generalised)."""
+        C, H, W = planes.shape
+        out = np.zeros(w * w * C, np.float32)
+        self.L.or_extract_window(_ptr(planes), C, W, H, ax, ay, w, _ptr(out))
+        return out
+
+    def project(self, v, mean, basis):
+        v = _c(v, np.float32)
+        out = np.zeros(basis.shape[0], np.float64)
+        self.L.or_project(_ptr(v), v.size, _ptr(mean), _ptr(basis), basis.shape[0], _ptr(out))
         return out
 
     # index math -------------------------------------------------------------
