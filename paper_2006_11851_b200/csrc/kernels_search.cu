@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <float.h>
 
+#include <cub/cub.cuh>
+
 #include "numerics.cuh"
 #include "psg_internal.h"
 
@@ -1053,6 +1055,117 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
   const int64_t cap = (int64_t)ctx->num_sms * 16;
   if (blocks > cap) blocks = cap;
   search_kernel<<<(int)blocks, 32 * kSearchWarps, 0, ctx->stream>>>(a);
+  PSG_LAUNCHED(ctx);
+}
+
+// ----------------------------------------------------------------------------
+// Locality order for unstructured query sets (search-only workloads): each
+// query's greedy-descent leaf (fp32 centroid distances) is a sort key, so the
+// tile kernel's 32-query tiles share candidates.  Ordering only; results are
+// scattered back and are independent of it.
+__global__ void greedy_leaf_key_kernel(const double* __restrict__ q, int64_t nq, int d,
+                                       DevTree tree, uint32_t* __restrict__ keys,
+                                       int32_t* __restrict__ order) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nq;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double* qi = q + i * d;
+    int2 m = tree.meta[0];
+    int node = 0;
+    while (m.y < 0) {
+      const int fc = m.x, nc = -m.y;
+      float bd = __int_as_float(0x7f800000);
+      int bc = 0;
+      for (int c = 0; c < nc; ++c) {
+        const float* cen = tree.centroid32 + (int64_t)(fc + c) * d;
+        float s = 0.f;
+        for (int j = 0; j < d; ++j) {
+          const float t = (float)qi[j] - cen[j];
+          s = fmaf(t, t, s);
+        }
+        if (s < bd) {
+          bd = s;
+          bc = c;
+        }
+      }
+      node = fc + bc;
+      m = tree.meta[node];
+    }
+    keys[i] = (uint32_t)node;
+    order[i] = (int32_t)i;
+  }
+}
+
+template <class T>
+__global__ void gather_rows_kernel(const T* __restrict__ src, const int32_t* __restrict__ order,
+                                   int64_t n, int width, T* __restrict__ dst) {
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < n * width;
+       f += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = f / width;
+    const int j = (int)(f - i * width);
+    dst[f] = src[(int64_t)order[i] * width + j];
+  }
+}
+
+template <class T>
+__global__ void scatter_kernel(const T* __restrict__ src, const int32_t* __restrict__ order,
+                               int64_t n, T* __restrict__ dst) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[order[i]] = src[i];
+}
+
+size_t sort_pairs_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, (int)n);
+  return bytes;
+}
+
+void sort_pairs_u32(psg_ctx* ctx, const uint32_t* kin, uint32_t* kout, const int32_t* vin,
+                    int32_t* vout, int64_t n, void* temp, size_t temp_bytes) {
+  PSG_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, kin, kout, vin, vout, (int)n, 0, 32,
+                                           ctx->stream));
+  ctx->launches++;
+}
+
+void launch_greedy_keys(psg_ctx* ctx, const double* q, int64_t nq, int d, const DevTree& tree,
+                        uint32_t* keys, int32_t* order) {
+  ProfScope _prof(ctx, K_SEARCH);
+  int64_t blocks = (nq + 255) / 256;
+  if (blocks > (int64_t)ctx->num_sms * 32) blocks = (int64_t)ctx->num_sms * 32;
+  greedy_leaf_key_kernel<<<(int)blocks, 256, 0, ctx->stream>>>(q, nq, d, tree, keys, order);
+  PSG_LAUNCHED(ctx);
+}
+
+void launch_gather_rows_f64(psg_ctx* ctx, const double* src, const int32_t* order, int64_t n,
+                            int width, double* dst) {
+  int64_t blocks = (n * width + 255) / 256;
+  if (blocks > (int64_t)ctx->num_sms * 32) blocks = (int64_t)ctx->num_sms * 32;
+  gather_rows_kernel<double><<<(int)blocks, 256, 0, ctx->stream>>>(src, order, n, width, dst);
+  PSG_LAUNCHED(ctx);
+}
+
+void launch_scatter_i32(psg_ctx* ctx, const int32_t* src, const int32_t* order, int64_t n,
+                        int32_t* dst) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > (int64_t)ctx->num_sms * 32) blocks = (int64_t)ctx->num_sms * 32;
+  scatter_kernel<int32_t><<<(int)blocks, 256, 0, ctx->stream>>>(src, order, n, dst);
+  PSG_LAUNCHED(ctx);
+}
+
+void launch_scatter_f64(psg_ctx* ctx, const double* src, const int32_t* order, int64_t n,
+                        double* dst) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > (int64_t)ctx->num_sms * 32) blocks = (int64_t)ctx->num_sms * 32;
+  scatter_kernel<double><<<(int)blocks, 256, 0, ctx->stream>>>(src, order, n, dst);
+  PSG_LAUNCHED(ctx);
+}
+
+void launch_scatter_i64(psg_ctx* ctx, const int64_t* src, const int32_t* order, int64_t n,
+                        int64_t* dst) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > (int64_t)ctx->num_sms * 32) blocks = (int64_t)ctx->num_sms * 32;
+  scatter_kernel<int64_t><<<(int)blocks, 256, 0, ctx->stream>>>(src, order, n, dst);
   PSG_LAUNCHED(ctx);
 }
 

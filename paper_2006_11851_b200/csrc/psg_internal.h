@@ -191,6 +191,20 @@ struct SearchArgs {
   int* flags;
 };
 void launch_search(psg_ctx* ctx, const SearchArgs& a);
+// Locality ordering of unstructured queries (search-only workloads).
+void launch_greedy_keys(psg_ctx* ctx, const double* q, int64_t nq, int d, const DevTree& tree,
+                        uint32_t* keys, int32_t* order);
+size_t sort_pairs_temp_bytes(int64_t n);
+void sort_pairs_u32(psg_ctx* ctx, const uint32_t* kin, uint32_t* kout, const int32_t* vin,
+                    int32_t* vout, int64_t n, void* temp, size_t temp_bytes);
+void launch_gather_rows_f64(psg_ctx* ctx, const double* src, const int32_t* order, int64_t n,
+                            int width, double* dst);
+void launch_scatter_i32(psg_ctx* ctx, const int32_t* src, const int32_t* order, int64_t n,
+                        int32_t* dst);
+void launch_scatter_f64(psg_ctx* ctx, const double* src, const int32_t* order, int64_t n,
+                        double* dst);
+void launch_scatter_i64(psg_ctx* ctx, const int64_t* src, const int32_t* order, int64_t n,
+                        int64_t* dst);
 void launch_make_fp32_copies(psg_ctx* ctx, const double* soa, int64_t N, int d, int dp,
                              float* aos32, float* pn);
 // Full-D distance between query windows and assigned candidates (optimizer.cpp:117-124).

@@ -1059,7 +1059,30 @@ psg_status psg_index_query(psg_ctx* ctx, const psg_index* index, const float* Q,
     a.out_d2 = d2.p;
     a.out_scanned = sc.p;
     a.flags = ctx->d_flags;
-    psg::launch_search(ctx, a);
+    const bool reorder = budget.mode == PSG_EXACT && nq >= 64 && ix.d > 0 && !ctx->legacy_search;
+    if (reorder) {
+      // tiles of 32 queries share a traversal: give them neighbours in the tree
+      psg::DBuf<uint32_t> k0(nq), k1(nq);
+      psg::DBuf<int32_t> o0(nq), o1(nq), id_s(nq);
+      psg::DBuf<double> qs((size_t)nq * ix.d), d2_s(nq);
+      psg::DBuf<int64_t> sc_s(nq);
+      psg::launch_greedy_keys(ctx, qp.p, nq, ix.d, ix.tree, k0.p, o0.p);
+      const size_t tb = psg::sort_pairs_temp_bytes(nq);
+      psg::DBuf<char> tmp(tb ? tb : 1);
+      psg::sort_pairs_u32(ctx, k0.p, k1.p, o0.p, o1.p, nq, tmp.p, tb);
+      psg::launch_gather_rows_f64(ctx, qp.p, o1.p, nq, ix.d, qs.p);
+      a.q = qs.p;
+      a.out_idx = id_s.p;
+      a.out_d2 = d2_s.p;
+      a.out_scanned = sc_s.p;
+      psg::launch_search(ctx, a);
+      psg::launch_scatter_i32(ctx, id_s.p, o1.p, nq, id.p);
+      psg::launch_scatter_f64(ctx, d2_s.p, o1.p, nq, d2.p);
+      psg::launch_scatter_i64(ctx, sc_s.p, o1.p, nq, sc.p);
+      PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    } else {
+      psg::launch_search(ctx, a);
+    }
     if (ix.from_vectors) {
       psg::launch_rescore_vectors(ctx, q.p, nq, ix, id.p, dd.p);
     } else {
