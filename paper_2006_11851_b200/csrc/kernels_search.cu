@@ -1025,6 +1025,10 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
   ProfScope _prof(ctx, K_SEARCH);
   if (a.nq <= 0) return;
   if (a.d > kMaxD) fail(PSG_E_DOMAIN, "retained PCA dimension > 64 is not supported");
+  if (a.mode == PSG_EXACT && a.proj32_q4 && a.tree.centroid32 && ctx->mma_search &&
+      !ctx->legacy_search) {
+    if (launch_search_mma(ctx, a)) return;
+  }
   const bool tile_ok = a.tree.max_children <= kTileMaxB &&
                        1 + a.tree.max_depth * (a.tree.max_children - 1) <= kTileStack;
   if (a.mode == PSG_EXACT && a.proj32_q4 && a.tree.centroid32 && tile_ok && !ctx->legacy_search) {

@@ -129,6 +129,7 @@ struct psg_ctx {
   size_t pinned_bytes = 0;
   int* d_flags = nullptr;
   bool legacy_search = false;  // PERSYN_SEARCH=warp: per-query warp kernel instead of tiles
+  bool mma_search = false;     // PERSYN_SEARCH=mma: tcgen05 tile kernel
 };
 
 struct psg_index {
@@ -191,6 +192,8 @@ struct SearchArgs {
   int* flags;
 };
 void launch_search(psg_ctx* ctx, const SearchArgs& a);
+// tcgen05 (UMMA) tile search; returns false when the tree shape is unsupported.
+bool launch_search_mma(psg_ctx* ctx, const SearchArgs& a);
 // Locality ordering of unstructured queries (search-only workloads).
 void launch_greedy_keys(psg_ctx* ctx, const double* q, int64_t nq, int d, const DevTree& tree,
                         uint32_t* keys, int32_t* order);

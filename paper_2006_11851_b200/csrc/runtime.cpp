@@ -863,7 +863,10 @@ psg_status psg_ctx_create(int device, void* stream, psg_ctx** out) {
     auto c = std::make_unique<psg_ctx>();
     c->device = device;
     c->num_sms = prop.multiProcessorCount;
-    if (const char* e = std::getenv("PERSYN_SEARCH")) c->legacy_search = std::string(e) == "warp";
+    if (const char* e = std::getenv("PERSYN_SEARCH")) {
+      c->legacy_search = std::string(e) == "warp";
+      c->mma_search = std::string(e) == "mma";
+    }
     if (stream) {
       c->stream = static_cast<cudaStream_t>(stream);
     } else {
