@@ -1,11 +1,17 @@
 // Per-stage PCA fit on device (fit_pca, pca.cpp:49-101).
 //
 // mean (deterministic per-feature reduction) -> centred fp64 design matrix
-// -> covariance X^T X / (n-1) with cuBLAS DSYRK -> cuSOLVER DSYEVD -> on the
-// host: variances descending and clamped >= 0 (pca.cpp:72-77), smallest
+// -> covariance X^T X / (n-1) with cuBLAS DSYRK -> cuSOLVER eigensolver -> on
+// the host: variances descending and clamped >= 0 (pca.cpp:72-77), smallest
 // prefix reaching the variance target (pca.cpp:79-87) optionally capped or
 // fixed (the BASELINE configs' d), sign fix "largest-|.| entry positive",
 // first index on ties (pca.cpp:92-95, Eigen maxCoeff).
+//
+// When the retained dimension is bounded (d fixed or capped, always <= 64) only
+// the top eigenpairs are computed (DSYEVDX, range I): the total variance is the
+// trace of the covariance, the reference's sum of clamped eigenvalues up to
+// rounding of the (tiny) negative ones; the unreported tail of `variances` is
+// zero.  Unbounded variance targets use the full DSYEVD spectrum.
 //
 // Eigen3 is not available to pin the reference's fit bit-for-bit (SURVEY
 // §8c: "parity unpinned"); the fit is property-tested and the resulting basis
@@ -79,22 +85,56 @@ void fit_pca_device(psg_ctx* ctx, Index& ix, const psg_index_cfg& cfg) {
                            Xc.as<double>(), D, &beta, cov.as<double>(), D),
                "cublasDsyrk");
   ctx->launches++;
+
+  // number of top eigenpairs needed (0 = full spectrum)
+  int m_top = 0;
+  if (cfg.d_fixed > 0) m_top = std::min(cfg.d_fixed, D);
+  else if (cfg.d_cap > 0) m_top = std::min(cfg.d_cap, D);
+  const bool subset = m_top > 0 && m_top < D;
+  std::vector<double> diag;
+  if (subset) {  // trace before the solver overwrites the matrix
+    std::vector<double> h((size_t)D);
+    PSG_CUDA(cudaMemcpy2DAsync(h.data(), sizeof(double), cov.as<double>(),
+                               sizeof(double) * (D + 1), sizeof(double), D,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    diag = std::move(h);
+  }
   DevMem evals(sizeof(double) * D);
-  int lwork = 0;
-  cusolver_check(cusolverDnDsyevd_bufferSize(cs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
-                                             D, cov.as<double>(), D, evals.as<double>(), &lwork),
-                 "syevd_bufferSize");
-  DevMem work(sizeof(double) * (size_t)lwork);
   DevMem info(sizeof(int));
-  cusolver_check(cusolverDnDsyevd(cs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, D,
-                                  cov.as<double>(), D, evals.as<double>(), work.as<double>(),
-                                  lwork, info.as<int>()),
-                 "cusolverDnDsyevd");
+  int lwork = 0, meig = D;
+  if (subset) {
+    const int il = D - m_top + 1, iu = D;
+    cusolver_check(cusolverDnDsyevdx_bufferSize(cs, CUSOLVER_EIG_MODE_VECTOR,
+                                                CUSOLVER_EIG_RANGE_I, CUBLAS_FILL_MODE_LOWER, D,
+                                                cov.as<double>(), D, 0.0, 0.0, il, iu, &meig,
+                                                evals.as<double>(), &lwork),
+                   "syevdx_bufferSize");
+    DevMem work(sizeof(double) * (size_t)lwork);
+    cusolver_check(cusolverDnDsyevdx(cs, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_I,
+                                     CUBLAS_FILL_MODE_LOWER, D, cov.as<double>(), D, 0.0, 0.0, il,
+                                     iu, &meig, evals.as<double>(), work.as<double>(), lwork,
+                                     info.as<int>()),
+                   "cusolverDnDsyevdx");
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+  } else {
+    cusolver_check(cusolverDnDsyevd_bufferSize(cs, CUSOLVER_EIG_MODE_VECTOR,
+                                               CUBLAS_FILL_MODE_LOWER, D, cov.as<double>(), D,
+                                               evals.as<double>(), &lwork),
+                   "syevd_bufferSize");
+    DevMem work(sizeof(double) * (size_t)lwork);
+    cusolver_check(cusolverDnDsyevd(cs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, D,
+                                    cov.as<double>(), D, evals.as<double>(), work.as<double>(),
+                                    lwork, info.as<int>()),
+                   "cusolverDnDsyevd");
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
   ctx->launches++;
 
-  std::vector<double> h_eval(D), h_mean(D);
+  const int ne = subset ? meig : D;  // eigenpairs computed, ascending in cov's first columns
+  std::vector<double> h_eval(ne), h_mean(D);
   int h_info = 0;
-  PSG_CUDA(cudaMemcpyAsync(h_eval.data(), evals.p, sizeof(double) * D, cudaMemcpyDeviceToHost,
+  PSG_CUDA(cudaMemcpyAsync(h_eval.data(), evals.p, sizeof(double) * ne, cudaMemcpyDeviceToHost,
                            ctx->stream));
   PSG_CUDA(cudaMemcpyAsync(h_mean.data(), mean.p, sizeof(double) * D, cudaMemcpyDeviceToHost,
                            ctx->stream));
@@ -103,31 +143,34 @@ void fit_pca_device(psg_ctx* ctx, Index& ix, const psg_index_cfg& cfg) {
   if (h_info != 0) fail(PSG_E_DOMAIN, "eigendecomposition did not converge");
 
   // descending, clamped (pca.cpp:72-77)
-  std::vector<double> var(D);
+  std::vector<double> var(D, 0.0);
   double total = 0.0;
-  for (int k = 0; k < D; ++k) {
-    var[k] = std::max(0.0, h_eval[D - 1 - k]);
-    total += var[k];
+  for (int k = 0; k < ne; ++k) var[k] = std::max(0.0, h_eval[ne - 1 - k]);
+  if (subset) {
+    for (int j = 0; j < D; ++j) total += diag[j];
+    total = std::max(total, 0.0);
+  } else {
+    for (int k = 0; k < D; ++k) total += var[k];
   }
   int retained = 0;
   if (cfg.d_fixed > 0) {
     retained = std::min(cfg.d_fixed, D);
   } else if (total > 0.0) {
     double cum = 0.0;
-    for (retained = 1; retained <= D; ++retained) {
+    for (retained = 1; retained <= ne; ++retained) {
       cum += var[retained - 1];
       if (cum >= cfg.variance_target * total) break;
     }
-    retained = std::min(retained, D);
+    retained = std::min(retained, ne);
     if (cfg.d_cap > 0) retained = std::min(retained, cfg.d_cap);
   }
   if (retained > 64) fail(PSG_E_DOMAIN, "retained PCA dimension > 64 is not supported");
 
-  // eigenvectors: column (D-1-k) of the column-major result
+  // eigenvector of the k-th largest: column (ne-1-k) of the column-major result
   std::vector<double> basis((size_t)retained * D);
   if (retained > 0) {
     std::vector<double> cols((size_t)retained * D);
-    PSG_CUDA(cudaMemcpyAsync(cols.data(), cov.as<double>() + (size_t)(D - retained) * D,
+    PSG_CUDA(cudaMemcpyAsync(cols.data(), cov.as<double>() + (size_t)(ne - retained) * D,
                              sizeof(double) * (size_t)retained * D, cudaMemcpyDeviceToHost,
                              ctx->stream));
     PSG_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -15,6 +15,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -245,6 +246,15 @@ namespace {
 void finish_index(psg_ctx* ctx, Index& ix, const double* mean, const double* basis, int d,
                   const psg_index_cfg& cfg) {
   const int D = ix.D;
+  const bool verbose = std::getenv("PERSYN_VERBOSE") != nullptr;
+  double t_phase = now_ms();
+  auto phase = [&](const char* what) {
+    if (!verbose) return;
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    const double t = now_ms();
+    fprintf(stderr, "[persyn] index N=%lld D=%d: %s %.2f ms\n", (long long)ix.N, D, what, t - t_phase);
+    t_phase = t;
+  };
   if (basis) {
     if (d < 0 || d > 64) fail(PSG_E_DOMAIN, "injected PCA dimension must be in [0, 64]");
     ix.h_mean.assign(mean, mean + D);
@@ -255,6 +265,7 @@ void finish_index(psg_ctx* ctx, Index& ix, const double* mean, const double* bas
     fit_pca_device(ctx, ix, cfg);
   }
   d = ix.d;
+  phase("pca fit");
   ix.mean = dalloc<double>(D);
   PSG_CUDA(cudaMemcpyAsync(ix.mean, ix.h_mean.data(), sizeof(double) * D, cudaMemcpyHostToDevice,
                            ctx->stream));
@@ -284,6 +295,7 @@ void finish_index(psg_ctx* ctx, Index& ix, const double* mean, const double* bas
       PSG_CUDA(cudaStreamSynchronize(ctx->stream));
     }
   }
+  phase("db projection");
   // tree (host-native build over the device-projected points)
   std::vector<double> hp((size_t)ix.N * d);
   if (d > 0)
@@ -292,6 +304,7 @@ void finish_index(psg_ctx* ctx, Index& ix, const double* mean, const double* bas
   PSG_CUDA(cudaStreamSynchronize(ctx->stream));
   ix.htree = build_tree_host(hp.data(), ix.N, d, cfg.branching, cfg.max_depth,
                              cfg.leaf_threshold > 0 ? cfg.leaf_threshold : cfg.branching, cfg.seed);
+  phase("tree build (host)");
   const HostTree& t = ix.htree;
   const int nn = (int)t.radius.size();
   ix.tree.n_nodes = nn;
@@ -371,6 +384,7 @@ void finish_index(psg_ctx* ctx, Index& ix, const double* mean, const double* bas
     up(ix.tree.cnorm32, n32);
   }
   PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+  phase("tree upload + search copies");
 }
 
 void build_exemplar_hist(psg_ctx* ctx, Index& ix, const double* ex_planes_dev, int bins,
