@@ -149,6 +149,25 @@ psg_status psg_index_projected(const psg_index* index, double* out);
 /* Leaves in tree order (KmTree::leaves, km_tree.cpp:286-298). */
 psg_status psg_index_leaves(const psg_index* index, int32_t* ids, int32_t* sizes,
                             int64_t* n_leaves);
+/*
+ * Tree replay: replaces the index's k-means tree by an externally built one,
+ * e.g. the reference's KmTree (KmTree::build, km_tree.cpp:141-195) recovered
+ * from its public structure_json() and leaves() (km_tree.cpp:286-318).  With
+ * the reference's tree imported, greedy and backtrack(m) queries reproduce
+ * KmTree::query (km_tree.cpp:213-250) bit-for-bit, including the heap
+ * tie-break on the reference's post-order node ids.  Centroids and radii are
+ * recomputed from the leaf membership with the reference's ordered loops.
+ *   n_children[n_nodes]: child counts in pre-order DFS (children in order)
+ *   leaf_sizes[n_leaves], leaf_ids[N]: KmTree::leaves(), concatenated
+ */
+typedef struct {
+  int64_t n_nodes;
+  const int32_t* n_children;
+  int64_t n_leaves;
+  const int32_t* leaf_sizes;
+  const int32_t* leaf_ids;
+} psg_tree_import;
+psg_status psg_index_import_tree(psg_ctx* ctx, psg_index* index, const psg_tree_import* tree);
 /* Exemplar histogram [slots][bins] (pipeline.cpp:379-385). */
 psg_status psg_index_histograms(const psg_index* index, double* mass);
 /*

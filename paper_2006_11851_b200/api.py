@@ -192,6 +192,26 @@ class SearchIndex:
         N.check(N.lib.psg_index_leaves(self.h, _p(ids), _p(sizes), ct.byref(nl)))
         return ids, sizes[: nl.value].copy()
 
+    def import_tree(self, n_children, leaf_sizes, leaf_ids):
+        """Replace the tree by an external one (psg_index_import_tree): child
+        counts in pre-order DFS and KmTree::leaves() (km_tree.cpp:286-318)."""
+        nc = _c(n_children, np.int32)
+        ls = _c(leaf_sizes, np.int32)
+        li = _c(leaf_ids, np.int32)
+        t = N.psg_tree_import(nc.size, nc.ctypes.data, ls.size, ls.ctypes.data, li.ctypes.data)
+        N.check(N.lib.psg_index_import_tree(self.ctx.h, self.h, ct.byref(t)))
+        dims = np.zeros(10, np.int64)
+        N.check(N.lib.psg_index_info(self.h, _p(dims)))
+        self.n_nodes, self.n_leaves, self.depth = (int(v) for v in dims[7:10])
+
+    def import_reference_tree(self, structure_json, leaves):
+        """Import the reference's KmTree from structure_json() (str or dict) and
+        leaves() (a list of id lists)."""
+        n_children = preorder_child_counts(structure_json)
+        sizes = np.array([len(l) for l in leaves], np.int32)
+        ids = np.concatenate([np.asarray(l, np.int32) for l in leaves])
+        self.import_tree(n_children, sizes, ids)
+
     def histograms(self, slots=3, bins=16) -> np.ndarray:
         out = np.zeros((slots, bins))
         N.check(N.lib.psg_index_histograms(self.h, _p(out)))
@@ -212,6 +232,21 @@ class SearchIndex:
         N.check(N.lib.psg_index_query(self.ctx.h, self.h, _p(Q), n, budget.c(), _p(idx), _p(dist),
                                       _p(dpca), _p(sc)))
         return idx, dist, dpca, sc
+
+
+def preorder_child_counts(structure_json) -> np.ndarray:
+    """Child counts in pre-order DFS from KmTree::structure_json()
+    (km_tree.cpp:300-318: {"root": {"size", "children": [...]}})."""
+    import json as _json
+    j = _json.loads(structure_json) if isinstance(structure_json, (str, bytes)) else structure_json
+    out = []
+    stack = [j["root"]]
+    while stack:
+        node = stack.pop()
+        kids = node.get("children", [])
+        out.append(len(kids))
+        stack.extend(reversed(kids))
+    return np.array(out, np.int32)
 
 
 def make_pca_tree_index(exemplar: np.ndarray, window: int, variance_target: float = 0.95,

@@ -177,7 +177,8 @@ void launch_project_vectors(psg_ctx* ctx, const float* X, int64_t n, int D, cons
 // ----------------------------------------------------------------------------
 // Tree search: one warp per query (persistent grid-stride over queries).
 constexpr int kSearchWarps = 4;
-constexpr int kStack = 256;
+constexpr int kStack = 512;   // warp-per-query kernel (deep imported trees, backtrack frontier)
+constexpr int kStackX = 256;  // search_exact_kernel
 constexpr int kMaxD = 64;
 
 struct WarpLexMin {
@@ -362,6 +363,8 @@ __global__ void __launch_bounds__(32 * kSearchWarps) search_kernel(SearchArgs a)
     } else {
       // backtrack(m), km_tree.cpp:232-250: best-first on (dist^2 to centroid,
       // node id); frontier kept as an unsorted pool, min found by the warp.
+      // The node id of the tie-break is the tree's tie id (the reference's
+      // post-order id for an imported tree, km_tree.cpp:159,187-188).
       int size = 1;
       if (lane == 0) {
         sn[0] = 0;
@@ -379,7 +382,7 @@ __global__ void __launch_bounds__(32 * kSearchWarps) search_kernel(SearchArgs a)
           int32_t nid = 0x7fffffff;
           if (s < size) {
             k = sk[s];
-            nid = sn[s];
+            nid = a.tree.tie ? a.tree.tie[sn[s]] : sn[s];
           }
           const WarpLexMin m = warp_lexmin(k, nid);
           if (lex_less(m.d2, m.id, bk, bn)) {
@@ -390,10 +393,12 @@ __global__ void __launch_bounds__(32 * kSearchWarps) search_kernel(SearchArgs a)
         // locate the slot of the winner and remove it (swap with last)
         for (int s0 = 0; s0 < size; s0 += 32) {
           const int s = s0 + lane;
-          const bool hit = s < size && sn[s] == bn && sk[s] == bk;
+          const bool hit =
+              s < size && sk[s] == bk && (a.tree.tie ? a.tree.tie[sn[s]] : sn[s]) == bn;
           const unsigned hm = __ballot_sync(0xffffffffu, hit);
           if (hm && bslot < 0) bslot = s0 + __ffs(hm) - 1;
         }
+        const int node = sn[bslot];
         __syncwarp();
         if (lane == 0) {
           sn[bslot] = sn[size - 1];
@@ -401,7 +406,6 @@ __global__ void __launch_bounds__(32 * kSearchWarps) search_kernel(SearchArgs a)
         }
         --size;
         __syncwarp();
-        const int node = bn;
         const int nc = a.tree.n_children[node];
         if (nc == 0) {
           scan_leaf(a, qs, node, lane, best, best_id, scanned);
@@ -454,8 +458,8 @@ __global__ void __launch_bounds__(256) search_exact_kernel(SearchArgs a) {
   constexpr int W = 8;
   __shared__ double qs_all[W][DP];
   __shared__ __align__(16) float q32_all[W][DP];
-  __shared__ int2 st_meta[W][kStack];   // node meta: {first child | leaf start, -children | count}
-  __shared__ float st_key[W][kStack];
+  __shared__ int2 st_meta[W][kStackX];   // node meta: {first child | leaf start, -children | count}
+  __shared__ float st_key[W][kStackX];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* qs = qs_all[warp];
   float* q32 = q32_all[warp];
@@ -691,7 +695,7 @@ __global__ void __launch_bounds__(256) search_exact_kernel(SearchArgs a) {
           const float ol = __shfl_sync(0xffffffffu, lb2, o);
           if (((km >> o) & 1u) && (ol < lb2 || (ol == lb2 && o < c))) ++rank;
         }
-        if (top + nkeep > kStack) {
+        if (top + nkeep > kStackX) {
           if (lane == 0) atomicOr(a.flags, FLAG_STACK_OVERFLOW);
           break;
         }
@@ -1238,6 +1242,43 @@ void launch_rescore_windows(psg_ctx* ctx, const float* mirror, int img_w, int C,
   rescore_windows_kernel<<<(int)blocks, threads, 0, ctx->stream>>>(
       mirror, img_w, C, w, anchors.xs, anchors.ys, anchors.nx, anchors.count, ix.ex_mirror,
       ix.ew, ix.nxe, idx, dist);
+  PSG_LAUNCHED(ctx);
+}
+
+// Explicit query vectors against a window index's candidates (batched
+// PcaTreeIndex::nearest rescoring, optimizer.cpp:232-234): the candidate
+// window is read from the exemplar mirror in (dy, dx, c) order.
+__global__ void rescore_query_windows_kernel(const float* __restrict__ Q, int64_t nq, int C, int w,
+                                             const float* __restrict__ ex_mirror, int ew, int nxe,
+                                             const int32_t* __restrict__ idx,
+                                             double* __restrict__ dist) {
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nq;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t id = idx[a];
+    const int ex = id % nxe, ey = id / nxe;
+    const int row = w * C;
+    const float* v = Q + a * (int64_t)row * w;
+    double acc = 0.0;
+    for (int dy = 0; dy < w; ++dy) {
+      const float* z = ex_mirror + ((int64_t)(ey + dy) * ew + ex) * C;
+      for (int jj = 0; jj < row; ++jj) {
+        const double t = dsub((double)v[dy * row + jj], (double)z[jj]);
+        acc = dadd(acc, dmul(t, t));
+      }
+    }
+    dist[a] = sqrt(acc);
+  }
+}
+
+void launch_rescore_query_windows(psg_ctx* ctx, const float* Q, int64_t nq, const Index& ix,
+                                  const int32_t* idx, double* dist) {
+  ProfScope _prof(ctx, K_RESCORE);
+  if (nq <= 0) return;
+  const int threads = 128;
+  int64_t blocks = (nq + threads - 1) / threads;
+  if (blocks > (int64_t)ctx->num_sms * 32) blocks = (int64_t)ctx->num_sms * 32;
+  rescore_query_windows_kernel<<<(int)blocks, threads, 0, ctx->stream>>>(
+      Q, nq, ix.C, ix.w, ix.ex_mirror, ix.ew, ix.nxe, idx, dist);
   PSG_LAUNCHED(ctx);
 }
 

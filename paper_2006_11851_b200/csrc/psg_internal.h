@@ -58,6 +58,7 @@ struct DevTree {
   float* boxlo = nullptr;       // [kBoxDims][n_nodes] per-dim minimum over the subtree
   float* boxhi = nullptr;       // [kBoxDims][n_nodes]
   int2* meta = nullptr;         // {first_child, -n_children} or {leaf_start, leaf_count}
+  int32_t* tie = nullptr;       // optional backtrack tie-break id per node (null = node index)
 };
 constexpr int kBoxDims = 8;     // leading PCA dims carrying bounding boxes
 
@@ -66,6 +67,7 @@ struct HostTree {
   std::vector<int32_t> first_child, n_children, leaf_start, leaf_count, depth;
   std::vector<int32_t> perm;  // leaf order -> point id
   std::vector<double> boxlo, boxhi;  // [n_nodes][kBoxDims]
+  std::vector<int32_t> tie;          // empty = node index (own trees)
   int max_depth = 0;
   int n_leaves = 0;
 };
@@ -213,6 +215,8 @@ void launch_make_fp32_copies(psg_ctx* ctx, const double* soa, int64_t N, int d, 
 // Full-D distance between query windows and assigned candidates (optimizer.cpp:117-124).
 void launch_rescore_windows(psg_ctx* ctx, const float* mirror, int img_w, int C, int w,
                             AnchorSet anchors, const Index& ix, const int32_t* idx, double* dist);
+void launch_rescore_query_windows(psg_ctx* ctx, const float* Q, int64_t nq, const Index& ix,
+                                  const int32_t* idx, double* dist);
 void launch_rescore_vectors(psg_ctx* ctx, const float* Q, int64_t nq, const Index& ix,
                             const int32_t* idx, double* dist);
 // M-step pieces.
@@ -287,6 +291,10 @@ void launch_fit_to(psg_ctx* ctx, const double* in, int W, int H, int ow, int oh,
 // ---- host pieces --------------------------------------------------------------
 HostTree build_tree_host(const double* proj, int64_t N, int d, int branching, int max_depth,
                          int leaf_threshold, uint64_t seed);
+// Replay of an external tree (pre-order child counts + DFS leaf lists).
+HostTree import_tree_host(const double* proj, int64_t N, int d, const int32_t* n_children_pre,
+                          int64_t n_nodes, const int32_t* leaf_sizes, int64_t n_leaves,
+                          const int32_t* leaf_ids);
 void fit_pca_device(psg_ctx* ctx, Index& ix, const psg_index_cfg& cfg);
 int64_t plan_host(int W, int H, int w, int sp, int p, int32_t* mult);
 std::vector<int32_t> axis_positions(int extent, int window, int step);

@@ -234,6 +234,7 @@ Index::~Index() {
   cudaFree(tree.boxlo);
   cudaFree(tree.boxhi);
   cudaFree(tree.meta);
+  cudaFree(tree.tie);
   cudaFree(pnorm32);
   cudaFree(ex_hist);
 }
@@ -243,68 +244,27 @@ Index::~Index() {
 // pipeline.cpp:276-292).
 namespace {
 
-void finish_index(psg_ctx* ctx, Index& ix, const double* mean, const double* basis, int d,
-                  const psg_index_cfg& cfg) {
-  const int D = ix.D;
-  const bool verbose = std::getenv("PERSYN_VERBOSE") != nullptr;
-  double t_phase = now_ms();
-  auto phase = [&](const char* what) {
-    if (!verbose) return;
-    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
-    const double t = now_ms();
-    fprintf(stderr, "[persyn] index N=%lld D=%d: %s %.2f ms\n", (long long)ix.N, D, what, t - t_phase);
-    t_phase = t;
-  };
-  if (basis) {
-    if (d < 0 || d > 64) fail(PSG_E_DOMAIN, "injected PCA dimension must be in [0, 64]");
-    ix.h_mean.assign(mean, mean + D);
-    ix.h_basis.assign(basis, basis + (size_t)d * D);
-    ix.h_var.assign(D, 0.0);
-    ix.d = d;
-  } else {
-    fit_pca_device(ctx, ix, cfg);
-  }
-  d = ix.d;
-  phase("pca fit");
-  ix.mean = dalloc<double>(D);
-  PSG_CUDA(cudaMemcpyAsync(ix.mean, ix.h_mean.data(), sizeof(double) * D, cudaMemcpyHostToDevice,
-                           ctx->stream));
-  // transposed, zero-padded basis [D][KP] for the projection kernel
-  const int KP = d <= 32 ? 32 : 64;
-  std::vector<double> bt((size_t)D * KP, 0.0);
-  for (int k = 0; k < d; ++k)
-    for (int j = 0; j < D; ++j) bt[(size_t)j * KP + k] = ix.h_basis[(size_t)k * D + j];
-  ix.basis = dalloc<double>(bt.size());
-  PSG_CUDA(cudaMemcpyAsync(ix.basis, bt.data(), sizeof(double) * bt.size(), cudaMemcpyHostToDevice,
-                           ctx->stream));
-  // project the database (pca.cpp:103-113)
-  ix.proj = dalloc<double>((size_t)ix.N * (d > 0 ? d : 1));
-  if (d > 0) {
-    if (ix.from_vectors) {
-      launch_project_vectors(ctx, ix.vectors, ix.N, D, ix.mean, ix.basis, d, ix.proj);
-    } else {
-      DBuf<int32_t> xs(ix.nxe), ys(ix.eh - ix.w + 1);
-      std::vector<int32_t> hx(ix.nxe), hy(ix.eh - ix.w + 1);
-      for (int i = 0; i < ix.nxe; ++i) hx[i] = i;
-      for (int i = 0; i < ix.eh - ix.w + 1; ++i) hy[i] = i;
-      xs.upload(ctx, hx.data(), hx.size());
-      ys.upload(ctx, hy.data(), hy.size());
-      AnchorSet as{xs.p, ys.p, ix.nxe, ix.N};
-      launch_project_windows(ctx, ix.ex_mirror, ix.ew, ix.C, ix.w, as, ix.mean, ix.basis, d,
-                             ix.proj);
-      PSG_CUDA(cudaStreamSynchronize(ctx->stream));
-    }
-  }
-  phase("db projection");
-  // tree (host-native build over the device-projected points)
-  std::vector<double> hp((size_t)ix.N * d);
-  if (d > 0)
-    PSG_CUDA(cudaMemcpyAsync(hp.data(), ix.proj, sizeof(double) * hp.size(),
-                             cudaMemcpyDeviceToHost, ctx->stream));
-  PSG_CUDA(cudaStreamSynchronize(ctx->stream));
-  ix.htree = build_tree_host(hp.data(), ix.N, d, cfg.branching, cfg.max_depth,
-                             cfg.leaf_threshold > 0 ? cfg.leaf_threshold : cfg.branching, cfg.seed);
-  phase("tree build (host)");
+// Device copies of ix.htree (replacing any previous tree): exact fp64 tree
+// and leaf-ordered projected points, plus the conservative fp32 filter/bound
+// copies of the fast search kernels.
+void free_tree(Index& ix) {
+  DevTree& T = ix.tree;
+  for (void* p : {(void*)T.centroid, (void*)T.radius, (void*)T.first_child, (void*)T.n_children,
+                  (void*)T.leaf_start, (void*)T.leaf_count, (void*)T.centroid32,
+                  (void*)T.centroid32T, (void*)T.radius32, (void*)T.cnorm32, (void*)T.boxlo,
+                  (void*)T.boxhi, (void*)T.meta, (void*)T.tie, (void*)ix.perm, (void*)ix.proj_soa,
+                  (void*)ix.proj32_q4, (void*)ix.pnorm32})
+    cudaFree(p);
+  T = DevTree{};
+  ix.perm = nullptr;
+  ix.proj_soa = nullptr;
+  ix.proj32_q4 = nullptr;
+  ix.pnorm32 = nullptr;
+}
+
+void upload_tree(psg_ctx* ctx, Index& ix) {
+  free_tree(ix);
+  const int d = ix.d;
   const HostTree& t = ix.htree;
   const int nn = (int)t.radius.size();
   ix.tree.n_nodes = nn;
@@ -383,7 +343,76 @@ void finish_index(psg_ctx* ctx, Index& ix, const double* mean, const double* bas
     up(ix.tree.radius32, r32);
     up(ix.tree.cnorm32, n32);
   }
+  if (!t.tie.empty()) {
+    ix.tree.tie = dalloc<int32_t>(nn);
+    up(ix.tree.tie, t.tie);
+  }
   PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void finish_index(psg_ctx* ctx, Index& ix, const double* mean, const double* basis, int d,
+                  const psg_index_cfg& cfg) {
+  const int D = ix.D;
+  const bool verbose = std::getenv("PERSYN_VERBOSE") != nullptr;
+  double t_phase = now_ms();
+  auto phase = [&](const char* what) {
+    if (!verbose) return;
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    const double t = now_ms();
+    fprintf(stderr, "[persyn] index N=%lld D=%d: %s %.2f ms\n", (long long)ix.N, D, what, t - t_phase);
+    t_phase = t;
+  };
+  if (basis) {
+    if (d < 0 || d > 64) fail(PSG_E_DOMAIN, "injected PCA dimension must be in [0, 64]");
+    ix.h_mean.assign(mean, mean + D);
+    ix.h_basis.assign(basis, basis + (size_t)d * D);
+    ix.h_var.assign(D, 0.0);
+    ix.d = d;
+  } else {
+    fit_pca_device(ctx, ix, cfg);
+  }
+  d = ix.d;
+  phase("pca fit");
+  ix.mean = dalloc<double>(D);
+  PSG_CUDA(cudaMemcpyAsync(ix.mean, ix.h_mean.data(), sizeof(double) * D, cudaMemcpyHostToDevice,
+                           ctx->stream));
+  // transposed, zero-padded basis [D][KP] for the projection kernel
+  const int KP = d <= 32 ? 32 : 64;
+  std::vector<double> bt((size_t)D * KP, 0.0);
+  for (int k = 0; k < d; ++k)
+    for (int j = 0; j < D; ++j) bt[(size_t)j * KP + k] = ix.h_basis[(size_t)k * D + j];
+  ix.basis = dalloc<double>(bt.size());
+  PSG_CUDA(cudaMemcpyAsync(ix.basis, bt.data(), sizeof(double) * bt.size(), cudaMemcpyHostToDevice,
+                           ctx->stream));
+  // project the database (pca.cpp:103-113)
+  ix.proj = dalloc<double>((size_t)ix.N * (d > 0 ? d : 1));
+  if (d > 0) {
+    if (ix.from_vectors) {
+      launch_project_vectors(ctx, ix.vectors, ix.N, D, ix.mean, ix.basis, d, ix.proj);
+    } else {
+      DBuf<int32_t> xs(ix.nxe), ys(ix.eh - ix.w + 1);
+      std::vector<int32_t> hx(ix.nxe), hy(ix.eh - ix.w + 1);
+      for (int i = 0; i < ix.nxe; ++i) hx[i] = i;
+      for (int i = 0; i < ix.eh - ix.w + 1; ++i) hy[i] = i;
+      xs.upload(ctx, hx.data(), hx.size());
+      ys.upload(ctx, hy.data(), hy.size());
+      AnchorSet as{xs.p, ys.p, ix.nxe, ix.N};
+      launch_project_windows(ctx, ix.ex_mirror, ix.ew, ix.C, ix.w, as, ix.mean, ix.basis, d,
+                             ix.proj);
+      PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+  }
+  phase("db projection");
+  // tree (host-native build over the device-projected points)
+  std::vector<double> hp((size_t)ix.N * d);
+  if (d > 0)
+    PSG_CUDA(cudaMemcpyAsync(hp.data(), ix.proj, sizeof(double) * hp.size(),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+  PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+  ix.htree = build_tree_host(hp.data(), ix.N, d, cfg.branching, cfg.max_depth,
+                             cfg.leaf_threshold > 0 ? cfg.leaf_threshold : cfg.branching, cfg.seed);
+  phase("tree build (host)");
+  upload_tree(ctx, ix);
   phase("tree upload + search copies");
 }
 
@@ -1035,6 +1064,23 @@ psg_status psg_index_leaves(const psg_index* index, int32_t* ids, int32_t* sizes
   });
 }
 
+psg_status psg_index_import_tree(psg_ctx* ctx, psg_index* index, const psg_tree_import* tree) {
+  return guarded([&] {
+    psg::StreamScope _ss(ctx ? ctx->stream : nullptr);
+    if (!ctx || !index || !tree || !tree->n_children || !tree->leaf_sizes || !tree->leaf_ids)
+      fail(PSG_E_DOMAIN, "null argument");
+    psg::Index& ix = index->impl;
+    if (ix.d < 1) fail(PSG_E_DOMAIN, "tree import needs a PCA dimension >= 1");
+    std::vector<double> hp((size_t)ix.N * ix.d);
+    PSG_CUDA(cudaMemcpyAsync(hp.data(), ix.proj, sizeof(double) * hp.size(),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    ix.htree = psg::import_tree_host(hp.data(), ix.N, ix.d, tree->n_children, tree->n_nodes,
+                                     tree->leaf_sizes, tree->n_leaves, tree->leaf_ids);
+    psg::upload_tree(ctx, ix);
+  });
+}
+
 psg_status psg_index_histograms(const psg_index* index, double* mass) {
   return guarded([&] {
     const psg::Index& ix = index->impl;
@@ -1104,8 +1150,8 @@ psg_status psg_index_query(psg_ctx* ctx, const psg_index* index, const float* Q,
       psg::launch_rescore_vectors(ctx, q.p, nq, ix, id.p, dd.p);
     } else {
       // window index queried with explicit vectors: rescore against the
-      // materialised candidate row gathered from the exemplar
-      fail(PSG_E_DOMAIN, "psg_index_query needs a vector index; use psg_search_step for images");
+      // candidate window gathered from the exemplar
+      psg::launch_rescore_query_windows(ctx, q.p, nq, ix, id.p, dd.p);
     }
     id.download(ctx, idx, nq);
     dd.download(ctx, dist, nq);

@@ -407,4 +407,138 @@ HostTree build_tree_host(const double* P, int64_t N, int d, int branching, int m
   return t;
 }
 
+// Replay of an externally built tree (the reference's KmTree, recovered from
+// its public structure_json() + leaves(), km_tree.cpp:286-318).  Input:
+// child counts in pre-order DFS (children in the reference's order) and the
+// leaf member lists in DFS order.  Every node's id list is the ascending union
+// of its leaves (clusters preserve id order, km_tree.cpp:113-116), so centroid
+// and radius are recomputed with the reference's ordered fp64 loops
+// (km_tree.cpp:162-171).  The backtrack tie id is the reference's post-order
+// node id (km_tree.cpp:159,187-188).  Output layout: breadth-first,
+// contiguous children, like build_tree_host.
+HostTree import_tree_host(const double* P, int64_t N, int d, const int32_t* n_children_pre,
+                          int64_t n_nodes, const int32_t* leaf_sizes, int64_t n_leaves,
+                          const int32_t* leaf_ids) {
+  if (n_nodes < 1 || n_leaves < 1) fail(PSG_E_SHAPE, "tree import: empty tree");
+  struct PNode {
+    std::vector<int32_t> kids;  // pre-order indices of the children
+    int64_t leaf = -1;          // DFS leaf number
+    int32_t post = -1;
+    int depth = 0;
+  };
+  std::vector<PNode> pn((size_t)n_nodes);
+  // pre-order parse with an explicit stack of (node, children still expected)
+  int64_t leaf_no = 0, post = 0;
+  std::vector<std::pair<int64_t, int32_t>> st;
+  for (int64_t i = 0; i < n_nodes; ++i) {
+    const int32_t nc = n_children_pre[i];
+    if (nc < 0) fail(PSG_E_SHAPE, "tree import: negative child count");
+    if (i > 0) {
+      if (st.empty()) fail(PSG_E_SHAPE, "tree import: more nodes than the structure holds");
+      pn[(size_t)st.back().first].kids.push_back((int32_t)i);
+      pn[(size_t)i].depth = pn[(size_t)st.back().first].depth + 1;
+      --st.back().second;
+    }
+    if (nc == 0) {
+      if (leaf_no >= n_leaves) fail(PSG_E_SHAPE, "tree import: more leaves than leaf lists");
+      pn[(size_t)i].leaf = leaf_no++;
+      pn[(size_t)i].post = (int32_t)post++;
+    } else {
+      st.emplace_back(i, nc);
+    }
+    while (!st.empty() && st.back().second == 0) {  // subtree complete: post-order id
+      pn[(size_t)st.back().first].post = (int32_t)post++;
+      st.pop_back();
+    }
+  }
+  if (!st.empty() || leaf_no != n_leaves)
+    fail(PSG_E_SHAPE, "tree import: structure and leaf lists disagree");
+  // leaf lists, ids must form a permutation of [0, N)
+  std::vector<int64_t> loff((size_t)n_leaves + 1, 0);
+  for (int64_t l = 0; l < n_leaves; ++l) {
+    if (leaf_sizes[l] < 1) fail(PSG_E_SHAPE, "tree import: empty leaf");
+    loff[(size_t)l + 1] = loff[(size_t)l] + leaf_sizes[l];
+  }
+  if (loff.back() != N) fail(PSG_E_SHAPE, "tree import: leaves do not hold N points");
+  {
+    std::vector<char> seen((size_t)N, 0);
+    for (int64_t i = 0; i < N; ++i) {
+      const int32_t id = leaf_ids[i];
+      if (id < 0 || id >= N || seen[(size_t)id]) fail(PSG_E_SHAPE, "tree import: ids are not a permutation");
+      seen[(size_t)id] = 1;
+    }
+  }
+  // breadth-first relayout
+  std::vector<int64_t> order;  // BFS position -> pre-order index
+  order.reserve((size_t)n_nodes);
+  order.push_back(0);
+  std::vector<int32_t> bfs_of((size_t)n_nodes, -1);
+  for (size_t h = 0; h < order.size(); ++h) {
+    bfs_of[(size_t)order[h]] = (int32_t)h;
+    for (int32_t c : pn[(size_t)order[h]].kids) order.push_back(c);
+  }
+  // ascending id list per node, bottom-up (reverse BFS: children first)
+  std::vector<std::vector<int32_t>> ids((size_t)n_nodes);
+  for (int64_t h = n_nodes - 1; h >= 0; --h) {
+    const PNode& nd = pn[(size_t)order[(size_t)h]];
+    auto& v = ids[(size_t)h];
+    if (nd.leaf >= 0) {
+      v.assign(leaf_ids + loff[(size_t)nd.leaf], leaf_ids + loff[(size_t)nd.leaf + 1]);
+      std::sort(v.begin(), v.end());
+    } else {
+      for (int32_t c : nd.kids) {
+        const auto& cv = ids[(size_t)bfs_of[(size_t)c]];
+        v.insert(v.end(), cv.begin(), cv.end());
+      }
+      std::sort(v.begin(), v.end());
+    }
+  }
+  HostTree t;
+  const size_t nn = (size_t)n_nodes;
+  t.centroid.assign(nn * (size_t)d, 0.0);
+  t.radius.assign(nn, 0.0);
+  t.first_child.assign(nn, -1);
+  t.n_children.assign(nn, 0);
+  t.leaf_start.assign(nn, 0);
+  t.leaf_count.assign(nn, 0);
+  t.depth.assign(nn, 0);
+  t.tie.assign(nn, 0);
+  t.boxlo.assign(nn * kBoxDims, 0.0);
+  t.boxhi.assign(nn * kBoxDims, 0.0);
+  const int KB = std::min(d, kBoxDims);
+  for (size_t h = 0; h < nn; ++h) {
+    const PNode& nd = pn[(size_t)order[h]];
+    const auto& v = ids[h];
+    double* c = t.centroid.data() + h * d;
+    for (int32_t id : v)
+      for (int j = 0; j < d; ++j) c[j] += P[(size_t)id * d + j];
+    for (int j = 0; j < d; ++j) c[j] /= (double)v.size();
+    double r = 0.0;
+    for (int32_t id : v) r = std::max(r, std::sqrt(dist2(P + (size_t)id * d, c, d)));
+    t.radius[h] = r;
+    for (int j = 0; j < KB; ++j) {
+      double mn = P[(size_t)v[0] * d + j], mx = mn;
+      for (int32_t id : v) {
+        mn = std::min(mn, P[(size_t)id * d + j]);
+        mx = std::max(mx, P[(size_t)id * d + j]);
+      }
+      t.boxlo[h * kBoxDims + j] = mn;
+      t.boxhi[h * kBoxDims + j] = mx;
+    }
+    t.depth[h] = nd.depth;
+    t.max_depth = std::max(t.max_depth, nd.depth);
+    t.tie[h] = nd.post;
+    if (!nd.kids.empty()) {
+      t.first_child[h] = bfs_of[(size_t)nd.kids[0]];
+      t.n_children[h] = (int32_t)nd.kids.size();
+    } else {
+      t.leaf_start[h] = (int32_t)t.perm.size();
+      t.leaf_count[h] = (int32_t)v.size();
+      t.perm.insert(t.perm.end(), v.begin(), v.end());
+      t.n_leaves++;
+    }
+  }
+  return t;
+}
+
 }  // namespace psg

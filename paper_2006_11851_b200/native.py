@@ -27,6 +27,11 @@ PSG_OK, PSG_E_DOMAIN, PSG_E_SHAPE, PSG_E_LOGIC, PSG_E_IO, PSG_E_FORMAT, PSG_E_CU
 PSG_GREEDY, PSG_BACKTRACK, PSG_EXACT = 0, 1, 2
 
 
+class psg_tree_import(ct.Structure):
+    _fields_ = [("n_nodes", ct.c_int64), ("n_children", ct.c_void_p), ("n_leaves", ct.c_int64),
+                ("leaf_sizes", ct.c_void_p), ("leaf_ids", ct.c_void_p)]
+
+
 class psg_budget(ct.Structure):
     _fields_ = [("mode", ct.c_int), ("max_leaves", ct.c_int)]
 
@@ -106,6 +111,7 @@ _SIGS = {
     "psg_index_projected": (I, [VP, VP]),
     "psg_index_leaves": (I, [VP, VP, VP, VP]),
     "psg_index_histograms": (I, [VP, VP]),
+    "psg_index_import_tree": (I, [VP, VP, VP]),
     "psg_index_query": (I, [VP, VP, VP, I64, psg_budget, VP, VP, VP, VP]),
     "psg_search_step": (I, [VP, VP, VP, I, I, I, I, psg_budget, VP, VP, VP, VP]),
     "psg_update_step": (I, [VP, VP, VP, VP, VP, I, I, I, VP]),
