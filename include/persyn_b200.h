@@ -139,6 +139,20 @@ psg_status psg_index_create(psg_ctx* ctx, const double* ex_planes, int C, int ew
 psg_status psg_index_create_vectors(psg_ctx* ctx, const float* X, int64_t n, int D,
                                     const double* mean, const double* basis, int d,
                                     const psg_index_cfg* cfg, psg_index** out);
+/*
+ * Replaces make_brute_force_index(extract_all(exemplar, {w,1,..}))
+ * (optimizer.hpp:122-129, optimizer.cpp:168-212, the pixel-brute bench mode
+ * persyn_main.cpp:205-212): exact full-D nearest neighbour, the first index of
+ * the minimum fp64 dist^2; QueryBudget is ignored; points_scanned = N per
+ * query.  Computed as a tf32 tensor-core distance filter with exact fp64
+ * re-evaluation of the survivors (bit-identical result).  hist_bins > 0 also
+ * builds the exemplar histogram used by optimize_level.
+ */
+psg_status psg_index_create_brute(psg_ctx* ctx, const double* ex_planes, int C, int ew, int eh,
+                                  int w, int hist_bins, int hist_include_scale, psg_index** out);
+/* Same over an explicit fp32 candidate set X[n][D]. */
+psg_status psg_index_create_brute_vectors(psg_ctx* ctx, const float* X, int64_t n, int D,
+                                          psg_index** out);
 void psg_index_destroy(psg_index* index);
 /* dims: {N, D, d, C, w, ew, eh, n_nodes, n_leaves, max_depth_built} */
 psg_status psg_index_info(const psg_index* index, int64_t dims[10]);

@@ -269,6 +269,29 @@ def make_pca_tree_index(exemplar: np.ndarray, window: int, variance_target: floa
     return SearchIndex(ctx, h, None)
 
 
+def make_brute_force_index(exemplar: np.ndarray, window: int, *, hist_bins: int = 0,
+                           hist_include_scale: bool = False,
+                           ctx: Optional[Context] = None) -> SearchIndex:
+    """make_brute_force_index(extract_all(exemplar, {w,1,..})) (optimizer.cpp:168-212)."""
+    ctx = ctx or default_context()
+    ex = _c(exemplar, np.float64)
+    C, eh, ew = ex.shape
+    h = ct.c_void_p()
+    N.check(N.lib.psg_index_create_brute(ctx.h, _p(ex), C, ew, eh, window, hist_bins,
+                                         int(hist_include_scale), ct.byref(h)))
+    return SearchIndex(ctx, h, None)
+
+
+def make_brute_force_vector_index(X: np.ndarray, *, ctx: Optional[Context] = None) -> SearchIndex:
+    """make_brute_force_index over an explicit candidate matrix X[n][D]."""
+    ctx = ctx or default_context()
+    X = _c(X, np.float32)
+    h = ct.c_void_p()
+    N.check(N.lib.psg_index_create_brute_vectors(ctx.h, _p(X), X.shape[0], X.shape[1],
+                                                 ct.byref(h)))
+    return SearchIndex(ctx, h, None)
+
+
 def make_vector_index(X: np.ndarray, variance_target: float = 0.95, branching: int = 8,
                       seed: int = 0, *, mean=None, basis=None, d_fixed: int = 0,
                       max_depth: int = 0, ctx: Optional[Context] = None) -> SearchIndex:

@@ -97,7 +97,30 @@ struct Index {
   int hist_bins = 0, hist_slots = 0;
   std::vector<double> h_ex_hist;
   double* ex_hist = nullptr;
+  // brute-force index (BruteForceIndex, optimizer.cpp:168-212): tensor-core
+  // filter operand, tf32-rounded centred rows in UMMA tiles + norms
+  bool brute = false;
+  int brute_nch = 0;            // K chunks of 32 fp32
+  int brute_ptiles = 0;         // 256-point tiles
+  float* brute_op = nullptr;    // [ptiles][nch][256 * 32]
+  float* brute_n2 = nullptr;    // [ptiles * 256] |p - mu|^2 (fp32)
+  float* brute_nup = nullptr;   // [ptiles * 256] |p - mu| rounded up
+  float* brute_mu = nullptr;    // [nch * 32] centring vector
   ~Index();
+};
+
+// A set of fp32 rows read in the reference's feature order: explicit vectors
+// [n][D], or w x w windows of an fp32 mirror [H][img_w][C] (pixel-major,
+// channel-minor, neighborhood.cpp:128-135) at anchors (xs[r % nx], ys[r / nx])
+// — or the dense lattice (r % nx, r / nx) when xs is null.
+struct RowSrc {
+  const float* base = nullptr;
+  int kind = 0;  // 0 = vectors, 1 = windows
+  int D = 0;
+  int img_w = 0, C = 0, w = 0;
+  const int32_t* xs = nullptr;
+  const int32_t* ys = nullptr;
+  int nx = 1;
 };
 
 }  // namespace psg
@@ -193,6 +216,12 @@ struct SearchArgs {
   int32_t* out_visited;     // optional: nodes visited (QueryStats, km_tree.hpp:27-30)
   int* flags;
 };
+// Brute-force index: build the filter operand once per index; exact search of
+// nq query rows (lexicographic min of (fp64 dist^2, id), optimizer.cpp:175-205).
+void brute_prepare(psg_ctx* ctx, Index& ix);
+void launch_brute_search(psg_ctx* ctx, const Index& ix, const RowSrc& qsrc, int64_t nq,
+                         int32_t* out_idx, double* out_d2, int64_t* out_scanned,
+                         int64_t* out_exact);
 void launch_search(psg_ctx* ctx, const SearchArgs& a);
 // tcgen05 (UMMA) tile search; returns false when the tree shape is unsupported.
 bool launch_search_mma(psg_ctx* ctx, const SearchArgs& a);

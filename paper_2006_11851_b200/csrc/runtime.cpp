@@ -237,6 +237,10 @@ Index::~Index() {
   cudaFree(tree.tie);
   cudaFree(pnorm32);
   cudaFree(ex_hist);
+  cudaFree(brute_op);
+  cudaFree(brute_n2);
+  cudaFree(brute_nup);
+  cudaFree(brute_mu);
 }
 
 // ---------------------------------------------------------------------------
@@ -651,6 +655,23 @@ void level_search(psg_level& L, bool seeded, int32_t* out_idx, double* out_dist)
   psg_ctx* ctx = L.ctx;
   const Index& ix = *L.ix;
   const AnchorSet as = owned_anchors(L);
+  if (ix.brute) {  // BruteForceIndex: exact full-D scan on the tensor cores
+    RowSrc qs;
+    qs.base = L.mirror.p;
+    qs.kind = 1;
+    qs.img_w = L.W;
+    qs.C = L.C;
+    qs.w = L.w;
+    qs.xs = as.xs;
+    qs.ys = as.ys;
+    qs.nx = as.nx;
+    launch_brute_search(ctx, ix, qs, L.Ao, out_idx + L.off, L.d2.p, L.scanned.p, L.exact_evals.p);
+    PSG_CUDA(cudaMemsetAsync(L.visited.p, 0, sizeof(int32_t) * L.Ao, ctx->stream));
+    launch_rescore_windows(ctx, L.mirror.p, L.W, L.C, L.w, as, ix, out_idx + L.off,
+                           out_dist + L.off);
+    L.unique_queries += L.Ao;
+    return;
+  }
   if (ix.d > 0)
     launch_project_windows(ctx, L.mirror.p, L.W, L.C, L.w, as, ix.mean, ix.basis, ix.d, L.qproj.p);
   SearchArgs a{};
@@ -1016,6 +1037,61 @@ psg_status psg_index_create_vectors(psg_ctx* ctx, const float* X, int64_t n, int
   });
 }
 
+psg_status psg_index_create_brute(psg_ctx* ctx, const double* ex_planes, int C, int ew, int eh,
+                                  int w, int hist_bins, int hist_include_scale, psg_index** out) {
+  return guarded([&] {
+    psg::StreamScope _ss(ctx ? ctx->stream : nullptr);
+    if (!ctx || !ex_planes || !out) fail(PSG_E_DOMAIN, "null argument");
+    *out = nullptr;
+    if (ew < 1 || eh < 1) fail(PSG_E_DOMAIN, "empty exemplar");
+    if (C < 4 || C > 8) fail(PSG_E_SHAPE, "channels must be 3 + G with G in [1, 5]");
+    if (w < 2 || w % 2) fail(PSG_E_DOMAIN, "neighborhood width must be even and >= 2");
+    if (ew < w || eh < w) fail(PSG_E_DOMAIN, "exemplar smaller than the neighborhood window");
+    psg::DBuf<double> ex((size_t)C * ew * eh);
+    ex.upload(ctx, ex_planes, ex.n);
+    auto h = std::make_unique<psg_index>();
+    psg::Index& ix = h->impl;
+    ix.ctx = ctx;
+    ix.brute = true;
+    ix.C = C;
+    ix.w = w;
+    ix.ew = ew;
+    ix.eh = eh;
+    ix.D = w * w * C;
+    ix.nxe = ew - w + 1;
+    ix.N = (int64_t)ix.nxe * (eh - w + 1);
+    ix.ex_mirror = psg::dalloc<float>((size_t)ew * eh * C);
+    psg::launch_make_mirror(ctx, ex.p, C, ew, eh, ix.ex_mirror);
+    psg::build_exemplar_hist(ctx, ix, ex.p, hist_bins, hist_include_scale);
+    psg::brute_prepare(ctx, ix);
+    *out = h.release();
+  });
+}
+
+psg_status psg_index_create_brute_vectors(psg_ctx* ctx, const float* X, int64_t n, int D,
+                                          psg_index** out) {
+  return guarded([&] {
+    psg::StreamScope _ss(ctx ? ctx->stream : nullptr);
+    if (!ctx || !X || !out) fail(PSG_E_DOMAIN, "null argument");
+    *out = nullptr;
+    if (n < 1) fail(PSG_E_DOMAIN, "empty candidate set");  // optimizer.cpp:171
+    if (D < 1) fail(PSG_E_DOMAIN, "vector dimension must be >= 1");
+    auto h = std::make_unique<psg_index>();
+    psg::Index& ix = h->impl;
+    ix.ctx = ctx;
+    ix.brute = true;
+    ix.from_vectors = true;
+    ix.D = D;
+    ix.N = n;
+    ix.nxe = 1;
+    ix.vectors = psg::dalloc<float>((size_t)n * D);
+    PSG_CUDA(cudaMemcpyAsync(ix.vectors, X, sizeof(float) * (size_t)n * D, cudaMemcpyHostToDevice,
+                             ctx->stream));
+    psg::brute_prepare(ctx, ix);
+    *out = h.release();
+  });
+}
+
 void psg_index_destroy(psg_index* index) { delete index; }
 
 psg_status psg_index_info(const psg_index* index, int64_t dims[10]) {
@@ -1103,6 +1179,13 @@ psg_status psg_index_query(psg_ctx* ctx, const psg_index* index, const float* Q,
     psg::DBuf<double> qp((size_t)nq * (ix.d > 0 ? ix.d : 1)), d2(nq), dd(nq);
     psg::DBuf<int32_t> id(nq);
     psg::DBuf<int64_t> sc(nq);
+    if (ix.brute) {
+      psg::RowSrc qs;
+      qs.base = q.p;
+      qs.kind = 0;
+      qs.D = ix.D;
+      psg::launch_brute_search(ctx, ix, qs, nq, id.p, d2.p, sc.p, nullptr);
+    }
     if (ix.d > 0) psg::launch_project_vectors(ctx, q.p, nq, ix.D, ix.mean, ix.basis, ix.d, qp.p);
     psg::SearchArgs a{};
     a.q = qp.p;
@@ -1123,7 +1206,9 @@ psg_status psg_index_query(psg_ctx* ctx, const psg_index* index, const float* Q,
     a.out_scanned = sc.p;
     a.flags = ctx->d_flags;
     const bool reorder = budget.mode == PSG_EXACT && nq >= 64 && ix.d > 0 && !ctx->legacy_search;
-    if (reorder) {
+    if (ix.brute) {
+      // searched above (the budget does not apply, optimizer.cpp:172-173)
+    } else if (reorder) {
       // tiles of 32 queries share a traversal: give them neighbours in the tree
       psg::DBuf<uint32_t> k0(nq), k1(nq);
       psg::DBuf<int32_t> o0(nq), o1(nq), id_s(nq);
