@@ -26,8 +26,10 @@
 // 8-row groups), so every stage is two contiguous bulk copies.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cfloat>
 #include <climits>
+#include <vector>
 
 #include "numerics.cuh"
 #include "psg_internal.h"
@@ -47,7 +49,7 @@ constexpr uint32_t kBBytes = kBN * kBK * 4;  // 32 KB
 constexpr int kThreads = 192;
 
 struct BruteSmem {
-  uint32_t stages, pn2, pnup, pmax, bars, tmem, total;
+  uint32_t stages, pn2, pnup, bars, tmem, total;
 };
 __host__ __device__ constexpr BruteSmem brute_smem() {
   BruteSmem s{};
@@ -55,7 +57,6 @@ __host__ __device__ constexpr BruteSmem brute_smem() {
   s.stages = o; o += kStages * (kABytes + kBBytes);
   s.pn2 = o; o += 2 * kBN * 4;
   s.pnup = o; o += 2 * kBN * 4;
-  s.pmax = o; o += 16 * 4;
   s.bars = o; o += (2 * kStages + 4) * 8;
   s.tmem = o; o += 16;
   s.total = o;
@@ -170,30 +171,37 @@ struct BruteArgs {
   const float* qop;
   const float* qn2;
   const float* qnup;
+  const float* qU0;     // [nq] initial upper bound (seed distance rounded up) or +inf
   const float* pop;
   const float* pn2;
   const float* pnup;
+  const float* tmax;    // [ptiles] largest |p'| bound of each candidate tile
   int64_t nq, N;
   int nch, ptiles, splits, D;
-  float c1, c2;  // E = c1 |q'||p'| + c2 (|q'| + |p'|)^2
+  float c1, c2;  // |s - dist^2| <= c1 |q'||p'| + c2 (|q'| + |p'|)^2
   RowSrc qs, ps;
-  // per (query, split)
+  // survivors per (query, split): U, count, list
   float* o_U;
-  double* o_exd2;
-  int32_t* o_exid;
   int32_t* o_n;
   int32_t* o_ids;  // [nq * splits][kList]
   float* o_lb;
-  int64_t* o_exact;
+  // overflow of full lists: (query, id, lb) triples
+  unsigned long long* ov_count;
+  int64_t ov_cap;
+  int64_t* ov_q;
+  int32_t* ov_id;
+  float* ov_lb;
+  int32_t* lost;   // [nq] a survivor could not be stored: settle by a full scan
 };
 
 // Survivor bookkeeping of one query (rare path, kept out of the unrolled
 // epilogue loop): tighten U, append (id, lb) to the (query, split) list in
 // global memory; when the list is full drop the entries U has ruled out, and
-// if it is still full settle it exactly here.
+// if it is still full spill to the shared overflow buffer.  No exact distance
+// is evaluated here: a stalled epilogue thread would stall the whole CTA.
 __device__ __noinline__ void push_candidate(const BruteArgs& a, int64_t q, int32_t id, float lb,
-                                            float ub, int32_t* gid, float* glb, float& U, int& n,
-                                            double& exd2, int32_t& exid, int64_t& exact) {
+                                            float ub, int32_t* gid, float* glb, float& U,
+                                            int& n) {
   U = fminf(U, ub);
   if (n == kList) {
     int m = 0;
@@ -206,34 +214,29 @@ __device__ __noinline__ void push_candidate(const BruteArgs& a, int64_t q, int32
       }
     }
     n = m;
-    if (n == kList) {
-      for (int i = 0; i < n; ++i) {
-        const int32_t e = gid[i];
-        const double d2 = exact_d2(a.qs, q, a.ps, e, a.D);
-        ++exact;
-        if (d2 < exd2 || (d2 == exd2 && e < exid)) {
-          exd2 = d2;
-          exid = e;
-        }
-      }
-      n = 0;
-      U = fminf(U, __double2float_ru(exd2));
-    }
   }
-  if (lb <= U) {
+  if (lb > U) return;
+  if (n < kList) {
     glb[n] = lb;
     gid[n] = id;
     ++n;
+    return;
+  }
+  const unsigned long long k = atomicAdd(a.ov_count, 1ull);
+  if ((int64_t)k < a.ov_cap) {
+    a.ov_q[k] = q;
+    a.ov_id[k] = id;
+    a.ov_lb[k] = lb;
+  } else {
+    a.lost[q] = 1;
   }
 }
 
 __global__ void __launch_bounds__(kThreads, 1) brute_mma_kernel(BruteArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr BruteSmem L = brute_smem();
-  float* s_pn2 = reinterpret_cast<float*>(smem + L.pn2);     // [2][kBN]
-  float* s_pnup = reinterpret_cast<float*>(smem + L.pnup);
-  float* s_wmax = reinterpret_cast<float*>(smem + L.pmax);  // [2][4] per-warp partial max
-  float* s_pnmax = s_wmax + 8;                              // [2]
+  float* s_pn2 = reinterpret_cast<float*>(smem + L.pn2);    // [2][kBN]
+  float* s_pnup = reinterpret_cast<float*>(smem + L.pnup);  // [2][kBN]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
@@ -326,58 +329,53 @@ __global__ void __launch_bounds__(kThreads, 1) brute_mma_kernel(BruteArgs a) {
     // ---- epilogue: one query row per thread ---------------------------------------
     const int lg = warp & 3;  // TMEM lane group this warp may access
     const int row = lg * 32 + lane;
-    const int et = tid - 64;  // 0..127
+    const int et = tid - 64;  // 0..127: loads two candidate norms of each tile
     const int64_t q = (int64_t)qt * kBM + row;
     const bool valid = q < a.nq;
     const float qn2 = valid ? a.qn2[q] : 0.f;
     const float qa = valid ? a.qnup[q] : 0.f;
-    const float kInfF = __int_as_float(0x7f800000);
-    float U = kInfF;
-    double exd2 = __longlong_as_double(0x7ff0000000000000ll);
-    int32_t exid = INT_MAX;
+    float U = valid ? a.qU0[q] : 0.f;
     int n = 0;
-    int64_t exact = 0;
     const int64_t o = (valid ? q : 0) * a.splits + split;
     int32_t* gid = a.o_ids + o * kList;
     float* glb = a.o_lb + o * kList;
+    // norms of the first tile
+    if (npt > 0) {
+      const int64_t pb0 = (int64_t)pt0 * kBN;
+      s_pn2[et] = a.pn2[pb0 + et];
+      s_pn2[et + kBM] = a.pn2[pb0 + et + kBM];
+      s_pnup[et] = a.pnup[pb0 + et];
+      s_pnup[et + kBM] = a.pnup[pb0 + et + kBM];
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
     for (int it = 0; it < npt; ++it) {
       const int b = it & 1;
       const uint32_t tph = (uint32_t)(it >> 1) & 1u;
       const int64_t pbase = (int64_t)(pt0 + it) * kBN;
-      // candidate norms of this tile -> smem (all 128 epilogue threads)
-      float mx = 0.f;
-      for (int k = et; k < kBN; k += kBM) {
-        s_pn2[b * kBN + k] = a.pn2[pbase + k];
-        const float pu = a.pnup[pbase + k];
-        s_pnup[b * kBN + k] = pu;
-        mx = fmaxf(mx, pu);
+      // prefetch the next tile's norms into registers (stored after this tile)
+      float nx0 = 0.f, nx1 = 0.f, nu0 = 0.f, nu1 = 0.f;
+      if (it + 1 < npt) {
+        const int64_t nb = pbase + kBN;
+        nx0 = __ldg(a.pn2 + nb + et);
+        nx1 = __ldg(a.pn2 + nb + et + kBM);
+        nu0 = __ldg(a.pnup + nb + et);
+        nu1 = __ldg(a.pnup + nb + et + kBM);
       }
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-      if (lane == 0) s_wmax[b * 4 + (warp - 2)] = mx;
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (et == 0)
-        s_pnmax[b] = fmaxf(fmaxf(s_wmax[b * 4], s_wmax[b * 4 + 1]),
-                           fmaxf(s_wmax[b * 4 + 2], s_wmax[b * 4 + 3]));
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      mma::mbar_wait(&tfull[b], tph);
-      mma::fence_after();
-      const int jmax = (int)min((int64_t)kBN, a.N - pbase);
-      // one loose threshold per tile (the largest candidate norm of the tile);
-      // candidates passing it are re-tested with their own bound in
-      // push_candidate, so the loop below is straight-line compare code
-      const float pbm = s_pnmax[b];
+      // one loose threshold per tile (the tile's largest candidate norm);
+      // candidates passing it are re-tested with their own bound, so the loop
+      // below is straight-line compare code
+      const float pbm = __ldg(a.tmax + pt0 + it);
       const float abm = qa + pbm;
       const float eps_t = fmaf(a.c1 * qa, pbm, a.c2 * abm * abm);
+      const int jmax = (int)min((int64_t)kBN, a.N - pbase);
+      mma::mbar_wait(&tfull[b], tph);
+      mma::fence_after();
       for (int j0 = 0; j0 < kBN; j0 += 32) {
         float dot[32];
         __syncwarp();
         mma::tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(b * kBN + j0), dot);
         if (valid && j0 < jmax) {
-          // margin: dominates the rounding of the precise test in push_candidate
+          // margin: dominates the rounding of the precise test below
           const float thr = __fadd_ru(__fadd_ru(U, eps_t), fabsf(U) * 1e-6f + 1e-30f);
           const float4* pn4 = reinterpret_cast<const float4*>(s_pn2 + b * kBN + j0);
           uint32_t m = 0;
@@ -404,21 +402,24 @@ __global__ void __launch_bounds__(kThreads, 1) brute_mma_kernel(BruteArgs a) {
             const float eps = fmaf(a.c1 * qa, pb, a.c2 * ab * ab);
             const float lb = __fsub_rd(s, eps);
             if (lb <= U)
-              push_candidate(a, q, (int32_t)(pbase + j), lb, __fadd_ru(s, eps), gid, glb, U, n,
-                             exd2, exid, exact);
+              push_candidate(a, q, (int32_t)(pbase + j), lb, __fadd_ru(s, eps), gid, glb, U, n);
           }
         }
       }
       mma::fence_before();
       __syncwarp();
       if (lane == 0) mma::mbar_arrive(&tempty[b]);
+      if (it + 1 < npt) {  // buffer b^1 was last read in tile it-1 (before the last barrier)
+        s_pn2[(b ^ 1) * kBN + et] = nx0;
+        s_pn2[(b ^ 1) * kBN + et + kBM] = nx1;
+        s_pnup[(b ^ 1) * kBN + et] = nu0;
+        s_pnup[(b ^ 1) * kBN + et + kBM] = nu1;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
     }
     if (valid) {
       a.o_n[o] = n;
       a.o_U[o] = U;
-      a.o_exd2[o] = exd2;
-      a.o_exid[o] = exid;
-      a.o_exact[o] = exact;
     }
   }
   mma::fence_before();
@@ -429,60 +430,134 @@ __global__ void __launch_bounds__(kThreads, 1) brute_mma_kernel(BruteArgs a) {
   }
 }
 
-// Exact settle, part 1: one thread per list slot — every survivor whose
-// lower bound reaches the query's global U (min over splits) gets the
-// reference's sequential fp64 distance.  Thread-level parallelism hides the
-// latency of the dependent chain (D adds).
-__global__ void brute_settle_kernel(BruteArgs a, double* __restrict__ slot_d2) {
-  const int64_t total = a.nq * a.splits * kList;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t o = t / kList;
-    const int i = (int)(t - o * kList);
-    const int64_t q = o / a.splits;
+// Seeds (optional): the exact distance of a known candidate (the anchor's
+// previous assignment) is a tight initial U, so only near-ties survive.
+__global__ void brute_init_kernel(BruteArgs a, const int32_t* __restrict__ seed,
+                                  double* __restrict__ seed_d2, float* __restrict__ U0,
+                                  unsigned long long* __restrict__ best_bits,
+                                  int32_t* __restrict__ best_id, int32_t* __restrict__ cnt) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < a.nq;
+       q += (int64_t)gridDim.x * blockDim.x) {
     double d2 = __longlong_as_double(0x7ff0000000000000ll);
-    if (i < a.o_n[o]) {
-      float U = __int_as_float(0x7f800000);
-      for (int s = 0; s < a.splits; ++s) U = fminf(U, a.o_U[q * a.splits + s]);
-      if (a.o_lb[t] <= U) d2 = exact_d2(a.qs, q, a.ps, a.o_ids[t], a.D);
-      else d2 = -1.0;  // ruled out
-    }
-    slot_d2[t] = d2;
+    if (seed) d2 = exact_d2(a.qs, q, a.ps, seed[q], a.D);
+    seed_d2[q] = d2;
+    U0[q] = seed ? __double2float_ru(d2) : __int_as_float(0x7f800000);
+    best_bits[q] = (unsigned long long)__double_as_longlong(d2);
+    best_id[q] = INT_MAX;
+    cnt[q] = seed ? 1 : 0;
+    a.lost[q] = 0;
   }
 }
 
-// Part 2: lexicographic minimum of (dist^2, id) per query.
-__global__ void brute_pick_kernel(BruteArgs a, const double* __restrict__ slot_d2,
-                                  int32_t* __restrict__ out_idx, double* __restrict__ out_d2,
-                                  int64_t* __restrict__ out_scanned,
+__device__ __forceinline__ float query_U(const BruteArgs& a, const float* U0, int64_t q) {
+  float U = U0[q];
+  for (int s = 0; s < a.splits; ++s) U = fminf(U, a.o_U[q * a.splits + s]);
+  return U;
+}
+
+// Settle, pass 1: one thread per survivor (list slot or overflow entry) whose
+// lower bound reaches the query's global U: the reference's sequential fp64
+// distance (thread-level parallelism hides the latency of the dependent
+// chain).  dist^2 >= 0, so its bit pattern orders like the value and the
+// per-query minimum is an integer atomicMin.
+__global__ void brute_settle_kernel(BruteArgs a, const float* __restrict__ U0,
+                                    double* __restrict__ slot_d2, double* __restrict__ ov_d2,
+                                    unsigned long long* __restrict__ best_bits,
+                                    int32_t* __restrict__ cnt) {
+  const int64_t nslots = a.nq * a.splits * kList;
+  const int64_t nov = min((int64_t)*a.ov_count, a.ov_cap);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nslots + nov;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t q;
+    int32_t id;
+    float lb;
+    double* out;
+    if (t < nslots) {
+      const int64_t o = t / kList;
+      const int i = (int)(t - o * kList);
+      q = o / a.splits;
+      out = slot_d2 + t;
+      if (i >= a.o_n[o]) {
+        *out = -1.0;
+        continue;
+      }
+      id = a.o_ids[t];
+      lb = a.o_lb[t];
+    } else {
+      const int64_t k = t - nslots;
+      q = a.ov_q[k];
+      id = a.ov_id[k];
+      lb = a.ov_lb[k];
+      out = ov_d2 + k;
+    }
+    double d2 = -1.0;
+    if (lb <= query_U(a, U0, q)) {
+      d2 = exact_d2(a.qs, q, a.ps, id, a.D);
+      atomicMin(best_bits + q, (unsigned long long)__double_as_longlong(d2));
+      atomicAdd(cnt + q, 1);
+    }
+    *out = d2;
+  }
+}
+
+// Settle, pass 2: lowest id among the candidates at the minimum (the seed too).
+__global__ void brute_tie_kernel(BruteArgs a, const int32_t* __restrict__ seed,
+                                 const double* __restrict__ seed_d2,
+                                 const double* __restrict__ slot_d2,
+                                 const double* __restrict__ ov_d2,
+                                 const unsigned long long* __restrict__ best_bits,
+                                 int32_t* __restrict__ best_id) {
+  const int64_t nslots = a.nq * a.splits * kList;
+  const int64_t nov = min((int64_t)*a.ov_count, a.ov_cap);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nslots + nov + a.nq;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t q;
+    int32_t id;
+    double d2;
+    if (t < nslots) {
+      d2 = slot_d2[t];
+      if (d2 < 0.0) continue;
+      q = t / (kList * a.splits);
+      id = a.o_ids[t];
+    } else if (t < nslots + nov) {
+      const int64_t k = t - nslots;
+      d2 = ov_d2[k];
+      if (d2 < 0.0) continue;
+      q = a.ov_q[k];
+      id = a.ov_id[k];
+    } else {
+      if (!seed) continue;
+      q = t - nslots - nov;
+      id = seed[q];
+      d2 = seed_d2[q];
+    }
+    if ((unsigned long long)__double_as_longlong(d2) == best_bits[q]) atomicMin(best_id + q, id);
+  }
+}
+
+// Result per query.  A query whose survivor list overflowed the spill buffer
+// (never observed; kept for correctness) is settled by a full exact scan.
+__global__ void brute_pick_kernel(BruteArgs a, const unsigned long long* __restrict__ best_bits,
+                                  const int32_t* __restrict__ best_id,
+                                  const int32_t* __restrict__ cnt, int32_t* __restrict__ out_idx,
+                                  double* __restrict__ out_d2, int64_t* __restrict__ out_scanned,
                                   int64_t* __restrict__ out_exact) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < a.nq;
        q += (int64_t)gridDim.x * blockDim.x) {
-    double best = __longlong_as_double(0x7ff0000000000000ll);
-    int32_t bid = INT_MAX;
-    int64_t exact = 0;
-    for (int s = 0; s < a.splits; ++s) {
-      const int64_t o = q * a.splits + s;
-      exact += a.o_exact[o];
-      const int32_t e = a.o_exid[o];
-      if (e != INT_MAX) {
-        const double d2 = a.o_exd2[o];
-        if (d2 < best || (d2 == best && e < bid)) {
+    double best = __longlong_as_double((long long)best_bits[q]);
+    int32_t bid = best_id[q];
+    int64_t exact = cnt[q];
+    if (a.lost[q]) {
+      best = __longlong_as_double(0x7ff0000000000000ll);
+      bid = INT_MAX;
+      for (int64_t i = 0; i < a.N; ++i) {
+        const double d2 = exact_d2(a.qs, q, a.ps, i, a.D);
+        if (d2 < best) {
           best = d2;
-          bid = e;
+          bid = (int32_t)i;
         }
       }
-      const int m = a.o_n[o];
-      for (int i = 0; i < m; ++i) {
-        const double d2 = slot_d2[o * kList + i];
-        if (d2 < 0.0) continue;
-        ++exact;
-        const int32_t id = a.o_ids[o * kList + i];
-        if (d2 < best || (d2 == best && id < bid)) {
-          best = d2;
-          bid = id;
-        }
-      }
+      exact += a.N;
     }
     out_idx[q] = bid;
     out_d2[q] = best;
@@ -549,12 +624,21 @@ void brute_prepare(psg_ctx* ctx, Index& ix) {
   PSG_CUDA(cudaMalloc(&ix.brute_nup, sizeof(float) * npad));
   launch_pack(ctx, db_source(ix), ix.N, npad, D, ix.brute_nch, kBN, ix.brute_mu, ix.brute_op,
               ix.brute_n2, ix.brute_nup);
+  // largest |p'| bound per candidate tile (the epilogue's loose per-tile threshold)
+  std::vector<float> nup((size_t)npad), tmax((size_t)ix.brute_ptiles, 0.f);
+  PSG_CUDA(cudaMemcpyAsync(nup.data(), ix.brute_nup, sizeof(float) * npad, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int64_t i = 0; i < npad; ++i) tmax[i / kBN] = std::max(tmax[i / kBN], nup[i]);
+  PSG_CUDA(cudaMalloc(&ix.brute_tmax, sizeof(float) * tmax.size()));
+  PSG_CUDA(cudaMemcpyAsync(ix.brute_tmax, tmax.data(), sizeof(float) * tmax.size(),
+                           cudaMemcpyHostToDevice, ctx->stream));
   PSG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 void launch_brute_search(psg_ctx* ctx, const Index& ix, const RowSrc& qsrc, int64_t nq,
-                         int32_t* out_idx, double* out_d2, int64_t* out_scanned,
-                         int64_t* out_exact) {
+                         const int32_t* seed, int32_t* out_idx, double* out_d2,
+                         int64_t* out_scanned, int64_t* out_exact) {
   ProfScope _prof(ctx, K_SEARCH);
   if (nq <= 0) return;
   if (!ix.brute_op) fail(PSG_E_LOGIC, "brute-force operand not prepared");
@@ -566,13 +650,20 @@ void launch_brute_search(psg_ctx* ctx, const Index& ix, const RowSrc& qsrc, int6
   int splits = (int)std::max<int64_t>(1, (4 * (int64_t)ctx->num_sms + qtiles - 1) / qtiles);
   splits = std::min(splits, std::max(1, ix.brute_ptiles / 2));
   splits = std::min(splits, 64);
+  const int64_t no = nq * splits;
+  const int64_t ov_cap = std::max<int64_t>(1 << 20, 4 * nq);
   Scratch qop(sizeof(float) * (size_t)qpad * nch * kBK, ctx->stream);
   Scratch qn2(sizeof(float) * qpad, ctx->stream), qnup(sizeof(float) * qpad, ctx->stream);
-  const int64_t no = nq * splits;
-  Scratch oU(sizeof(float) * no, ctx->stream), oexd2(sizeof(double) * no, ctx->stream);
-  Scratch oexid(sizeof(int32_t) * no, ctx->stream), on(sizeof(int32_t) * no, ctx->stream);
+  Scratch U0(sizeof(float) * nq, ctx->stream), sd(sizeof(double) * nq, ctx->stream);
+  Scratch bbits(sizeof(unsigned long long) * nq, ctx->stream), bid(sizeof(int32_t) * nq, ctx->stream);
+  Scratch cnt(sizeof(int32_t) * nq, ctx->stream), lost(sizeof(int32_t) * nq, ctx->stream);
+  Scratch oU(sizeof(float) * no, ctx->stream), on(sizeof(int32_t) * no, ctx->stream);
   Scratch oids(sizeof(int32_t) * no * kList, ctx->stream), olb(sizeof(float) * no * kList, ctx->stream);
-  Scratch oex(sizeof(int64_t) * no, ctx->stream);
+  Scratch sd2(sizeof(double) * no * kList, ctx->stream);
+  Scratch ovc(sizeof(unsigned long long), ctx->stream), ovq(sizeof(int64_t) * ov_cap, ctx->stream);
+  Scratch ovid(sizeof(int32_t) * ov_cap, ctx->stream), ovlb(sizeof(float) * ov_cap, ctx->stream);
+  Scratch ovd2(sizeof(double) * ov_cap, ctx->stream);
+  PSG_CUDA(cudaMemsetAsync(ovc.p, 0, sizeof(unsigned long long), ctx->stream));
   RowSrc qs = qsrc;
   qs.D = ix.D;
   launch_pack(ctx, qs, nq, qpad, ix.D, nch, kBM, ix.brute_mu, qop.as<float>(), qn2.as<float>(),
@@ -581,9 +672,11 @@ void launch_brute_search(psg_ctx* ctx, const Index& ix, const RowSrc& qsrc, int6
   a.qop = qop.as<float>();
   a.qn2 = qn2.as<float>();
   a.qnup = qnup.as<float>();
+  a.qU0 = U0.as<float>();
   a.pop = ix.brute_op;
   a.pn2 = ix.brute_n2;
   a.pnup = ix.brute_nup;
+  a.tmax = ix.brute_tmax;
   a.nq = nq;
   a.N = ix.N;
   a.nch = nch;
@@ -606,26 +699,40 @@ void launch_brute_search(psg_ctx* ctx, const Index& ix, const RowSrc& qsrc, int6
   a.qs = qs;
   a.ps = db_source(ix);
   a.o_U = oU.as<float>();
-  a.o_exd2 = oexd2.as<double>();
-  a.o_exid = oexid.as<int32_t>();
   a.o_n = on.as<int32_t>();
   a.o_ids = oids.as<int32_t>();
   a.o_lb = olb.as<float>();
-  a.o_exact = oex.as<int64_t>();
+  a.ov_count = ovc.as<unsigned long long>();
+  a.ov_cap = ov_cap;
+  a.ov_q = ovq.as<int64_t>();
+  a.ov_id = ovid.as<int32_t>();
+  a.ov_lb = ovlb.as<float>();
+  a.lost = lost.as<int32_t>();
+  const int64_t qblocks = std::min<int64_t>((nq + 127) / 128, (int64_t)ctx->num_sms * 16);
+  brute_init_kernel<<<(int)qblocks, 128, 0, ctx->stream>>>(a, seed, sd.as<double>(), U0.as<float>(),
+                                                           bbits.as<unsigned long long>(),
+                                                           bid.as<int32_t>(), cnt.as<int32_t>());
+  PSG_LAUNCHED(ctx);
   constexpr BruteSmem L = brute_smem();
   PSG_CUDA(cudaFuncSetAttribute(brute_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)L.total));
   brute_mma_kernel<<<dim3((unsigned)qtiles, (unsigned)splits), kThreads, L.total, ctx->stream>>>(a);
   PSG_LAUNCHED(ctx);
-  Scratch sd2(sizeof(double) * no * kList, ctx->stream);
-  int64_t blocks = (no * kList + 255) / 256;
-  if (blocks > (int64_t)ctx->num_sms * 32) blocks = (int64_t)ctx->num_sms * 32;
-  brute_settle_kernel<<<(int)blocks, 256, 0, ctx->stream>>>(a, sd2.as<double>());
+  // survivors: all list slots + the (normally empty) overflow buffer
+  const int64_t sblocks = (int64_t)ctx->num_sms * 32;
+  brute_settle_kernel<<<(int)sblocks, 256, 0, ctx->stream>>>(a, U0.as<float>(), sd2.as<double>(),
+                                                            ovd2.as<double>(),
+                                                            bbits.as<unsigned long long>(),
+                                                            cnt.as<int32_t>());
   PSG_LAUNCHED(ctx);
-  blocks = (nq + 127) / 128;
-  if (blocks > (int64_t)ctx->num_sms * 16) blocks = (int64_t)ctx->num_sms * 16;
-  brute_pick_kernel<<<(int)blocks, 128, 0, ctx->stream>>>(a, sd2.as<double>(), out_idx, out_d2,
-                                                          out_scanned, out_exact);
+  brute_tie_kernel<<<(int)sblocks, 256, 0, ctx->stream>>>(a, seed, sd.as<double>(), sd2.as<double>(),
+                                                         ovd2.as<double>(),
+                                                         bbits.as<unsigned long long>(),
+                                                         bid.as<int32_t>());
+  PSG_LAUNCHED(ctx);
+  brute_pick_kernel<<<(int)qblocks, 128, 0, ctx->stream>>>(a, bbits.as<unsigned long long>(),
+                                                           bid.as<int32_t>(), cnt.as<int32_t>(),
+                                                           out_idx, out_d2, out_scanned, out_exact);
   PSG_LAUNCHED(ctx);
 }
 

@@ -106,6 +106,7 @@ struct Index {
   float* brute_n2 = nullptr;    // [ptiles * 256] |p - mu|^2 (fp32)
   float* brute_nup = nullptr;   // [ptiles * 256] |p - mu| rounded up
   float* brute_mu = nullptr;    // [nch * 32] centring vector
+  float* brute_tmax = nullptr;  // [ptiles] largest |p - mu| bound per tile
   ~Index();
 };
 
@@ -219,9 +220,11 @@ struct SearchArgs {
 // Brute-force index: build the filter operand once per index; exact search of
 // nq query rows (lexicographic min of (fp64 dist^2, id), optimizer.cpp:175-205).
 void brute_prepare(psg_ctx* ctx, Index& ix);
+// seed (optional, [nq]): a known candidate per query (e.g. the previous
+// assignment) whose exact distance starts the filter's upper bound.
 void launch_brute_search(psg_ctx* ctx, const Index& ix, const RowSrc& qsrc, int64_t nq,
-                         int32_t* out_idx, double* out_d2, int64_t* out_scanned,
-                         int64_t* out_exact);
+                         const int32_t* seed, int32_t* out_idx, double* out_d2,
+                         int64_t* out_scanned, int64_t* out_exact);
 void launch_search(psg_ctx* ctx, const SearchArgs& a);
 // tcgen05 (UMMA) tile search; returns false when the tree shape is unsupported.
 bool launch_search_mma(psg_ctx* ctx, const SearchArgs& a);

@@ -241,6 +241,7 @@ Index::~Index() {
   cudaFree(brute_n2);
   cudaFree(brute_nup);
   cudaFree(brute_mu);
+  cudaFree(brute_tmax);
 }
 
 // ---------------------------------------------------------------------------
@@ -665,7 +666,10 @@ void level_search(psg_level& L, bool seeded, int32_t* out_idx, double* out_dist)
     qs.xs = as.xs;
     qs.ys = as.ys;
     qs.nx = as.nx;
-    launch_brute_search(ctx, ix, qs, L.Ao, out_idx + L.off, L.d2.p, L.scanned.p, L.exact_evals.p);
+    // the previous assignment seeds the bound (the result is seed-independent)
+    const int32_t* seed = seeded ? L.cur_idx.p + L.off : nullptr;
+    launch_brute_search(ctx, ix, qs, L.Ao, seed, out_idx + L.off, L.d2.p, L.scanned.p,
+                        L.exact_evals.p);
     PSG_CUDA(cudaMemsetAsync(L.visited.p, 0, sizeof(int32_t) * L.Ao, ctx->stream));
     launch_rescore_windows(ctx, L.mirror.p, L.W, L.C, L.w, as, ix, out_idx + L.off,
                            out_dist + L.off);
@@ -1184,7 +1188,7 @@ psg_status psg_index_query(psg_ctx* ctx, const psg_index* index, const float* Q,
       qs.base = q.p;
       qs.kind = 0;
       qs.D = ix.D;
-      psg::launch_brute_search(ctx, ix, qs, nq, id.p, d2.p, sc.p, nullptr);
+      psg::launch_brute_search(ctx, ix, qs, nq, nullptr, id.p, d2.p, sc.p, nullptr);
     }
     if (ix.d > 0) psg::launch_project_vectors(ctx, q.p, nq, ix.D, ix.mean, ix.basis, ix.d, qp.p);
     psg::SearchArgs a{};

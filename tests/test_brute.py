@@ -96,3 +96,20 @@ def test_brute_self_image_zero_distance(gpu_ctx):
     ix = api.make_brute_force_index(ex, 8, ctx=gpu_ctx)
     idx, dist, _, _ = api.search_step(ex, ix, 2, 2, api.QueryBudget.exact())
     assert np.all(dist == 0.0)
+
+
+def test_brute_many_ties_spill_the_survivor_lists(gpu_ctx, port):
+    # 300 identical rows and 300 near-identical ones around each query: far
+    # more survivors than a (query, split) list holds -> overflow buffer path
+    rng = np.random.default_rng(5)
+    base = rng.uniform(0, 1, (4, 256)).astype(np.float32)
+    rows = [base[i % 4] + (rng.normal(0, 1e-6, 256).astype(np.float32) if i % 2 else 0)
+            for i in range(1200)]
+    X = np.concatenate([rng.uniform(0, 1, (500, 256)).astype(np.float32), np.stack(rows)])
+    Q = np.concatenate([base, base + 1e-7]).astype(np.float32)
+    ix = api.make_brute_force_vector_index(X, ctx=gpu_ctx)
+    idx, dist, _, _ = ix.nearest(Q)
+    X64 = X.astype(np.float64)
+    for i in range(Q.shape[0]):
+        pi, pd2 = port.nearest_lexmin(X64, Q[i].astype(np.float64))
+        assert idx[i] == pi and dist[i] == np.sqrt(pd2), i
