@@ -895,7 +895,28 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
             // bound covers it
             float2 sa = make_float2(0.f, 0.f), sb = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int k = 0; k < DP / 4; ++k) {
+            for (int k = 0; k < DP / 16; ++k) {
+              const float4 p = pr[k];
+              const float2 u0 = __fadd2_rn(q2[2 * k], make_float2(p.x, p.y));
+              const float2 u1 = __fadd2_rn(q2[2 * k + 1], make_float2(p.z, p.w));
+              sa = __ffma2_rn(u0, u0, sa);
+              sb = __ffma2_rn(u1, u1, sb);
+            }
+            if (!__any_sync(0xffffffffu, (sa.x + sa.y) + (sb.x + sb.y) <= thr)) continue;
+#pragma unroll
+            for (int k = DP / 16; k < DP / 8; ++k) {
+              const float4 p = pr[k];
+              const float2 u0 = __fadd2_rn(q2[2 * k], make_float2(p.x, p.y));
+              const float2 u1 = __fadd2_rn(q2[2 * k + 1], make_float2(p.z, p.w));
+              sa = __ffma2_rn(u0, u0, sa);
+              sb = __ffma2_rn(u1, u1, sb);
+            }
+            // early exit after the leading (highest-variance) half of the PCA
+            // dims: rounded sums of non-negative terms only grow, so a partial
+            // sum above thr already rules the point out for this lane
+            if (!__any_sync(0xffffffffu, (sa.x + sa.y) + (sb.x + sb.y) <= thr)) continue;
+#pragma unroll
+            for (int k = DP / 8; k < DP / 4; ++k) {
               const float4 p = pr[k];
               const float2 u0 = __fadd2_rn(q2[2 * k], make_float2(p.x, p.y));
               const float2 u1 = __fadd2_rn(q2[2 * k + 1], make_float2(p.z, p.w));
