@@ -223,7 +223,28 @@ def roofline_for(kernels: dict, step_ms: float, A: int, P: int, C: int, d: int, 
                 "frac": None, "traffic": None}
     roof["kernel"] = dom
     roof["peak_src"] = peaks["src"] if roof["bound"] == "hbm" else "derived"
+    if dom == "search_kernel":
+        roof["traffic"], roof["traffic_src"] = ncu_traffic("search_tile_kernel")
     return roof, per
+
+
+def ncu_traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed ncu --set full summary (profiles/r1/<kernel>_*_summary.json),
+    or None.  Read-only evidence: never measured under the profiler here."""
+    files = sorted((ROOT / "profiles").glob(f"*/{kernel}_*_summary.json"))
+    if not files:
+        return None, None
+    f = files[-1]
+    try:
+        m = json.loads(f.read_text())["metrics"]
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        tot = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            tot += float(m[k]["value"].replace(",", "")) * scale[m[k]["unit"]]
+        return tot, str(f.relative_to(ROOT))
+    except (KeyError, ValueError):
+        return None, None
 
 
 def run_ours(args):
