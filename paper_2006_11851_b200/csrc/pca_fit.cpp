@@ -20,7 +20,10 @@
 #include <cusolverDn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "psg_internal.h"
@@ -68,6 +71,17 @@ void fit_pca_device(psg_ctx* ctx, Index& ix, const psg_index_cfg& cfg) {
   cublas_check(cublasSetStream(cb, ctx->stream), "cublasSetStream");
   cusolver_check(cusolverDnSetStream(cs, ctx->stream), "cusolverDnSetStream");
 
+  const bool verbose = std::getenv("PERSYN_VERBOSE") != nullptr;
+  auto tick = [&](const char* what) {
+    if (!verbose) return;
+    static thread_local std::chrono::steady_clock::time_point t0;
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    const auto t1 = std::chrono::steady_clock::now();
+    if (what) fprintf(stderr, "[persyn]   pca %s %.2f ms\n", what,
+                      std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
+  tick(nullptr);
   DevMem mean(sizeof(double) * D);
   DevMem Xc(sizeof(double) * (size_t)n * D);
   if (ix.from_vectors) {
@@ -85,6 +99,7 @@ void fit_pca_device(psg_ctx* ctx, Index& ix, const psg_index_cfg& cfg) {
                            Xc.as<double>(), D, &beta, cov.as<double>(), D),
                "cublasDsyrk");
   ctx->launches++;
+  tick("mean + centre + dsyrk");
 
   // number of top eigenpairs needed (0 = full spectrum)
   int m_top = 0;
@@ -131,6 +146,7 @@ void fit_pca_device(psg_ctx* ctx, Index& ix, const psg_index_cfg& cfg) {
   }
   ctx->launches++;
 
+  tick(subset ? "syevdx" : "syevd");
   const int ne = subset ? meig : D;  // eigenpairs computed, ascending in cov's first columns
   std::vector<double> h_eval(ne), h_mean(D);
   int h_info = 0;

@@ -323,6 +323,10 @@ void launch_fit_to(psg_ctx* ctx, const double* in, int W, int H, int ow, int oh,
 // ---- host pieces --------------------------------------------------------------
 HostTree build_tree_host(const double* proj, int64_t N, int d, int branching, int max_depth,
                          int leaf_threshold, uint64_t seed);
+// Same construction on the device (level-synchronous, deterministic); P is
+// the device [N][d] projected database.
+HostTree build_tree_device(psg_ctx* ctx, const double* P, int64_t N, int d, int branching,
+                           int max_depth, int leaf_threshold, uint64_t seed);
 // Replay of an external tree (pre-order child counts + DFS leaf lists).
 HostTree import_tree_host(const double* proj, int64_t N, int d, const int32_t* n_children_pre,
                           int64_t n_nodes, const int32_t* leaf_sizes, int64_t n_leaves,

@@ -408,15 +408,22 @@ void finish_index(psg_ctx* ctx, Index& ix, const double* mean, const double* bas
     }
   }
   phase("db projection");
-  // tree (host-native build over the device-projected points)
-  std::vector<double> hp((size_t)ix.N * d);
-  if (d > 0)
-    PSG_CUDA(cudaMemcpyAsync(hp.data(), ix.proj, sizeof(double) * hp.size(),
-                             cudaMemcpyDeviceToHost, ctx->stream));
-  PSG_CUDA(cudaStreamSynchronize(ctx->stream));
-  ix.htree = build_tree_host(hp.data(), ix.N, d, cfg.branching, cfg.max_depth,
-                             cfg.leaf_threshold > 0 ? cfg.leaf_threshold : cfg.branching, cfg.seed);
-  phase("tree build (host)");
+  // k-means tree over the device-projected points: built on the device
+  // (PERSYN_TREE=host selects the native host builder, same rules)
+  const int lt = cfg.leaf_threshold > 0 ? cfg.leaf_threshold : cfg.branching;
+  const char* tb = std::getenv("PERSYN_TREE");
+  if (tb && std::string(tb) == "host") {
+    std::vector<double> hp((size_t)ix.N * d);
+    if (d > 0)
+      PSG_CUDA(cudaMemcpyAsync(hp.data(), ix.proj, sizeof(double) * hp.size(),
+                               cudaMemcpyDeviceToHost, ctx->stream));
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    ix.htree = build_tree_host(hp.data(), ix.N, d, cfg.branching, cfg.max_depth, lt, cfg.seed);
+    phase("tree build (host)");
+  } else {
+    ix.htree = build_tree_device(ctx, ix.proj, ix.N, d, cfg.branching, cfg.max_depth, lt, cfg.seed);
+    phase("tree build (device)");
+  }
   upload_tree(ctx, ix);
   phase("tree upload + search copies");
 }
@@ -1132,13 +1139,14 @@ psg_status psg_index_leaves(const psg_index* index, int32_t* ids, int32_t* sizes
   return guarded([&] {
     const psg::HostTree& t = index->impl.htree;
     *n_leaves = t.n_leaves;
-    int64_t li = 0;
-    for (size_t i = 0; i < t.n_children.size(); ++i) {
+    int64_t li = 0, off = 0;
+    for (size_t i = 0; i < t.n_children.size(); ++i) {  // leaves in node (BFS) order
       if (t.n_children[i] != 0) continue;
       if (sizes) sizes[li] = t.leaf_count[i];
       if (ids)
         std::copy(t.perm.begin() + t.leaf_start[i], t.perm.begin() + t.leaf_start[i] + t.leaf_count[i],
-                  ids + t.leaf_start[i]);
+                  ids + off);
+      off += t.leaf_count[i];
       ++li;
     }
   });

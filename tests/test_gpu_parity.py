@@ -276,3 +276,31 @@ def test_exact_search_ties_and_duplicates(gpu_ctx, port):
     idx2, dist2, _, _ = api.search_step(ex, ix, 2, 2, api.QueryBudget.exact())
     i2, d2, _ = port.search_step(ex, 8, 2, 2, cand, proj, mean, basis)
     assert np.all(dist2 == 0.0) and np.array_equal(idx2, i2)
+
+
+@pytest.mark.parametrize("b,depth", [(4, 3), (8, 4), (16, 0)])
+def test_device_tree_build_valid_and_deterministic(gpu_ctx, port, b, depth, monkeypatch):
+    """KmTree::build rules on the device: leaves partition the ids, splits stop at
+    the depth cap / leaf threshold, identical on rebuild; the host builder
+    (PERSYN_TREE=host) obeys the same invariants."""
+    ex, init = _stage(size=40)
+    cand, mean, basis, proj = _injected(port, ex, 8, 12)
+    runs = []
+    for builder in ("device", "device", "host"):
+        if builder == "host":
+            monkeypatch.setenv("PERSYN_TREE", "host")
+        ix = api.make_pca_tree_index(ex, 8, mean=mean, basis=basis, branching=b, max_depth=depth,
+                                     seed=5, ctx=gpu_ctx)
+        monkeypatch.delenv("PERSYN_TREE", raising=False)
+        ids, sizes = ix.leaves()
+        assert np.array_equal(np.sort(ids), np.arange(ix.count))
+        assert sizes.sum() == ix.count and np.all(sizes > 0)
+        if depth:
+            assert ix.depth <= depth
+        else:
+            assert np.all(sizes < b)  # unbounded depth: leaves below the threshold
+        runs.append((ids, sizes, ix.n_nodes))
+        i_e, d_e, _, _ = api.search_step(init, ix, 4, 2, api.QueryBudget.exact())
+        i_p, d_p, _ = port.search_step(init, 8, 4, 2, cand, proj, mean, basis)
+        assert np.array_equal(i_e, i_p) and np.array_equal(d_e, d_p)
+    assert all(np.array_equal(a, c) for a, c in zip(runs[0][:2], runs[1][:2]))
