@@ -128,6 +128,7 @@ __global__ void stats_node_kernel(Lv v, const double* psum, const double* pmin,
 __global__ void radius_kernel(Lv v, const double* cent, unsigned long long* rbits) {
   GRID_LOOP(p, v.N) {
     const int node = v.node_of[p];
+    if (node < 0) continue;
     const double r = sqrt(dist2_p(v.P + (int64_t)v.ids[p] * v.d, cent + (int64_t)node * v.d, v.d));
     atomicMax(rbits + node, (unsigned long long)__double_as_longlong(r));
   }
@@ -165,7 +166,7 @@ __global__ void kpp_first_kernel(Lv v, Km k) {
 __global__ void kpp_d2_kernel(Lv v, Km k, int c) {
   GRID_LOOP(p, v.N) {
     const int node = v.node_of[p];
-    if (!k.picking[node] || k.nc[node] != c) continue;
+    if (node < 0 || !k.picking[node] || k.nc[node] != c) continue;
     const double dd = dist2_p(v.P + (int64_t)v.ids[p] * v.d,
                               k.centers + ((int64_t)node * kMaxB + c - 1) * v.d, v.d);
     k.d2[p] = c == 1 ? dd : fmin(k.d2[p], dd);
@@ -228,7 +229,7 @@ __global__ void kpp_pick_kernel(Lv v, Km k, int c, const double* pd2) {
 __global__ void assign_kernel(Lv v, Km k) {
   GRID_LOOP(p, v.N) {
     const int node = v.node_of[p];
-    if (v.kk[node] <= 0 || k.done[node]) continue;
+    if (node < 0 || v.kk[node] <= 0 || k.done[node]) continue;
     const double* x = v.P + (int64_t)v.ids[p] * v.d;
     const double* cs = k.centers + (int64_t)node * kMaxB * v.d;
     int best = 0;
@@ -476,6 +477,8 @@ HostTree build_tree_device(psg_ctx* ctx, const double* P, int64_t N, int d, int 
     v.node_of = node_of.as<int32_t>();
     v.kk = d_kk.as<int32_t>();
 
+    // positions of earlier leaves belong to no node of this level (-1)
+    PSG_CUDA(cudaMemsetAsync(node_of.p, 0xFF, sizeof(int32_t) * N, st));
     node_of_kernel<<<grid_for(ctx, L, 128), 128, 0, st>>>(v, node_of.as<int32_t>());
     PSG_LAUNCHED(ctx);
     // ---- statistics ----

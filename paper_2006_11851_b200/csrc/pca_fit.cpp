@@ -83,23 +83,31 @@ void fit_pca_device(psg_ctx* ctx, Index& ix, const psg_index_cfg& cfg) {
   };
   tick(nullptr);
   DevMem mean(sizeof(double) * D);
-  DevMem Xc(sizeof(double) * (size_t)n * D);
-  if (ix.from_vectors) {
-    launch_vector_mean(ctx, ix.vectors, n, D, mean.as<double>());
-    launch_center_vectors(ctx, ix.vectors, n, D, mean.as<double>(), Xc.as<double>());
-  } else {
-    launch_window_mean(ctx, ix.ex_mirror, ix.ew, ix.C, ix.w, ix.nxe, n, mean.as<double>());
-    launch_center_windows(ctx, ix.ex_mirror, ix.ew, ix.C, ix.w, ix.nxe, n, mean.as<double>(),
-                          Xc.as<double>());
-  }
-  // Row-major Xc[n][D] is column-major D x n: cov = Xc^T Xc = A A^T.
   DevMem cov(sizeof(double) * (size_t)D * D);
-  const double alpha = 1.0 / (double)(n - 1), beta = 0.0;
-  cublas_check(cublasDsyrk(cb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, D, (int)n, &alpha,
-                           Xc.as<double>(), D, &beta, cov.as<double>(), D),
-               "cublasDsyrk");
-  ctx->launches++;
-  tick("mean + centre + dsyrk");
+  const bool structured = !ix.from_vectors && (size_t)ix.eh * ix.w * sizeof(double) <= 200 * 1024;
+  if (structured) {
+    // window database: box sums of product images (kernels_pca.cu), no N x D matrix
+    launch_window_mean(ctx, ix.ex_mirror, ix.ew, ix.C, ix.w, ix.nxe, n, mean.as<double>());
+    launch_window_cov(ctx, ix.ex_mirror, ix.ew, ix.eh, ix.C, ix.w, mean.as<double>(),
+                      cov.as<double>());
+  } else {
+    DevMem Xc(sizeof(double) * (size_t)n * D);
+    if (ix.from_vectors) {
+      launch_vector_mean(ctx, ix.vectors, n, D, mean.as<double>());
+      launch_center_vectors(ctx, ix.vectors, n, D, mean.as<double>(), Xc.as<double>());
+    } else {
+      launch_window_mean(ctx, ix.ex_mirror, ix.ew, ix.C, ix.w, ix.nxe, n, mean.as<double>());
+      launch_center_windows(ctx, ix.ex_mirror, ix.ew, ix.C, ix.w, ix.nxe, n, mean.as<double>(),
+                            Xc.as<double>());
+    }
+    // Row-major Xc[n][D] is column-major D x n: cov = Xc^T Xc = A A^T.
+    const double alpha = 1.0 / (double)(n - 1), beta = 0.0;
+    cublas_check(cublasDsyrk(cb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, D, (int)n, &alpha,
+                             Xc.as<double>(), D, &beta, cov.as<double>(), D),
+                 "cublasDsyrk");
+    ctx->launches++;
+  }
+  tick(structured ? "window covariance (box sums)" : "mean + centre + dsyrk");
 
   // number of top eigenpairs needed (0 = full spectrum)
   int m_top = 0;
@@ -203,6 +211,7 @@ void fit_pca_device(psg_ctx* ctx, Index& ix, const psg_index_cfg& cfg) {
       for (int j = 0; j < D; ++j) basis[(size_t)k * D + j] = sgn * comp[j];
     }
   }
+  tick("selection + basis download");
   ix.h_mean = std::move(h_mean);
   ix.h_basis = std::move(basis);
   ix.h_var = std::move(var);

@@ -310,6 +310,10 @@ void launch_window_mean(psg_ctx* ctx, const float* mirror, int img_w, int C, int
                         int64_t N, double* mean);
 void launch_center_windows(psg_ctx* ctx, const float* mirror, int img_w, int C, int w, int nxe,
                            int64_t N, const double* mean, double* Xc);
+// Covariance [D][D] (full, symmetric) of the dense window database of an
+// exemplar mirror, from its window means (kernels_pca.cu).
+void launch_window_cov(psg_ctx* ctx, const float* ex_mirror, int ew, int eh, int C, int w,
+                       const double* wmean, double* cov);
 void launch_vector_mean(psg_ctx* ctx, const float* X, int64_t N, int D, double* mean);
 void launch_center_vectors(psg_ctx* ctx, const float* X, int64_t N, int D, const double* mean,
                            double* Xc);

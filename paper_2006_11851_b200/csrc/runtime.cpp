@@ -1742,9 +1742,18 @@ extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, doubl
         }
         rep.total_nn_calls += calls;
         rep.final_energy = last.energy;
+        if (std::getenv("PERSYN_VERBOSE")) {
+          const double tr = now_ms();
+          index.reset();
+          fprintf(stderr, "[persyn] stage l=%d w=%d: index %.2f ms, optimize %.2f ms, teardown %.2f ms\n",
+                  l, w, index_ms, now_ms() - to - (now_ms() - tr), now_ms() - tr);
+        }
       }
     }
     rep.part2_millis = now_ms() - t1;
+    if (std::getenv("PERSYN_VERBOSE"))
+      fprintf(stderr, "[persyn] synthesize: part1 %.2f ms, part2 %.2f ms\n", rep.part1_millis,
+              rep.part2_millis);
     state.download(ctx, out_planes, (size_t)C * req->out_w * req->out_h);
     PSG_CUDA(cudaStreamSynchronize(ctx->stream));
     if (report) *report = rep;

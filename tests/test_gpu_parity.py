@@ -304,3 +304,27 @@ def test_device_tree_build_valid_and_deterministic(gpu_ctx, port, b, depth, monk
         i_p, d_p, _ = port.search_step(init, 8, 4, 2, cand, proj, mean, basis)
         assert np.array_equal(i_e, i_p) and np.array_equal(d_e, d_p)
     assert all(np.array_equal(a, c) for a, c in zip(runs[0][:2], runs[1][:2]))
+
+
+@pytest.mark.parametrize("G,w,kw", [(1, 8, dict(d_cap=12)), (2, 16, dict(d_fixed=20)),
+                                    (2, 4, dict(variance_target=0.9))])
+def test_device_pca_fit_matches_numpy(gpu_ctx, port, G, w, kw):
+    """Window covariance from box sums (no N x D matrix) + top-d eigensolver vs
+    the numpy restatement of fit_pca on the materialised windows."""
+    ex, _ = _stage(size=40, G=G)
+    ix = api.make_pca_tree_index(ex, w, ctx=gpu_ctx, **kw)
+    mean, basis, var = ix.pca()
+    cand = port.extract_all(ex, w, 1)
+    m2, b2, v2 = fit_pca(cand, kw.get("variance_target", 0.95), kw.get("d_fixed", 0),
+                         kw.get("d_cap", 0))
+    k = basis.shape[0]
+    assert k == b2.shape[0]
+    assert np.allclose(mean, m2, atol=1e-12)
+    assert np.allclose(var[:k], v2[:k], rtol=1e-9, atol=1e-12)
+    assert np.allclose(basis @ basis.T, np.eye(k), atol=1e-10)
+    gaps = np.abs(np.diff(v2[: k + 1])) / v2[0]
+    ok = np.ones(k, bool)                     # well-separated components only
+    ok[:-1] &= gaps[:-1] > 1e-6
+    ok[1:] &= gaps[:-1] > 1e-6
+    ok &= gaps[:k] > 1e-6
+    assert np.allclose(np.abs(np.sum(basis * b2, axis=1))[ok], 1.0, atol=1e-6)
