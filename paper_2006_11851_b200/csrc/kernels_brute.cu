@@ -616,12 +616,12 @@ void brute_prepare(psg_ctx* ctx, Index& ix) {
   PSG_CUDA(cudaStreamSynchronize(ctx->stream));
   std::vector<float> mu((size_t)ix.brute_nch * kBK, 0.f);
   for (int j = 0; j < D; ++j) mu[j] = (float)hm[j];
-  PSG_CUDA(cudaMalloc(&ix.brute_mu, sizeof(float) * mu.size()));
+  PSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ix.brute_mu), sizeof(float) * mu.size(), ctx->stream));
   PSG_CUDA(cudaMemcpyAsync(ix.brute_mu, mu.data(), sizeof(float) * mu.size(),
                            cudaMemcpyHostToDevice, ctx->stream));
-  PSG_CUDA(cudaMalloc(&ix.brute_op, sizeof(float) * (size_t)npad * ix.brute_nch * kBK));
-  PSG_CUDA(cudaMalloc(&ix.brute_n2, sizeof(float) * npad));
-  PSG_CUDA(cudaMalloc(&ix.brute_nup, sizeof(float) * npad));
+  PSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ix.brute_op), sizeof(float) * (size_t)npad * ix.brute_nch * kBK, ctx->stream));
+  PSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ix.brute_n2), sizeof(float) * npad, ctx->stream));
+  PSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ix.brute_nup), sizeof(float) * npad, ctx->stream));
   launch_pack(ctx, db_source(ix), ix.N, npad, D, ix.brute_nch, kBN, ix.brute_mu, ix.brute_op,
               ix.brute_n2, ix.brute_nup);
   // largest |p'| bound per candidate tile (the epilogue's loose per-tile threshold)
@@ -630,7 +630,7 @@ void brute_prepare(psg_ctx* ctx, Index& ix) {
                            ctx->stream));
   PSG_CUDA(cudaStreamSynchronize(ctx->stream));
   for (int64_t i = 0; i < npad; ++i) tmax[i / kBN] = std::max(tmax[i / kBN], nup[i]);
-  PSG_CUDA(cudaMalloc(&ix.brute_tmax, sizeof(float) * tmax.size()));
+  PSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ix.brute_tmax), sizeof(float) * tmax.size(), ctx->stream));
   PSG_CUDA(cudaMemcpyAsync(ix.brute_tmax, tmax.data(), sizeof(float) * tmax.size(),
                            cudaMemcpyHostToDevice, ctx->stream));
   PSG_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -150,9 +150,11 @@ struct psg_ctx {
   // cuBLAS / cuSOLVER handles (opaque here, created lazily by pca.cpp)
   void* cublas = nullptr;
   void* cusolver = nullptr;
-  // pinned staging
-  void* pinned = nullptr;
-  size_t pinned_bytes = 0;
+  // pinned staging: 64-byte slots for per-level stats read-back, carved from
+  // pinned blocks that live as long as the context (cudaMallocHost/FreeHost
+  // synchronise the device and cost milliseconds: never per level)
+  std::vector<void*> pinned_blocks;
+  std::vector<double*> pinned_free;
   int* d_flags = nullptr;
   bool legacy_search = false;  // PERSYN_SEARCH=warp: per-query warp kernel instead of tiles
   bool mma_search = false;     // PERSYN_SEARCH=mma: tcgen05 tile kernel
@@ -336,6 +338,7 @@ HostTree import_tree_host(const double* proj, int64_t N, int d, const int32_t* n
                           int64_t n_nodes, const int32_t* leaf_sizes, int64_t n_leaves,
                           const int32_t* leaf_ids);
 void fit_pca_device(psg_ctx* ctx, Index& ix, const psg_index_cfg& cfg);
+void create_solver_handles(psg_ctx* ctx);  // cuBLAS + cuSOLVER handles of a context
 int64_t plan_host(int W, int H, int w, int sp, int p, int32_t* mult);
 std::vector<int32_t> axis_positions(int extent, int window, int step);
 

@@ -76,9 +76,9 @@ struct DBuf {
 };
 
 template <class T>
-T* dalloc(size_t count) {
+T* dalloc(size_t count) {  // long-lived (index) buffers, from the stream-ordered pool
   T* p = nullptr;
-  if (count) PSG_CUDA(cudaMalloc(&p, sizeof(T) * count));
+  if (count) PSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, t_stream));
   return p;
 }
 
@@ -213,35 +213,10 @@ int64_t plan_host(int W, int H, int w, int sp, int p, int32_t* mult) {
 double pow_cr_host(double x, double y) { return pow_cr(x, y); }
 
 Index::~Index() {
-  cudaFree(ex_mirror);
-  cudaFree(vectors);
-  cudaFree(mean);
-  cudaFree(basis);
-  cudaFree(proj);
-  cudaFree(proj_soa);
-  cudaFree(perm);
-  cudaFree(tree.centroid);
-  cudaFree(tree.radius);
-  cudaFree(tree.first_child);
-  cudaFree(tree.n_children);
-  cudaFree(tree.leaf_start);
-  cudaFree(tree.leaf_count);
-  cudaFree(tree.centroid32);
-  cudaFree(tree.radius32);
-  cudaFree(tree.cnorm32);
-  cudaFree(proj32_q4);
-  cudaFree(tree.centroid32T);
-  cudaFree(tree.boxlo);
-  cudaFree(tree.boxhi);
-  cudaFree(tree.meta);
-  cudaFree(tree.tie);
-  cudaFree(pnorm32);
-  cudaFree(ex_hist);
-  cudaFree(brute_op);
-  cudaFree(brute_n2);
-  cudaFree(brute_nup);
-  cudaFree(brute_mu);
-  cudaFree(brute_tmax);
+  // stream-ordered frees (the allocations come from the context's pool)
+  cudaStream_t st = ctx ? ctx->stream : nullptr;
+  for (void* p : {(void*)ex_mirror, (void*)vectors, (void*)mean, (void*)basis, (void*)proj, (void*)proj_soa, (void*)perm, (void*)tree.centroid, (void*)tree.radius, (void*)tree.first_child, (void*)tree.n_children, (void*)tree.leaf_start, (void*)tree.leaf_count, (void*)tree.centroid32, (void*)tree.radius32, (void*)tree.cnorm32, (void*)proj32_q4, (void*)tree.centroid32T, (void*)tree.boxlo, (void*)tree.boxhi, (void*)tree.meta, (void*)tree.tie, (void*)pnorm32, (void*)ex_hist, (void*)brute_op, (void*)brute_n2, (void*)brute_nup, (void*)brute_mu, (void*)brute_tmax})
+    if (p) cudaFreeAsync(p, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -253,13 +228,14 @@ namespace {
 // and leaf-ordered projected points, plus the conservative fp32 filter/bound
 // copies of the fast search kernels.
 void free_tree(Index& ix) {
+  cudaStream_t ctx_stream = ix.ctx ? ix.ctx->stream : nullptr;
   DevTree& T = ix.tree;
   for (void* p : {(void*)T.centroid, (void*)T.radius, (void*)T.first_child, (void*)T.n_children,
                   (void*)T.leaf_start, (void*)T.leaf_count, (void*)T.centroid32,
                   (void*)T.centroid32T, (void*)T.radius32, (void*)T.cnorm32, (void*)T.boxlo,
                   (void*)T.boxhi, (void*)T.meta, (void*)T.tie, (void*)ix.perm, (void*)ix.proj_soa,
                   (void*)ix.proj32_q4, (void*)ix.pnorm32})
-    cudaFree(p);
+    if (p) cudaFreeAsync(p, ctx_stream);
   T = DevTree{};
   ix.perm = nullptr;
   ix.proj_soa = nullptr;
@@ -507,7 +483,7 @@ struct psg_level {
   int64_t unique_queries = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   ~psg_level() {
-    if (stats_host) cudaFreeHost(stats_host);
+    if (stats_host && ctx) ctx->pinned_free.push_back(stats_host);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
   }
@@ -626,7 +602,15 @@ void level_setup_band(psg_level& L, psg_ctx* ctx, const Index& ix, const psg_ban
   L.exact_evals.alloc(L.Ao);
   L.visited.alloc(L.Ao);
   L.stats_dev.alloc(8 + 6 * 296);
-  PSG_CUDA(cudaMallocHost(&L.stats_host, sizeof(double) * 8));
+  if (ctx->pinned_free.empty()) {
+    void* blk = nullptr;
+    PSG_CUDA(cudaMallocHost(&blk, 64 * 64));
+    ctx->pinned_blocks.push_back(blk);
+    for (int i = 0; i < 64; ++i)
+      ctx->pinned_free.push_back(reinterpret_cast<double*>(static_cast<char*>(blk) + 64 * i));
+  }
+  L.stats_host = ctx->pinned_free.back();
+  ctx->pinned_free.pop_back();
   PSG_CUDA(cudaEventCreate(&L.ev0));
   PSG_CUDA(cudaEventCreate(&L.ev1));
 }
@@ -956,6 +940,7 @@ psg_status psg_ctx_create(int device, void* stream, psg_ctx** out) {
     }
     PSG_CUDA(cudaMalloc(&c->d_flags, sizeof(int)));
     PSG_CUDA(cudaMemsetAsync(c->d_flags, 0, sizeof(int), c->stream));
+    psg::create_solver_handles(c.get());  // once per context, not inside a stage build
     *out = c.release();
   });
 }
@@ -972,6 +957,7 @@ void psg_ctx_destroy(psg_ctx* ctx) {
   if (ctx->cublas) cublasDestroy(static_cast<cublasHandle_t>(ctx->cublas));
   if (ctx->cusolver) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(ctx->cusolver));
   cudaFree(ctx->d_flags);
+  for (void* b : ctx->pinned_blocks) cudaFreeHost(b);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -1692,6 +1678,7 @@ extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, doubl
         if (W < w || H < w || ew[l] < w || eh[l] < w) continue;
         if ((int64_t)(ew[l] - w + 1) * (eh[l] - w + 1) < 2) continue;  // fit_pca needs n >= 2
         const double ti = now_ms();
+        {  // stage scope: index and level are released before the next stage
         psg_index_cfg icfg = req->index;
         icfg.seed = (req->seed ^ (0x9E3779B97F4A7C15ull * (uint64_t)(l + 1))) ^ (uint64_t)w;
         if (req->cfg.histogram_matching) {
@@ -1742,12 +1729,13 @@ extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, doubl
         }
         rep.total_nn_calls += calls;
         rep.final_energy = last.energy;
-        if (std::getenv("PERSYN_VERBOSE")) {
-          const double tr = now_ms();
-          index.reset();
-          fprintf(stderr, "[persyn] stage l=%d w=%d: index %.2f ms, optimize %.2f ms, teardown %.2f ms\n",
-                  l, w, index_ms, now_ms() - to - (now_ms() - tr), now_ms() - tr);
+        if (std::getenv("PERSYN_VERBOSE"))
+          fprintf(stderr, "[persyn] stage l=%d w=%d: index %.2f ms, optimize %.2f ms\n", l, w,
+                  index_ms, now_ms() - to);
         }
+        if (std::getenv("PERSYN_VERBOSE"))
+          fprintf(stderr, "[persyn] stage l=%d w=%d: wall incl. teardown %.2f ms\n", l, w,
+                  now_ms() - ti);
       }
     }
     rep.part2_millis = now_ms() - t1;
