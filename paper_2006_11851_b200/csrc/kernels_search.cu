@@ -793,6 +793,7 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
       qn2 += v0 * v0 + v1 * v1;
     }
     const float qn = __double2float_ru(sqrt(qn2) * (1.0 + 1e-12));
+    const float qdelta = 1.2e-7f * qn;  // >= |float(q_j) - q_j| for every j
     // invalid lanes hold best = -1: every bound (>= 0) prunes them
     double best = valid ? kInf : -1.0;
     int32_t best_id = 0x7fffffff;
@@ -973,34 +974,39 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
       // per-lane bounds go to shared scratch, warp-min keys to a uniform array
 #pragma unroll 1
       for (int c = 0; c < nc; ++c) {
-        const float4* cr = reinterpret_cast<const float4*>(stage + c * RS);
-        float2 sa = make_float2(0.f, 0.f), sb = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int k = 0; k < DP / 4; ++k) {
-          const float4 p = cr[k];
-          const float2 u0 = __fadd2_rn(q2[2 * k], make_float2(p.x, p.y));
-          const float2 u1 = __fadd2_rn(q2[2 * k + 1], make_float2(p.z, p.w));
-          sa = __ffma2_rn(u0, u0, sa);
-          sb = __ffma2_rn(u1, u1, sb);
-        }
-        const float s = (sa.x + sa.y) + (sb.x + sb.y);
+        // box bound first (8 leading dims): the box is rounded outward and the
+        // fp32 query differs from the fp64 one by <= 2^-24 |q_j| <= qdelta;
+        // subtraction / accumulation rounding is covered by the final factor
         float bx = 0.f;
 #pragma unroll
         for (int j = 0; j < kBoxDims; ++j) {
           if (j < KB) {
             const float lo = boxs[c][2 * j], hi = boxs[c][2 * j + 1];
             const float qj = (j & 1) ? q2[j >> 1].y : q2[j >> 1].x;
-            float gap = fmaxf(lo - qj, qj - hi) - 2.4e-7f * (fabsf(qj) + fabsf(lo) + fabsf(hi));
-            gap = fmaxf(gap, 0.f);
+            const float gap = fmaxf(fmaxf(lo - qj, qj - hi) - qdelta, 0.f);
             bx = fmaf(gap, gap, bx);
           }
         }
-        const float dc = sqrtf(s);
-        const float rad = aux0[c];
-        const float slack = 2e-5f * (1.f + dc + rad + qn + aux1[c]);
-        const float lb = dc - rad - slack;
-        float lb2 = lb > 0.f ? lb * lb * (1.f - 1e-6f) : 0.f;
-        lb2 = fmaxf(lb2, bx * (1.f - 1e-5f));
+        bx *= 1.f - 1e-5f;
+        float lb2 = bx;
+        if (__any_sync(0xffffffffu, (double)bx <= best)) {  // else: pruned for every lane
+          const float4* cr = reinterpret_cast<const float4*>(stage + c * RS);
+          float2 sa = make_float2(0.f, 0.f), sb = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int k = 0; k < DP / 4; ++k) {
+            const float4 p = cr[k];
+            const float2 u0 = __fadd2_rn(q2[2 * k], make_float2(p.x, p.y));
+            const float2 u1 = __fadd2_rn(q2[2 * k + 1], make_float2(p.z, p.w));
+            sa = __ffma2_rn(u0, u0, sa);
+            sb = __ffma2_rn(u1, u1, sb);
+          }
+          const float s = (sa.x + sa.y) + (sb.x + sb.y);
+          const float dc = sqrtf(s);
+          const float rad = aux0[c];
+          const float slack = 2e-5f * (1.f + dc + rad + qn + aux1[c]);
+          const float lb = dc - rad - slack;
+          lb2 = fmaxf(lb > 0.f ? lb * lb * (1.f - 1e-6f) : 0.f, bx);
+        }
         tlb[c][lane] = lb2;
         const bool want = (double)lb2 <= best;
         // non-negative floats order like their bit patterns
@@ -1057,6 +1063,7 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
   const bool tile_ok = a.tree.max_children <= kTileMaxB &&
                        1 + a.tree.max_depth * (a.tree.max_children - 1) <= kTileStack;
   if (a.mode == PSG_EXACT && a.proj32_q4 && a.tree.centroid32 && tile_ok && !ctx->legacy_search) {
+    if (ctx->hmma_tile && a.d <= 32 && launch_search_hmma(ctx, a)) return;
     const int64_t tiles = (a.nq + 31) / 32;
     const int wpb = a.d <= 32 ? 3 : 2;  // static smem <= 48 KB per CTA
     int64_t blocks = (tiles + wpb - 1) / wpb;

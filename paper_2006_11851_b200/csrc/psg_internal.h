@@ -158,6 +158,7 @@ struct psg_ctx {
   int* d_flags = nullptr;
   bool legacy_search = false;  // PERSYN_SEARCH=warp: per-query warp kernel instead of tiles
   bool mma_search = false;     // PERSYN_SEARCH=mma: tcgen05 tile kernel
+  bool hmma_tile = false;      // PERSYN_SEARCH=hmma: leaf filter on mma.sync (bf16 split)
 };
 
 struct psg_index {
@@ -230,6 +231,8 @@ void launch_brute_search(psg_ctx* ctx, const Index& ix, const RowSrc& qsrc, int6
 void launch_search(psg_ctx* ctx, const SearchArgs& a);
 // tcgen05 (UMMA) tile search; returns false when the tree shape is unsupported.
 bool launch_search_mma(psg_ctx* ctx, const SearchArgs& a);
+// Tile search with the leaf filter on mma.sync (bf16 split); false if unsupported.
+bool launch_search_hmma(psg_ctx* ctx, const SearchArgs& a);
 // Locality ordering of unstructured queries (search-only workloads).
 void launch_greedy_keys(psg_ctx* ctx, const double* q, int64_t nq, int d, const DevTree& tree,
                         uint32_t* keys, int32_t* order);

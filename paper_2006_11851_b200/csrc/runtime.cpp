@@ -925,6 +925,7 @@ psg_status psg_ctx_create(int device, void* stream, psg_ctx** out) {
     if (const char* e = std::getenv("PERSYN_SEARCH")) {
       c->legacy_search = std::string(e) == "warp";
       c->mma_search = std::string(e) == "mma";
+      c->hmma_tile = std::string(e) == "hmma";
     }
     if (stream) {
       c->stream = static_cast<cudaStream_t>(stream);
