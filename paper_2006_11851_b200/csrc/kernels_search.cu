@@ -760,7 +760,6 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
   const int d = a.d;
   const int N = (int)a.N;
   const int nn = a.tree.n_nodes;
-  const int KB = d < kBoxDims ? d : kBoxDims;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
   const float kInfF = __int_as_float(0x7f800000);
   // image queries: 8 x 4 anchor tiles (overlapping windows share candidates);
@@ -829,6 +828,8 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
       }
     }
 
+    // best rounded up to float: float compares against it can only keep more
+    float bestf = __double2float_ru(best);
     if (lane == 0) sm_[0] = a.tree.meta[0];
     slb[0][lane] = 0.f;
     int top = 1;
@@ -840,7 +841,7 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
       int2 node = make_int2(0, 0);
       while (top > 0) {
         const int2 md = sm_[top - 1];
-        const bool want = (double)slb[top - 1][lane] <= best;
+        const bool want = slb[top - 1][lane] <= bestf;
         if (!__any_sync(0xffffffffu, want)) {  // km_tree.cpp:265 prune, per lane
           --top;
           continue;
@@ -887,7 +888,7 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
           // best rounded up to float: a float compare can only keep more points.
           // thr >= s for every point that can pass the precise test below
           // (eps is increasing in s and |p| <= pnorm_max)
-          float best_up = __double2float_ru(best);
+          float best_up = bestf;
           float thr = best_up * (1.f + 1e-4f) +
                       1.01e-6f * (qn + a.pnorm_max) * (sqrtf(2.f * best_up + 1.f) + 1e-3f) + 1e-30f;
           for (int i = 0; i < cn; ++i) {
@@ -940,6 +941,7 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
                   best = d2;
                   best_id = id;
                   best_up = __double2float_ru(best);
+                  bestf = best_up;
                   thr = best_up * (1.f + 1e-4f) +
                         1.01e-6f * (qn + a.pnorm_max) * (sqrtf(2.f * best_up + 1.f) + 1e-3f) + 1e-30f;
                 }
@@ -964,7 +966,7 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
         aux1[lane] = a.tree.cnorm32[fc + lane];
         cmeta[lane] = a.tree.meta[fc + lane];
       }
-      for (int f = lane; f < nc * KB; f += 32) {
+      for (int f = lane; f < nc * kBoxDims; f += 32) {  // dims >= d hold [0, 0]
         const int c = f % nc, j = f / nc;
         boxs[c][2 * j] = __ldg(a.tree.boxlo + (int64_t)j * nn + fc + c);
         boxs[c][2 * j + 1] = __ldg(a.tree.boxhi + (int64_t)j * nn + fc + c);
@@ -978,18 +980,18 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
         // fp32 query differs from the fp64 one by <= 2^-24 |q_j| <= qdelta;
         // subtraction / accumulation rounding is covered by the final factor
         float bx = 0.f;
+        // all kBoxDims dims: for j >= d both the box ([0, 0]) and q_j (0) are
+        // zero-padded, so those terms vanish
 #pragma unroll
         for (int j = 0; j < kBoxDims; ++j) {
-          if (j < KB) {
-            const float lo = boxs[c][2 * j], hi = boxs[c][2 * j + 1];
-            const float qj = (j & 1) ? q2[j >> 1].y : q2[j >> 1].x;
-            const float gap = fmaxf(fmaxf(lo - qj, qj - hi) - qdelta, 0.f);
-            bx = fmaf(gap, gap, bx);
-          }
+          const float lo = boxs[c][2 * j], hi = boxs[c][2 * j + 1];
+          const float qj = (j & 1) ? q2[j >> 1].y : q2[j >> 1].x;
+          const float gap = fmaxf(fmaxf(lo - qj, qj - hi) - qdelta, 0.f);
+          bx = fmaf(gap, gap, bx);
         }
         bx *= 1.f - 1e-5f;
         float lb2 = bx;
-        if (__any_sync(0xffffffffu, (double)bx <= best)) {  // else: pruned for every lane
+        if (__any_sync(0xffffffffu, bx <= bestf)) {  // else: pruned for every lane
           const float4* cr = reinterpret_cast<const float4*>(stage + c * RS);
           float2 sa = make_float2(0.f, 0.f), sb = make_float2(0.f, 0.f);
 #pragma unroll
@@ -1008,7 +1010,7 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
           lb2 = fmaxf(lb > 0.f ? lb * lb * (1.f - 1e-6f) : 0.f, bx);
         }
         tlb[c][lane] = lb2;
-        const bool want = (double)lb2 <= best;
+        const bool want = lb2 <= bestf;
         // non-negative floats order like their bit patterns
         const unsigned key = __reduce_min_sync(0xffffffffu, want ? __float_as_uint(lb2) : 0xffffffffu);
         if (lane == 0) tkey[c] = key;
