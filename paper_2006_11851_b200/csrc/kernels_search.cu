@@ -891,10 +891,14 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
           float best_up = bestf;
           float thr = best_up * (1.f + 1e-4f) +
                       1.01e-6f * (qn + a.pnorm_max) * (sqrtf(2.f * best_up + 1.f) + 1e-3f) + 1e-30f;
-          for (int i = 0; i < cn; ++i) {
+          // phase 1, branch-free over the batch: the 8 leading (highest
+          // variance) PCA dims of every staged point against the batch-start
+          // threshold; rounded sums of non-negative terms only grow, so a
+          // partial sum above thr already rules the point out for this lane
+          uint32_t pass = 0;
+#pragma unroll 4
+          for (int i = 0; i < 32; ++i) {
             const float4* pr = reinterpret_cast<const float4*>(stage + i * RS);
-            // packed fp32x2 (FADD2/FFMA2); partial sums in any order: the filter
-            // bound covers it
             float2 sa = make_float2(0.f, 0.f), sb = make_float2(0.f, 0.f);
 #pragma unroll
             for (int k = 0; k < DP / 16; ++k) {
@@ -904,9 +908,20 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
               sa = __ffma2_rn(u0, u0, sa);
               sb = __ffma2_rn(u1, u1, sb);
             }
-            if (!__any_sync(0xffffffffu, (sa.x + sa.y) + (sb.x + sb.y) <= thr)) continue;
+            pass |= ((sa.x + sa.y) + (sb.x + sb.y) <= thr ? 1u : 0u) << i;
+          }
+          if (cn < 32) pass &= (1u << cn) - 1u;
+          uint32_t todo = __reduce_or_sync(0xffffffffu, pass);
+          // phase 2: the points some lane still wants, all dims, in batch order
+          while (todo) {
+            const int i = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const float4* pr = reinterpret_cast<const float4*>(stage + i * RS);
+            // packed fp32x2 (FADD2/FFMA2); partial sums in any order: the filter
+            // bound covers it
+            float2 sa = make_float2(0.f, 0.f), sb = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int k = DP / 16; k < DP / 8; ++k) {
+            for (int k = 0; k < DP / 8; ++k) {
               const float4 p = pr[k];
               const float2 u0 = __fadd2_rn(q2[2 * k], make_float2(p.x, p.y));
               const float2 u1 = __fadd2_rn(q2[2 * k + 1], make_float2(p.z, p.w));
