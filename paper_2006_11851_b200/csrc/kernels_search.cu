@@ -972,10 +972,6 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
       const int nc = -node.y;
       const int fc = node.x;
       __syncwarp();
-      for (int f = lane; f < nc * DP; f += 32) {
-        const int c = f / DP, j = f - c * DP;
-        stage[c * RS + j] = j < d ? -__ldg(a.tree.centroid32 + (int64_t)(fc + c) * d + j) : 0.f;
-      }
       if (lane < nc) {
         aux0[lane] = a.tree.radius32[fc + lane];
         aux1[lane] = a.tree.cnorm32[fc + lane];
@@ -987,16 +983,14 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
         boxs[c][2 * j + 1] = __ldg(a.tree.boxhi + (int64_t)j * nn + fc + c);
       }
       __syncwarp();
-      // per-child bounds: rolled loop (keeps the kernel inside the I-cache);
-      // per-lane bounds go to shared scratch, warp-min keys to a uniform array
-#pragma unroll 1
+      // phase 1: box bound of every child (8 leading dims).  The box is rounded
+      // outward and the fp32 query differs from the fp64 one by <= 2^-24 |q_j|
+      // <= qdelta; subtraction / accumulation rounding is covered by the final
+      // factor.  For j >= d both the box ([0, 0]) and q_j (0) are zero-padded.
+      uint32_t boxpass = 0;
+#pragma unroll 2
       for (int c = 0; c < nc; ++c) {
-        // box bound first (8 leading dims): the box is rounded outward and the
-        // fp32 query differs from the fp64 one by <= 2^-24 |q_j| <= qdelta;
-        // subtraction / accumulation rounding is covered by the final factor
         float bx = 0.f;
-        // all kBoxDims dims: for j >= d both the box ([0, 0]) and q_j (0) are
-        // zero-padded, so those terms vanish
 #pragma unroll
         for (int j = 0; j < kBoxDims; ++j) {
           const float lo = boxs[c][2 * j], hi = boxs[c][2 * j + 1];
@@ -1005,25 +999,38 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
           bx = fmaf(gap, gap, bx);
         }
         bx *= 1.f - 1e-5f;
-        float lb2 = bx;
-        if (__any_sync(0xffffffffu, bx <= bestf)) {  // else: pruned for every lane
-          const float4* cr = reinterpret_cast<const float4*>(stage + c * RS);
-          float2 sa = make_float2(0.f, 0.f), sb = make_float2(0.f, 0.f);
+        tlb[c][lane] = bx;
+        boxpass |= (bx <= bestf ? 1u : 0u) << c;
+      }
+      const uint32_t todo = __reduce_or_sync(0xffffffffu, boxpass);  // else pruned for all lanes
+      if (lane < nc && !((todo >> lane) & 1u)) tkey[lane] = 0xffffffffu;
+      // centroids of the children some lane still wants (one coalesced row each)
+      for (uint32_t m = todo; m; m &= m - 1) {
+        const int c = __ffs(m) - 1;
+        for (int j = lane; j < DP; j += 32)
+          stage[c * RS + j] = j < d ? -__ldg(a.tree.centroid32 + (int64_t)(fc + c) * d + j) : 0.f;
+      }
+      __syncwarp();
+      // phase 2: ball bound (|q - c| - radius)+ of those children, max with the box
+#pragma unroll 1
+      for (uint32_t m = todo; m; m &= m - 1) {
+        const int c = __ffs(m) - 1;
+        const float4* cr = reinterpret_cast<const float4*>(stage + c * RS);
+        float2 sa = make_float2(0.f, 0.f), sb = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int k = 0; k < DP / 4; ++k) {
-            const float4 p = cr[k];
-            const float2 u0 = __fadd2_rn(q2[2 * k], make_float2(p.x, p.y));
-            const float2 u1 = __fadd2_rn(q2[2 * k + 1], make_float2(p.z, p.w));
-            sa = __ffma2_rn(u0, u0, sa);
-            sb = __ffma2_rn(u1, u1, sb);
-          }
-          const float s = (sa.x + sa.y) + (sb.x + sb.y);
-          const float dc = sqrtf(s);
-          const float rad = aux0[c];
-          const float slack = 2e-5f * (1.f + dc + rad + qn + aux1[c]);
-          const float lb = dc - rad - slack;
-          lb2 = fmaxf(lb > 0.f ? lb * lb * (1.f - 1e-6f) : 0.f, bx);
+        for (int k = 0; k < DP / 4; ++k) {
+          const float4 p = cr[k];
+          const float2 u0 = __fadd2_rn(q2[2 * k], make_float2(p.x, p.y));
+          const float2 u1 = __fadd2_rn(q2[2 * k + 1], make_float2(p.z, p.w));
+          sa = __ffma2_rn(u0, u0, sa);
+          sb = __ffma2_rn(u1, u1, sb);
         }
+        const float s = (sa.x + sa.y) + (sb.x + sb.y);
+        const float dc = sqrtf(s);
+        const float rad = aux0[c];
+        const float slack = 2e-5f * (1.f + dc + rad + qn + aux1[c]);
+        const float lb = dc - rad - slack;
+        const float lb2 = fmaxf(lb > 0.f ? lb * lb * (1.f - 1e-6f) : 0.f, tlb[c][lane]);
         tlb[c][lane] = lb2;
         const bool want = lb2 <= bestf;
         // non-negative floats order like their bit patterns
