@@ -896,19 +896,19 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
           // threshold; rounded sums of non-negative terms only grow, so a
           // partial sum above thr already rules the point out for this lane
           uint32_t pass = 0;
-#pragma unroll 4
+#pragma unroll
           for (int i = 0; i < 32; ++i) {
             const float4* pr = reinterpret_cast<const float4*>(stage + i * RS);
-            float2 sa = make_float2(0.f, 0.f), sb = make_float2(0.f, 0.f);
+            float2 sa = make_float2(0.f, 0.f);
 #pragma unroll
             for (int k = 0; k < DP / 16; ++k) {
               const float4 p = pr[k];
               const float2 u0 = __fadd2_rn(q2[2 * k], make_float2(p.x, p.y));
               const float2 u1 = __fadd2_rn(q2[2 * k + 1], make_float2(p.z, p.w));
               sa = __ffma2_rn(u0, u0, sa);
-              sb = __ffma2_rn(u1, u1, sb);
+              sa = __ffma2_rn(u1, u1, sa);
             }
-            pass |= ((sa.x + sa.y) + (sb.x + sb.y) <= thr ? 1u : 0u) << i;
+            if (sa.x + sa.y <= thr) pass |= 1u << i;
           }
           if (cn < 32) pass &= (1u << cn) - 1u;
           uint32_t todo = __reduce_or_sync(0xffffffffu, pass);
