@@ -799,33 +799,15 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
     int64_t scanned = 0, exact_evals = 0;
     int32_t visited = 0;
 
-    // ---- coherence seeds (exact fp64), per lane ------------------------------------
+    // ---- seed (exact fp64): the query's previous assignment is the initial
+    // upper bound.  (Lattice neighbours' shifted assignments were tried too: on
+    // the bench stage they cost more exact evaluations than they save.)
     if (a.seed_idx && valid) {
-      const int qix = a.qxs ? (int)(q % a.qnx) : 0, qiy = a.qxs ? (int)(q / a.qnx) : 0;
-#pragma unroll 1
-      for (int k = 0; k < 5; ++k) {
-        int32_t cand = -1;
-        if (k == 0) {
-          cand = a.seed_idx[q];
-        } else if (a.qxs) {
-          const int nix = qix + (k == 1 ? -1 : k == 2 ? 1 : 0);
-          const int niy = qiy + (k == 3 ? -1 : k == 4 ? 1 : 0);
-          if (nix >= 0 && nix < a.qnx && niy >= 0 && niy < qny) {
-            const int32_t e = a.seed_idx[(int64_t)niy * a.qnx + nix];
-            const int ex = e % a.nxe + (a.qxs[qix] - a.qxs[nix]);
-            const int ey = e / a.nxe + (a.qys[qiy] - a.qys[niy]);
-            if (ex >= 0 && ex < a.nxe && ey >= 0 && ey < a.nye) cand = ey * a.nxe + ex;
-          }
-        }
-        if (cand < 0) continue;
-        const double d2 = dist2_seq_cold(qrow, a.proj + (int64_t)cand * d, d);
-        ++scanned;
-        ++exact_evals;
-        if (lex_less(d2, cand, best, best_id)) {
-          best = d2;
-          best_id = cand;
-        }
-      }
+      const int32_t cand = a.seed_idx[q];
+      best = dist2_seq_cold(qrow, a.proj + (int64_t)cand * d, d);
+      best_id = cand;
+      ++scanned;
+      ++exact_evals;
     }
 
     // best rounded up to float: float compares against it can only keep more
