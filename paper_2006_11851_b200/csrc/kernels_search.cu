@@ -132,6 +132,97 @@ __global__ void __launch_bounds__(256) project_kernel(
   }
 }
 
+// d <= 32: lane = (anchor group g2, k pair kp): each thread accumulates 2
+// consecutive k for RQ anchors, so one double2 basis load and RQ broadcast
+// double2 loads of the centred window feed 4 * RQ fp64 ops per 2 j (the
+// per-(anchor, k) order over j is unchanged: bit-identical to project_kernel).
+template <int RQ, bool kWindows>
+__global__ void __launch_bounds__(256) project2_kernel(
+    const float* __restrict__ src, int img_w, int C, int w, const int32_t* __restrict__ xs,
+    const int32_t* __restrict__ ys, int nx, int64_t n, int D, int JC,
+    const double* __restrict__ mean, const double* __restrict__ basisT,  // [D][32]
+    int d, double* __restrict__ out) {
+  constexpr int TQ = 8 * 2 * RQ;  // anchors per block: 8 warps x 2 groups x RQ
+  extern __shared__ __align__(16) double smem2[];
+  const int JCp = JC + 2;  // even (double2 aligned), breaks the power-of-two stride
+  double* cen = smem2;             // [TQ][JCp]
+  double* bas = smem2 + TQ * JCp;  // [JC][32]
+  __shared__ int64_t base_s[TQ];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g2 = lane >> 4, kp = lane & 15;
+  const int64_t q0 = (int64_t)blockIdx.x * TQ;
+  if (tid < TQ) {
+    const int64_t qi = q0 + tid;
+    int64_t b = -1;
+    if (qi < n) {
+      if (kWindows) {
+        const int ax = xs[qi % nx], ay = ys[qi / nx];
+        b = ((int64_t)ay * img_w + ax) * C;
+      } else {
+        b = qi * (int64_t)D;
+      }
+    }
+    base_s[tid] = b;
+  }
+  double acc0[RQ], acc1[RQ];
+#pragma unroll
+  for (int r = 0; r < RQ; ++r) acc0[r] = acc1[r] = 0.0;
+  const int qb = (warp * 2 + g2) * RQ;  // first anchor (block-local) of this thread
+  const int n_chunks = (D + JC - 1) / JC;
+  for (int ch = 0; ch < n_chunks; ++ch) {
+    const int j0 = ch * JC;
+    const int jc = min(JC, D - j0);
+    __syncthreads();
+    for (int f = tid; f < TQ * jc; f += 256) {
+      const int q = f / jc, jj = f - q * jc;
+      const int64_t b = base_s[q];
+      double v = 0.0;
+      if (b >= 0) {
+        const float x = kWindows ? src[b + (int64_t)ch * img_w * C + jj] : src[b + j0 + jj];
+        v = dsub((double)x, mean[j0 + jj]);
+      }
+      cen[q * JCp + jj] = v;
+    }
+    if (jc & 1)  // odd chunk: zero pad column so the double2 loop can read it
+      for (int q = tid; q < TQ; q += 256) cen[q * JCp + jc] = 0.0;
+    for (int f = tid; f < jc * 32; f += 256) bas[f] = basisT[(int64_t)j0 * 32 + f];
+    if (jc & 1)
+      for (int f = tid; f < 32; f += 256) bas[jc * 32 + f] = 0.0;
+    __syncthreads();
+    const int jc2 = jc & ~1;
+#pragma unroll 2
+    for (int jj = 0; jj < jc2; jj += 2) {
+      const double2 b0 = *reinterpret_cast<const double2*>(bas + jj * 32 + 2 * kp);
+      const double2 b1 = *reinterpret_cast<const double2*>(bas + (jj + 1) * 32 + 2 * kp);
+#pragma unroll
+      for (int r = 0; r < RQ; ++r) {
+        const double2 c = *reinterpret_cast<const double2*>(cen + (qb + r) * JCp + jj);
+        acc0[r] = dadd(acc0[r], dmul(c.x, b0.x));
+        acc1[r] = dadd(acc1[r], dmul(c.x, b0.y));
+        acc0[r] = dadd(acc0[r], dmul(c.y, b1.x));
+        acc1[r] = dadd(acc1[r], dmul(c.y, b1.y));
+      }
+    }
+    if (jc & 1) {  // last odd column
+      const int jj = jc - 1;
+      const double2 b0 = *reinterpret_cast<const double2*>(bas + jj * 32 + 2 * kp);
+#pragma unroll
+      for (int r = 0; r < RQ; ++r) {
+        const double c = cen[(qb + r) * JCp + jj];
+        acc0[r] = dadd(acc0[r], dmul(c, b0.x));
+        acc1[r] = dadd(acc1[r], dmul(c, b0.y));
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RQ; ++r) {
+    const int64_t qi = q0 + qb + r;
+    if (qi >= n) continue;
+    if (2 * kp < d) out[qi * d + 2 * kp] = acc0[r];
+    if (2 * kp + 1 < d) out[qi * d + 2 * kp + 1] = acc1[r];
+  }
+}
+
 template <bool kWindows>
 static void launch_project(psg_ctx* ctx, const float* src, int img_w, int C, int w,
                            const int32_t* xs, const int32_t* ys, int nx, int64_t n, int D, int JC,
@@ -143,11 +234,13 @@ static void launch_project(psg_ctx* ctx, const float* src, int img_w, int C, int
   const int JCp = JC | 1;
   const int blocks = (int)((n + TQ - 1) / TQ);
   if (d <= 32) {
-    const size_t sm = sizeof(double) * ((size_t)TQ * JCp + (size_t)JC * 32);
-    auto k = project_kernel<1, RQ, kWindows>;
+    constexpr int TQ2 = 8 * 2 * RQ;
+    const size_t sm = sizeof(double) * ((size_t)TQ2 * (JC + 2) + (size_t)(JC + 1) * 32);
+    auto k = project2_kernel<RQ, kWindows>;
     PSG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    k<<<blocks, 256, sm, ctx->stream>>>(src, img_w, C, w, xs, ys, nx, n, D, JC, mean, basisT, d,
-                                         out);
+    const int blocks2 = (int)((n + TQ2 - 1) / TQ2);
+    k<<<blocks2, 256, sm, ctx->stream>>>(src, img_w, C, w, xs, ys, nx, n, D, JC, mean, basisT, d,
+                                          out);
   } else if (d <= 64) {
     const size_t sm = sizeof(double) * ((size_t)TQ * JCp + (size_t)JC * 64);
     auto k = project_kernel<2, RQ, kWindows>;
