@@ -369,12 +369,10 @@ def run_ours(args):
                                       convergence_fraction=1e-9, histogram_bins=16,
                                       histogram_matching=True, nbhd_width=args.window,
                                       spacing=sp, patch_width=2, budget=budget)
-        calls_e2e = 2
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(calls_e2e):
-            import ctypes as ct
-            from paper_2006_11851_b200 import native as N
+        import ctypes as ct
+        from paper_2006_11851_b200 import native as N
+
+        def e2e_call():
             c = e2e_cfg.c()
             st = (N.psg_iter_stats * n_it)()
             n = ct.c_int()
@@ -382,6 +380,12 @@ def run_ours(args):
                                              cfg.out, cfg.out, ct.byref(c), None,
                                              ct.c_void_p(out_pinned.data_ptr()),
                                              ct.cast(st, ct.c_void_p), ct.byref(n)))
+        e2e_call()  # warm-up: pool growth for the call's level buffers
+        calls_e2e = 3
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(calls_e2e):
+            e2e_call()
         torch.cuda.synchronize()
         t_e2e = (time.perf_counter() - t0) / calls_e2e
         result["e2e"] = {"value": n_it / t_e2e, "unit": UNIT,
