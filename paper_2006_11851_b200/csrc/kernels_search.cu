@@ -350,6 +350,150 @@ __device__ __forceinline__ void scan_leaf(const SearchArgs& a, const double* __r
   scanned += cnt;
 }
 
+// Greedy / backtrack(m) with one thread per query (km_tree.cpp:213-250): the
+// reference's fp64 keys dist^2(q, centroid) (j ascending), best-first frontier
+// as a binary min-heap on (key, tie id) in thread-local memory, leaves scanned
+// with the exact fp64 chain against the row-major projected database;
+// lexicographic (dist^2, id) minimum (km_tree.cpp:134).  Budget queries touch
+// ~m leaves, so a query per thread keeps every lane busy (the warp-per-query
+// search_kernel leaves most lanes idle on ~15-point leaves).
+constexpr int kHeapCap = 384;
+
+template <int DP>
+__global__ void __launch_bounds__(128) search_budget_kernel(SearchArgs a) {
+  const int d = a.d;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < a.nq;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    double qs[DP];
+#pragma unroll
+    for (int j = 0; j < DP; ++j) qs[j] = j < d ? a.q[q * d + j] : 0.0;
+    auto key_of = [&](int node) {
+      const double* c = a.tree.centroid + (int64_t)node * d;
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < DP; ++j)
+        if (j < d) {
+          const double t = dsub(qs[j], c[j]);
+          acc = dadd(acc, dmul(t, t));
+        }
+      return acc;
+    };
+    double best = __longlong_as_double(0x7ff0000000000000ll);
+    int32_t best_id = 0x7fffffff;
+    int64_t scanned = 0;
+    int32_t visited = 0;
+    auto scan = [&](int node) {
+      const int32_t s0 = a.tree.leaf_start[node], cnt = a.tree.leaf_count[node];
+      for (int i = 0; i < cnt; ++i) {
+        const int32_t id = a.perm[s0 + i];
+        const double* p = a.proj + (int64_t)id * d;
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < DP; ++j)
+          if (j < d) {
+            const double t = dsub(qs[j], p[j]);
+            acc = dadd(acc, dmul(t, t));
+          }
+        if (acc < best || (acc == best && id < best_id)) {
+          best = acc;
+          best_id = id;
+        }
+      }
+      scanned += cnt;
+    };
+    if (a.mode == PSG_GREEDY) {
+      int node = 0;
+      ++visited;
+      while (a.tree.n_children[node] > 0) {
+        const int fc = a.tree.first_child[node], nc = a.tree.n_children[node];
+        double bd = __longlong_as_double(0x7ff0000000000000ll);
+        int next = fc;
+        for (int c = 0; c < nc; ++c) {
+          const double k = key_of(fc + c);
+          if (k < bd) {  // strict: the first child in order wins ties
+            bd = k;
+            next = fc + c;
+          }
+        }
+        node = next;
+        ++visited;
+      }
+      scan(node);
+    } else {
+      double hk[kHeapCap];
+      int32_t hn[kHeapCap], ht[kHeapCap];
+      int size = 0;
+      auto less = [&](int i, int j) {
+        return hk[i] < hk[j] || (hk[i] == hk[j] && ht[i] < ht[j]);
+      };
+      auto push = [&](double k, int32_t node) {
+        if (size == kHeapCap) {
+          atomicOr(a.flags, FLAG_STACK_OVERFLOW);
+          return;
+        }
+        int i = size++;
+        hk[i] = k;
+        hn[i] = node;
+        ht[i] = a.tree.tie ? a.tree.tie[node] : node;
+        while (i > 0) {
+          const int par = (i - 1) >> 1;
+          if (!less(i, par)) break;
+          const double tk = hk[i];
+          hk[i] = hk[par];
+          hk[par] = tk;
+          const int32_t tn = hn[i];
+          hn[i] = hn[par];
+          hn[par] = tn;
+          const int32_t tt = ht[i];
+          ht[i] = ht[par];
+          ht[par] = tt;
+          i = par;
+        }
+      };
+      push(0.0, 0);
+      int leaves = 0;
+      while (size > 0 && leaves < a.max_leaves) {
+        const int node = hn[0];
+        --size;
+        hk[0] = hk[size];
+        hn[0] = hn[size];
+        ht[0] = ht[size];
+        for (int i = 0;;) {  // sift down
+          const int l = 2 * i + 1, r = l + 1;
+          int m = i;
+          if (l < size && less(l, m)) m = l;
+          if (r < size && less(r, m)) m = r;
+          if (m == i) break;
+          const double tk = hk[i];
+          hk[i] = hk[m];
+          hk[m] = tk;
+          const int32_t tn = hn[i];
+          hn[i] = hn[m];
+          hn[m] = tn;
+          const int32_t tt = ht[i];
+          ht[i] = ht[m];
+          ht[m] = tt;
+          i = m;
+        }
+        ++visited;
+        const int nc = a.tree.n_children[node];
+        if (nc == 0) {
+          scan(node);
+          ++leaves;
+        } else {
+          const int fc = a.tree.first_child[node];
+          for (int c = 0; c < nc; ++c) push(key_of(fc + c), fc + c);
+        }
+      }
+    }
+    a.out_idx[q] = best_id;
+    a.out_d2[q] = best;
+    if (a.out_scanned) a.out_scanned[q] = scanned;
+    if (a.out_exact) a.out_exact[q] = scanned;
+    if (a.out_visited) a.out_visited[q] = visited;
+  }
+}
+
 __global__ void __launch_bounds__(32 * kSearchWarps) search_kernel(SearchArgs a) {
   __shared__ double qs_all[kSearchWarps][kMaxD];
   __shared__ int32_t st_node[kSearchWarps][kStack];
@@ -1183,6 +1327,20 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
       search_exact_kernel<32><<<(int)blocks, 256, 0, ctx->stream>>>(a);
     else
       search_exact_kernel<64><<<(int)blocks, 256, 0, ctx->stream>>>(a);
+    PSG_LAUNCHED(ctx);
+    return;
+  }
+  // thread-per-query kernel for greedy and short backtracks; longer frontiers
+  // (m > 2) spill the per-thread heap and run faster warp-per-query
+  if (a.mode != PSG_EXACT && !ctx->legacy_search &&
+      (a.mode == PSG_GREEDY || a.max_leaves <= 2)) {
+    int64_t blocks = (a.nq + 127) / 128;
+    const int64_t cap = (int64_t)ctx->num_sms * 64;
+    if (blocks > cap) blocks = cap;
+    if (a.d <= 32)
+      search_budget_kernel<32><<<(int)blocks, 128, 0, ctx->stream>>>(a);
+    else
+      search_budget_kernel<64><<<(int)blocks, 128, 0, ctx->stream>>>(a);
     PSG_LAUNCHED(ctx);
     return;
   }
