@@ -170,7 +170,7 @@ def run_reference(args):
     r = cpu_reference_sample(args.window, args.steps, args.warmup, threads)
     line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000.0 / r["value"], "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1000.0 / r["value"], "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE cfg3 generator)",
             "config": {"workload": "cfg3 finest stage 1024^2, w=8 sp=2 p=2, d=32, exact, C=4",
                        "parallelism": "host threads", "l2": "n/a (CPU)"},
