@@ -1119,11 +1119,10 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
           for (int i = 0; i < 32; ++i) {
             const float4* pr = reinterpret_cast<const float4*>(stage + i * RS);
             float2 sa = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int k = 0; k < DP / 16; ++k) {
-              const float4 p = pr[k];
-              const float2 u0 = __fadd2_rn(q2[2 * k], make_float2(p.x, p.y));
-              const float2 u1 = __fadd2_rn(q2[2 * k + 1], make_float2(p.z, p.w));
+            {
+              const float4 p = pr[0];
+              const float2 u0 = __fadd2_rn(q2[0], make_float2(p.x, p.y));
+              const float2 u1 = __fadd2_rn(q2[1], make_float2(p.z, p.w));
               sa = __ffma2_rn(u0, u0, sa);
               sa = __ffma2_rn(u1, u1, sa);
             }
