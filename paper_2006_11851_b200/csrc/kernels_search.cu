@@ -1506,7 +1506,21 @@ __global__ void rescore_windows_kernel(const float* __restrict__ mirror, int img
     for (int dy = 0; dy < w; ++dy) {
       const float* v = mirror + ((int64_t)(ay + dy) * img_w + ax) * C;
       const float* z = ex_mirror + ((int64_t)(ey + dy) * ew + ex) * C;
-      for (int jj = 0; jj < row; ++jj) {
+      int jj = 0;
+      for (; jj + 8 <= row; jj += 8) {  // loads batched ahead of the sequential adds
+        float vv[8], zz[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          vv[u] = __ldg(v + jj + u);
+          zz[u] = __ldg(z + jj + u);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const double t = dsub((double)vv[u], (double)zz[u]);
+          acc = dadd(acc, dmul(t, t));
+        }
+      }
+      for (; jj < row; ++jj) {
         const double t = dsub((double)v[jj], (double)z[jj]);
         acc = dadd(acc, dmul(t, t));
       }
