@@ -88,6 +88,8 @@ __global__ void __launch_bounds__(256) project_kernel(
   for (int ch = 0; ch < n_chunks; ++ch) {
     const int j0 = ch * JC;
     const int jc = min(JC, D - j0);
+    // windows: chunk j0 is window row j0 / R at offset j0 % R (R = w * C)
+    const int64_t roff = kWindows ? (int64_t)(j0 / (w * C)) * img_w * C + j0 % (w * C) : 0;
     __syncthreads();
     for (int f = tid; f < TQ * jc; f += 256) {
       const int q = f / jc, jj = f - q * jc;
@@ -97,7 +99,7 @@ __global__ void __launch_bounds__(256) project_kernel(
         float x;
         if (kWindows) {
           // window row ch (= dy) of anchor q: contiguous w*C floats
-          x = src[b + (int64_t)ch * img_w * C + jj];
+          x = src[b + roff + jj];
         } else {
           x = src[b + j0 + jj];
         }
@@ -172,13 +174,15 @@ __global__ void __launch_bounds__(256) project2_kernel(
   for (int ch = 0; ch < n_chunks; ++ch) {
     const int j0 = ch * JC;
     const int jc = min(JC, D - j0);
+    // windows: chunk j0 is window row j0 / R at offset j0 % R (R = w * C)
+    const int64_t roff = kWindows ? (int64_t)(j0 / (w * C)) * img_w * C + j0 % (w * C) : 0;
     __syncthreads();
     for (int f = tid; f < TQ * jc; f += 256) {
       const int q = f / jc, jj = f - q * jc;
       const int64_t b = base_s[q];
       double v = 0.0;
       if (b >= 0) {
-        const float x = kWindows ? src[b + (int64_t)ch * img_w * C + jj] : src[b + j0 + jj];
+        const float x = kWindows ? src[b + roff + jj] : src[b + j0 + jj];
         v = dsub((double)x, mean[j0 + jj]);
       }
       cen[q * JCp + jj] = v;
@@ -256,7 +260,15 @@ static void launch_project(psg_ctx* ctx, const float* src, int img_w, int C, int
 void launch_project_windows(psg_ctx* ctx, const float* mirror, int img_w, int C, int w,
                             AnchorSet anchors, const double* mean, const double* basisT, int d,
                             double* out) {
-  const int JC = w * C;
+  // chunk = one window row (w * C floats), or its largest divisor <= 160 for
+  // very wide rows (bounded shared memory; chunk j0 is row j0 / R, offset j0 % R)
+  const int R = w * C;
+  int JC = R;
+  if (R > 160) {
+    JC = 1;
+    for (int c = 1; c <= 160; ++c)
+      if (R % c == 0) JC = c;
+  }
   launch_project<true>(ctx, mirror, img_w, C, w, anchors.xs, anchors.ys, anchors.nx,
                        anchors.count, w * w * C, JC, mean, basisT, d, out);
 }
