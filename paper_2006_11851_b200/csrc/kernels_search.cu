@@ -260,15 +260,12 @@ static void launch_project(psg_ctx* ctx, const float* src, int img_w, int C, int
 void launch_project_windows(psg_ctx* ctx, const float* mirror, int img_w, int C, int w,
                             AnchorSet anchors, const double* mean, const double* basisT, int d,
                             double* out) {
-  // chunk = one window row (w * C floats), or its largest divisor <= 160 for
-  // very wide rows (bounded shared memory; chunk j0 is row j0 / R, offset j0 % R)
+  // chunk = the largest divisor of a window row (w * C floats) <= 48 (bounded
+  // shared memory; chunk j0 is row j0 / R, offset j0 % R)
   const int R = w * C;
-  int JC = R;
-  if (R > 160) {
-    JC = 1;
-    for (int c = 1; c <= 160; ++c)
-      if (R % c == 0) JC = c;
-  }
+  int JC = 1;
+  for (int c = 1; c <= 48 && c <= R; ++c)  // small chunks: several blocks per SM
+    if (R % c == 0) JC = c;
   launch_project<true>(ctx, mirror, img_w, C, w, anchors.xs, anchors.ys, anchors.nx,
                        anchors.count, w * w * C, JC, mean, basisT, d, out);
 }
