@@ -1,0 +1,90 @@
+"""Every device code path that can serve a request gives the same answer.
+
+The library picks a kernel per request (tile search, tcgen05 / mma.sync tile
+variants, warp-per-query fallback, thread-per-query budget kernel; subspace
+iteration or the direct eigensolver for the PCA fit; device or host tree
+build).  Selection can be forced per context with PERSYN_SEARCH /
+PERSYN_EIG / PERSYN_TREE; each variant is checked against the oracle here.
+"""
+import numpy as np
+import pytest
+
+from oracle.oracle import fit_pca
+from paper_2006_11851_b200 import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+api = pytest.importorskip("paper_2006_11851_b200.api")
+
+
+def _stage(size=40, out=56, G=2, seed=4):
+    ex = wl.rgbs_planes(wl.sinusoid_exemplar(size, 8, 2.0, seed), G)
+    init = wl.init_output(ex, out, out, G, seed)
+    return ex, init
+
+
+@pytest.mark.parametrize("variant", ["default", "warp", "mma", "hmma"])
+@pytest.mark.parametrize("d", [16, 32])
+def test_exact_search_variants_bit_exact(port, monkeypatch, variant, d):
+    if variant != "default":
+        monkeypatch.setenv("PERSYN_SEARCH", variant)
+    ctx = api.Context(0)
+    monkeypatch.delenv("PERSYN_SEARCH", raising=False)
+    ex, init = _stage()
+    cand = port.extract_all(ex, 8, 1)
+    mean, basis, _ = fit_pca(cand, d_fixed=d)
+    proj = port.project_all(cand, mean, basis)
+    ix = api.make_pca_tree_index(ex, 8, mean=mean, basis=basis, branching=8, max_depth=3,
+                                 hist_bins=16, ctx=ctx)
+    i_p, d_p, c_p = port.search_step(init, 8, 2, 2, cand, proj, mean, basis)
+    idx, dist, calls, _ = api.search_step(init, ix, 2, 2, api.QueryBudget.exact())
+    assert calls == c_p
+    assert np.array_equal(idx, i_p) and np.array_equal(dist, d_p)
+    # a seeded (EM) search goes through the same kernels with a previous assignment
+    cfg = api.OptimizerConfig(max_iterations=2, min_iterations=2, convergence_fraction=1e-9,
+                              nbhd_width=8, spacing=2, patch_width=2,
+                              budget=api.QueryBudget.exact())
+    out, stats = api.optimize_level(init, ix, cfg)
+    exm = port.build_histograms(ex, 16, 3)
+    out_p, st_p = port.optimize_level(init, 8, 2, 2, cand, proj, mean, basis, max_it=2,
+                                      min_it=2, frac=1e-9, bins=16, ex_mass=exm)
+    assert np.max(np.abs(out - out_p)) <= 1.0 / 255
+    assert [s.changed for s in stats] == [int(r[2]) for r in st_p]
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 8])
+def test_budget_kernels_agree(gpu_ctx, port, monkeypatch, m):
+    """backtrack(m): thread-per-query kernel (m <= 2) and warp-per-query kernel
+    (m > 2, and forced with PERSYN_SEARCH=warp) return identical answers."""
+    ex, init = _stage()
+    cand = port.extract_all(ex, 8, 1)
+    mean, basis, _ = fit_pca(cand, d_fixed=12)
+    monkeypatch.setenv("PERSYN_SEARCH", "warp")
+    warp_ctx = api.Context(0)
+    monkeypatch.delenv("PERSYN_SEARCH", raising=False)
+    res = []
+    for ctx in (gpu_ctx, warp_ctx):
+        ix = api.make_pca_tree_index(ex, 8, mean=mean, basis=basis, branching=4, max_depth=4,
+                                     seed=3, ctx=ctx)
+        res.append(api.search_step(init, ix, 2, 2, api.QueryBudget.backtrack(m)))
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    assert res[0][3] == res[1][3]  # points scanned
+
+
+def test_eigensolver_paths_agree(gpu_ctx, monkeypatch):
+    """Top-d PCA pairs by subspace iteration vs the direct DSYEVDX solver."""
+    ex, _ = _stage(size=48, G=2)
+    a = api.make_pca_tree_index(ex, 16, d_fixed=24, ctx=gpu_ctx)   # D = 1280: subspace
+    monkeypatch.setenv("PERSYN_EIG", "direct")
+    b = api.make_pca_tree_index(ex, 16, d_fixed=24, ctx=gpu_ctx)
+    monkeypatch.delenv("PERSYN_EIG", raising=False)
+    ma, ba, va = a.pca()
+    mb, bb, vb = b.pca()
+    assert np.array_equal(ma, mb)
+    assert np.allclose(va[:24], vb[:24], rtol=1e-10, atol=1e-13)
+    gaps = np.abs(np.diff(vb[:25])) / vb[0]
+    ok = np.ones(24, bool)
+    ok[:-1] &= gaps[:-1] > 1e-6
+    ok[1:] &= gaps[:-1] > 1e-6
+    ok &= gaps[:24] > 1e-6
+    assert np.allclose(np.abs(np.sum(ba * bb, axis=1))[ok], 1.0, atol=1e-8)
