@@ -301,6 +301,7 @@ class Ref:
             L.ref_kmtree_query.argtypes = [_VP, _VP, _I, _I, _I, _VP, _VP, _VP, _VP]
             L.ref_kmtree_leaves.argtypes = [_VP, _VP, _VP, _VP]
             L.ref_kmtree_structure_json.argtypes = [_VP, ct.c_char_p, _I64, _VP]
+            L.ref_trace_jsonl.argtypes = [_VP, _VP, _I, ct.c_char_p, _I64, _VP]
             L.ref_brute_force_nearest.argtypes = [_VP, _I64, _I, _VP, _VP, _VP]
             L.ref_index_create.restype = _VP
             L.ref_index_create.argtypes = [_VP, _I, _I, _I, _VP, _VP, _I, _I, _I, ct.c_uint64]
@@ -397,6 +398,18 @@ class Ref:
         nl = np.zeros(1, np.int64)
         self._check(self.L.ref_kmtree_leaves(h, _ptr(ids), _ptr(sizes), _ptr(nl)), "leaves")
         return ids, sizes[: nl[0]].copy()
+
+    def trace_jsonl(self, stats7, millis):
+        """EnergyTrace::to_jsonl of the given records (ref_trace_jsonl)."""
+        st = _c(stats7, np.float64)
+        ms = _c(millis, np.float64)
+        n = np.zeros(1, np.int64)
+        self._check(self.L.ref_trace_jsonl(_ptr(st), _ptr(ms), len(ms), None, 0, _ptr(n)),
+                    "trace_jsonl")
+        buf = ct.create_string_buffer(int(n[0]) + 1)
+        self._check(self.L.ref_trace_jsonl(_ptr(st), _ptr(ms), len(ms), buf, int(n[0]) + 1,
+                                           _ptr(n)), "trace_jsonl")
+        return buf.value.decode()
 
     def kmtree_structure_json(self, h):
         n = np.zeros(1, np.int64)

@@ -463,6 +463,32 @@ int ref_optimize_level(void* h, const double* init, int W, int H, int w, int sp,
   });
 }
 
+// EnergyTrace::to_jsonl (optimizer.cpp:411-424) over given iteration records
+// (stats7: iteration, energy, changed, nn_calls, ... as ref_optimize_level),
+// to pin the JSONL trace format of the device path.
+int ref_trace_jsonl(const double* stats7, const double* millis, int n, char* buf, int64_t cap,
+                    int64_t* len) {
+  return guard([&] {
+    EnergyTrace tr;
+    for (int i = 0; i < n; ++i) {
+      IterationStats it;
+      it.iteration = static_cast<int>(stats7[7 * i]);
+      it.energy = stats7[7 * i + 1];
+      it.changed = static_cast<std::int64_t>(stats7[7 * i + 2]);
+      it.nn_calls = static_cast<std::int64_t>(stats7[7 * i + 3]);
+      it.millis = millis[i];
+      tr.iterations.push_back(it);
+    }
+    const std::string out = tr.to_jsonl();
+    *len = static_cast<int64_t>(out.size());
+    if (buf && cap > 0) {
+      const size_t k = std::min<size_t>(out.size(), static_cast<size_t>(cap - 1));
+      std::memcpy(buf, out.data(), k);
+      buf[k] = 0;
+    }
+  });
+}
+
 // One pass of optimize_level's loop body (optimizer.cpp:453-497) driven
 // through the reference's own public functions (irls_weight, build_histograms,
 // histogram_penalty, update_step, assignment_distances, search_step,

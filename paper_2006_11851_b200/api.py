@@ -308,6 +308,20 @@ def make_vector_index(X: np.ndarray, variance_target: float = 0.95, branching: i
 
 
 # ---------------------------------------------------------------------------
+def trace_jsonl(stats) -> str:
+    """EnergyTrace::to_jsonl (optimizer.cpp:411-424): one compact
+    {"iter","energy","changed","nn_calls","millis"} object per line, keys in
+    that order, numbers in shortest round-trip form (as nlohmann::json)."""
+    import json as _json
+    out = []
+    for s in stats:
+        out.append(_json.dumps({"iter": int(s.iteration), "energy": float(s.energy),
+                                "changed": int(s.changed), "nn_calls": int(s.nn_calls),
+                                "millis": float(s.millis)}, separators=(",", ":")))
+        out.append("\n")
+    return "".join(out)
+
+
 def search_step(out: np.ndarray, index: SearchIndex, spacing: int, patch_width: int,
                 budget: QueryBudget):
     """(assignments, distances, nn_calls, points_scanned) — optimizer.cpp:275-348."""
