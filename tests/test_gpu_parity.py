@@ -328,3 +328,31 @@ def test_device_pca_fit_matches_numpy(gpu_ctx, port, G, w, kw):
     ok[1:] &= gaps[:-1] > 1e-6
     ok &= gaps[:k] > 1e-6
     assert np.allclose(np.abs(np.sum(basis * b2, axis=1))[ok], 1.0, atol=1e-6)
+
+
+@pytest.mark.slow
+def test_optimize_level_cfg1_finest_stage_matches_reference(gpu_ctx, port, ref):
+    """BASELINE cfg1 finest stage at full size with one guidance plane (C = 4,
+    the reference's own channel layout): 128^2 exemplar, 256^2 output, w = 8,
+    sp = 2 (15,625 anchors, 250,000 plan calls per search), d = 32 injected,
+    exact search, histogram matching on, 3 EM iterations — device vs the
+    reference's optimize_level (oracle/_ref, all host threads)."""
+    ex = wl.rgbs_planes(wl.sinusoid_exemplar(128, 16, 2.0, 1), 1)
+    init = wl.init_output(ex, 256, 256, 1, 1)
+    cand, mean, basis, proj = _injected(port, ex, 8, 32)
+    ix = api.make_pca_tree_index(ex, 8, mean=mean, basis=basis, branching=8, max_depth=3,
+                                 hist_bins=16, ctx=gpu_ctx)
+    cfg = api.OptimizerConfig(max_iterations=3, min_iterations=3, convergence_fraction=1e-9,
+                              nbhd_width=8, spacing=2, patch_width=2,
+                              budget=api.QueryBudget.exact())
+    out, stats = api.optimize_level(init, ix, cfg)
+    h = ref.index_create(ex, 8, mean, basis, kind="tree", branching=8, seed=1)
+    out_r, st_r, _ = h.optimize_level(init, 8, 2, 2, max_it=3, min_it=3, frac=1e-9, bins=16,
+                                      hist_on=True, mode="exact")
+    assert len(stats) == len(st_r) == 3
+    assert np.max(np.abs(out - out_r)) <= 1.0 / 255
+    q = lambda a: np.rint(np.clip(a, 0, 1) * 255)  # image_io.cpp:18-21
+    assert np.mean(q(out[:3]) != q(out_r[:3])) < 1e-4
+    for s, r in zip(stats, st_r):
+        assert s.changed == r[2] and s.nn_calls == r[3]
+        assert abs(s.energy - r[1]) <= 1e-4 * abs(r[1])
