@@ -432,8 +432,8 @@ __global__ void __launch_bounds__(128) search_budget_kernel(SearchArgs a) {
       double hk[kHeapCap];
       int32_t hn[kHeapCap], ht[kHeapCap];
       int size = 0;
-      auto less = [&](int i, int j) {
-        return hk[i] < hk[j] || (hk[i] == hk[j] && ht[i] < ht[j]);
+      auto less = [](const double* k, const int32_t* t, int i, int j) {
+        return k[i] < k[j] || (k[i] == k[j] && t[i] < t[j]);
       };
       auto push = [&](double k, int32_t node) {
         if (size == kHeapCap) {
@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(128) search_budget_kernel(SearchArgs a) {
         ht[i] = a.tree.tie ? a.tree.tie[node] : node;
         while (i > 0) {
           const int par = (i - 1) >> 1;
-          if (!less(i, par)) break;
+          if (!less(hk, ht, i, par)) break;
           const double tk = hk[i];
           hk[i] = hk[par];
           hk[par] = tk;
@@ -470,8 +470,8 @@ __global__ void __launch_bounds__(128) search_budget_kernel(SearchArgs a) {
         for (int i = 0;;) {  // sift down
           const int l = 2 * i + 1, r = l + 1;
           int m = i;
-          if (l < size && less(l, m)) m = l;
-          if (r < size && less(r, m)) m = r;
+          if (l < size && less(hk, ht, l, m)) m = l;
+          if (r < size && less(hk, ht, r, m)) m = r;
           if (m == i) break;
           const double tk = hk[i];
           hk[i] = hk[m];
