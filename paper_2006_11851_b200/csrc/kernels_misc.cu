@@ -127,6 +127,35 @@ __global__ void downsample_kernel(const double* __restrict__ in, int W, int H, i
   }
 }
 
+// Guidance ramps (BASELINE cfg: "row index / (H-1) as fp32", widened to
+// fp64): even planes vary with the row, odd planes with the column.  IEEE
+// fp32 division, identical to the host rule.
+__global__ void ramp_planes_kernel(int G, int W, int H, double* __restrict__ out) {
+  const int64_t P = (int64_t)W * H;
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < P * G;
+       f += (int64_t)gridDim.x * blockDim.x) {
+    const int g = (int)(f / P);
+    const int64_t i = f - (int64_t)g * P;
+    const int y = (int)(i / W), x = (int)(i - (int64_t)y * W);
+    double v;
+    if (g % 2 == 0)
+      v = H > 1 ? (double)__fdiv_rn((float)y, (float)(H - 1)) : 0.5;
+    else
+      v = W > 1 ? (double)__fdiv_rn((float)x, (float)(W - 1)) : 0.5;
+    out[f] = v;
+  }
+}
+
+void launch_ramp_planes(psg_ctx* ctx, int G, int W, int H, double* out) {
+  ProfScope _prof(ctx, K_PYRAMID);
+  const int64_t n = (int64_t)W * H * G;
+  if (n <= 0) return;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > (int64_t)ctx->num_sms * 32) blocks = (int64_t)ctx->num_sms * 32;
+  ramp_planes_kernel<<<(int)blocks, 256, 0, ctx->stream>>>(G, W, H, out);
+  PSG_LAUNCHED(ctx);
+}
+
 void launch_downsample(psg_ctx* ctx, const double* in, int W, int H, int f, double* out) {
   ProfScope _prof(ctx, K_PYRAMID);
   const int ow = W / f, oh = H / f;

@@ -326,6 +326,8 @@ void launch_gather_soa(psg_ctx* ctx, const double* proj, int64_t N, int d, const
                        double* soa);
 // Pyramid helpers.
 void launch_downsample(psg_ctx* ctx, const double* in, int W, int H, int f, double* out);
+// G guidance ramps [G][H][W] (row ramp on even planes, column ramp on odd ones).
+void launch_ramp_planes(psg_ctx* ctx, int G, int W, int H, double* out);
 void launch_upsample_bilinear(psg_ctx* ctx, const double* in, int W, int H, int f, double* out);
 void launch_fit_to(psg_ctx* ctx, const double* in, int W, int H, int ow, int oh, double* out);
 

@@ -1545,20 +1545,6 @@ uint64_t splitmix64(uint64_t x) {
   return x ^ (x >> 31);
 }
 
-// Guidance ramps as fp32 then widened (BASELINE cfg 0: "row index/63 as fp32").
-void ramp_planes(int G, int W, int H, double* out) {
-  const size_t P = (size_t)W * H;
-  for (int g = 0; g < G; ++g)
-    for (int y = 0; y < H; ++y)
-      for (int x = 0; x < W; ++x) {
-        double v;
-        if (g % 2 == 0)
-          v = H > 1 ? (double)((float)y / (float)(H - 1)) : 0.5;
-        else
-          v = W > 1 ? (double)((float)x / (float)(W - 1)) : 0.5;
-        out[g * P + (size_t)y * W + x] = v;
-      }
-}
 
 }  // namespace
 }  // namespace psg
@@ -1612,14 +1598,9 @@ extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, doubl
       }
       const size_t op = (size_t)ow[l] * oh[l];
       og_lv[l].alloc((size_t)G * op);
-      if (req->guidance_kind == 0) {
-        std::vector<double> g((size_t)G * lp), go((size_t)G * op);
-        ramp_planes(G, ew[l], eh[l], g.data());
-        ramp_planes(G, ow[l], oh[l], go.data());
-        PSG_CUDA(cudaMemcpyAsync(ex_lv[l].p + 3 * lp, g.data(), sizeof(double) * g.size(),
-                                 cudaMemcpyHostToDevice, ctx->stream));
-        og_lv[l].upload(ctx, go.data(), go.size());
-        PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (req->guidance_kind == 0) {  // ramps generated on the device
+        launch_ramp_planes(ctx, G, ew[l], eh[l], ex_lv[l].p + 3 * lp);
+        launch_ramp_planes(ctx, G, ow[l], oh[l], og_lv[l].p);
       } else {
         for (int g = 0; g < G; ++g) {
           if (f == 1) {
