@@ -144,6 +144,8 @@ int subspace_top_eigen(psg_ctx* ctx, cublasHandle_t cb, cusolverDnHandle_t cs, d
   }
   householder(Q.as<double>());
   const int max_it = 200;
+  double prev_worst = 0.0;
+  int prev_it = 0;
   std::vector<double> hth(k), hres(m);
   for (int it = 1; it <= max_it; ++it) {
     cublas_check(cublasDsymm(cb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, D, k, &one, cov, D,
@@ -175,6 +177,20 @@ int subspace_top_eigen(psg_ctx* ctx, cublasHandle_t cb, cusolverDnHandle_t cs, d
       if (verbose)
         fprintf(stderr, "[persyn]     subspace it %d (k=%d): max residual %.3e x theta_max\n", it,
                 k, worst / scale);
+      // too slow a contraction (flat spectrum around the m-th eigenvalue):
+      // hand over to the direct solver instead of iterating to the cap
+      if (prev_worst > 0.0 && worst > 1e-11 * scale) {
+        const double rate = std::pow(worst / prev_worst, 1.0 / (it - prev_it));
+        const double need = rate < 1.0 ? std::log(1e-11 * scale / worst) / std::log(rate) : 1e30;
+        if (it + need > max_it) {
+          if (verbose)
+            fprintf(stderr, "[persyn]     subspace: %.3f per step, %.0f more steps: direct solver\n",
+                    rate, need);
+          return 0;
+        }
+      }
+      prev_worst = worst;
+      prev_it = it;
       if (worst <= 1e-11 * scale) {
         PSG_CUDA(cudaMemcpyAsync(evals, theta.as<double>() + (k - m), sizeof(double) * m,
                                  cudaMemcpyDeviceToDevice, st));
