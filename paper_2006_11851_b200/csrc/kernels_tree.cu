@@ -73,9 +73,9 @@ struct Lv {
        i += (int64_t)gridDim.x * blockDim.x)
 
 __global__ void node_of_kernel(Lv v, int32_t* node_of) {
-  GRID_LOOP(node, v.L) {
-    const int64_t s = v.nstart[node];
-    for (int64_t p = s; p < s + v.ncount[node]; ++p) node_of[p] = (int32_t)node;
+  GRID_LOOP(t, (int64_t)v.nchunks * kChunk) {  // (chunk, offset): one position each
+    const int ch = (int)(t / kChunk), i = (int)(t % kChunk);
+    if (i < v.clen[ch]) node_of[v.cbeg[ch] + i] = v.cnode[ch];
   }
 }
 
@@ -185,43 +185,74 @@ __global__ void kpp_part_kernel(Lv v, Km k, int c, double* pd2) {
 }
 
 // D^2 sampling: r = u * total, first point where the running remainder
-// reaches <= 0 (km_tree.cpp:54-63), walked chunk by chunk.
+// reaches <= 0 (km_tree.cpp:54-63), walked chunk by chunk.  One warp per
+// node: lanes load 32 consecutive values (coalesced) and the sequential
+// subtraction runs over shuffled registers, in the same order as a serial walk.
 __global__ void kpp_pick_kernel(Lv v, Km k, int c, const double* pd2) {
-  GRID_LOOP(node, v.L) {
-    if (!k.picking[node] || k.nc[node] != c) continue;
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t node = wid; node < v.L; node += nw) {
+    if (!k.picking[node] || k.nc[node] != c) continue;  // warp-uniform
     const int c0 = v.nch0[node], nch = v.nnch[node];
     double total = 0.0;
-    for (int i = 0; i < nch; ++i) total += pd2[c0 + i];
+    for (int g = 0; g < nch; g += 32) {
+      const double x = g + lane < nch ? pd2[c0 + g + lane] : 0.0;
+      const int m = min(32, nch - g);
+      for (int i = 0; i < m; ++i) total += __shfl_sync(0xffffffffu, x, i);
+    }
     if (!(total > 0.0)) {
-      k.picking[node] = 0;
+      if (lane == 0) k.picking[node] = 0;
       continue;
     }
     uint64_t s = k.rng[node];
     double r = (double)(smix_next(s) >> 11) * (1.0 / 9007199254740992.0) * total;
-    k.rng[node] = s;
     int64_t chosen = v.nstart[node] + v.ncount[node] - 1;
-    for (int i = 0; i < nch; ++i) {
-      const int ch = c0 + i;
-      if (r - pd2[ch] > 0.0 && i + 1 < nch) {
-        r -= pd2[ch];
-        continue;
-      }
-      const int64_t b = v.cbeg[ch];
-      bool found = false;
-      for (int q = 0; q < v.clen[ch]; ++q) {
-        r -= k.d2[b + q];
-        if (r <= 0.0) {
-          chosen = b + q;
-          found = true;
-          break;
+    // chunk walk: skip whole chunks while the remainder stays positive
+    int ch_sel = nch - 1;
+    for (int g = 0; g < nch; g += 32) {
+      const double x = g + lane < nch ? pd2[c0 + g + lane] : 0.0;
+      const int m = min(32, nch - g);
+      int hit = -1;
+      for (int i = 0; i < m; ++i) {
+        const double xi = __shfl_sync(0xffffffffu, x, i);
+        if (hit < 0) {
+          if (r - xi > 0.0 && g + i + 1 < nch) r -= xi;
+          else hit = g + i;
         }
       }
-      if (found || i + 1 == nch) break;
+      if (hit >= 0) {
+        ch_sel = hit;
+        break;
+      }
     }
+    {
+      const int ch = c0 + ch_sel;
+      const int64_t b = v.cbeg[ch];
+      const int n = v.clen[ch];
+      bool found = false;
+      for (int g = 0; g < n && !found; g += 32) {
+        const double x = g + lane < n ? k.d2[b + g + lane] : 0.0;
+        const int m = min(32, n - g);
+        for (int i = 0; i < m; ++i) {
+          const double xi = __shfl_sync(0xffffffffu, x, i);
+          if (!found) {
+            r -= xi;
+            if (r <= 0.0) {
+              chosen = b + g + i;
+              found = true;
+            }
+          }
+        }
+      }
+    }
+    if (lane == 0) k.rng[node] = s;
     const double* src = v.P + (int64_t)v.ids[chosen] * v.d;
-    for (int j = 0; j < v.d; ++j) k.centers[((int64_t)node * kMaxB + c) * v.d + j] = src[j];
-    k.nc[node] = c + 1;
-    if (c + 1 >= v.kk[node]) k.picking[node] = 0;
+    for (int j = lane; j < v.d; j += 32) k.centers[((int64_t)node * kMaxB + c) * v.d + j] = src[j];
+    if (lane == 0) {
+      k.nc[node] = c + 1;
+      if (c + 1 >= v.kk[node]) k.picking[node] = 0;
+    }
   }
 }
 
@@ -245,7 +276,50 @@ __global__ void assign_kernel(Lv v, Km k) {
   }
 }
 
-__global__ void lloyd_part_kernel(Lv v, Km k, double* psc, int32_t* pcnt) {
+// Per chunk, the positions of each cluster in chunk order (a stable counting
+// sort): the sums below then walk only their own cluster's points.
+__global__ void lloyd_sort_kernel(Lv v, Km k, int32_t* sorted, int32_t* pcnt) {
+  // one warp per chunk: ballots per cluster over groups of 32 points
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t ch = wid; ch < v.nchunks; ch += nw) {
+    const int node = v.cnode[ch];
+    if (v.kk[node] <= 0 || k.done[node]) continue;  // warp-uniform
+    const int64_t b = v.cbeg[ch];
+    const int n = v.clen[ch], nc = k.nc[node];
+    // counts
+    int my = 0;  // lane c < nc holds cluster c's count
+    for (int g = 0; g < n; g += 32) {
+      const int a = g + lane < n ? k.asg[b + g + lane] : -1;
+      for (int c = 0; c < nc; ++c) {
+        const int cnt = __popc(__ballot_sync(0xffffffffu, a == c));
+        if (lane == c) my += cnt;
+      }
+    }
+    if (lane < nc) pcnt[(int64_t)ch * kMaxB + lane] = my;
+    // exclusive offsets
+    int off = 0;
+    for (int c = 0; c < nc; ++c) {
+      const int cc = __shfl_sync(0xffffffffu, my, c);
+      if (lane > c) off += cc;
+    }
+    // stable scatter: chunk order within each cluster
+    for (int g = 0; g < n; g += 32) {
+      const int a = g + lane < n ? k.asg[b + g + lane] : -1;
+      for (int c = 0; c < nc; ++c) {
+        const unsigned m = __ballot_sync(0xffffffffu, a == c);
+        const int base = __shfl_sync(0xffffffffu, off, c);
+        if (a == c) sorted[b + base + __popc(m & lt)] = (int32_t)(g + lane);
+        if (lane == c) off += __popc(m);
+      }
+    }
+  }
+}
+
+__global__ void lloyd_part_kernel(Lv v, Km k, const int32_t* sorted, const int32_t* pcnt,
+                                  double* psc) {
   GRID_LOOP(t, (int64_t)v.nchunks * kMaxB * v.d) {
     const int j = (int)(t % v.d);
     const int64_t cc = t / v.d;
@@ -254,39 +328,36 @@ __global__ void lloyd_part_kernel(Lv v, Km k, double* psc, int32_t* pcnt) {
     const int node = v.cnode[ch];
     if (v.kk[node] <= 0 || k.done[node] || c >= k.nc[node]) continue;
     const int64_t b = v.cbeg[ch];
+    int first = 0;
+    for (int o = 0; o < c; ++o) first += pcnt[(int64_t)ch * kMaxB + o];
+    const int n = pcnt[cc];
     double s = 0.0;
-    int cnt = 0;
-    for (int i = 0; i < v.clen[ch]; ++i) {
-      if (k.asg[b + i] != c) continue;
-      s += v.P[(int64_t)v.ids[b + i] * v.d + j];
-      ++cnt;
-    }
+#pragma unroll 4
+    for (int i = 0; i < n; ++i)  // chunk order within the cluster
+      s += v.P[(int64_t)v.ids[b + sorted[b + first + i]] * v.d + j];
     psc[t] = s;
-    if (j == 0) pcnt[cc] = cnt;
   }
 }
 
 __global__ void lloyd_update_kernel(Lv v, Km k, const double* psc, const int32_t* pcnt,
                                     double* mv2) {
-  GRID_LOOP(t, (int64_t)v.L * kMaxB) {
-    const int node = (int)(t / kMaxB), c = (int)(t % kMaxB);
+  GRID_LOOP(t, (int64_t)v.L * kMaxB * v.d) {
+    const int j = (int)(t % v.d);
+    const int64_t nc_ = t / v.d;
+    const int node = (int)(nc_ / kMaxB), c = (int)(nc_ % kMaxB);
     mv2[t] = 0.0;
     if (v.kk[node] <= 0 || k.done[node] || c >= k.nc[node]) continue;
     const int c0 = v.nch0[node], nch = v.nnch[node];
     int64_t n = 0;
     for (int i = 0; i < nch; ++i) n += pcnt[(int64_t)(c0 + i) * kMaxB + c];
     if (n == 0) continue;  // empty cluster keeps its centroid (km_tree.cpp:95-96)
-    double m = 0.0;
+    double s = 0.0;
+    for (int i = 0; i < nch; ++i) s += psc[(((int64_t)(c0 + i) * kMaxB) + c) * v.d + j];
+    const double nv = s / (double)n;
     double* ctr = k.centers + ((int64_t)node * kMaxB + c) * v.d;
-    for (int j = 0; j < v.d; ++j) {
-      double s = 0.0;
-      for (int i = 0; i < nch; ++i) s += psc[(((int64_t)(c0 + i) * kMaxB) + c) * v.d + j];
-      const double nv = s / (double)n;
-      const double dd = nv - ctr[j];
-      m += dd * dd;
-      ctr[j] = nv;
-    }
-    mv2[t] = m;
+    const double dd = nv - ctr[j];
+    mv2[t] = dd * dd;
+    ctr[j] = nv;
   }
 }
 
@@ -294,7 +365,11 @@ __global__ void lloyd_conv_kernel(Lv v, Km k, const double* mv2, int* active) {
   GRID_LOOP(node, v.L) {
     if (v.kk[node] <= 0 || k.done[node]) continue;
     double m = 0.0;
-    for (int c = 0; c < k.nc[node]; ++c) m = fmax(m, sqrt(mv2[(int64_t)node * kMaxB + c]));
+    for (int c = 0; c < k.nc[node]; ++c) {
+      double m2 = 0.0;  // squared move of centre c, dims in order
+      for (int j = 0; j < v.d; ++j) m2 += mv2[((int64_t)node * kMaxB + c) * v.d + j];
+      m = fmax(m, sqrt(m2));
+    }
     if (m < 1e-6) k.done[node] = 1;  // km_tree.cpp:109
     else atomicAdd(active, 1);
   }
@@ -479,7 +554,8 @@ HostTree build_tree_device(psg_ctx* ctx, const double* P, int64_t N, int d, int 
 
     // positions of earlier leaves belong to no node of this level (-1)
     PSG_CUDA(cudaMemsetAsync(node_of.p, 0xFF, sizeof(int32_t) * N, st));
-    node_of_kernel<<<grid_for(ctx, L, 128), 128, 0, st>>>(v, node_of.as<int32_t>());
+    node_of_kernel<<<grid_for(ctx, (int64_t)nchunks * kChunk, 256), 256, 0, st>>>(
+        v, node_of.as<int32_t>());
     PSG_LAUNCHED(ctx);
     // ---- statistics ----
     DevArr psum(sizeof(double) * (size_t)nchunks * dd, st);
@@ -528,20 +604,25 @@ HostTree build_tree_device(psg_ctx* ctx, const double* P, int64_t N, int d, int 
         PSG_LAUNCHED(ctx);
         kpp_part_kernel<<<grid_for(ctx, nchunks, 128), 128, 0, st>>>(v, k, c, pd2.as<double>());
         PSG_LAUNCHED(ctx);
-        kpp_pick_kernel<<<grid_for(ctx, L, 128), 128, 0, st>>>(v, k, c, pd2.as<double>());
+        kpp_pick_kernel<<<grid_for(ctx, (int64_t)L * 32, 128), 128, 0, st>>>(v, k, c,
+                                                                          pd2.as<double>());
         PSG_LAUNCHED(ctx);
       }
       DevArr psc(sizeof(double) * (size_t)nchunks * kMaxB * dd, st);
       DevArr pcnt(sizeof(int32_t) * (size_t)nchunks * kMaxB, st);
-      DevArr mv2(sizeof(double) * (size_t)L * kMaxB, st);
+      DevArr mv2(sizeof(double) * (size_t)L * kMaxB * dd, st);
+      DevArr sorted(sizeof(int32_t) * (size_t)N, st);
       DevArr active(sizeof(int), st);
       assign_kernel<<<grid_for(ctx, N, 256), 256, 0, st>>>(v, k);
       PSG_LAUNCHED(ctx);
       for (int sweep = 0; sweep < 20; ++sweep) {  // km_tree.cpp:86-111
-        lloyd_part_kernel<<<grid_for(ctx, (int64_t)nchunks * kMaxB * dd, 128), 128, 0, st>>>(
-            v, k, psc.as<double>(), pcnt.as<int32_t>());
+        lloyd_sort_kernel<<<grid_for(ctx, (int64_t)nchunks * 32, 128), 128, 0, st>>>(
+            v, k, sorted.as<int32_t>(), pcnt.as<int32_t>());
         PSG_LAUNCHED(ctx);
-        lloyd_update_kernel<<<grid_for(ctx, (int64_t)L * kMaxB, 128), 128, 0, st>>>(
+        lloyd_part_kernel<<<grid_for(ctx, (int64_t)nchunks * kMaxB * dd, 128), 128, 0, st>>>(
+            v, k, sorted.as<int32_t>(), pcnt.as<int32_t>(), psc.as<double>());
+        PSG_LAUNCHED(ctx);
+        lloyd_update_kernel<<<grid_for(ctx, (int64_t)L * kMaxB * dd, 128), 128, 0, st>>>(
             v, k, psc.as<double>(), pcnt.as<int32_t>(), mv2.as<double>());
         PSG_LAUNCHED(ctx);
         PSG_CUDA(cudaMemsetAsync(active.p, 0, sizeof(int), st));
