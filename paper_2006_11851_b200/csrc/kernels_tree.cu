@@ -257,19 +257,45 @@ __global__ void kpp_pick_kernel(Lv v, Km k, int c, const double* pd2) {
 }
 
 // ---- Lloyd ------------------------------------------------------------------------------
+// Nearest centre per point (strict <: the lowest centre wins ties,
+// km_tree.cpp:76-80).  DP > 0: the point is held in registers (loaded once for
+// all centres); DP = 0: generic d.
+template <int DP>
 __global__ void assign_kernel(Lv v, Km k) {
   GRID_LOOP(p, v.N) {
     const int node = v.node_of[p];
     if (node < 0 || v.kk[node] <= 0 || k.done[node]) continue;
     const double* x = v.P + (int64_t)v.ids[p] * v.d;
     const double* cs = k.centers + (int64_t)node * kMaxB * v.d;
+    const int nc = k.nc[node];
     int best = 0;
-    double bd = dist2_p(x, cs, v.d);
-    for (int c = 1; c < k.nc[node]; ++c) {
-      const double dd = dist2_p(x, cs + (int64_t)c * v.d, v.d);
-      if (dd < bd) {  // strict: the lowest centre wins ties (km_tree.cpp:76-80)
-        bd = dd;
-        best = c;
+    double bd = 0.0;
+    if (DP > 0) {
+      double xr[DP > 0 ? DP : 1];
+#pragma unroll
+      for (int j = 0; j < DP; ++j) xr[j] = j < v.d ? x[j] : 0.0;
+      for (int c = 0; c < nc; ++c) {
+        const double* cc = cs + (int64_t)c * v.d;
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < DP; ++j)
+          if (j < v.d) {
+            const double t = xr[j] - cc[j];
+            acc += t * t;
+          }
+        if (c == 0 || acc < bd) {
+          bd = acc;
+          best = c;
+        }
+      }
+    } else {
+      bd = dist2_p(x, cs, v.d);
+      for (int c = 1; c < nc; ++c) {
+        const double dd = dist2_p(x, cs + (int64_t)c * v.d, v.d);
+        if (dd < bd) {
+          bd = dd;
+          best = c;
+        }
       }
     }
     k.asg[p] = best;
@@ -450,6 +476,16 @@ int grid_for(psg_ctx* ctx, int64_t n, int threads) {
   return (int)std::max<int64_t>(b, 1);
 }
 
+void launch_assign(psg_ctx* ctx, const Lv& v, const Km& k, int64_t N) {
+  const int g = grid_for(ctx, N, 256);
+  if (v.d <= 32)
+    assign_kernel<32><<<g, 256, 0, ctx->stream>>>(v, k);
+  else if (v.d <= 64)
+    assign_kernel<64><<<g, 256, 0, ctx->stream>>>(v, k);
+  else
+    assign_kernel<0><<<g, 256, 0, ctx->stream>>>(v, k);
+}
+
 }  // namespace
 
 HostTree build_tree_device(psg_ctx* ctx, const double* P, int64_t N, int d, int branching,
@@ -613,7 +649,7 @@ HostTree build_tree_device(psg_ctx* ctx, const double* P, int64_t N, int d, int 
       DevArr mv2(sizeof(double) * (size_t)L * kMaxB * dd, st);
       DevArr sorted(sizeof(int32_t) * (size_t)N, st);
       DevArr active(sizeof(int), st);
-      assign_kernel<<<grid_for(ctx, N, 256), 256, 0, st>>>(v, k);
+      launch_assign(ctx, v, k, N);
       PSG_LAUNCHED(ctx);
       for (int sweep = 0; sweep < 20; ++sweep) {  // km_tree.cpp:86-111
         lloyd_sort_kernel<<<grid_for(ctx, (int64_t)nchunks * 32, 128), 128, 0, st>>>(
@@ -629,7 +665,7 @@ HostTree build_tree_device(psg_ctx* ctx, const double* P, int64_t N, int d, int 
         lloyd_conv_kernel<<<grid_for(ctx, L, 128), 128, 0, st>>>(v, k, mv2.as<double>(),
                                                                  active.as<int>());
         PSG_LAUNCHED(ctx);
-        assign_kernel<<<grid_for(ctx, N, 256), 256, 0, st>>>(v, k);
+        launch_assign(ctx, v, k, N);
         PSG_LAUNCHED(ctx);
         if (sweep % 4 == 3) {
           int h = 0;
