@@ -242,7 +242,10 @@ __global__ void __launch_bounds__(kStatsThreads) stats_partial_kernel(StatsArgs 
       const double d = a.after_dist[i];
       la = dadd(la, dmul(dmul(a.eff[i], d), d));  // optimizer.cpp:482
     }
-    if (a.next_dist) en = dadd(en, pow_cr(a.next_dist[i], a.r));  // optimizer.cpp:129
+    // energy sum d^r (optimizer.cpp:129): a telemetry value with a 1e-4
+    // tolerance (the summation order differs anyway), so CUDA's pow (< 2 ulp)
+    // instead of the correctly rounded one the IRLS weights need
+    if (a.next_dist) en = dadd(en, pow(a.next_dist[i], a.r));
     if (a.cur_idx && a.next_idx) ch += a.cur_idx[i] != a.next_idx[i];
     if (a.scanned) {
       su += a.scanned[i];
