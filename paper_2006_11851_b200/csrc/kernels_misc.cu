@@ -156,6 +156,48 @@ void launch_ramp_planes(psg_ctx* ctx, int G, int W, int H, double* out) {
   PSG_LAUNCHED(ctx);
 }
 
+// Seed for a stage's first search from the previous stage's assignment
+// (synthesize driver): each new anchor takes the previous anchor whose window
+// centre is nearest (in the previous stage's pixel grid, scale = 1 for the
+// next window size of a level, 2^k across levels) and shifts that anchor's
+// exemplar window by the same offset.  Only the search bound uses it.
+__device__ __forceinline__ int nearest_centre(const int32_t* __restrict__ pos, int n, double half,
+                                              double c) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if ((double)pos[mid] + half <= c) lo = mid;
+    else hi = mid - 1;
+  }
+  if (lo + 1 < n && fabs((double)pos[lo + 1] + half - c) < fabs((double)pos[lo] + half - c)) ++lo;
+  return lo;
+}
+
+__global__ void carry_seed_kernel(CarryArgs a) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < a.nq; q += stride) {
+    const int bx = (int)(q % a.nx), by = (int)(q / a.nx);
+    const double inv = 1.0 / a.scale, ph = 0.5 * a.pw;
+    const double cx = ((double)a.xs[bx] + 0.5 * a.w) * inv;
+    const double cy = ((double)a.ys[by] + 0.5 * a.w) * inv;
+    const int j = nearest_centre(a.pxs, a.pnx, ph, cx);
+    const int k = nearest_centre(a.pys, a.pny, ph, cy);
+    const int32_t e = a.pidx[(int64_t)k * a.pnx + j];
+    const double ecx = (double)(e % a.pnxe) + ph + (cx - ((double)a.pxs[j] + ph));
+    const double ecy = (double)(e / a.pnxe) + ph + (cy - ((double)a.pys[k] + ph));
+    const int tx = min(max((int)lrint(ecx * a.scale - 0.5 * a.w), 0), a.nxe - 1);
+    const int ty = min(max((int)lrint(ecy * a.scale - 0.5 * a.w), 0), a.nye - 1);
+    a.out[q] = ty * a.nxe + tx;
+  }
+}
+
+void launch_carry_seed(psg_ctx* ctx, const CarryArgs& a) {
+  ProfScope _prof(ctx, K_PYRAMID);
+  if (a.nq <= 0) return;
+  carry_seed_kernel<<<grid_cap(ctx, a.nq, 256), 256, 0, ctx->stream>>>(a);
+  PSG_LAUNCHED(ctx);
+}
+
 void launch_downsample(psg_ctx* ctx, const double* in, int W, int H, int f, double* out) {
   ProfScope _prof(ctx, K_PYRAMID);
   const int ow = W / f, oh = H / f;

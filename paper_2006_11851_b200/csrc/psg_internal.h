@@ -328,6 +328,21 @@ void launch_gather_soa(psg_ctx* ctx, const double* proj, int64_t N, int d, const
 void launch_downsample(psg_ctx* ctx, const double* in, int W, int H, int f, double* out);
 // G guidance ramps [G][H][W] (row ramp on even planes, column ramp on odd ones).
 void launch_ramp_planes(psg_ctx* ctx, int G, int W, int H, double* out);
+// Synthesize driver: first-search seeds carried from the previous stage.
+struct CarryArgs {
+  const int32_t* xs;   // new stage: owned anchor columns / rows (device)
+  const int32_t* ys;
+  int nx;
+  int64_t nq;
+  int w, nxe, nye;     // new window, exemplar window grid
+  const int32_t* pidx; // previous stage: final assignment [pny][pnx]
+  const int32_t* pxs;
+  const int32_t* pys;
+  int pnx, pny, pw, pnxe;
+  int scale;           // previous pixel grid -> new (1, or 2^levels)
+  int32_t* out;        // [nq]
+};
+void launch_carry_seed(psg_ctx* ctx, const CarryArgs& a);
 void launch_upsample_bilinear(psg_ctx* ctx, const double* in, int W, int H, int f, double* out);
 void launch_fit_to(psg_ctx* ctx, const double* in, int W, int H, int ow, int oh, double* out);
 

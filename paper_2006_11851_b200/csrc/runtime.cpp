@@ -643,7 +643,9 @@ void level_set_hist(psg_level& L, const double* ex_hist_host) {
 AnchorSet owned_anchors(psg_level& L) { return AnchorSet{L.xs.p, L.ys.p + L.nh, L.nx, L.Ao}; }
 
 // E-step over the owned anchors of the level's current (local) image.
-void level_search(psg_level& L, bool seeded, int32_t* out_idx, double* out_dist) {
+// seed: per-owned-anchor exemplar ids evaluated first (only the bound; the
+// result does not depend on it), or null.
+void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* out_dist) {
   psg_ctx* ctx = L.ctx;
   const Index& ix = *L.ix;
   const AnchorSet as = owned_anchors(L);
@@ -657,8 +659,6 @@ void level_search(psg_level& L, bool seeded, int32_t* out_idx, double* out_dist)
     qs.xs = as.xs;
     qs.ys = as.ys;
     qs.nx = as.nx;
-    // the previous assignment seeds the bound (the result is seed-independent)
-    const int32_t* seed = seeded ? L.cur_idx.p + L.off : nullptr;
     launch_brute_search(ctx, ix, qs, L.Ao, seed, out_idx + L.off, L.d2.p, L.scanned.p,
                         L.exact_evals.p);
     PSG_CUDA(cudaMemsetAsync(L.visited.p, 0, sizeof(int32_t) * L.Ao, ctx->stream));
@@ -673,7 +673,7 @@ void level_search(psg_level& L, bool seeded, int32_t* out_idx, double* out_dist)
   a.q = L.qproj.p;
   a.nq = L.Ao;
   a.d = ix.d;
-  a.seed_idx = (seeded && L.cfg.budget.mode == PSG_EXACT) ? L.cur_idx.p + L.off : nullptr;
+  a.seed_idx = L.cfg.budget.mode == PSG_EXACT ? seed : nullptr;
   a.proj = ix.proj;
   a.proj_soa = ix.proj_soa;
   a.proj32_q4 = ix.proj32_q4;
@@ -707,11 +707,12 @@ void level_read_stats(psg_level& L) {
   check_flags(L.ctx);  // synchronizes the stream
 }
 
-void level_prime(psg_level& L) {
+// seed (optional, device, one id per owned anchor): see level_search.
+void level_prime(psg_level& L, const int32_t* seed = nullptr) {
   if (L.primed) return;
   psg_ctx* ctx = L.ctx;
   PSG_CUDA(cudaEventRecord(L.ev0, ctx->stream));
-  level_search(L, false, L.cur_idx.p, L.cur_dist.p);
+  level_search(L, seed, L.cur_idx.p, L.cur_dist.p);
   StatsArgs s{};
   s.scanned = L.scanned.p;
   s.mult = L.mult.p;
@@ -800,7 +801,7 @@ void phase_search(psg_level& L) {
   psg_ctx* ctx = L.ctx;
   launch_rescore_windows(ctx, L.mirror.p, L.W, L.C, L.w, owned_anchors(L), *L.ix,
                          L.cur_idx.p + L.off, L.after.p + L.off);
-  level_search(L, true, L.next_idx.p, L.next_dist.p);
+  level_search(L, L.cur_idx.p + L.off, L.next_idx.p, L.next_dist.p);
   StatsArgs s{};
   s.cur_dist = L.cur_dist.p + L.off;
   s.after_dist = L.after.p + L.off;
@@ -1640,6 +1641,12 @@ extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, doubl
     rep.part1_millis = now_ms() - t0;
 
     const double t1 = now_ms();
+    // the previous stage's final assignment seeds each stage's first search
+    struct Carry {
+      DBuf<int32_t> idx, xs, ys;
+      int nx = 0, ny = 0, nh = 0, w = 0, nxe = 0, level = -1;
+      int64_t off = 0;
+    } carry;
     for (int l = 0; l < L; ++l) {
       const int W = ow[l], H = oh[l];
       const size_t op = (size_t)W * H;
@@ -1681,18 +1688,58 @@ extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, doubl
         PSG_CUDA(cudaMemcpyAsync(lv.planes.p, state.p, sizeof(double) * C * op,
                                  cudaMemcpyDeviceToDevice, ctx->stream));
         launch_make_mirror(ctx, lv.planes.p, C, W, H, lv.mirror.p);
-        level_prime(lv);
+        DBuf<int32_t> seeds;
+        if (carry.level >= 0 && !std::getenv("PERSYN_NO_CARRY")) {
+          const AnchorSet as = owned_anchors(lv);
+          seeds.alloc((size_t)as.count);
+          CarryArgs ca{};
+          ca.xs = as.xs;
+          ca.ys = as.ys;
+          ca.nx = as.nx;
+          ca.nq = as.count;
+          ca.w = w;
+          ca.nxe = index->impl.nxe;
+          ca.nye = index->impl.eh - w + 1;
+          ca.pidx = carry.idx.p + carry.off;
+          ca.pxs = carry.xs.p;
+          ca.pys = carry.ys.p + carry.nh;
+          ca.pnx = carry.nx;
+          ca.pny = carry.ny;
+          ca.pw = carry.w;
+          ca.pnxe = carry.nxe;
+          ca.scale = 1 << (l - carry.level);
+          ca.out = seeds.p;
+          launch_carry_seed(ctx, ca);
+        }
+        level_prime(lv, seeds.p);
+        if (std::getenv("PERSYN_VERBOSE"))
+          fprintf(stderr, "[persyn] stage l=%d w=%d: first search %.2f ms (%s)\n", l, w,
+                  lv.pending_ms, seeds.p ? "carried seed" : "unseeded");
         psg_iter_stats last{};
         int iters = 0;
         int64_t calls = 0;
+        const bool verbose = std::getenv("PERSYN_VERBOSE") != nullptr;
+        std::string its;
         for (int it = 0; it < cfg.max_iterations; ++it) {
           const bool conv = level_step(lv, &last, true);
           calls += last.nn_calls;
           ++iters;
+          if (verbose) its += " " + std::to_string(last.millis).substr(0, 5);
           if (conv) break;
         }
+        if (verbose) fprintf(stderr, "[persyn] stage l=%d w=%d: iteration ms%s\n", l, w, its.c_str());
         PSG_CUDA(cudaMemcpyAsync(state.p, lv.planes.p, sizeof(double) * C * op,
                                  cudaMemcpyDeviceToDevice, ctx->stream));
+        std::swap(carry.idx, lv.cur_idx);  // the level frees the swapped-in buffers
+        std::swap(carry.xs, lv.xs);
+        std::swap(carry.ys, lv.ys);
+        carry.nx = lv.nx;
+        carry.ny = (int)(lv.Ao / lv.nx);
+        carry.nh = lv.nh;
+        carry.off = lv.off;
+        carry.w = w;
+        carry.nxe = index->impl.nxe;
+        carry.level = l;
         PSG_CUDA(cudaStreamSynchronize(ctx->stream));
         if (rep.n_stages < 16) {
           psg_stage_report& sr = rep.stages[rep.n_stages++];
@@ -1715,9 +1762,15 @@ extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, doubl
           fprintf(stderr, "[persyn] stage l=%d w=%d: index %.2f ms, optimize %.2f ms\n", l, w,
                   index_ms, now_ms() - to);
         }
-        if (std::getenv("PERSYN_VERBOSE"))
-          fprintf(stderr, "[persyn] stage l=%d w=%d: wall incl. teardown %.2f ms\n", l, w,
-                  now_ms() - ti);
+        if (std::getenv("PERSYN_VERBOSE")) {
+          cudaMemPool_t pool;
+          uint64_t cur = 0, high = 0;
+          PSG_CUDA(cudaDeviceGetDefaultMemPool(&pool, ctx->device));
+          PSG_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &cur));
+          PSG_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &high));
+          fprintf(stderr, "[persyn] stage l=%d w=%d: wall incl. teardown %.2f ms (pool reserved "
+                  "%.0f MB, used high %.0f MB)\n", l, w, now_ms() - ti, cur / 1e6, high / 1e6);
+        }
       }
     }
     rep.part2_millis = now_ms() - t1;

@@ -237,6 +237,27 @@ def test_synthesize_runs_multires(gpu_ctx):
     assert rep["total_nn_calls"] > 0
 
 
+def test_synthesize_carried_seed_is_result_neutral(gpu_ctx, monkeypatch):
+    """The driver seeds each stage's first search with the previous stage's
+    assignment; exact search is a lexicographic min, so the seed may change the
+    work, never the result."""
+    ex = wl.rgbs_planes(wl.sinusoid_exemplar(64, 16, 2.0, 3), 2)
+    cfg = api.OptimizerConfig(max_iterations=2, min_iterations=2, convergence_fraction=1e-9,
+                              budget=api.QueryBudget.exact())
+    runs = []
+    for carry in (True, False):
+        if carry:
+            monkeypatch.delenv("PERSYN_NO_CARRY", raising=False)
+        else:
+            monkeypatch.setenv("PERSYN_NO_CARRY", "1")
+        runs.append(api.synthesize(ex, 128, 128, 3, (16, 8), cfg, variance_target=0.95, d_cap=32,
+                                   branching=8, max_depth=3, seed=1))
+    (o1, r1), (o2, r2) = runs
+    assert np.array_equal(o1, o2)
+    assert [s["final_energy"] for s in r1["stages"]] == [s["final_energy"] for s in r2["stages"]]
+    assert r1["total_nn_calls"] == r2["total_nn_calls"]
+
+
 @pytest.mark.parametrize("size,out,G,d,b,depth", [(128, 256, 2, 32, 8, 4), (256, 1024, 2, 32, 8, 4),
                                                   (96, 192, 1, 48, 16, 3)])
 def test_exact_search_full_size_sampled(gpu_ctx, port, size, out, G, d, b, depth):
