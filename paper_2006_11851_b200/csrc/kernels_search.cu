@@ -977,6 +977,13 @@ __global__ void __launch_bounds__(256) search_exact_kernel(SearchArgs a) {
 // lexicographic (fp64 dist^2, id) minimum.  Spatially consecutive anchors have
 // overlapping windows and hence overlapping candidate sets, so the shared
 // traversal visits little more than each query alone.
+// three-input max (FMNMX3 on sm_100)
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
 constexpr int kTileStack = 48;
 constexpr int kTileMaxB = 16;
 
@@ -988,7 +995,7 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
   __shared__ __align__(16) float stage_all[kTileWarps][32 * RS];
   __shared__ float aux_all[kTileWarps][2][32];
   __shared__ int2 cmeta_all[kTileWarps][kTileMaxB];
-  __shared__ float box_all[kTileWarps][kTileMaxB][2 * kBoxDims];
+  __shared__ __align__(16) float box_all[kTileWarps][kTileMaxB][2 * kBoxDims];
   __shared__ int32_t pid_all[kTileWarps][32];
   __shared__ float tlb_all[kTileWarps][kTileMaxB][32];
   __shared__ unsigned tkey_all[kTileWarps][kTileMaxB];
@@ -1034,11 +1041,13 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
     for (int j = 0; j < DP / 2; ++j) {
       const double v0 = (valid && 2 * j < d) ? qrow[2 * j] : 0.0;
       const double v1 = (valid && 2 * j + 1 < d) ? qrow[2 * j + 1] : 0.0;
-      q2[j] = make_float2((float)v0, (float)v1);
+      // held negated: u = p + (-q) is one FADD2 against plainly staged rows
+      q2[j] = make_float2(-(float)v0, -(float)v1);
       qn2 += v0 * v0 + v1 * v1;
     }
     const float qn = __double2float_ru(sqrt(qn2) * (1.0 + 1e-12));
-    const float qdelta = 1.2e-7f * qn;  // >= |float(q_j) - q_j| for every j
+    // box margin: >= |float(q_j) - q_j| + the rounding of (-q_j -/+ margin)
+    const float qdelta2 = 2.4e-7f * qn;
     // invalid lanes hold best = -1: every bound (>= 0) prunes them
     double best = valid ? kInf : -1.0;
     int32_t best_id = 0x7fffffff;
@@ -1105,10 +1114,8 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
             const float4* col = reinterpret_cast<const float4*>(a.proj32_q4) + pos;
             float4* dst = reinterpret_cast<float4*>(stage + lane * RS);
 #pragma unroll
-            for (int k = 0; k < DP / 4; ++k) {  // staged negated: u = q + (-p) with FADD2
-              const float4 v = (4 * k < d) ? __ldg(col + (int64_t)k * N) : make_float4(0.f, 0.f, 0.f, 0.f);
-              dst[k] = make_float4(-v.x, -v.y, -v.z, -v.w);
-            }
+            for (int k = 0; k < DP / 4; ++k)
+              dst[k] = (4 * k < d) ? __ldg(col + (int64_t)k * N) : make_float4(0.f, 0.f, 0.f, 0.f);
             aux0[lane] = a.pnorm32[pos];
             pid[lane] = a.perm[pos];
           }
@@ -1204,26 +1211,41 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
         aux1[lane] = a.tree.cnorm32[fc + lane];
         cmeta[lane] = a.tree.meta[fc + lane];
       }
-      for (int f = lane; f < nc * kBoxDims; f += 32) {  // dims >= d hold [0, 0]
-        const int c = f % nc, j = f / nc;
-        boxs[c][2 * j] = __ldg(a.tree.boxlo + (int64_t)j * nn + fc + c);
-        boxs[c][2 * j + 1] = __ldg(a.tree.boxhi + (int64_t)j * nn + fc + c);
+#pragma unroll
+      for (int f = lane; f < kTileMaxB * kBoxDims; f += 32) {  // dims >= d hold [0, 0]
+        const int c = f % kTileMaxB, j = f / kTileMaxB;
+        if (c < nc) {  // stored (lo, -hi): one FADD2 per dim below
+          boxs[c][2 * j] = __ldg(a.tree.boxlo + (int64_t)j * nn + fc + c);
+          boxs[c][2 * j + 1] = -__ldg(a.tree.boxhi + (int64_t)j * nn + fc + c);
+        }
       }
       __syncwarp();
-      // phase 1: box bound of every child (8 leading dims).  The box is rounded
-      // outward and the fp32 query differs from the fp64 one by <= 2^-24 |q_j|
-      // <= qdelta; subtraction / accumulation rounding is covered by the final
-      // factor.  For j >= d both the box ([0, 0]) and q_j (0) are zero-padded.
+      // phase 1: box bound of every child (8 leading dims):
+      // gap_j = max(lo_j - q_j - m, q_j - hi_j - m, 0) as one FADD2 + FMNMX3.
+      // The box is rounded outward; the fp32 query differs from the fp64 one by
+      // <= 2^-24 |q_j| and (-q_j - m), (q_j - m) round by <= 2^-24 (|q_j| + m):
+      // m = qdelta2 = 2.4e-7 |q| covers both.  The remaining roundings are
+      // relative to the results, covered by the final factor.  For j >= d the
+      // box ([0, 0]) and q_j (0) are zero-padded: the gap is 0.
+      float2 tq[kBoxDims];
+#pragma unroll
+      for (int j = 0; j < kBoxDims; ++j) {
+        const float nq = (j & 1) ? q2[j >> 1].y : q2[j >> 1].x;  // -q_j
+        tq[j] = make_float2(nq - qdelta2, -nq - qdelta2);
+      }
       uint32_t boxpass = 0;
 #pragma unroll 2
       for (int c = 0; c < nc; ++c) {
         float bx = 0.f;
+        const float4* bc = reinterpret_cast<const float4*>(boxs[c]);
 #pragma unroll
-        for (int j = 0; j < kBoxDims; ++j) {
-          const float lo = boxs[c][2 * j], hi = boxs[c][2 * j + 1];
-          const float qj = (j & 1) ? q2[j >> 1].y : q2[j >> 1].x;
-          const float gap = fmaxf(fmaxf(lo - qj, qj - hi) - qdelta, 0.f);
-          bx = fmaf(gap, gap, bx);
+        for (int j2 = 0; j2 < kBoxDims / 2; ++j2) {
+          const float4 bb = bc[j2];
+          const float2 u0 = __fadd2_rn(make_float2(bb.x, bb.y), tq[2 * j2]);
+          const float2 u1 = __fadd2_rn(make_float2(bb.z, bb.w), tq[2 * j2 + 1]);
+          const float g0 = fmax3(u0.x, u0.y, 0.f), g1 = fmax3(u1.x, u1.y, 0.f);
+          bx = fmaf(g0, g0, bx);
+          bx = fmaf(g1, g1, bx);
         }
         bx *= 1.f - 1e-5f;
         tlb[c][lane] = bx;
@@ -1235,7 +1257,7 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
       for (uint32_t m = todo; m; m &= m - 1) {
         const int c = __ffs(m) - 1;
         for (int j = lane; j < DP; j += 32)
-          stage[c * RS + j] = j < d ? -__ldg(a.tree.centroid32 + (int64_t)(fc + c) * d + j) : 0.f;
+          stage[c * RS + j] = j < d ? __ldg(a.tree.centroid32 + (int64_t)(fc + c) * d + j) : 0.f;
       }
       __syncwarp();
       // phase 2: ball bound (|q - c| - radius)+ of those children, max with the box
@@ -1277,17 +1299,18 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
       int myslot = -1;
       if (kept) {
         int rank = 0;
-        for (int o = 0; o < nc; ++o) {
+        for (uint32_t m = keepmask; m; m &= m - 1) {
+          const int o = __ffs(m) - 1;
           const unsigned ko = tkey[o];
-          if (ko != 0xffffffffu && (ko < mykey || (ko == mykey && o < lane))) ++rank;
+          if (ko < mykey || (ko == mykey && o < lane)) ++rank;
         }
         myslot = top + nkeep - 1 - rank;
         sm_[myslot] = cmeta[lane];
       }
 #pragma unroll 1
-      for (int c = 0; c < nc; ++c) {
-        const int slot = __shfl_sync(0xffffffffu, myslot, c);
-        if (slot >= 0) slb[slot][lane] = tlb[c][lane];
+      for (uint32_t m = keepmask; m; m &= m - 1) {
+        const int c = __ffs(m) - 1;
+        slb[__shfl_sync(0xffffffffu, myslot, c)][lane] = tlb[c][lane];
       }
       top += nkeep;
       __syncwarp();
