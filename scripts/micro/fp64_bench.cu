@@ -1,5 +1,6 @@
 // Microbenchmark: fp64 DMUL + DADD (separate, no FMA: the exact projection's
-// operation mix) throughput on sm_100a.
+// operation mix) throughput on sm_100a.  Both operations are loop-carried
+// (an invariant product would be hoisted out of the loop by the compiler).
 #include <cstdio>
 #include <cuda_runtime.h>
 __global__ void k(double* out, int iters, double b) {
@@ -7,7 +8,10 @@ __global__ void k(double* out, int iters, double b) {
   for (int t = 0; t < 16; ++t) { acc[t] = threadIdx.x * t; c[t] = 1.0 + t * 1e-3; }
   for (int i = 0; i < iters; ++i) {
 #pragma unroll
-    for (int t = 0; t < 16; ++t) acc[t] = __dadd_rn(acc[t], __dmul_rn(c[t], b));
+    for (int t = 0; t < 16; ++t) {
+      c[t] = __dmul_rn(c[t], b);  // loop-carried: the multiply cannot be hoisted
+      acc[t] = __dadd_rn(acc[t], c[t]);
+    }
   }
   double s = 0;
   for (int t = 0; t < 16; ++t) s += acc[t];
