@@ -1021,8 +1021,14 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
   const int tnx = a.qxs ? (a.qnx + 7) / 8 : 0;
   const int64_t n_tiles = a.qxs ? (int64_t)tnx * ((qny + 3) / 4) : (a.nq + 31) / 32;
 
-  for (int64_t t = (int64_t)blockIdx.x * kTileWarps + warp; t < n_tiles;
-       t += (int64_t)gridDim.x * kTileWarps) {
+  // persistent warps fetch tiles from a global ticket: tile costs vary ~4x,
+  // and a fast warp must not idle until its CTA's slowest warp finishes
+  for (;;) {
+    int64_t t = 0;
+    if (lane == 0) t = atomicAdd(reinterpret_cast<unsigned long long*>(a.sched), 1ull);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= n_tiles) break;
+    if (a.tile_order) t = a.tile_order[t];  // costliest tiles first (previous search)
     int64_t q;
     bool valid;
     if (a.qxs) {
@@ -1324,6 +1330,28 @@ __global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs
     }
     __syncwarp();
   }
+  // the last warp out re-arms the ticket for the next launch on the stream
+  if (lane == 0) {
+    __threadfence();
+    const unsigned long long total = (unsigned long long)gridDim.x * kTileWarps;
+    unsigned long long* s = reinterpret_cast<unsigned long long*>(a.sched);
+    if (atomicAdd(s + 1, 1ull) == total - 1) {
+      s[0] = 0;
+      s[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+template <int DP, int W>
+static int tile_resident_ctas(psg_ctx* ctx) {
+  static int per_sm = 0;
+  if (!per_sm) {
+    PSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, search_tile_kernel<DP, W>,
+                                                           32 * W, 0));
+    if (per_sm < 1) per_sm = 1;
+  }
+  return per_sm * ctx->num_sms;
 }
 
 void launch_search(psg_ctx* ctx, const SearchArgs& a) {
@@ -1338,10 +1366,11 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
                        1 + a.tree.max_depth * (a.tree.max_children - 1) <= kTileStack;
   if (a.mode == PSG_EXACT && a.proj32_q4 && a.tree.centroid32 && tile_ok && !ctx->legacy_search) {
     if (ctx->hmma_tile && a.d <= 32 && launch_search_hmma(ctx, a)) return;
+    if (!a.sched) fail(PSG_E_LOGIC, "tile search launched without its scheduler counters");
     const int64_t tiles = (a.nq + 31) / 32;
     const int wpb = a.d <= 32 ? 3 : 2;  // static smem <= 48 KB per CTA
     int64_t blocks = (tiles + wpb - 1) / wpb;
-    const int64_t cap = (int64_t)ctx->num_sms * 24;
+    const int64_t cap = a.d <= 32 ? tile_resident_ctas<32, 3>(ctx) : tile_resident_ctas<64, 2>(ctx);
     if (blocks > cap) blocks = cap;
     if (a.d <= 32)
       search_tile_kernel<32, 3><<<(int)blocks, 32 * 3, 0, ctx->stream>>>(a);
@@ -1436,6 +1465,59 @@ __global__ void scatter_kernel(const T* __restrict__ src, const int32_t* __restr
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     dst[order[i]] = src[i];
+}
+
+// Tile schedule for the next search of the same anchors: the previous search's
+// per-tile work (its shared scan count, held by every lane of the tile) sorted
+// into 64 quarter-octave buckets, costliest bucket first -- long tiles start
+// first and the tail is short tiles.  One CTA: count, scan, scatter.  (The
+// order within a bucket may vary run to run; every tile's result and counters
+// are independent of when it runs.)
+constexpr int kOrderBuckets = 64;
+
+__device__ __forceinline__ int tile_cost_bucket(int64_t c) {
+  const float l = log2f((float)c + 1.f) * 4.f;
+  return kOrderBuckets - 1 - min(kOrderBuckets - 1, (int)l);  // descending cost
+}
+
+__global__ void __launch_bounds__(1024) tile_order_kernel(const int64_t* __restrict__ scanned,
+                                                          int qnx, int tnx, int64_t n_tiles,
+                                                          int32_t* __restrict__ order) {
+  __shared__ int cnt[kOrderBuckets], pos[kOrderBuckets];
+  if (threadIdx.x < kOrderBuckets) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+    const int tx = (int)(t % tnx), ty = (int)(t / tnx);
+    atomicAdd(&cnt[tile_cost_bucket(scanned[(int64_t)ty * 4 * qnx + tx * 8])], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int b = 0; b < kOrderBuckets; ++b) {
+      pos[b] = acc;
+      acc += cnt[b];
+    }
+  }
+  __syncthreads();
+  for (int64_t t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+    const int tx = (int)(t % tnx), ty = (int)(t / tnx);
+    const int b = tile_cost_bucket(scanned[(int64_t)ty * 4 * qnx + tx * 8]);
+    order[atomicAdd(&pos[b], 1)] = (int32_t)t;
+  }
+}
+
+int64_t image_tile_count(int64_t nq, int qnx) {
+  const int qny = (int)(nq / qnx);
+  return (int64_t)((qnx + 7) / 8) * ((qny + 3) / 4);
+}
+
+void launch_tile_order(psg_ctx* ctx, const int64_t* prev_scanned, int64_t nq, int qnx,
+                       int32_t* order) {
+  ProfScope _prof(ctx, K_SCHED);
+  const int64_t nt = image_tile_count(nq, qnx);
+  if (nt <= 0) return;
+  tile_order_kernel<<<1, 1024, 0, ctx->stream>>>(prev_scanned, qnx, (qnx + 7) / 8, nt, order);
+  PSG_LAUNCHED(ctx);
 }
 
 size_t sort_pairs_temp_bytes(int64_t n) {

@@ -129,7 +129,7 @@ struct RowSrc {
 namespace psg {
 enum KernelKind : int {
   K_MIRROR = 0, K_PROJECT, K_SEARCH, K_RESCORE, K_WEIGHTS, K_HIST, K_PENALTY, K_MSTEP, K_STATS,
-  K_BUILD, K_PYRAMID, K_COUNT
+  K_BUILD, K_PYRAMID, K_SCHED, K_COUNT
 };
 extern const char* const kKernelNames[K_COUNT];
 }  // namespace psg
@@ -156,6 +156,7 @@ struct psg_ctx {
   std::vector<void*> pinned_blocks;
   std::vector<double*> pinned_free;
   int* d_flags = nullptr;
+  int64_t* d_sched = nullptr;  // search tile scheduler (2 counters)
   bool legacy_search = false;  // PERSYN_SEARCH=warp: per-query warp kernel instead of tiles
   bool mma_search = false;     // PERSYN_SEARCH=mma: tcgen05 tile kernel
   bool hmma_tile = false;      // PERSYN_SEARCH=hmma: leaf filter on mma.sync (bf16 split)
@@ -219,7 +220,14 @@ struct SearchArgs {
   int64_t* out_exact;       // optional: points evaluated in exact fp64
   int32_t* out_visited;     // optional: nodes visited (QueryStats, km_tree.hpp:27-30)
   int* flags;
+  int64_t* sched = nullptr;  // [2] tile ticket + warps done (self re-arming, zeroed at ctx creation)
+  const int32_t* tile_order = nullptr;  // optional tile permutation (image tiles)
 };
+// Tile permutation for the next exact search of the same anchors: descending
+// previous per-tile work (order: [image_tile_count(nq, qnx)]).
+int64_t image_tile_count(int64_t nq, int qnx);
+void launch_tile_order(psg_ctx* ctx, const int64_t* prev_scanned, int64_t nq, int qnx,
+                       int32_t* order);
 // Brute-force index: build the filter operand once per index; exact search of
 // nq query rows (lexicographic min of (fp64 dist^2, id), optimizer.cpp:175-205).
 void brute_prepare(psg_ctx* ctx, Index& ix);

@@ -137,7 +137,7 @@ double now_ms() {
 const char* const kKernelNames[K_COUNT] = {
     "make_mirror", "project_kernel", "search_kernel", "rescore_kernel", "weights_kernel",
     "hist_kernels", "penalty_kernel", "mstep_kernel", "stats_kernel", "build_kernels",
-    "pyramid_kernels"};
+    "pyramid_kernels", "tile_schedule"};
 
 ProfScope::ProfScope(psg_ctx* c, int k) : ctx(c), kind(k) {
   if (!ctx->profile) return;
@@ -695,6 +695,15 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
   a.out_exact = L.exact_evals.p;
   a.out_visited = L.visited.p;
   a.flags = ctx->d_flags;
+  a.sched = ctx->d_sched;
+  // seeded exact search: the previous search of these anchors left its
+  // per-query scan counts in L.scanned -> schedule the costliest tiles first
+  DBuf<int32_t> order;
+  if (a.seed_idx && a.mode == PSG_EXACT && !std::getenv("PERSYN_NO_TILE_ORDER")) {
+    order.alloc((size_t)image_tile_count(a.nq, a.qnx));
+    launch_tile_order(ctx, L.scanned.p, a.nq, a.qnx, order.p);
+    a.tile_order = order.p;
+  }
   launch_search(ctx, a);
   launch_rescore_windows(ctx, L.mirror.p, L.W, L.C, L.w, as, ix, out_idx + L.off,
                          out_dist + L.off);
@@ -942,6 +951,8 @@ psg_status psg_ctx_create(int device, void* stream, psg_ctx** out) {
     }
     PSG_CUDA(cudaMalloc(&c->d_flags, sizeof(int)));
     PSG_CUDA(cudaMemsetAsync(c->d_flags, 0, sizeof(int), c->stream));
+    PSG_CUDA(cudaMalloc(&c->d_sched, 2 * sizeof(int64_t)));
+    PSG_CUDA(cudaMemsetAsync(c->d_sched, 0, 2 * sizeof(int64_t), c->stream));
     psg::create_solver_handles(c.get());  // once per context, not inside a stage build
     *out = c.release();
   });
@@ -959,6 +970,7 @@ void psg_ctx_destroy(psg_ctx* ctx) {
   if (ctx->cublas) cublasDestroy(static_cast<cublasHandle_t>(ctx->cublas));
   if (ctx->cusolver) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(ctx->cusolver));
   cudaFree(ctx->d_flags);
+  cudaFree(ctx->d_sched);
   for (void* b : ctx->pinned_blocks) cudaFreeHost(b);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -1205,6 +1217,7 @@ psg_status psg_index_query(psg_ctx* ctx, const psg_index* index, const float* Q,
     a.out_d2 = d2.p;
     a.out_scanned = sc.p;
     a.flags = ctx->d_flags;
+    a.sched = ctx->d_sched;
     const bool reorder = budget.mode == PSG_EXACT && nq >= 64 && ix.d > 0 && !ctx->legacy_search;
     if (ix.brute) {
       // searched above (the budget does not apply, optimizer.cpp:172-173)
