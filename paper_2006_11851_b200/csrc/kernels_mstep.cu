@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "numerics.cuh"
 #include "psg_internal.h"
@@ -154,15 +155,83 @@ void launch_penalty(psg_ctx* ctx, const Index& ix, const int32_t* idx, int64_t A
   PSG_LAUNCHED(ctx);
 }
 
+// The penalty depends on the candidate only: one table entry per exemplar
+// window (N ids) replaces the per-anchor sums (A ~ 4N at sp = 2), and
+// consecutive threads read consecutive exemplar pixels (coalesced), where the
+// per-anchor form gathers one random window per thread.  Same sequential sum
+// per entry as penalty_kernel, so table[idx[a]] is bit-identical to pen[a].
+__global__ void penalty_table_kernel(const float* __restrict__ ex_mirror, int ew, int C, int w,
+                                     int nxe, int64_t N, const double* __restrict__ excess,
+                                     int bins, int slots, double* __restrict__ table) {
+  extern __shared__ double ex_s[];
+  for (int i = threadIdx.x; i < bins * slots; i += blockDim.x) ex_s[i] = excess[i];
+  __syncthreads();
+  const double area = (double)(w * w);
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < N;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int ex = (int)(id % nxe), ey = (int)(id / nxe);
+    double total = 0.0;
+    for (int dy = 0; dy < w; ++dy) {
+      const float* z = ex_mirror + ((int64_t)(ey + dy) * ew + ex) * C;
+      for (int dx = 0; dx < w; ++dx)
+        for (int s = 0; s < slots; ++s) {
+          const int b = bin_of_f32(__ldg(z + dx * C + s), bins);
+          total = dadd(total, ex_s[s * bins + b]);
+        }
+    }
+    table[id] = total / area;
+  }
+}
+
+void launch_penalty_table(psg_ctx* ctx, const Index& ix, const double* excess, int bins,
+                          int slots, double* table) {
+  ProfScope _prof(ctx, K_PENALTY);
+  if (ix.N <= 0) return;
+  const size_t sm = sizeof(double) * bins * slots;
+  penalty_table_kernel<<<grid_for(ctx, ix.N, 128), 128, sm, ctx->stream>>>(
+      ix.ex_mirror, ix.ew, ix.C, ix.w, ix.nxe, ix.N, excess, bins, slots, table);
+  PSG_LAUNCHED(ctx);
+}
+
+// pen[a] = table[idx[a]]; eff[a] = irls[a] / (1 + pen[a]) (optimizer.hpp:32-34).
+__global__ void eff_gather_kernel(const double* __restrict__ irls,
+                                  const double* __restrict__ table,
+                                  const int32_t* __restrict__ idx, int64_t A,
+                                  double* __restrict__ pen, double* __restrict__ eff, int* flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double p = table[idx[i]];
+    pen[i] = p;
+    const double we = irls[i] / dadd(1.0, p);
+    eff[i] = we;
+    if (!(we > 0.0) || !isfinite(we)) atomicOr(flags, FLAG_BAD_WEIGHT);
+  }
+}
+
+void launch_eff_gather(psg_ctx* ctx, const double* irls, const double* table, const int32_t* idx,
+                       int64_t A, double* pen, double* eff, int* flags) {
+  ProfScope _prof(ctx, K_WEIGHTS);
+  if (A <= 0) return;
+  eff_gather_kernel<<<grid_for(ctx, A, 256), 256, 0, ctx->stream>>>(irls, table, idx, A, pen, eff,
+                                                                    flags);
+  PSG_LAUNCHED(ctx);
+}
+
 // ---- M-step: gather form ----------------------------------------------------------
 // One thread per output pixel.  The reference scatters anchors in ascending
 // id into per-pixel accumulators; for a fixed pixel that is exactly the
 // ascending (iy, ix) order of its covering anchors, which this loop walks.
-// No atomics, bit-identical sums.
-template <int CMAX>
+// No atomics, bit-identical sums.  NC > 0: the channel count is a compile-time
+// constant (no predicated channel lanes); NC = 0: any C <= 8.  The candidate id
+// is split with a float-reciprocal quotient and one correction step (exact
+// for ids < 2^24, checked by the launcher).
+template <int NC>
 __global__ void __launch_bounds__(256) mstep_kernel(MstepArgs a) {
+  constexpr int CMAX = NC > 0 ? NC : 8;
+  const int C = NC > 0 ? NC : a.C;
   const int64_t P = (int64_t)a.W * a.H;
   const int64_t PS = (int64_t)a.W * a.plane_rows;  // plane stride (band: rows >= H)
+  const float inv_nxe = 1.f / (float)a.nxe;
   for (int64_t pix = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pix < P;
        pix += (int64_t)gridDim.x * blockDim.x) {
     const int y = (int)(pix / a.W), x = (int)(pix - (int64_t)y * a.W);
@@ -174,16 +243,26 @@ __global__ void __launch_bounds__(256) mstep_kernel(MstepArgs a) {
     const int ix0 = a.col_lo[x], ix1 = a.col_hi[x];
     for (int iy = iy0; iy < iy1; ++iy) {
       const int dy = y - a.ys[iy];
+      const int64_t arow = (int64_t)iy * a.nx;
       for (int ix = ix0; ix < ix1; ++ix) {
-        const int64_t an = (int64_t)iy * a.nx + ix;
-        const double we = a.eff[an];
-        const int32_t id = a.idx[an];
-        const int dx = x - a.xs[ix];
-        const int ex = id % a.nxe + dx, ey = id / a.nxe + dy;
-        const float* z = a.ex_mirror + ((int64_t)ey * a.ew + ex) * a.C;
+        const double we = a.eff[arow + ix];
+        const int32_t id = a.idx[arow + ix];
+        int ey = __float2int_rz((float)id * inv_nxe);
+        int ex = id - ey * a.nxe;
+        if (ex < 0) {
+          --ey;
+          ex += a.nxe;
+        } else if (ex >= a.nxe) {
+          ++ey;
+          ex -= a.nxe;
+        }
+        const float* z = a.ex_mirror + ((int64_t)(ey + dy) * a.ew + ex + (x - a.xs[ix])) * C;
+        float zv[CMAX];
+#pragma unroll
+        for (int c = 0; c < CMAX; ++c) zv[c] = (NC > 0 || c < C) ? __ldg(z + c) : 0.f;
 #pragma unroll
         for (int c = 0; c < CMAX; ++c)
-          if (c < a.C) acc[c] = dadd(acc[c], dmul(we, (double)z[c]));
+          if (NC > 0 || c < C) acc[c] = dadd(acc[c], dmul(we, (double)zv[c]));
         wsum = dadd(wsum, we);
       }
     }
@@ -194,11 +273,11 @@ __global__ void __launch_bounds__(256) mstep_kernel(MstepArgs a) {
     const double inv = 1.0 / wsum;  // optimizer.cpp:393
 #pragma unroll
     for (int c = 0; c < CMAX; ++c) {
-      if (c >= a.C) break;
+      if (NC == 0 && c >= C) break;
       double v = dmul(acc[c], inv);
       v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);  // std::clamp(.., 0, 1)
       a.planes[c * PS + pix] = v;
-      if (a.mirror) a.mirror[pix * a.C + c] = (float)v;
+      if (a.mirror) a.mirror[pix * C + c] = (float)v;
     }
   }
 }
@@ -207,13 +286,12 @@ void launch_mstep(psg_ctx* ctx, const MstepArgs& a) {
   ProfScope _prof(ctx, K_MSTEP);
   const int64_t P = (int64_t)a.W * a.H;
   if (P <= 0) return;
+  if (a.C > 8) fail(PSG_E_DOMAIN, "more than 8 channels are not supported");
   const int blocks = grid_for(ctx, P, 256, 16);
-  if (a.C <= 4) {
-    mstep_kernel<4><<<blocks, 256, 0, ctx->stream>>>(a);
-  } else if (a.C <= 8) {
-    mstep_kernel<8><<<blocks, 256, 0, ctx->stream>>>(a);
-  } else {
-    fail(PSG_E_DOMAIN, "more than 8 channels are not supported");
+  switch (a.C) {
+    case 4: mstep_kernel<4><<<blocks, 256, 0, ctx->stream>>>(a); break;
+    case 5: mstep_kernel<5><<<blocks, 256, 0, ctx->stream>>>(a); break;
+    default: mstep_kernel<0><<<blocks, 256, 0, ctx->stream>>>(a); break;
   }
   PSG_LAUNCHED(ctx);
 }
@@ -276,30 +354,56 @@ __global__ void __launch_bounds__(kStatsThreads) stats_partial_kernel(StatsArgs 
     o[4] = (double)si[1][0];
     o[5] = (double)si[2][0];
   }
-}
-
-__global__ void stats_final_kernel(const double* __restrict__ part, int nb,
-                                   double* __restrict__ out) {
-  const int k = threadIdx.x;
-  if (k >= 6) return;
-  if (k < 3) {
-    double acc = 0.0;
-    for (int b = 0; b < nb; ++b) acc = dadd(acc, part[b * 6 + k]);
-    out[k] = acc;
-  } else {
-    long long acc = 0;
-    for (int b = 0; b < nb; ++b) acc += (long long)part[b * 6 + k];
-    out[k] = (double)acc;
+  // the last CTA to finish folds the partials in a fixed order (
+  // run-to-run identical); the ticket re-arms itself for the next launch
+  __shared__ bool last;
+  if (t == 0) {
+    __threadfence();
+    const unsigned long long prev = atomicAdd(a.ticket, 1ull);
+    last = prev == gridDim.x - 1;
   }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int nb = gridDim.x;
+  // fixed two-level fold: thread t sums blocks t, t + 256, ... then the tree
+  double f0 = 0.0, f1 = 0.0, f2 = 0.0;
+  long long g0 = 0, g1 = 0, g2 = 0;
+  for (int b = t; b < nb; b += blockDim.x) {
+    const double* o = part + b * 6;
+    f0 = dadd(f0, __ldcg(o + 0));
+    f1 = dadd(f1, __ldcg(o + 1));
+    f2 = dadd(f2, __ldcg(o + 2));
+    g0 += (long long)__ldcg(o + 3);
+    g1 += (long long)__ldcg(o + 4);
+    g2 += (long long)__ldcg(o + 5);
+  }
+  sd[0][t] = f0;
+  sd[1][t] = f1;
+  sd[2][t] = f2;
+  si[0][t] = g0;
+  si[1][t] = g1;
+  si[2][t] = g2;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (t < s) {
+      for (int k = 0; k < 3; ++k) sd[k][t] = dadd(sd[k][t], sd[k][t + s]);
+      for (int k = 0; k < 3; ++k) si[k][t] += si[k][t + s];
+    }
+    __syncthreads();
+  }
+  if (t < 3) a.out[t] = sd[t][0];
+  if (t >= 3 && t < 6) a.out[t] = (double)si[t - 3][0];
+  if (t == 0) *a.ticket = 0ull;
 }
 
 void launch_stats(psg_ctx* ctx, const StatsArgs& a) {
   ProfScope _prof(ctx, K_STATS);
   const int nb = (int)std::min<int64_t>(kStatsBlocks, std::max<int64_t>(1, (a.A + 255) / 256));
-  stats_partial_kernel<<<nb, kStatsThreads, 0, ctx->stream>>>(a, a.out + 8);
-  stats_final_kernel<<<1, 32, 0, ctx->stream>>>(a.out + 8, nb, a.out);
+  StatsArgs b = a;
+  if (!b.ticket) b.ticket = reinterpret_cast<unsigned long long*>(ctx->d_sched + 2);
+  stats_partial_kernel<<<nb, kStatsThreads, 0, ctx->stream>>>(b, a.out + 8);
   PSG_LAUNCHED(ctx);
-  ctx->launches++;
 }
 
 }  // namespace psg

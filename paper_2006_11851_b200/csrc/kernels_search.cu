@@ -1604,6 +1604,37 @@ void launch_make_fp32_copies(psg_ctx* ctx, const double* soa, int64_t N, int d, 
 // Full-D rescoring (optimizer.cpp:117-124, :232-234): one thread per query,
 // j ascending over the window (dy, dx, c) against the candidate's dense
 // exemplar window — the candidate matrix is never materialised.
+__device__ __forceinline__ double window_dist2(const float* __restrict__ mirror, int img_w, int C,
+                                               int w, int ax, int ay,
+                                               const float* __restrict__ ex_mirror, int ew,
+                                               int ex, int ey) {
+  const int row = w * C;
+  double acc = 0.0;
+  for (int dy = 0; dy < w; ++dy) {
+    const float* v = mirror + ((int64_t)(ay + dy) * img_w + ax) * C;
+    const float* z = ex_mirror + ((int64_t)(ey + dy) * ew + ex) * C;
+    int jj = 0;
+    for (; jj + 8 <= row; jj += 8) {  // loads batched ahead of the sequential adds
+      float vv[8], zz[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        vv[u] = __ldg(v + jj + u);
+        zz[u] = __ldg(z + jj + u);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double t = dsub((double)vv[u], (double)zz[u]);
+        acc = dadd(acc, dmul(t, t));
+      }
+    }
+    for (; jj < row; ++jj) {
+      const double t = dsub((double)v[jj], (double)z[jj]);
+      acc = dadd(acc, dmul(t, t));
+    }
+  }
+  return acc;
+}
+
 __global__ void rescore_windows_kernel(const float* __restrict__ mirror, int img_w, int C, int w,
                                        const int32_t* __restrict__ xs,
                                        const int32_t* __restrict__ ys, int nx, int64_t n,
@@ -1612,42 +1643,63 @@ __global__ void rescore_windows_kernel(const float* __restrict__ mirror, int img
                                        double* __restrict__ dist) {
   for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n;
        a += (int64_t)gridDim.x * blockDim.x) {
-    const int ax = xs[a % nx], ay = ys[a / nx];
     const int32_t id = idx[a];
-    const int ex = id % nxe, ey = id / nxe;
-    const int row = w * C;
-    double acc = 0.0;
-    for (int dy = 0; dy < w; ++dy) {
-      const float* v = mirror + ((int64_t)(ay + dy) * img_w + ax) * C;
-      const float* z = ex_mirror + ((int64_t)(ey + dy) * ew + ex) * C;
-      int jj = 0;
-      for (; jj + 8 <= row; jj += 8) {  // loads batched ahead of the sequential adds
-        float vv[8], zz[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          vv[u] = __ldg(v + jj + u);
-          zz[u] = __ldg(z + jj + u);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const double t = dsub((double)vv[u], (double)zz[u]);
-          acc = dadd(acc, dmul(t, t));
-        }
-      }
-      for (; jj < row; ++jj) {
-        const double t = dsub((double)v[jj], (double)z[jj]);
-        acc = dadd(acc, dmul(t, t));
-      }
-    }
-    dist[a] = sqrt(acc);
+    dist[a] = sqrt(window_dist2(mirror, img_w, C, w, xs[a % nx], ys[a / nx], ex_mirror, ew,
+                                id % nxe, id / nxe));
+  }
+}
+
+// Rescoring after a search seeded with prev_idx on the SAME image: an anchor
+// whose assignment did not change has the distance prev_dist already (the
+// lsq-after diagnostic computed it: same window, same candidate, same chain),
+// so only the changed anchors (~10% once EM settles) are recomputed.  Each
+// CTA compacts its changed anchors so that the chains run on contiguous lanes.
+constexpr int kRescoreBlock = 256;
+__global__ void __launch_bounds__(kRescoreBlock) rescore_changed_kernel(
+    const float* __restrict__ mirror, int img_w, int C, int w, const int32_t* __restrict__ xs,
+    const int32_t* __restrict__ ys, int nx, int64_t n, const float* __restrict__ ex_mirror, int ew,
+    int nxe, const int32_t* __restrict__ idx, const int32_t* __restrict__ prev_idx,
+    const double* __restrict__ prev_dist, double* __restrict__ dist) {
+  __shared__ int list[kRescoreBlock];
+  __shared__ int cnt;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) cnt = 0;
+  __syncthreads();
+  const int64_t a = (int64_t)blockIdx.x * kRescoreBlock + tid;
+  bool todo = false;
+  if (a < n) {
+    if (idx[a] == prev_idx[a])
+      dist[a] = prev_dist[a];
+    else
+      todo = true;
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, todo);
+  int base = 0;
+  if (lane == 0 && m) base = atomicAdd(&cnt, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (todo) list[base + __popc(m & ((1u << lane) - 1u))] = tid;
+  __syncthreads();
+  for (int i = tid; i < cnt; i += kRescoreBlock) {
+    const int64_t b = (int64_t)blockIdx.x * kRescoreBlock + list[i];
+    const int32_t id = idx[b];
+    dist[b] = sqrt(window_dist2(mirror, img_w, C, w, xs[b % nx], ys[b / nx], ex_mirror, ew,
+                                id % nxe, id / nxe));
   }
 }
 
 void launch_rescore_windows(psg_ctx* ctx, const float* mirror, int img_w, int C, int w,
                             AnchorSet anchors, const Index& ix, const int32_t* idx,
-                            double* dist) {
+                            double* dist, const int32_t* prev_idx, const double* prev_dist) {
   ProfScope _prof(ctx, K_RESCORE);
   if (anchors.count <= 0) return;
+  if (prev_idx && prev_dist) {
+    const int64_t blocks = (anchors.count + kRescoreBlock - 1) / kRescoreBlock;
+    rescore_changed_kernel<<<(unsigned)blocks, kRescoreBlock, 0, ctx->stream>>>(
+        mirror, img_w, C, w, anchors.xs, anchors.ys, anchors.nx, anchors.count, ix.ex_mirror,
+        ix.ew, ix.nxe, idx, prev_idx, prev_dist, dist);
+    PSG_LAUNCHED(ctx);
+    return;
+  }
   const int threads = 128;
   int64_t blocks = (anchors.count + threads - 1) / threads;
   if (blocks > (int64_t)ctx->num_sms * 32) blocks = (int64_t)ctx->num_sms * 32;

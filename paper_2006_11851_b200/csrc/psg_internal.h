@@ -156,7 +156,7 @@ struct psg_ctx {
   std::vector<void*> pinned_blocks;
   std::vector<double*> pinned_free;
   int* d_flags = nullptr;
-  int64_t* d_sched = nullptr;  // search tile scheduler (2 counters)
+  int64_t* d_sched = nullptr;  // [0..1] search tile scheduler, [2] stats fold ticket
   bool legacy_search = false;  // PERSYN_SEARCH=warp: per-query warp kernel instead of tiles
   bool mma_search = false;     // PERSYN_SEARCH=mma: tcgen05 tile kernel
   bool hmma_tile = false;      // PERSYN_SEARCH=hmma: leaf filter on mma.sync (bf16 split)
@@ -259,7 +259,8 @@ void launch_make_fp32_copies(psg_ctx* ctx, const double* soa, int64_t N, int d, 
                              float* aos32, float* pn);
 // Full-D distance between query windows and assigned candidates (optimizer.cpp:117-124).
 void launch_rescore_windows(psg_ctx* ctx, const float* mirror, int img_w, int C, int w,
-                            AnchorSet anchors, const Index& ix, const int32_t* idx, double* dist);
+                            AnchorSet anchors, const Index& ix, const int32_t* idx, double* dist,
+                            const int32_t* prev_idx = nullptr, const double* prev_dist = nullptr);
 void launch_rescore_query_windows(psg_ctx* ctx, const float* Q, int64_t nq, const Index& ix,
                                   const int32_t* idx, double* dist);
 void launch_rescore_vectors(psg_ctx* ctx, const float* Q, int64_t nq, const Index& ix,
@@ -284,6 +285,11 @@ void launch_hist_fold(psg_ctx* ctx, const unsigned long long* counts, int bins, 
                       int64_t P, const double* ex_mass, double* mass, double* excess);
 void launch_penalty(psg_ctx* ctx, const Index& ix, const int32_t* idx, int64_t A,
                     const double* excess, int bins, int slots, double* pen);
+// Penalty of every candidate id [0, N) (table), then per-anchor gather + eff.
+void launch_penalty_table(psg_ctx* ctx, const Index& ix, const double* excess, int bins,
+                          int slots, double* table);
+void launch_eff_gather(psg_ctx* ctx, const double* irls, const double* table, const int32_t* idx,
+                       int64_t A, double* pen, double* eff, int* flags);
 struct MstepArgs {
   const int32_t* xs;
   const int32_t* ys;
@@ -316,6 +322,7 @@ struct StatsArgs {
   int64_t A;
   double r;
   double* out;  // [6]: lsq_before, lsq_after, energy, changed, scanned_plan, unique_scanned
+  unsigned long long* ticket = nullptr;  // self re-arming last-block counter (ctx->d_sched + 2)
 };
 void launch_stats(psg_ctx* ctx, const StatsArgs& a);
 // PCA helpers.

@@ -472,7 +472,7 @@ struct psg_level {
   psg::DBuf<int64_t> scanned, exact_evals;
   psg::DBuf<int32_t> visited;
   psg::DBuf<unsigned long long> counts;
-  psg::DBuf<double> out_mass, excess, ex_hist, stats_dev;
+  psg::DBuf<double> out_mass, excess, ex_hist, stats_dev, pen_table;
   double* stats_host = nullptr;  // pinned [8]
   bool hist_on = false;
   int slots = 3;
@@ -638,14 +638,20 @@ void level_set_hist(psg_level& L, const double* ex_hist_host) {
   L.counts.alloc(n);
   L.out_mass.alloc(n);
   L.excess.alloc(n);
+  // per-candidate penalty table: worth it when anchors outnumber candidates
+  if (ix.N > 0 && ix.N <= L.Ao) L.pen_table.alloc(ix.N);
 }
 
 AnchorSet owned_anchors(psg_level& L) { return AnchorSet{L.xs.p, L.ys.p + L.nh, L.nx, L.Ao}; }
 
 // E-step over the owned anchors of the level's current (local) image.
 // seed: per-owned-anchor exemplar ids evaluated first (only the bound; the
-// result does not depend on it), or null.
-void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* out_dist) {
+// result does not depend on it), or null.  seed_dist (optional): the full-D
+// distances of the seed assignment on this same image (the lsq-after
+// diagnostic) — anchors that keep their assignment reuse them.
+void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* out_dist,
+                  const double* seed_dist = nullptr) {
+  if (!seed || std::getenv("PERSYN_RESCORE_ALL")) seed_dist = nullptr;
   psg_ctx* ctx = L.ctx;
   const Index& ix = *L.ix;
   const AnchorSet as = owned_anchors(L);
@@ -663,7 +669,7 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
                         L.exact_evals.p);
     PSG_CUDA(cudaMemsetAsync(L.visited.p, 0, sizeof(int32_t) * L.Ao, ctx->stream));
     launch_rescore_windows(ctx, L.mirror.p, L.W, L.C, L.w, as, ix, out_idx + L.off,
-                           out_dist + L.off);
+                           out_dist + L.off, seed_dist ? seed : nullptr, seed_dist);
     L.unique_queries += L.Ao;
     return;
   }
@@ -706,7 +712,7 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
   }
   launch_search(ctx, a);
   launch_rescore_windows(ctx, L.mirror.p, L.W, L.C, L.w, as, ix, out_idx + L.off,
-                         out_dist + L.off);
+                         out_dist + L.off, seed_dist ? seed : nullptr, seed_dist);
   L.unique_queries += L.Ao;
 }
 
@@ -740,6 +746,8 @@ void level_prime(psg_level& L, const int32_t* seed = nullptr) {
 
 MstepArgs mstep_args(psg_level& L) {
   const Index& ix = *L.ix;
+  if (ix.N >= (1 << 24))  // mstep_kernel splits ids with a float reciprocal
+    fail(PSG_E_DOMAIN, "exemplar has >= 2^24 candidate windows");
   MstepArgs m{};
   m.xs = L.xs.p;
   m.ys = L.ys.p;
@@ -797,6 +805,12 @@ void phase_penalty(psg_level& L, const unsigned long long* global_counts) {
   const int bins = L.cfg.histogram_bins;
   launch_hist_fold(ctx, global_counts, bins, L.slots, (int64_t)L.W * L.H, L.ex_hist.p,
                    L.out_mass.p, L.excess.p);
+  if (L.pen_table.p && !std::getenv("PERSYN_PENALTY_PER_ANCHOR")) {
+    launch_penalty_table(ctx, *L.ix, L.excess.p, bins, L.slots, L.pen_table.p);
+    launch_eff_gather(ctx, L.irls.p + L.off, L.pen_table.p, L.cur_idx.p + L.off, L.Ao,
+                      L.pen.p + L.off, L.eff.p + L.off, ctx->d_flags);
+    return;
+  }
   launch_penalty(ctx, *L.ix, L.cur_idx.p + L.off, L.Ao, L.excess.p, bins, L.slots,
                  L.pen.p + L.off);
   launch_eff_from(ctx, L.irls.p + L.off, L.pen.p + L.off, L.Ao, L.eff.p + L.off, ctx->d_flags);
@@ -810,7 +824,7 @@ void phase_search(psg_level& L) {
   psg_ctx* ctx = L.ctx;
   launch_rescore_windows(ctx, L.mirror.p, L.W, L.C, L.w, owned_anchors(L), *L.ix,
                          L.cur_idx.p + L.off, L.after.p + L.off);
-  level_search(L, L.cur_idx.p + L.off, L.next_idx.p, L.next_dist.p);
+  level_search(L, L.cur_idx.p + L.off, L.next_idx.p, L.next_dist.p, L.after.p + L.off);
   StatsArgs s{};
   s.cur_dist = L.cur_dist.p + L.off;
   s.after_dist = L.after.p + L.off;
@@ -951,8 +965,8 @@ psg_status psg_ctx_create(int device, void* stream, psg_ctx** out) {
     }
     PSG_CUDA(cudaMalloc(&c->d_flags, sizeof(int)));
     PSG_CUDA(cudaMemsetAsync(c->d_flags, 0, sizeof(int), c->stream));
-    PSG_CUDA(cudaMalloc(&c->d_sched, 2 * sizeof(int64_t)));
-    PSG_CUDA(cudaMemsetAsync(c->d_sched, 0, 2 * sizeof(int64_t), c->stream));
+    PSG_CUDA(cudaMalloc(&c->d_sched, 4 * sizeof(int64_t)));  // [2]: stats fold ticket
+    PSG_CUDA(cudaMemsetAsync(c->d_sched, 0, 4 * sizeof(int64_t), c->stream));
     psg::create_solver_handles(c.get());  // once per context, not inside a stage build
     *out = c.release();
   });
