@@ -138,13 +138,14 @@ __global__ void __launch_bounds__(256) project_kernel(
 // consecutive k for RQ anchors, so one double2 basis load and RQ broadcast
 // double2 loads of the centred window feed 4 * RQ fp64 ops per 2 j (the
 // per-(anchor, k) order over j is unchanged: bit-identical to project_kernel).
-template <int RQ, bool kWindows>
-__global__ void __launch_bounds__(256) project2_kernel(
+template <int RQ, bool kWindows, int JCT>
+__global__ void __launch_bounds__(256, 3) project2_kernel(
     const float* __restrict__ src, int img_w, int C, int w, const int32_t* __restrict__ xs,
-    const int32_t* __restrict__ ys, int nx, int64_t n, int D, int JC,
+    const int32_t* __restrict__ ys, int nx, int64_t n, int D, int JC_,
     const double* __restrict__ mean, const double* __restrict__ basisT,  // [D][32]
     int d, double* __restrict__ out) {
   constexpr int TQ = 8 * 2 * RQ;  // anchors per block: 8 warps x 2 groups x RQ
+  const int JC = JCT > 0 ? JCT : JC_;  // JCT > 0: window chunks are always full (JC | w*C)
   extern __shared__ __align__(16) double smem2[];
   const int JCp = JC + 2;  // even (double2 aligned), breaks the power-of-two stride
   double* cen = smem2;             // [TQ][JCp]
@@ -173,19 +174,47 @@ __global__ void __launch_bounds__(256) project2_kernel(
   const int n_chunks = (D + JC - 1) / JC;
   for (int ch = 0; ch < n_chunks; ++ch) {
     const int j0 = ch * JC;
-    const int jc = min(JC, D - j0);
+    const int jc = JCT > 0 ? JCT : min(JC, D - j0);
     // windows: chunk j0 is window row j0 / R at offset j0 % R (R = w * C)
     const int64_t roff = kWindows ? (int64_t)(j0 / (w * C)) * img_w * C + j0 % (w * C) : 0;
     __syncthreads();
-    for (int f = tid; f < TQ * jc; f += 256) {
-      const int q = f / jc, jj = f - q * jc;
-      const int64_t b = base_s[q];
-      double v = 0.0;
-      if (b >= 0) {
-        const float x = kWindows ? src[b + roff + jj] : src[b + j0 + jj];
-        v = dsub((double)x, mean[j0 + jj]);
+    if constexpr (JCT > 0) {
+      // fixed trip count: loads batched 4 deep (one latency per 4 elements)
+      constexpr int PER = (TQ * JCT + 255) / 256, H = 4;
+#pragma unroll
+      for (int h = 0; h < PER; h += H) {
+        float xv[H];
+        double mv[H];
+#pragma unroll
+        for (int k = 0; k < H; ++k) {
+          const int f = tid + 256 * (h + k);
+          const int q = f / JCT, jj = f - q * JCT;
+          xv[k] = 0.f;
+          mv[k] = 0.0;
+          if (h + k < PER && f < TQ * JCT && base_s[q] >= 0) {
+            xv[k] = __ldg(src + base_s[q] + roff + jj);
+            mv[k] = __ldg(mean + j0 + jj);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < H; ++k) {
+          const int f = tid + 256 * (h + k);
+          const int q = f / JCT, jj = f - q * JCT;
+          if (h + k < PER && f < TQ * JCT)
+            cen[q * JCp + jj] = base_s[q] >= 0 ? dsub((double)xv[k], mv[k]) : 0.0;
+        }
       }
-      cen[q * JCp + jj] = v;
+    } else {
+      for (int f = tid; f < TQ * jc; f += 256) {
+        const int q = f / jc, jj = f - q * jc;
+        const int64_t b = base_s[q];
+        double v = 0.0;
+        if (b >= 0) {
+          const float x = kWindows ? src[b + roff + jj] : src[b + j0 + jj];
+          v = dsub((double)x, mean[j0 + jj]);
+        }
+        cen[q * JCp + jj] = v;
+      }
     }
     if (jc & 1)  // odd chunk: zero pad column so the double2 loop can read it
       for (int q = tid; q < TQ; q += 256) cen[q * JCp + jc] = 0.0;
@@ -237,10 +266,20 @@ static void launch_project(psg_ctx* ctx, const float* src, int img_w, int C, int
   const int TQ = 8 * RQ;
   const int JCp = JC | 1;
   const int blocks = (int)((n + TQ - 1) / TQ);
-  if (d <= 32) {
+  if (d <= 32 && kWindows && (JC == 32 || JC == 40)) {
+    // compile-time chunk width: immediate shared-memory offsets in the
+    // multiply loop, multiply-shift staging indices
     constexpr int TQ2 = 8 * 2 * RQ;
     const size_t sm = sizeof(double) * ((size_t)TQ2 * (JC + 2) + (size_t)(JC + 1) * 32);
-    auto k = project2_kernel<RQ, kWindows>;
+    auto k = JC == 32 ? project2_kernel<RQ, kWindows, 32> : project2_kernel<RQ, kWindows, 40>;
+    PSG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    const int blocks2 = (int)((n + TQ2 - 1) / TQ2);
+    k<<<blocks2, 256, sm, ctx->stream>>>(src, img_w, C, w, xs, ys, nx, n, D, JC, mean, basisT, d,
+                                          out);
+  } else if (d <= 32) {
+    constexpr int TQ2 = 8 * 2 * RQ;
+    const size_t sm = sizeof(double) * ((size_t)TQ2 * (JC + 2) + (size_t)(JC + 1) * 32);
+    auto k = project2_kernel<RQ, kWindows, 0>;
     PSG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     const int blocks2 = (int)((n + TQ2 - 1) / TQ2);
     k<<<blocks2, 256, sm, ctx->stream>>>(src, img_w, C, w, xs, ys, nx, n, D, JC, mean, basisT, d,
