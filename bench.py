@@ -314,12 +314,14 @@ def run_ours(args):
         from paper_2006_11851_b200 import sharding as sh
         plans = sh.all_plans(cfg.out, cfg.out, args.window, sp, world)
         band = sh.GpuBand(index, init, plans[rank], plans, ocfg)
-        comm = sh.DistComm() if world > 1 or torch.distributed.is_initialized() else \
-            sh.LoopbackComm(1)
+        # the library runs on `stream`; exchanges are enqueued on it too
+        comm = sh.DistComm(stream_ordered=True) if world > 1 or \
+            torch.distributed.is_initialized() else sh.LoopbackComm(1)
         band.prime()
 
         def one_step():
-            g = sh.em_iteration([band], comm)
+            with torch.cuda.stream(stream):
+                g = sh.em_iteration([band], comm)
             return [api.IterationStats(0, g[2], int(g[3]), int(g[6] + g[7]), 0.0, g[0], g[1],
                                        int(g[4]), int(g[8]), int(g[5]))]
         A = plans[0]["nx"] * plans[0]["ny"]

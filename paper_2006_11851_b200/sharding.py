@@ -74,9 +74,16 @@ class LoopbackComm:
 
 
 class DistComm:
-    """One band per process over torch.distributed (NCCL: CUDA tensors; gloo: CPU)."""
+    """One band per process over torch.distributed (NCCL: CUDA tensors; gloo: CPU).
 
-    def __init__(self):
+    stream_ordered (NCCL): the library's context stream IS torch's current
+    stream, so every collective / P2P op is ordered after the kernels that
+    produced its buffer and before the kernels that consume it (torch makes
+    the NCCL stream wait on the current stream and `wait()` makes the current
+    stream wait on NCCL) -- no host synchronisation between phases.  Otherwise
+    each exchange is bracketed by a device synchronisation."""
+
+    def __init__(self, stream_ordered: bool = False):
         import torch
         import torch.distributed as dist
         self.dist = dist
@@ -85,11 +92,12 @@ class DistComm:
         self.ranks = [self.rank]
         self.cuda = dist.get_backend() == "nccl"
         self.device = torch.device("cuda", torch.cuda.current_device()) if self.cuda else None
+        self.stream_ordered = bool(stream_ordered) and self.cuda
 
     def _settle(self):
-        # library kernels run on the library's stream: make every exchange
+        # library kernels on a stream of their own: make every exchange
         # complete before the next phase reads or overwrites its buffers
-        if self.cuda:
+        if self.cuda and not self.stream_ordered:
             import torch
             torch.cuda.synchronize()
 
