@@ -38,6 +38,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "EM iterations/s at 1024^2 output (cfg3 finest stage, w=8, exact search)"
 UNIT = "iterations/s"
 BAND_ROWS = 24   # reference arm: rows of the output band per bounded sample
+FP32_PEAK_TFLOPS = 69.3  # measured FFMA / FFMA2 peak (scripts/micro/fp32_bench.cu)
 
 
 def parse():
@@ -222,7 +223,9 @@ def roofline_for(kernels: dict, step_ms: float, A: int, P: int, C: int, d: int, 
             per[name] = {"ms_per_launch": ms / n, "launches": n, "share": ms / max(step_ms, 1e-9)}
     ms, n = kernels[dom]
     t = ms / n / 1e3
-    fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12   # derived, TFLOP/s (FMA = 2)
+    # measured: scripts/micro/fp32_bench.cu on B200 -- FFMA and packed FFMA2
+    # both 69 TFLOP/s (FFMA2 halves issue slots, not pipe time)
+    fp32_peak = FP32_PEAK_TFLOPS
     if dom == "search_kernel":
         # exact search = fp32 filter over (query, candidate) pairs + rare exact
         # fp64 rechecks: algorithmic flops = 3*d per pair (sub, mul, add)
@@ -231,8 +234,8 @@ def roofline_for(kernels: dict, step_ms: float, A: int, P: int, C: int, d: int, 
         roof = {"bound": "fp32", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s",
                 "frac": ach / fp32_peak, "traffic": None,
                 "note": "irregular tree search: SIMT fp32 filter + fp64 exact recheck; neither "
-                        "HBM (working set L2-resident) nor tensor cores bind. Peak derived "
-                        "148 SM x 128 FP32 lanes x 2 x 1.965 GHz (not measured); flops = "
+                        "HBM (working set L2-resident) nor tensor cores bind. Peak measured "
+                        "(scripts/micro/fp32_bench.cu: FFMA = FFMA2 = 69.3 TFLOP/s); flops = "
                         "3*d*(query, point) pairs evaluated"}
     elif dom == "mstep_kernel":
         bytes_ = P * C * 12 + A * 12
@@ -248,7 +251,7 @@ def roofline_for(kernels: dict, step_ms: float, A: int, P: int, C: int, d: int, 
         roof = {"bound": "hbm", "achieved": None, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": None, "traffic": None}
     roof["kernel"] = dom
-    roof["peak_src"] = peaks["src"] if roof["bound"] == "hbm" else "derived"
+    roof["peak_src"] = peaks["src"] if roof["bound"] == "hbm" else "measured (scripts/micro/fp32_bench.cu)"
     if dom == "search_kernel":
         roof["traffic"], roof["traffic_src"] = ncu_traffic("search_tile_kernel")
     return roof, per
@@ -337,7 +340,6 @@ def run_ours(args):
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    ctx.profile(True)
     launches0 = ctx.launches
     stats = []
     with ClockSampler(local) as clk:
@@ -354,9 +356,20 @@ def run_ours(args):
         if world > 1:
             torch.distributed.barrier()
     launches = ctx.launches - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    # per-kernel times from separate profiled steps (event pairs around every
+    # launch perturb the step, so the timed steps above run without them)
+    n_prof = 3
+    ctx.profile(True)
+    ev_p = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    ev_p[0].record(stream)
+    for _ in range(n_prof):
+        stats_p = one_step()
+    ev_p[1].record(stream)
+    torch.cuda.synchronize()
     kernels = ctx.kernel_times()
     ctx.profile(False)
-    step_ms = [a.elapsed_time(b) for a, b in ev]
+    prof_ms = ev_p[0].elapsed_time(ev_p[1])
     ms = float(np.sum(step_ms))
     if world > 1:
         t = torch.tensor([ms], device="cuda")
@@ -367,7 +380,7 @@ def run_ours(args):
     P = cfg.out * cfg.out
     scanned_unique = float(np.mean([s.unique_points_scanned for s in stats])) / world
     calls = stats[-1].nn_calls
-    roof, per = roofline_for(kernels, ms_per_step * args.steps, A, P, C, index.retained_dim,
+    roof, per = roofline_for(kernels, prof_ms, A, P, C, index.retained_dim,
                              index.count, scanned_unique, measured_peaks())
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -386,6 +399,8 @@ def run_ours(args):
         "points_scanned_per_query": scanned_unique / A,
         "index_build_s": t_build, "gpu_launches": launches,
         "kernels": per, "roofline": roof,
+        "kernel_times_from": f"{n_prof} extra steps with CUDA events around every launch on the "
+                             "library stream, right after the timed region (shares of those steps)",
     }
     # ---- e2e through the public host-buffer API (pinned host memory) ------
     if not args.no_e2e and not sharded:
