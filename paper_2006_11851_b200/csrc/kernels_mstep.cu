@@ -229,6 +229,11 @@ template <int NC>
 __global__ void __launch_bounds__(256) mstep_kernel(MstepArgs a) {
   constexpr int CMAX = NC > 0 ? NC : 8;
   const int C = NC > 0 ? NC : a.C;
+  extern __shared__ unsigned int hist_s[];  // [slots][bins] when a.counts
+  if (a.counts) {
+    for (int i = threadIdx.x; i < a.bins * a.slots; i += blockDim.x) hist_s[i] = 0;
+    __syncthreads();
+  }
   const int64_t P = (int64_t)a.W * a.H;
   const int64_t PS = (int64_t)a.W * a.plane_rows;  // plane stride (band: rows >= H)
   const float inv_nxe = 1.f / (float)a.nxe;
@@ -278,7 +283,13 @@ __global__ void __launch_bounds__(256) mstep_kernel(MstepArgs a) {
       v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);  // std::clamp(.., 0, 1)
       a.planes[c * PS + pix] = v;
       if (a.mirror) a.mirror[pix * C + c] = (float)v;
+      if (a.counts && c < a.slots) atomicAdd(&hist_s[c * a.bins + bin_of_f64(v, a.bins)], 1u);
     }
+  }
+  if (a.counts) {  // same integer counts as hist_count_kernel over the written rows
+    __syncthreads();
+    for (int i = threadIdx.x; i < a.bins * a.slots; i += blockDim.x)
+      if (hist_s[i]) atomicAdd(&a.counts[i], (unsigned long long)hist_s[i]);
   }
 }
 
@@ -288,10 +299,17 @@ void launch_mstep(psg_ctx* ctx, const MstepArgs& a) {
   if (P <= 0) return;
   if (a.C > 8) fail(PSG_E_DOMAIN, "more than 8 channels are not supported");
   const int blocks = grid_for(ctx, P, 256, 16);
+  size_t sm = 0;
+  if (a.counts) {
+    if (a.slots > a.C) fail(PSG_E_DOMAIN, "histogram slots exceed the channel count");
+    sm = sizeof(unsigned int) * a.bins * a.slots;
+    PSG_CUDA(cudaMemsetAsync(a.counts, 0, sizeof(unsigned long long) * a.bins * a.slots,
+                             ctx->stream));
+  }
   switch (a.C) {
-    case 4: mstep_kernel<4><<<blocks, 256, 0, ctx->stream>>>(a); break;
-    case 5: mstep_kernel<5><<<blocks, 256, 0, ctx->stream>>>(a); break;
-    default: mstep_kernel<0><<<blocks, 256, 0, ctx->stream>>>(a); break;
+    case 4: mstep_kernel<4><<<blocks, 256, sm, ctx->stream>>>(a); break;
+    case 5: mstep_kernel<5><<<blocks, 256, sm, ctx->stream>>>(a); break;
+    default: mstep_kernel<0><<<blocks, 256, sm, ctx->stream>>>(a); break;
   }
   PSG_LAUNCHED(ctx);
 }

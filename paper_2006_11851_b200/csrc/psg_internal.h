@@ -307,6 +307,10 @@ struct MstepArgs {
   double* planes;  // out [C][plane_rows][W]
   float* mirror;   // out [H][W][C]
   int* flags;
+  // optional: histogram counts of the written pixels (build_histograms of the
+  // updated image, fused), u64 [slots][bins], zeroed by the launcher
+  unsigned long long* counts = nullptr;
+  int bins = 0, slots = 0;
 };
 void launch_mstep(psg_ctx* ctx, const MstepArgs& a);
 // Deterministic reductions for telemetry.

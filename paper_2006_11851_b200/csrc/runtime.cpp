@@ -475,6 +475,7 @@ struct psg_level {
   psg::DBuf<double> out_mass, excess, ex_hist, stats_dev, pen_table;
   double* stats_host = nullptr;  // pinned [8]
   bool hist_on = false;
+  bool counts_fresh = false;  // L.counts = histogram of the current owned rows (fused M-step)
   int slots = 3;
   bool primed = false;
   int iter = 0;
@@ -808,9 +809,10 @@ void phase_weights(psg_level& L) {
   wa.eff = L.eff.p + L.off;
   wa.flags = ctx->d_flags;
   launch_weights(ctx, wa);
-  if (L.hist_on)
+  if (L.hist_on && !L.counts_fresh)
     launch_hist_count(ctx, L.planes.p, (int64_t)L.W * L.Hu, L.P, L.cfg.histogram_bins, L.slots,
                       L.counts.p);
+  L.counts_fresh = false;
 }
 
 // Phase 2: fold the global counts (1/P over the WHOLE image), penalties and
@@ -833,7 +835,17 @@ void phase_penalty(psg_level& L, const unsigned long long* global_counts) {
 }
 
 // Phase 3: M-step of the owned pixel rows (halo anchor rows must be filled).
-void phase_update(psg_level& L) { launch_mstep(L.ctx, mstep_args(L)); }
+void phase_update(psg_level& L) {
+  MstepArgs m = mstep_args(L);
+  if (L.hist_on && !std::getenv("PERSYN_NO_FUSED_HIST")) {
+    // the next phase 1 histograms exactly the rows this M-step writes
+    m.counts = L.counts.p;
+    m.bins = L.cfg.histogram_bins;
+    m.slots = L.slots;
+  }
+  launch_mstep(L.ctx, m);
+  L.counts_fresh = m.counts != nullptr;
+}
 
 // Phase 4: lsq diagnostic, E-step, telemetry partials of the owned anchors.
 void phase_search(psg_level& L) {
@@ -910,6 +922,7 @@ bool level_step(psg_level& L, psg_iter_stats* st, bool honor) {
 
 // Host rows [p0, e1) of the global image (planes [C][Hl][W]).
 void upload_state(psg_level& L, const double* host_planes) {
+  L.counts_fresh = false;
   L.planes.upload(L.ctx, host_planes, (size_t)L.P * L.C);
   launch_make_mirror(L.ctx, L.planes.p, L.C, L.W, L.Hl, L.mirror.p);
 }
@@ -1519,6 +1532,7 @@ psg_status psg_level_state_dev(psg_level* level, void** planes_dev, void** idx_d
   return guarded([&] {
     psg::StreamScope _ss(level->ctx->stream);
     if (planes_dev) *planes_dev = level->planes.p;
+    level->counts_fresh = false;  // the caller may write the planes
     if (idx_dev) *idx_dev = level->cur_idx.p;
     if (dist_dev) *dist_dev = level->cur_dist.p;
   });
