@@ -436,6 +436,44 @@ def run_ours(args):
                          "d2h_bytes_per_step": int(init.nbytes),
                          "step": f"one psg_optimize_level call (host buffers, {n_it} EM iterations "
                                  f"incl. the priming search), index resident"}
+    if not args.no_e2e and sharded:
+        # row bands: each rank uploads its band rows from host memory, primes,
+        # runs 10 EM iterations with the NCCL exchanges and downloads its owned
+        # rows + assignments; max over ranks of the device-synchronised wall time
+        n_it = 10
+        from paper_2006_11851_b200 import sharding as sh
+
+        def e2e_band():
+            b = sh.GpuBand(index, init, plans[rank], plans, ocfg)
+            with torch.cuda.stream(stream):
+                sh.run_sharded([b], comm, n_it, n_it, total_anchors=A)
+            out = b.owned()
+            del b
+            return out
+
+        e2e_band()  # warm-up
+        ts = []
+        for _ in range(3):
+            if world > 1:
+                torch.distributed.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            own = e2e_band()
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        t_e2e = float(np.mean(ts))
+        if world > 1:
+            t = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            t_e2e = float(t.item())
+        p = plans[rank]
+        h2d = (p["e1"] - p["p0"]) * cfg.out * C * 8
+        d2h = own[0].nbytes + own[1].nbytes + own[2].nbytes
+        result["e2e"] = {"value": n_it / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                         "d2h_bytes_per_step": int(d2h),
+                         "step": f"per rank: band create from host rows, priming search, {n_it} "
+                                 "EM iterations with NCCL halo exchange, download of owned rows "
+                                 "(bytes: rank 0's); max over ranks"}
     result["clocks"] = clk.summary()
     # ---- CPU baseline (rank 0, N = 1) -------------------------------------------
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
