@@ -155,6 +155,9 @@ struct psg_ctx {
   // synchronise the device and cost milliseconds: never per level)
   std::vector<void*> pinned_blocks;
   std::vector<double*> pinned_free;
+  // side stream for kernels that overlap the critical path (fork / join by events)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_tile = nullptr;
   int* d_flags = nullptr;
   int64_t* d_sched = nullptr;  // [0..1] search tile scheduler, [2] stats fold ticket
   bool legacy_search = false;  // PERSYN_SEARCH=warp: per-query warp kernel instead of tiles

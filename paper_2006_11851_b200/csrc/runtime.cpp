@@ -39,6 +39,15 @@ struct StreamScope {
   ~StreamScope() { t_stream = prev; }
 };
 
+// Launches inside the scope go to the context's side stream (the launchers
+// use ctx->stream); the caller orders it against the main stream with events.
+struct SideScope {
+  psg_ctx* ctx;
+  cudaStream_t main;
+  explicit SideScope(psg_ctx* c) : ctx(c), main(c->stream) { ctx->stream = ctx->side; }
+  ~SideScope() { ctx->stream = main; }
+};
+
 template <class T>
 struct DBuf {
   T* p = nullptr;
@@ -651,7 +660,7 @@ AnchorSet owned_anchors(psg_level& L) { return AnchorSet{L.xs.p, L.ys.p + L.nh, 
 // distances of the seed assignment on this same image (the lsq-after
 // diagnostic) — anchors that keep their assignment reuse them.
 void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* out_dist,
-                  const double* seed_dist = nullptr) {
+                  const double* seed_dist = nullptr, cudaEvent_t seed_dist_ready = nullptr) {
   if (!seed || std::getenv("PERSYN_RESCORE_ALL")) seed_dist = nullptr;
   psg_ctx* ctx = L.ctx;
   const Index& ix = *L.ix;
@@ -669,6 +678,7 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
     launch_brute_search(ctx, ix, qs, L.Ao, seed, out_idx + L.off, L.d2.p, L.scanned.p,
                         L.exact_evals.p);
     PSG_CUDA(cudaMemsetAsync(L.visited.p, 0, sizeof(int32_t) * L.Ao, ctx->stream));
+    if (seed_dist_ready) PSG_CUDA(cudaStreamWaitEvent(ctx->stream, seed_dist_ready, 0));
     launch_rescore_windows(ctx, L.mirror.p, L.W, L.C, L.w, as, ix, out_idx + L.off,
                            out_dist + L.off, seed_dist ? seed : nullptr, seed_dist);
     L.unique_queries += L.Ao;
@@ -724,10 +734,20 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
   DBuf<int32_t> order;
   if (a.seed_idx && !greedy_seed.p && a.mode == PSG_EXACT && !std::getenv("PERSYN_NO_TILE_ORDER")) {
     order.alloc((size_t)image_tile_count(a.nq, a.qnx));
-    launch_tile_order(ctx, L.scanned.p, a.nq, a.qnx, order.p);
+    if (seed_dist_ready) {  // concurrent mode: the one-CTA sort overlaps the projection
+      {
+        SideScope side(ctx);
+        launch_tile_order(ctx, L.scanned.p, a.nq, a.qnx, order.p);
+      }
+      PSG_CUDA(cudaEventRecord(ctx->ev_tile, ctx->side));
+      PSG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_tile, 0));
+    } else {
+      launch_tile_order(ctx, L.scanned.p, a.nq, a.qnx, order.p);
+    }
     a.tile_order = order.p;
   }
   launch_search(ctx, a);
+  if (seed_dist_ready) PSG_CUDA(cudaStreamWaitEvent(ctx->stream, seed_dist_ready, 0));
   launch_rescore_windows(ctx, L.mirror.p, L.W, L.C, L.w, as, ix, out_idx + L.off,
                          out_dist + L.off, seed_dist ? seed : nullptr, seed_dist);
   L.unique_queries += L.Ao;
@@ -850,9 +870,27 @@ void phase_update(psg_level& L) {
 // Phase 4: lsq diagnostic, E-step, telemetry partials of the owned anchors.
 void phase_search(psg_level& L) {
   psg_ctx* ctx = L.ctx;
-  launch_rescore_windows(ctx, L.mirror.p, L.W, L.C, L.w, owned_anchors(L), *L.ix,
-                         L.cur_idx.p + L.off, L.after.p + L.off);
-  level_search(L, L.cur_idx.p + L.off, L.next_idx.p, L.next_dist.p, L.after.p + L.off);
+  // the lsq diagnostic (L1-bound) runs on the side stream, overlapping the
+  // projection (fp64-bound); the post-search rescoring waits for it.  Serial
+  // when profiling (per-launch events live on the main stream).
+  const bool conc = ctx->side && !ctx->profile && !std::getenv("PERSYN_SERIAL");
+  cudaEvent_t ready = nullptr;
+  if (conc) {
+    PSG_CUDA(cudaEventRecord(ctx->ev_fork, ctx->stream));
+    PSG_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+    {
+      SideScope side(ctx);
+      launch_rescore_windows(ctx, L.mirror.p, L.W, L.C, L.w, owned_anchors(L), *L.ix,
+                             L.cur_idx.p + L.off, L.after.p + L.off);
+    }
+    PSG_CUDA(cudaEventRecord(ctx->ev_join, ctx->side));
+    ready = ctx->ev_join;
+  } else {
+    launch_rescore_windows(ctx, L.mirror.p, L.W, L.C, L.w, owned_anchors(L), *L.ix,
+                           L.cur_idx.p + L.off, L.after.p + L.off);
+  }
+  level_search(L, L.cur_idx.p + L.off, L.next_idx.p, L.next_dist.p, L.after.p + L.off, ready);
+  if (ready) PSG_CUDA(cudaStreamWaitEvent(ctx->stream, ready, 0));  // stats read `after`
   StatsArgs s{};
   s.cur_dist = L.cur_dist.p + L.off;
   s.after_dist = L.after.p + L.off;
@@ -992,6 +1030,9 @@ psg_status psg_ctx_create(int device, void* stream, psg_ctx** out) {
       uint64_t keep = UINT64_MAX;
       PSG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     }
+    PSG_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&c->ev_fork, &c->ev_join, &c->ev_tile})
+      PSG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     PSG_CUDA(cudaMalloc(&c->d_flags, sizeof(int)));
     PSG_CUDA(cudaMemsetAsync(c->d_flags, 0, sizeof(int), c->stream));
     PSG_CUDA(cudaMalloc(&c->d_sched, 4 * sizeof(int64_t)));  // [2]: stats fold ticket
@@ -1010,6 +1051,12 @@ void psg_ctx_destroy(psg_ctx* ctx) {
     cudaEventDestroy(p.b);
   }
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->side) {
+    cudaStreamSynchronize(ctx->side);
+    cudaStreamDestroy(ctx->side);
+  }
+  for (cudaEvent_t e : {ctx->ev_fork, ctx->ev_join, ctx->ev_tile})
+    if (e) cudaEventDestroy(e);
   if (ctx->cublas) cublasDestroy(static_cast<cublasHandle_t>(ctx->cublas));
   if (ctx->cusolver) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(ctx->cusolver));
   cudaFree(ctx->d_flags);
