@@ -815,9 +815,15 @@ MstepArgs mstep_args(psg_level& L) {
 
 // Phase 1: IRLS weights of the owned anchors; local histogram counts of the
 // owned pixel rows (the caller sums them over ranks: exact integers).
-void phase_weights(psg_level& L) {
+// side: the weights kernel goes to the side stream (joined by ctx->ev_join
+// before the effective weights are formed, see phase_penalty).
+void phase_weights(psg_level& L, bool side = false) {
   psg_ctx* ctx = L.ctx;
   PSG_CUDA(cudaEventRecord(L.ev0, ctx->stream));
+  if (side) {
+    PSG_CUDA(cudaEventRecord(ctx->ev_fork, ctx->stream));
+    PSG_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+  }
   WeightArgs wa{};
   wa.dist = L.cur_dist.p + L.off;
   wa.idx = L.cur_idx.p + L.off;
@@ -828,7 +834,15 @@ void phase_weights(psg_level& L) {
   wa.irls = L.irls.p + L.off;
   wa.eff = L.eff.p + L.off;
   wa.flags = ctx->d_flags;
-  launch_weights(ctx, wa);
+  if (side) {
+    {
+      SideScope sc(ctx);
+      launch_weights(ctx, wa);
+    }
+    PSG_CUDA(cudaEventRecord(ctx->ev_join, ctx->side));
+  } else {
+    launch_weights(ctx, wa);
+  }
   if (L.hist_on && !L.counts_fresh)
     launch_hist_count(ctx, L.planes.p, (int64_t)L.W * L.Hu, L.P, L.cfg.histogram_bins, L.slots,
                       L.counts.p);
@@ -837,20 +851,27 @@ void phase_weights(psg_level& L) {
 
 // Phase 2: fold the global counts (1/P over the WHOLE image), penalties and
 // effective weights of the owned anchors.
-void phase_penalty(psg_level& L, const unsigned long long* global_counts) {
-  if (!L.hist_on) return;
+// weights_ready: event the IRLS weights were recorded on (side stream), or null.
+void phase_penalty(psg_level& L, const unsigned long long* global_counts,
+                   cudaEvent_t weights_ready = nullptr) {
   psg_ctx* ctx = L.ctx;
+  if (!L.hist_on) {
+    if (weights_ready) PSG_CUDA(cudaStreamWaitEvent(ctx->stream, weights_ready, 0));
+    return;
+  }
   const int bins = L.cfg.histogram_bins;
   launch_hist_fold(ctx, global_counts, bins, L.slots, (int64_t)L.W * L.H, L.ex_hist.p,
                    L.out_mass.p, L.excess.p);
   if (L.pen_table.p && !std::getenv("PERSYN_PENALTY_PER_ANCHOR")) {
     launch_penalty_table(ctx, *L.ix, L.excess.p, bins, L.slots, L.pen_table.p);
+    if (weights_ready) PSG_CUDA(cudaStreamWaitEvent(ctx->stream, weights_ready, 0));
     launch_eff_gather(ctx, L.irls.p + L.off, L.pen_table.p, L.cur_idx.p + L.off, L.Ao,
                       L.pen.p + L.off, L.eff.p + L.off, ctx->d_flags);
     return;
   }
   launch_penalty(ctx, *L.ix, L.cur_idx.p + L.off, L.Ao, L.excess.p, bins, L.slots,
                  L.pen.p + L.off);
+  if (weights_ready) PSG_CUDA(cudaStreamWaitEvent(ctx->stream, weights_ready, 0));
   launch_eff_from(ctx, L.irls.p + L.off, L.pen.p + L.off, L.Ao, L.eff.p + L.off, ctx->d_flags);
 }
 
@@ -946,8 +967,11 @@ void phase_partials(psg_level& L, double out[9]) {
 // One EM iteration on a single device (optimizer.cpp:450-513).  Returns true
 // when converged under the reference's rule.
 bool level_step(psg_level& L, psg_iter_stats* st, bool honor) {
-  phase_weights(L);
-  phase_penalty(L, L.counts.p);
+  psg_ctx* ctx = L.ctx;
+  // IRLS weights (side stream) overlap the histogram fold + penalty table
+  const bool conc = ctx->side && !ctx->profile && !std::getenv("PERSYN_SERIAL");
+  phase_weights(L, conc);
+  phase_penalty(L, L.counts.p, conc ? ctx->ev_join : nullptr);
   phase_update(L);
   phase_search(L);
   double g[9];
