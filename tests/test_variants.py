@@ -88,3 +88,35 @@ def test_eigensolver_paths_agree(gpu_ctx, monkeypatch):
     ok[1:] &= gaps[:-1] > 1e-6
     ok &= gaps[:24] > 1e-6
     assert np.allclose(np.abs(np.sum(ba * bb, axis=1))[ok], 1.0, atol=1e-8)
+
+
+@pytest.mark.parametrize("env", [{}, {"PERSYN_SERIAL": "1"}, {"PERSYN_GRAPH": "1"},
+                                 {"PERSYN_RESCORE_ALL": "1", "PERSYN_NO_FUSED_HIST": "1",
+                                  "PERSYN_PENALTY_PER_ANCHOR": "1"}])
+def test_em_scheduling_variants_bit_identical(gpu_ctx, monkeypatch, env):
+    """The EM step's scheduling choices -- side-stream overlap (default) or one
+    stream, CUDA-graph replay, changed-only rescoring, the M-step's fused
+    histogram and the per-candidate penalty table -- never change a bit."""
+    ex, init = _stage()
+    ix = api.make_pca_tree_index(ex, 8, d_fixed=16, branching=8, max_depth=3, seed=1,
+                                 hist_bins=16, ctx=gpu_ctx)
+    cfg = api.OptimizerConfig(max_iterations=5, min_iterations=5, convergence_fraction=1e-9,
+                              nbhd_width=8, spacing=2, patch_width=2,
+                              budget=api.QueryBudget.exact())
+
+    def run():
+        lv = api.Level(init, ix, cfg)
+        lv.prime()
+        st = lv.iterate(5)
+        planes, idx, dist = lv.download()
+        return planes, idx, dist, [(s.energy, s.changed, s.lsq_energy_after) for s in st]
+
+    ref = run()
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    got = run()
+    for k in env:
+        monkeypatch.delenv(k)
+    for a, b in zip(ref[:3], got[:3]):
+        assert np.array_equal(a, b)
+    assert ref[3] == got[3]
