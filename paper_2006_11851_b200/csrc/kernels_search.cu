@@ -358,10 +358,31 @@ __device__ __forceinline__ double dist2_seq(const double* __restrict__ q,
 
 // Out-of-line copy for rarely executed call sites (seeds, filter survivors):
 // keeps the hot loops of the tile kernel small enough for the I-cache.
+// Loads are issued 8 at a time (16-byte vectors when the rows are 16-byte
+// aligned) ahead of the sequential chain: one memory latency per 8 dims
+// instead of one per dim.  Same j-ascending sub, mul, add.
 __device__ __noinline__ double dist2_seq_cold(const double* __restrict__ q,
                                              const double* __restrict__ p, int d) {
   double acc = 0.0;
-  for (int j = 0; j < d; ++j) {
+  int j = 0;
+  if (((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(p)) & 15) == 0) {
+    for (; j + 8 <= d; j += 8) {
+      double2 qv[4], pv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        qv[u] = __ldg(reinterpret_cast<const double2*>(q + j) + u);
+        pv[u] = __ldg(reinterpret_cast<const double2*>(p + j) + u);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        double t = dsub(qv[u].x, pv[u].x);
+        acc = dadd(acc, dmul(t, t));
+        t = dsub(qv[u].y, pv[u].y);
+        acc = dadd(acc, dmul(t, t));
+      }
+    }
+  }
+  for (; j < d; ++j) {
     const double t = dsub(q[j], p[j]);
     acc = dadd(acc, dmul(t, t));
   }
