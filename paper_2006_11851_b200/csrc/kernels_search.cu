@@ -15,6 +15,16 @@
 #include "numerics.cuh"
 #include "psg_internal.h"
 
+// d <= 32 tile kernel: 5 CTAs x 3 warps per SM, i.e. a 128-register cap
+// (measured: 128 regs + 36 B spill 1.78 ms/search; uncapped 165 regs at 4
+// CTAs 1.87 ms).  Exact-recheck load batch in double2 (4 = 8 dims).
+#ifndef TILE_MIN_CTAS
+#define TILE_MIN_CTAS 5
+#endif
+#ifndef RECHECK_BATCH
+#define RECHECK_BATCH 4
+#endif
+
 namespace psg {
 
 // ----------------------------------------------------------------------------
@@ -361,20 +371,21 @@ __device__ __forceinline__ double dist2_seq(const double* __restrict__ q,
 // Loads are issued 8 at a time (16-byte vectors when the rows are 16-byte
 // aligned) ahead of the sequential chain: one memory latency per 8 dims
 // instead of one per dim.  Same j-ascending sub, mul, add.
+constexpr int kRB = RECHECK_BATCH;  // double2 per batch
 __device__ __noinline__ double dist2_seq_cold(const double* __restrict__ q,
                                              const double* __restrict__ p, int d) {
   double acc = 0.0;
   int j = 0;
   if (((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(p)) & 15) == 0) {
-    for (; j + 8 <= d; j += 8) {
-      double2 qv[4], pv[4];
+    for (; j + 2 * kRB <= d; j += 2 * kRB) {
+      double2 qv[kRB], pv[kRB];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kRB; ++u) {
         qv[u] = __ldg(reinterpret_cast<const double2*>(q + j) + u);
         pv[u] = __ldg(reinterpret_cast<const double2*>(p + j) + u);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kRB; ++u) {
         double t = dsub(qv[u].x, pv[u].x);
         acc = dadd(acc, dmul(t, t));
         t = dsub(qv[u].y, pv[u].y);
@@ -1048,7 +1059,7 @@ constexpr int kTileStack = 48;
 constexpr int kTileMaxB = 16;
 
 template <int DP, int kTileWarps>
-__global__ void __launch_bounds__(32 * kTileWarps) search_tile_kernel(SearchArgs a) {
+__global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : 1) search_tile_kernel(SearchArgs a) {
   constexpr int RS = DP + 4;  // padded staging row (floats): conflict-free 16 B accesses
   __shared__ int2 st_meta[kTileWarps][kTileStack];
   __shared__ float st_lb[kTileWarps][kTileStack][32];
