@@ -1041,6 +1041,14 @@ bool level_step(psg_level& L, psg_iter_stats* st, bool honor) {
 }
 
 // Host rows [p0, e1) of the global image (planes [C][Hl][W]).
+// Device rows [p0, e1) of the global image (planes [C][Hl][W]).
+void upload_state_dev(psg_level& L, const double* dev_planes) {
+  L.counts_fresh = false;
+  PSG_CUDA(cudaMemcpyAsync(L.planes.p, dev_planes, sizeof(double) * (size_t)L.P * L.C,
+                           cudaMemcpyDeviceToDevice, L.ctx->stream));
+  launch_make_mirror(L.ctx, L.planes.p, L.C, L.W, L.Hl, L.mirror.p);
+}
+
 void upload_state(psg_level& L, const double* host_planes) {
   L.counts_fresh = false;
   L.planes.upload(L.ctx, host_planes, (size_t)L.P * L.C);
@@ -1506,9 +1514,13 @@ psg_status psg_level_create(psg_ctx* ctx, const psg_index* index, const double* 
     if (ix.from_vectors) fail(PSG_E_SHAPE, "optimize_level needs an exemplar-window index");
     psg::validate_cfg(*cfg, ix.w, W, H);
     auto L = std::make_unique<psg_level>();
+    // the image copy is issued first: from pinned host memory it is a DMA that
+    // overlaps the host-side level setup (plan, covering ranges, lattices)
+    psg::DBuf<double> staged((size_t)W * H * ix.C);
+    staged.upload(ctx, init, (size_t)W * H * ix.C);
     psg::level_setup(*L, ctx, ix, W, H, *cfg, true);
     psg::level_set_hist(*L, ex_hist);
-    psg::upload_state(*L, init);
+    psg::upload_state_dev(*L, staged.p);
     *out = L.release();
   });
 }
