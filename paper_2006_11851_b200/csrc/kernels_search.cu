@@ -10,16 +10,19 @@
 #include <cuda_runtime.h>
 #include <float.h>
 
+#include <cuda_bf16.h>
 #include <cub/cub.cuh>
 
 #include "numerics.cuh"
 #include "psg_internal.h"
 
-// d <= 32 tile kernel: 5 CTAs x 3 warps per SM, i.e. a 128-register cap
-// (measured: 128 regs + 36 B spill 1.78 ms/search; uncapped 165 regs at 4
-// CTAs 1.87 ms).  Exact-recheck load batch in double2 (4 = 8 dims).
+// d <= 32 tile kernel: 4 CTAs x 4 warps per SM = 16 warps, a 128-register cap
+// (the bf16 stack bounds keep a 4-warp CTA under 48 KB of static shared
+// memory).  Measured per search on the bench stage: 3 warps x 5 CTAs 1.78 ms
+// (36 B spill), uncapped 165 registers at 4 x 3 warps 1.87 ms, 4 x 4 warps
+// 1.71 ms.  Exact-recheck load batch in double2 (4 = 8 dims).
 #ifndef TILE_MIN_CTAS
-#define TILE_MIN_CTAS 5
+#define TILE_MIN_CTAS 4
 #endif
 #ifndef RECHECK_BATCH
 #define RECHECK_BATCH 4
@@ -1062,7 +1065,9 @@ template <int DP, int kTileWarps>
 __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : 1) search_tile_kernel(SearchArgs a) {
   constexpr int RS = DP + 4;  // padded staging row (floats): conflict-free 16 B accesses
   __shared__ int2 st_meta[kTileWarps][kTileStack];
-  __shared__ float st_lb[kTileWarps][kTileStack][32];
+  // per-lane node bounds of the stack as bf16 rounded DOWN: still valid lower
+  // bounds (pruning only loosens by < 0.4%), half the largest shared array
+  __shared__ __nv_bfloat16 st_lb[kTileWarps][kTileStack][32];
   __shared__ __align__(16) float stage_all[kTileWarps][32 * RS];
   __shared__ float aux_all[kTileWarps][2][32];
   __shared__ int2 cmeta_all[kTileWarps][kTileMaxB];
@@ -1072,7 +1077,7 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : 1)
   __shared__ unsigned tkey_all[kTileWarps][kTileMaxB];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int2* sm_ = st_meta[warp];
-  float(*slb)[32] = st_lb[warp];
+  __nv_bfloat16(*slb)[32] = st_lb[warp];
   float* stage = stage_all[warp];
   float* aux0 = aux_all[warp][0];
   float* aux1 = aux_all[warp][1];
@@ -1145,7 +1150,7 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : 1)
     // best rounded up to float: float compares against it can only keep more
     float bestf = __double2float_ru(best);
     if (lane == 0) sm_[0] = a.tree.meta[0];
-    slb[0][lane] = 0.f;
+    slb[0][lane] = __float2bfloat16_rd(0.f);
     int top = 1;
     __syncwarp();
     while (top > 0) {
@@ -1155,7 +1160,7 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : 1)
       int2 node = make_int2(0, 0);
       while (top > 0) {
         const int2 md = sm_[top - 1];
-        const bool want = slb[top - 1][lane] <= bestf;
+        const bool want = __bfloat162float(slb[top - 1][lane]) <= bestf;
         if (!__any_sync(0xffffffffu, want)) {  // km_tree.cpp:265 prune, per lane
           --top;
           continue;
@@ -1387,7 +1392,7 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : 1)
 #pragma unroll 1
       for (uint32_t m = keepmask; m; m &= m - 1) {
         const int c = __ffs(m) - 1;
-        slb[__shfl_sync(0xffffffffu, myslot, c)][lane] = tlb[c][lane];
+        slb[__shfl_sync(0xffffffffu, myslot, c)][lane] = __float2bfloat16_rd(tlb[c][lane]);
       }
       top += nkeep;
       __syncwarp();
@@ -1439,12 +1444,12 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
     if (ctx->hmma_tile && a.d <= 32 && launch_search_hmma(ctx, a)) return;
     if (!a.sched) fail(PSG_E_LOGIC, "tile search launched without its scheduler counters");
     const int64_t tiles = (a.nq + 31) / 32;
-    const int wpb = a.d <= 32 ? 3 : 2;  // static smem <= 48 KB per CTA
+    const int wpb = a.d <= 32 ? 4 : 2;  // static smem <= 48 KB per CTA
     int64_t blocks = (tiles + wpb - 1) / wpb;
-    const int64_t cap = a.d <= 32 ? tile_resident_ctas<32, 3>(ctx) : tile_resident_ctas<64, 2>(ctx);
+    const int64_t cap = a.d <= 32 ? tile_resident_ctas<32, 4>(ctx) : tile_resident_ctas<64, 2>(ctx);
     if (blocks > cap) blocks = cap;
     if (a.d <= 32)
-      search_tile_kernel<32, 3><<<(int)blocks, 32 * 3, 0, ctx->stream>>>(a);
+      search_tile_kernel<32, 4><<<(int)blocks, 32 * 4, 0, ctx->stream>>>(a);
     else
       search_tile_kernel<64, 2><<<(int)blocks, 32 * 2, 0, ctx->stream>>>(a);
     PSG_LAUNCHED(ctx);
