@@ -160,10 +160,12 @@ void launch_penalty(psg_ctx* ctx, const Index& ix, const int32_t* idx, int64_t A
 // consecutive threads read consecutive exemplar pixels (coalesced), where the
 // per-anchor form gathers one random window per thread.  Same sequential sum
 // per entry as penalty_kernel, so table[idx[a]] is bit-identical to pen[a].
+template <int NS>  // NS > 0: compile-time histogram slot count
 __global__ void penalty_table_kernel(const float* __restrict__ ex_mirror, int ew, int C, int w,
                                      int nxe, int64_t N, const double* __restrict__ excess,
-                                     int bins, int slots, double* __restrict__ table) {
+                                     int bins, int slots_, double* __restrict__ table) {
   extern __shared__ double ex_s[];
+  const int slots = NS > 0 ? NS : slots_;
   for (int i = threadIdx.x; i < bins * slots; i += blockDim.x) ex_s[i] = excess[i];
   __syncthreads();
   const double area = (double)(w * w);
@@ -173,7 +175,21 @@ __global__ void penalty_table_kernel(const float* __restrict__ ex_mirror, int ew
     double total = 0.0;
     for (int dy = 0; dy < w; ++dy) {
       const float* z = ex_mirror + ((int64_t)(ey + dy) * ew + ex) * C;
-      for (int dx = 0; dx < w; ++dx)
+      int dx = 0;
+      if constexpr (NS > 0) {
+        // 4 pixels' loads and bins ahead of their sequential adds
+        for (; dx + 4 <= w; dx += 4) {
+          int b[4 * NS];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+              b[u * NS + s] = s * bins + bin_of_f32(__ldg(z + (dx + u) * C + s), bins);
+#pragma unroll
+          for (int k = 0; k < 4 * NS; ++k) total = dadd(total, ex_s[b[k]]);
+        }
+      }
+      for (; dx < w; ++dx)
         for (int s = 0; s < slots; ++s) {
           const int b = bin_of_f32(__ldg(z + dx * C + s), bins);
           total = dadd(total, ex_s[s * bins + b]);
@@ -188,8 +204,9 @@ void launch_penalty_table(psg_ctx* ctx, const Index& ix, const double* excess, i
   ProfScope _prof(ctx, K_PENALTY);
   if (ix.N <= 0) return;
   const size_t sm = sizeof(double) * bins * slots;
-  penalty_table_kernel<<<grid_for(ctx, ix.N, 128), 128, sm, ctx->stream>>>(
-      ix.ex_mirror, ix.ew, ix.C, ix.w, ix.nxe, ix.N, excess, bins, slots, table);
+  auto k = slots == 3 ? penalty_table_kernel<3> : penalty_table_kernel<0>;
+  k<<<grid_for(ctx, ix.N, 128), 128, sm, ctx->stream>>>(ix.ex_mirror, ix.ew, ix.C, ix.w, ix.nxe,
+                                                        ix.N, excess, bins, slots, table);
   PSG_LAUNCHED(ctx);
 }
 

@@ -9,6 +9,7 @@
 
 #include <math.h>
 #include <stdint.h>
+#include <string.h>
 
 #ifdef __CUDACC__
 #define PSG_HD __host__ __device__ __forceinline__
@@ -150,6 +151,19 @@ PSG_HD double pow_cr(double x, double y) {
 // the sequential sum is a function of the count alone.  Within one binade a
 // constant increment is exact after two in-binade steps (ties-to-even makes
 // the ulp-count even after one tie step), which lets us jump in bulk.
+// frexp exponent of a positive normal double, and 2^e, from the bit pattern
+PSG_HD int exp_of(double x) {
+  int64_t b;
+  memcpy(&b, &x, sizeof b);
+  return (int)((b >> 52) & 0x7ff) - 1022;
+}
+PSG_HD double pow2(int e) {  // 2^e for -1022 <= e <= 1023
+  const int64_t b = (int64_t)(e + 1023) << 52;
+  double x;
+  memcpy(&x, &b, sizeof x);
+  return x;
+}
+
 PSG_HD double hist_mass(int64_t count, double inv) {
   double m = 0.0;
   int64_t rem = count;
@@ -157,20 +171,20 @@ PSG_HD double hist_mass(int64_t count, double inv) {
     const double m1 = dadd(m, inv);
     --rem;
     if (rem == 0 || m == 0.0) { m = m1; continue; }
-    int e0, e1;
-    frexp(m, &e0);
-    frexp(m1, &e1);
+    // m, m1 >= inv > 0 are normal (inv = 1/P): exponents from the bits
+    const int e0 = exp_of(m), e1 = exp_of(m1);
     if (e0 != e1) { m = m1; continue; }
     const double m2 = dadd(m1, inv);
     --rem;
-    int e2;
-    frexp(m2, &e2);
+    const int e2 = exp_of(m2);
     if (e2 != e1 || rem == 0) { m = m2; continue; }
-    // steady state inside binade [2^(e2-1), 2^e2): ulp u = 2^(e2-53)
-    const double u = ldexp(1.0, e2 - 53);
-    const double top = ldexp(1.0, e2);
-    const int64_t T = (int64_t)((top - m2) / u);      // exact
-    const int64_t delta = (int64_t)((m2 - m1) / u);   // exact
+    // steady state inside binade [2^(e2-1), 2^e2): ulp u = 2^(e2-53); the
+    // differences below are multiples of u, so scaling by 1/u is exact
+    const double inv_u = pow2(53 - e2);
+    const double top = pow2(e2);
+    const int64_t T = (int64_t)dmul(dsub(top, m2), inv_u);      // exact
+    const int64_t delta = (int64_t)dmul(dsub(m2, m1), inv_u);   // exact
+    const double u = pow2(e2 - 53);
     int64_t k = (T - 1) / delta;
     if (k > rem) k = rem;
     m = dadd(m2, dmul((double)k, (double)delta * u));  // exact: below top
