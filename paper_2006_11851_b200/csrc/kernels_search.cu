@@ -24,6 +24,9 @@
 #ifndef TILE_MIN_CTAS
 #define TILE_MIN_CTAS 4
 #endif
+#ifndef TILE64_MIN_CTAS
+#define TILE64_MIN_CTAS 6  // d in (32, 64]: 6 CTAs x 2 warps (168 registers): cfg4 finest search 31 -> 27 ms
+#endif
 #ifndef RECHECK_BATCH
 #define RECHECK_BATCH 4
 #endif
@@ -1062,7 +1065,7 @@ constexpr int kTileStack = 48;
 constexpr int kTileMaxB = 16;
 
 template <int DP, int kTileWarps>
-__global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : 1) search_tile_kernel(SearchArgs a) {
+__global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TILE64_MIN_CTAS) search_tile_kernel(SearchArgs a) {
   constexpr int RS = DP + 4;  // padded staging row (floats): conflict-free 16 B accesses
   __shared__ int2 st_meta[kTileWarps][kTileStack];
   // per-lane node bounds of the stack as bf16 rounded DOWN: still valid lower

@@ -24,7 +24,7 @@ def _stage(size=40, out=56, G=2, seed=4):
 
 
 @pytest.mark.parametrize("variant", ["default", "warp", "mma", "hmma"])
-@pytest.mark.parametrize("d", [16, 32])
+@pytest.mark.parametrize("d", [16, 32, 48])
 def test_exact_search_variants_bit_exact(port, monkeypatch, variant, d):
     if variant != "default":
         monkeypatch.setenv("PERSYN_SEARCH", variant)
