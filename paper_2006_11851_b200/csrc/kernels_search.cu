@@ -272,6 +272,98 @@ __global__ void __launch_bounds__(256, 3) project2_kernel(
   }
 }
 
+// 32 < d <= 48 (cfg4: d = 48) windows: lane (g2, kp) accumulates THREE
+// consecutive k (3 kp .. 3 kp + 2) for RQ anchors, so 16 lanes cover 48
+// components (the KPT = 2 kernel leaves 16 of its 64 lanes idle at d = 48).
+// Same per-(anchor, k) j-sequential chains: bit-identical.  basisT is
+// [D][64] (zero-padded).
+template <int RQ, int JCT>
+__global__ void __launch_bounds__(256, 2) project48_kernel(
+    const float* __restrict__ src, int img_w, int C, int w, const int32_t* __restrict__ xs,
+    const int32_t* __restrict__ ys, int nx, int64_t n, int D,
+    const double* __restrict__ mean, const double* __restrict__ basisT,  // [D][64]
+    int d, double* __restrict__ out) {
+  constexpr int TQ = 8 * 2 * RQ, JC = JCT, JCp = JC + 2, BS = 64;
+  extern __shared__ __align__(16) double smem48[];
+  double* cen = smem48;             // [TQ][JCp]
+  double* bas = smem48 + TQ * JCp;  // [JC][64]
+  __shared__ int64_t base_s[TQ];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g2 = lane >> 4, kp = lane & 15;
+  const int64_t q0 = (int64_t)blockIdx.x * TQ;
+  if (tid < TQ) {
+    const int64_t qi = q0 + tid;
+    int64_t b = -1;
+    if (qi < n) b = ((int64_t)ys[qi / nx] * img_w + xs[qi % nx]) * C;
+    base_s[tid] = b;
+  }
+  double acc[3][RQ];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int r = 0; r < RQ; ++r) acc[i][r] = 0.0;
+  const int qb = (warp * 2 + g2) * RQ;
+  const int n_chunks = D / JC;  // JC | w * C
+  for (int ch = 0; ch < n_chunks; ++ch) {
+    const int j0 = ch * JC;
+    const int64_t roff = (int64_t)(j0 / (w * C)) * img_w * C + j0 % (w * C);
+    __syncthreads();
+    constexpr int PER = (TQ * JC + 255) / 256, H = 4;
+#pragma unroll
+    for (int h = 0; h < PER; h += H) {
+      float xv[H];
+      double mv[H];
+#pragma unroll
+      for (int k = 0; k < H; ++k) {
+        const int f = tid + 256 * (h + k);
+        const int q = f / JC, jj = f - q * JC;
+        xv[k] = 0.f;
+        mv[k] = 0.0;
+        if (h + k < PER && f < TQ * JC && base_s[q] >= 0) {
+          xv[k] = __ldg(src + base_s[q] + roff + jj);
+          mv[k] = __ldg(mean + j0 + jj);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < H; ++k) {
+        const int f = tid + 256 * (h + k);
+        const int q = f / JC, jj = f - q * JC;
+        if (h + k < PER && f < TQ * JC)
+          cen[q * JCp + jj] = base_s[q] >= 0 ? dsub((double)xv[k], mv[k]) : 0.0;
+      }
+    }
+    for (int f = tid; f < JC * BS / 2; f += 256)
+      reinterpret_cast<double2*>(bas)[f] =
+          __ldg(reinterpret_cast<const double2*>(basisT + (int64_t)j0 * BS) + f);
+    __syncthreads();
+#pragma unroll 2
+    for (int jj = 0; jj < JC; jj += 2) {
+      double b0[3], b1[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        b0[i] = bas[jj * BS + 3 * kp + i];
+        b1[i] = bas[(jj + 1) * BS + 3 * kp + i];
+      }
+#pragma unroll
+      for (int r = 0; r < RQ; ++r) {
+        const double2 c = *reinterpret_cast<const double2*>(cen + (qb + r) * JCp + jj);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) acc[i][r] = dadd(acc[i][r], dmul(c.x, b0[i]));
+#pragma unroll
+        for (int i = 0; i < 3; ++i) acc[i][r] = dadd(acc[i][r], dmul(c.y, b1[i]));
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RQ; ++r) {
+    const int64_t qi = q0 + qb + r;
+    if (qi >= n) continue;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      if (3 * kp + i < d) out[qi * d + 3 * kp + i] = acc[i][r];
+  }
+}
+
 template <bool kWindows>
 static void launch_project(psg_ctx* ctx, const float* src, int img_w, int C, int w,
                            const int32_t* xs, const int32_t* ys, int nx, int64_t n, int D, int JC,
@@ -300,6 +392,13 @@ static void launch_project(psg_ctx* ctx, const float* src, int img_w, int C, int
     const int blocks2 = (int)((n + TQ2 - 1) / TQ2);
     k<<<blocks2, 256, sm, ctx->stream>>>(src, img_w, C, w, xs, ys, nx, n, D, JC, mean, basisT, d,
                                           out);
+  } else if (d <= 48 && kWindows && (JC == 32 || JC == 40) && !std::getenv("PERSYN_PROJECT_KPT2")) {
+    constexpr int TQ2 = 8 * 2 * RQ;
+    const size_t sm = sizeof(double) * ((size_t)TQ2 * (JC + 2) + (size_t)JC * 64);
+    auto k = JC == 32 ? project48_kernel<RQ, 32> : project48_kernel<RQ, 40>;
+    PSG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    const int blocks2 = (int)((n + TQ2 - 1) / TQ2);
+    k<<<blocks2, 256, sm, ctx->stream>>>(src, img_w, C, w, xs, ys, nx, n, D, mean, basisT, d, out);
   } else if (d <= 64) {
     const size_t sm = sizeof(double) * ((size_t)TQ * JCp + (size_t)JC * 64);
     auto k = project_kernel<2, RQ, kWindows>;
