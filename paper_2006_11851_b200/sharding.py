@@ -142,11 +142,17 @@ class DistComm:
         import torch
         (p,) = parts
         t = torch.tensor(p, dtype=torch.float64, device=self.device)
-        out = [torch.zeros_like(t) for _ in range(self.world)]
-        self.dist.all_gather(out, t)
+        if self.cuda:  # one gather, one device->host copy
+            flat = torch.empty(self.world * PARTIALS, dtype=torch.float64, device=self.device)
+            self.dist.all_gather_into_tensor(flat, t)
+            rows = flat.cpu().numpy().reshape(self.world, PARTIALS)
+        else:
+            out = [torch.zeros_like(t) for _ in range(self.world)]
+            self.dist.all_gather(out, t)
+            rows = [o.numpy() for o in out]
         tot = np.zeros(PARTIALS)
-        for o in out:  # rank order
-            tot = tot + o.cpu().numpy()
+        for r in rows:  # rank order: the same sum on every rank
+            tot = tot + r
         return [tot]
 
 
