@@ -278,10 +278,19 @@ __global__ void __launch_bounds__(256) mstep_kernel(MstepArgs a) {
           ++ey;
           ex -= a.nxe;
         }
-        const float* z = a.ex_mirror + ((int64_t)(ey + dy) * a.ew + ex + (x - a.xs[ix])) * C;
+        const int64_t zp = (int64_t)(ey + dy) * a.ew + ex + (x - a.xs[ix]);
         float zv[CMAX];
+        if (NC > 0 && a.ex8) {  // 32-byte padded pixel: two 16-byte loads
+          const float4* z4 = reinterpret_cast<const float4*>(a.ex8 + zp * 8);
+          const float4 z0 = __ldg(z4), z1 = __ldg(z4 + 1);
+          const float zc[8] = {z0.x, z0.y, z0.z, z0.w, z1.x, z1.y, z1.z, z1.w};
 #pragma unroll
-        for (int c = 0; c < CMAX; ++c) zv[c] = (NC > 0 || c < C) ? __ldg(z + c) : 0.f;
+          for (int c = 0; c < CMAX; ++c) zv[c] = zc[c];
+        } else {
+          const float* z = a.ex_mirror + zp * C;
+#pragma unroll
+          for (int c = 0; c < CMAX; ++c) zv[c] = (NC > 0 || c < C) ? __ldg(z + c) : 0.f;
+        }
 #pragma unroll
         for (int c = 0; c < CMAX; ++c)
           if (NC > 0 || c < C) acc[c] = dadd(acc[c], dmul(we, (double)zv[c]));

@@ -43,6 +43,29 @@ __global__ void make_mirror_kernel(const double* __restrict__ planes, int C, int
   }
 }
 
+// planes -> [H][W][8] fp32, channels zero-padded to 8 (32-byte pixels): the
+// candidate side of the rescoring reads a window row as 16-byte vectors.
+__global__ void make_mirror8_kernel(const double* __restrict__ planes, int C, int64_t P,
+                                    float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float v[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v[c] = c < C ? (float)planes[c * P + i] : 0.f;
+    float4* o = reinterpret_cast<float4*>(out + i * 8);
+    o[0] = make_float4(v[0], v[1], v[2], v[3]);
+    o[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+}
+
+void launch_make_mirror8(psg_ctx* ctx, const double* planes, int C, int W, int H, float* out) {
+  ProfScope _prof(ctx, K_MIRROR);
+  const int64_t P = (int64_t)W * H;
+  int blocks = (int)std::min<int64_t>((P + 255) / 256, (int64_t)ctx->num_sms * 16);
+  make_mirror8_kernel<<<std::max(blocks, 1), 256, 0, ctx->stream>>>(planes, C, P, out);
+  PSG_LAUNCHED(ctx);
+}
+
 void launch_make_mirror(psg_ctx* ctx, const double* planes, int C, int W, int H, float* mirror) {
   ProfScope _prof(ctx, K_MIRROR);
   const int64_t P = (int64_t)W * H;
@@ -1782,6 +1805,41 @@ void launch_make_fp32_copies(psg_ctx* ctx, const double* soa, int64_t N, int d, 
 // Full-D rescoring (optimizer.cpp:117-124, :232-234): one thread per query,
 // j ascending over the window (dy, dx, c) against the candidate's dense
 // exemplar window — the candidate matrix is never materialised.
+// Candidate rows from the 8-channel padded exemplar mirror (two 16-byte
+// loads per pixel), NC = C at compile time; same (dy, dx, c) order.
+template <int NC>
+__device__ __forceinline__ double window_dist2_pad(const float* __restrict__ mirror, int img_w,
+                                                   int w, int ax, int ay,
+                                                   const float* __restrict__ ex8, int ew, int ex,
+                                                   int ey) {
+  double acc = 0.0;
+  for (int dy = 0; dy < w; ++dy) {
+    const float* v = mirror + ((int64_t)(ay + dy) * img_w + ax) * NC;
+    const float4* z4 = reinterpret_cast<const float4*>(ex8 + ((int64_t)(ey + dy) * ew + ex) * 8);
+#pragma unroll 2
+    for (int dx = 0; dx < w; ++dx) {
+      const float4 z0 = __ldg(z4 + 2 * dx);
+      const float4 z1 = __ldg(z4 + 2 * dx + 1);
+      const float zc[8] = {z0.x, z0.y, z0.z, z0.w, z1.x, z1.y, z1.z, z1.w};
+      float vc[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) vc[c] = __ldg(v + dx * NC + c);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const double t = dsub((double)vc[c], (double)zc[c]);
+        acc = dadd(acc, dmul(t, t));
+      }
+    }
+  }
+  return acc;
+}
+
+__device__ __forceinline__ double window_dist2_any(const float* __restrict__ mirror, int img_w,
+                                                   int C, int w, int ax, int ay,
+                                                   const float* __restrict__ ex_mirror,
+                                                   const float* __restrict__ ex8, int ew, int ex,
+                                                   int ey);
+
 __device__ __forceinline__ double window_dist2(const float* __restrict__ mirror, int img_w, int C,
                                                int w, int ax, int ay,
                                                const float* __restrict__ ex_mirror, int ew,
@@ -1813,17 +1871,28 @@ __device__ __forceinline__ double window_dist2(const float* __restrict__ mirror,
   return acc;
 }
 
+__device__ __forceinline__ double window_dist2_any(const float* __restrict__ mirror, int img_w,
+                                                   int C, int w, int ax, int ay,
+                                                   const float* __restrict__ ex_mirror,
+                                                   const float* __restrict__ ex8, int ew, int ex,
+                                                   int ey) {
+  if (ex8 && C == 5) return window_dist2_pad<5>(mirror, img_w, w, ax, ay, ex8, ew, ex, ey);
+  if (ex8 && C == 4) return window_dist2_pad<4>(mirror, img_w, w, ax, ay, ex8, ew, ex, ey);
+  return window_dist2(mirror, img_w, C, w, ax, ay, ex_mirror, ew, ex, ey);
+}
+
 __global__ void rescore_windows_kernel(const float* __restrict__ mirror, int img_w, int C, int w,
                                        const int32_t* __restrict__ xs,
                                        const int32_t* __restrict__ ys, int nx, int64_t n,
-                                       const float* __restrict__ ex_mirror, int ew, int nxe,
+                                       const float* __restrict__ ex_mirror,
+                                       const float* __restrict__ ex8, int ew, int nxe,
                                        const int32_t* __restrict__ idx,
                                        double* __restrict__ dist) {
   for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n;
        a += (int64_t)gridDim.x * blockDim.x) {
     const int32_t id = idx[a];
-    dist[a] = sqrt(window_dist2(mirror, img_w, C, w, xs[a % nx], ys[a / nx], ex_mirror, ew,
-                                id % nxe, id / nxe));
+    dist[a] = sqrt(window_dist2_any(mirror, img_w, C, w, xs[a % nx], ys[a / nx], ex_mirror, ex8,
+                                    ew, id % nxe, id / nxe));
   }
 }
 
@@ -1835,8 +1904,9 @@ __global__ void rescore_windows_kernel(const float* __restrict__ mirror, int img
 constexpr int kRescoreBlock = 256;
 __global__ void __launch_bounds__(kRescoreBlock) rescore_changed_kernel(
     const float* __restrict__ mirror, int img_w, int C, int w, const int32_t* __restrict__ xs,
-    const int32_t* __restrict__ ys, int nx, int64_t n, const float* __restrict__ ex_mirror, int ew,
-    int nxe, const int32_t* __restrict__ idx, const int32_t* __restrict__ prev_idx,
+    const int32_t* __restrict__ ys, int nx, int64_t n, const float* __restrict__ ex_mirror,
+    const float* __restrict__ ex8, int ew, int nxe, const int32_t* __restrict__ idx,
+    const int32_t* __restrict__ prev_idx,
     const double* __restrict__ prev_dist, double* __restrict__ dist) {
   __shared__ int list[kRescoreBlock];
   __shared__ int cnt;
@@ -1860,8 +1930,8 @@ __global__ void __launch_bounds__(kRescoreBlock) rescore_changed_kernel(
   for (int i = tid; i < cnt; i += kRescoreBlock) {
     const int64_t b = (int64_t)blockIdx.x * kRescoreBlock + list[i];
     const int32_t id = idx[b];
-    dist[b] = sqrt(window_dist2(mirror, img_w, C, w, xs[b % nx], ys[b / nx], ex_mirror, ew,
-                                id % nxe, id / nxe));
+    dist[b] = sqrt(window_dist2_any(mirror, img_w, C, w, xs[b % nx], ys[b / nx], ex_mirror, ex8,
+                                    ew, id % nxe, id / nxe));
   }
 }
 
@@ -1870,11 +1940,12 @@ void launch_rescore_windows(psg_ctx* ctx, const float* mirror, int img_w, int C,
                             double* dist, const int32_t* prev_idx, const double* prev_dist) {
   ProfScope _prof(ctx, K_RESCORE);
   if (anchors.count <= 0) return;
+  const float* ex8 = std::getenv("PERSYN_NO_EX8") ? nullptr : ix.ex_mirror8;
   if (prev_idx && prev_dist) {
     const int64_t blocks = (anchors.count + kRescoreBlock - 1) / kRescoreBlock;
     rescore_changed_kernel<<<(unsigned)blocks, kRescoreBlock, 0, ctx->stream>>>(
         mirror, img_w, C, w, anchors.xs, anchors.ys, anchors.nx, anchors.count, ix.ex_mirror,
-        ix.ew, ix.nxe, idx, prev_idx, prev_dist, dist);
+        ex8, ix.ew, ix.nxe, idx, prev_idx, prev_dist, dist);
     PSG_LAUNCHED(ctx);
     return;
   }
@@ -1882,7 +1953,7 @@ void launch_rescore_windows(psg_ctx* ctx, const float* mirror, int img_w, int C,
   int64_t blocks = (anchors.count + threads - 1) / threads;
   if (blocks > (int64_t)ctx->num_sms * 32) blocks = (int64_t)ctx->num_sms * 32;
   rescore_windows_kernel<<<(int)blocks, threads, 0, ctx->stream>>>(
-      mirror, img_w, C, w, anchors.xs, anchors.ys, anchors.nx, anchors.count, ix.ex_mirror,
+      mirror, img_w, C, w, anchors.xs, anchors.ys, anchors.nx, anchors.count, ix.ex_mirror, ex8,
       ix.ew, ix.nxe, idx, dist);
   PSG_LAUNCHED(ctx);
 }

@@ -80,6 +80,7 @@ struct Index {
   int64_t N = 0;
   int nxe = 0;              // dense DB anchors per row (ew - w + 1)
   float* ex_mirror = nullptr;  // [eh][ew][C] fp32 (image index)
+  float* ex_mirror8 = nullptr; // [eh][ew][8] fp32, channels zero-padded (C <= 8)
   float* vectors = nullptr;    // [N][D] fp32 (vector index)
   double* mean = nullptr;      // [D]
   double* basis = nullptr;     // [d][D]
@@ -191,6 +192,7 @@ struct AnchorSet {
 
 // planes [C][H][W] fp64 -> mirror [H][W][C] fp32
 void launch_make_mirror(psg_ctx* ctx, const double* planes, int C, int W, int H, float* mirror);
+void launch_make_mirror8(psg_ctx* ctx, const double* planes, int C, int W, int H, float* out);
 // Exact fp64 projection of window features (pca.cpp:27-41).
 void launch_project_windows(psg_ctx* ctx, const float* mirror, int img_w, int C, int w,
                             AnchorSet anchors, const double* mean, const double* basis, int d,
@@ -307,6 +309,7 @@ struct MstepArgs {
   int plane_rows;     // rows allocated per plane (plane stride = W * plane_rows)
   const float* ex_mirror;
   int ew, nxe;
+  const float* ex8 = nullptr;  // optional [eh][ew][8] padded candidate pixels
   double* planes;  // out [C][plane_rows][W]
   float* mirror;   // out [H][W][C]
   int* flags;

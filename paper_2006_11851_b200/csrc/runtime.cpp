@@ -224,7 +224,7 @@ double pow_cr_host(double x, double y) { return pow_cr(x, y); }
 Index::~Index() {
   // stream-ordered frees (the allocations come from the context's pool)
   cudaStream_t st = ctx ? ctx->stream : nullptr;
-  for (void* p : {(void*)ex_mirror, (void*)vectors, (void*)mean, (void*)basis, (void*)proj, (void*)proj_soa, (void*)perm, (void*)tree.centroid, (void*)tree.radius, (void*)tree.first_child, (void*)tree.n_children, (void*)tree.leaf_start, (void*)tree.leaf_count, (void*)tree.centroid32, (void*)tree.radius32, (void*)tree.cnorm32, (void*)proj32_q4, (void*)tree.centroid32T, (void*)tree.boxlo, (void*)tree.boxhi, (void*)tree.meta, (void*)tree.tie, (void*)pnorm32, (void*)ex_hist, (void*)brute_op, (void*)brute_n2, (void*)brute_nup, (void*)brute_mu, (void*)brute_tmax})
+  for (void* p : {(void*)ex_mirror, (void*)ex_mirror8, (void*)vectors, (void*)mean, (void*)basis, (void*)proj, (void*)proj_soa, (void*)perm, (void*)tree.centroid, (void*)tree.radius, (void*)tree.first_child, (void*)tree.n_children, (void*)tree.leaf_start, (void*)tree.leaf_count, (void*)tree.centroid32, (void*)tree.radius32, (void*)tree.cnorm32, (void*)proj32_q4, (void*)tree.centroid32T, (void*)tree.boxlo, (void*)tree.boxhi, (void*)tree.meta, (void*)tree.tie, (void*)pnorm32, (void*)ex_hist, (void*)brute_op, (void*)brute_n2, (void*)brute_nup, (void*)brute_mu, (void*)brute_tmax})
     if (p) cudaFreeAsync(p, st);
 }
 
@@ -452,6 +452,10 @@ std::unique_ptr<psg_index> create_index_from_device_planes(psg_ctx* ctx, const d
   ix.N = (int64_t)ix.nxe * (eh - w + 1);
   ix.ex_mirror = dalloc<float>((size_t)ew * eh * C);
   launch_make_mirror(ctx, ex_dev, C, ew, eh, ix.ex_mirror);
+  if (C <= 8) {
+    ix.ex_mirror8 = dalloc<float>((size_t)ew * eh * 8);
+    launch_make_mirror8(ctx, ex_dev, C, ew, eh, ix.ex_mirror8);
+  }
   build_exemplar_hist(ctx, ix, ex_dev, cfg.hist_bins, cfg.hist_include_scale);
   finish_index(ctx, ix, mean, basis, d, cfg);
   return h;
@@ -809,6 +813,7 @@ MstepArgs mstep_args(psg_level& L) {
   m.C = L.C;
   m.w = L.w;
   m.ex_mirror = ix.ex_mirror;
+  m.ex8 = std::getenv("PERSYN_NO_EX8") ? nullptr : ix.ex_mirror8;
   m.ew = ix.ew;
   m.nxe = ix.nxe;
   m.planes = L.planes.p;
@@ -1253,6 +1258,10 @@ psg_status psg_index_create_brute(psg_ctx* ctx, const double* ex_planes, int C, 
     ix.N = (int64_t)ix.nxe * (eh - w + 1);
     ix.ex_mirror = psg::dalloc<float>((size_t)ew * eh * C);
     psg::launch_make_mirror(ctx, ex.p, C, ew, eh, ix.ex_mirror);
+    if (C <= 8) {
+      ix.ex_mirror8 = psg::dalloc<float>((size_t)ew * eh * 8);
+      psg::launch_make_mirror8(ctx, ex.p, C, ew, eh, ix.ex_mirror8);
+    }
     psg::build_exemplar_hist(ctx, ix, ex.p, hist_bins, hist_include_scale);
     psg::brute_prepare(ctx, ix);
     *out = h.release();
