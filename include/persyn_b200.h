@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define PSG_ABI_VERSION 1
+#define PSG_ABI_VERSION 2
 
 typedef enum {
   PSG_OK = 0,
@@ -73,7 +73,20 @@ typedef struct {
   uint64_t seed;          /* tree seed (pipeline.cpp:54-56 level_seed)        */
   int hist_bins;          /* exemplar histogram bins, 0 = none                */
   int hist_include_scale; /* histogram over guidance planes too               */
+  int tree_kind;          /* psg_tree_kind                                    */
 } psg_index_cfg;
+
+/* Which k-means tree an index builds.  Exact queries return the same answer on
+ * any tree (km_tree.cpp:251-278); greedy / backtrack(m) answers depend on it.
+ *  PSG_TREE_DEVICE    : built on the device, level-synchronous, one RNG stream
+ *                       per node, optional depth cap (max_depth).
+ *  PSG_TREE_REFERENCE : the reference's own tree, KmTree::build
+ *                       (km_tree.cpp:141-195) replicated exactly -- one
+ *                       std::mt19937_64 consumed in the recursion's order,
+ *                       unbounded depth (max_depth must be 0) -- so that
+ *                       greedy / backtrack(m) answers equal the reference's
+ *                       make_pca_tree_index (optimizer.cpp:214-224). */
+typedef enum { PSG_TREE_DEVICE = 0, PSG_TREE_REFERENCE = 1 } psg_tree_kind;
 
 /* OptimizerConfig (include/persyn/optimizer.hpp:37-52). */
 typedef struct {
@@ -182,7 +195,7 @@ typedef struct {
   const int32_t* leaf_ids;
 } psg_tree_import;
 psg_status psg_index_import_tree(psg_ctx* ctx, psg_index* index, const psg_tree_import* tree);
-/* Exemplar histogram [slots][bins] (pipeline.cpp:379-385). */
+/* Exemplar histogram [slots][bins] (pipeline.cpp:286-292). */
 psg_status psg_index_histograms(const psg_index* index, double* mass);
 /*
  * Batched SearchIndex::nearest (PcaTreeIndex::nearest, optimizer.cpp:226-236):

@@ -221,6 +221,14 @@ inline LevelResult optimize_level(const RgbsImage& init, const GpuSearchIndex& i
   const psg_opt_cfg c = to_cfg(cfg);
   const auto planes = planes_of(init);
   std::vector<double> masses;
+  if (exemplar_hist && cfg.histogram_matching) {
+    // HistogramSet::compatible (optimizer.cpp:65-67, thrown at :93-95): the
+    // library reads bins x (3 or 4) masses in the output set's channel order
+    std::vector<int> ids{0, 1, 2};
+    if (cfg.histogram_include_scale) ids.push_back(3);
+    if (exemplar_hist->bins() != cfg.histogram_bins || exemplar_hist->channel_ids() != ids)
+      throw ShapeError("output/exemplar histograms disagree on bins or channels");
+  }
   if (exemplar_hist) masses = masses_of(*exemplar_hist);
   std::vector<psg_iter_stats> st(static_cast<std::size_t>(cfg.max_iterations));
   std::vector<double> out(planes.size());

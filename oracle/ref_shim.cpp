@@ -422,7 +422,7 @@ int ref_assignment_distances(void* h, const double* planes, int W, int H, int w,
   });
 }
 
-// Exemplar histogram of the index's exemplar (pipeline.cpp:379-385 equivalent).
+// Exemplar histogram of the index's exemplar (pipeline.cpp:286-292 equivalent).
 int ref_index_histograms(void* h, int bins, int include_scale, double* mass) {
   return guard([&] {
     const HistogramSet hs =

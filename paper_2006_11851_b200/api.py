@@ -149,10 +149,14 @@ def default_context() -> Context:
     return _default_ctx
 
 
+TREE_DEVICE, TREE_REFERENCE = 0, 1  # psg_tree_kind
+
+
 def index_cfg(variance_target=0.95, d_cap=0, d_fixed=0, branching=4, max_depth=0,
-              leaf_threshold=0, seed=0, hist_bins=0, hist_include_scale=False) -> N.psg_index_cfg:
+              leaf_threshold=0, seed=0, hist_bins=0, hist_include_scale=False,
+              tree_kind=TREE_DEVICE) -> N.psg_index_cfg:
     return N.psg_index_cfg(variance_target, d_cap, d_fixed, branching, max_depth, leaf_threshold,
-                           seed, hist_bins, int(hist_include_scale))
+                           seed, hist_bins, int(hist_include_scale), int(tree_kind))
 
 
 class SearchIndex:
@@ -253,13 +257,16 @@ def make_pca_tree_index(exemplar: np.ndarray, window: int, variance_target: floa
                         branching: int = 4, seed: int = 0, *, mean=None, basis=None,
                         d_cap: int = 0, d_fixed: int = 0, max_depth: int = 0,
                         hist_bins: int = 0, hist_include_scale: bool = False,
+                        tree_kind: int = TREE_DEVICE,
                         ctx: Optional[Context] = None) -> SearchIndex:
-    """make_pca_tree_index(extract_all(exemplar, {w,1,..}), variance, b, seed)."""
+    """make_pca_tree_index(extract_all(exemplar, {w,1,..}), variance, b, seed).
+    tree_kind=TREE_REFERENCE builds the reference's own KmTree (same greedy /
+    backtrack answers as the reference); the default is the device tree."""
     ctx = ctx or default_context()
     ex = _c(exemplar, np.float64)
     C, eh, ew = ex.shape
     cfg = index_cfg(variance_target, d_cap, d_fixed, branching, max_depth, 0, seed, hist_bins,
-                    hist_include_scale)
+                    hist_include_scale, tree_kind)
     m = _c(mean, np.float64) if mean is not None else None
     b = _c(basis, np.float64) if basis is not None else None
     d = b.shape[0] if b is not None else 0
@@ -294,10 +301,12 @@ def make_brute_force_vector_index(X: np.ndarray, *, ctx: Optional[Context] = Non
 
 def make_vector_index(X: np.ndarray, variance_target: float = 0.95, branching: int = 8,
                       seed: int = 0, *, mean=None, basis=None, d_fixed: int = 0,
-                      max_depth: int = 0, ctx: Optional[Context] = None) -> SearchIndex:
+                      max_depth: int = 0, tree_kind: int = TREE_DEVICE,
+                      ctx: Optional[Context] = None) -> SearchIndex:
     ctx = ctx or default_context()
     X = _c(X, np.float32)
-    cfg = index_cfg(variance_target, 0, d_fixed, branching, max_depth, 0, seed)
+    cfg = index_cfg(variance_target, 0, d_fixed, branching, max_depth, 0, seed,
+                    tree_kind=tree_kind)
     m = _c(mean, np.float64) if mean is not None else None
     b = _c(basis, np.float64) if basis is not None else None
     d = b.shape[0] if b is not None else 0
@@ -355,13 +364,27 @@ def update_step(idx, irls, pen, index: SearchIndex, W: int, H: int, spacing: int
     return out
 
 
+def _check_level_inputs(x: np.ndarray, index: SearchIndex, cfg: OptimizerConfig,
+                        exemplar_hist: Optional[np.ndarray]):
+    """The C ABI reads C*H*W doubles of the image and bins*slots doubles of the
+    exemplar histogram (C = index.channels): validate before handing it raw
+    pointers (optimizer.cpp:278-286, :93 HistogramSet::compatible)."""
+    if x.ndim != 3 or x.shape[0] != index.channels:
+        raise ShapeError(N.PSG_E_SHAPE, "image channels do not match the index")
+    if cfg.nbhd_width != index.window:
+        raise ShapeError(N.PSG_E_SHAPE, "candidate dim does not match the grid window")
+    if exemplar_hist is not None:
+        slots = index.channels if cfg.histogram_include_scale else 3
+        if np.asarray(exemplar_hist).size != cfg.histogram_bins * slots:
+            raise ShapeError(N.PSG_E_SHAPE, "histogram sets are not compatible")
+
+
 def optimize_level(init: np.ndarray, index: SearchIndex, cfg: OptimizerConfig,
                    exemplar_hist: Optional[np.ndarray] = None):
     """(image, [IterationStats]) — optimizer.cpp:426-516."""
     x = _c(init, np.float64)
+    _check_level_inputs(x, index, cfg, exemplar_hist)
     C, H, W = x.shape
-    if cfg.nbhd_width != index.window:
-        raise ShapeError(N.PSG_E_SHAPE, "candidate dim does not match the grid window")
     c = cfg.c()
     out = np.zeros_like(x)
     stats = (N.psg_iter_stats * max(cfg.max_iterations, 1))()
@@ -378,6 +401,7 @@ class Level:
     def __init__(self, init: np.ndarray, index: SearchIndex, cfg: OptimizerConfig,
                  exemplar_hist: Optional[np.ndarray] = None):
         x = _c(init, np.float64)
+        _check_level_inputs(x, index, cfg, exemplar_hist)
         self.C, self.H, self.W = x.shape
         self.index = index
         self.cfg = cfg

@@ -415,7 +415,7 @@ static void launch_project(psg_ctx* ctx, const float* src, int img_w, int C, int
     const int blocks2 = (int)((n + TQ2 - 1) / TQ2);
     k<<<blocks2, 256, sm, ctx->stream>>>(src, img_w, C, w, xs, ys, nx, n, D, JC, mean, basisT, d,
                                           out);
-  } else if (d <= 48 && kWindows && (JC == 32 || JC == 40) && !std::getenv("PERSYN_PROJECT_KPT2")) {
+  } else if (d <= 48 && kWindows && (JC == 32 || JC == 40) && !ctx->knobs.project_kpt2) {
     constexpr int TQ2 = 8 * 2 * RQ;
     const size_t sm = sizeof(double) * ((size_t)TQ2 * (JC + 2) + (size_t)JC * 64);
     auto k = JC == 32 ? project48_kernel<RQ, 32> : project48_kernel<RQ, 40>;
@@ -1191,7 +1191,7 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
   constexpr int RS = DP + 4;  // padded staging row (floats): conflict-free 16 B accesses
   __shared__ int2 st_meta[kTileWarps][kTileStack];
   // per-lane node bounds of the stack as bf16 rounded DOWN: still valid lower
-  // bounds (pruning only loosens by < 0.4%), half the largest shared array
+  // bounds (pruning only loosens by < 2^-7 = 0.78%), half the largest shared array
   __shared__ __nv_bfloat16 st_lb[kTileWarps][kTileStack][32];
   __shared__ __align__(16) float stage_all[kTileWarps][32 * RS];
   __shared__ float aux_all[kTileWarps][2][32];
@@ -1559,14 +1559,9 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
   ProfScope _prof(ctx, K_SEARCH);
   if (a.nq <= 0) return;
   if (a.d > kMaxD) fail(PSG_E_DOMAIN, "retained PCA dimension > 64 is not supported");
-  if (a.mode == PSG_EXACT && a.proj32_q4 && a.tree.centroid32 && ctx->mma_search &&
-      !ctx->legacy_search) {
-    if (launch_search_mma(ctx, a)) return;
-  }
   const bool tile_ok = a.tree.max_children <= kTileMaxB &&
                        1 + a.tree.max_depth * (a.tree.max_children - 1) <= kTileStack;
-  if (a.mode == PSG_EXACT && a.proj32_q4 && a.tree.centroid32 && tile_ok && !ctx->legacy_search) {
-    if (ctx->hmma_tile && a.d <= 32 && launch_search_hmma(ctx, a)) return;
+  if (a.mode == PSG_EXACT && a.proj32_q4 && a.tree.centroid32 && tile_ok && !ctx->knobs.legacy_search) {
     if (!a.sched) fail(PSG_E_LOGIC, "tile search launched without its scheduler counters");
     const int64_t tiles = (a.nq + 31) / 32;
     const int wpb = a.d <= 32 ? 4 : 2;  // static smem <= 48 KB per CTA
@@ -1593,7 +1588,7 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
   }
   // thread-per-query kernel for greedy and short backtracks; longer frontiers
   // (m > 2) spill the per-thread heap and run faster warp-per-query
-  if (a.mode != PSG_EXACT && !ctx->legacy_search &&
+  if (a.mode != PSG_EXACT && !ctx->knobs.legacy_search &&
       (a.mode == PSG_GREEDY || a.max_leaves <= 2)) {
     int64_t blocks = (a.nq + 127) / 128;
     const int64_t cap = (int64_t)ctx->num_sms * 64;
@@ -1677,8 +1672,8 @@ __global__ void scatter_kernel(const T* __restrict__ src, const int32_t* __restr
 constexpr int kOrderBuckets = 64;
 
 __device__ __forceinline__ int tile_cost_bucket(int64_t c) {
-  const float l = log2f((float)c + 1.f) * 4.f;
-  return kOrderBuckets - 1 - min(kOrderBuckets - 1, (int)l);  // descending cost
+  const float l = log2f((float)max(c, (int64_t)0) + 1.f) * 4.f;
+  return kOrderBuckets - 1 - max(0, min(kOrderBuckets - 1, (int)l));  // descending cost
 }
 
 __global__ void __launch_bounds__(1024) tile_order_kernel(const int64_t* __restrict__ scanned,
@@ -1940,7 +1935,7 @@ void launch_rescore_windows(psg_ctx* ctx, const float* mirror, int img_w, int C,
                             double* dist, const int32_t* prev_idx, const double* prev_dist) {
   ProfScope _prof(ctx, K_RESCORE);
   if (anchors.count <= 0) return;
-  const float* ex8 = std::getenv("PERSYN_NO_EX8") ? nullptr : ix.ex_mirror8;
+  const float* ex8 = ctx->knobs.no_ex8 ? nullptr : ix.ex_mirror8;
   if (prev_idx && prev_dist) {
     const int64_t blocks = (anchors.count + kRescoreBlock - 1) / kRescoreBlock;
     rescore_changed_kernel<<<(unsigned)blocks, kRescoreBlock, 0, ctx->stream>>>(

@@ -235,7 +235,7 @@ void fit_pca_device(psg_ctx* ctx, Index& ix, const psg_index_cfg& cfg) {
   cublas_check(cublasSetStream(cb, ctx->stream), "cublasSetStream");
   cusolver_check(cusolverDnSetStream(cs, ctx->stream), "cusolverDnSetStream");
 
-  const bool verbose = std::getenv("PERSYN_VERBOSE") != nullptr;
+  const bool verbose = ctx->knobs.verbose;
   auto tick = [&](const char* what) {
     if (!verbose) return;
     static thread_local std::chrono::steady_clock::time_point t0;
@@ -292,7 +292,7 @@ void fit_pca_device(psg_ctx* ctx, Index& ix, const psg_index_cfg& cfg) {
   PSG_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int), ctx->stream));
   int lwork = 0, meig = D;
   bool iterative = false;
-  if (subset && std::getenv("PERSYN_EIG") == nullptr) {
+  if (subset && !ctx->knobs.eig_direct) {
     meig = subspace_top_eigen(ctx, cb, cs, cov.as<double>(), D, m_top, evals.as<double>(), verbose);
     iterative = meig > 0;
   }

@@ -161,9 +161,25 @@ struct psg_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_tile = nullptr;
   int* d_flags = nullptr;
   int64_t* d_sched = nullptr;  // [0..1] search tile scheduler, [2] stats fold ticket
-  bool legacy_search = false;  // PERSYN_SEARCH=warp: per-query warp kernel instead of tiles
-  bool mma_search = false;     // PERSYN_SEARCH=mma: tcgen05 tile kernel
-  bool hmma_tile = false;      // PERSYN_SEARCH=hmma: leaf filter on mma.sync (bf16 split)
+  // Scheduling / variant switches, read ONCE from the environment at
+  // psg_ctx_create (never inside per-iteration code).  Every variant computes
+  // bit-identical results (tests/test_variants.py); the defaults are the
+  // measured-fastest choices.
+  struct Knobs {
+    bool legacy_search = false;       // PERSYN_SEARCH=warp: per-query warp kernel, no tiles
+    bool verbose = false;             // PERSYN_VERBOSE: stage / phase timings on stderr
+    bool rescore_all = false;         // PERSYN_RESCORE_ALL: rescore every anchor after a search
+    bool no_greedy_seed = false;      // PERSYN_NO_GREEDY_SEED: unseeded priming search
+    bool no_tile_order = false;       // PERSYN_NO_TILE_ORDER: tiles in index order
+    bool no_ex8 = false;              // PERSYN_NO_EX8: unpadded exemplar mirror
+    bool penalty_per_anchor = false;  // PERSYN_PENALTY_PER_ANCHOR: no per-candidate table
+    bool no_fused_hist = false;       // PERSYN_NO_FUSED_HIST: separate histogram pass
+    bool serial = false;              // PERSYN_SERIAL: no side stream
+    bool graph = false;               // PERSYN_GRAPH: one CUDA graph per EM iteration
+    bool project_kpt2 = false;        // PERSYN_PROJECT_KPT2: 2-per-lane d<=48 projection
+    bool no_carry = false;            // PERSYN_NO_CARRY: stages do not seed from the previous
+    bool eig_direct = false;          // PERSYN_EIG: dense eigensolver instead of subspace iteration
+  } knobs;
 };
 
 struct psg_index {
@@ -243,9 +259,7 @@ void launch_brute_search(psg_ctx* ctx, const Index& ix, const RowSrc& qsrc, int6
                          int64_t* out_scanned, int64_t* out_exact);
 void launch_search(psg_ctx* ctx, const SearchArgs& a);
 // tcgen05 (UMMA) tile search; returns false when the tree shape is unsupported.
-bool launch_search_mma(psg_ctx* ctx, const SearchArgs& a);
 // Tile search with the leaf filter on mma.sync (bf16 split); false if unsupported.
-bool launch_search_hmma(psg_ctx* ctx, const SearchArgs& a);
 // Locality ordering of unstructured queries (search-only workloads).
 void launch_greedy_keys(psg_ctx* ctx, const double* q, int64_t nq, int d, const DevTree& tree,
                         uint32_t* keys, int32_t* order);
@@ -372,8 +386,10 @@ void launch_upsample_bilinear(psg_ctx* ctx, const double* in, int W, int H, int 
 void launch_fit_to(psg_ctx* ctx, const double* in, int W, int H, int ow, int oh, double* out);
 
 // ---- host pieces --------------------------------------------------------------
-HostTree build_tree_host(const double* proj, int64_t N, int d, int branching, int max_depth,
-                         int leaf_threshold, uint64_t seed);
+// KmTree::build replica (tree_kind = PSG_TREE_REFERENCE): the reference's own
+// tree, bit for bit (host, the shared sequential engine; tree_host.cpp).
+HostTree build_reference_tree_host(const double* proj, int64_t N, int d, int branching,
+                                   int leaf_threshold, uint64_t seed);
 // Same construction on the device (level-synchronous, deterministic); P is
 // the device [N][d] projected database.
 HostTree build_tree_device(psg_ctx* ctx, const double* P, int64_t N, int d, int branching,

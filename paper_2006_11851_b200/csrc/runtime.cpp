@@ -68,6 +68,10 @@ struct DBuf {
     release();
     n = count;
     s = t_stream;
+    // every C-ABI entry point that allocates sets its context stream
+    // (StreamScope): a block freed on the legacy stream could be reused
+    // under a kernel still running on the context's non-blocking stream
+    if (count && !s) throw Error(PSG_E_LOGIC, "device allocation outside a context stream scope");
     if (count) PSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, s));
   }
   void release() {
@@ -343,7 +347,7 @@ void upload_tree(psg_ctx* ctx, Index& ix) {
 void finish_index(psg_ctx* ctx, Index& ix, const double* mean, const double* basis, int d,
                   const psg_index_cfg& cfg) {
   const int D = ix.D;
-  const bool verbose = std::getenv("PERSYN_VERBOSE") != nullptr;
+  const bool verbose = ctx->knobs.verbose;
   double t_phase = now_ms();
   auto phase = [&](const char* what) {
     if (!verbose) return;
@@ -393,18 +397,20 @@ void finish_index(psg_ctx* ctx, Index& ix, const double* mean, const double* bas
     }
   }
   phase("db projection");
-  // k-means tree over the device-projected points: built on the device
-  // (PERSYN_TREE=host selects the native host builder, same rules)
+  // k-means tree over the device-projected points: the device tree, or the
+  // reference's own KmTree::build replica (tree_kind, persyn_b200.h)
   const int lt = cfg.leaf_threshold > 0 ? cfg.leaf_threshold : cfg.branching;
-  const char* tb = std::getenv("PERSYN_TREE");
-  if (tb && std::string(tb) == "host") {
+  if (cfg.tree_kind == PSG_TREE_REFERENCE) {
+    if (cfg.max_depth != 0) fail(PSG_E_DOMAIN, "the reference tree has no depth cap (max_depth 0)");
     std::vector<double> hp((size_t)ix.N * d);
     if (d > 0)
       PSG_CUDA(cudaMemcpyAsync(hp.data(), ix.proj, sizeof(double) * hp.size(),
                                cudaMemcpyDeviceToHost, ctx->stream));
     PSG_CUDA(cudaStreamSynchronize(ctx->stream));
-    ix.htree = build_tree_host(hp.data(), ix.N, d, cfg.branching, cfg.max_depth, lt, cfg.seed);
-    phase("tree build (host)");
+    ix.htree = build_reference_tree_host(hp.data(), ix.N, d, cfg.branching, lt, cfg.seed);
+    phase("tree build (reference replica)");
+  } else if (cfg.tree_kind != PSG_TREE_DEVICE) {
+    fail(PSG_E_DOMAIN, "unknown tree_kind");
   } else {
     ix.htree = build_tree_device(ctx, ix.proj, ix.N, d, cfg.branching, cfg.max_depth, lt, cfg.seed);
     phase("tree build (device)");
@@ -494,6 +500,7 @@ struct psg_level {
   bool counts_fresh = false;  // L.counts = histogram of the current owned rows (fused M-step)
   int slots = 3;
   bool primed = false;
+  bool scanned_valid = false;  // L.scanned holds a search of these anchors (tile order)
   int iter = 0;
   int64_t pending_calls = 0, pending_scanned = 0;
   double pending_ms = 0.0;
@@ -671,7 +678,7 @@ AnchorSet owned_anchors(psg_level& L) { return AnchorSet{L.xs.p, L.ys.p + L.nh, 
 // diagnostic) — anchors that keep their assignment reuse them.
 void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* out_dist,
                   const double* seed_dist = nullptr, cudaEvent_t seed_dist_ready = nullptr) {
-  if (!seed || std::getenv("PERSYN_RESCORE_ALL")) seed_dist = nullptr;
+  if (!seed || L.ctx->knobs.rescore_all) seed_dist = nullptr;
   psg_ctx* ctx = L.ctx;
   const Index& ix = *L.ix;
   const AnchorSet as = owned_anchors(L);
@@ -728,7 +735,7 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
   // distances start every query's bound (~4% faster priming search on the
   // bench stage); the result does not depend on the seeds
   DBuf<int32_t> greedy_seed;
-  if (!a.seed_idx && a.mode == PSG_EXACT && !std::getenv("PERSYN_NO_GREEDY_SEED")) {
+  if (!a.seed_idx && a.mode == PSG_EXACT && !ctx->knobs.no_greedy_seed) {
     greedy_seed.alloc((size_t)L.Ao);
     SearchArgs g = a;
     g.mode = PSG_GREEDY;
@@ -742,7 +749,8 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
   // seeded exact search: the previous search of these anchors left its
   // per-query scan counts in L.scanned -> schedule the costliest tiles first
   DBuf<int32_t>& order = L.tile_order;  // kept: no allocation inside a captured iteration
-  if (a.seed_idx && !greedy_seed.p && a.mode == PSG_EXACT && !std::getenv("PERSYN_NO_TILE_ORDER")) {
+  if (a.seed_idx && !greedy_seed.p && a.mode == PSG_EXACT && L.scanned_valid &&
+      !ctx->knobs.no_tile_order) {
     const size_t nt = (size_t)image_tile_count(a.nq, a.qnx);
     if (order.n < nt) order.alloc(nt);
     if (seed_dist_ready) {  // concurrent mode: the one-CTA sort overlaps the projection
@@ -758,6 +766,7 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
     a.tile_order = order.p;
   }
   launch_search(ctx, a);
+  L.scanned_valid = true;
   if (seed_dist_ready) PSG_CUDA(cudaStreamWaitEvent(ctx->stream, seed_dist_ready, 0));
   launch_rescore_windows(ctx, L.mirror.p, L.W, L.C, L.w, as, ix, out_idx + L.off,
                          out_dist + L.off, seed_dist ? seed : nullptr, seed_dist);
@@ -813,7 +822,7 @@ MstepArgs mstep_args(psg_level& L) {
   m.C = L.C;
   m.w = L.w;
   m.ex_mirror = ix.ex_mirror;
-  m.ex8 = std::getenv("PERSYN_NO_EX8") ? nullptr : ix.ex_mirror8;
+  m.ex8 = L.ctx->knobs.no_ex8 ? nullptr : ix.ex_mirror8;
   m.ew = ix.ew;
   m.nxe = ix.nxe;
   m.planes = L.planes.p;
@@ -874,7 +883,7 @@ void phase_penalty(psg_level& L, const unsigned long long* global_counts,
   const int bins = L.cfg.histogram_bins;
   launch_hist_fold(ctx, global_counts, bins, L.slots, (int64_t)L.W * L.H, L.ex_hist.p,
                    L.out_mass.p, L.excess.p);
-  if (L.pen_table.p && !std::getenv("PERSYN_PENALTY_PER_ANCHOR")) {
+  if (L.pen_table.p && !ctx->knobs.penalty_per_anchor) {
     launch_penalty_table(ctx, *L.ix, L.excess.p, bins, L.slots, L.pen_table.p);
     if (weights_ready) PSG_CUDA(cudaStreamWaitEvent(ctx->stream, weights_ready, 0));
     launch_eff_gather(ctx, L.irls.p + L.off, L.pen_table.p, L.cur_idx.p + L.off, L.Ao,
@@ -890,7 +899,7 @@ void phase_penalty(psg_level& L, const unsigned long long* global_counts,
 // Phase 3: M-step of the owned pixel rows (halo anchor rows must be filled).
 void phase_update(psg_level& L) {
   MstepArgs m = mstep_args(L);
-  if (L.hist_on && !std::getenv("PERSYN_NO_FUSED_HIST")) {
+  if (L.hist_on && !L.ctx->knobs.no_fused_hist) {
     // the next phase 1 histograms exactly the rows this M-step writes
     m.counts = L.counts.p;
     m.bins = L.cfg.histogram_bins;
@@ -906,7 +915,7 @@ void phase_search_enqueue(psg_level& L) {
   // the lsq diagnostic (L1-bound) runs on the side stream, overlapping the
   // projection (fp64-bound); the post-search rescoring waits for it.  Serial
   // when profiling (per-launch events live on the main stream).
-  const bool conc = ctx->side && !ctx->profile && !std::getenv("PERSYN_SERIAL");
+  const bool conc = ctx->side && !ctx->profile && !ctx->knobs.serial;
   cudaEvent_t ready = nullptr;
   if (conc) {
     PSG_CUDA(cudaEventRecord(ctx->ev_fork, ctx->stream));
@@ -1001,12 +1010,12 @@ void step_body(psg_level& L, bool conc, bool mark) {
 bool level_step(psg_level& L, psg_iter_stats* st, bool honor) {
   psg_ctx* ctx = L.ctx;
   // IRLS weights (side stream) overlap the histogram fold + penalty table
-  const bool conc = ctx->side && !ctx->profile && !std::getenv("PERSYN_SERIAL");
+  const bool conc = ctx->side && !ctx->profile && !ctx->knobs.serial;
   // opt-in (PERSYN_GRAPH=1): one graph launch per iteration in the steady
   // state (same topology once the fused M-step keeps the counts fresh).
   // Measured on the bench stage: +0.3% iterations/s, but -2% e2e (two graph
   // instantiations per level), so launches stay eager by default.
-  const bool graph = conc && std::getenv("PERSYN_GRAPH") && (!L.hist_on || L.counts_fresh);
+  const bool graph = conc && ctx->knobs.graph && (!L.hist_on || L.counts_fresh);
   if (graph) {
     cudaGraphExec_t& ge = L.graph[L.iter & 1];
     if (!ge) {
@@ -1108,10 +1117,23 @@ psg_status psg_ctx_create(int device, void* stream, psg_ctx** out) {
     auto c = std::make_unique<psg_ctx>();
     c->device = device;
     c->num_sms = prop.multiProcessorCount;
-    if (const char* e = std::getenv("PERSYN_SEARCH")) {
-      c->legacy_search = std::string(e) == "warp";
-      c->mma_search = std::string(e) == "mma";
-      c->hmma_tile = std::string(e) == "hmma";
+    {
+      auto on = [](const char* k) { return std::getenv(k) != nullptr; };
+      auto& kn = c->knobs;
+      const char* e = std::getenv("PERSYN_SEARCH");
+      kn.legacy_search = e && std::string(e) == "warp";
+      kn.verbose = on("PERSYN_VERBOSE");
+      kn.rescore_all = on("PERSYN_RESCORE_ALL");
+      kn.no_greedy_seed = on("PERSYN_NO_GREEDY_SEED");
+      kn.no_tile_order = on("PERSYN_NO_TILE_ORDER");
+      kn.no_ex8 = on("PERSYN_NO_EX8");
+      kn.penalty_per_anchor = on("PERSYN_PENALTY_PER_ANCHOR");
+      kn.no_fused_hist = on("PERSYN_NO_FUSED_HIST");
+      kn.serial = on("PERSYN_SERIAL");
+      kn.graph = on("PERSYN_GRAPH");
+      kn.project_kpt2 = on("PERSYN_PROJECT_KPT2");
+      kn.no_carry = on("PERSYN_NO_CARRY");
+      kn.eig_direct = on("PERSYN_EIG");
     }
     if (stream) {
       c->stream = static_cast<cudaStream_t>(stream);
@@ -1407,7 +1429,7 @@ psg_status psg_index_query(psg_ctx* ctx, const psg_index* index, const float* Q,
     a.out_scanned = sc.p;
     a.flags = ctx->d_flags;
     a.sched = ctx->d_sched;
-    const bool reorder = budget.mode == PSG_EXACT && nq >= 64 && ix.d > 0 && !ctx->legacy_search;
+    const bool reorder = budget.mode == PSG_EXACT && nq >= 64 && ix.d > 0 && !ctx->knobs.legacy_search;
     if (ix.brute) {
       // searched above (the budget does not apply, optimizer.cpp:172-173)
     } else if (reorder) {
@@ -1648,7 +1670,10 @@ psg_status psg_band_commit(psg_level* level, const double* global_partials, psg_
 }
 
 psg_status psg_level_prime(psg_level* level) {
-  return guarded([&] { psg::level_prime(*level); });
+  return guarded([&] {
+    psg::StreamScope _ss(level->ctx->stream);
+    psg::level_prime(*level);
+  });
 }
 
 psg_status psg_level_iterate(psg_level* level, int n, int honor_convergence,
@@ -1895,7 +1920,7 @@ extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, doubl
                                  cudaMemcpyDeviceToDevice, ctx->stream));
         launch_make_mirror(ctx, lv.planes.p, C, W, H, lv.mirror.p);
         DBuf<int32_t> seeds;
-        if (carry.level >= 0 && !std::getenv("PERSYN_NO_CARRY")) {
+        if (carry.level >= 0 && !ctx->knobs.no_carry) {
           const AnchorSet as = owned_anchors(lv);
           seeds.alloc((size_t)as.count);
           CarryArgs ca{};
@@ -1918,13 +1943,13 @@ extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, doubl
           launch_carry_seed(ctx, ca);
         }
         level_prime(lv, seeds.p);
-        if (std::getenv("PERSYN_VERBOSE"))
+        if (ctx->knobs.verbose)
           fprintf(stderr, "[persyn] stage l=%d w=%d: first search %.2f ms (%s)\n", l, w,
                   lv.pending_ms, seeds.p ? "carried seed" : "unseeded");
         psg_iter_stats last{};
         int iters = 0;
         int64_t calls = 0;
-        const bool verbose = std::getenv("PERSYN_VERBOSE") != nullptr;
+        const bool verbose = ctx->knobs.verbose;
         std::string its;
         for (int it = 0; it < cfg.max_iterations; ++it) {
           const bool conv = level_step(lv, &last, true);
@@ -1964,11 +1989,11 @@ extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, doubl
         }
         rep.total_nn_calls += calls;
         rep.final_energy = last.energy;
-        if (std::getenv("PERSYN_VERBOSE"))
+        if (ctx->knobs.verbose)
           fprintf(stderr, "[persyn] stage l=%d w=%d: index %.2f ms, optimize %.2f ms\n", l, w,
                   index_ms, now_ms() - to);
         }
-        if (std::getenv("PERSYN_VERBOSE")) {
+        if (ctx->knobs.verbose) {
           cudaMemPool_t pool;
           uint64_t cur = 0, high = 0;
           PSG_CUDA(cudaDeviceGetDefaultMemPool(&pool, ctx->device));
@@ -1980,7 +2005,7 @@ extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, doubl
       }
     }
     rep.part2_millis = now_ms() - t1;
-    if (std::getenv("PERSYN_VERBOSE"))
+    if (ctx->knobs.verbose)
       fprintf(stderr, "[persyn] synthesize: part1 %.2f ms, part2 %.2f ms\n", rep.part1_millis,
               rep.part2_millis);
     state.download(ctx, out_planes, (size_t)C * req->out_w * req->out_h);

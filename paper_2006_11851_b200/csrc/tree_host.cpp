@@ -1,127 +1,30 @@
-// k-means tree build (native host runtime, per stage).
+// Host side of the k-means tree: import / replay of the reference's own
+// tree, and the opt-in replica of KmTree::build that produces it.
 //
-// Same construction as KmTree::build (km_tree.cpp:141-195): node centroid =
-// mean of its points in ascending id order, radius = max distance; a node is
-// split with k = min(b, n) k-means++/Lloyd clusters (km_tree.cpp:34-119:
-// <= 20 sweeps, stop when the largest centroid move < 1e-6, strict-< reassign,
-// empty clusters dropped) when it holds >= leaf_threshold points, is above
-// the depth cap (the BASELINE configs' "depth"), and the split yields >= 2
-// clusters.  Differences from the reference, none of which changes an exact
-// query result (exact search is tree-independent, km_tree.cpp:251-278):
-//   * breadth-first node ids with contiguous children (GPU-friendly);
-//   * one splitmix64 stream per node instead of one shared mt19937_64 in DFS
-//     order, so nodes build in parallel and deterministically;
-//   * optional depth cap;
-//   * Lloyd sums are accumulated per fixed 4096-point chunk and combined in
-//     chunk order, so a large node is clustered by all host threads with a
-//     result independent of the thread count.
+// The default tree is built on the device (kernels_tree.cu: level-synchronous
+// k-means++/Lloyd, one splitmix64 stream per node, optional depth cap).  Exact
+// queries do not depend on the tree (km_tree.cpp:251-278), but greedy and
+// backtrack(m) answers do; the reference's default budget is backtrack(4)
+// (optimizer.hpp:48, persyn_main.cpp:79).  psg_index_cfg.tree_kind =
+// PSG_TREE_REFERENCE therefore rebuilds the reference's tree itself:
+// KmTree::build (km_tree.cpp:141-195) draws its k-means++ seeds from ONE
+// std::mt19937_64 shared by all nodes in the recursion's (pre-)order, with
+// libstdc++'s uniform_int / uniform_real distributions.  Every draw depends on
+// all draws before it, so the replica is a sequential walk by construction; it
+// uses the same engine and distribution types from the same C++ library, the
+// same fp64 loops (sequential j, no FMA: -ffp-contract=off) and the same
+// tie rules, and emits the tree in the public structure_json() + leaves()
+// form that import_tree_host replays (post-order tie ids included).
 #include <algorithm>
-#include <atomic>
 #include <cmath>
-#include <condition_variable>
 #include <cstring>
-#include <functional>
-#include <mutex>
-#include <thread>
+#include <random>
 #include <vector>
 
 #include "psg_internal.h"
 
 namespace psg {
 namespace {
-
-// Minimal persistent pool: run(n, fn) calls fn(i) for i in [0, n) on all
-// workers (the caller participates) and returns when every index is done.
-class Pool {
- public:
-  static Pool& get() {
-    static Pool p;
-    return p;
-  }
-  int size() const { return (int)workers_.size() + 1; }
-  void run(int64_t n, const std::function<void(int64_t)>& fn) {
-    if (n <= 0) return;
-    if (workers_.empty() || n == 1) {
-      for (int64_t i = 0; i < n; ++i) fn(i);
-      return;
-    }
-    {
-      std::lock_guard<std::mutex> g(m_);
-      fn_ = &fn;
-      n_ = n;
-      next_.store(0);
-      done_ = 0;
-      ++gen_;
-    }
-    cv_.notify_all();
-    work();
-    std::unique_lock<std::mutex> lk(m_);
-    cv_done_.wait(lk, [&] { return done_ == (int)workers_.size(); });
-    fn_ = nullptr;
-  }
-
- private:
-  Pool() {
-    unsigned hw = std::thread::hardware_concurrency();
-    if (hw == 0) hw = 1;
-    for (unsigned i = 1; i < hw && i < 64; ++i) workers_.emplace_back([this] { loop(); });
-  }
-  ~Pool() {
-    {
-      std::lock_guard<std::mutex> g(m_);
-      stop_ = true;
-      ++gen_;
-    }
-    cv_.notify_all();
-    for (auto& t : workers_) t.join();
-  }
-  void work() {
-    for (;;) {
-      const int64_t i = next_.fetch_add(1);
-      if (i >= n_) break;
-      (*fn_)(i);
-    }
-  }
-  void loop() {
-    uint64_t seen = 0;
-    for (;;) {
-      {
-        std::unique_lock<std::mutex> lk(m_);
-        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
-        if (stop_) return;
-        seen = gen_;
-      }
-      work();
-      {
-        std::lock_guard<std::mutex> g(m_);
-        ++done_;
-      }
-      cv_done_.notify_one();
-    }
-  }
-  std::vector<std::thread> workers_;
-  std::mutex m_;
-  std::condition_variable cv_, cv_done_;
-  const std::function<void(int64_t)>* fn_ = nullptr;
-  std::atomic<int64_t> next_{0};
-  int64_t n_ = 0;
-  int done_ = 0;
-  uint64_t gen_ = 0;
-  bool stop_ = false;
-};
-
-constexpr int64_t kChunk = 4096;
-
-struct SplitMix {
-  uint64_t s;
-  uint64_t next() {
-    uint64_t z = (s += 0x9E3779B97F4A7C15ull);
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    return z ^ (z >> 31);
-  }
-  double uniform01() { return (next() >> 11) * (1.0 / 9007199254740992.0); }
-};
 
 inline double dist2(const double* a, const double* b, int d) {
   double acc = 0.0;
@@ -132,279 +35,134 @@ inline double dist2(const double* a, const double* b, int d) {
   return acc;
 }
 
-// dist2(p, centers[c0 + i]) for i < m <= 8, each accumulated in j order
-// exactly like dist2(); the m independent chains hide the add latency.
-inline void dist2_block(const double* p, const double* centers, int c0, int m, int d,
-                        double* out) {
-  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  const double* c = centers + (size_t)c0 * d;
-  if (m == 8) {
-    for (int j = 0; j < d; ++j) {
-      const double pj = p[j];
-#pragma GCC unroll 8
-      for (int i = 0; i < 8; ++i) {
-        const double t = pj - c[(size_t)i * d + j];
-        acc[i] += t * t;
-      }
-    }
-  } else {
-    for (int j = 0; j < d; ++j) {
-      const double pj = p[j];
-      for (int i = 0; i < m; ++i) {
-        const double t = pj - c[(size_t)i * d + j];
-        acc[i] += t * t;
-      }
-    }
+// Clusterer::run (km_tree.cpp:34-119) over ascending ids: k-means++ seeding
+// (first centre uniform_int(0, n-1); then D^2 sampling with
+// uniform_real(0, total) and the subtract-until-<=0 scan), a strict-<
+// reassign (lowest centre wins ties), <= 20 Lloyd sweeps with ordered sums
+// (empty clusters keep their centre) stopping when the largest move < 1e-6,
+// then the non-empty clusters, each in ascending id order.
+std::vector<std::vector<int32_t>> kmeans_reference(const double* P, int d,
+                                                   const std::vector<int32_t>& ids, int k,
+                                                   std::mt19937_64& rng) {
+  const size_t n = ids.size();
+  auto pt = [&](size_t i) { return P + (size_t)ids[i] * d; };
+  std::vector<double> ctr;
+  ctr.reserve((size_t)k * d);
+  std::uniform_int_distribution<std::size_t> first(0, n - 1);
+  {
+    const double* c0 = pt(first(rng));
+    ctr.insert(ctr.end(), c0, c0 + d);
   }
-  for (int i = 0; i < m; ++i) out[i] = acc[i];
-}
-
-// dist2(P[ids[i]], c) for 4 consecutive ids at once (independent chains).
-inline void dist2_points4(const double* P, const int32_t* ids, const double* c, int d,
-                          double* out) {
-  const double* a0 = P + (size_t)ids[0] * d;
-  const double* a1 = P + (size_t)ids[1] * d;
-  const double* a2 = P + (size_t)ids[2] * d;
-  const double* a3 = P + (size_t)ids[3] * d;
-  double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-  for (int j = 0; j < d; ++j) {
-    const double cj = c[j];
-    const double t0 = a0[j] - cj, t1 = a1[j] - cj, t2 = a2[j] - cj, t3 = a3[j] - cj;
-    s0 += t0 * t0;
-    s1 += t1 * t1;
-    s2 += t2 * t2;
-    s3 += t3 * t3;
-  }
-  out[0] = s0;
-  out[1] = s1;
-  out[2] = s2;
-  out[3] = s3;
-}
-
-struct Job {
-  std::vector<int32_t> ids;
-  int depth;
-};
-
-// fn(chunk, lo, hi) over [0, n) in fixed kChunk pieces, in parallel when
-// `parallel` (chunk boundaries do not depend on the thread count).
-void for_chunks(int64_t n, bool parallel,
-                const std::function<void(int64_t, int64_t, int64_t)>& fn) {
-  const int64_t nch = (n + kChunk - 1) / kChunk;
-  auto body = [&](int64_t c) { fn(c, c * kChunk, std::min(n, (c + 1) * kChunk)); };
-  if (parallel && nch > 1) {
-    Pool::get().run(nch, body);
-  } else {
-    for (int64_t c = 0; c < nch; ++c) body(c);
-  }
-}
-
-// k-means++ + Lloyd over ids (ascending); returns non-empty clusters with
-// ascending ids.
-std::vector<std::vector<int32_t>> cluster(const double* P, int d, const std::vector<int32_t>& ids,
-                                          int k, uint64_t seed, bool parallel) {
-  const int64_t n = (int64_t)ids.size();
-  const int64_t nch = (n + kChunk - 1) / kChunk;
-  SplitMix rng{seed};
-  std::vector<double> centers;
-  centers.reserve((size_t)k * d);
-  const size_t first = rng.next() % n;
-  centers.insert(centers.end(), P + (size_t)ids[first] * d, P + (size_t)ids[first] * d + d);
   std::vector<double> d2(n);
-  for_chunks(n, parallel, [&](int64_t, int64_t lo, int64_t hi) {
-    int64_t i = lo;
-    for (; i + 4 <= hi; i += 4) dist2_points4(P, ids.data() + i, centers.data(), d, &d2[i]);
-    for (; i < hi; ++i) d2[i] = dist2(P + (size_t)ids[i] * d, centers.data(), d);
-  });
+  for (size_t i = 0; i < n; ++i) d2[i] = dist2(pt(i), ctr.data(), d);
   int nc = 1;
   while (nc < k) {
     double total = 0.0;
     for (double v : d2) total += v;
     if (total <= 0.0) break;
-    double r = rng.uniform01() * total;
-    int64_t chosen = n - 1;
-    for (int64_t i = 0; i < n; ++i) {
+    std::uniform_real_distribution<double> pick(0.0, total);
+    double r = pick(rng);
+    size_t chosen = n - 1;
+    for (size_t i = 0; i < n; ++i) {
       r -= d2[i];
       if (r <= 0.0) {
         chosen = i;
         break;
       }
     }
-    const double* c = P + (size_t)ids[chosen] * d;
-    centers.insert(centers.end(), c, c + d);
+    const double* c = pt(chosen);
+    ctr.insert(ctr.end(), c, c + d);
+    const double* cn = ctr.data() + (size_t)nc * d;
     ++nc;
-    for_chunks(n, parallel, [&](int64_t, int64_t lo, int64_t hi) {
-      int64_t i = lo;
-      double t[4];
-      for (; i + 4 <= hi; i += 4) {
-        dist2_points4(P, ids.data() + i, c, d, t);
-        for (int q = 0; q < 4; ++q) d2[i + q] = std::min(d2[i + q], t[q]);
-      }
-      for (; i < hi; ++i) d2[i] = std::min(d2[i], dist2(P + (size_t)ids[i] * d, c, d));
-    });
+    for (size_t i = 0; i < n; ++i) d2[i] = std::min(d2[i], dist2(pt(i), cn, d));
   }
   std::vector<int> assign(n);
   auto reassign = [&] {
-    for_chunks(n, parallel, [&](int64_t, int64_t lo, int64_t hi) {
-      for (int64_t i = lo; i < hi; ++i) {
-        const double* p = P + (size_t)ids[i] * d;
-        int best = 0;
-        double bd = 0.0;
-        double dd[8];
-        for (int c0 = 0; c0 < nc; c0 += 8) {
-          const int m = std::min(8, nc - c0);
-          dist2_block(p, centers.data(), c0, m, d, dd);
-          for (int q = 0; q < m; ++q) {
-            if (c0 + q == 0) {
-              bd = dd[0];
-            } else if (dd[q] < bd) {  // strict <: lowest cluster on ties
-              bd = dd[q];
-              best = c0 + q;
-            }
-          }
+    for (size_t i = 0; i < n; ++i) {
+      int best = 0;
+      double bd = dist2(pt(i), ctr.data(), d);
+      for (int c = 1; c < nc; ++c) {
+        const double v = dist2(pt(i), ctr.data() + (size_t)c * d, d);
+        if (v < bd) {
+          bd = v;
+          best = c;
         }
-        assign[i] = best;
       }
-    });
+      assign[i] = best;
+    }
   };
   reassign();
-  std::vector<double> sums((size_t)nc * d), csum((size_t)nch * nc * d);
-  std::vector<int64_t> sizes(nc), csz((size_t)nch * nc);
+  std::vector<double> sums((size_t)nc * d);
+  std::vector<size_t> sizes((size_t)nc);
   for (int sweep = 0; sweep < 20; ++sweep) {
-    for_chunks(n, parallel, [&](int64_t ch, int64_t lo, int64_t hi) {
-      double* s = csum.data() + (size_t)ch * nc * d;
-      int64_t* z = csz.data() + (size_t)ch * nc;
-      std::fill(s, s + (size_t)nc * d, 0.0);
-      std::fill(z, z + nc, 0);
-      for (int64_t i = lo; i < hi; ++i) {
-        const double* p = P + (size_t)ids[i] * d;
-        double* sc = s + (size_t)assign[i] * d;
-        for (int j = 0; j < d; ++j) sc[j] += p[j];
-        ++z[assign[i]];
-      }
-    });
     std::fill(sums.begin(), sums.end(), 0.0);
     std::fill(sizes.begin(), sizes.end(), 0);
-    for (int64_t ch = 0; ch < nch; ++ch)  // fixed chunk order: deterministic
-      for (int c = 0; c < nc; ++c) {
-        sizes[c] += csz[(size_t)ch * nc + c];
-        for (int j = 0; j < d; ++j)
-          sums[(size_t)c * d + j] += csum[((size_t)ch * nc + c) * d + j];
-      }
+    for (size_t i = 0; i < n; ++i) {
+      const double* p = pt(i);
+      double* s = sums.data() + (size_t)assign[i] * d;
+      for (int j = 0; j < d; ++j) s[j] += p[j];
+      ++sizes[(size_t)assign[i]];
+    }
     double movement = 0.0;
     for (int c = 0; c < nc; ++c) {
-      if (sizes[c] == 0) continue;
+      if (sizes[(size_t)c] == 0) continue;
       double move = 0.0;
       for (int j = 0; j < d; ++j) {
-        const double v = sums[(size_t)c * d + j] / (double)sizes[c];
-        const double t = v - centers[(size_t)c * d + j];
+        const double v = sums[(size_t)c * d + j] / sizes[(size_t)c];
+        const double t = v - ctr[(size_t)c * d + j];
         move += t * t;
-        centers[(size_t)c * d + j] = v;
+        ctr[(size_t)c * d + j] = v;
       }
       movement = std::max(movement, std::sqrt(move));
     }
     if (movement < 1e-6) break;
     reassign();
   }
-  std::vector<std::vector<int32_t>> clusters(nc);
-  for (int64_t i = 0; i < n; ++i) clusters[assign[i]].push_back(ids[i]);
-  clusters.erase(std::remove_if(clusters.begin(), clusters.end(),
-                                [](const std::vector<int32_t>& c) { return c.empty(); }),
-                 clusters.end());
-  return clusters;
-}
-
-uint64_t node_seed(uint64_t seed, int64_t node) {
-  SplitMix s{seed ^ (0xD1B54A32D192ED03ull * (uint64_t)(node + 1))};
-  return s.next();
+  std::vector<std::vector<int32_t>> out((size_t)nc);
+  for (size_t i = 0; i < n; ++i) out[(size_t)assign[i]].push_back(ids[i]);
+  out.erase(std::remove_if(out.begin(), out.end(),
+                           [](const std::vector<int32_t>& v) { return v.empty(); }),
+            out.end());
+  return out;
 }
 
 }  // namespace
 
-HostTree build_tree_host(const double* P, int64_t N, int d, int branching, int max_depth,
-                         int leaf_threshold, uint64_t seed) {
+// KmTree::build(points, d, N, branching, leaf_threshold, seed)
+// (km_tree.cpp:141-195) as a pre-order walk: a node holding
+// >= leaf_threshold points (and d > 0) is clustered with k = min(b, n), and
+// split when >= 2 clusters are non-empty; its children are then built one
+// subtree at a time in cluster order -- the recursion's order, hence the
+// order in which the shared engine is consumed.
+HostTree build_reference_tree_host(const double* P, int64_t N, int d, int branching,
+                                   int leaf_threshold, uint64_t seed) {
   if (N < 1) fail(PSG_E_DOMAIN, "cannot build a tree over zero points");
   if (branching < 2) fail(PSG_E_DOMAIN, "tree branching must be >= 2");
   if (leaf_threshold <= 0) leaf_threshold = branching;
-  HostTree t;
-  std::vector<Job> level(1);
-  level[0].ids.resize(N);
-  for (int64_t i = 0; i < N; ++i) level[0].ids[i] = (int32_t)i;
-  level[0].depth = 0;
-  int32_t leaf_cursor = 0;
-  t.perm.reserve(N);
-  const int threads = Pool::get().size();
-
-  while (!level.empty()) {
-    const size_t base = t.radius.size();
-    const size_t L = level.size();
-    std::vector<std::vector<std::vector<int32_t>>> splits(L);
-    std::vector<double> cent(L * (size_t)d), rad(L);
-    const int KB = std::min(d, kBoxDims);
-    std::vector<double> blo(L * kBoxDims, 0.0), bhi(L * kBoxDims, 0.0);
-    // few big nodes: parallel inside each node; many nodes: one node per task
-    const bool inner = (int64_t)L < threads;
-    auto work = [&](size_t i) {
-      const auto& ids = level[i].ids;
-      double* c = cent.data() + i * d;
-      for (int j = 0; j < d; ++j) c[j] = 0.0;
-      for (int32_t id : ids)
-        for (int j = 0; j < d; ++j) c[j] += P[(size_t)id * d + j];
-      for (int j = 0; j < d; ++j) c[j] /= (double)ids.size();
-      double r = 0.0;
-      for (int32_t id : ids) r = std::max(r, std::sqrt(dist2(P + (size_t)id * d, c, d)));
-      rad[i] = r;
-      for (int j = 0; j < KB; ++j) {
-        double mn = P[(size_t)ids[0] * d + j], mx = mn;
-        for (int32_t id : ids) {
-          mn = std::min(mn, P[(size_t)id * d + j]);
-          mx = std::max(mx, P[(size_t)id * d + j]);
-        }
-        blo[i * kBoxDims + j] = mn;
-        bhi[i * kBoxDims + j] = mx;
-      }
-      const bool can = (int64_t)ids.size() >= leaf_threshold && d > 0 &&
-                       (max_depth <= 0 || level[i].depth < max_depth);
-      if (can) {
-        const int k = (int)std::min<size_t>((size_t)branching, ids.size());
-        auto cl = cluster(P, d, ids, k, node_seed(seed, (int64_t)(base + i)), inner);
-        if (cl.size() >= 2) splits[i] = std::move(cl);
-      }
-    };
-    if (inner) {
-      for (size_t i = 0; i < L; ++i) work(i);
-    } else {
-      Pool::get().run((int64_t)L, [&](int64_t i) { work((size_t)i); });
-    }
-    // Emit this level's nodes; children go to the next level, contiguous.
-    std::vector<Job> next_level;
-    const size_t first_next = base + L;
-    for (size_t i = 0; i < L; ++i) {
-      t.centroid.insert(t.centroid.end(), cent.begin() + i * d, cent.begin() + (i + 1) * d);
-      t.radius.push_back(rad[i]);
-      t.boxlo.insert(t.boxlo.end(), blo.begin() + i * kBoxDims, blo.begin() + (i + 1) * kBoxDims);
-      t.boxhi.insert(t.boxhi.end(), bhi.begin() + i * kBoxDims, bhi.begin() + (i + 1) * kBoxDims);
-      t.depth.push_back(level[i].depth);
-      t.max_depth = std::max(t.max_depth, level[i].depth);
-      if (!splits[i].empty()) {
-        t.first_child.push_back((int32_t)(first_next + next_level.size()));
-        t.n_children.push_back((int32_t)splits[i].size());
-        t.leaf_start.push_back(0);
-        t.leaf_count.push_back(0);
-        for (auto& c : splits[i]) next_level.push_back(Job{std::move(c), level[i].depth + 1});
-      } else {
-        t.first_child.push_back(-1);
-        t.n_children.push_back(0);
-        t.leaf_start.push_back(leaf_cursor);
-        t.leaf_count.push_back((int32_t)level[i].ids.size());
-        t.perm.insert(t.perm.end(), level[i].ids.begin(), level[i].ids.end());
-        leaf_cursor += (int32_t)level[i].ids.size();
-        t.n_leaves++;
+  std::mt19937_64 rng(seed);
+  std::vector<int32_t> n_children, leaf_sizes, leaf_ids;
+  leaf_ids.reserve((size_t)N);
+  std::vector<std::vector<int32_t>> todo(1);
+  todo[0].resize((size_t)N);
+  for (int64_t i = 0; i < N; ++i) todo[0][(size_t)i] = (int32_t)i;
+  while (!todo.empty()) {
+    std::vector<int32_t> ids = std::move(todo.back());
+    todo.pop_back();
+    if ((int64_t)ids.size() >= leaf_threshold && d > 0) {
+      const int k = (int)std::min<size_t>((size_t)branching, ids.size());
+      auto cl = kmeans_reference(P, d, ids, k, rng);
+      if (cl.size() >= 2) {
+        n_children.push_back((int32_t)cl.size());
+        for (size_t c = cl.size(); c-- > 0;) todo.push_back(std::move(cl[c]));
+        continue;
       }
     }
-    level = std::move(next_level);
+    n_children.push_back(0);
+    leaf_sizes.push_back((int32_t)ids.size());
+    leaf_ids.insert(leaf_ids.end(), ids.begin(), ids.end());
   }
-  return t;
+  return import_tree_host(P, N, d, n_children.data(), (int64_t)n_children.size(),
+                          leaf_sizes.data(), (int64_t)leaf_sizes.size(), leaf_ids.data());
 }
 
 // Replay of an externally built tree (the reference's KmTree, recovered from

@@ -39,7 +39,8 @@ class psg_budget(ct.Structure):
 class psg_index_cfg(ct.Structure):
     _fields_ = [("variance_target", ct.c_double), ("d_cap", ct.c_int), ("d_fixed", ct.c_int),
                 ("branching", ct.c_int), ("max_depth", ct.c_int), ("leaf_threshold", ct.c_int),
-                ("seed", ct.c_uint64), ("hist_bins", ct.c_int), ("hist_include_scale", ct.c_int)]
+                ("seed", ct.c_uint64), ("hist_bins", ct.c_int), ("hist_include_scale", ct.c_int),
+                ("tree_kind", ct.c_int)]
 
 
 class psg_opt_cfg(ct.Structure):

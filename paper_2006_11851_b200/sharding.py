@@ -207,6 +207,8 @@ class GpuBand:
         self.torch = torch
         self.plan, self.plans = plan, plans
         self.index = index
+        from .api import _check_level_inputs
+        _check_level_inputs(np.asarray(init_full), index, cfg, exemplar_hist)
         self.C = init_full.shape[0]
         self.W, self.H = plan["W"], plan["H"]
         rows = np.ascontiguousarray(init_full[:, plan["p0"]:plan["e1"], :], dtype=np.float64)

@@ -26,7 +26,7 @@ def test_library_exports_every_header_symbol():
     exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
     missing = [s for s in syms if s not in exported]
     assert not missing, missing
-    assert N.lib.psg_abi_version() == 1
+    assert N.lib.psg_abi_version() == 2
 
 
 def test_library_is_built_for_sm100a():

@@ -302,17 +302,13 @@ def test_exact_search_ties_and_duplicates(gpu_ctx, port):
 @pytest.mark.parametrize("b,depth", [(4, 3), (8, 4), (16, 0)])
 def test_device_tree_build_valid_and_deterministic(gpu_ctx, port, b, depth, monkeypatch):
     """KmTree::build rules on the device: leaves partition the ids, splits stop at
-    the depth cap / leaf threshold, identical on rebuild; the host builder
-    (PERSYN_TREE=host) obeys the same invariants."""
+    the depth cap / leaf threshold, identical on rebuild."""
     ex, init = _stage(size=40)
     cand, mean, basis, proj = _injected(port, ex, 8, 12)
     runs = []
-    for builder in ("device", "device", "host"):
-        if builder == "host":
-            monkeypatch.setenv("PERSYN_TREE", "host")
+    for _ in range(2):
         ix = api.make_pca_tree_index(ex, 8, mean=mean, basis=basis, branching=b, max_depth=depth,
                                      seed=5, ctx=gpu_ctx)
-        monkeypatch.delenv("PERSYN_TREE", raising=False)
         ids, sizes = ix.leaves()
         assert np.array_equal(np.sort(ids), np.arange(ix.count))
         assert sizes.sum() == ix.count and np.all(sizes > 0)

@@ -1,11 +1,13 @@
-"""Greedy / backtrack(m) parity through a replayed reference tree.
+"""Greedy / backtrack(m) parity through the reference's own tree.
 
 The reference's default budget is backtrack(4) (optimizer.hpp:48), whose
 answer depends on the tree.  The reference's KmTree is rebuilt on the device
 from its public structure_json() + leaves() (psg_index_import_tree), after
 which greedy and backtrack queries must reproduce KmTree::query
 (km_tree.cpp:213-250) exactly: index, distance and points scanned — including
-the frontier tie-break on the reference's post-order node ids.
+the frontier tie-break on the reference's post-order node ids.  The same tree is
+also rebuilt by the library itself (tree_kind=TREE_REFERENCE, a replica of
+KmTree::build with the same std::mt19937_64 stream), with no import.
 """
 import json
 
@@ -118,3 +120,45 @@ def test_replayed_tree_optimize_level_backtrack4(gpu_ctx, port, ref, hist):
         assert s.changed == r[2] and s.nn_calls == r[3]
         assert abs(s.energy - r[1]) <= 1e-4 * abs(r[1])
         assert s.points_scanned == r[6]
+
+
+# ---- the library's own replica of KmTree::build (no import) -----------------------------
+@pytest.mark.gpu
+@pytest.mark.parametrize("b,seed,d", [(4, 7, 12), (8, 3, 16), (16, 11, 8)])
+def test_reference_tree_kind_equals_reference_tree(gpu_ctx, port, ref, b, seed, d):
+    """make_pca_tree_index(tree_kind=TREE_REFERENCE) builds the reference's tree
+    (same leaves, same post-order tie ids): every budget answers like
+    KmTree::query on the reference's own PcaTreeIndex."""
+    ex, init = _stage()
+    cand = port.extract_all(ex, 8, 1)
+    mean, basis, _ = fit_pca(cand, d_fixed=d)
+    h, sj, leaves = _ref_tree(ref, ex, 8, mean, basis, b, seed)
+    ix = api.make_pca_tree_index(ex, 8, mean=mean, basis=basis, branching=b, seed=seed,
+                                 tree_kind=api.TREE_REFERENCE, ctx=gpu_ctx)
+    assert ix.n_leaves == len(leaves)
+    ids, sizes = ix.leaves()
+    assert sorted(map(tuple, np.split(ids, np.cumsum(sizes)[:-1]))) == \
+        sorted(map(tuple, leaves))
+    rng = np.random.default_rng(seed)
+    Q = port.extract_all(init, 8, 1)[rng.choice(41 * 41, 120, replace=False)]
+    for mode, m, bud in [("greedy", 1, api.QueryBudget.greedy()),
+                         ("backtrack", 4, api.QueryBudget.backtrack(4)),
+                         ("backtrack", 8, api.QueryBudget.backtrack(8))]:
+        idx, dist, _, scanned = ix.nearest(Q, bud)
+        for i in range(Q.shape[0]):
+            ri, rd, rs = h.nearest(Q[i], mode=mode, max_leaves=m)
+            assert (idx[i], dist[i], scanned[i]) == (ri, rd, rs), (mode, m, i)
+    idx, dist, calls, scanned = api.search_step(init, ix, 2, 2, api.QueryBudget.backtrack(4))
+    i_r, d_r, c_r, s_r = h.search_step(init, 8, 2, 2, mode="backtrack", max_leaves=4)
+    assert (calls, scanned) == (c_r, s_r)
+    assert np.array_equal(idx, i_r) and np.array_equal(dist, d_r)
+
+
+@pytest.mark.gpu
+def test_reference_tree_kind_rejects_depth_cap(gpu_ctx, port):
+    ex, _ = _stage(size=24)
+    cand = port.extract_all(ex, 8, 1)
+    mean, basis, _ = fit_pca(cand, d_fixed=8)
+    with pytest.raises(api.DomainError):
+        api.make_pca_tree_index(ex, 8, mean=mean, basis=basis, branching=4, max_depth=3,
+                                tree_kind=api.TREE_REFERENCE, ctx=gpu_ctx)
