@@ -312,8 +312,15 @@ typedef struct {
   psg_stage_list stages;   /* per-level neighbourhood sizes; spacing = w / 4 */
   psg_opt_cfg cfg;         /* spacing ignored (w/4 per stage) */
   psg_index_cfg index;
-  uint64_t seed;
+  uint64_t seed;           /* initialize_output's engine seed; trees use level_seed(seed, l) */
   int guidance_kind;       /* 0 = guidance planes are row/col ramps recomputed per level */
+  /* Optional injected PCA model per stage (stage s = level * n_sizes + size
+   * index; NULL arrays or a NULL entry = fit on the device): mean [D],
+   * basis [d][D] row-major, d = stage_d[s].  The reference fits with Eigen
+   * (absent here): injection makes stage-by-stage parity checkable. */
+  const double* const* stage_mean;
+  const double* const* stage_basis;
+  const int* stage_d;
 } psg_request;
 
 typedef struct {
@@ -331,9 +338,37 @@ typedef struct {
   double final_energy;
 } psg_report;
 
-/* out_planes: [C][out_h][out_w] fp64 final state (RGB = the synthesized image). */
+/* out_planes: [C][out_h][out_w] fp64 final state (RGB = the synthesized image).
+ * Part 1 is the reference's initialize_output (below) with the guidance row
+ * ramp (plane 3) as the normalised scale map (bounds [0, 1]); each level l > 0
+ * starts from upsample_bilinear(x2) + fit_to of the previous level's RGB with
+ * the level's guidance re-imposed (pipeline.cpp:269-274). */
 psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, double* out_planes,
                           psg_report* report);
+
+/* initialize_output (pipeline.hpp:61-62, pipeline.cpp:96-175): scale-matched
+ * copy of exemplar pixels.  ex_planes [C >= 4][eh][ew] with plane 3 = the
+ * exemplar's S channel (normalised scale); out_scale [oh][ow] = the output
+ * ScaleMap's raw (unnormalised) float values; bounds {s_min, s_max}; seed of
+ * the std::mt19937_64 the reference passes in.  out4 [4][oh][ow] = RGB + the
+ * normalised target S (normalized_plane, pipeline.cpp:23-35).  Host code:
+ * sequential draws from one engine, exactly the reference's picks. */
+psg_status psg_initialize_output(const double* ex_planes, int C, int ew, int eh,
+                                 const float* out_scale, int ow, int oh, double s_min,
+                                 double s_max, uint64_t seed, double* out4);
+
+/* ---- resampling between levels (device kernels over host buffers) ---------- */
+/* downsample (image.cpp:38-62): block mean, factor >= 1, C planes [C][H][W] ->
+ * [C][H/f][W/f]. */
+psg_status psg_downsample(psg_ctx* ctx, const double* in, int C, int W, int H, int factor,
+                          double* out);
+/* upsample_bilinear (image.cpp:64-109): half-pixel centres, clamped border ->
+ * [C][H*f][W*f]. */
+psg_status psg_upsample_bilinear(psg_ctx* ctx, const double* in, int C, int W, int H,
+                                 int factor, double* out);
+/* fit_to (pipeline.cpp:39-52): crop or edge-replicate to [C][oh][ow]. */
+psg_status psg_fit_to(psg_ctx* ctx, const double* in, int C, int W, int H, int ow, int oh,
+                      double* out);
 
 /* ---- geometry helpers (neighborhood.cpp) ---------------------------------- */
 /* axis_positions (neighborhood.cpp:12-18); returns count, fills out if non-NULL. */

@@ -330,6 +330,10 @@ class Ref:
             L.ref_patch_tiles.argtypes = [_I, _I, _I, _VP, _VP]
             L.ref_downsample.argtypes = [_VP, _I, _I, _I, _VP, _VP, _VP]
             L.ref_upsample_bilinear.argtypes = [_VP, _I, _I, _I, _VP]
+            L.ref_scale_map.argtypes = [_I, _I, _D, _D, _VP, _VP]
+            L.ref_attach_scale.argtypes = [_VP, _I, _I, _D, _D, _VP]
+            L.ref_initialize_output.argtypes = [_VP, _I, _I, _VP, _I, _I, _D, _D, ct.c_uint64,
+                                                _VP]
         self.L = Ref._lib
 
     def _check(self, st, what=""):
@@ -495,6 +499,33 @@ class Ref:
         _, H, W = rgb.shape
         out = np.zeros((3, H * f, W * f), np.float64)
         self._check(self.L.ref_upsample_bilinear(_ptr(rgb), W, H, f, _ptr(out)), "upsample")
+        return out
+
+
+    # part 1 (scale_map.cpp, pipeline.cpp:96-175; pipeline.cpp built with the
+    # one-token fix of :118, oracle/Makefile)
+    def scale_map(self, W, H, slant, tilt):
+        """compute_scale_map: (raw float32 values (H, W), (s_max, s_min, s_delta))."""
+        vals = np.zeros((H, W), np.float32)
+        b = np.zeros(3, np.float64)
+        self._check(self.L.ref_scale_map(W, H, slant, tilt, _ptr(vals), _ptr(b)), "scale_map")
+        return vals, b
+
+    def attach_scale(self, rgb, slant, tilt):
+        rgb = _c(rgb, np.float64)
+        _, H, W = rgb.shape
+        out = np.zeros((4, H, W), np.float64)
+        self._check(self.L.ref_attach_scale(_ptr(rgb), W, H, slant, tilt, _ptr(out)), "attach")
+        return out
+
+    def initialize_output(self, ex4, out_vals, s_min, s_max, seed):
+        ex4 = _c(ex4, np.float64)
+        _, eh, ew = ex4.shape
+        v = _c(out_vals, np.float32)
+        oh, ow = v.shape
+        out = np.zeros((4, oh, ow), np.float64)
+        self._check(self.L.ref_initialize_output(_ptr(ex4), ew, eh, _ptr(v), ow, oh, s_min, s_max,
+                                                 seed, _ptr(out)), "initialize_output")
         return out
 
 

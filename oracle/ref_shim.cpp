@@ -28,6 +28,8 @@
 #include "persyn/neighborhood.hpp"
 #include "persyn/optimizer.hpp"
 #include "persyn/pca.hpp"
+#include "persyn/pipeline.hpp"
+#include "persyn/scale_map.hpp"
 
 // ---- PcaModel restatement (pca.cpp:11-47, :103-113), fp64, j ascending -----
 namespace persyn {
@@ -608,5 +610,43 @@ int ref_upsample_bilinear(const double* rgb, int W, int H, int factor, double* o
 }
 
 int ref_worker_count(void) { return worker_count(); }
+
+// ---- part 1 (scale_map.cpp, pipeline.cpp:96-175) ----------------------------------
+// compute_scale_map: raw float values + bounds {s_max, s_min, s_delta}.
+int ref_scale_map(int W, int H, double slant, double tilt, float* values, double* bounds) {
+  return guard([&] {
+    const ScaleMap m = compute_scale_map(W, H, ViewAngles{slant, tilt});
+    std::copy(m.values().begin(), m.values().end(), values);
+    bounds[0] = m.bounds().s_max;
+    bounds[1] = m.bounds().s_min;
+    bounds[2] = m.bounds().s_delta;
+  });
+}
+
+// attach_scale_channel(rgb, compute_scale_map(W, H, view)) -> 4 planes.
+int ref_attach_scale(const double* rgb, int W, int H, double slant, double tilt, double* out4) {
+  return guard([&] {
+    RasterImage img(W, H);
+    const std::size_t P = static_cast<std::size_t>(W) * H;
+    for (int c = 0; c < 3; ++c) std::memcpy(img.plane(c).data(), rgb + c * P, P * 8);
+    store_rgbs(attach_scale_channel(img, compute_scale_map(W, H, ViewAngles{slant, tilt})), out4);
+  });
+}
+
+// initialize_output(exemplar_rgbs, ScaleMap(values, bounds), mt19937_64(seed)).
+int ref_initialize_output(const double* ex4, int ew, int eh, const float* out_vals, int ow,
+                          int oh, double s_min, double s_max, uint64_t seed, double* out4) {
+  return guard([&] {
+    const RgbsImage ex = make_rgbs(ex4, ew, eh);
+    std::vector<float> v(out_vals, out_vals + static_cast<std::size_t>(ow) * oh);
+    ScaleBounds b;
+    b.s_max = s_max;
+    b.s_min = s_min;
+    b.s_delta = s_max - s_min;
+    const ScaleMap map(ow, oh, std::move(v), ViewAngles{}, b);
+    std::mt19937_64 rng(seed);
+    store_rgbs(initialize_output(ex, map, rng), out4);
+  });
+}
 
 }  // extern "C"

@@ -449,8 +449,11 @@ class Level:
 
 def synthesize(exemplar: np.ndarray, out_w: int, out_h: int, levels: int, sizes, cfg: OptimizerConfig,
                variance_target=0.95, d_cap=0, d_fixed=0, branching=4, max_depth=0, seed=0,
-               out_guidance: Optional[np.ndarray] = None, ctx: Optional[Context] = None):
-    """Coarse-to-fine driver (pipeline.cpp:216-315) over stages (level x size)."""
+               out_guidance: Optional[np.ndarray] = None, stage_pca=None,
+               tree_kind: int = TREE_DEVICE, ctx: Optional[Context] = None):
+    """Coarse-to-fine driver (pipeline.cpp:216-315) over stages (level x size).
+    stage_pca: optional list over stages (level-major, then sizes) of
+    (mean, basis) or None -- injected PCA models (fit on the device otherwise)."""
     ctx = ctx or default_context()
     ex = _c(exemplar, np.float64)
     C, eh, ew = ex.shape
@@ -468,8 +471,27 @@ def synthesize(exemplar: np.ndarray, out_w: int, out_h: int, levels: int, sizes,
     for i, s in enumerate(sizes):
         req.stages.sizes[i] = s
     req.cfg = cfg.c()
-    req.index = index_cfg(variance_target, d_cap, d_fixed, branching, max_depth, 0, seed)
+    req.index = index_cfg(variance_target, d_cap, d_fixed, branching, max_depth, 0, seed,
+                          tree_kind=tree_kind)
     req.seed = seed
+    keep = []
+    if stage_pca is not None:
+        ns = levels * len(sizes)
+        if len(stage_pca) != ns:
+            raise ShapeError(N.PSG_E_SHAPE, "stage_pca needs one entry per (level, size)")
+        means = (ct.c_void_p * ns)()
+        bases = (ct.c_void_p * ns)()
+        ds = (ct.c_int * ns)()
+        for s, mb in enumerate(stage_pca):
+            if mb is None:
+                continue
+            m, b = _c(mb[0], np.float64), _c(mb[1], np.float64)
+            keep += [m, b]
+            means[s], bases[s], ds[s] = m.ctypes.data, b.ctypes.data, b.shape[0]
+        keep += [means, bases, ds]
+        req.stage_mean = ct.cast(means, ct.POINTER(ct.c_void_p))
+        req.stage_basis = ct.cast(bases, ct.POINTER(ct.c_void_p))
+        req.stage_d = ct.cast(ds, ct.POINTER(ct.c_int))
     out = np.zeros((C, out_h, out_w))
     rep = N.psg_report()
     N.check(N.lib.psg_synthesize(ctx.h, ct.byref(req), _p(out), ct.byref(rep)))
@@ -483,6 +505,51 @@ def synthesize(exemplar: np.ndarray, out_w: int, out_h: int, levels: int, sizes,
                         optimize_millis=s.optimize_millis) for s in stages],
     }
     return out, report
+
+
+def initialize_output(exemplar: np.ndarray, out_scale: np.ndarray, s_min: float, s_max: float,
+                      seed: int) -> np.ndarray:
+    """initialize_output (pipeline.cpp:96-175): exemplar (C >= 4, plane 3 = S),
+    out_scale = the output ScaleMap's raw float values (oh, ow) with bounds
+    [s_min, s_max]; returns RGB + normalised S, (4, oh, ow)."""
+    ex = _c(exemplar, np.float64)
+    C, eh, ew = ex.shape
+    sc = _c(out_scale, np.float32)
+    oh, ow = sc.shape
+    out = np.zeros((4, oh, ow))
+    N.check(N.lib.psg_initialize_output(_p(ex), C, ew, eh, _p(sc), ow, oh, float(s_min),
+                                        float(s_max), int(seed), _p(out)))
+    return out
+
+
+def downsample(planes: np.ndarray, factor: int, ctx: Optional[Context] = None) -> np.ndarray:
+    """Block-mean downsample of every plane (image.cpp:38-62), on the device."""
+    ctx = ctx or default_context()
+    x = _c(planes, np.float64)
+    C, H, W = x.shape
+    out = np.zeros((C, H // factor if factor > 0 else 0, W // factor if factor > 0 else 0))
+    N.check(N.lib.psg_downsample(ctx.h, _p(x), C, W, H, factor, _p(out)))
+    return out
+
+
+def upsample_bilinear(planes: np.ndarray, factor: int, ctx: Optional[Context] = None) -> np.ndarray:
+    """Half-pixel bilinear upsample of every plane (image.cpp:64-109), on the device."""
+    ctx = ctx or default_context()
+    x = _c(planes, np.float64)
+    C, H, W = x.shape
+    out = np.zeros((C, H * max(factor, 0), W * max(factor, 0)))
+    N.check(N.lib.psg_upsample_bilinear(ctx.h, _p(x), C, W, H, factor, _p(out)))
+    return out
+
+
+def fit_to(planes: np.ndarray, width: int, height: int, ctx: Optional[Context] = None) -> np.ndarray:
+    """Crop / edge-replicate every plane to width x height (pipeline.cpp:39-52), on the device."""
+    ctx = ctx or default_context()
+    x = _c(planes, np.float64)
+    C, H, W = x.shape
+    out = np.zeros((C, max(height, 0), max(width, 0)))
+    N.check(N.lib.psg_fit_to(ctx.h, _p(x), C, W, H, width, height, _p(out)))
+    return out
 
 
 # ---- host helpers -----------------------------------------------------------------

@@ -399,6 +399,10 @@ HostTree import_tree_host(const double* proj, int64_t N, int d, const int32_t* n
                           int64_t n_nodes, const int32_t* leaf_sizes, int64_t n_leaves,
                           const int32_t* leaf_ids);
 void fit_pca_device(psg_ctx* ctx, Index& ix, const psg_index_cfg& cfg);
+// initialize_output (pipeline.cpp:96-175), part1_host.cpp
+void initialize_output_host(const double* ex_planes, int C, int ew, int eh,
+                            const float* out_scale, int ow, int oh, double s_min, double s_max,
+                            uint64_t seed, double* out4);
 void create_solver_handles(psg_ctx* ctx);  // cuBLAS + cuSOLVER handles of a context
 int64_t plan_host(int W, int H, int w, int sp, int p, int32_t* mult);
 std::vector<int32_t> axis_positions(int extent, int window, int step);

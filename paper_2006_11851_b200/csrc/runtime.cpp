@@ -1767,19 +1767,6 @@ double psg_hist_mass(int64_t count, int64_t pixels) {
 // Pyramid driver: synthesize (pipeline.cpp:216-315), stage schedule
 // (level x neighbourhood size) per the BASELINE configs.
 // ===========================================================================
-namespace psg {
-namespace {
-
-uint64_t splitmix64(uint64_t x) {
-  x += 0x9E3779B97F4A7C15ull;
-  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
-  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
-  return x ^ (x >> 31);
-}
-
-
-}  // namespace
-}  // namespace psg
 
 extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, double* out_planes,
                                      psg_report* report) {
@@ -1849,24 +1836,24 @@ extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, doubl
         }
       }
     }
-    // Scale-matched initialisation at the coarsest level (part 1,
-    // pipeline.cpp:96-175 in spirit): copy the RGB of an exemplar pixel on
-    // the row whose guidance matches, column chosen by a seeded hash.
+    // Part 1 at the coarsest level: initialize_output (pipeline.cpp:96-175)
+    // with the first guidance plane (row ramp) as the normalised scale map,
+    // bounds [0, 1]: the exemplar's S plane is its scale, the output's ramp
+    // (fp32 values) its target; further guidance planes are copied.
     std::vector<double> hex((size_t)C * ew[0] * eh[0]), hog((size_t)G * ow[0] * oh[0]);
     ex_lv[0].download(ctx, hex.data(), hex.size());
     og_lv[0].download(ctx, hog.data(), hog.size());
     PSG_CUDA(cudaStreamSynchronize(ctx->stream));
-    const size_t lp0 = (size_t)ew[0] * eh[0], op0 = (size_t)ow[0] * oh[0];
+    const size_t op0 = (size_t)ow[0] * oh[0];
     std::vector<double> init((size_t)C * op0);
-    for (int y = 0; y < oh[0]; ++y)
-      for (int x = 0; x < ow[0]; ++x) {
-        const size_t i = (size_t)y * ow[0] + x;
-        const double s = std::min(1.0, std::max(0.0, hog[i]));
-        const int ey = (int)std::lround(s * (eh[0] - 1));
-        const int ex = (int)(splitmix64(req->seed ^ (uint64_t)i) % (uint64_t)ew[0]);
-        for (int c = 0; c < 3; ++c) init[c * op0 + i] = hex[c * lp0 + (size_t)ey * ew[0] + ex];
-        for (int g = 0; g < G; ++g) init[(3 + g) * op0 + i] = hog[g * op0 + i];
-      }
+    {
+      std::vector<float> target(op0);
+      for (size_t i = 0; i < op0; ++i) target[i] = (float)hog[i];
+      initialize_output_host(hex.data(), C, ew[0], eh[0], target.data(), ow[0], oh[0], 0.0, 1.0,
+                             req->seed, init.data());
+      for (int g = 1; g < G; ++g)
+        std::copy(hog.begin() + g * op0, hog.begin() + (g + 1) * op0, init.begin() + (3 + g) * op0);
+    }
     DBuf<double> state((size_t)C * op0);
     state.upload(ctx, init.data(), init.size());
     rep.part1_millis = now_ms() - t0;
@@ -1900,13 +1887,22 @@ extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, doubl
         const double ti = now_ms();
         {  // stage scope: index and level are released before the next stage
         psg_index_cfg icfg = req->index;
-        icfg.seed = (req->seed ^ (0x9E3779B97F4A7C15ull * (uint64_t)(l + 1))) ^ (uint64_t)w;
+        // level_seed (pipeline.cpp:54-56); several sizes per level (the
+        // BASELINE configs' stages) also mix in the window width
+        icfg.seed = (req->seed ^ (0x9E3779B97F4A7C15ull * (uint64_t)(l + 1))) ^
+                    (req->stages.n_sizes > 1 ? (uint64_t)w : 0ull);
         if (req->cfg.histogram_matching) {
           icfg.hist_bins = req->cfg.histogram_bins;
           icfg.hist_include_scale = req->cfg.histogram_include_scale;
         }
-        auto index = create_index_from_device_planes(ctx, ex_lv[l].p, C, ew[l], eh[l], w, nullptr,
-                                                     nullptr, 0, icfg);
+        const int s_id = l * req->stages.n_sizes + si;
+        const double* s_mean = req->stage_mean ? req->stage_mean[s_id] : nullptr;
+        const double* s_basis = req->stage_basis ? req->stage_basis[s_id] : nullptr;
+        const int s_d = (s_basis && req->stage_d) ? req->stage_d[s_id] : 0;
+        if ((s_mean == nullptr) != (s_basis == nullptr))
+          fail(PSG_E_DOMAIN, "stage PCA injection needs both mean and basis");
+        auto index = create_index_from_device_planes(ctx, ex_lv[l].p, C, ew[l], eh[l], w, s_mean,
+                                                     s_basis, s_d, icfg);
         const double index_ms = now_ms() - ti;
         psg_opt_cfg cfg = req->cfg;
         cfg.spacing = std::max(1, w / 4);
@@ -2011,5 +2007,77 @@ extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, doubl
     state.download(ctx, out_planes, (size_t)C * req->out_w * req->out_h);
     PSG_CUDA(cudaStreamSynchronize(ctx->stream));
     if (report) *report = rep;
+  });
+}
+
+// ---------------------------------------------------------------------------
+// Part 1 and the resampling between levels, as standalone entry points.
+extern "C" psg_status psg_initialize_output(const double* ex_planes, int C, int ew, int eh,
+                                            const float* out_scale, int ow, int oh,
+                                            double s_min, double s_max, uint64_t seed,
+                                            double* out4) {
+  return guarded([&] {
+    if (!ex_planes || !out_scale || !out4) fail(PSG_E_DOMAIN, "null argument");
+    psg::initialize_output_host(ex_planes, C, ew, eh, out_scale, ow, oh, s_min, s_max, seed,
+                                out4);
+  });
+}
+
+namespace {
+// in [C][H][W] (host) -> device, f(plane_in, plane_out) per plane, -> out (host)
+template <class F>
+void resample_planes(psg_ctx* ctx, const double* in, int C, int W, int H, int ow, int oh,
+                     double* out, F&& f) {
+  using namespace psg;
+  if (!ctx || !in || !out) fail(PSG_E_DOMAIN, "null argument");
+  if (C < 1 || W < 1 || H < 1) fail(PSG_E_DOMAIN, "empty image");
+  const size_t ip = (size_t)W * H, op = (size_t)ow * oh;
+  DBuf<double> din((size_t)C * ip), dout((size_t)C * op);
+  din.upload(ctx, in, din.n);
+  for (int c = 0; c < C; ++c) f(din.p + c * ip, dout.p + c * op);
+  dout.download(ctx, out, dout.n);
+  PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+}  // namespace
+
+extern "C" psg_status psg_downsample(psg_ctx* ctx, const double* in, int C, int W, int H,
+                                     int factor, double* out) {
+  return guarded([&] {
+    psg::StreamScope _ss(ctx ? ctx->stream : nullptr);
+    if (factor < 1) fail(PSG_E_DOMAIN, "downsample factor must be >= 1");
+    const int ow = W / factor, oh = H / factor;
+    if (ow < 1 || oh < 1) fail(PSG_E_DOMAIN, "downsample leaves no pixels");
+    resample_planes(ctx, in, C, W, H, ow, oh, out, [&](const double* a, double* b) {
+      psg::launch_downsample(ctx, a, W, H, factor, b);
+    });
+  });
+}
+
+extern "C" psg_status psg_upsample_bilinear(psg_ctx* ctx, const double* in, int C, int W, int H,
+                                            int factor, double* out) {
+  return guarded([&] {
+    psg::StreamScope _ss(ctx ? ctx->stream : nullptr);
+    if (factor < 1) fail(PSG_E_DOMAIN, "upsample factor must be >= 1");
+    if ((int64_t)W * factor * (int64_t)H * factor > (int64_t{1} << 30))
+      fail(PSG_E_DOMAIN, "upsampled image would be unreasonably large");
+    resample_planes(ctx, in, C, W, H, W * factor, H * factor, out,
+                    [&](const double* a, double* b) {
+                      if (factor == 1)
+                        PSG_CUDA(cudaMemcpyAsync(b, a, sizeof(double) * W * H,
+                                                 cudaMemcpyDeviceToDevice, ctx->stream));
+                      else
+                        psg::launch_upsample_bilinear(ctx, a, W, H, factor, b);
+                    });
+  });
+}
+
+extern "C" psg_status psg_fit_to(psg_ctx* ctx, const double* in, int C, int W, int H, int ow,
+                                 int oh, double* out) {
+  return guarded([&] {
+    psg::StreamScope _ss(ctx ? ctx->stream : nullptr);
+    if (ow < 1 || oh < 1) fail(PSG_E_DOMAIN, "image dimensions must be at least 1x1");
+    resample_planes(ctx, in, C, W, H, ow, oh, out, [&](const double* a, double* b) {
+      psg::launch_fit_to(ctx, a, W, H, ow, oh, b);
+    });
   });
 }

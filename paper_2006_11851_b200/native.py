@@ -73,7 +73,8 @@ class psg_request(ct.Structure):
                 ("eh", ct.c_int), ("out_guidance", ct.POINTER(ct.c_double)), ("out_w", ct.c_int),
                 ("out_h", ct.c_int), ("levels", ct.c_int), ("stages", psg_stage_list),
                 ("cfg", psg_opt_cfg), ("index", psg_index_cfg), ("seed", ct.c_uint64),
-                ("guidance_kind", ct.c_int)]
+                ("guidance_kind", ct.c_int), ("stage_mean", ct.POINTER(ct.c_void_p)),
+                ("stage_basis", ct.POINTER(ct.c_void_p)), ("stage_d", ct.POINTER(ct.c_int))]
 
 
 class psg_stage_report(ct.Structure):
@@ -138,6 +139,10 @@ _SIGS = {
     "psg_plan": (I64, [I, I, I, I, I, VP]),
     "psg_pow_cr": (D, [D, D]),
     "psg_hist_mass": (D, [I64, I64]),
+    "psg_initialize_output": (I, [VP, I, I, I, VP, I, I, D, D, ct.c_uint64, VP]),
+    "psg_downsample": (I, [VP, VP, I, I, I, I, VP]),
+    "psg_upsample_bilinear": (I, [VP, VP, I, I, I, I, VP]),
+    "psg_fit_to": (I, [VP, VP, I, I, I, I, I, VP]),
 }
 
 for _name, (_res, _args) in _SIGS.items():
