@@ -54,6 +54,10 @@ def parse():
     ap.add_argument("--out", default="")
     ap.add_argument("--sharded", action="store_true",
                     help="use the row-band path even on one GPU")
+    ap.add_argument("--no-c4", action="store_true",
+                    help="skip the same-config (C = 4) device line")
+    ap.add_argument("--no-synthesize", action="store_true",
+                    help="skip the whole-cfg3 psg_synthesize wall time")
     return ap.parse_args()
 
 
@@ -62,6 +66,11 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def wl_mod():
+    from paper_2006_11851_b200 import workloads as wl
+    return wl
 
 
 def stage_inputs(G: int, window: int):
@@ -281,6 +290,57 @@ def ncu_traffic(kernel: str):
         return None, None
 
 
+def time_level_steps(api, ctx, stream, index, init, ocfg, steps, warmup, flush):
+    """Device-resident EM iterations of one Level on `stream`: `warmup`
+    untimed, then `steps` timed with CUDA events (L2 flushed before each)."""
+    import torch
+    level = api.Level(init, index, ocfg)
+    level.prime()
+    for _ in range(warmup):
+        level.iterate(1)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    torch.cuda.synchronize()
+    stats = []
+    for k in range(steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(float(k))
+            ev[k][0].record(stream)
+        stats += level.iterate(1)
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    ms = float(np.sum([a.elapsed_time(b) for a, b in ev]))
+    return ms, stats, level
+
+
+def e2e_optimize_level(api, ctx, index, init, ocfg_kw, n_it, calls=3):
+    """psg_optimize_level with pinned host buffers: wall time per call (H2D of
+    the init, priming + n_it EM iterations, D2H of the image)."""
+    import ctypes as ct
+    import torch
+    from paper_2006_11851_b200 import native as N
+    pinned = torch.empty(init.shape, dtype=torch.float64, pin_memory=True)
+    pinned.numpy()[...] = init
+    out_pinned = torch.empty(init.shape, dtype=torch.float64, pin_memory=True)
+    cfg = api.OptimizerConfig(max_iterations=n_it, min_iterations=n_it, **ocfg_kw)
+    H, W = init.shape[1], init.shape[2]
+
+    def call():
+        c = cfg.c()
+        st = (N.psg_iter_stats * n_it)()
+        n = ct.c_int()
+        N.check(N.lib.psg_optimize_level(ctx.h, index.h, ct.c_void_p(pinned.data_ptr()), W, H,
+                                         ct.byref(c), None, ct.c_void_p(out_pinned.data_ptr()),
+                                         ct.cast(st, ct.c_void_p), ct.byref(n)))
+    call()  # warm-up: pool growth for the call's level buffers
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(calls):
+        call()
+    torch.cuda.synchronize()
+    return (time.perf_counter() - t0) / calls
+
+
 def run_ours(args):
     import torch
     rank, world, local = dist_env()
@@ -297,8 +357,11 @@ def run_ours(args):
     ctx = api.Context(local, stream.cuda_stream)
     sharded = world > 1 or args.sharded
     t_build = time.perf_counter()
-    index = api.make_pca_tree_index(ex, args.window, d_fixed=32, branching=8, max_depth=4,
-                                    seed=1, hist_bins=16, ctx=ctx)
+    index = api.make_pca_tree_index(ex, args.window, ctx=ctx,
+                                    **(dict(d_fixed=32, branching=8, max_depth=4, seed=1,
+                                            hist_bins=16) if args.budget == "exact" else
+                                       dict(d_fixed=32, branching=8, max_depth=0, seed=1,
+                                            hist_bins=16, tree_kind=api.TREE_REFERENCE)))
     if world > 1:
         # every rank must hold bit-identical PCA models: rank 0's is broadcast
         mean, basis, _ = index.pca()
@@ -407,35 +470,65 @@ def run_ours(args):
         "kernel_times_from": f"{n_prof} extra steps with CUDA events around every launch on the "
                              "library stream, right after the timed region (shares of those steps)",
     }
+    ocfg_kw = dict(convergence_fraction=1e-9, histogram_bins=16, histogram_matching=True,
+                   nbhd_width=args.window, spacing=sp, patch_width=2, budget=budget)
+    tree_kw = dict(d_fixed=32, branching=8, max_depth=4, seed=1, hist_bins=16)
+    if args.budget != "exact":
+        # tree-dependent budgets: the reference's own KmTree (same construction
+        # and engine stream as the reference arm's make_pca_tree_index)
+        tree_kw.update(max_depth=0, tree_kind=api.TREE_REFERENCE)
+    # ---- same-config line: the reference arm's workload exactly (C = 4) --------------
+    if not args.no_c4 and not sharded and world == 1:
+        cfg4_, ex4, init4, _ = stage_inputs(1, args.window)
+        index4 = api.make_pca_tree_index(ex4, args.window, ctx=ctx, **tree_kw)
+        ms4, st4, lv4 = time_level_steps(api, ctx, stream, index4, init4, ocfg, args.steps,
+                                         args.warmup, flush)
+        del lv4
+        res4 = {"value": args.steps / (ms4 / 1e3), "unit": UNIT,
+                "ms_per_step": ms4 / args.steps,
+                "workload": "cfg3 finest stage with ONE guidance plane (C = 4, D = 256): the "
+                            "reference arm's exact workload (the reference hard-codes C = 4, "
+                            "image.hpp:70); same exemplar / output / w / d / tree / budget",
+                "energy_last": st4[-1].energy}
+        if not args.no_e2e:
+            t4 = e2e_optimize_level(api, ctx, index4, init4, ocfg_kw, 10)
+            res4["e2e"] = {"value": 10 / t4, "unit": UNIT, "h2d_bytes_per_step": int(init4.nbytes),
+                           "d2h_bytes_per_step": int(init4.nbytes),
+                           "step": "one psg_optimize_level call (host buffers, 10 EM iterations "
+                                   "incl. the priming search)"}
+        result["same_config_c4"] = res4
+        del index4
+    # ---- whole cfg3 pyramid through psg_synthesize (host buffers) ---------------------
+    if not args.no_synthesize and not sharded and world == 1:
+        cfg3 = cfg
+        rgb = wl_mod().sinusoid_exemplar(cfg3.ex_size, cfg3.n_sin, cfg3.ramp, cfg3.seed)
+        exs = wl_mod().rgbs_planes(rgb, cfg3.G)
+        scfg = api.OptimizerConfig(max_iterations=cfg3.iterations, min_iterations=cfg3.iterations,
+                                   convergence_fraction=1e-9, histogram_bins=16,
+                                   histogram_matching=True, budget=budget)
+        skw = dict(variance_target=0.95, d_fixed=cfg3.d_fixed, branching=cfg3.branching,
+                   max_depth=cfg3.depth, seed=cfg3.seed, ctx=ctx)
+        api.synthesize(exs, cfg3.out, cfg3.out, cfg3.levels, cfg3.sizes, scfg, **skw)  # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, srep = api.synthesize(exs, cfg3.out, cfg3.out, cfg3.levels, cfg3.sizes, scfg, **skw)
+        torch.cuda.synchronize()
+        t_syn = time.perf_counter() - t0
+        result["synthesize_cfg3"] = {
+            "wall_s": t_syn, "unit": "s",
+            "workload": "BASELINE configs[3] end to end: exemplar 256^2 C=5 -> 1024^2, 3 levels x "
+                        "sizes {32,16,8}, d=32, b=8 depth 4, 10 EM iterations per stage, "
+                        "initialize_output + per-stage device index builds + EM; host buffers",
+            "em_iterations": sum(s["iterations"] for s in srep["stages"]),
+            "index_build_s": sum(s["index_millis"] for s in srep["stages"]) / 1e3,
+            "optimize_s": sum(s["optimize_millis"] for s in srep["stages"]) / 1e3,
+            "total_nn_calls": srep["total_nn_calls"]}
     # ---- e2e through the public host-buffer API (pinned host memory) ------
     if not args.no_e2e and not sharded:
         n_it = 10  # cfg3: 10 EM iterations per stage
-        pinned = torch.empty(init.shape, dtype=torch.float64, pin_memory=True)
-        pinned.numpy()[...] = init
-        out_pinned = torch.empty(init.shape, dtype=torch.float64, pin_memory=True)
-        e2e_cfg = api.OptimizerConfig(max_iterations=n_it, min_iterations=n_it,
-                                      convergence_fraction=1e-9, histogram_bins=16,
-                                      histogram_matching=True, nbhd_width=args.window,
-                                      spacing=sp, patch_width=2, budget=budget)
-        import ctypes as ct
-        from paper_2006_11851_b200 import native as N
-
-        def e2e_call():
-            c = e2e_cfg.c()
-            st = (N.psg_iter_stats * n_it)()
-            n = ct.c_int()
-            N.check(N.lib.psg_optimize_level(ctx.h, index.h, ct.c_void_p(pinned.data_ptr()),
-                                             cfg.out, cfg.out, ct.byref(c), None,
-                                             ct.c_void_p(out_pinned.data_ptr()),
-                                             ct.cast(st, ct.c_void_p), ct.byref(n)))
-        e2e_call()  # warm-up: pool growth for the call's level buffers
-        calls_e2e = 3
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(calls_e2e):
-            e2e_call()
-        torch.cuda.synchronize()
-        t_e2e = (time.perf_counter() - t0) / calls_e2e
+        t_e2e = e2e_optimize_level(api, ctx, index, init, dict(
+            convergence_fraction=1e-9, histogram_bins=16, histogram_matching=True,
+            nbhd_width=args.window, spacing=sp, patch_width=2, budget=budget), n_it)
         result["e2e"] = {"value": n_it / t_e2e, "unit": UNIT,
                          "h2d_bytes_per_step": int(init.nbytes),
                          "d2h_bytes_per_step": int(init.nbytes),

@@ -1216,11 +1216,17 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
   const int nn = a.tree.n_nodes;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
   const float kInfF = __int_as_float(0x7f800000);
+  const int64_t nq = a.nq_dev ? (int64_t)*a.nq_dev : a.nq;
+  // approximate queries (tensor-core projection): every comparison uses the
+  // best distance inflated by the query's error band, (sqrt(best) + 2 delta)^2,
+  // so every point that can be the exact winner is evaluated; `second` keeps
+  // the smallest other evaluated distance (kernels_project_tc.cu)
+  const bool approx = a.qdelta != nullptr;
   // image queries: 8 x 4 anchor tiles (overlapping windows share candidates);
   // vector queries: 32 consecutive rows
-  const int qny = a.qxs ? (int)(a.nq / a.qnx) : 0;
+  const int qny = a.qxs ? (int)(nq / a.qnx) : 0;
   const int tnx = a.qxs ? (a.qnx + 7) / 8 : 0;
-  const int64_t n_tiles = a.qxs ? (int64_t)tnx * ((qny + 3) / 4) : (a.nq + 31) / 32;
+  const int64_t n_tiles = a.qxs ? (int64_t)tnx * ((qny + 3) / 4) : (nq + 31) / 32;
 
   // persistent warps fetch tiles from a global ticket: tile costs vary ~4x,
   // and a fast warp must not idle until its CTA's slowest warp finishes
@@ -1239,9 +1245,19 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
       q = valid ? (int64_t)iy * a.qnx + ix : 0;
     } else {
       q = t * 32 + lane;
-      valid = q < a.nq;
+      valid = q < nq;
     }
     const double* qrow = a.q + (valid ? q : 0) * d;
+    const float dq = (approx && valid) ? a.qdelta[q] : 0.f;
+    const bool trav = valid && !(dq > 3.0e38f);  // delta = inf: exact fallback only
+    const double twod = 2.0 * (double)dq;
+    // float threshold for a best distance: the best itself, or its band
+    auto infl = [&](double b) -> float {
+      if (!approx || !(b > 0.0) || b == kInf) return __double2float_ru(b);
+      const double r = sqrt(b) * (1.0 + 1e-12) + twod;
+      return __double2float_ru(r * r * (1.0 + 1e-15));
+    };
+    double second = kInf;
     float2 q2[DP / 2];
     double qn2 = 0.0;
 #pragma unroll
@@ -1256,7 +1272,7 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
     // box margin: >= |float(q_j) - q_j| + the rounding of (-q_j -/+ margin)
     const float qdelta2 = 2.4e-7f * qn;
     // invalid lanes hold best = -1: every bound (>= 0) prunes them
-    double best = valid ? kInf : -1.0;
+    double best = trav ? kInf : -1.0;
     int32_t best_id = 0x7fffffff;
     int64_t scanned = 0, exact_evals = 0;
     int32_t visited = 0;
@@ -1264,7 +1280,7 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
     // ---- seed (exact fp64): the query's previous assignment is the initial
     // upper bound.  (Lattice neighbours' shifted assignments were tried too: on
     // the bench stage they cost more exact evaluations than they save.)
-    if (a.seed_idx && valid) {
+    if (a.seed_idx && trav) {
       const int32_t cand = a.seed_idx[q];
       best = dist2_seq_cold(qrow, a.proj + (int64_t)cand * d, d);
       best_id = cand;
@@ -1273,7 +1289,7 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
     }
 
     // best rounded up to float: float compares against it can only keep more
-    float bestf = __double2float_ru(best);
+    float bestf = infl(best);
     if (lane == 0) sm_[0] = a.tree.meta[0];
     slb[0][lane] = __float2bfloat16_rd(0.f);
     int top = 1;
@@ -1394,12 +1410,15 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
                 const double d2 = dist2_seq_cold(qrow, a.proj + (int64_t)id * d, d);
                 ++exact_evals;
                 if (lex_less(d2, id, best, best_id)) {
+                  if (best_id != id) second = fmin(second, best);
                   best = d2;
                   best_id = id;
-                  best_up = __double2float_ru(best);
+                  best_up = infl(best);
                   bestf = best_up;
                   thr = best_up * (1.f + 1e-4f) +
                         1.01e-6f * (qn + a.pnorm_max) * (sqrtf(2.f * best_up + 1.f) + 1e-3f) + 1e-30f;
+                } else if (id != best_id) {
+                  second = fmin(second, d2);
                 }
               }
             }
@@ -1523,6 +1542,19 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
       __syncwarp();
     }
     if (valid) {
+      if (approx) {
+        // unique within the band -> it is the exact chain's winner; otherwise
+        // (near-tie, or no usable band) the exact fallback re-searches it
+        bool amb = !trav;
+        if (trav) {
+          const double r = sqrt(best) * (1.0 + 1e-12) + twod;
+          amb = second <= r * r * (1.0 + 1e-15);
+        }
+        if (amb) {
+          a.amb_list[atomicAdd(a.amb_count, 1)] = (int32_t)q;
+          if (best_id == 0x7fffffff) best_id = a.seed_idx ? a.seed_idx[q] : 0;
+        }
+      }
       a.out_idx[q] = best_id;
       a.out_d2[q] = best;
       if (a.out_scanned) a.out_scanned[q] = scanned;
@@ -1553,6 +1585,11 @@ static int tile_resident_ctas(psg_ctx* ctx) {
     if (per_sm < 1) per_sm = 1;
   }
   return per_sm * ctx->num_sms;
+}
+
+bool search_uses_tiles(psg_ctx* ctx, const DevTree& tree, int d, bool exact) {
+  return exact && d <= kMaxD && tree.centroid32 && !ctx->knobs.legacy_search &&
+         tree.max_children <= kTileMaxB && 1 + tree.max_depth * (tree.max_children - 1) <= kTileStack;
 }
 
 void launch_search(psg_ctx* ctx, const SearchArgs& a) {

@@ -108,6 +108,15 @@ struct Index {
   float* brute_nup = nullptr;   // [ptiles * 256] |p - mu| rounded up
   float* brute_mu = nullptr;    // [nch * 32] centring vector
   float* brute_tmax = nullptr;  // [ptiles] largest |p - mu| bound per tile
+  // tensor-core window projection (kernels_project_tc.cu): the basis rounded to
+  // Bq = rint(B * 2^22) as three signed base-256 digit slices in UMMA K-major
+  // layout over 8-byte pixels, plus row sums for the error bound
+  bool tc = false;
+  int tc_np = 0;               // UMMA N: d + 1 (a ones row for sum v) rounded up to 16
+  int tc_kb = 0;               // K bytes per slice: w * w * 8 (8-byte pixels), multiple of 32
+  int8_t* tc_b = nullptr;      // [3][kb / 16][np][16]
+  double* tc_bmu = nullptr;    // [d] B . mean (rounded from long double)
+  double* tc_err = nullptr;    // [d] 2^-22 |B_k|_1 + 2^-52 |B mu_k| + 1e-12
   ~Index();
 };
 
@@ -179,6 +188,7 @@ struct psg_ctx {
     bool project_kpt2 = false;        // PERSYN_PROJECT_KPT2: 2-per-lane d<=48 projection
     bool no_carry = false;            // PERSYN_NO_CARRY: stages do not seed from the previous
     bool eig_direct = false;          // PERSYN_EIG: dense eigensolver instead of subspace iteration
+    bool exact_projection = false;    // PERSYN_EXACT_PROJECTION: fp64 SIMT projection of every query
   } knobs;
 };
 
@@ -213,6 +223,33 @@ void launch_make_mirror8(psg_ctx* ctx, const double* planes, int C, int W, int H
 void launch_project_windows(psg_ctx* ctx, const float* mirror, int img_w, int C, int w,
                             AnchorSet anchors, const double* mean, const double* basis, int d,
                             double* out);
+// ---- tensor-core projection (kernels_project_tc.cu) --------------------------------
+// Quantised digit mirror of an fp32 mirror: V = rint(v * 2^21) for v in [0, 1]
+// as three u8 base-256 digits, 8-byte pixels (channels >= C zero): q8
+// [3][H][W][8] bytes.  A value outside [0, 1] (or NaN) sets *bad (the
+// projection then reports delta = +inf for every query: exact fallback).
+void launch_make_digits(psg_ctx* ctx, const float* mirror, int C, int W, int H, uint8_t* q8,
+                        int64_t slice_bytes, int* bad);
+// Builds ix.tc_* from the host basis (false: basis not representable, keep the
+// exact fp64 projection).
+bool tc_prepare(psg_ctx* ctx, Index& ix);
+// q^ = B^ v^ - B.mu on the tensor cores (tcgen05.mma kind::i8, exact int32
+// accumulation), delta[q] = a rigorous bound on |q^ - q| (2-norm; +inf when a
+// window holds a value outside [0, 1]).  out [n][d] fp64.
+void launch_project_windows_tc(psg_ctx* ctx, const uint8_t* q8, int64_t slice_bytes, int img_w,
+                               const int* bad, AnchorSet anchors, const Index& ix, double* out,
+                               float* delta);
+// Exact (reference-chain) projection of listed anchors: out [count][d] compact,
+// count read on the device (*count), list = anchor ids.
+void launch_project_list(psg_ctx* ctx, const float* mirror, int img_w, int C, int w,
+                         AnchorSet anchors, const int32_t* list, const int* count,
+                         const Index& ix, double* out);
+// compact seeds / scatter of a fallback search over listed anchors
+void launch_list_gather_i32(psg_ctx* ctx, const int32_t* src, const int32_t* list,
+                            const int* count, int32_t* out);
+void launch_list_scatter(psg_ctx* ctx, const int32_t* list, const int* count,
+                         const int32_t* idx_c, const int64_t* sc_c, const int64_t* ex_c,
+                         int32_t* idx, int64_t* scanned, int64_t* exact);
 void launch_project_vectors(psg_ctx* ctx, const float* X, int64_t n, int D, const double* mean,
                             const double* basis, int d, double* out);
 // Exact NN search over the tree (km_tree.cpp:197-284 semantics).
@@ -243,6 +280,13 @@ struct SearchArgs {
   int* flags;
   int64_t* sched = nullptr;  // [2] tile ticket + warps done (self re-arming, zeroed at ctx creation)
   const int32_t* tile_order = nullptr;  // optional tile permutation (image tiles)
+  // approximate queries (tensor-core projection): q holds q^ with |q^ - q|
+  // <= qdelta[i]; the search keeps every point within (|q^ - p*| + 2 delta)
+  // and lists the queries whose winner is not separated by that band
+  const float* qdelta = nullptr;
+  int32_t* amb_list = nullptr;  // [nq] ambiguous query ids
+  int* amb_count = nullptr;     // device counter (zeroed by the caller)
+  const int* nq_dev = nullptr;  // optional: query count read on the device
 };
 // Tile permutation for the next exact search of the same anchors: descending
 // previous per-tile work (order: [image_tile_count(nq, qnx)]).
@@ -258,6 +302,8 @@ void launch_brute_search(psg_ctx* ctx, const Index& ix, const RowSrc& qsrc, int6
                          const int32_t* seed, int32_t* out_idx, double* out_d2,
                          int64_t* out_scanned, int64_t* out_exact);
 void launch_search(psg_ctx* ctx, const SearchArgs& a);
+// true when an exact search of this tree runs on the tile kernel
+bool search_uses_tiles(psg_ctx* ctx, const DevTree& tree, int d, bool exact);
 // tcgen05 (UMMA) tile search; returns false when the tree shape is unsupported.
 // Tile search with the leaf filter on mma.sync (bf16 split); false if unsupported.
 // Locality ordering of unstructured queries (search-only workloads).

@@ -228,7 +228,7 @@ double pow_cr_host(double x, double y) { return pow_cr(x, y); }
 Index::~Index() {
   // stream-ordered frees (the allocations come from the context's pool)
   cudaStream_t st = ctx ? ctx->stream : nullptr;
-  for (void* p : {(void*)ex_mirror, (void*)ex_mirror8, (void*)vectors, (void*)mean, (void*)basis, (void*)proj, (void*)proj_soa, (void*)perm, (void*)tree.centroid, (void*)tree.radius, (void*)tree.first_child, (void*)tree.n_children, (void*)tree.leaf_start, (void*)tree.leaf_count, (void*)tree.centroid32, (void*)tree.radius32, (void*)tree.cnorm32, (void*)proj32_q4, (void*)tree.centroid32T, (void*)tree.boxlo, (void*)tree.boxhi, (void*)tree.meta, (void*)tree.tie, (void*)pnorm32, (void*)ex_hist, (void*)brute_op, (void*)brute_n2, (void*)brute_nup, (void*)brute_mu, (void*)brute_tmax})
+  for (void* p : {(void*)ex_mirror, (void*)ex_mirror8, (void*)vectors, (void*)mean, (void*)basis, (void*)proj, (void*)proj_soa, (void*)perm, (void*)tree.centroid, (void*)tree.radius, (void*)tree.first_child, (void*)tree.n_children, (void*)tree.leaf_start, (void*)tree.leaf_count, (void*)tree.centroid32, (void*)tree.radius32, (void*)tree.cnorm32, (void*)proj32_q4, (void*)tree.centroid32T, (void*)tree.boxlo, (void*)tree.boxhi, (void*)tree.meta, (void*)tree.tie, (void*)pnorm32, (void*)ex_hist, (void*)brute_op, (void*)brute_n2, (void*)brute_nup, (void*)brute_mu, (void*)brute_tmax, (void*)tc_b, (void*)tc_bmu, (void*)tc_err})
     if (p) cudaFreeAsync(p, st);
 }
 
@@ -378,6 +378,8 @@ void finish_index(psg_ctx* ctx, Index& ix, const double* mean, const double* bas
   ix.basis = dalloc<double>(bt.size());
   PSG_CUDA(cudaMemcpyAsync(ix.basis, bt.data(), sizeof(double) * bt.size(), cudaMemcpyHostToDevice,
                            ctx->stream));
+  // the E-step's tensor-core projection operand (window indexes)
+  if (!ix.from_vectors && d > 0) tc_prepare(ctx, ix);
   // project the database (pca.cpp:103-113)
   ix.proj = dalloc<double>((size_t)ix.N * (d > 0 ? d : 1));
   if (d > 0) {
@@ -493,6 +495,14 @@ struct psg_level {
   psg::DBuf<unsigned long long> counts;
   psg::DBuf<double> out_mass, excess, ex_hist, stats_dev, pen_table;
   psg::DBuf<int32_t> tile_order;
+  // tensor-core projection (kernels_project_tc.cu): digit mirror, per-query
+  // error bands, ambiguous-query list and the exact fallback's compact buffers
+  psg::DBuf<uint8_t> q8;
+  psg::DBuf<int> q8_bad, amb_n;
+  psg::DBuf<float> qdelta;
+  psg::DBuf<int32_t> amb, seed_c, idx_c;
+  psg::DBuf<double> q_ex, d2_c;
+  psg::DBuf<int64_t> sc_c, ex_c;
   // one EM iteration captured as a CUDA graph per cur/next parity (level_step)
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
   double* stats_host = nullptr;  // pinned [8]
@@ -701,8 +711,33 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
     L.unique_queries += L.Ao;
     return;
   }
-  if (ix.d > 0)
+  // exact budget on the tile kernel: tensor-core projection with an error
+  // band + exact fallback for the ambiguous queries (kernels_project_tc.cu)
+  const bool tc = ix.tc && ix.d > 0 && L.cfg.budget.mode == PSG_EXACT &&
+                  !ctx->knobs.exact_projection && search_uses_tiles(ctx, ix.tree, ix.d, true);
+  const int64_t q8_slice = (int64_t)L.W * L.Hl * 8;
+  if (tc) {
+    if (!L.q8.p) {
+      L.q8.alloc((size_t)3 * q8_slice);
+      L.q8_bad.alloc(1);
+      L.amb_n.alloc(1);
+      L.qdelta.alloc((size_t)L.Ao);
+      L.amb.alloc((size_t)L.Ao);
+      L.seed_c.alloc((size_t)L.Ao);
+      L.idx_c.alloc((size_t)L.Ao);
+      L.q_ex.alloc((size_t)L.Ao * ix.d);
+      L.d2_c.alloc((size_t)L.Ao);
+      L.sc_c.alloc((size_t)L.Ao);
+      L.ex_c.alloc((size_t)L.Ao);
+    }
+    PSG_CUDA(cudaMemsetAsync(L.q8_bad.p, 0, sizeof(int), ctx->stream));
+    PSG_CUDA(cudaMemsetAsync(L.amb_n.p, 0, sizeof(int), ctx->stream));
+    launch_make_digits(ctx, L.mirror.p, L.C, L.W, L.Hl, L.q8.p, q8_slice, L.q8_bad.p);
+    launch_project_windows_tc(ctx, L.q8.p, q8_slice, L.W, L.q8_bad.p, as, ix, L.qproj.p,
+                              L.qdelta.p);
+  } else if (ix.d > 0) {
     launch_project_windows(ctx, L.mirror.p, L.W, L.C, L.w, as, ix.mean, ix.basis, ix.d, L.qproj.p);
+  }
   SearchArgs a{};
   a.q = L.qproj.p;
   a.nq = L.Ao;
@@ -743,6 +778,7 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
     g.out_idx = greedy_seed.p;
     g.out_exact = nullptr;
     g.out_visited = nullptr;
+    g.qdelta = nullptr;
     launch_search(ctx, g);
     a.seed_idx = greedy_seed.p;
   }
@@ -765,7 +801,36 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
     }
     a.tile_order = order.p;
   }
+  if (tc) {
+    a.qdelta = L.qdelta.p;
+    a.amb_list = L.amb.p;
+    a.amb_count = L.amb_n.p;
+  }
   launch_search(ctx, a);
+  if (tc) {
+    // queries whose winner is not separated by their band: the reference's
+    // exact projection chain, then an exact search seeded with the band winner
+    launch_project_list(ctx, L.mirror.p, L.W, L.C, L.w, as, L.amb.p, L.amb_n.p, ix, L.q_ex.p);
+    launch_list_gather_i32(ctx, out_idx + L.off, L.amb.p, L.amb_n.p, L.seed_c.p);
+    SearchArgs f = a;
+    f.q = L.q_ex.p;
+    f.nq_dev = L.amb_n.p;
+    f.qxs = nullptr;
+    f.qys = nullptr;
+    f.seed_idx = L.seed_c.p;
+    f.out_idx = L.idx_c.p;
+    f.out_d2 = L.d2_c.p;
+    f.out_scanned = L.sc_c.p;
+    f.out_exact = L.ex_c.p;
+    f.out_visited = nullptr;
+    f.qdelta = nullptr;
+    f.amb_list = nullptr;
+    f.amb_count = nullptr;
+    f.tile_order = nullptr;
+    launch_search(ctx, f);
+    launch_list_scatter(ctx, L.amb.p, L.amb_n.p, L.idx_c.p, L.sc_c.p, L.ex_c.p, out_idx + L.off,
+                        L.scanned.p, L.exact_evals.p);
+  }
   L.scanned_valid = true;
   if (seed_dist_ready) PSG_CUDA(cudaStreamWaitEvent(ctx->stream, seed_dist_ready, 0));
   launch_rescore_windows(ctx, L.mirror.p, L.W, L.C, L.w, as, ix, out_idx + L.off,
@@ -1134,6 +1199,7 @@ psg_status psg_ctx_create(int device, void* stream, psg_ctx** out) {
       kn.project_kpt2 = on("PERSYN_PROJECT_KPT2");
       kn.no_carry = on("PERSYN_NO_CARRY");
       kn.eig_direct = on("PERSYN_EIG");
+      kn.exact_projection = on("PERSYN_EXACT_PROJECTION");
     }
     if (stream) {
       c->stream = static_cast<cudaStream_t>(stream);

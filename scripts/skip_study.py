@@ -5,6 +5,9 @@ at a time; after each, project every anchor's window in fp64 (torch) and find
 its exact two nearest database points in PCA space.  Report the movement
 delta = |q_t - q_ref| against the gap sqrt(d2) - sqrt(d1), and the fraction of
 anchors for which d(q_t, p*) < sqrt(sec_ref) - delta (a skip is provable).
+Also simulates Verlet-style candidate lists: at a (re)build the list holds every
+point within d1 + 2m of q_ref; while |q - q_ref| <= m the nearest point of q is
+provably in the list.  Reports rebuild fractions and list sizes per margin m.
 Study only: nothing here is product code.
 """
 import sys
@@ -52,24 +55,48 @@ def main(iters=10, hist=True):
         win = win.permute(1, 2, 3, 4, 0).reshape(len(ys) * len(xs), -1)
         return (win.double() - mean_t) @ basis_t.T
 
-    def top2(q):
-        out_d, out_i = [], []
+    Pf = P.float()
+    pnf = pn.float()
+    margins = [0.02, 0.05, 0.1, 0.2]
+
+    def top2(q, refd1=None):
+        out_d, out_i, cnt = [], [], []
         for s in range(0, q.shape[0], 4096):
             qq = q[s:s + 4096]
             d2 = (qq * qq).sum(1, keepdim=True) + pn[None] - 2.0 * qq @ P.T
             v, i = torch.topk(d2, 2, largest=False)
             out_d.append(v.clamp_min(0))
             out_i.append(i)
-        return torch.cat(out_d), torch.cat(out_i)
+            # list sizes: points within (d1 + 2m)
+            qf = qq.float()
+            d2f = ((qf * qf).sum(1, keepdim=True) + pnf[None] - 2.0 * qf @ Pf.T).clamp_min(0)
+            r1 = v[:, 0].clamp_min(0).sqrt().float()
+            cnt.append(torch.stack([(d2f <= ((r1 + 2 * m) ** 2)[:, None]).sum(1)
+                                    for m in margins], 1))
+        return torch.cat(out_d), torch.cat(out_i), torch.cat(cnt)
 
     ref_q = ref_sec = ref_id = None
     prev_q = None
+    vq = [None] * len(margins)  # Verlet reference queries per margin
+    vcnt = [None] * len(margins)
     for t in range(iters + 1):
         if t > 0:
             L.iterate(1)
         planes, idx, _ = L.download()
         q = queries(planes)
-        d, i = top2(q)
+        d, i, cnt = top2(q)
+        vl = []
+        for k, m in enumerate(margins):
+            if vq[k] is None:
+                vq[k], vcnt[k] = q.clone(), cnt[:, k].clone()
+                vl.append("init")
+                continue
+            rebuild = (q - vq[k]).norm(dim=1) > m
+            vq[k] = torch.where(rebuild[:, None], q, vq[k])
+            vcnt[k] = torch.where(rebuild, cnt[:, k], vcnt[k])
+            vl.append(f"m={m}: rebuild {rebuild.float().mean().item():.3f} "
+                      f"list mean {vcnt[k].float().mean().item():.1f} "
+                      f"p90 {torch.quantile(vcnt[k][:200000].float(), 0.9).item():.0f}")
         lib_idx = torch.tensor(idx, device="cuda")
         agree = (lib_idx == i[:, 0]).float().mean().item()
         line = f"it {t}: top1 agrees with library {agree:.5f}"
@@ -94,6 +121,7 @@ def main(iters=10, hist=True):
             ref_q, ref_sec, ref_id = q.clone(), d[:, 1].clone(), i[:, 0].clone()
         prev_q = q
         print(line, flush=True)
+        print("    verlet: " + " | ".join(vl), flush=True)
 
 
 if __name__ == "__main__":
