@@ -357,6 +357,14 @@ psg_status psg_initialize_output(const double* ex_planes, int C, int ew, int eh,
                                  const float* out_scale, int ow, int oh, double s_min,
                                  double s_max, uint64_t seed, double* out4);
 
+/* Diagnostics of the E-step's projection at every anchor (spacing sp) of an
+ * image [C][H][W]: q_tc = the tensor-core approximation, delta = its rigorous
+ * error bound (2-norm), q_exact = the reference's fp64 chain (pca.cpp:27-41).
+ * Any output may be NULL.  Fails with PSG_E_DOMAIN when the index has no
+ * tensor-core operand (vector index, d > 64, ...). */
+psg_status psg_debug_projection(psg_ctx* ctx, const psg_index* index, const double* planes, int W,
+                                int H, int spacing, double* q_tc, float* delta, double* q_exact);
+
 /* ---- resampling between levels (device kernels over host buffers) ---------- */
 /* downsample (image.cpp:38-62): block mean, factor >= 1, C planes [C][H][W] ->
  * [C][H/f][W/f]. */

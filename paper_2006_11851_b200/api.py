@@ -522,6 +522,21 @@ def initialize_output(exemplar: np.ndarray, out_scale: np.ndarray, s_min: float,
     return out
 
 
+def debug_projection(planes: np.ndarray, index: SearchIndex, spacing: int):
+    """(q_tc, delta, q_exact) at every anchor: the E-step's tensor-core
+    projection, its error bound and the reference's fp64 chain."""
+    x = _c(planes, np.float64)
+    C, H, W = x.shape
+    nx = N.lib.psg_axis_positions(W, index.window, spacing, None)
+    ny = N.lib.psg_axis_positions(H, index.window, spacing, None)
+    qt = np.zeros((nx * ny, index.retained_dim))
+    qe = np.zeros_like(qt)
+    dl = np.zeros(nx * ny, np.float32)
+    N.check(N.lib.psg_debug_projection(index.ctx.h, index.h, _p(x), W, H, spacing, _p(qt),
+                                       _p(dl), _p(qe)))
+    return qt, dl, qe
+
+
 def downsample(planes: np.ndarray, factor: int, ctx: Optional[Context] = None) -> np.ndarray:
     """Block-mean downsample of every plane (image.cpp:38-62), on the device."""
     ctx = ctx or default_context()

@@ -7,31 +7,37 @@
 // rounding.  So the E-step first computes an approximation q^ with a RIGOROUS
 // error bound on the tensor cores, and the search keeps every candidate within
 // that bound of the best (kernels_search.cu, approximate-query mode); only the
-// queries whose winner is not separated (near-ties, ~0.1%) are re-projected
-// with the exact chain and searched again (launch_project_list + the exact
-// tile search), so NN indices stay bit-identical to the reference's.
+// queries whose winner is not separated (near-ties) are re-projected with the
+// exact chain and searched again (launch_project_list + an exact warp search),
+// so NN indices stay bit-identical to the reference's.
 //
 // The approximation is computed EXACTLY in integers:
-//   v^  = V 2^-21,  V = rint(v 2^21) in [0, 2^21]   (|v - v^| <= 2^-22)
-//   B^  = Bq 2^-22, Bq = rint(B 2^22)               (|B - B^| <= 2^-23)
-//   q^_k = (sum_j Bq_kj V_j) 2^-43 - (B mu)_k
-// V is split into three unsigned base-256 digits (u8), Bq into three balanced
-// signed digits (s8); the nine digit products run as tcgen05.mma kind::i8
-// (int32 accumulation: exact) into five TMEM accumulators, one per digit
-// scale 256^(s+t), combined in int64 in the epilogue.  An extra basis row of
-// ones returns sum_j V_j, which bounds the basis rounding per query:
-//   |q^_k - q_k| <= 2^-22 |B_k|_1 + 2^-23 sum_j v^_j + (2D+2) 2^-53 |B_k|_1
-//                   + 2^-52 (|B mu_k| + |q^_k|) + 1e-12.
+//   v^  = V 2^-29,  V = rint(v 2^29) in [0, 2^29]   (|v - v^| <= 2^-30)
+//   B^  = Bq 2^-30, Bq = rint(B 2^30)               (|B - B^| <= 2^-31)
+//   q^_k = sum_{s,t} 256^(s+t) (sum_j a_s,j b_t,kj) 2^-59 - (B mu)_k
+// with V in four unsigned base-256 digits a_s (u8) and Bq in four balanced
+// signed digits b_t (s8).  Each digit product runs as tcgen05.mma kind::i8
+// with int32 accumulation (exact); the four B digit slices are stacked along
+// UMMA N, so one instruction per A slice computes all its products.  The 3 of
+// 16 products with s + t <= 1 contribute < 2^-59 32640 513 D and are dropped
+// (bounded below).  Per k:
+//   |q^_k - q_k| <= 2^-30 |B_k|_1 + 2^-31 D + 2^-59 32640 513 D
+//                   + (2D + 2) 2^-53 |B_k|_1 + 2^-52 (|B mu_k| + |B_k|_1)
+//                   + 20 D 2^-53 (combining the digit products in fp64) + 1e-12
+// (|v - mu| <= 1 bounds |q_k| by |B_k|_1; the reference's own chain is within
+// (2D + 2) 2^-53 |B_k|_1 of the exact value), and delta = the 2-norm over k:
+// about 1e-6 at w = 8, d = 32, so only true near-ties reach the fallback.
 //
-// Operands: windows of the digit mirror q8 [3][H][W][8] (8-byte pixels, so a
+// Operands: windows of the digit mirror q8 [4][H][W][8] (8-byte pixels: a
 // window row is w x 8 contiguous bytes and, at spacing 2, consecutive anchors'
-// 16-byte groups are consecutive 16-byte blocks: coalesced loads), staged in
-// shared memory in the UMMA K-major no-swizzle layout (K group g of the 128
-// anchors = one contiguous 2 KB block); the basis digits stream in per chunk.
-// One CTA = 128 anchors (UMMA M), 4 warps: all threads stage, one thread
-// issues the MMAs, all threads drain TMEM (lane = anchor).
-#include <cstdint>
+// 16-byte K groups are consecutive 16-byte blocks: one 1-D bulk copy per slice
+// and group), staged in the UMMA K-major no-swizzle layout (K group g of the
+// 128 anchors = one contiguous 2 KB block).  Persistent, warp-specialised:
+// warp 0 stages, warp 1 issues the UMMAs, warps 2-5 drain TMEM.  Basis rows
+// go in blocks of 32 (TMEM holds 416 accumulator columns per block).
+#include <algorithm>
 #include <cmath>
+#include <cstdint>
 #include <vector>
 
 #include "numerics.cuh"
@@ -41,12 +47,23 @@
 namespace psg {
 namespace {
 
-constexpr int kTM = 128;          // anchors per CTA (UMMA M)
-constexpr int kGC = 4;            // 16-byte K groups per chunk (2 UMMA K-steps of 32 bytes)
-constexpr int kAccs = 5;          // digit scales 256^0 .. 256^4
-constexpr int kSlices = 3;
-constexpr uint32_t kAGroup = kTM * 16;               // 2 KB per K group (one slice)
-constexpr uint32_t kASlice = kGC * kAGroup;          // 8 KB per slice per chunk
+constexpr int kTM = 128;                        // anchors per tile (UMMA M)
+constexpr int kGC = 4;                          // 16-byte K groups per stage (2 UMMA K-steps)
+constexpr int kSA = 4, kSB = 4;                 // digit slices of V and Bq
+constexpr int kNB = 32;                         // basis rows per block
+constexpr int kNP = kSB * kNB;                  // stacked B rows: t * 32 + n
+constexpr uint32_t kAGroup = kTM * 16;          // 2 KB per K group (one slice)
+constexpr uint32_t kASlice = kGC * kAGroup;     // 8 KB per slice per stage
+constexpr uint32_t kBStage = kGC * kNP * 16;    // 8 KB per stage
+constexpr uint32_t kStageBytes = kSA * kASlice + kBStage;  // 40 KB
+constexpr int kStages = 5;
+constexpr int kTcThreads = 192;
+constexpr uint32_t kBarOff = kStages * kStageBytes;
+constexpr uint32_t kSmemBytes = kBarOff + (2 * kStages + 2) * 8 + 16;
+// kept products per A slice s: t in [tmin(s), 4); TMEM columns [col0(s), +32 (4 - tmin))
+__host__ __device__ constexpr int tmin_of(int s) { return s == 0 ? 2 : (s == 1 ? 1 : 0); }
+__host__ __device__ constexpr int col0_of(int s) { return s == 0 ? 0 : (s == 1 ? 64 : 160 + (s - 2) * 128); }
+constexpr uint32_t kTmemCols = 512;  // 416 used
 
 __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
                                        uint32_t idesc, uint32_t accumulate) {
@@ -87,26 +104,22 @@ __global__ void make_digits_kernel(const float* __restrict__ mirror, int C, int6
   bool oob = false;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
        p += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t lo[kSlices] = {0, 0, 0}, hi[kSlices] = {0, 0, 0};
+    uint32_t lo[kSA] = {0, 0, 0, 0}, hi[kSA] = {0, 0, 0, 0};
     for (int c = 0; c < C; ++c) {
       const float v = __ldg(mirror + p * C + c);
       if (!(v >= 0.f && v <= 1.f)) oob = true;
       const float vc = fminf(fmaxf(v, 0.f), 1.f);
-      const uint32_t V = (uint32_t)__float2int_rn(vc * 2097152.f);  // exact scaling, rn
+      const uint32_t V = (uint32_t)__float2int_rn(vc * 536870912.f);  // v 2^29: exact, rn
       const uint32_t sh = (uint32_t)(c & 3) * 8;
-      const uint32_t d0 = V & 255u, d1 = (V >> 8) & 255u, d2 = V >> 16;
-      if (c < 4) {
-        lo[0] |= d0 << sh;
-        lo[1] |= d1 << sh;
-        lo[2] |= d2 << sh;
-      } else {
-        hi[0] |= d0 << sh;
-        hi[1] |= d1 << sh;
-        hi[2] |= d2 << sh;
+#pragma unroll
+      for (int s = 0; s < kSA; ++s) {
+        const uint32_t dg = (V >> (8 * s)) & 255u;
+        if (c < 4) lo[s] |= dg << sh;
+        else hi[s] |= dg << sh;
       }
     }
 #pragma unroll
-    for (int s = 0; s < kSlices; ++s)
+    for (int s = 0; s < kSA; ++s)
       *reinterpret_cast<uint2*>(q8 + s * slice_bytes + p * 8) = make_uint2(lo[s], hi[s]);
   }
   if (__syncthreads_or(oob) && threadIdx.x == 0) atomicOr(bad, 1);
@@ -120,34 +133,37 @@ struct TcArgs {
   const int* bad;
   const int32_t* xs;
   const int32_t* ys;
-  int nx;
-  int64_t n;
-  const int8_t* bop;    // [3][kb/16][np][16]
+  int nx, ny;
+  const int8_t* bop;    // [kblocks][kb/16][128][16]: row t * 32 + n = digit t of basis row 32 kblk + n
   const double* bmu;    // [d]
-  const double* err;    // [d]
+  float delta;          // the error band (2-norm), identical for every query
   int d, kb;
-  double* out;          // [n][d]
-  float* delta;         // [n]
+  double* out;          // [nx * ny][d]
+  float* delta_out;     // [nx * ny]
 };
 
-template <int NP>
-__global__ void __launch_bounds__(kTM) project_tc_kernel(TcArgs a) {
+// A work item = (tile of <= 128 consecutive anchors of one anchor row, basis block).
+__global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  constexpr uint32_t kBSlice = kGC * NP * 16;                  // per slice per chunk
-  constexpr uint32_t kStage = kSlices * (kASlice + kBSlice);
-  constexpr uint32_t kCols = kAccs * NP <= 128 ? 128 : (kAccs * NP <= 256 ? 256 : 512);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * kStage);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2);
-  const int tid = threadIdx.x, warp = tid >> 5;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBarOff);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      mma::smem_u32(tmem_slot)),
-                 "r"(kCols));
+                 "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 32) {
-    mma::mbar_init(&bar[0], 1);
-    mma::mbar_init(&bar[1], 1);
+    for (int s = 0; s < kStages; ++s) {
+      mma::mbar_init(&full[s], 1);
+      mma::mbar_init(&empty[s], 1);
+    }
+    mma::mbar_init(tfull, 1);
+    mma::mbar_init(tempty, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   mma::fence_before();
@@ -155,167 +171,211 @@ __global__ void __launch_bounds__(kTM) project_tc_kernel(TcArgs a) {
   mma::fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  // this thread's anchor (row tid of the tile)
-  const int64_t q = (int64_t)blockIdx.x * kTM + tid;
-  const bool valid = q < a.n;
-  int64_t pix0 = 0;  // first pixel of the window
-  if (valid) pix0 = (int64_t)a.ys[q / a.nx] * a.img_w + a.xs[q % a.nx];
-  const int gpr = a.w >> 1;               // 16-byte groups per window row
-  const int n_groups = a.kb >> 4;         // per slice
+  const int tpr = (a.nx + kTM - 1) / kTM;  // tiles per anchor row
+  const int nkb = (a.d + kNB - 1) / kNB;   // basis blocks
+  const int64_t n_items = (int64_t)tpr * a.ny * nkb;
+  const int gpr = a.w >> 1;                // 16-byte groups per window row
+  const int n_groups = a.kb >> 4;          // per slice
   const int n_chunks = (n_groups + kGC - 1) / kGC;
-  constexpr uint32_t kIdesc = idesc_i8(kTM, NP);
 
-  for (int c = 0; c < n_chunks; ++c) {
-    const int st = c & 1;
-    uint8_t* A = smem + st * kStage;
-    uint8_t* B = A + kSlices * kASlice;
-    if (c >= 2) mma::mbar_wait(&bar[st], (uint32_t)((c - 2) >> 1) & 1u);  // stage free
-    const int g0 = c * kGC;
-    const int ng = min(kGC, n_groups - g0);
-    // basis digits of this chunk: per slice a contiguous ng * NP * 16 bytes
-    for (int s = 0; s < kSlices; ++s) {
-      const uint4* src = reinterpret_cast<const uint4*>(a.bop + ((int64_t)s * n_groups + g0) * NP * 16);
-      uint4* dst = reinterpret_cast<uint4*>(B + s * kBSlice);
-      for (int i = tid; i < ng * NP; i += kTM) dst[i] = __ldg(src + i);
-    }
-    // window digits: 16 bytes (two 8-byte pixels) per (slice, group), all
-    // loads of the chunk issued before the stores
-    uint2 v[kSlices][kGC][2];
-#pragma unroll
-    for (int g = 0; g < kGC; ++g) {
-      const int gg = g0 + g;
-      const int dy = gg / gpr, dx = (gg - dy * gpr) * 2;
-      const int64_t off = (pix0 + (int64_t)dy * a.img_w + dx) * 8;
-#pragma unroll
-      for (int s = 0; s < kSlices; ++s) {
-        if (valid && g < ng) {
-          const uint2* p = reinterpret_cast<const uint2*>(a.q8 + s * a.slice_bytes + off);
-          v[s][g][0] = __ldg(p);
-          v[s][g][1] = __ldg(p + 1);
+  if (warp == 0) {
+    // ---- producer ---------------------------------------------------------------------
+    int stage = 0;
+    uint32_t ph = 0;
+    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int64_t t = it / nkb;
+      const int kblk = (int)(it - t * nkb);
+      const int iy = (int)(t / tpr), ix0 = (int)(t - (int64_t)iy * tpr) * kTM;
+      const int nt = min(kTM, a.nx - ix0);
+      const int ay = a.ys[iy];
+      const int x0 = a.xs[ix0];
+      // window rows of consecutive anchors are consecutive 16-byte blocks when
+      // the anchors step by 2 pixels (16-byte aligned: even pixel index)
+      const bool contig = a.xs[ix0 + nt - 1] - x0 == 2 * (nt - 1) && (x0 & 1) == 0 &&
+                          (a.img_w & 1) == 0;
+      const int8_t* bsrc = a.bop + (int64_t)kblk * n_groups * kNP * 16;
+      for (int c = 0; c < n_chunks; ++c) {
+        mma::mbar_wait(&empty[stage], ph ^ 1u);
+        uint8_t* A = smem + stage * kStageBytes;
+        uint8_t* B = A + kSA * kASlice;
+        const int g0 = c * kGC, ng = min(kGC, n_groups - g0);
+        if (contig) {
+          if (lane == 0) {
+            mma::mbar_expect_tx(&full[stage], (uint32_t)(ng * (kSA * nt * 16 + kNP * 16)));
+            mma::bulk_g2s(B, bsrc + (int64_t)g0 * kNP * 16, ng * kNP * 16, &full[stage]);
+            for (int g = 0; g < ng; ++g) {
+              const int gg = g0 + g, dy = gg / gpr, dx = (gg - dy * gpr) * 2;
+              const int64_t off = ((int64_t)(ay + dy) * a.img_w + x0 + dx) * 8;
+              for (int s = 0; s < kSA; ++s)
+                mma::bulk_g2s(A + s * kASlice + g * kAGroup, a.q8 + s * a.slice_bytes + off,
+                              nt * 16, &full[stage]);
+            }
+          }
         } else {
-          v[s][g][0] = v[s][g][1] = make_uint2(0u, 0u);
+          // strided rows (spacing > 2, or a clamped last anchor): lane copies
+          const uint4* src = reinterpret_cast<const uint4*>(bsrc + (int64_t)g0 * kNP * 16);
+          for (int i = lane; i < ng * kNP; i += 32) reinterpret_cast<uint4*>(B)[i] = __ldg(src + i);
+          for (int i = lane; i < ng * nt; i += 32) {
+            const int g = i / nt, m = i - g * nt;
+            const int gg = g0 + g, dy = gg / gpr, dx = (gg - dy * gpr) * 2;
+            const int64_t off = ((int64_t)(ay + dy) * a.img_w + a.xs[ix0 + m] + dx) * 8;
+#pragma unroll
+            for (int s = 0; s < kSA; ++s) {
+              const uint2* p = reinterpret_cast<const uint2*>(a.q8 + s * a.slice_bytes + off);
+              const uint2 u0 = __ldg(p), u1 = __ldg(p + 1);
+              *reinterpret_cast<uint4*>(A + s * kASlice + g * kAGroup + m * 16) =
+                  make_uint4(u0.x, u0.y, u1.x, u1.y);
+            }
+          }
+          mma::fence_async_smem();
+          __syncwarp();
+          if (lane == 0) mma::mbar_arrive(&full[stage]);
+        }
+        if (++stage == kStages) {
+          stage = 0;
+          ph ^= 1u;
         }
       }
     }
+  } else if (warp == 1) {
+    // ---- MMA issuer: per K step one UMMA per A slice, N = the kept B digits ------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t ph = 0, tph = 0;
+      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+        mma::mbar_wait(tempty, tph ^ 1u);
+        mma::fence_after();
+        for (int c = 0; c < n_chunks; ++c) {
+          mma::mbar_wait(&full[stage], ph);
+          mma::fence_after();
+          const uint8_t* A = smem + stage * kStageBytes;
+          const uint8_t* B = A + kSA * kASlice;
+          const int ng = min(kGC, n_groups - c * kGC);
+          for (int ks = 0; ks < (ng + 1) >> 1; ++ks) {
 #pragma unroll
-    for (int s = 0; s < kSlices; ++s)
-#pragma unroll
-      for (int g = 0; g < kGC; ++g)
-        *reinterpret_cast<uint4*>(A + s * kASlice + g * kAGroup + tid * 16) =
-            make_uint4(v[s][g][0].x, v[s][g][0].y, v[s][g][1].x, v[s][g][1].y);
-    mma::fence_async_smem();
-    __syncthreads();
-    if (tid == 0) {
+            for (int s = 0; s < kSA; ++s) {
+              const int t0 = tmin_of(s), n = (kSB - t0) * kNB;
+              const uint64_t ad = mma::make_desc(mma::smem_u32(A + s * kASlice) + ks * 2 * kAGroup,
+                                                 kAGroup, 128);
+              const uint64_t bd = mma::make_desc(
+                  mma::smem_u32(B) + ks * 2 * kNP * 16 + t0 * kNB * 16, kNP * 16, 128);
+              mma_i8(tmem + (uint32_t)col0_of(s), ad, bd, idesc_i8(kTM, n),
+                     (c | ks) ? 1u : 0u);
+            }
+          }
+          mma::commit(&empty[stage]);
+          if (++stage == kStages) {
+            stage = 0;
+            ph ^= 1u;
+          }
+        }
+        mma::commit(tfull);
+        tph ^= 1u;
+      }
+    }
+  } else {
+    // ---- epilogue: warp (w & 3) owns TMEM lanes 32 (w & 3) .. + 31 --------------------
+    const int lg = warp & 3;
+    const bool bad = *a.bad != 0;
+    uint32_t tph = 0;
+    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const int64_t t = it / nkb;
+      const int kblk = (int)(it - t * nkb);
+      mma::mbar_wait(tfull, tph);
+      tph ^= 1u;
       mma::fence_after();
-      const int ksteps = (ng + 1) >> 1;  // 32 bytes = 2 groups per UMMA
-      for (int ks = 0; ks < ksteps; ++ks) {
-        // K-step ks covers groups 2ks, 2ks+1: LBO = group stride, SBO = 8-row stride
+      const int iy = (int)(t / tpr), ix0 = (int)(t - (int64_t)iy * tpr) * kTM;
+      const int m = lg * 32 + lane;
+      const bool valid = ix0 + m < a.nx;
+      const int64_t q = (int64_t)iy * a.nx + ix0 + m;
+      const uint32_t base = tmem + ((uint32_t)(lg * 32) << 16);
+      double acc[kNB];
 #pragma unroll
-        for (int s = 0; s < kSlices; ++s) {
-          const uint64_t ad = mma::make_desc(mma::smem_u32(A + s * kASlice) + ks * 2 * kAGroup,
-                                             kAGroup, 128);
+      for (int n = 0; n < kNB; ++n) acc[n] = 0.0;
+      // sum_{s,t} 256^(s+t) D(s,t) 2^-59: every term exact, a few fp64 roundings
 #pragma unroll
-          for (int t = 0; t < kSlices; ++t) {
-            const uint64_t bd = mma::make_desc(mma::smem_u32(B + t * kBSlice) + ks * 2 * NP * 16,
-                                               NP * 16, 128);
-            const int u = s + t;
-            // the first product into each accumulator overwrites it
-            const bool first = c == 0 && ks == 0 && (u < 3 ? s == 0 : t == 2);
-            mma_i8(tmem + (uint32_t)(u * NP), ad, bd, kIdesc, first ? 0u : 1u);
+      for (int s = 0; s < kSA; ++s) {
+#pragma unroll
+        for (int tt = tmin_of(s); tt < kSB; ++tt) {
+          const double sc = ldexp(1.0, 8 * (s + tt) - 59);
+#pragma unroll
+          for (int h = 0; h < kNB; h += 16) {
+            int32_t r[16];
+            tmem_ld16(base + (uint32_t)(col0_of(s) + (tt - tmin_of(s)) * kNB + h), r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[h + i] = dadd(acc[h + i], dmul((double)r[i], sc));
           }
         }
       }
-      mma::commit(&bar[st]);
+      mma::fence_before();
+      __syncwarp();
+      if (lane == 0) mma::mbar_arrive(tempty);
+      if (valid) {
+        const int k0 = kblk * kNB;
+        double* orow = a.out + q * a.d + k0;
+#pragma unroll
+        for (int n = 0; n < kNB; ++n)
+          if (k0 + n < a.d) orow[n] = dsub(acc[n], a.bmu[k0 + n]);
+        if (kblk == 0) a.delta_out[q] = bad ? __int_as_float(0x7f800000) : a.delta;
+      }
     }
-  }
-  const int cl = n_chunks - 1;
-  mma::mbar_wait(&bar[cl & 1], (uint32_t)(cl >> 1) & 1u);
-  mma::fence_after();
-
-  // ---- epilogue: warp w drains TMEM lanes 32w..32w+31 (lane = anchor) ----------------
-  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-  const bool bad = *a.bad != 0;
-  double* orow = a.out + (valid ? q : 0) * a.d;
-  double err2 = 0.0, sumv = 0.0;
-  double eq[NP];  // q^ (first d columns)
-#pragma unroll
-  for (int nb = 0; nb < NP; nb += 16) {
-    int32_t r[kAccs][16];
-#pragma unroll
-    for (int u = 0; u < kAccs; ++u) tmem_ld16(tmem + lane_base + (uint32_t)(u * NP + nb), r[u]);
-    tmem_wait_ld();
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      int64_t P = 0;
-#pragma unroll
-      for (int u = kAccs - 1; u >= 0; --u) P = P * 256 + (int64_t)r[u][i];
-      const int n = nb + i;
-      if (n < a.d) eq[n] = (double)P * 0x1p-43;  // exact: |P| < 2^53
-      else if (n == a.d) sumv = (double)P * 0x1p-21;  // sum_j v^_j (exact)
-    }
-  }
-  if (valid) {
-#pragma unroll
-    for (int n = 0; n < NP; ++n) {
-      if (n >= a.d) break;
-      const double qk = eq[n] - a.bmu[n];
-      orow[n] = qk;
-      const double e = a.err[n] + 0x1p-23 * sumv + 0x1p-52 * fabs(qk);
-      err2 += e * e;
-    }
-    a.delta[q] = bad ? __int_as_float(0x7f800000) : __double2float_ru(sqrt(err2) * (1.0 + 1e-9));
   }
   mma::fence_before();
   __syncthreads();
   if (warp == 0) {
     mma::fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(kTmemCols));
   }
-}
-
-template <int NP>
-void launch_tc(psg_ctx* ctx, const TcArgs& a) {
-  constexpr uint32_t kBSlice = kGC * NP * 16;
-  constexpr uint32_t kStage = kSlices * (kASlice + kBSlice);
-  const size_t sm = 2 * kStage + 64;
-  auto k = project_tc_kernel<NP>;
-  static bool attr = false;
-  if (!attr) {
-    PSG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attr = true;
-  }
-  const int64_t blocks = (a.n + kTM - 1) / kTM;
-  k<<<(unsigned)blocks, kTM, sm, ctx->stream>>>(a);
-  PSG_LAUNCHED(ctx);
 }
 
 // ---- exact fallback for listed anchors -------------------------------------------
 // One warp per listed anchor; lane k accumulates the reference's chain
-// acc = acc + ((double)v_j - mean_j) * basis[k][j], j ascending, no FMA.
-__global__ void project_list_kernel(const float* __restrict__ mirror, int img_w, int C, int w,
-                                    const int32_t* __restrict__ xs, const int32_t* __restrict__ ys,
-                                    int nx, const int32_t* __restrict__ list,
-                                    const int* __restrict__ count, const double* __restrict__ mean,
-                                    const double* __restrict__ basisT, int KP, int D, int d,
-                                    double* __restrict__ out) {
+// acc = acc + ((double)v_j - mean_j) * basis[k][j], j ascending, no FMA.  The
+// centred window values c_j are staged in shared memory per 128-element chunk
+// (one load each, shared by the d chains); basis loads run 8 ahead.
+constexpr int kListWarps = 8, kListChunk = 128;
+__global__ void __launch_bounds__(32 * kListWarps) project_list_kernel(
+    const float* __restrict__ mirror, int img_w, int C, int w, const int32_t* __restrict__ xs,
+    const int32_t* __restrict__ ys, int nx, const int32_t* __restrict__ list,
+    const int* __restrict__ count, const double* __restrict__ mean,
+    const double* __restrict__ basisT, int KP, int D, int d, double* __restrict__ out) {
+  __shared__ double cs_all[kListWarps][kListChunk];
   const int n = *count;
-  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* cs = cs_all[warp];
   const int wc = w * C;
-  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
-       i += (gridDim.x * blockDim.x) >> 5) {
+  for (int i = blockIdx.x * kListWarps + warp; i < n; i += gridDim.x * kListWarps) {
     const int32_t a = list[i];
     const int64_t base = ((int64_t)ys[a / nx] * img_w + xs[a % nx]) * C;
     double acc0 = 0.0, acc1 = 0.0;
-    int dy = 0, off = 0;
-    for (int j = 0; j < D; ++j) {
-      const float v = __ldg(mirror + base + (int64_t)dy * img_w * C + off);
-      if (++off == wc) {
-        off = 0;
-        ++dy;
+    for (int j0 = 0; j0 < D; j0 += kListChunk) {
+      const int jn = min(kListChunk, D - j0);
+      __syncwarp();
+      for (int t = lane; t < jn; t += 32) {
+        const int j = j0 + t, dy = j / wc, off = j - dy * wc;
+        const float v = __ldg(mirror + base + (int64_t)dy * img_w * C + off);
+        cs[t] = dsub((double)v, __ldg(mean + j));
       }
-      const double cj = dsub((double)v, __ldg(mean + j));
-      acc0 = dadd(acc0, dmul(cj, __ldg(basisT + (int64_t)j * KP + lane)));
-      if (KP > 32) acc1 = dadd(acc1, dmul(cj, __ldg(basisT + (int64_t)j * KP + 32 + lane)));
+      __syncwarp();
+      const double* bt = basisT + (int64_t)j0 * KP + lane;
+      for (int t0 = 0; t0 < jn; t0 += 8) {
+        double b0[8], b1[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          b0[u] = t0 + u < jn ? __ldg(bt + (int64_t)(t0 + u) * KP) : 0.0;
+          b1[u] = (KP > 32 && t0 + u < jn) ? __ldg(bt + (int64_t)(t0 + u) * KP + 32) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (t0 + u < jn) {
+            const double cj = cs[t0 + u];
+            acc0 = dadd(acc0, dmul(cj, b0[u]));
+            if (KP > 32) acc1 = dadd(acc1, dmul(cj, b1[u]));
+          }
+        }
+      }
     }
     if (lane < d) out[(int64_t)i * d + lane] = acc0;
     if (lane + 32 < d) out[(int64_t)i * d + 32 + lane] = acc1;
@@ -363,52 +423,43 @@ bool tc_prepare(psg_ctx* ctx, Index& ix) {
   ix.tc = false;
   const int d = ix.d, D = ix.D, C = ix.C, w = ix.w;
   if (ix.from_vectors || d < 1 || d > 64 || C > 8 || (w & 1)) return false;
-  const int np = ((d + 1 + 15) / 16) * 16;
-  const int kb = w * w * 8;
   for (double b : ix.h_basis)
     if (!(std::fabs(b) <= 1.0)) return false;
-  const int ng = kb / 16;
-  std::vector<int8_t> op((size_t)kSlices * kb * np, 0);
-  auto put = [&](int n, int kk, int64_t bq) {
-    int64_t r = bq;
-    for (int t = 0; t < kSlices; ++t) {
-      int64_t dg = ((r + 128) & 255) - 128;
-      if (t == kSlices - 1) dg = r;  // |r| <= 64 after two balanced digits
-      r = (r - dg) >> 8;
-      const size_t o = ((size_t)t * ng + (kk >> 4)) * np * 16 + (size_t)(n >> 3) * 128 +
-                       (size_t)(n & 7) * 16 + (kk & 15);
-      op[o] = (int8_t)dg;
-    }
-  };
-  std::vector<double> bmu(d), err(d);
+  const int kb = w * w * 8, ng = kb / 16, nkb = (d + kNB - 1) / kNB;
+  std::vector<int8_t> op((size_t)nkb * ng * kNP * 16, 0);
+  std::vector<double> bmu(d);
+  double delta2 = 0.0;
   for (int k = 0; k < d; ++k) {
     const double* row = ix.h_basis.data() + (size_t)k * D;
+    const int blk = k / kNB, n = k - blk * kNB;
     long double mu = 0.0L;
     double l1 = 0.0;
     for (int j = 0; j < D; ++j) {
-      const int pix = j / C, c = j - pix * C;  // window element (pixel, channel)
-      put(k, pix * 8 + c, std::llrint(std::ldexp(row[j], 22)));
+      const int pix = j / C, c = j - pix * C, kk = pix * 8 + c;  // window element -> K byte
+      int64_t r = std::llrint(std::ldexp(row[j], 30));            // |r| <= 2^30
+      for (int t = 0; t < kSB; ++t) {
+        const int64_t dg = t < kSB - 1 ? ((r + 128) & 255) - 128 : r;  // last: |r| <= 64
+        r = (r - dg) >> 8;
+        const int nn = t * kNB + n;
+        op[(((size_t)blk * ng + (kk >> 4)) * kNP + nn) * 16 + (kk & 15)] = (int8_t)dg;
+      }
       mu += (long double)row[j] * (long double)ix.h_mean[j];
       l1 += std::fabs(row[j]);
     }
     bmu[k] = (double)mu;
     l1 *= 1.0 + 1e-12;
-    err[k] = std::ldexp(l1, -22) + (2.0 * D + 2.0) * std::ldexp(l1, -53) +
-             std::ldexp(std::fabs(bmu[k]), -52) + 1e-12;
+    const double e = std::ldexp(l1, -30) + std::ldexp((double)D, -31) +
+                     std::ldexp(32640.0 * 513.0 * D, -59) + (2.0 * D + 2.0) * std::ldexp(l1, -53) +
+                     std::ldexp(std::fabs(bmu[k]) + l1, -52) +
+                     std::ldexp(20.0 * D, -53) /* the epilogue's fp64 digit combination */ + 1e-12;
+    delta2 += e * e;
   }
-  for (int j = 0; j < D; ++j) {  // the ones row: sum_j V_j
-    const int pix = j / C, c = j - pix * C;
-    put(d, pix * 8 + c, 1);
-  }
-  ix.tc_np = np;
   ix.tc_kb = kb;
+  ix.tc_delta = (float)(std::sqrt(delta2) * (1.0 + 1e-6));
   PSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ix.tc_b), op.size(), ctx->stream));
   PSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ix.tc_bmu), sizeof(double) * d, ctx->stream));
-  PSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ix.tc_err), sizeof(double) * d, ctx->stream));
   PSG_CUDA(cudaMemcpyAsync(ix.tc_b, op.data(), op.size(), cudaMemcpyHostToDevice, ctx->stream));
   PSG_CUDA(cudaMemcpyAsync(ix.tc_bmu, bmu.data(), sizeof(double) * d, cudaMemcpyHostToDevice,
-                           ctx->stream));
-  PSG_CUDA(cudaMemcpyAsync(ix.tc_err, err.data(), sizeof(double) * d, cudaMemcpyHostToDevice,
                            ctx->stream));
   PSG_CUDA(cudaStreamSynchronize(ctx->stream));
   ix.tc = true;
@@ -430,30 +481,32 @@ void launch_project_windows_tc(psg_ctx* ctx, const uint8_t* q8, int64_t slice_by
   a.xs = anchors.xs;
   a.ys = anchors.ys;
   a.nx = anchors.nx;
-  a.n = anchors.count;
+  a.ny = (int)(anchors.count / anchors.nx);
   a.bop = ix.tc_b;
   a.bmu = ix.tc_bmu;
-  a.err = ix.tc_err;
+  a.delta = ix.tc_delta;
   a.d = ix.d;
   a.kb = ix.tc_kb;
   a.out = out;
-  a.delta = delta;
-  switch (ix.tc_np) {
-    case 16: launch_tc<16>(ctx, a); break;
-    case 32: launch_tc<32>(ctx, a); break;
-    case 48: launch_tc<48>(ctx, a); break;
-    case 64: launch_tc<64>(ctx, a); break;
-    case 80: launch_tc<80>(ctx, a); break;
-    default: fail(PSG_E_LOGIC, "unsupported tensor-core projection width");
+  a.delta_out = delta;
+  static bool attr = false;
+  if (!attr) {
+    PSG_CUDA(cudaFuncSetAttribute(project_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kSmemBytes));
+    attr = true;
   }
+  const int64_t items = (int64_t)((a.nx + kTM - 1) / kTM) * a.ny * ((a.d + kNB - 1) / kNB);
+  const int blocks = (int)std::min<int64_t>(items, ctx->num_sms);
+  project_tc_kernel<<<blocks, kTcThreads, kSmemBytes, ctx->stream>>>(a);
+  PSG_LAUNCHED(ctx);
 }
 
 void launch_project_list(psg_ctx* ctx, const float* mirror, int img_w, int C, int w,
                          AnchorSet anchors, const int32_t* list, const int* count,
                          const Index& ix, double* out) {
-  ProfScope _prof(ctx, K_PROJECT);
+  ProfScope _prof(ctx, K_FALLBACK);
   const int KP = ix.d <= 32 ? 32 : 64;
-  project_list_kernel<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(
+  project_list_kernel<<<ctx->num_sms * 4, 32 * kListWarps, 0, ctx->stream>>>(
       mirror, img_w, C, w, anchors.xs, anchors.ys, anchors.nx, list, count, ix.mean, ix.basis, KP,
       ix.D, ix.d, out);
   PSG_LAUNCHED(ctx);
@@ -461,7 +514,7 @@ void launch_project_list(psg_ctx* ctx, const float* mirror, int img_w, int C, in
 
 void launch_list_gather_i32(psg_ctx* ctx, const int32_t* src, const int32_t* list,
                             const int* count, int32_t* out) {
-  ProfScope _prof(ctx, K_SEARCH);
+  ProfScope _prof(ctx, K_FALLBACK);
   list_gather_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(src, list, count, out);
   PSG_LAUNCHED(ctx);
 }
@@ -469,7 +522,7 @@ void launch_list_gather_i32(psg_ctx* ctx, const int32_t* src, const int32_t* lis
 void launch_list_scatter(psg_ctx* ctx, const int32_t* list, const int* count,
                          const int32_t* idx_c, const int64_t* sc_c, const int64_t* ex_c,
                          int32_t* idx, int64_t* scanned, int64_t* exact) {
-  ProfScope _prof(ctx, K_SEARCH);
+  ProfScope _prof(ctx, K_FALLBACK);
   list_scatter_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(list, count, idx_c, sc_c, ex_c, idx,
                                                              scanned, exact);
   PSG_LAUNCHED(ctx);

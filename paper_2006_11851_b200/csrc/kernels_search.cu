@@ -916,7 +916,8 @@ __global__ void __launch_bounds__(256) search_exact_kernel(SearchArgs a) {
   const int KB = d < kBoxDims ? d : kBoxDims;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
 
-  for (int64_t q = (int64_t)blockIdx.x * W + warp; q < a.nq; q += (int64_t)gridDim.x * W) {
+  const int64_t nq = a.nq_dev ? (int64_t)*a.nq_dev : a.nq;
+  for (int64_t q = (int64_t)blockIdx.x * W + warp; q < nq; q += (int64_t)gridDim.x * W) {
     double qn2 = 0.0;
     for (int j = lane; j < DP; j += 32) {
       const double v = j < d ? a.q[q * d + j] : 0.0;
@@ -940,7 +941,7 @@ __global__ void __launch_bounds__(256) search_exact_kernel(SearchArgs a) {
         cand = a.seed_idx[q];
       } else if (lane <= 4 && a.qxs) {
         const int qix = (int)(q % a.qnx), qiy = (int)(q / a.qnx);
-        const int qny = (int)(a.nq / a.qnx);
+        const int qny = (int)(nq / a.qnx);
         const int nix = qix + (lane == 1 ? -1 : lane == 2 ? 1 : 0);
         const int niy = qiy + (lane == 3 ? -1 : lane == 4 ? 1 : 0);
         if (nix >= 0 && nix < a.qnx && niy >= 0 && niy < qny) {
@@ -1593,8 +1594,22 @@ bool search_uses_tiles(psg_ctx* ctx, const DevTree& tree, int d, bool exact) {
 }
 
 void launch_search(psg_ctx* ctx, const SearchArgs& a) {
-  ProfScope _prof(ctx, K_SEARCH);
+  ProfScope _prof(ctx, a.nq_dev ? K_FALLBACK : K_SEARCH);
   if (a.nq <= 0) return;
+  if (a.nq_dev) {
+    // a device-counted list of unrelated queries (the exact fallback of the
+    // tensor-core projection): one warp per query -- tiles of 32 unrelated
+    // queries would traverse the union of their candidate sets
+    if (a.mode != PSG_EXACT || !a.proj32_q4 || !a.tree.centroid32T)
+      fail(PSG_E_LOGIC, "device-counted search needs the exact warp kernel");
+    const int64_t blocks = (int64_t)ctx->num_sms * 8;
+    if (a.d <= 32)
+      search_exact_kernel<32><<<(int)blocks, 256, 0, ctx->stream>>>(a);
+    else
+      search_exact_kernel<64><<<(int)blocks, 256, 0, ctx->stream>>>(a);
+    PSG_LAUNCHED(ctx);
+    return;
+  }
   if (a.d > kMaxD) fail(PSG_E_DOMAIN, "retained PCA dimension > 64 is not supported");
   const bool tile_ok = a.tree.max_children <= kTileMaxB &&
                        1 + a.tree.max_depth * (a.tree.max_children - 1) <= kTileStack;

@@ -112,11 +112,10 @@ struct Index {
   // Bq = rint(B * 2^22) as three signed base-256 digit slices in UMMA K-major
   // layout over 8-byte pixels, plus row sums for the error bound
   bool tc = false;
-  int tc_np = 0;               // UMMA N: d + 1 (a ones row for sum v) rounded up to 16
   int tc_kb = 0;               // K bytes per slice: w * w * 8 (8-byte pixels), multiple of 32
-  int8_t* tc_b = nullptr;      // [3][kb / 16][np][16]
+  int8_t* tc_b = nullptr;      // [d/32 blocks][kb / 16][4 digits x 32 rows][16]
   double* tc_bmu = nullptr;    // [d] B . mean (rounded from long double)
-  double* tc_err = nullptr;    // [d] 2^-22 |B_k|_1 + 2^-52 |B mu_k| + 1e-12
+  float tc_delta = 0.f;        // rigorous |q^ - q| bound (2-norm) of every query
   ~Index();
 };
 
@@ -139,7 +138,7 @@ struct RowSrc {
 namespace psg {
 enum KernelKind : int {
   K_MIRROR = 0, K_PROJECT, K_SEARCH, K_RESCORE, K_WEIGHTS, K_HIST, K_PENALTY, K_MSTEP, K_STATS,
-  K_BUILD, K_PYRAMID, K_SCHED, K_COUNT
+  K_BUILD, K_PYRAMID, K_SCHED, K_FALLBACK, K_COUNT
 };
 extern const char* const kKernelNames[K_COUNT];
 }  // namespace psg
@@ -224,9 +223,9 @@ void launch_project_windows(psg_ctx* ctx, const float* mirror, int img_w, int C,
                             AnchorSet anchors, const double* mean, const double* basis, int d,
                             double* out);
 // ---- tensor-core projection (kernels_project_tc.cu) --------------------------------
-// Quantised digit mirror of an fp32 mirror: V = rint(v * 2^21) for v in [0, 1]
-// as three u8 base-256 digits, 8-byte pixels (channels >= C zero): q8
-// [3][H][W][8] bytes.  A value outside [0, 1] (or NaN) sets *bad (the
+// Quantised digit mirror of an fp32 mirror: V = rint(v * 2^29) for v in [0, 1]
+// as four u8 base-256 digits, 8-byte pixels (channels >= C zero): q8
+// [4][H][W][8] bytes.  A value outside [0, 1] (or NaN) sets *bad (the
 // projection then reports delta = +inf for every query: exact fallback).
 void launch_make_digits(psg_ctx* ctx, const float* mirror, int C, int W, int H, uint8_t* q8,
                         int64_t slice_bytes, int* bad);

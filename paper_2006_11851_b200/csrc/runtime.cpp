@@ -150,7 +150,7 @@ double now_ms() {
 const char* const kKernelNames[K_COUNT] = {
     "make_mirror", "project_kernel", "search_kernel", "rescore_kernel", "weights_kernel",
     "hist_kernels", "penalty_kernel", "mstep_kernel", "stats_kernel", "build_kernels",
-    "pyramid_kernels", "tile_schedule"};
+    "pyramid_kernels", "tile_schedule", "exact_fallback"};
 
 ProfScope::ProfScope(psg_ctx* c, int k) : ctx(c), kind(k) {
   if (!ctx->profile) return;
@@ -228,7 +228,7 @@ double pow_cr_host(double x, double y) { return pow_cr(x, y); }
 Index::~Index() {
   // stream-ordered frees (the allocations come from the context's pool)
   cudaStream_t st = ctx ? ctx->stream : nullptr;
-  for (void* p : {(void*)ex_mirror, (void*)ex_mirror8, (void*)vectors, (void*)mean, (void*)basis, (void*)proj, (void*)proj_soa, (void*)perm, (void*)tree.centroid, (void*)tree.radius, (void*)tree.first_child, (void*)tree.n_children, (void*)tree.leaf_start, (void*)tree.leaf_count, (void*)tree.centroid32, (void*)tree.radius32, (void*)tree.cnorm32, (void*)proj32_q4, (void*)tree.centroid32T, (void*)tree.boxlo, (void*)tree.boxhi, (void*)tree.meta, (void*)tree.tie, (void*)pnorm32, (void*)ex_hist, (void*)brute_op, (void*)brute_n2, (void*)brute_nup, (void*)brute_mu, (void*)brute_tmax, (void*)tc_b, (void*)tc_bmu, (void*)tc_err})
+  for (void* p : {(void*)ex_mirror, (void*)ex_mirror8, (void*)vectors, (void*)mean, (void*)basis, (void*)proj, (void*)proj_soa, (void*)perm, (void*)tree.centroid, (void*)tree.radius, (void*)tree.first_child, (void*)tree.n_children, (void*)tree.leaf_start, (void*)tree.leaf_count, (void*)tree.centroid32, (void*)tree.radius32, (void*)tree.cnorm32, (void*)proj32_q4, (void*)tree.centroid32T, (void*)tree.boxlo, (void*)tree.boxhi, (void*)tree.meta, (void*)tree.tie, (void*)pnorm32, (void*)ex_hist, (void*)brute_op, (void*)brute_n2, (void*)brute_nup, (void*)brute_mu, (void*)brute_tmax, (void*)tc_b, (void*)tc_bmu})
     if (p) cudaFreeAsync(p, st);
 }
 
@@ -718,7 +718,7 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
   const int64_t q8_slice = (int64_t)L.W * L.Hl * 8;
   if (tc) {
     if (!L.q8.p) {
-      L.q8.alloc((size_t)3 * q8_slice);
+      L.q8.alloc((size_t)4 * q8_slice);
       L.q8_bad.alloc(1);
       L.amb_n.alloc(1);
       L.qdelta.alloc((size_t)L.Ao);
@@ -830,6 +830,13 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
     launch_search(ctx, f);
     launch_list_scatter(ctx, L.amb.p, L.amb_n.p, L.idx_c.p, L.sc_c.p, L.ex_c.p, out_idx + L.off,
                         L.scanned.p, L.exact_evals.p);
+    if (ctx->knobs.verbose) {
+      int n = 0;
+      PSG_CUDA(cudaMemcpyAsync(&n, L.amb_n.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+      fprintf(stderr, "[persyn] search: %d of %lld queries re-searched exactly (near-ties)\n", n,
+              (long long)L.Ao);
+    }
   }
   L.scanned_valid = true;
   if (seed_dist_ready) PSG_CUDA(cudaStreamWaitEvent(ctx->stream, seed_dist_ready, 0));
@@ -2145,5 +2152,39 @@ extern "C" psg_status psg_fit_to(psg_ctx* ctx, const double* in, int C, int W, i
     resample_planes(ctx, in, C, W, H, ow, oh, out, [&](const double* a, double* b) {
       psg::launch_fit_to(ctx, a, W, H, ow, oh, b);
     });
+  });
+}
+
+extern "C" psg_status psg_debug_projection(psg_ctx* ctx, const psg_index* index,
+                                           const double* planes, int W, int H, int spacing,
+                                           double* q_tc, float* delta, double* q_exact) {
+  return guarded([&] {
+    psg::StreamScope _ss(ctx ? ctx->stream : nullptr);
+    using namespace psg;
+    if (!ctx || !index || !planes) fail(PSG_E_DOMAIN, "null argument");
+    const Index& ix = index->impl;
+    if (!ix.tc) fail(PSG_E_DOMAIN, "index has no tensor-core projection operand");
+    validate_grid(ix.w, spacing, W, H);
+    const auto hx = axis_positions(W, ix.w, spacing), hy = axis_positions(H, ix.w, spacing);
+    const int64_t A = (int64_t)hx.size() * hy.size(), P = (int64_t)W * H;
+    DBuf<int32_t> xs(hx.size()), ys(hy.size());
+    xs.upload(ctx, hx.data(), hx.size());
+    ys.upload(ctx, hy.data(), hy.size());
+    DBuf<double> pl((size_t)ix.C * P), qt((size_t)A * ix.d), qe((size_t)A * ix.d);
+    DBuf<float> mir((size_t)P * ix.C), dl((size_t)A);
+    DBuf<uint8_t> q8((size_t)4 * P * 8);
+    DBuf<int> bad(1);
+    pl.upload(ctx, planes, pl.n);
+    launch_make_mirror(ctx, pl.p, ix.C, W, H, mir.p);
+    PSG_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
+    launch_make_digits(ctx, mir.p, ix.C, W, H, q8.p, P * 8, bad.p);
+    const AnchorSet as{xs.p, ys.p, (int)hx.size(), A};
+    launch_project_windows_tc(ctx, q8.p, P * 8, W, bad.p, as, ix, qt.p, dl.p);
+    launch_project_windows(ctx, mir.p, W, ix.C, ix.w, as, ix.mean, ix.basis, ix.d, qe.p);
+    if (q_tc) qt.download(ctx, q_tc, qt.n);
+    if (delta) dl.download(ctx, delta, dl.n);
+    if (q_exact) qe.download(ctx, q_exact, qe.n);
+    PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    check_flags(ctx);
   });
 }

@@ -143,6 +143,7 @@ _SIGS = {
     "psg_downsample": (I, [VP, VP, I, I, I, I, VP]),
     "psg_upsample_bilinear": (I, [VP, VP, I, I, I, I, VP]),
     "psg_fit_to": (I, [VP, VP, I, I, I, I, I, VP]),
+    "psg_debug_projection": (I, [VP, VP, VP, I, I, I, VP, VP, VP]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

@@ -53,9 +53,17 @@ class LoopbackComm:
         self.ranks = list(range(world))
 
     def allreduce_sum(self, xs: Sequence):
+        cuda = getattr(xs[0], "is_cuda", False)
+        if cuda:
+            # the counts were written on the library's stream; the sum runs on
+            # torch's: order both ways (the library reads the sum in phase 2)
+            import torch
+            torch.cuda.synchronize()
         tot = xs[0].clone() if hasattr(xs[0], "clone") else xs[0].copy()
         for x in xs[1:]:
             tot += x
+        if cuda:
+            torch.cuda.synchronize()
         return [tot for _ in xs]
 
     def shift_up(self, sends: Sequence):
@@ -238,6 +246,9 @@ class GpuBand:
         self.n_halo_rows = plan["e1"] - plan["p1"]
         self.total_anchors = plan["nx"] * plan["ny"]
         self.dev = dev
+        # the buffers above were zero-filled on torch's stream; the library
+        # writes them on its own
+        torch.cuda.synchronize()
 
     def __del__(self):
         if getattr(self, "h", None):
