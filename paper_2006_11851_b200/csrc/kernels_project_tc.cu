@@ -330,32 +330,44 @@ __global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(TcArgs a) {
   }
 }
 
-// ---- exact fallback for listed anchors -------------------------------------------
-// One warp per listed anchor; lane k accumulates the reference's chain
-// acc = acc + ((double)v_j - mean_j) * basis[k][j], j ascending, no FMA.  The
-// centred window values c_j are staged in shared memory per 128-element chunk
-// (one load each, shared by the d chains); basis loads run 8 ahead.
+// ---- exact fallback for the ambiguous queries ------------------------------------------
+// One warp per listed query.  Lane k accumulates the reference's projection
+// chain acc = acc + ((double)v_j - mean_j) * basis[k][j], j ascending, no FMA
+// (the centred window values are staged per 128-element chunk in shared
+// memory, basis loads run 8 ahead).  Then, when the band held exactly two
+// points, lanes 0 and 1 evaluate the reference's dist2 chain (km_tree.cpp:
+// 15-22) for each and the lexicographic (dist^2, id) minimum is the answer.
 constexpr int kListWarps = 8, kListChunk = 128;
-__global__ void __launch_bounds__(32 * kListWarps) project_list_kernel(
-    const float* __restrict__ mirror, int img_w, int C, int w, const int32_t* __restrict__ xs,
-    const int32_t* __restrict__ ys, int nx, const int32_t* __restrict__ list,
-    const int* __restrict__ count, const double* __restrict__ mean,
-    const double* __restrict__ basisT, int KP, int D, int d, double* __restrict__ out) {
+__device__ __forceinline__ double dist2_chain(const double* q, const double* p, int d) {
+  double acc = 0.0;
+  for (int j = 0; j < d; ++j) {
+    const double t = dsub(q[j], __ldg(p + j));
+    acc = dadd(acc, dmul(t, t));
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(32 * kListWarps) resolve_kernel(
+    ResolveArgs r, const double* __restrict__ mean, const double* __restrict__ basisT, int KP,
+    int D, int d, const double* __restrict__ proj) {
   __shared__ double cs_all[kListWarps][kListChunk];
-  const int n = *count;
+  __shared__ double qs_all[kListWarps][64];
+  const int n = *r.count;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* cs = cs_all[warp];
-  const int wc = w * C;
+  double* qs = qs_all[warp];
+  const int wc = r.w * r.C;
   for (int i = blockIdx.x * kListWarps + warp; i < n; i += gridDim.x * kListWarps) {
-    const int32_t a = list[i];
-    const int64_t base = ((int64_t)ys[a / nx] * img_w + xs[a % nx]) * C;
+    const int32_t a = r.list[i];
+    const int64_t base =
+        ((int64_t)r.anchors.ys[a / r.anchors.nx] * r.img_w + r.anchors.xs[a % r.anchors.nx]) * r.C;
     double acc0 = 0.0, acc1 = 0.0;
     for (int j0 = 0; j0 < D; j0 += kListChunk) {
       const int jn = min(kListChunk, D - j0);
       __syncwarp();
       for (int t = lane; t < jn; t += 32) {
         const int j = j0 + t, dy = j / wc, off = j - dy * wc;
-        const float v = __ldg(mirror + base + (int64_t)dy * img_w * C + off);
+        const float v = __ldg(r.mirror + base + (int64_t)dy * r.img_w * r.C + off);
         cs[t] = dsub((double)v, __ldg(mean + j));
       }
       __syncwarp();
@@ -377,8 +389,31 @@ __global__ void __launch_bounds__(32 * kListWarps) project_list_kernel(
         }
       }
     }
-    if (lane < d) out[(int64_t)i * d + lane] = acc0;
-    if (lane + 32 < d) out[(int64_t)i * d + 32 + lane] = acc1;
+    if (lane < d) qs[lane] = acc0;
+    if (lane + 32 < d) qs[lane + 32] = acc1;
+    __syncwarp();
+    const int32_t c0 = r.c0[i], c1 = r.c1[i];
+    if (c1 >= 0) {
+      double dd = 0.0;
+      if (lane < 2) dd = dist2_chain(qs, proj + (int64_t)(lane ? c1 : c0) * d, d);
+      const double d1 = __shfl_sync(0xffffffffu, dd, 1);
+      if (lane == 0) {
+        const bool take1 = d1 < dd || (d1 == dd && c1 < c0);
+        r.idx[a] = take1 ? c1 : c0;
+        if (r.scanned) r.scanned[a] += 2;
+        if (r.exact) r.exact[a] += 2;
+      }
+    } else {
+      int slot = 0;
+      if (lane == 0) slot = atomicAdd(r.full_count, 1);
+      slot = __shfl_sync(0xffffffffu, slot, 0);
+      if (lane < d) r.full_q[(int64_t)slot * d + lane] = acc0;
+      if (lane + 32 < d) r.full_q[(int64_t)slot * d + 32 + lane] = acc1;
+      if (lane == 0) {
+        r.full_anchor[slot] = a;
+        r.full_seed[slot] = c0;
+      }
+    }
   }
 }
 
@@ -501,14 +536,11 @@ void launch_project_windows_tc(psg_ctx* ctx, const uint8_t* q8, int64_t slice_by
   PSG_LAUNCHED(ctx);
 }
 
-void launch_project_list(psg_ctx* ctx, const float* mirror, int img_w, int C, int w,
-                         AnchorSet anchors, const int32_t* list, const int* count,
-                         const Index& ix, double* out) {
+void launch_resolve(psg_ctx* ctx, const ResolveArgs& r, const Index& ix) {
   ProfScope _prof(ctx, K_FALLBACK);
   const int KP = ix.d <= 32 ? 32 : 64;
-  project_list_kernel<<<ctx->num_sms * 4, 32 * kListWarps, 0, ctx->stream>>>(
-      mirror, img_w, C, w, anchors.xs, anchors.ys, anchors.nx, list, count, ix.mean, ix.basis, KP,
-      ix.D, ix.d, out);
+  resolve_kernel<<<ctx->num_sms * 2, 32 * kListWarps, 0, ctx->stream>>>(r, ix.mean, ix.basis, KP,
+                                                                        ix.D, ix.d, ix.proj);
   PSG_LAUNCHED(ctx);
 }
 

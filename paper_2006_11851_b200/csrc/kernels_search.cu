@@ -1187,7 +1187,7 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 constexpr int kTileStack = 48;
 constexpr int kTileMaxB = 16;
 
-template <int DP, int kTileWarps>
+template <int DP, int kTileWarps, bool kApprox>
 __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TILE64_MIN_CTAS) search_tile_kernel(SearchArgs a) {
   constexpr int RS = DP + 4;  // padded staging row (floats): conflict-free 16 B accesses
   __shared__ int2 st_meta[kTileWarps][kTileStack];
@@ -1201,6 +1201,10 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
   __shared__ int32_t pid_all[kTileWarps][32];
   __shared__ float tlb_all[kTileWarps][kTileMaxB][32];
   __shared__ unsigned tkey_all[kTileWarps][kTileMaxB];
+  // approximate-query bookkeeping, per lane (touched only on exact
+  // evaluations and at the end: kept out of the register file)
+  __shared__ float band2_all[kTileWarps][32], sec_all[kTileWarps][32], thi_all[kTileWarps][32];
+  __shared__ int32_t sid_all[kTileWarps][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int2* sm_ = st_meta[warp];
   __nv_bfloat16(*slb)[32] = st_lb[warp];
@@ -1222,7 +1226,7 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
   // best distance inflated by the query's error band, (sqrt(best) + 2 delta)^2,
   // so every point that can be the exact winner is evaluated; `second` keeps
   // the smallest other evaluated distance (kernels_project_tc.cu)
-  const bool approx = a.qdelta != nullptr;
+  constexpr bool approx = kApprox;  // a.qdelta != nullptr
   // image queries: 8 x 4 anchor tiles (overlapping windows share candidates);
   // vector queries: 32 consecutive rows
   const int qny = a.qxs ? (int)(nq / a.qnx) : 0;
@@ -1249,16 +1253,36 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
       valid = q < nq;
     }
     const double* qrow = a.q + (valid ? q : 0) * d;
-    const float dq = (approx && valid) ? a.qdelta[q] : 0.f;
-    const bool trav = valid && !(dq > 3.0e38f);  // delta = inf: exact fallback only
-    const double twod = 2.0 * (double)dq;
+    bool trav = valid;
+    if (approx) {
+      const float twod = valid ? 2.f * a.qdelta[q] : 0.f;
+      trav = valid && !(twod > 3.0e38f);  // delta = inf: exact fallback only
+      band2_all[warp][lane] = twod;
+      sec_all[warp][lane] = kInfF;
+      thi_all[warp][lane] = kInfF;
+      sid_all[warp][lane] = -1;
+    }
     // float threshold for a best distance: the best itself, or its band
     auto infl = [&](double b) -> float {
       if (!approx || !(b > 0.0) || b == kInf) return __double2float_ru(b);
-      const double r = sqrt(b) * (1.0 + 1e-12) + twod;
+      const double r = sqrt(b) * (1.0 + 1e-12) + (double)band2_all[warp][lane];
       return __double2float_ru(r * r * (1.0 + 1e-15));
     };
-    double second = kInf;
+    // the two smallest other evaluated distances (rounded down: lower bounds)
+    // and the closer one's id: an ambiguous query with only one other point
+    // in its band is settled by two exact evaluations, no re-search
+    auto push = [&](double v, int32_t id) {
+      if (!approx || id == sid_all[warp][lane]) return;
+      const float vf = __double2float_rd(v);
+      const float sv = sec_all[warp][lane];
+      if (vf < sv) {
+        thi_all[warp][lane] = sv;
+        sec_all[warp][lane] = vf;
+        sid_all[warp][lane] = id;
+      } else {
+        thi_all[warp][lane] = fminf(thi_all[warp][lane], vf);
+      }
+    };
     float2 q2[DP / 2];
     double qn2 = 0.0;
 #pragma unroll
@@ -1411,7 +1435,7 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
                 const double d2 = dist2_seq_cold(qrow, a.proj + (int64_t)id * d, d);
                 ++exact_evals;
                 if (lex_less(d2, id, best, best_id)) {
-                  if (best_id != id) second = fmin(second, best);
+                  if (best_id != id && best_id != 0x7fffffff) push(best, best_id);
                   best = d2;
                   best_id = id;
                   best_up = infl(best);
@@ -1419,7 +1443,7 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
                   thr = best_up * (1.f + 1e-4f) +
                         1.01e-6f * (qn + a.pnorm_max) * (sqrtf(2.f * best_up + 1.f) + 1e-3f) + 1e-30f;
                 } else if (id != best_id) {
-                  second = fmin(second, d2);
+                  push(d2, id);
                 }
               }
             }
@@ -1546,14 +1570,19 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
       if (approx) {
         // unique within the band -> it is the exact chain's winner; otherwise
         // (near-tie, or no usable band) the exact fallback re-searches it
-        bool amb = !trav;
+        bool amb = !trav, pair = false;
         if (trav) {
-          const double r = sqrt(best) * (1.0 + 1e-12) + twod;
-          amb = second <= r * r * (1.0 + 1e-15);
+          const double r = sqrt(best) * (1.0 + 1e-12) + (double)band2_all[warp][lane];
+          const double band = r * r * (1.0 + 1e-15);
+          amb = (double)sec_all[warp][lane] <= band;
+          pair = amb && (double)thi_all[warp][lane] > band;  // exactly {best, second} in the band
         }
         if (amb) {
-          a.amb_list[atomicAdd(a.amb_count, 1)] = (int32_t)q;
           if (best_id == 0x7fffffff) best_id = a.seed_idx ? a.seed_idx[q] : 0;
+          const int slot = atomicAdd(a.amb_count, 1);
+          a.amb_list[slot] = (int32_t)q;
+          a.amb_c0[slot] = best_id;
+          a.amb_c1[slot] = pair ? sid_all[warp][lane] : -1;
         }
       }
       a.out_idx[q] = best_id;
@@ -1581,7 +1610,7 @@ template <int DP, int W>
 static int tile_resident_ctas(psg_ctx* ctx) {
   static int per_sm = 0;
   if (!per_sm) {
-    PSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, search_tile_kernel<DP, W>,
+    PSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, search_tile_kernel<DP, W, false>,
                                                            32 * W, 0));
     if (per_sm < 1) per_sm = 1;
   }
@@ -1621,9 +1650,11 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
     const int64_t cap = a.d <= 32 ? tile_resident_ctas<32, 4>(ctx) : tile_resident_ctas<64, 2>(ctx);
     if (blocks > cap) blocks = cap;
     if (a.d <= 32)
-      search_tile_kernel<32, 4><<<(int)blocks, 32 * 4, 0, ctx->stream>>>(a);
+      (a.qdelta ? search_tile_kernel<32, 4, true> : search_tile_kernel<32, 4, false>)
+          <<<(int)blocks, 32 * 4, 0, ctx->stream>>>(a);
     else
-      search_tile_kernel<64, 2><<<(int)blocks, 32 * 2, 0, ctx->stream>>>(a);
+      (a.qdelta ? search_tile_kernel<64, 2, true> : search_tile_kernel<64, 2, false>)
+          <<<(int)blocks, 32 * 2, 0, ctx->stream>>>(a);
     PSG_LAUNCHED(ctx);
     return;
   }

@@ -238,11 +238,28 @@ bool tc_prepare(psg_ctx* ctx, Index& ix);
 void launch_project_windows_tc(psg_ctx* ctx, const uint8_t* q8, int64_t slice_bytes, int img_w,
                                const int* bad, AnchorSet anchors, const Index& ix, double* out,
                                float* delta);
-// Exact (reference-chain) projection of listed anchors: out [count][d] compact,
-// count read on the device (*count), list = anchor ids.
-void launch_project_list(psg_ctx* ctx, const float* mirror, int img_w, int C, int w,
-                         AnchorSet anchors, const int32_t* list, const int* count,
-                         const Index& ix, double* out);
+// Exact fallback for the ambiguous queries of an approximate search (count
+// read on the device): the reference's projection chain of each listed
+// window, then either the exact lexicographic min over its two band
+// candidates (c1 >= 0: written to idx[], counters += 2) or, when the band
+// held more, the projection appended to a re-search list (full_*).
+struct ResolveArgs {
+  const float* mirror;
+  int img_w, C, w;
+  AnchorSet anchors;
+  const int32_t* list;
+  const int* count;
+  const int32_t* c0;
+  const int32_t* c1;
+  int32_t* idx;
+  int64_t* scanned;
+  int64_t* exact;
+  int32_t* full_anchor;
+  int32_t* full_seed;
+  int* full_count;
+  double* full_q;  // [count][d]
+};
+void launch_resolve(psg_ctx* ctx, const ResolveArgs& r, const Index& ix);
 // compact seeds / scatter of a fallback search over listed anchors
 void launch_list_gather_i32(psg_ctx* ctx, const int32_t* src, const int32_t* list,
                             const int* count, int32_t* out);
@@ -284,6 +301,8 @@ struct SearchArgs {
   // and lists the queries whose winner is not separated by that band
   const float* qdelta = nullptr;
   int32_t* amb_list = nullptr;  // [nq] ambiguous query ids
+  int32_t* amb_c0 = nullptr;    // [nq] their band winner
+  int32_t* amb_c1 = nullptr;    // [nq] the only other point in the band, or -1 (re-search)
   int* amb_count = nullptr;     // device counter (zeroed by the caller)
   const int* nq_dev = nullptr;  // optional: query count read on the device
 };

@@ -500,7 +500,8 @@ struct psg_level {
   psg::DBuf<uint8_t> q8;
   psg::DBuf<int> q8_bad, amb_n;
   psg::DBuf<float> qdelta;
-  psg::DBuf<int32_t> amb, seed_c, idx_c;
+  psg::DBuf<int32_t> amb, amb_c0, amb_c1, full_anchor, seed_c, idx_c;
+  psg::DBuf<int> full_n;
   psg::DBuf<double> q_ex, d2_c;
   psg::DBuf<int64_t> sc_c, ex_c;
   // one EM iteration captured as a CUDA graph per cur/next parity (level_step)
@@ -723,6 +724,10 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
       L.amb_n.alloc(1);
       L.qdelta.alloc((size_t)L.Ao);
       L.amb.alloc((size_t)L.Ao);
+      L.amb_c0.alloc((size_t)L.Ao);
+      L.amb_c1.alloc((size_t)L.Ao);
+      L.full_anchor.alloc((size_t)L.Ao);
+      L.full_n.alloc(1);
       L.seed_c.alloc((size_t)L.Ao);
       L.idx_c.alloc((size_t)L.Ao);
       L.q_ex.alloc((size_t)L.Ao * ix.d);
@@ -732,6 +737,7 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
     }
     PSG_CUDA(cudaMemsetAsync(L.q8_bad.p, 0, sizeof(int), ctx->stream));
     PSG_CUDA(cudaMemsetAsync(L.amb_n.p, 0, sizeof(int), ctx->stream));
+    PSG_CUDA(cudaMemsetAsync(L.full_n.p, 0, sizeof(int), ctx->stream));
     launch_make_digits(ctx, L.mirror.p, L.C, L.W, L.Hl, L.q8.p, q8_slice, L.q8_bad.p);
     launch_project_windows_tc(ctx, L.q8.p, q8_slice, L.W, L.q8_bad.p, as, ix, L.qproj.p,
                               L.qdelta.p);
@@ -805,16 +811,36 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
     a.qdelta = L.qdelta.p;
     a.amb_list = L.amb.p;
     a.amb_count = L.amb_n.p;
+    a.amb_c0 = L.amb_c0.p;
+    a.amb_c1 = L.amb_c1.p;
   }
   launch_search(ctx, a);
   if (tc) {
     // queries whose winner is not separated by their band: the reference's
-    // exact projection chain, then an exact search seeded with the band winner
-    launch_project_list(ctx, L.mirror.p, L.W, L.C, L.w, as, L.amb.p, L.amb_n.p, ix, L.q_ex.p);
-    launch_list_gather_i32(ctx, out_idx + L.off, L.amb.p, L.amb_n.p, L.seed_c.p);
+    // exact projection chain, then the exact minimum over the two band
+    // candidates -- or, when the band held more, an exact search seeded with
+    // the band winner
+    ResolveArgs rv{};
+    rv.mirror = L.mirror.p;
+    rv.img_w = L.W;
+    rv.C = L.C;
+    rv.w = L.w;
+    rv.anchors = as;
+    rv.list = L.amb.p;
+    rv.count = L.amb_n.p;
+    rv.c0 = L.amb_c0.p;
+    rv.c1 = L.amb_c1.p;
+    rv.idx = out_idx + L.off;
+    rv.scanned = L.scanned.p;
+    rv.exact = L.exact_evals.p;
+    rv.full_anchor = L.full_anchor.p;
+    rv.full_seed = L.seed_c.p;
+    rv.full_count = L.full_n.p;
+    rv.full_q = L.q_ex.p;
+    launch_resolve(ctx, rv, ix);
     SearchArgs f = a;
     f.q = L.q_ex.p;
-    f.nq_dev = L.amb_n.p;
+    f.nq_dev = L.full_n.p;
     f.qxs = nullptr;
     f.qys = nullptr;
     f.seed_idx = L.seed_c.p;
@@ -826,16 +852,19 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
     f.qdelta = nullptr;
     f.amb_list = nullptr;
     f.amb_count = nullptr;
+    f.amb_c0 = nullptr;
+    f.amb_c1 = nullptr;
     f.tile_order = nullptr;
     launch_search(ctx, f);
-    launch_list_scatter(ctx, L.amb.p, L.amb_n.p, L.idx_c.p, L.sc_c.p, L.ex_c.p, out_idx + L.off,
-                        L.scanned.p, L.exact_evals.p);
+    launch_list_scatter(ctx, L.full_anchor.p, L.full_n.p, L.idx_c.p, L.sc_c.p, L.ex_c.p,
+                        out_idx + L.off, L.scanned.p, L.exact_evals.p);
     if (ctx->knobs.verbose) {
-      int n = 0;
-      PSG_CUDA(cudaMemcpyAsync(&n, L.amb_n.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      int n[2] = {0, 0};
+      PSG_CUDA(cudaMemcpyAsync(&n[0], L.amb_n.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      PSG_CUDA(cudaMemcpyAsync(&n[1], L.full_n.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
       PSG_CUDA(cudaStreamSynchronize(ctx->stream));
-      fprintf(stderr, "[persyn] search: %d of %lld queries re-searched exactly (near-ties)\n", n,
-              (long long)L.Ao);
+      fprintf(stderr, "[persyn] search: %d of %lld queries settled exactly (near-ties), %d of them "
+              "re-searched\n", n[0], (long long)L.Ao, n[1]);
     }
   }
   L.scanned_valid = true;
