@@ -297,6 +297,37 @@ psg_status psg_band_phase3(psg_level* level, const void* recv_dev, int n_send_ro
 psg_status psg_band_phase4(psg_level* level, const float* recv_rows_dev, double* partials);
 psg_status psg_band_commit(psg_level* level, const double* global_partials, psg_iter_stats* st);
 
+/* ---- multi-GPU: NCCL inside the library (shard.cpp) -------------------------
+ * One process (or thread) per GPU, one psg_ctx per GPU.  Rank 0 makes a
+ * unique id (128 bytes) and the caller distributes it (MPI, a file,
+ * torch.distributed, ...); every rank then creates its communicator.  NCCL is
+ * loaded at psg_comm_unique_id / psg_comm_create (libnccl.so.2).
+ * psg_band_iterate runs n EM iterations of a band created with
+ * psg_band_create (after psg_level_prime) with the four exchanges of the
+ * phase list above enqueued as NCCL collectives / send-recv on the context
+ * stream; the convergence rule (optimizer.cpp:509-513) uses the global
+ * `changed`, so every rank stops after the same iteration, and stats hold the
+ * global (rank-order) sums.  Results are bit-identical to one device. */
+typedef struct psg_comm psg_comm;
+psg_status psg_comm_unique_id(void* id128);
+psg_status psg_comm_create(psg_ctx* ctx, const void* id128, int world, int rank, psg_comm** out);
+void psg_comm_destroy(psg_comm* comm);
+psg_status psg_band_iterate(psg_level* band, psg_comm* comm, int n, int honor_convergence,
+                            psg_iter_stats* stats, int* n_done);
+/* optimize_level (optimizer.cpp:426-516) of this rank's row band:
+ * rows = [C][e1-p0][W] host rows of the initial image (psg_shard_plan(W, H, w,
+ * spacing, rank, world)); out_rows = [C][p1-p0][W] the band's owned rows. */
+psg_status psg_optimize_level_sharded(psg_ctx* ctx, psg_comm* comm, const psg_index* index,
+                                      const double* rows, int W, int H, const psg_opt_cfg* cfg,
+                                      const double* ex_hist, double* out_rows,
+                                      psg_iter_stats* stats, int* n_iters);
+/* The same band schedule for `world` bands of one image in this process, the
+ * exchanges as device copies (tests the exchange buffers on one GPU). */
+psg_status psg_optimize_level_loopback(psg_ctx* ctx, const psg_index* index, const double* init,
+                                       int W, int H, const psg_opt_cfg* cfg, const double* ex_hist,
+                                       int world, double* out_planes, psg_iter_stats* stats,
+                                       int* n_iters);
+
 /* ---- pyramid driver (synthesize, pipeline.hpp:69, pipeline.cpp:216-315) --- */
 typedef struct {
   int n_sizes;

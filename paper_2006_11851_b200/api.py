@@ -447,6 +447,123 @@ class Level:
         return planes, idx, dist
 
 
+# ---- multi-GPU row bands (shard.cpp: NCCL inside the library) ---------------------
+def _nccl_first():
+    """The library dlopens libnccl.so.2 on first use; when torch is importable,
+    let torch load ITS NCCL first (one libnccl.so.2 per process: the library
+    then reuses it instead of pulling in an older system copy)."""
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
+
+
+def comm_unique_id() -> bytes:
+    """A fresh NCCL unique id (rank 0 makes it, the caller distributes it)."""
+    _nccl_first()
+    buf = ct.create_string_buffer(128)
+    N.check(N.lib.psg_comm_unique_id(buf))
+    return buf.raw
+
+
+class Communicator:
+    """One rank of a row-band job (psg_comm_create); `ctx` is this GPU's context."""
+
+    def __init__(self, ctx: Context, unique_id: bytes, world: int, rank: int):
+        if len(unique_id) != 128:
+            raise ShapeError(N.PSG_E_SHAPE, "an NCCL unique id is 128 bytes")
+        self.ctx, self.world, self.rank = ctx, world, rank
+        _nccl_first()
+        h = ct.c_void_p()
+        N.check(N.lib.psg_comm_create(ctx.h, ct.create_string_buffer(unique_id, 128), world, rank,
+                                      ct.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            N.lib.psg_comm_destroy(self.h)
+            self.h = None
+
+
+def shard_plan(W: int, H: int, w: int, spacing: int, rank: int, world: int) -> dict:
+    b = N.psg_band()
+    N.check(N.lib.psg_shard_plan(W, H, w, spacing, rank, world, ct.byref(b)))
+    return {f: getattr(b, f) for f, _ in N.psg_band._fields_}
+
+
+class Band:
+    """This rank's row band of a Level (psg_band_create), iterated over NCCL
+    by the library (psg_band_iterate)."""
+
+    def __init__(self, init_full: np.ndarray, index: SearchIndex, cfg: OptimizerConfig,
+                 comm: Communicator, exemplar_hist: Optional[np.ndarray] = None):
+        x = _c(init_full, np.float64)
+        _check_level_inputs(x, index, cfg, exemplar_hist)
+        C, H, W = x.shape
+        self.plan = shard_plan(W, H, index.window, cfg.spacing, comm.rank, comm.world)
+        p = self.plan
+        rows = np.ascontiguousarray(x[:, p["p0"]:p["e1"], :])
+        b = N.psg_band(*[p[f] for f, _ in N.psg_band._fields_])
+        c = cfg.c()
+        eh = _c(exemplar_hist, np.float64) if exemplar_hist is not None else None
+        h = ct.c_void_p()
+        N.check(N.lib.psg_band_create(index.ctx.h, index.h, _p(rows), ct.byref(b), ct.byref(c),
+                                      _p(eh), ct.byref(h)))
+        self.h, self.comm, self.index, self.C, self.W = h, comm, index, C, W
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            N.lib.psg_level_destroy(self.h)
+            self.h = None
+
+    def prime(self):
+        N.check(N.lib.psg_level_prime(self.h))
+
+    def iterate(self, n: int, honor_convergence: bool = False):
+        stats = (N.psg_iter_stats * max(n, 1))()
+        done = ct.c_int()
+        N.check(N.lib.psg_band_iterate(self.h, self.comm.h, n, int(honor_convergence),
+                                       ct.cast(stats, ct.c_void_p), ct.byref(done)))
+        return [IterationStats.of(stats[i]) for i in range(done.value)]
+
+
+def optimize_level_sharded(init_full: np.ndarray, index: SearchIndex, cfg: OptimizerConfig,
+                           comm: Communicator, exemplar_hist: Optional[np.ndarray] = None):
+    """(owned rows [C][p1-p0][W], plan, [IterationStats]) of this rank's band."""
+    x = _c(init_full, np.float64)
+    _check_level_inputs(x, index, cfg, exemplar_hist)
+    C, H, W = x.shape
+    p = shard_plan(W, H, index.window, cfg.spacing, comm.rank, comm.world)
+    rows = np.ascontiguousarray(x[:, p["p0"]:p["e1"], :])
+    out = np.zeros((C, p["p1"] - p["p0"], W))
+    c = cfg.c()
+    stats = (N.psg_iter_stats * max(cfg.max_iterations, 1))()
+    n = ct.c_int()
+    eh = _c(exemplar_hist, np.float64) if exemplar_hist is not None else None
+    N.check(N.lib.psg_optimize_level_sharded(index.ctx.h, comm.h, index.h, _p(rows), W, H,
+                                             ct.byref(c), _p(eh), _p(out),
+                                             ct.cast(stats, ct.c_void_p), ct.byref(n)))
+    return out, p, [IterationStats.of(stats[i]) for i in range(n.value)]
+
+
+def optimize_level_loopback(init: np.ndarray, index: SearchIndex, cfg: OptimizerConfig,
+                            world: int, exemplar_hist: Optional[np.ndarray] = None):
+    """The row-band schedule for `world` bands in this process (exchanges as
+    device copies): (image, [IterationStats]); bit-identical to optimize_level."""
+    x = _c(init, np.float64)
+    _check_level_inputs(x, index, cfg, exemplar_hist)
+    C, H, W = x.shape
+    out = np.zeros_like(x)
+    c = cfg.c()
+    stats = (N.psg_iter_stats * max(cfg.max_iterations, 1))()
+    n = ct.c_int()
+    eh = _c(exemplar_hist, np.float64) if exemplar_hist is not None else None
+    N.check(N.lib.psg_optimize_level_loopback(index.ctx.h, index.h, _p(x), W, H, ct.byref(c),
+                                              _p(eh), world, _p(out),
+                                              ct.cast(stats, ct.c_void_p), ct.byref(n)))
+    return out, [IterationStats.of(stats[i]) for i in range(n.value)]
+
+
 def synthesize(exemplar: np.ndarray, out_w: int, out_h: int, levels: int, sizes, cfg: OptimizerConfig,
                variance_target=0.95, d_cap=0, d_fixed=0, branching=4, max_depth=0, seed=0,
                out_guidance: Optional[np.ndarray] = None, stage_pca=None,

@@ -196,6 +196,79 @@ struct psg_index {
 };
 
 namespace psg {
+extern thread_local std::string g_last_error;
+void set_last_error(const std::string& m);
+// Stream of the C-ABI call in flight (set by StreamScope in every entry point
+// that allocates): DBuf allocations are ordered on it.
+extern thread_local cudaStream_t t_stream;
+// Stream of the API call in flight: per-call buffers come from the device's
+// stream-ordered memory pool (cudaMallocAsync), which keeps freed blocks, so
+// repeated optimize_level / search_step calls do not pay cudaMalloc.
+struct StreamScope {
+  cudaStream_t prev;
+  explicit StreamScope(cudaStream_t s) : prev(t_stream) { t_stream = s; }
+  ~StreamScope() { t_stream = prev; }
+};
+
+// Launches inside the scope go to the context's side stream (the launchers
+// use ctx->stream); the caller orders it against the main stream with events.
+struct SideScope {
+  psg_ctx* ctx;
+  cudaStream_t main;
+  explicit SideScope(psg_ctx* c) : ctx(c), main(c->stream) { ctx->stream = ctx->side; }
+  ~SideScope() { ctx->stream = main; }
+};
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  explicit DBuf(size_t count) { alloc(count); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr, o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+    std::swap(s, o.s);
+    return *this;
+  }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    s = t_stream;
+    // every C-ABI entry point that allocates sets its context stream
+    // (StreamScope): a block freed on the legacy stream could be reused
+    // under a kernel still running on the context's non-blocking stream
+    if (count && !s) throw Error(PSG_E_LOGIC, "device allocation outside a context stream scope");
+    if (count) PSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, s));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { release(); }
+  void upload(psg_ctx* ctx, const T* h, size_t count) {
+    if (count) PSG_CUDA(cudaMemcpyAsync(p, h, sizeof(T) * count, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  void download(psg_ctx* ctx, T* h, size_t count) const {
+    if (count) PSG_CUDA(cudaMemcpyAsync(h, p, sizeof(T) * count, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+};
+
+
+// ---- row-band helpers shared by runtime.cpp and shard.cpp ------------------------
+void band_info(const psg_level* L, psg_band* plan, psg_opt_cfg* cfg, int* C, int* hist_on,
+               int* iterations_done);
+psg_status band_download_owned(psg_level* L, double* rows);  // [C][p1-p0][W] host
+int index_window(const psg_index* ix);
+int index_channels(const psg_index* ix);
+}  // namespace psg
+
+namespace psg {
 
 // RAII event pair around one kernel launch when profiling is enabled.
 struct ProfScope {

@@ -27,67 +27,11 @@
 
 namespace psg {
 
-namespace {
 thread_local std::string g_last_error;
-// Stream of the API call in flight: per-call buffers come from the device's
-// stream-ordered memory pool (cudaMallocAsync), which keeps freed blocks, so
-// repeated optimize_level / search_step calls do not pay cudaMalloc.
 thread_local cudaStream_t t_stream = nullptr;
-struct StreamScope {
-  cudaStream_t prev;
-  explicit StreamScope(cudaStream_t s) : prev(t_stream) { t_stream = s; }
-  ~StreamScope() { t_stream = prev; }
-};
+void set_last_error(const std::string& m) { g_last_error = m; }
 
-// Launches inside the scope go to the context's side stream (the launchers
-// use ctx->stream); the caller orders it against the main stream with events.
-struct SideScope {
-  psg_ctx* ctx;
-  cudaStream_t main;
-  explicit SideScope(psg_ctx* c) : ctx(c), main(c->stream) { ctx->stream = ctx->side; }
-  ~SideScope() { ctx->stream = main; }
-};
-
-template <class T>
-struct DBuf {
-  T* p = nullptr;
-  size_t n = 0;
-  cudaStream_t s = nullptr;
-  DBuf() = default;
-  explicit DBuf(size_t count) { alloc(count); }
-  DBuf(const DBuf&) = delete;
-  DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr, o.n = 0; }
-  DBuf& operator=(DBuf&& o) noexcept {
-    std::swap(p, o.p);
-    std::swap(n, o.n);
-    std::swap(s, o.s);
-    return *this;
-  }
-  void alloc(size_t count) {
-    release();
-    n = count;
-    s = t_stream;
-    // every C-ABI entry point that allocates sets its context stream
-    // (StreamScope): a block freed on the legacy stream could be reused
-    // under a kernel still running on the context's non-blocking stream
-    if (count && !s) throw Error(PSG_E_LOGIC, "device allocation outside a context stream scope");
-    if (count) PSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, s));
-  }
-  void release() {
-    if (p) cudaFreeAsync(p, s);
-    p = nullptr;
-    n = 0;
-  }
-  ~DBuf() { release(); }
-  void upload(psg_ctx* ctx, const T* h, size_t count) {
-    if (count) PSG_CUDA(cudaMemcpyAsync(p, h, sizeof(T) * count, cudaMemcpyHostToDevice, ctx->stream));
-  }
-  void download(psg_ctx* ctx, T* h, size_t count) const {
-    if (count) PSG_CUDA(cudaMemcpyAsync(h, p, sizeof(T) * count, cudaMemcpyDeviceToHost, ctx->stream));
-  }
-};
-
+namespace {
 template <class T>
 T* dalloc(size_t count) {  // long-lived (index) buffers, from the stream-ordered pool
   T* p = nullptr;
@@ -2217,3 +2161,30 @@ extern "C" psg_status psg_debug_projection(psg_ctx* ctx, const psg_index* index,
     check_flags(ctx);
   });
 }
+
+// ---------------------------------------------------------------------------
+// Row-band helpers for shard.cpp.
+namespace psg {
+void band_info(const psg_level* L, psg_band* plan, psg_opt_cfg* cfg, int* C, int* hist_on,
+               int* iterations_done) {
+  if (plan) *plan = L->band;
+  if (cfg) *cfg = L->cfg;
+  if (C) *C = L->C;
+  if (hist_on) *hist_on = L->hist_on ? 1 : 0;
+  if (iterations_done) *iterations_done = L->iter;
+}
+
+psg_status band_download_owned(psg_level* L, double* rows) {
+  return guarded([&] {
+    StreamScope _ss(L->ctx->stream);
+    const size_t own = (size_t)L->Hu * L->W;
+    for (int c = 0; c < L->C; ++c)
+      PSG_CUDA(cudaMemcpyAsync(rows + c * own, L->planes.p + (size_t)c * L->P, sizeof(double) * own,
+                               cudaMemcpyDeviceToHost, L->ctx->stream));
+    PSG_CUDA(cudaStreamSynchronize(L->ctx->stream));
+  });
+}
+
+int index_window(const psg_index* ix) { return ix->impl.w; }
+int index_channels(const psg_index* ix) { return ix->impl.C; }
+}  // namespace psg

@@ -144,6 +144,14 @@ _SIGS = {
     "psg_upsample_bilinear": (I, [VP, VP, I, I, I, I, VP]),
     "psg_fit_to": (I, [VP, VP, I, I, I, I, I, VP]),
     "psg_debug_projection": (I, [VP, VP, VP, I, I, I, VP, VP, VP]),
+    "psg_comm_unique_id": (I, [VP]),
+    "psg_comm_create": (I, [VP, VP, I, I, PP]),
+    "psg_comm_destroy": (None, [VP]),
+    "psg_band_iterate": (I, [VP, VP, I, I, VP, VP]),
+    "psg_optimize_level_sharded": (I, [VP, VP, VP, VP, I, I, ct.POINTER(psg_opt_cfg), VP, VP,
+                                       VP, VP]),
+    "psg_optimize_level_loopback": (I, [VP, VP, VP, I, I, ct.POINTER(psg_opt_cfg), VP, I, VP,
+                                        VP, VP]),
 }
 
 for _name, (_res, _args) in _SIGS.items():
