@@ -381,21 +381,20 @@ def run_ours(args):
                                histogram_matching=True, nbhd_width=args.window, spacing=sp,
                                patch_width=2, budget=budget)
     if sharded:
-        # row bands over the ranks, NCCL halo exchange
-        from paper_2006_11851_b200 import sharding as sh
-        plans = sh.all_plans(cfg.out, cfg.out, args.window, sp, world)
-        band = sh.GpuBand(index, init, plans[rank], plans, ocfg)
-        # the library runs on `stream`; exchanges are enqueued on it too
-        comm = sh.DistComm(stream_ordered=True) if world > 1 or \
-            torch.distributed.is_initialized() else sh.LoopbackComm(1)
+        # row bands over the ranks; the library runs every exchange itself
+        # (NCCL on its context stream, shard.cpp); torch.distributed only
+        # carries the NCCL unique id and the timing reductions
+        uid = [api.comm_unique_id() if rank == 0 else None]
+        if world > 1:
+            torch.distributed.broadcast_object_list(uid, src=0)
+        comm = api.Communicator(ctx, uid[0], world, rank)
+        band = api.Band(init, index, ocfg, comm)
         band.prime()
 
         def one_step():
-            with torch.cuda.stream(stream):
-                g = sh.em_iteration([band], comm)
-            return [api.IterationStats(0, g[2], int(g[3]), int(g[6] + g[7]), 0.0, g[0], g[1],
-                                       int(g[4]), int(g[8]), int(g[5]))]
-        A = plans[0]["nx"] * plans[0]["ny"]
+            return band.iterate(1)
+        plan0 = api.shard_plan(cfg.out, cfg.out, args.window, sp, 0, world)
+        A = plan0["nx"] * plan0["ny"]
     else:
         level = api.Level(init, index, ocfg)
         level.prime()
@@ -458,7 +457,7 @@ def run_ours(args):
         "config": {"workload": "cfg3 finest stage: exemplar 256^2 C=5, output 1024^2, w=8 sp=2 "
                                "p=2, PCA d=32, tree b=8 depth 4, exact search, hist on",
                    "anchors": A, "plan_calls_per_search": int(calls // 1),
-                   "parallelism": (f"row bands x{world} (NCCL halo exchange)" if sharded
+                   "parallelism": (f"row bands x{world} (library NCCL halo exchange)" if sharded
                                    else "1 GPU"),
                    "l2": "flushed (256 MB write) before every timed step"},
         "nn_queries_per_s": {"unique_anchor_queries": A / (ms_per_step / 1e3),
@@ -539,15 +538,14 @@ def run_ours(args):
         # runs 10 EM iterations with the NCCL exchanges and downloads its owned
         # rows + assignments; max over ranks of the device-synchronised wall time
         n_it = 10
-        from paper_2006_11851_b200 import sharding as sh
+        e2e_cfg = api.OptimizerConfig(max_iterations=n_it, min_iterations=n_it,
+                                      convergence_fraction=1e-9, histogram_bins=16,
+                                      histogram_matching=True, nbhd_width=args.window,
+                                      spacing=sp, patch_width=2, budget=budget)
 
         def e2e_band():
-            b = sh.GpuBand(index, init, plans[rank], plans, ocfg)
-            with torch.cuda.stream(stream):
-                sh.run_sharded([b], comm, n_it, n_it, total_anchors=A)
-            out = b.owned()
-            del b
-            return out
+            out, plan, _ = api.optimize_level_sharded(init, index, e2e_cfg, comm)
+            return out, plan
 
         e2e_band()  # warm-up
         ts = []
@@ -564,14 +562,15 @@ def run_ours(args):
             t = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             t_e2e = float(t.item())
-        p = plans[rank]
+        p = own[1]
         h2d = (p["e1"] - p["p0"]) * cfg.out * C * 8
-        d2h = own[0].nbytes + own[1].nbytes + own[2].nbytes
+        d2h = own[0].nbytes
         result["e2e"] = {"value": n_it / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                          "d2h_bytes_per_step": int(d2h),
-                         "step": f"per rank: band create from host rows, priming search, {n_it} "
-                                 "EM iterations with NCCL halo exchange, download of owned rows "
-                                 "(bytes: rank 0's); max over ranks"}
+                         "step": f"per rank: psg_optimize_level_sharded (band rows from host, "
+                                 f"priming search, {n_it} EM iterations with the library's NCCL "
+                                 "exchanges, owned rows back to host; bytes: rank 0's); max over "
+                                 "ranks"}
     result["clocks"] = clk.summary()
     # ---- CPU baseline (rank 0, N = 1) -------------------------------------------
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
