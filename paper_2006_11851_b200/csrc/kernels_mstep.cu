@@ -263,6 +263,56 @@ __global__ void __launch_bounds__(256) mstep_kernel(MstepArgs a) {
     double wsum = 0.0;
     const int iy0 = a.row_lo[y], iy1 = a.row_hi[y];
     const int ix0 = a.col_lo[x], ix1 = a.col_hi[x];
+    if (NC > 0 && a.ex8 && iy1 - iy0 == 4 && ix1 - ix0 == 4) {
+      // interior pixel (w / spacing = 4 at every stage): the 16 covering
+      // anchors' (eff, id) are loaded together, then their candidate pixels
+      // eight at a time, ahead of the sequential ascending-anchor fp64 chain
+      double we[16];
+      int32_t id[16];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int64_t ai = (int64_t)(iy0 + r) * a.nx + ix0 + c;
+          we[r * 4 + c] = __ldg(a.eff + ai);
+          id[r * 4 + c] = __ldg(a.idx + ai);
+        }
+      int dys[4], dxs[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) dys[r] = y - a.ys[iy0 + r];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) dxs[c] = x - a.xs[ix0 + c];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float4 z0[8], z1[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int j = h * 8 + k;
+          int ey = __float2int_rz((float)id[j] * inv_nxe);
+          int ex = id[j] - ey * a.nxe;
+          if (ex < 0) {
+            --ey;
+            ex += a.nxe;
+          } else if (ex >= a.nxe) {
+            ++ey;
+            ex -= a.nxe;
+          }
+          const int64_t zp = (int64_t)(ey + dys[j >> 2]) * a.ew + ex + dxs[j & 3];
+          const float4* z4 = reinterpret_cast<const float4*>(a.ex8 + zp * 8);
+          z0[k] = __ldg(z4);
+          z1[k] = NC > 4 ? __ldg(z4 + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const double w = we[h * 8 + k];
+          const float zc[8] = {z0[k].x, z0[k].y, z0[k].z, z0[k].w,
+                               z1[k].x, z1[k].y, z1[k].z, z1[k].w};
+#pragma unroll
+          for (int c = 0; c < CMAX; ++c) acc[c] = dadd(acc[c], dmul(w, (double)zc[c]));
+          wsum = dadd(wsum, w);
+        }
+      }
+    } else
     for (int iy = iy0; iy < iy1; ++iy) {
       const int dy = y - a.ys[iy];
       const int64_t arow = (int64_t)iy * a.nx;

@@ -539,7 +539,7 @@ void launch_project_windows_tc(psg_ctx* ctx, const uint8_t* q8, int64_t slice_by
 void launch_resolve(psg_ctx* ctx, const ResolveArgs& r, const Index& ix) {
   ProfScope _prof(ctx, K_FALLBACK);
   const int KP = ix.d <= 32 ? 32 : 64;
-  resolve_kernel<<<ctx->num_sms * 2, 32 * kListWarps, 0, ctx->stream>>>(r, ix.mean, ix.basis, KP,
+  resolve_kernel<<<64, 32 * kListWarps, 0, ctx->stream>>>(r, ix.mean, ix.basis, KP,
                                                                         ix.D, ix.d, ix.proj);
   PSG_LAUNCHED(ctx);
 }

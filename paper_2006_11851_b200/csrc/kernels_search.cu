@@ -1155,11 +1155,18 @@ __global__ void __launch_bounds__(256) search_exact_kernel(SearchArgs a) {
       }
     }
     if (lane == 0) {
-      a.out_idx[q] = best_id;
-      a.out_d2[q] = best;
-      if (a.out_scanned) a.out_scanned[q] = scanned;
-      if (a.out_exact) a.out_exact[q] = exact_evals;
-      if (a.out_visited) a.out_visited[q] = visited;
+      if (a.out_map) {  // a listed query: results go to its anchor, counters add
+        const int32_t qa = a.out_map[q];
+        a.out_idx[qa] = best_id;
+        if (a.out_scanned) a.out_scanned[qa] += scanned;
+        if (a.out_exact) a.out_exact[qa] += exact_evals;
+      } else {
+        a.out_idx[q] = best_id;
+        a.out_d2[q] = best;
+        if (a.out_scanned) a.out_scanned[q] = scanned;
+        if (a.out_exact) a.out_exact[q] = exact_evals;
+        if (a.out_visited) a.out_visited[q] = visited;
+      }
     }
     __syncwarp();
   }
@@ -1631,7 +1638,7 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
     // queries would traverse the union of their candidate sets
     if (a.mode != PSG_EXACT || !a.proj32_q4 || !a.tree.centroid32T)
       fail(PSG_E_LOGIC, "device-counted search needs the exact warp kernel");
-    const int64_t blocks = (int64_t)ctx->num_sms * 8;
+    const int64_t blocks = 32;  // re-searches are rare: a few hundred warps
     if (a.d <= 32)
       search_exact_kernel<32><<<(int)blocks, 256, 0, ctx->stream>>>(a);
     else

@@ -378,6 +378,7 @@ struct SearchArgs {
   int32_t* amb_c1 = nullptr;    // [nq] the only other point in the band, or -1 (re-search)
   int* amb_count = nullptr;     // device counter (zeroed by the caller)
   const int* nq_dev = nullptr;  // optional: query count read on the device
+  const int32_t* out_map = nullptr;  // optional (warp kernel): query -> output slot, counters add
 };
 // Tile permutation for the next exact search of the same anchors: descending
 // previous per-tile work (order: [image_tile_count(nq, qnx)]).

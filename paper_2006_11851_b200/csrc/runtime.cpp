@@ -444,10 +444,9 @@ struct psg_level {
   psg::DBuf<uint8_t> q8;
   psg::DBuf<int> q8_bad, amb_n;
   psg::DBuf<float> qdelta;
-  psg::DBuf<int32_t> amb, amb_c0, amb_c1, full_anchor, seed_c, idx_c;
+  psg::DBuf<int32_t> amb, amb_c0, amb_c1, full_anchor, seed_c;
   psg::DBuf<int> full_n;
-  psg::DBuf<double> q_ex, d2_c;
-  psg::DBuf<int64_t> sc_c, ex_c;
+  psg::DBuf<double> q_ex;
   // one EM iteration captured as a CUDA graph per cur/next parity (level_step)
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
   double* stats_host = nullptr;  // pinned [8]
@@ -673,11 +672,7 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
       L.full_anchor.alloc((size_t)L.Ao);
       L.full_n.alloc(1);
       L.seed_c.alloc((size_t)L.Ao);
-      L.idx_c.alloc((size_t)L.Ao);
       L.q_ex.alloc((size_t)L.Ao * ix.d);
-      L.d2_c.alloc((size_t)L.Ao);
-      L.sc_c.alloc((size_t)L.Ao);
-      L.ex_c.alloc((size_t)L.Ao);
     }
     PSG_CUDA(cudaMemsetAsync(L.q8_bad.p, 0, sizeof(int), ctx->stream));
     PSG_CUDA(cudaMemsetAsync(L.amb_n.p, 0, sizeof(int), ctx->stream));
@@ -788,10 +783,11 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
     f.qxs = nullptr;
     f.qys = nullptr;
     f.seed_idx = L.seed_c.p;
-    f.out_idx = L.idx_c.p;
-    f.out_d2 = L.d2_c.p;
-    f.out_scanned = L.sc_c.p;
-    f.out_exact = L.ex_c.p;
+    f.out_map = L.full_anchor.p;  // results straight to the anchors
+    f.out_idx = out_idx + L.off;
+    f.out_d2 = nullptr;
+    f.out_scanned = L.scanned.p;
+    f.out_exact = L.exact_evals.p;
     f.out_visited = nullptr;
     f.qdelta = nullptr;
     f.amb_list = nullptr;
@@ -800,8 +796,6 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
     f.amb_c1 = nullptr;
     f.tile_order = nullptr;
     launch_search(ctx, f);
-    launch_list_scatter(ctx, L.full_anchor.p, L.full_n.p, L.idx_c.p, L.sc_c.p, L.ex_c.p,
-                        out_idx + L.off, L.scanned.p, L.exact_evals.p);
     if (ctx->knobs.verbose) {
       int n[2] = {0, 0};
       PSG_CUDA(cudaMemcpyAsync(&n[0], L.amb_n.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
