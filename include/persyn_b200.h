@@ -352,13 +352,20 @@ typedef struct {
   const double* const* stage_mean;
   const double* const* stage_basis;
   const int* stage_d;
+  int index_kind;          /* psg_index_kind (IndexKind, pipeline.hpp:13-16) */
+  psg_iter_stats* trace;   /* optional [trace_cap]: every stage's iterations, in order */
+  int trace_cap;
 } psg_request;
+
+/* IndexKind (pipeline.hpp): the per-stage SearchIndex of synthesize. */
+typedef enum { PSG_INDEX_PCA_TREE = 0, PSG_INDEX_BRUTE_FORCE = 1 } psg_index_kind;
 
 typedef struct {
   int level, w, W, H, ew, eh, d, iterations;
   double final_energy;
   int64_t nn_calls;
   double index_millis, optimize_millis;
+  int trace_first, trace_count; /* this stage's iterations in psg_request.trace */
 } psg_stage_report;
 
 typedef struct {
@@ -367,6 +374,7 @@ typedef struct {
   double part1_millis, part2_millis;
   int64_t total_nn_calls;
   double final_energy;
+  int n_trace; /* iterations run (may exceed trace_cap) */
 } psg_report;
 
 /* out_planes: [C][out_h][out_w] fp64 final state (RGB = the synthesized image).

@@ -334,6 +334,12 @@ class Ref:
             L.ref_attach_scale.argtypes = [_VP, _I, _I, _D, _D, _VP]
             L.ref_initialize_output.argtypes = [_VP, _I, _I, _VP, _I, _I, _D, _D, ct.c_uint64,
                                                 _VP]
+            L.ref_report_json.argtypes = [ct.c_char_p, _D, _D, _I64, _I, _VP, _VP, ct.c_char_p,
+                                          _VP, _VP, ct.c_char_p, _I64, _VP]
+            L.ref_modes_format.argtypes = [ct.c_char_p, _VP, _VP, _VP, _VP, _I, _I, ct.c_char_p,
+                                           _I64, _VP]
+            L.ref_save_scale_map.argtypes = [_VP, _I, _I, _D, _D, _D, _D, ct.c_char_p]
+            L.ref_load_scale_map.argtypes = [ct.c_char_p, _VP, _VP, _VP]
         self.L = Ref._lib
 
     def _check(self, st, what=""):
@@ -527,6 +533,46 @@ class Ref:
         self._check(self.L.ref_initialize_output(_ptr(ex4), ew, eh, _ptr(v), ow, oh, s_min, s_max,
                                                  seed, _ptr(out)), "initialize_output")
         return out
+
+
+    def _text(self, fn, *args):
+        n = np.zeros(1, np.int64)
+        self._check(fn(*args, None, 0, _ptr(n)), "format")
+        buf = ct.create_string_buffer(int(n[0]) + 1)
+        self._check(fn(*args, buf, int(n[0]) + 1, _ptr(n)), "format")
+        return buf.value.decode()
+
+    def report_json(self, config_echo, part1, part2, total_calls, levels):
+        """levels: [(width, height, index name, [(iter, energy, changed, nn_calls, millis)])]"""
+        w = np.array([l[0] for l in levels], np.int32)
+        h = np.array([l[1] for l in levels], np.int32)
+        names = "\n".join(l[2] for l in levels).encode()
+        ni = np.array([len(l[3]) for l in levels], np.int32)
+        st = np.array([list(t) for l in levels for t in l[3]] or [[0] * 5], np.float64)
+        return self._text(self.L.ref_report_json, config_echo.encode(), part1, part2, total_calls,
+                          len(levels), _ptr(w), _ptr(h), names, _ptr(ni), _ptr(st))
+
+    def save_scale_map(self, values, slant, tilt, s_min, s_max, path):
+        v = _c(values, np.float32)
+        H, W = v.shape
+        self._check(self.L.ref_save_scale_map(_ptr(v), W, H, slant, tilt, s_min, s_max,
+                                              str(path).encode()), "save_scale_map")
+
+    def load_scale_map(self, path):
+        wh = np.zeros(2, np.int32)
+        vb = np.zeros(4, np.float64)
+        self._check(self.L.ref_load_scale_map(str(path).encode(), _ptr(wh), _ptr(vb), None), "load")
+        v = np.zeros((wh[1], wh[0]), np.float32)
+        self._check(self.L.ref_load_scale_map(str(path).encode(), _ptr(wh), _ptr(vb), _ptr(v)),
+                    "load")
+        return v, tuple(vb)
+
+    def modes_format(self, runs, which):
+        names = "\n".join(r[0] for r in runs).encode()
+        cols = [np.array([r[k] for r in runs], np.float64) for k in (1, 2, 4)]
+        calls = np.array([r[3] for r in runs], np.int64)
+        return self._text(self.L.ref_modes_format, names, _ptr(cols[0]), _ptr(cols[1]),
+                          _ptr(calls), _ptr(cols[2]), len(runs), which)
 
 
 class RefIndex:

@@ -633,6 +633,105 @@ int ref_attach_scale(const double* rgb, int W, int H, double slant, double tilt,
   });
 }
 
+// ---- report / bench formats (pipeline.cpp:182-214, :336-357) -------------------------
+static void put_text(const std::string& out, char* buf, int64_t cap, int64_t* len) {
+  *len = static_cast<int64_t>(out.size());
+  if (buf && cap > 0) {
+    const size_t k = std::min<size_t>(out.size(), static_cast<size_t>(cap - 1));
+    std::memcpy(buf, out.data(), k);
+    buf[k] = 0;
+  }
+}
+
+static std::vector<std::string> split_lines(const char* s) {
+  std::vector<std::string> v;
+  std::string cur;
+  for (const char* p = s; *p; ++p) {
+    if (*p == '\n') {
+      v.push_back(cur);
+      cur.clear();
+    } else {
+      cur += *p;
+    }
+  }
+  v.push_back(cur);
+  return v;
+}
+
+// SynthesisReport::to_json over given levels; stats5 per iteration:
+// iter, energy, changed, nn_calls, millis.
+int ref_report_json(const char* config_echo, double part1, double part2, int64_t total_calls,
+                    int n_levels, const int* widths, const int* heights, const char* index_names,
+                    const int* n_iters, const double* stats5, char* buf, int64_t cap,
+                    int64_t* len) {
+  return guard([&] {
+    SynthesisReport r;
+    r.config_echo = config_echo;
+    r.part1_millis = part1;
+    r.part2_millis = part2;
+    r.total_nn_calls = total_calls;
+    const auto names = split_lines(index_names);
+    const double* s = stats5;
+    for (int l = 0; l < n_levels; ++l) {
+      LevelReport lr;
+      lr.width = widths[l];
+      lr.height = heights[l];
+      lr.index = names[static_cast<size_t>(l)];
+      for (int i = 0; i < n_iters[l]; ++i, s += 5) {
+        IterationStats it;
+        it.iteration = static_cast<int>(s[0]);
+        it.energy = s[1];
+        it.changed = static_cast<std::int64_t>(s[2]);
+        it.nn_calls = static_cast<std::int64_t>(s[3]);
+        it.millis = s[4];
+        lr.trace.iterations.push_back(it);
+      }
+      r.levels.push_back(std::move(lr));
+    }
+    put_text(r.to_json(), buf, cap, len);
+  });
+}
+
+// save_scale_map / load_scale_map (scale_map.cpp:125-201, the PSM1 container).
+int ref_save_scale_map(const float* values, int W, int H, double slant, double tilt, double s_min,
+                       double s_max, const char* path) {
+  return guard([&] {
+    ScaleBounds b;
+    b.s_min = s_min;
+    b.s_max = s_max;
+    b.s_delta = s_max - s_min;
+    save_scale_map(ScaleMap(W, H, std::vector<float>(values, values + (size_t)W * H),
+                            ViewAngles{slant, tilt}, b),
+                   path);
+  });
+}
+
+int ref_load_scale_map(const char* path, int* wh, double* view_bounds, float* values) {
+  return guard([&] {
+    const ScaleMap m = load_scale_map(path);
+    wh[0] = m.width();
+    wh[1] = m.height();
+    view_bounds[0] = m.view().slant_deg;
+    view_bounds[1] = m.view().tilt_deg;
+    view_bounds[2] = m.bounds().s_min;
+    view_bounds[3] = m.bounds().s_max;
+    if (values) std::copy(m.values().begin(), m.values().end(), values);
+  });
+}
+
+// modes_to_json (which = 0) / modes_to_csv (which = 1).
+int ref_modes_format(const char* names, const double* wall, const double* part2,
+                     const int64_t* calls, const double* energy, int n, int which, char* buf,
+                     int64_t cap, int64_t* len) {
+  return guard([&] {
+    const auto nm = split_lines(names);
+    std::vector<ModeRun> runs;
+    for (int i = 0; i < n; ++i)
+      runs.push_back({nm[static_cast<size_t>(i)], wall[i], part2[i], calls[i], energy[i]});
+    put_text(which == 0 ? modes_to_json(runs) : modes_to_csv(runs), buf, cap, len);
+  });
+}
+
 // initialize_output(exemplar_rgbs, ScaleMap(values, bounds), mt19937_64(seed)).
 int ref_initialize_output(const double* ex4, int ew, int eh, const float* out_vals, int ow,
                           int oh, double s_min, double s_max, uint64_t seed, double* out4) {

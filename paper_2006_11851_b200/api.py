@@ -567,7 +567,8 @@ def optimize_level_loopback(init: np.ndarray, index: SearchIndex, cfg: Optimizer
 def synthesize(exemplar: np.ndarray, out_w: int, out_h: int, levels: int, sizes, cfg: OptimizerConfig,
                variance_target=0.95, d_cap=0, d_fixed=0, branching=4, max_depth=0, seed=0,
                out_guidance: Optional[np.ndarray] = None, stage_pca=None,
-               tree_kind: int = TREE_DEVICE, ctx: Optional[Context] = None):
+               tree_kind: int = TREE_DEVICE, index_kind: int = 0,
+               ctx: Optional[Context] = None):
     """Coarse-to-fine driver (pipeline.cpp:216-315) over stages (level x size).
     stage_pca: optional list over stages (level-major, then sizes) of
     (mean, basis) or None -- injected PCA models (fit on the device otherwise)."""
@@ -609,6 +610,11 @@ def synthesize(exemplar: np.ndarray, out_w: int, out_h: int, levels: int, sizes,
         req.stage_mean = ct.cast(means, ct.POINTER(ct.c_void_p))
         req.stage_basis = ct.cast(bases, ct.POINTER(ct.c_void_p))
         req.stage_d = ct.cast(ds, ct.POINTER(ct.c_int))
+    req.index_kind = int(index_kind)
+    cap = levels * len(sizes) * max(cfg.max_iterations, 1)
+    trace = (N.psg_iter_stats * cap)()
+    req.trace = ct.cast(trace, ct.c_void_p)
+    req.trace_cap = cap
     out = np.zeros((C, out_h, out_w))
     rep = N.psg_report()
     N.check(N.lib.psg_synthesize(ctx.h, ct.byref(req), _p(out), ct.byref(rep)))
@@ -619,9 +625,195 @@ def synthesize(exemplar: np.ndarray, out_w: int, out_h: int, levels: int, sizes,
         "stages": [dict(level=s.level, w=s.w, W=s.W, H=s.H, ew=s.ew, eh=s.eh, d=s.d,
                         iterations=s.iterations, final_energy=s.final_energy,
                         nn_calls=s.nn_calls, index_millis=s.index_millis,
-                        optimize_millis=s.optimize_millis) for s in stages],
+                        optimize_millis=s.optimize_millis,
+                        trace=[IterationStats.of(trace[i]) for i in
+                               range(s.trace_first, min(cap, s.trace_first + s.trace_count))])
+                   for s in stages],
+        "index": "brute-force" if index_kind == INDEX_BRUTE_FORCE else "pca-tree",
     }
     return out, report
+
+
+INDEX_PCA_TREE, INDEX_BRUTE_FORCE = 0, 1  # psg_index_kind (IndexKind, pipeline.hpp)
+
+
+# ---- compare_modes / the bench table (pipeline.cpp:317-357, persyn_main.cpp:196-272) ----
+@dataclass
+class ModeSpec:
+    """pipeline.hpp ModeSpec: name, patch width, index kind, budget."""
+    name: str
+    patch_width: int = 2
+    index: int = INDEX_PCA_TREE
+    budget: QueryBudget = field(default_factory=lambda: QueryBudget.backtrack(4))
+
+
+@dataclass
+class ModeRun:
+    name: str
+    wall_millis: float
+    part2_millis: float
+    nn_calls: int
+    final_energy: float
+
+
+# the modes of `persyn bench` (persyn_main.cpp:205-212)
+BENCH_MODES = (ModeSpec("pixel-brute", 1, INDEX_BRUTE_FORCE, QueryBudget.exact()),
+               ModeSpec("pixel-tree", 1, INDEX_PCA_TREE, QueryBudget.backtrack(4)),
+               ModeSpec("patch-tree", 2, INDEX_PCA_TREE, QueryBudget.backtrack(4)))
+
+
+def compare_modes(exemplar: np.ndarray, out_w: int, out_h: int, levels: int, sizes,
+                  cfg: OptimizerConfig, modes, *, seed: int = 0, variance_target: float = 0.95,
+                  branching: int = 4, d_cap: int = 0, ctx: Optional[Context] = None):
+    """compare_modes (pipeline.cpp:317-334): the same request under each mode
+    (patch width, index kind, budget) with identical seeds.  Tree budgets run
+    on the reference's own KmTree construction (tree_kind=TREE_REFERENCE)."""
+    if not modes:
+        raise DomainError(N.PSG_E_DOMAIN, "no modes to compare")
+    runs = []
+    import time as _time
+    for m in modes:
+        c = OptimizerConfig(**{**cfg.__dict__, "patch_width": m.patch_width, "budget": m.budget})
+        t0 = _time.perf_counter()
+        _, rep = synthesize(exemplar, out_w, out_h, levels, sizes, c,
+                            variance_target=variance_target, d_cap=d_cap, branching=branching,
+                            max_depth=0, seed=seed, tree_kind=TREE_REFERENCE, index_kind=m.index,
+                            ctx=ctx)
+        wall = (_time.perf_counter() - t0) * 1e3
+        # ModeRun{name, part1 + part2, part2, total_nn_calls, final_energy}
+        # (pipeline.cpp:327-331); `wall` (host time of the call) is returned too
+        runs.append(ModeRun(m.name, rep["part1_millis"] + rep["part2_millis"],
+                            rep["part2_millis"], int(rep["total_nn_calls"]),
+                            float(rep["final_energy"])))
+        runs[-1].host_millis = wall
+    return runs
+
+
+def synthesis_report_json(rep: dict, config: dict) -> str:
+    """SynthesisReport::to_json (pipeline.cpp:182-208): {config, part1_millis,
+    part2_millis, total_nn_calls, final_energy, levels: [{width, height, index,
+    iterations: [{iter, energy, changed, nn_calls, millis}]}]} -- one entry per
+    stage (a level x neighbourhood size), nlohmann dump(2) formatting.
+    `config` is the request echo (config_json, pipeline.cpp:58-88)."""
+    import json as _json
+    stages = rep["stages"]
+    final = stages[-1]["trace"][-1].energy if stages and stages[-1]["trace"] else 0.0
+    j = {"config": config, "part1_millis": float(rep["part1_millis"]),
+         "part2_millis": float(rep["part2_millis"]), "total_nn_calls": int(rep["total_nn_calls"]),
+         "final_energy": float(final), "levels": []}
+    for s in stages:
+        j["levels"].append({"width": int(s["W"]), "height": int(s["H"]),
+                            "index": rep.get("index_describe", rep.get("index", "pca-tree")),
+                            "iterations": [{"iter": int(t.iteration), "energy": float(t.energy),
+                                            "changed": int(t.changed),
+                                            "nn_calls": int(t.nn_calls),
+                                            "millis": float(t.millis)} for t in s["trace"]]})
+    return _json.dumps(j, indent=2)
+
+
+class FormatError(PersynError):
+    """errors.hpp FormatError (a malformed file)."""
+
+
+def save_scale_map(path, values: np.ndarray, slant_deg: float, tilt_deg: float, s_min: float,
+                   s_max: float) -> None:
+    """save_scale_map (scale_map.cpp:125-145): "PSM1\\n", a compact JSON header
+    {width, height, sigma, tau, smin, smax}, "\\n", then width*height
+    little-endian float32 values, row-major, bottom row first."""
+    import json as _json
+    v = np.ascontiguousarray(values, dtype="<f4")
+    H, W = v.shape
+    head = _json.dumps({"width": W, "height": H, "sigma": float(slant_deg),
+                        "tau": float(tilt_deg), "smin": float(s_min), "smax": float(s_max)},
+                       separators=(",", ":"))
+    with open(path, "wb") as f:
+        f.write(b"PSM1\n" + head.encode() + b"\n" + v.tobytes())
+
+
+def load_scale_map(path):
+    """load_scale_map (scale_map.cpp:147-201): (values (H, W) float32,
+    (slant, tilt, smin, smax)); FormatError on any malformed container."""
+    import json as _json
+    data = open(path, "rb").read()
+    nl = data.find(b"\n")
+    if nl < 0 or data[:nl] != b"PSM1":
+        raise FormatError(N.PSG_E_FORMAT, f"{path}: missing PSM1 magic line")
+    nl2 = data.find(b"\n", nl + 1)
+    if nl2 < 0:
+        raise FormatError(N.PSG_E_FORMAT, f"{path}: missing PSM1 header line")
+    try:
+        h = _json.loads(data[nl + 1:nl2])
+        W, H = int(h["width"]), int(h["height"])
+        view = (float(h["sigma"]), float(h["tau"]), float(h["smin"]), float(h["smax"]))
+    except (ValueError, KeyError, TypeError) as e:
+        raise FormatError(N.PSG_E_FORMAT, f"{path}: bad PSM1 header: {e}")
+    if W < 1 or H < 1:
+        raise FormatError(N.PSG_E_FORMAT, f"{path}: PSM1 header has empty dimensions")
+    payload = data[nl2 + 1:]
+    if len(payload) < 4 * W * H:
+        raise FormatError(N.PSG_E_FORMAT, f"{path}: truncated PSM1 payload")
+    if len(payload) > 4 * W * H:
+        raise FormatError(N.PSG_E_FORMAT, f"{path}: trailing bytes after PSM1 payload")
+    v = np.frombuffer(payload, dtype="<f4").reshape(H, W).copy()
+    if not np.all((v >= view[2] - 1e-9) & (v <= view[3] + 1e-9)):
+        raise FormatError(N.PSG_E_FORMAT, f"{path}: scale value outside the header bounds")
+    return v, view
+
+
+def _cpp_to_string(v: float) -> str:
+    """std::to_string(double): printf("%f")."""
+    return "%f" % v
+
+
+def modes_to_json(runs) -> str:
+    """modes_to_json (pipeline.cpp:336-346): nlohmann ordered_json dump(2)."""
+    import json as _json
+    return _json.dumps([{"mode": r.name, "wall_millis": r.wall_millis,
+                         "part2_millis": r.part2_millis, "nn_calls": int(r.nn_calls),
+                         "final_energy": r.final_energy} for r in runs], indent=2)
+
+
+def modes_to_csv(runs) -> str:
+    """modes_to_csv (pipeline.cpp:348-357)."""
+    out = "mode,wall_millis,part2_millis,nn_calls,final_energy\n"
+    for r in runs:
+        out += (f"{r.name},{_cpp_to_string(r.wall_millis)},{_cpp_to_string(r.part2_millis)},"
+                f"{int(r.nn_calls)},{_cpp_to_string(r.final_energy)}\n")
+    return out
+
+
+def bench_table(exemplar: np.ndarray, sizes_wh, levels: int, nbhd_sizes, iterations: int,
+                reps: int, seed: int = 0, modes=BENCH_MODES, ctx: Optional[Context] = None):
+    """`persyn bench` (persyn_main.cpp:196-272): per output size and mode,
+    mean / stddev of part-2 milliseconds and mean nn_calls over `reps` seeds;
+    returns (json, csv) in the reference's formats."""
+    import json as _json
+    import math as _math
+    if reps < 1:
+        raise DomainError(N.PSG_E_DOMAIN, "bench needs at least 1 repetition")
+    if not sizes_wh:
+        raise DomainError(N.PSG_E_DOMAIN, "no benchmark sizes given")
+    cfg = OptimizerConfig(max_iterations=iterations, convergence_fraction=1e-6)
+    cells = []
+    for (w, h) in sizes_wh:
+        for m in modes:
+            part2, calls = [], []
+            for rep in range(reps):
+                r = compare_modes(exemplar, w, h, levels, nbhd_sizes, cfg, [m], seed=seed + rep,
+                                  ctx=ctx)[0]
+                part2.append(r.part2_millis)
+                calls.append(float(r.nn_calls))
+            mean = sum(part2) / len(part2)
+            var = sum((v - mean) ** 2 for v in part2)
+            sd = _math.sqrt(var / (len(part2) - 1)) if len(part2) > 1 else 0.0
+            cells.append((f"{w}x{h}", m.name, mean, sd, sum(calls) / len(calls)))
+    js = _json.dumps([{"size": c[0], "mode": c[1], "reps": reps, "mean_ms": c[2],
+                       "stddev_ms": c[3], "mean_nn_calls": c[4]} for c in cells], indent=2) + "\n"
+    csv = "size,mode,reps,mean_ms,stddev_ms,mean_nn_calls\n"
+    for c in cells:
+        csv += (f"{c[0]},{c[1]},{reps},{_cpp_to_string(c[2])},{_cpp_to_string(c[3])},"
+                f"{_cpp_to_string(c[4])}\n")
+    return js, csv
 
 
 def initialize_output(exemplar: np.ndarray, out_scale: np.ndarray, s_min: float, s_max: float,

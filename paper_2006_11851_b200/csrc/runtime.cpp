@@ -1111,6 +1111,37 @@ void upload_state(psg_level& L, const double* host_planes) {
 }  // namespace
 }  // namespace psg
 
+namespace psg {
+// BruteForceIndex over an exemplar already on the device (psg_index_create_brute,
+// psg_synthesize with index_kind = brute force).
+std::unique_ptr<psg_index> create_brute_from_device_planes(psg_ctx* ctx, const double* ex_dev,
+                                                           int C, int ew, int eh, int w,
+                                                           int hist_bins, int hist_include_scale) {
+  if (w < 2 || w % 2) fail(PSG_E_DOMAIN, "neighborhood width must be even and >= 2");
+  if (ew < w || eh < w) fail(PSG_E_DOMAIN, "exemplar smaller than the neighborhood window");
+  auto h = std::make_unique<psg_index>();
+  Index& ix = h->impl;
+  ix.ctx = ctx;
+  ix.brute = true;
+  ix.C = C;
+  ix.w = w;
+  ix.ew = ew;
+  ix.eh = eh;
+  ix.D = w * w * C;
+  ix.nxe = ew - w + 1;
+  ix.N = (int64_t)ix.nxe * (eh - w + 1);
+  ix.ex_mirror = dalloc<float>((size_t)ew * eh * C);
+  launch_make_mirror(ctx, ex_dev, C, ew, eh, ix.ex_mirror);
+  if (C <= 8) {
+    ix.ex_mirror8 = dalloc<float>((size_t)ew * eh * 8);
+    launch_make_mirror8(ctx, ex_dev, C, ew, eh, ix.ex_mirror8);
+  }
+  build_exemplar_hist(ctx, ix, ex_dev, hist_bins, hist_include_scale);
+  brute_prepare(ctx, ix);
+  return h;
+}
+}  // namespace psg
+
 // ===========================================================================
 // C ABI
 // ===========================================================================
@@ -1303,30 +1334,11 @@ psg_status psg_index_create_brute(psg_ctx* ctx, const double* ex_planes, int C, 
     *out = nullptr;
     if (ew < 1 || eh < 1) fail(PSG_E_DOMAIN, "empty exemplar");
     if (C < 4 || C > 8) fail(PSG_E_SHAPE, "channels must be 3 + G with G in [1, 5]");
-    if (w < 2 || w % 2) fail(PSG_E_DOMAIN, "neighborhood width must be even and >= 2");
-    if (ew < w || eh < w) fail(PSG_E_DOMAIN, "exemplar smaller than the neighborhood window");
     psg::DBuf<double> ex((size_t)C * ew * eh);
     ex.upload(ctx, ex_planes, ex.n);
-    auto h = std::make_unique<psg_index>();
-    psg::Index& ix = h->impl;
-    ix.ctx = ctx;
-    ix.brute = true;
-    ix.C = C;
-    ix.w = w;
-    ix.ew = ew;
-    ix.eh = eh;
-    ix.D = w * w * C;
-    ix.nxe = ew - w + 1;
-    ix.N = (int64_t)ix.nxe * (eh - w + 1);
-    ix.ex_mirror = psg::dalloc<float>((size_t)ew * eh * C);
-    psg::launch_make_mirror(ctx, ex.p, C, ew, eh, ix.ex_mirror);
-    if (C <= 8) {
-      ix.ex_mirror8 = psg::dalloc<float>((size_t)ew * eh * 8);
-      psg::launch_make_mirror8(ctx, ex.p, C, ew, eh, ix.ex_mirror8);
-    }
-    psg::build_exemplar_hist(ctx, ix, ex.p, hist_bins, hist_include_scale);
-    psg::brute_prepare(ctx, ix);
-    *out = h.release();
+    *out = psg::create_brute_from_device_planes(ctx, ex.p, C, ew, eh, w, hist_bins,
+                                                hist_include_scale)
+               .release();
   });
 }
 
@@ -1899,6 +1911,7 @@ extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, doubl
     rep.part1_millis = now_ms() - t0;
 
     const double t1 = now_ms();
+    int n_trace = 0;  // iterations recorded into req->trace
     // the previous stage's final assignment seeds each stage's first search
     struct Carry {
       DBuf<int32_t> idx, xs, ys;
@@ -1941,8 +1954,11 @@ extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, doubl
         const int s_d = (s_basis && req->stage_d) ? req->stage_d[s_id] : 0;
         if ((s_mean == nullptr) != (s_basis == nullptr))
           fail(PSG_E_DOMAIN, "stage PCA injection needs both mean and basis");
-        auto index = create_index_from_device_planes(ctx, ex_lv[l].p, C, ew[l], eh[l], w, s_mean,
-                                                     s_basis, s_d, icfg);
+        auto index = req->index_kind == PSG_INDEX_BRUTE_FORCE
+                         ? create_brute_from_device_planes(ctx, ex_lv[l].p, C, ew[l], eh[l], w,
+                                                           icfg.hist_bins, icfg.hist_include_scale)
+                         : create_index_from_device_planes(ctx, ex_lv[l].p, C, ew[l], eh[l], w,
+                                                           s_mean, s_basis, s_d, icfg);
         const double index_ms = now_ms() - ti;
         psg_opt_cfg cfg = req->cfg;
         cfg.spacing = std::max(1, w / 4);
@@ -1987,8 +2003,11 @@ extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, doubl
         int64_t calls = 0;
         const bool verbose = ctx->knobs.verbose;
         std::string its;
+        const int trace_first = n_trace;
         for (int it = 0; it < cfg.max_iterations; ++it) {
           const bool conv = level_step(lv, &last, true);
+          if (req->trace && n_trace < req->trace_cap) req->trace[n_trace] = last;
+          ++n_trace;
           calls += last.nn_calls;
           ++iters;
           if (verbose) its += " " + std::to_string(last.millis).substr(0, 5);
@@ -2022,6 +2041,8 @@ extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, doubl
           sr.nn_calls = calls;
           sr.index_millis = index_ms;
           sr.optimize_millis = now_ms() - to;
+          sr.trace_first = trace_first;
+          sr.trace_count = n_trace - trace_first;
         }
         rep.total_nn_calls += calls;
         rep.final_energy = last.energy;
@@ -2041,6 +2062,7 @@ extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, doubl
       }
     }
     rep.part2_millis = now_ms() - t1;
+    rep.n_trace = n_trace;
     if (ctx->knobs.verbose)
       fprintf(stderr, "[persyn] synthesize: part1 %.2f ms, part2 %.2f ms\n", rep.part1_millis,
               rep.part2_millis);

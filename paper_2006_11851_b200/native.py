@@ -74,20 +74,23 @@ class psg_request(ct.Structure):
                 ("out_h", ct.c_int), ("levels", ct.c_int), ("stages", psg_stage_list),
                 ("cfg", psg_opt_cfg), ("index", psg_index_cfg), ("seed", ct.c_uint64),
                 ("guidance_kind", ct.c_int), ("stage_mean", ct.POINTER(ct.c_void_p)),
-                ("stage_basis", ct.POINTER(ct.c_void_p)), ("stage_d", ct.POINTER(ct.c_int))]
+                ("stage_basis", ct.POINTER(ct.c_void_p)), ("stage_d", ct.POINTER(ct.c_int)),
+                ("index_kind", ct.c_int), ("trace", ct.c_void_p), ("trace_cap", ct.c_int)]
 
 
 class psg_stage_report(ct.Structure):
     _fields_ = [("level", ct.c_int), ("w", ct.c_int), ("W", ct.c_int), ("H", ct.c_int),
                 ("ew", ct.c_int), ("eh", ct.c_int), ("d", ct.c_int), ("iterations", ct.c_int),
                 ("final_energy", ct.c_double), ("nn_calls", ct.c_int64),
-                ("index_millis", ct.c_double), ("optimize_millis", ct.c_double)]
+                ("index_millis", ct.c_double), ("optimize_millis", ct.c_double),
+                ("trace_first", ct.c_int), ("trace_count", ct.c_int)]
 
 
 class psg_report(ct.Structure):
     _fields_ = [("n_stages", ct.c_int), ("stages", psg_stage_report * 16),
                 ("part1_millis", ct.c_double), ("part2_millis", ct.c_double),
-                ("total_nn_calls", ct.c_int64), ("final_energy", ct.c_double)]
+                ("total_nn_calls", ct.c_int64), ("final_energy", ct.c_double),
+                ("n_trace", ct.c_int)]
 
 
 VP = ct.c_void_p
