@@ -352,7 +352,7 @@ typedef struct {
   const double* const* stage_mean;
   const double* const* stage_basis;
   const int* stage_d;
-  int index_kind;          /* psg_index_kind (IndexKind, pipeline.hpp:13-16) */
+  int index_kind;          /* a psg_index_kind: IndexKind, pipeline.hpp:13-16 */
   psg_iter_stats* trace;   /* optional [trace_cap]: every stage's iterations, in order */
   int trace_cap;
 } psg_request;
