@@ -428,8 +428,14 @@ static void launch_project(psg_ctx* ctx, const float* src, int img_w, int C, int
     PSG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     k<<<blocks, 256, sm, ctx->stream>>>(src, img_w, C, w, xs, ys, nx, n, D, JC, mean, basisT, d,
                                          out);
+  } else if (d <= kMaxDP) {
+    const size_t sm = sizeof(double) * ((size_t)TQ * JCp + (size_t)JC * 128);
+    auto k = project_kernel<4, RQ, kWindows>;
+    PSG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k<<<blocks, 256, sm, ctx->stream>>>(src, img_w, C, w, xs, ys, nx, n, D, JC, mean, basisT, d,
+                                         out);
   } else {
-    fail(PSG_E_DOMAIN, "retained PCA dimension > 64 is not supported");
+    fail(PSG_E_DOMAIN, "retained PCA dimension > 128 is not supported");
   }
   PSG_LAUNCHED(ctx);
 }
@@ -458,7 +464,7 @@ void launch_project_vectors(psg_ctx* ctx, const float* X, int64_t n, int D, cons
 constexpr int kSearchWarps = 4;
 constexpr int kStack = 512;   // warp-per-query kernel (deep imported trees, backtrack frontier)
 constexpr int kStackX = 256;  // search_exact_kernel
-constexpr int kMaxD = 64;
+constexpr int kMaxD = kMaxDP;  // the warp kernels; the tile kernel takes d <= 64
 
 struct WarpLexMin {
   double d2;
@@ -1625,7 +1631,7 @@ static int tile_resident_ctas(psg_ctx* ctx) {
 }
 
 bool search_uses_tiles(psg_ctx* ctx, const DevTree& tree, int d, bool exact) {
-  return exact && d <= kMaxD && tree.centroid32 && !ctx->knobs.legacy_search &&
+  return exact && d <= 64 && tree.centroid32 && !ctx->knobs.legacy_search &&
          tree.max_children <= kTileMaxB && 1 + tree.max_depth * (tree.max_children - 1) <= kTileStack;
 }
 
@@ -1641,13 +1647,15 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
     const int64_t blocks = 32;  // re-searches are rare: a few hundred warps
     if (a.d <= 32)
       search_exact_kernel<32><<<(int)blocks, 256, 0, ctx->stream>>>(a);
-    else
+    else if (a.d <= 64)
       search_exact_kernel<64><<<(int)blocks, 256, 0, ctx->stream>>>(a);
+    else
+      search_exact_kernel<kMaxDP><<<(int)blocks, 256, 0, ctx->stream>>>(a);
     PSG_LAUNCHED(ctx);
     return;
   }
-  if (a.d > kMaxD) fail(PSG_E_DOMAIN, "retained PCA dimension > 64 is not supported");
-  const bool tile_ok = a.tree.max_children <= kTileMaxB &&
+  if (a.d > kMaxD) fail(PSG_E_DOMAIN, "retained PCA dimension > 128 is not supported");
+  const bool tile_ok = a.d <= 64 && a.tree.max_children <= kTileMaxB &&
                        1 + a.tree.max_depth * (a.tree.max_children - 1) <= kTileStack;
   if (a.mode == PSG_EXACT && a.proj32_q4 && a.tree.centroid32 && tile_ok && !ctx->knobs.legacy_search) {
     if (!a.sched) fail(PSG_E_LOGIC, "tile search launched without its scheduler counters");
@@ -1671,14 +1679,17 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
     if (blocks > cap) blocks = cap;
     if (a.d <= 32)
       search_exact_kernel<32><<<(int)blocks, 256, 0, ctx->stream>>>(a);
-    else
+    else if (a.d <= 64)
       search_exact_kernel<64><<<(int)blocks, 256, 0, ctx->stream>>>(a);
+    else
+      search_exact_kernel<kMaxDP><<<(int)blocks, 256, 0, ctx->stream>>>(a);
     PSG_LAUNCHED(ctx);
     return;
   }
   // thread-per-query kernel for greedy and short backtracks; longer frontiers
-  // (m > 2) spill the per-thread heap and run faster warp-per-query
-  if (a.mode != PSG_EXACT && !ctx->knobs.legacy_search &&
+  // (m > 2) spill the per-thread heap and run faster warp-per-query (as does
+  // d > 64: the per-thread query would not fit the register file)
+  if (a.mode != PSG_EXACT && !ctx->knobs.legacy_search && a.d <= 64 &&
       (a.mode == PSG_GREEDY || a.max_leaves <= 2)) {
     int64_t blocks = (a.nq + 127) / 128;
     const int64_t cap = (int64_t)ctx->num_sms * 64;

@@ -360,7 +360,7 @@ void fit_pca_device(psg_ctx* ctx, Index& ix, const psg_index_cfg& cfg) {
     retained = std::min(retained, ne);
     if (cfg.d_cap > 0) retained = std::min(retained, cfg.d_cap);
   }
-  if (retained > 64) fail(PSG_E_DOMAIN, "retained PCA dimension > 64 is not supported");
+  if (retained > kMaxDP) fail(PSG_E_DOMAIN, "retained PCA dimension > 128 is not supported");
 
   // eigenvector of the k-th largest: column (ne-1-k) of the column-major result
   std::vector<double> basis((size_t)retained * D);

@@ -11,6 +11,9 @@
 #include "persyn_b200.h"
 
 namespace psg {
+// largest retained PCA dimension (the warp search kernels and the fp64
+// projection; the tile search and the tensor-core projection take d <= 64)
+constexpr int kMaxDP = 128;
 
 // ---- error plumbing (status codes of include/persyn_b200.h) -----------------
 struct Error : std::runtime_error {

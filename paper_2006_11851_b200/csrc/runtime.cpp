@@ -230,7 +230,7 @@ void upload_tree(psg_ctx* ctx, Index& ix) {
   ix.proj_soa = dalloc<double>((size_t)ix.N * (d > 0 ? d : 1));
   launch_gather_soa(ctx, ix.proj, ix.N, d, ix.perm, ix.proj_soa);
   // fp32 bound/filter copies (conservative rounding, see search_exact_kernel)
-  ix.dp = d <= 32 ? 32 : 64;
+  ix.dp = d <= 32 ? 32 : (d <= 64 ? 64 : kMaxDP);
   ix.proj32_q4 = dalloc<float>((size_t)ix.N * ix.dp);
   ix.pnorm32 = dalloc<float>(ix.N);
   launch_make_fp32_copies(ctx, ix.proj_soa, ix.N, d, ix.dp, ix.proj32_q4, ix.pnorm32);
@@ -301,7 +301,7 @@ void finish_index(psg_ctx* ctx, Index& ix, const double* mean, const double* bas
     t_phase = t;
   };
   if (basis) {
-    if (d < 0 || d > 64) fail(PSG_E_DOMAIN, "injected PCA dimension must be in [0, 64]");
+    if (d < 0 || d > kMaxDP) fail(PSG_E_DOMAIN, "injected PCA dimension must be in [0, 128]");
     ix.h_mean.assign(mean, mean + D);
     ix.h_basis.assign(basis, basis + (size_t)d * D);
     ix.h_var.assign(D, 0.0);
@@ -315,7 +315,7 @@ void finish_index(psg_ctx* ctx, Index& ix, const double* mean, const double* bas
   PSG_CUDA(cudaMemcpyAsync(ix.mean, ix.h_mean.data(), sizeof(double) * D, cudaMemcpyHostToDevice,
                            ctx->stream));
   // transposed, zero-padded basis [D][KP] for the projection kernel
-  const int KP = d <= 32 ? 32 : 64;
+  const int KP = d <= 32 ? 32 : (d <= 64 ? 64 : kMaxDP);
   std::vector<double> bt((size_t)D * KP, 0.0);
   for (int k = 0; k < d; ++k)
     for (int j = 0; j < D; ++j) bt[(size_t)j * KP + k] = ix.h_basis[(size_t)k * D + j];

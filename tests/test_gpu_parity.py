@@ -373,3 +373,43 @@ def test_optimize_level_cfg1_finest_stage_matches_reference(gpu_ctx, port, ref):
     for s, r in zip(stats, st_r):
         assert s.changed == r[2] and s.nn_calls == r[3]
         assert abs(s.energy - r[1]) <= 1e-4 * abs(r[1])
+
+
+@pytest.mark.parametrize("d", [80, 128])
+def test_retained_dim_above_64(gpu_ctx, port, ref, d):
+    """d in (64, 128]: the warp search kernel and the fp64 projection (the tile
+    kernel and the tensor-core projection take d <= 64): still bit-exact."""
+    ex, init = _stage(size=40, out=56)
+    cand, mean, basis, proj = _injected(port, ex, 8, d)
+    ix = api.make_pca_tree_index(ex, 8, mean=mean, basis=basis, branching=8, max_depth=3,
+                                 hist_bins=16, ctx=gpu_ctx)
+    assert ix.retained_dim == d and np.array_equal(ix.projected(), proj)
+    idx, dist, calls, _ = api.search_step(init, ix, 2, 2, api.QueryBudget.exact())
+    i_p, d_p, c_p = port.search_step(init, 8, 2, 2, cand, proj, mean, basis)
+    assert calls == c_p and np.array_equal(idx, i_p) and np.array_equal(dist, d_p)
+    b_idx, b_d, _, _ = api.search_step(init, ix, 2, 2, api.QueryBudget.backtrack(ix.n_leaves))
+    assert np.array_equal(b_idx, i_p)
+    h = ref.index_create(ex, 8, mean, basis, kind="tree", branching=8, seed=1)
+    cfg = api.OptimizerConfig(max_iterations=2, min_iterations=2, convergence_fraction=1e-9,
+                              nbhd_width=8, spacing=2, patch_width=2,
+                              budget=api.QueryBudget.exact())
+    out, stats = api.optimize_level(init, ix, cfg)
+    out_r, st_r, _ = h.optimize_level(init, 8, 2, 2, max_it=2, min_it=2, frac=1e-9, bins=16,
+                                      hist_on=True, mode="exact")
+    assert np.max(np.abs(out - out_r)) <= 1.0 / 255
+    assert [s.changed for s in stats] == [int(r[2]) for r in st_r]
+
+
+def test_variance_rule_may_retain_more_than_64(gpu_ctx, port):
+    """A high variance target on a 16x16 window keeps more than 64 components
+    (the reference has no cap): the device fit and search follow."""
+    ex, init = _stage(size=48, out=64)
+    ix = api.make_pca_tree_index(ex, 16, variance_target=0.98, branching=8, max_depth=3,
+                                 ctx=gpu_ctx)
+    assert 64 < ix.retained_dim <= 128
+    mean, basis, _ = ix.pca()
+    cand = port.extract_all(ex, 16, 1)
+    proj = port.project_all(cand, mean, basis)
+    idx, dist, _, _ = api.search_step(init, ix, 4, 2, api.QueryBudget.exact())
+    i_p, d_p, _ = port.search_step(init, 16, 4, 2, cand, proj, mean, basis)
+    assert np.array_equal(idx, i_p) and np.array_equal(dist, d_p)
