@@ -23,7 +23,7 @@
 // (bounded below).  Per k:
 //   |q^_k - q_k| <= 2^-30 |B_k|_1 + 2^-31 D + 2^-59 32640 513 D
 //                   + (2D + 2) 2^-53 |B_k|_1 + 2^-52 (|B mu_k| + |B_k|_1)
-//                   + 20 D 2^-53 (combining the digit products in fp64) + 1e-12
+//                   + 20 D 2^-53 (the final fp64 conversion, generous) + 1e-12
 // (|v - mu| <= 1 bounds |q_k| by |B_k|_1; the reference's own chain is within
 // (2D + 2) 2^-53 |B_k|_1 of the exact value), and delta = the 2-norm over k:
 // about 1e-6 at w = 8, d = 32, so only true near-ties reach the fallback.
@@ -33,7 +33,7 @@
 // 16-byte K groups are consecutive 16-byte blocks: one 1-D bulk copy per slice
 // and group), staged in the UMMA K-major no-swizzle layout (K group g of the
 // 128 anchors = one contiguous 2 KB block).  Persistent, warp-specialised:
-// warp 0 stages, warp 1 issues the UMMAs, warps 2-5 drain TMEM.  Basis rows
+// warp 0 stages, warp 1 issues the UMMAs, warps 2-9 drain TMEM.  Basis rows
 // go in blocks of 32 (TMEM holds 416 accumulator columns per block).
 #include <algorithm>
 #include <cmath>
@@ -57,9 +57,21 @@ constexpr uint32_t kASlice = kGC * kAGroup;     // 8 KB per slice per stage
 constexpr uint32_t kBStage = kGC * kNP * 16;    // 8 KB per stage
 constexpr uint32_t kStageBytes = kSA * kASlice + kBStage;  // 40 KB
 constexpr int kStages = 5;
-constexpr int kTcThreads = 192;
+constexpr int kTcThreads = 320;  // producer, MMA issuer, 8 epilogue warps
 constexpr uint32_t kBarOff = kStages * kStageBytes;
-constexpr uint32_t kSmemBytes = kBarOff + (2 * kStages + 2) * 8 + 16;
+constexpr uint32_t kSmemBytes = kBarOff + (2 * kStages + 3) * 8 + 16;
+// strip mode (spacing 2, w % 4 == 0, one basis block, w <= 8): the basis digits
+// stay resident (<= 64 KB) and a stage is ONE window row of the tile: per digit
+// slice the contiguous strip of 2 (nt - 1) + w pixels.  K group g' of that row
+// is the strip at byte offset 16 g' (row m at 16 m): the UMMA descriptor points
+// into the strip with a 16-byte leading-dimension offset, so each row is
+// copied once instead of once per K group (w / 2 times).
+constexpr uint32_t kBresBytes = 64 * 1024;
+constexpr uint32_t kStripSlot = 2304;                // >= 16 * 127 + 8 * 8
+constexpr int kStripStages = 8;
+constexpr uint32_t kStripStage = kSA * kStripSlot;
+constexpr uint32_t kStripBarOff = kBresBytes + kStripStages * kStripStage;
+constexpr uint32_t kStripSmemBytes = kStripBarOff + (2 * kStripStages + 3) * 8 + 16;
 // kept products per A slice s: t in [tmin(s), 4); TMEM columns [col0(s), +32 (4 - tmin))
 __host__ __device__ constexpr int tmin_of(int s) { return s == 0 ? 2 : (s == 1 ? 1 : 0); }
 __host__ __device__ constexpr int col0_of(int s) { return s == 0 ? 0 : (s == 1 ? 64 : 160 + (s - 2) * 128); }
@@ -143,13 +155,16 @@ struct TcArgs {
 };
 
 // A work item = (tile of <= 128 consecutive anchors of one anchor row, basis block).
+template <bool kStrip>
 __global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBarOff);
-  uint64_t* empty = full + kStages;
-  uint64_t* tfull = empty + kStages;
+  constexpr int S = kStrip ? kStripStages : kStages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (kStrip ? kStripBarOff : kBarOff));
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  uint64_t* bfull = tempty + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -158,12 +173,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(TcArgs a) {
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 32) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < S; ++s) {
       mma::mbar_init(&full[s], 1);
       mma::mbar_init(&empty[s], 1);
     }
     mma::mbar_init(tfull, 1);
-    mma::mbar_init(tempty, 4);
+    mma::mbar_init(tempty, 8);
+    mma::mbar_init(bfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   mma::fence_before();
@@ -178,7 +194,70 @@ __global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(TcArgs a) {
   const int n_groups = a.kb >> 4;          // per slice
   const int n_chunks = (n_groups + kGC - 1) / kGC;
 
-  if (warp == 0) {
+  if (kStrip && warp == 0) {
+    // ---- producer (strip mode): the basis once, then one window row per stage --------
+    if (lane == 0) {
+      mma::mbar_expect_tx(bfull, (uint32_t)(n_groups * kNP * 16));
+      mma::bulk_g2s(smem, a.bop, n_groups * kNP * 16, bfull);
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int iy = (int)(it / tpr), ix0 = (int)(it - (int64_t)iy * tpr) * kTM;
+        const int nt = min(kTM, a.nx - ix0);
+        const int ay = a.ys[iy], x0 = a.xs[ix0];
+        const uint32_t len = (uint32_t)(16 * (nt - 1) + 8 * a.w);
+        for (int dy = 0; dy < a.w; ++dy) {
+          mma::mbar_wait(&empty[stage], ph ^ 1u);
+          uint8_t* A = smem + kBresBytes + stage * kStripStage;
+          mma::mbar_expect_tx(&full[stage], kSA * len);
+          const int64_t off = ((int64_t)(ay + dy) * a.img_w + x0) * 8;
+          for (int s = 0; s < kSA; ++s)
+            mma::bulk_g2s(A + s * kStripSlot, a.q8 + s * a.slice_bytes + off, len, &full[stage]);
+          if (++stage == S) {
+            stage = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (kStrip && warp == 1) {
+    // ---- MMA issuer (strip mode) -------------------------------------------------------
+    if (lane == 0) {
+      mma::mbar_wait(bfull, 0);
+      int stage = 0;
+      uint32_t ph = 0, tph = 0;
+      const int ksr = gpr >> 1;  // K steps per window row
+      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+        mma::mbar_wait(tempty, tph ^ 1u);
+        mma::fence_after();
+        for (int dy = 0; dy < a.w; ++dy) {
+          mma::mbar_wait(&full[stage], ph);
+          mma::fence_after();
+          const uint8_t* A = smem + kBresBytes + stage * kStripStage;
+          for (int ks = 0; ks < ksr; ++ks) {
+            const int g = dy * gpr + 2 * ks;
+#pragma unroll
+            for (int s = 0; s < kSA; ++s) {
+              const int t0 = tmin_of(s), n = (kSB - t0) * kNB;
+              const uint64_t ad =
+                  mma::make_desc(mma::smem_u32(A + s * kStripSlot) + 32 * ks, 16, 128);
+              const uint64_t bd = mma::make_desc(
+                  mma::smem_u32(smem) + (g * kNP + t0 * kNB) * 16, kNP * 16, 128);
+              mma_i8(tmem + (uint32_t)col0_of(s), ad, bd, idesc_i8(kTM, n),
+                     (dy | ks) ? 1u : 0u);
+            }
+          }
+          mma::commit(&empty[stage]);
+          if (++stage == S) {
+            stage = 0;
+            ph ^= 1u;
+          }
+        }
+        mma::commit(tfull);
+        tph ^= 1u;
+      }
+    }
+  } else if (warp == 0) {
     // ---- producer ---------------------------------------------------------------------
     int stage = 0;
     uint32_t ph = 0;
@@ -274,8 +353,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(TcArgs a) {
       }
     }
   } else {
-    // ---- epilogue: warp (w & 3) owns TMEM lanes 32 (w & 3) .. + 31 --------------------
-    const int lg = warp & 3;
+    // ---- epilogue: warp w (2..9) owns TMEM lanes 32 (w & 3) .. + 31 and basis
+    // columns [16 h, 16 h + 16), h = (w - 2) / 4.  The digit products are
+    // combined EXACTLY in two int64 halves, q^ 2^59 = P_hi 2^32 + P_lo
+    // (|P_lo| < 2^54, |P_hi| < 2^44), so TMEM is released right after the loads
+    // and the next tile's MMAs overlap the conversion and the stores.
+    const int lg = warp & 3, h = (warp - 2) >> 2;
     const bool bad = *a.bad != 0;
     uint32_t tph = 0;
     for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
@@ -289,22 +372,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(TcArgs a) {
       const bool valid = ix0 + m < a.nx;
       const int64_t q = (int64_t)iy * a.nx + ix0 + m;
       const uint32_t base = tmem + ((uint32_t)(lg * 32) << 16);
-      double acc[kNB];
+      long long plo[16], phi[16];
 #pragma unroll
-      for (int n = 0; n < kNB; ++n) acc[n] = 0.0;
-      // sum_{s,t} 256^(s+t) D(s,t) 2^-59: every term exact, a few fp64 roundings
+      for (int n = 0; n < 16; ++n) plo[n] = phi[n] = 0;
 #pragma unroll
       for (int s = 0; s < kSA; ++s) {
 #pragma unroll
         for (int tt = tmin_of(s); tt < kSB; ++tt) {
-          const double sc = ldexp(1.0, 8 * (s + tt) - 59);
+          int32_t r[16];
+          tmem_ld16(base + (uint32_t)(col0_of(s) + (tt - tmin_of(s)) * kNB + 16 * h), r);
+          tmem_wait_ld();
+          const int u = s + tt;
 #pragma unroll
-          for (int h = 0; h < kNB; h += 16) {
-            int32_t r[16];
-            tmem_ld16(base + (uint32_t)(col0_of(s) + (tt - tmin_of(s)) * kNB + h), r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 16; ++i) acc[h + i] = dadd(acc[h + i], dmul((double)r[i], sc));
+          for (int i = 0; i < 16; ++i) {
+            if (u <= 3) plo[i] += (long long)r[i] << (8 * u);
+            else phi[i] += (long long)r[i] << (8 * (u - 4));
           }
         }
       }
@@ -312,12 +394,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(TcArgs a) {
       __syncwarp();
       if (lane == 0) mma::mbar_arrive(tempty);
       if (valid) {
-        const int k0 = kblk * kNB;
+        const int k0 = kblk * kNB + 16 * h;
         double* orow = a.out + q * a.d + k0;
 #pragma unroll
-        for (int n = 0; n < kNB; ++n)
-          if (k0 + n < a.d) orow[n] = dsub(acc[n], a.bmu[k0 + n]);
-        if (kblk == 0) a.delta_out[q] = bad ? __int_as_float(0x7f800000) : a.delta;
+        for (int n = 0; n < 16; ++n)
+          if (k0 + n < a.d) {
+            const double qh = dadd((double)phi[n] * 0x1p-27, (double)plo[n] * 0x1p-59);
+            orow[n] = dsub(qh, a.bmu[k0 + n]);
+          }
+        if (kblk == 0 && h == 0) a.delta_out[q] = bad ? __int_as_float(0x7f800000) : a.delta;
       }
     }
   }
@@ -341,7 +426,7 @@ constexpr int kListWarps = 8, kListChunk = 128;
 __device__ __forceinline__ double dist2_chain(const double* q, const double* p, int d) {
   double acc = 0.0;
   for (int j = 0; j < d; ++j) {
-    const double t = dsub(q[j], __ldg(p + j));
+    const double t = dsub(q[j], p[j]);
     acc = dadd(acc, dmul(t, t));
   }
   return acc;
@@ -352,6 +437,7 @@ __global__ void __launch_bounds__(32 * kListWarps) resolve_kernel(
     int D, int d, const double* __restrict__ proj) {
   __shared__ double cs_all[kListWarps][kListChunk];
   __shared__ double qs_all[kListWarps][64];
+  __shared__ double ps_all[kListWarps][2][64];  // the two band candidates' rows
   const int n = *r.count;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* cs = cs_all[warp];
@@ -394,8 +480,14 @@ __global__ void __launch_bounds__(32 * kListWarps) resolve_kernel(
     __syncwarp();
     const int32_t c0 = r.c0[i], c1 = r.c1[i];
     if (c1 >= 0) {
+      double(*ps)[64] = ps_all[warp];
+      for (int j = lane; j < d; j += 32) {  // coalesced rows, then the chains from SMEM
+        ps[0][j] = __ldg(proj + (int64_t)c0 * d + j);
+        ps[1][j] = __ldg(proj + (int64_t)c1 * d + j);
+      }
+      __syncwarp();
       double dd = 0.0;
-      if (lane < 2) dd = dist2_chain(qs, proj + (int64_t)(lane ? c1 : c0) * d, d);
+      if (lane < 2) dd = dist2_chain(qs, ps[lane], d);
       const double d1 = __shfl_sync(0xffffffffu, dd, 1);
       if (lane == 0) {
         const bool take1 = d1 < dd || (d1 == dd && c1 < c0);
@@ -502,8 +594,8 @@ bool tc_prepare(psg_ctx* ctx, Index& ix) {
 }
 
 void launch_project_windows_tc(psg_ctx* ctx, const uint8_t* q8, int64_t slice_bytes, int img_w,
-                               const int* bad, AnchorSet anchors, const Index& ix, double* out,
-                               float* delta) {
+                               const int* bad, AnchorSet anchors, bool stride2, const Index& ix,
+                               double* out, float* delta) {
   ProfScope _prof(ctx, K_PROJECT);
   if (anchors.count <= 0) return;
   if (!ix.tc) fail(PSG_E_LOGIC, "tensor-core projection without a prepared basis");
@@ -526,13 +618,22 @@ void launch_project_windows_tc(psg_ctx* ctx, const uint8_t* q8, int64_t slice_by
   a.delta_out = delta;
   static bool attr = false;
   if (!attr) {
-    PSG_CUDA(cudaFuncSetAttribute(project_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kSmemBytes));
+    PSG_CUDA(cudaFuncSetAttribute(project_tc_kernel<false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
+    PSG_CUDA(cudaFuncSetAttribute(project_tc_kernel<true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kStripSmemBytes));
     attr = true;
   }
-  const int64_t items = (int64_t)((a.nx + kTM - 1) / kTM) * a.ny * ((a.d + kNB - 1) / kNB);
+  const int nkb = (a.d + kNB - 1) / kNB;
+  const int64_t items = (int64_t)((a.nx + kTM - 1) / kTM) * a.ny * nkb;
   const int blocks = (int)std::min<int64_t>(items, ctx->num_sms);
-  project_tc_kernel<<<blocks, kTcThreads, kSmemBytes, ctx->stream>>>(a);
+  const bool strip = stride2 && nkb == 1 && a.w % 4 == 0 && a.w <= 8 && (img_w & 1) == 0 &&
+                     (uint32_t)(a.kb / 16) * kNP * 16 <= kBresBytes;
+  if (strip)
+    project_tc_kernel<true><<<blocks, kTcThreads, kStripSmemBytes, ctx->stream>>>(a);
+  else
+    project_tc_kernel<false><<<blocks, kTcThreads, kSmemBytes, ctx->stream>>>(a);
   PSG_LAUNCHED(ctx);
 }
 

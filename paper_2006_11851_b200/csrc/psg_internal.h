@@ -311,9 +311,11 @@ bool tc_prepare(psg_ctx* ctx, Index& ix);
 // q^ = B^ v^ - B.mu on the tensor cores (tcgen05.mma kind::i8, exact int32
 // accumulation), delta[q] = a rigorous bound on |q^ - q| (2-norm; +inf when a
 // window holds a value outside [0, 1]).  out [n][d] fp64.
+// stride2: every anchor x is even and consecutive anchors are 2 pixels apart
+// (spacing 2, W - w even): the strip-mode kernel applies.
 void launch_project_windows_tc(psg_ctx* ctx, const uint8_t* q8, int64_t slice_bytes, int img_w,
-                               const int* bad, AnchorSet anchors, const Index& ix, double* out,
-                               float* delta);
+                               const int* bad, AnchorSet anchors, bool stride2, const Index& ix,
+                               double* out, float* delta);
 // Exact fallback for the ambiguous queries of an approximate search (count
 // read on the device): the reference's projection chain of each listed
 // window, then either the exact lexicographic min over its two band

@@ -455,6 +455,7 @@ struct psg_level {
   int slots = 3;
   bool primed = false;
   bool scanned_valid = false;  // L.scanned holds a search of these anchors (tile order)
+  bool stride2 = false;        // anchor columns 0, 2, 4, ... (tensor-core strip mode)
   int iter = 0;
   int64_t pending_calls = 0, pending_scanned = 0;
   double pending_ms = 0.0;
@@ -527,6 +528,8 @@ void level_setup_band(psg_level& L, psg_ctx* ctx, const Index& ix, const psg_ban
   for (int iy = b.hlo; iy < b.a1; ++iy) hy.push_back(hyg[iy] - b.p0);
   L.nx = (int)hx.size();
   L.ny = (int)hy.size();
+  L.stride2 = !hx.empty() && hx[0] % 2 == 0;
+  for (size_t i = 1; i < hx.size(); ++i) L.stride2 = L.stride2 && hx[i] - hx[i - 1] == 2;
   L.nh = b.a0 - b.hlo;
   L.A = (int64_t)L.nx * L.ny;
   L.off = (int64_t)L.nh * L.nx;
@@ -678,8 +681,8 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
     PSG_CUDA(cudaMemsetAsync(L.amb_n.p, 0, sizeof(int), ctx->stream));
     PSG_CUDA(cudaMemsetAsync(L.full_n.p, 0, sizeof(int), ctx->stream));
     launch_make_digits(ctx, L.mirror.p, L.C, L.W, L.Hl, L.q8.p, q8_slice, L.q8_bad.p);
-    launch_project_windows_tc(ctx, L.q8.p, q8_slice, L.W, L.q8_bad.p, as, ix, L.qproj.p,
-                              L.qdelta.p);
+    launch_project_windows_tc(ctx, L.q8.p, q8_slice, L.W, L.q8_bad.p, as, L.stride2, ix,
+                              L.qproj.p, L.qdelta.p);
   } else if (ix.d > 0) {
     launch_project_windows(ctx, L.mirror.p, L.W, L.C, L.w, as, ix.mean, ix.basis, ix.d, L.qproj.p);
   }
@@ -2168,7 +2171,9 @@ extern "C" psg_status psg_debug_projection(psg_ctx* ctx, const psg_index* index,
     PSG_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), ctx->stream));
     launch_make_digits(ctx, mir.p, ix.C, W, H, q8.p, P * 8, bad.p);
     const AnchorSet as{xs.p, ys.p, (int)hx.size(), A};
-    launch_project_windows_tc(ctx, q8.p, P * 8, W, bad.p, as, ix, qt.p, dl.p);
+    bool stride2 = hx[0] % 2 == 0;
+    for (size_t i = 1; i < hx.size(); ++i) stride2 = stride2 && hx[i] - hx[i - 1] == 2;
+    launch_project_windows_tc(ctx, q8.p, P * 8, W, bad.p, as, stride2, ix, qt.p, dl.p);
     launch_project_windows(ctx, mir.p, W, ix.C, ix.w, as, ix.mean, ix.basis, ix.d, qe.p);
     if (q_tc) qt.download(ctx, q_tc, qt.n);
     if (delta) dl.download(ctx, delta, dl.n);

@@ -35,6 +35,9 @@ def main():
     for k in KEYS:
         if k in d:
             summary["metrics"][k] = {"value": d[k], "unit": u.get(k, "")}
+    for k in d:  # tensor sub-pipes (UTCIMMA / UTCHMMA activity)
+        if "pipe_tensor" in k and ("pct" in k or k.endswith(".avg")):
+            summary["metrics"][k] = {"value": d[k], "unit": u.get(k, "")}
     stalls = {k.replace("smsp__pcsamp_warps_issue_stalled_", ""): float(v.replace(",", ""))
               for k, v in d.items()
               if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")
