@@ -359,7 +359,13 @@ __global__ void __launch_bounds__(256) mstep_kernel(MstepArgs a) {
       v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);  // std::clamp(.., 0, 1)
       a.planes[c * PS + pix] = v;
       if (a.mirror) a.mirror[pix * C + c] = (float)v;
-      if (a.counts && c < a.slots) atomicAdd(&hist_s[c * a.bins + bin_of_f64(v, a.bins)], 1u);
+      if (a.counts && c < a.slots) {
+        // lanes with the same bin add once (neighbouring pixels share bins:
+        // unaggregated shared-memory atomics serialise)
+        const int key = c * a.bins + bin_of_f64(v, a.bins);
+        const unsigned peers = __match_any_sync(__activemask(), key);
+        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist_s[key], (unsigned)__popc(peers));
+      }
     }
   }
   if (a.counts) {  // same integer counts as hist_count_kernel over the written rows
@@ -374,7 +380,9 @@ void launch_mstep(psg_ctx* ctx, const MstepArgs& a) {
   const int64_t P = (int64_t)a.W * a.H;
   if (P <= 0) return;
   if (a.C > 8) fail(PSG_E_DOMAIN, "more than 8 channels are not supported");
-  const int blocks = grid_for(ctx, P, 256, 16);
+  // one pixel per thread: with the fused histogram every block ends in a
+  // barrier, and a grid-stride remainder would leave most threads waiting there
+  const int blocks = grid_for(ctx, P, 256, 1 << 20);
   size_t sm = 0;
   if (a.counts) {
     if (a.slots > a.C) fail(PSG_E_DOMAIN, "histogram slots exceed the channel count");

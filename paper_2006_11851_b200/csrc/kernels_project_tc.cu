@@ -457,13 +457,23 @@ __global__ void __launch_bounds__(32 * kListWarps) resolve_kernel(
         cs[t] = dsub((double)v, __ldg(mean + j));
       }
       __syncwarp();
+      // basis loads software-pipelined one 8-element batch ahead of the chain
       const double* bt = basisT + (int64_t)j0 * KP + lane;
+      double n0[8], n1[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        n0[u] = u < jn ? __ldg(bt + (int64_t)u * KP) : 0.0;
+        n1[u] = (KP > 32 && u < jn) ? __ldg(bt + (int64_t)u * KP + 32) : 0.0;
+      }
       for (int t0 = 0; t0 < jn; t0 += 8) {
         double b0[8], b1[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          b0[u] = t0 + u < jn ? __ldg(bt + (int64_t)(t0 + u) * KP) : 0.0;
-          b1[u] = (KP > 32 && t0 + u < jn) ? __ldg(bt + (int64_t)(t0 + u) * KP + 32) : 0.0;
+          b0[u] = n0[u];
+          b1[u] = n1[u];
+          const int tn = t0 + 8 + u;
+          n0[u] = tn < jn ? __ldg(bt + (int64_t)tn * KP) : 0.0;
+          n1[u] = (KP > 32 && tn < jn) ? __ldg(bt + (int64_t)tn * KP + 32) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
