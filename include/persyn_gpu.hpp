@@ -94,18 +94,23 @@ inline std::vector<double> masses_of(const HistogramSet& h) {
 class GpuSearchIndex final : public SearchIndex {
  public:
   // make_pca_tree_index(extract_all(exemplar, {w, 1, ..}), variance,
-  // branching, seed) (optimizer.cpp:256-262): PCA fit, projection and tree
-  // build on the device; d_cap > 0 caps the retained dimension.
+  // branching, seed) (optimizer.cpp:256-262): PCA fit and projection on the
+  // device, and the reference's own KmTree::build (km_tree.cpp:141-195,
+  // replayed with the same mt19937_64 stream: greedy / backtrack answers are
+  // the reference's for the same PCA model); d_cap > 0 caps the retained
+  // dimension; tree_kind = PSG_TREE_DEVICE builds the device tree instead.
   static std::unique_ptr<GpuSearchIndex> pca_tree(Context& ctx, const RgbsImage& exemplar, int w,
                                                   double variance_target = 0.95,
                                                   int branching = 4, std::uint64_t seed = 0,
-                                                  int d_cap = 0, int hist_bins = 16) {
+                                                  int d_cap = 0, int hist_bins = 16,
+                                                  int tree_kind = PSG_TREE_REFERENCE) {
     psg_index_cfg cfg{};
     cfg.variance_target = variance_target;
     cfg.d_cap = d_cap;
     cfg.branching = branching;
     cfg.seed = seed;
     cfg.hist_bins = hist_bins;
+    cfg.tree_kind = tree_kind;
     const auto planes = planes_of(exemplar);
     psg_index* h = nullptr;
     check(psg_index_create(ctx.get(), planes.data(), 4, exemplar.width(), exemplar.height(), w,
