@@ -235,72 +235,105 @@ void launch_eff_gather(psg_ctx* ctx, const double* irls, const double* table, co
 }
 
 // ---- M-step: gather form ----------------------------------------------------------
-// One thread per output pixel.  The reference scatters anchors in ascending
-// id into per-pixel accumulators; for a fixed pixel that is exactly the
-// ascending (iy, ix) order of its covering anchors, which this loop walks.
-// No atomics, bit-identical sums.  NC > 0: the channel count is a compile-time
-// constant (no predicated channel lanes); NC = 0: any C <= 8.  The candidate id
-// is split with a float-reciprocal quotient and one correction step (exact
-// for ids < 2^24, checked by the launcher).
+// The reference scatters anchors in ascending id into per-pixel accumulators;
+// for a fixed pixel that is exactly the ascending (iy, ix) order of its
+// covering anchors, which the gather walks.  No atomics, bit-identical sums.
+//
+// A CTA owns 32 x 8 output pixels (a warp = 32 consecutive pixels of a row):
+// the (eff, exemplar offset) of every anchor covering the tile is formed once
+// into shared memory -- the candidate id split into exemplar coordinates and
+// the anchor position folded into one offset zb, so the candidate pixel of
+// pixel (x, y) is zb + y * ew + x -- and each pixel then reads its covering
+// anchors from there.  Interior pixels (w / spacing = 4: exactly 4 x 4 covering
+// anchors) load all 16 entries and their candidate pixels eight at a time
+// ahead of the sequential fp64 chain; edge pixels walk the general ranges.
+// NC > 0: compile-time channel count; NC = 0: any C <= 8.
+struct MstepEntry {
+  double we;
+  int32_t zb;
+  int32_t pad;
+};
+constexpr int kMstepTX = 32, kMstepTY = 8;
+
+__host__ __device__ inline int mstep_span(int tile, int w, int sp) { return (tile + w - 2) / sp + 2; }
+
 template <int NC>
 __global__ void __launch_bounds__(256) mstep_kernel(MstepArgs a) {
   constexpr int CMAX = NC > 0 ? NC : 8;
   const int C = NC > 0 ? NC : a.C;
-  extern __shared__ unsigned int hist_s[];  // [slots][bins] when a.counts
-  if (a.counts) {
+  extern __shared__ __align__(16) unsigned char mstep_smem[];
+  const int cap_r = mstep_span(kMstepTY, a.w, a.sp), cap_c = mstep_span(kMstepTX, a.w, a.sp);
+  MstepEntry* ent = reinterpret_cast<MstepEntry*>(mstep_smem);
+  // per warp: its 32 pixels' fp32 mirror values [32][C], stored as whole lines
+  float* mir_s = reinterpret_cast<float*>(ent + cap_r * cap_c) + (threadIdx.x >> 5) * 32 * CMAX;
+  unsigned int* hist_s = reinterpret_cast<unsigned int*>(ent + cap_r * cap_c) + 8 * 32 * CMAX;
+  if (a.counts)
     for (int i = threadIdx.x; i < a.bins * a.slots; i += blockDim.x) hist_s[i] = 0;
-    __syncthreads();
-  }
-  const int64_t P = (int64_t)a.W * a.H;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t PS = (int64_t)a.W * a.plane_rows;  // plane stride (band: rows >= H)
-  const float inv_nxe = 1.f / (float)a.nxe;
-  for (int64_t pix = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pix < P;
-       pix += (int64_t)gridDim.x * blockDim.x) {
-    const int y = (int)(pix / a.W), x = (int)(pix - (int64_t)y * a.W);
+  const int tnx = (a.W + kMstepTX - 1) / kMstepTX;
+  const int n_tiles = tnx * ((a.H + kMstepTY - 1) / kMstepTY);
+  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const int x0 = (t % tnx) * kMstepTX, y0 = (t / tnx) * kMstepTY;
+    const int x1 = min(x0 + kMstepTX, a.W) - 1, y1 = min(y0 + kMstepTY, a.H) - 1;
+    const int r0 = a.row_lo[y0], c0 = a.col_lo[x0];
+    const int nr = a.row_hi[y1] - r0, ncl = a.col_hi[x1] - c0;
+    __syncthreads();  // the previous tile's entries are consumed
+    if (nr > cap_r || ncl > cap_c) {  // cannot happen: spans bounded by mstep_span
+      if (threadIdx.x == 0) atomicOr(a.flags, FLAG_STACK_OVERFLOW);
+      continue;
+    }
+    for (int e = threadIdx.x; e < nr * ncl; e += blockDim.x) {
+      const int iy = r0 + e / ncl, ix = c0 + e % ncl;
+      const int64_t ai = (int64_t)iy * a.nx + ix;
+      const int32_t id = __ldg(a.idx + ai);
+      const int ey = id / a.nxe, ex = id - ey * a.nxe;
+      MstepEntry m;
+      m.we = __ldg(a.eff + ai);
+      m.zb = (ey - a.ys[iy]) * a.ew + ex - a.xs[ix];
+      m.pad = 0;
+      ent[e] = m;
+    }
+    __syncthreads();
+    const int x = x0 + lane, y = y0 + warp;
+    if (y >= a.H) continue;  // warp-uniform
+    const int64_t pix = (int64_t)y * a.W + x;
+    // the warp's mirror row segment [x0, x0 + nw) is stored cooperatively
+    // after the pixel loop: C contiguous floats per pixel, lanes on
+    // consecutive words (the per-pixel stride-C stores wasted ~4/5 of every
+    // sector)
+    const int nw = min(32, a.W - x0);
+    if (x < a.W) {
+    const int base = y * a.ew + x;
     double acc[CMAX];
 #pragma unroll
     for (int c = 0; c < CMAX; ++c) acc[c] = 0.0;
     double wsum = 0.0;
-    const int iy0 = a.row_lo[y], iy1 = a.row_hi[y];
-    const int ix0 = a.col_lo[x], ix1 = a.col_hi[x];
+    const int iy0 = a.row_lo[y] - r0, iy1 = a.row_hi[y] - r0;
+    const int ix0 = a.col_lo[x] - c0, ix1 = a.col_hi[x] - c0;
     if (NC > 0 && a.ex8 && iy1 - iy0 == 4 && ix1 - ix0 == 4) {
-      // interior pixel (w / spacing = 4 at every stage): the 16 covering
-      // anchors' (eff, id) are loaded together, then their candidate pixels
-      // eight at a time, ahead of the sequential ascending-anchor fp64 chain
       double we[16];
-      int32_t id[16];
+      int32_t zp[16];
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          const int64_t ai = (int64_t)(iy0 + r) * a.nx + ix0 + c;
-          we[r * 4 + c] = __ldg(a.eff + ai);
-          id[r * 4 + c] = __ldg(a.idx + ai);
+          const MstepEntry m = ent[(iy0 + r) * ncl + ix0 + c];
+          we[r * 4 + c] = m.we;
+          zp[r * 4 + c] = m.zb + base;
         }
-      int dys[4], dxs[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) dys[r] = y - a.ys[iy0 + r];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) dxs[c] = x - a.xs[ix0 + c];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         float4 z0[8], z1[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          const int j = h * 8 + k;
-          int ey = __float2int_rz((float)id[j] * inv_nxe);
-          int ex = id[j] - ey * a.nxe;
-          if (ex < 0) {
-            --ey;
-            ex += a.nxe;
-          } else if (ex >= a.nxe) {
-            ++ey;
-            ex -= a.nxe;
+          const float* zr = a.ex8 + (int64_t)zp[h * 8 + k] * 8;
+          if (NC > 4) {
+            ldg256(zr, z0[k], z1[k]);
+          } else {
+            z0[k] = __ldg(reinterpret_cast<const float4*>(zr));
+            z1[k] = make_float4(0.f, 0.f, 0.f, 0.f);
           }
-          const int64_t zp = (int64_t)(ey + dys[j >> 2]) * a.ew + ex + dxs[j & 3];
-          const float4* z4 = reinterpret_cast<const float4*>(a.ex8 + zp * 8);
-          z0[k] = __ldg(z4);
-          z1[k] = NC > 4 ? __ldg(z4 + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -312,44 +345,32 @@ __global__ void __launch_bounds__(256) mstep_kernel(MstepArgs a) {
           wsum = dadd(wsum, w);
         }
       }
-    } else
-    for (int iy = iy0; iy < iy1; ++iy) {
-      const int dy = y - a.ys[iy];
-      const int64_t arow = (int64_t)iy * a.nx;
-      for (int ix = ix0; ix < ix1; ++ix) {
-        const double we = a.eff[arow + ix];
-        const int32_t id = a.idx[arow + ix];
-        int ey = __float2int_rz((float)id * inv_nxe);
-        int ex = id - ey * a.nxe;
-        if (ex < 0) {
-          --ey;
-          ex += a.nxe;
-        } else if (ex >= a.nxe) {
-          ++ey;
-          ex -= a.nxe;
+    } else {
+      for (int iy = iy0; iy < iy1; ++iy)
+        for (int ix = ix0; ix < ix1; ++ix) {
+          const MstepEntry m = ent[iy * ncl + ix];
+          const int64_t zq = (int64_t)m.zb + base;
+          float zv[CMAX];
+          if (NC > 0 && a.ex8) {  // 32-byte padded pixel: two 16-byte loads
+            float4 z0, z1;
+            ldg256(a.ex8 + zq * 8, z0, z1);
+            const float zc[8] = {z0.x, z0.y, z0.z, z0.w, z1.x, z1.y, z1.z, z1.w};
+#pragma unroll
+            for (int c = 0; c < CMAX; ++c) zv[c] = zc[c];
+          } else {
+            const float* z = a.ex_mirror + zq * C;
+#pragma unroll
+            for (int c = 0; c < CMAX; ++c) zv[c] = (NC > 0 || c < C) ? __ldg(z + c) : 0.f;
+          }
+#pragma unroll
+          for (int c = 0; c < CMAX; ++c)
+            if (NC > 0 || c < C) acc[c] = dadd(acc[c], dmul(m.we, (double)zv[c]));
+          wsum = dadd(wsum, m.we);
         }
-        const int64_t zp = (int64_t)(ey + dy) * a.ew + ex + (x - a.xs[ix]);
-        float zv[CMAX];
-        if (NC > 0 && a.ex8) {  // 32-byte padded pixel: two 16-byte loads
-          const float4* z4 = reinterpret_cast<const float4*>(a.ex8 + zp * 8);
-          const float4 z0 = __ldg(z4), z1 = __ldg(z4 + 1);
-          const float zc[8] = {z0.x, z0.y, z0.z, z0.w, z1.x, z1.y, z1.z, z1.w};
-#pragma unroll
-          for (int c = 0; c < CMAX; ++c) zv[c] = zc[c];
-        } else {
-          const float* z = a.ex_mirror + zp * C;
-#pragma unroll
-          for (int c = 0; c < CMAX; ++c) zv[c] = (NC > 0 || c < C) ? __ldg(z + c) : 0.f;
-        }
-#pragma unroll
-        for (int c = 0; c < CMAX; ++c)
-          if (NC > 0 || c < C) acc[c] = dadd(acc[c], dmul(we, (double)zv[c]));
-        wsum = dadd(wsum, we);
-      }
     }
     if (wsum <= 0.0) {
       atomicOr(a.flags, FLAG_UNCOVERED);
-      continue;
+      wsum = 1.0;  // flagged: the call fails; keep the warp together for the stores
     }
     const double inv = 1.0 / wsum;  // optimizer.cpp:393
 #pragma unroll
@@ -358,15 +379,22 @@ __global__ void __launch_bounds__(256) mstep_kernel(MstepArgs a) {
       double v = dmul(acc[c], inv);
       v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);  // std::clamp(.., 0, 1)
       a.planes[c * PS + pix] = v;
-      if (a.mirror) a.mirror[pix * C + c] = (float)v;
+      mir_s[lane * C + c] = (float)v;
       if (a.counts && c < a.slots) {
         // lanes with the same bin add once (neighbouring pixels share bins:
         // unaggregated shared-memory atomics serialise)
         const int key = c * a.bins + bin_of_f64(v, a.bins);
         const unsigned peers = __match_any_sync(__activemask(), key);
-        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist_s[key], (unsigned)__popc(peers));
+        if (lane == __ffs(peers) - 1) atomicAdd(&hist_s[key], (unsigned)__popc(peers));
       }
     }
+    }  // x < W
+    __syncwarp();
+    if (a.mirror) {
+      float* dst = a.mirror + ((int64_t)y * a.W + x0) * C;
+      for (int f = lane; f < nw * C; f += 32) dst[f] = mir_s[f];
+    }
+    __syncwarp();
   }
   if (a.counts) {  // same integer counts as hist_count_kernel over the written rows
     __syncthreads();
@@ -375,25 +403,36 @@ __global__ void __launch_bounds__(256) mstep_kernel(MstepArgs a) {
   }
 }
 
+template <int NC>
+static int mstep_blocks_per_sm(size_t sm) {
+  int n = 0;
+  PSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mstep_kernel<NC>, 256, sm));
+  return n < 1 ? 1 : n;
+}
+
 void launch_mstep(psg_ctx* ctx, const MstepArgs& a) {
   ProfScope _prof(ctx, K_MSTEP);
   const int64_t P = (int64_t)a.W * a.H;
   if (P <= 0) return;
   if (a.C > 8) fail(PSG_E_DOMAIN, "more than 8 channels are not supported");
-  // one pixel per thread: with the fused histogram every block ends in a
-  // barrier, and a grid-stride remainder would leave most threads waiting there
-  const int blocks = grid_for(ctx, P, 256, 1 << 20);
-  size_t sm = 0;
+  if (a.sp < 1) fail(PSG_E_LOGIC, "M-step without the grid spacing");
+  size_t sm = sizeof(MstepEntry) * mstep_span(kMstepTY, a.w, a.sp) * mstep_span(kMstepTX, a.w, a.sp) +
+              sizeof(float) * 8 * 32 * (a.C == 4 ? 4 : a.C == 5 ? 5 : 8);
   if (a.counts) {
     if (a.slots > a.C) fail(PSG_E_DOMAIN, "histogram slots exceed the channel count");
-    sm = sizeof(unsigned int) * a.bins * a.slots;
+    sm += sizeof(unsigned int) * a.bins * a.slots;
     PSG_CUDA(cudaMemsetAsync(a.counts, 0, sizeof(unsigned long long) * a.bins * a.slots,
                              ctx->stream));
   }
+  if (sm > 48 * 1024) fail(PSG_E_DOMAIN, "M-step tile footprint exceeds 48 KB of shared memory");
+  const int64_t tiles = (int64_t)((a.W + kMstepTX - 1) / kMstepTX) * ((a.H + kMstepTY - 1) / kMstepTY);
+  // persistent CTAs striding over the tiles: the histogram flush (one per
+  // CTA) and the barrier tail are paid per resident CTA, not per tile
+  auto blocks = [&](int per_sm) { return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)per_sm * ctx->num_sms)); };
   switch (a.C) {
-    case 4: mstep_kernel<4><<<blocks, 256, sm, ctx->stream>>>(a); break;
-    case 5: mstep_kernel<5><<<blocks, 256, sm, ctx->stream>>>(a); break;
-    default: mstep_kernel<0><<<blocks, 256, sm, ctx->stream>>>(a); break;
+    case 4: mstep_kernel<4><<<blocks(mstep_blocks_per_sm<4>(sm)), 256, sm, ctx->stream>>>(a); break;
+    case 5: mstep_kernel<5><<<blocks(mstep_blocks_per_sm<5>(sm)), 256, sm, ctx->stream>>>(a); break;
+    default: mstep_kernel<0><<<blocks(mstep_blocks_per_sm<0>(sm)), 256, sm, ctx->stream>>>(a); break;
   }
   PSG_LAUNCHED(ctx);
 }

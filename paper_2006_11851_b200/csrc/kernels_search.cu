@@ -1901,8 +1901,8 @@ void launch_make_fp32_copies(psg_ctx* ctx, const double* soa, int64_t N, int d, 
 // Full-D rescoring (optimizer.cpp:117-124, :232-234): one thread per query,
 // j ascending over the window (dy, dx, c) against the candidate's dense
 // exemplar window — the candidate matrix is never materialised.
-// Candidate rows from the 8-channel padded exemplar mirror (two 16-byte
-// loads per pixel), NC = C at compile time; same (dy, dx, c) order.
+// Candidate rows from the 8-channel padded exemplar mirror (one 32-byte
+// load per pixel), NC = C at compile time; same (dy, dx, c) order.
 template <int NC>
 __device__ __forceinline__ double window_dist2_pad(const float* __restrict__ mirror, int img_w,
                                                    int w, int ax, int ay,
@@ -1911,11 +1911,11 @@ __device__ __forceinline__ double window_dist2_pad(const float* __restrict__ mir
   double acc = 0.0;
   for (int dy = 0; dy < w; ++dy) {
     const float* v = mirror + ((int64_t)(ay + dy) * img_w + ax) * NC;
-    const float4* z4 = reinterpret_cast<const float4*>(ex8 + ((int64_t)(ey + dy) * ew + ex) * 8);
+    const float* z8 = ex8 + ((int64_t)(ey + dy) * ew + ex) * 8;
 #pragma unroll 2
     for (int dx = 0; dx < w; ++dx) {
-      const float4 z0 = __ldg(z4 + 2 * dx);
-      const float4 z1 = __ldg(z4 + 2 * dx + 1);
+      float4 z0, z1;
+      ldg256(z8 + 8 * dx, z0, z1);
       const float zc[8] = {z0.x, z0.y, z0.z, z0.w, z1.x, z1.y, z1.z, z1.w};
       float vc[NC];
 #pragma unroll

@@ -210,4 +210,14 @@ PSG_HD int bin_of_f64(double v, int bins) {
   return b < 0 ? 0 : (b > bins - 1 ? bins - 1 : b);
 }
 
+#ifdef __CUDACC__
+// One 32-byte read-only global load (LDG.E.256 on sm_100): a padded 8-float
+// exemplar pixel in one instruction, one sector per lane.
+__device__ __forceinline__ void ldg256(const float* p, float4& lo, float4& hi) {
+  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=f"(lo.x), "=f"(lo.y), "=f"(lo.z), "=f"(lo.w), "=f"(hi.x), "=f"(hi.y), "=f"(hi.z), "=f"(hi.w)
+      : "l"(p));
+}
+#endif
+
 }  // namespace psg

@@ -463,6 +463,7 @@ struct MstepArgs {
   const int32_t* idx;     // [A]
   const double* eff;      // [A]
   int W, H, C, w;     // H = rows written (a band writes its owned rows only)
+  int sp = 0;         // grid spacing (bounds the anchors covering a pixel tile)
   int plane_rows;     // rows allocated per plane (plane stride = W * plane_rows)
   const float* ex_mirror;
   int ew, nxe;

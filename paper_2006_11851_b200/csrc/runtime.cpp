@@ -863,6 +863,7 @@ MstepArgs mstep_args(psg_level& L) {
   m.plane_rows = L.Hl;
   m.C = L.C;
   m.w = L.w;
+  m.sp = L.cfg.spacing;
   m.ex_mirror = ix.ex_mirror;
   m.ex8 = L.ctx->knobs.no_ex8 ? nullptr : ix.ex_mirror8;
   m.ew = ix.ew;
