@@ -432,57 +432,64 @@ __device__ __forceinline__ double dist2_chain(const double* q, const double* p, 
   return acc;
 }
 
-__global__ void __launch_bounds__(32 * kListWarps) resolve_kernel(
+// One warp per listed query: the reference's projection chain for every
+// component (lane k: acc_k += c_j * B[k][j], j ascending), in chunks of 32
+// window features; the next chunk's basis rows and features are loaded into
+// registers while the current chunk's chain runs from shared memory.
+constexpr int kResolveWarps = 2, kRC = 32;
+__global__ void __launch_bounds__(32 * kResolveWarps) resolve_kernel(
     ResolveArgs r, const double* __restrict__ mean, const double* __restrict__ basisT, int KP,
     int D, int d, const double* __restrict__ proj) {
-  __shared__ double cs_all[kListWarps][kListChunk];
-  __shared__ double qs_all[kListWarps][64];
-  __shared__ double ps_all[kListWarps][2][64];  // the two band candidates' rows
+  __shared__ double bs_all[kResolveWarps][kRC][64];
+  __shared__ double cs_all[kResolveWarps][kRC];
+  __shared__ double qs_all[kResolveWarps][64];
+  __shared__ double ps_all[kResolveWarps][2][64];  // the two band candidates' rows
   const int n = *r.count;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double(*bs)[64] = bs_all[warp];
   double* cs = cs_all[warp];
   double* qs = qs_all[warp];
   const int wc = r.w * r.C;
-  for (int i = blockIdx.x * kListWarps + warp; i < n; i += gridDim.x * kListWarps) {
+  const int nch = (D + kRC - 1) / kRC;
+  for (int i = blockIdx.x * kResolveWarps + warp; i < n; i += gridDim.x * kResolveWarps) {
     const int32_t a = r.list[i];
     const int64_t base =
         ((int64_t)r.anchors.ys[a / r.anchors.nx] * r.img_w + r.anchors.xs[a % r.anchors.nx]) * r.C;
-    double acc0 = 0.0, acc1 = 0.0;
-    for (int j0 = 0; j0 < D; j0 += kListChunk) {
-      const int jn = min(kListChunk, D - j0);
-      __syncwarp();
-      for (int t = lane; t < jn; t += 32) {
-        const int j = j0 + t, dy = j / wc, off = j - dy * wc;
-        const float v = __ldg(r.mirror + base + (int64_t)dy * r.img_w * r.C + off);
-        cs[t] = dsub((double)v, __ldg(mean + j));
-      }
-      __syncwarp();
-      // basis loads software-pipelined one 8-element batch ahead of the chain
+    double nb0[kRC], nb1[kRC], ncs = 0.0;
+    auto load = [&](int ch) {
+      const int j0 = ch * kRC;
       const double* bt = basisT + (int64_t)j0 * KP + lane;
-      double n0[8], n1[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        n0[u] = u < jn ? __ldg(bt + (int64_t)u * KP) : 0.0;
-        n1[u] = (KP > 32 && u < jn) ? __ldg(bt + (int64_t)u * KP + 32) : 0.0;
+      for (int u = 0; u < kRC; ++u) {
+        const bool ok = j0 + u < D;
+        nb0[u] = ok ? __ldg(bt + (int64_t)u * KP) : 0.0;
+        nb1[u] = (KP > 32 && ok) ? __ldg(bt + (int64_t)u * KP + 32) : 0.0;
       }
-      for (int t0 = 0; t0 < jn; t0 += 8) {
-        double b0[8], b1[8];
+      const int j = j0 + lane;
+      if (j < D) {
+        const int dy = j / wc, off = j - dy * wc;
+        const float v = __ldg(r.mirror + base + (int64_t)dy * r.img_w * r.C + off);
+        ncs = dsub((double)v, __ldg(mean + j));
+      }
+    };
+    load(0);
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int ch = 0; ch < nch; ++ch) {
+      __syncwarp();
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          b0[u] = n0[u];
-          b1[u] = n1[u];
-          const int tn = t0 + 8 + u;
-          n0[u] = tn < jn ? __ldg(bt + (int64_t)tn * KP) : 0.0;
-          n1[u] = (KP > 32 && tn < jn) ? __ldg(bt + (int64_t)tn * KP + 32) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (t0 + u < jn) {
-            const double cj = cs[t0 + u];
-            acc0 = dadd(acc0, dmul(cj, b0[u]));
-            if (KP > 32) acc1 = dadd(acc1, dmul(cj, b1[u]));
-          }
-        }
+      for (int u = 0; u < kRC; ++u) {
+        bs[u][lane] = nb0[u];
+        if (KP > 32) bs[u][lane + 32] = nb1[u];
+      }
+      cs[lane] = ncs;
+      __syncwarp();
+      const int jn = min(kRC, D - ch * kRC);
+      if (ch + 1 < nch) load(ch + 1);
+#pragma unroll 8
+      for (int t = 0; t < jn; ++t) {
+        const double cj = cs[t];
+        acc0 = dadd(acc0, dmul(cj, bs[t][lane]));
+        if (KP > 32) acc1 = dadd(acc1, dmul(cj, bs[t][lane + 32]));
       }
     }
     if (lane < d) qs[lane] = acc0;
@@ -650,7 +657,7 @@ void launch_project_windows_tc(psg_ctx* ctx, const uint8_t* q8, int64_t slice_by
 void launch_resolve(psg_ctx* ctx, const ResolveArgs& r, const Index& ix) {
   ProfScope _prof(ctx, K_FALLBACK);
   const int KP = ix.d <= 32 ? 32 : 64;
-  resolve_kernel<<<64, 32 * kListWarps, 0, ctx->stream>>>(r, ix.mean, ix.basis, KP,
+  resolve_kernel<<<2 * ctx->num_sms, 32 * kResolveWarps, 0, ctx->stream>>>(r, ix.mean, ix.basis, KP,
                                                                         ix.D, ix.d, ix.proj);
   PSG_LAUNCHED(ctx);
 }

@@ -1995,53 +1995,105 @@ __global__ void rescore_windows_kernel(const float* __restrict__ mirror, int img
 // Rescoring after a search seeded with prev_idx on the SAME image: an anchor
 // whose assignment did not change has the distance prev_dist already (the
 // lsq-after diagnostic computed it: same window, same candidate, same chain),
-// so only the changed anchors (~10% once EM settles) are recomputed.  Each
-// CTA compacts its changed anchors so that the chains run on contiguous lanes.
+// so only the changed anchors (~5% once EM settles) are recomputed: they are
+// listed (warp-aggregated), then a warp per listed anchor forms its D squared
+// differences in parallel (coalesced window and candidate rows) and one lane
+// adds them in the reference's order j = (dy, dx, c) ascending.
 constexpr int kRescoreBlock = 256;
-__global__ void __launch_bounds__(kRescoreBlock) rescore_changed_kernel(
-    const float* __restrict__ mirror, int img_w, int C, int w, const int32_t* __restrict__ xs,
-    const int32_t* __restrict__ ys, int nx, int64_t n, const float* __restrict__ ex_mirror,
-    const float* __restrict__ ex8, int ew, int nxe, const int32_t* __restrict__ idx,
-    const int32_t* __restrict__ prev_idx,
-    const double* __restrict__ prev_dist, double* __restrict__ dist) {
-  __shared__ int list[kRescoreBlock];
-  __shared__ int cnt;
-  const int tid = threadIdx.x, lane = tid & 31;
-  if (tid == 0) cnt = 0;
-  __syncthreads();
-  const int64_t a = (int64_t)blockIdx.x * kRescoreBlock + tid;
-  bool todo = false;
-  if (a < n) {
-    if (idx[a] == prev_idx[a])
-      dist[a] = prev_dist[a];
-    else
-      todo = true;
+__global__ void __launch_bounds__(kRescoreBlock) rescore_mark_kernel(
+    int64_t n, const int32_t* __restrict__ idx, const int32_t* __restrict__ prev_idx,
+    const double* __restrict__ prev_dist, double* __restrict__ dist, int32_t* __restrict__ list,
+    int* __restrict__ count) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t a0 = blockIdx.x * (int64_t)blockDim.x; a0 < n; a0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = a0 + threadIdx.x;
+    bool todo = false;
+    if (a < n) {
+      if (idx[a] == prev_idx[a])
+        dist[a] = prev_dist[a];
+      else
+        todo = true;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, todo);
+    int base = 0;
+    if (lane == 0 && m) base = atomicAdd(count, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (todo) list[base + __popc(m & ((1u << lane) - 1u))] = (int32_t)a;
   }
-  const unsigned m = __ballot_sync(0xffffffffu, todo);
-  int base = 0;
-  if (lane == 0 && m) base = atomicAdd(&cnt, __popc(m));
-  base = __shfl_sync(0xffffffffu, base, 0);
-  if (todo) list[base + __popc(m & ((1u << lane) - 1u))] = tid;
-  __syncthreads();
-  for (int i = tid; i < cnt; i += kRescoreBlock) {
-    const int64_t b = (int64_t)blockIdx.x * kRescoreBlock + list[i];
+}
+
+constexpr int kRescoreChunk = 256;  // squared terms staged per warp round
+__global__ void __launch_bounds__(256) rescore_list_kernel(
+    const float* __restrict__ mirror, int img_w, int C, int w, const int32_t* __restrict__ xs,
+    const int32_t* __restrict__ ys, int nx, const float* __restrict__ ex_mirror,
+    const float* __restrict__ ex8, int ew, int nxe, const int32_t* __restrict__ idx,
+    const int32_t* __restrict__ list, const int* __restrict__ count, double* __restrict__ dist) {
+  __shared__ double sq_all[8][kRescoreChunk];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* sq = sq_all[warp];
+  const int n = *count;
+  const int D = w * w * C, row = w * C;
+  for (int i = blockIdx.x * 8 + warp; i < n; i += gridDim.x * 8) {
+    const int64_t b = list[i];
     const int32_t id = idx[b];
-    dist[b] = sqrt(window_dist2_any(mirror, img_w, C, w, xs[b % nx], ys[b / nx], ex_mirror, ex8,
-                                    ew, id % nxe, id / nxe));
+    const int ax = xs[b % nx], ay = ys[b / nx];
+    const int ex = id % nxe, ey = id / nxe;
+    double acc = 0.0;
+    for (int j0 = 0; j0 < D; j0 += kRescoreChunk) {
+#pragma unroll
+      for (int u = 0; u < kRescoreChunk / 32; ++u) {
+        const int j = j0 + u * 32 + lane;
+        if (j < D) {
+          const int dy = j / row, r = j - dy * row;  // r = dx * C + c
+          const float v = __ldg(mirror + ((int64_t)(ay + dy) * img_w + ax) * C + r);
+          float z;
+          if (ex8) {
+            const int dx = r / C, c = r - dx * C;
+            z = __ldg(ex8 + ((int64_t)(ey + dy) * ew + ex + dx) * 8 + c);
+          } else {
+            z = __ldg(ex_mirror + ((int64_t)(ey + dy) * ew + ex) * C + r);
+          }
+          const double t = dsub((double)v, (double)z);
+          sq[u * 32 + lane] = dmul(t, t);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const int m = min(kRescoreChunk, D - j0);
+        int k = 0;
+        for (; k + 8 <= m; k += 8) {
+          double s8[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) s8[u] = sq[k + u];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc = dadd(acc, s8[u]);
+        }
+        for (; k < m; ++k) acc = dadd(acc, sq[k]);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) dist[b] = sqrt(acc);
   }
 }
 
 void launch_rescore_windows(psg_ctx* ctx, const float* mirror, int img_w, int C, int w,
                             AnchorSet anchors, const Index& ix, const int32_t* idx,
-                            double* dist, const int32_t* prev_idx, const double* prev_dist) {
+                            double* dist, const int32_t* prev_idx, const double* prev_dist,
+                            int32_t* list, int* count) {
   ProfScope _prof(ctx, K_RESCORE);
   if (anchors.count <= 0) return;
   const float* ex8 = ctx->knobs.no_ex8 ? nullptr : ix.ex_mirror8;
   if (prev_idx && prev_dist) {
-    const int64_t blocks = (anchors.count + kRescoreBlock - 1) / kRescoreBlock;
-    rescore_changed_kernel<<<(unsigned)blocks, kRescoreBlock, 0, ctx->stream>>>(
-        mirror, img_w, C, w, anchors.xs, anchors.ys, anchors.nx, anchors.count, ix.ex_mirror,
-        ex8, ix.ew, ix.nxe, idx, prev_idx, prev_dist, dist);
+    if (!list || !count) fail(PSG_E_LOGIC, "changed-only rescoring without its list buffers");
+    PSG_CUDA(cudaMemsetAsync(count, 0, sizeof(int), ctx->stream));
+    int64_t blocks = (anchors.count + kRescoreBlock - 1) / kRescoreBlock;
+    if (blocks > (int64_t)ctx->num_sms * 8) blocks = (int64_t)ctx->num_sms * 8;
+    rescore_mark_kernel<<<(unsigned)blocks, kRescoreBlock, 0, ctx->stream>>>(anchors.count, idx, prev_idx,
+                                                                            prev_dist, dist, list, count);
+    PSG_LAUNCHED(ctx);
+    rescore_list_kernel<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(
+        mirror, img_w, C, w, anchors.xs, anchors.ys, anchors.nx, ix.ex_mirror, ex8, ix.ew, ix.nxe, idx,
+        list, count, dist);
     PSG_LAUNCHED(ctx);
     return;
   }
