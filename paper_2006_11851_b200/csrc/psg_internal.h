@@ -63,7 +63,10 @@ struct DevTree {
   int2* meta = nullptr;         // {first_child, -n_children} or {leaf_start, leaf_count}
   int32_t* tie = nullptr;       // optional backtrack tie-break id per node (null = node index)
 };
-constexpr int kBoxDims = 8;     // leading PCA dims carrying bounding boxes
+#ifndef PSG_BOX_DIMS
+#define PSG_BOX_DIMS 8
+#endif
+constexpr int kBoxDims = PSG_BOX_DIMS;  // leading PCA dims carrying bounding boxes
 
 struct HostTree {
   std::vector<double> centroid, radius;
@@ -422,7 +425,8 @@ void launch_make_fp32_copies(psg_ctx* ctx, const double* soa, int64_t N, int d, 
 // Full-D distance between query windows and assigned candidates (optimizer.cpp:117-124).
 void launch_rescore_windows(psg_ctx* ctx, const float* mirror, int img_w, int C, int w,
                             AnchorSet anchors, const Index& ix, const int32_t* idx, double* dist,
-                            const int32_t* prev_idx = nullptr, const double* prev_dist = nullptr);
+                            const int32_t* prev_idx = nullptr, const double* prev_dist = nullptr,
+                            int32_t* list = nullptr, int* count = nullptr);  // [count] scratch (changed-only)
 void launch_rescore_query_windows(psg_ctx* ctx, const float* Q, int64_t nq, const Index& ix,
                                   const int32_t* idx, double* dist);
 void launch_rescore_vectors(psg_ctx* ctx, const float* Q, int64_t nq, const Index& ix,

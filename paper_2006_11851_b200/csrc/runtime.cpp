@@ -439,6 +439,8 @@ struct psg_level {
   psg::DBuf<unsigned long long> counts;
   psg::DBuf<double> out_mass, excess, ex_hist, stats_dev, pen_table;
   psg::DBuf<int32_t> tile_order;
+  psg::DBuf<int32_t> resc_list;  // changed-only rescoring: the changed anchors
+  psg::DBuf<int> resc_n;
   // tensor-core projection (kernels_project_tc.cu): digit mirror, per-query
   // error bands, ambiguous-query list and the exact fallback's compact buffers
   psg::DBuf<uint8_t> q8;
@@ -584,6 +586,8 @@ void level_setup_band(psg_level& L, psg_ctx* ctx, const Index& ix, const psg_ban
   L.scanned.alloc(L.Ao);
   L.exact_evals.alloc(L.Ao);
   L.visited.alloc(L.Ao);
+  L.resc_list.alloc(L.Ao);
+  L.resc_n.alloc(1);
   L.stats_dev.alloc(8 + 6 * 296);
   L.tile_order.alloc((size_t)image_tile_count(L.Ao, L.nx));
   if (ctx->pinned_free.empty()) {
@@ -654,7 +658,8 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
     PSG_CUDA(cudaMemsetAsync(L.visited.p, 0, sizeof(int32_t) * L.Ao, ctx->stream));
     if (seed_dist_ready) PSG_CUDA(cudaStreamWaitEvent(ctx->stream, seed_dist_ready, 0));
     launch_rescore_windows(ctx, L.mirror.p, L.W, L.C, L.w, as, ix, out_idx + L.off,
-                           out_dist + L.off, seed_dist ? seed : nullptr, seed_dist);
+                           out_dist + L.off, seed_dist ? seed : nullptr, seed_dist, L.resc_list.p,
+                           L.resc_n.p);
     L.unique_queries += L.Ao;
     return;
   }
@@ -811,7 +816,8 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
   L.scanned_valid = true;
   if (seed_dist_ready) PSG_CUDA(cudaStreamWaitEvent(ctx->stream, seed_dist_ready, 0));
   launch_rescore_windows(ctx, L.mirror.p, L.W, L.C, L.w, as, ix, out_idx + L.off,
-                         out_dist + L.off, seed_dist ? seed : nullptr, seed_dist);
+                         out_dist + L.off, seed_dist ? seed : nullptr, seed_dist, L.resc_list.p,
+                         L.resc_n.p);
   L.unique_queries += L.Ao;
 }
 
