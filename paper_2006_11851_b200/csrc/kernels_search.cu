@@ -1190,6 +1190,16 @@ __global__ void __launch_bounds__(256) search_exact_kernel(SearchArgs a) {
 // lexicographic (fp64 dist^2, id) minimum.  Spatially consecutive anchors have
 // overlapping windows and hence overlapping candidate sets, so the shared
 // traversal visits little more than each query alone.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool full) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(full ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
+}
+
 // three-input max (FMNMX3 on sm_100)
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float r;
@@ -1373,12 +1383,14 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
             const int pos = bstart[b] + i;
             const float4* col = reinterpret_cast<const float4*>(a.proj32_q4) + pos;
             float4* dst = reinterpret_cast<float4*>(stage + lane * RS);
+            // asynchronous global -> shared copies (LDGSTS): no staging
+            // registers; dims >= d are zero-filled (src-size 0)
 #pragma unroll
-            for (int k = 0; k < DP / 4; ++k)
-              dst[k] = (4 * k < d) ? __ldg(col + (int64_t)k * N) : make_float4(0.f, 0.f, 0.f, 0.f);
-            aux0[lane] = a.pnorm32[pos];
-            pid[lane] = a.perm[pos];
+            for (int k = 0; k < DP / 4; ++k) cp_async16(dst + k, col + (int64_t)k * N, 4 * k < d);
+            cp_async4(aux0 + lane, a.pnorm32 + pos);
+            cp_async4(pid + lane, a.perm + pos);
           }
+          asm volatile("cp.async.wait_all;" ::: "memory");
           __syncwarp();
           // best rounded up to float: a float compare can only keep more points.
           // thr >= s for every point that can pass the precise test below
