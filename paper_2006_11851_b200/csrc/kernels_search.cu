@@ -27,6 +27,9 @@
 #ifndef TILE64_MIN_CTAS
 #define TILE64_MIN_CTAS 6  // d in (32, 64]: 6 CTAs x 2 warps (168 registers): cfg4 finest search 31 -> 27 ms
 #endif
+// leading PCA dims of the branch-free first filter phase (measured on the
+// bench stage: 4 -> 1.41 ms, 8 -> 1.50, 12 -> 1.75)
+#define P1_DIMS 4
 #ifndef RECHECK_BATCH
 #define RECHECK_BATCH 4
 #endif
@@ -1398,7 +1401,7 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
           float best_up = bestf;
           float thr = best_up * (1.f + 1e-4f) +
                       1.01e-6f * (qn + a.pnorm_max) * (sqrtf(2.f * best_up + 1.f) + 1e-3f) + 1e-30f;
-          // phase 1, branch-free over the batch: the 8 leading (highest
+          // phase 1, branch-free over the batch: the P1_DIMS leading (highest
           // variance) PCA dims of every staged point against the batch-start
           // threshold; rounded sums of non-negative terms only grow, so a
           // partial sum above thr already rules the point out for this lane
@@ -1407,10 +1410,11 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
           for (int i = 0; i < 32; ++i) {
             const float4* pr = reinterpret_cast<const float4*>(stage + i * RS);
             float2 sa = make_float2(0.f, 0.f);
-            {
-              const float4 p = pr[0];
-              const float2 u0 = __fadd2_rn(q2[0], make_float2(p.x, p.y));
-              const float2 u1 = __fadd2_rn(q2[1], make_float2(p.z, p.w));
+#pragma unroll
+            for (int k = 0; k < P1_DIMS / 4; ++k) {
+              const float4 p = pr[k];
+              const float2 u0 = __fadd2_rn(q2[2 * k], make_float2(p.x, p.y));
+              const float2 u1 = __fadd2_rn(q2[2 * k + 1], make_float2(p.z, p.w));
               sa = __ffma2_rn(u0, u0, sa);
               sa = __ffma2_rn(u1, u1, sa);
             }
