@@ -267,18 +267,55 @@ def roofline_for(kernels: dict, step_ms: float, A: int, P: int, C: int, d: int, 
     roof["kernel"] = dom
     roof["peak_src"] = peaks["src"] if roof["bound"] == "hbm" else "measured (scripts/micro/fp32_bench.cu)"
     if dom == "search_kernel":
-        roof["traffic"], roof["traffic_src"] = ncu_traffic("search_tile_kernel")
+        roof["traffic"], roof["traffic_src"] = ncu_traffic(("search_tile_kernel", "search"))
+    # the other judged kernels (north_star: search and M-step; PCA on tensor cores)
+    others = {}
+    if "mstep_kernel" in kernels and kernels["mstep_kernel"][1]:
+        ms_m, n_m = kernels["mstep_kernel"]
+        t_m = ms_m / n_m / 1e3
+        b_m = P * C * 12 + A * 12  # fp64 planes + fp32 mirror written, (eff, idx) read
+        tr, src = ncu_traffic(("mstep",))
+        others["mstep_kernel"] = {
+            "bound": "hbm", "achieved": b_m / t_m / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": b_m / t_m / 1e9 / peaks["hbm_gbs"], "traffic": tr, "traffic_src": src,
+            "note": "state and exemplar L2-resident: DRAM traffic is well below the algorithmic "
+                    "bytes; the binding unit is the L1 data pipe (16 candidate pixels per output "
+                    "pixel, ncu l1tex throughput ~70-85%)"}
+    if "project_kernel" in kernels and kernels["project_kernel"][1]:
+        ms_p, n_p = kernels["project_kernel"]
+        t_p = ms_p / n_p / 1e3
+        # tcgen05 kind::i8: 13 digit products x K (= w^2 * 8 bytes) x 32 basis rows per anchor
+        others["project_kernel"] = {"bound": "tensor", "unit": "ms", "ms_per_launch": t_p * 1e3,
+                                    "tensor_pipe_active_pct": ncu_metric(("projtc",), "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active"),
+                                    "src": ncu_traffic(("projtc",))[1]}
+    if others:
+        roof["others"] = others
     return roof, per
 
 
-def ncu_traffic(kernel: str):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
-    the committed ncu --set full summary (profiles/r1/<kernel>_*_summary.json),
-    or None.  Read-only evidence: never measured under the profiler here."""
-    files = sorted((ROOT / "profiles").glob(f"*/{kernel}_*_summary.json"))
+def ncu_metric(prefixes, metric):
+    files = []
+    for pre in prefixes:
+        files += (ROOT / "profiles").glob(f"*/{pre}_*_summary.json")
+    if not files:
+        return None
+    try:
+        return float(json.loads(sorted(files)[-1].read_text())["metrics"][metric]["value"].replace(",", ""))
+    except (KeyError, ValueError):
+        return None
+
+
+def ncu_traffic(prefixes):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the kernel
+    from the newest committed ncu --set full summary
+    (profiles/<round>/<prefix>_*_summary.json), or None.  Read-only evidence:
+    never measured under the profiler here."""
+    files = []
+    for pre in prefixes:
+        files += (ROOT / "profiles").glob(f"*/{pre}_*_summary.json")
     if not files:
         return None, None
-    f = files[-1]
+    f = sorted(files)[-1]
     try:
         m = json.loads(f.read_text())["metrics"]
         scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
