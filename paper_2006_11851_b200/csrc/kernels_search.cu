@@ -30,6 +30,17 @@
 // leading PCA dims of the branch-free first filter phase (measured on the
 // bench stage: 4 -> 1.41 ms, 8 -> 1.50, 12 -> 1.75)
 #define P1_DIMS 4
+// phase 2: the second half of the dims in expanded form |q~|^2 + |p~|^2 -
+// 2 q~.p~ (one FFMA2 per two dims; rounding covered by exp_slack).  Measured:
+// 1.41 -> 1.39 ms; all dims expanded (no half-way early exit) 1.52.
+#ifndef P2_EXP
+#define P2_EXP 1
+#endif
+#if P2_EXP
+#define PNORM_OF(i) (sqrtf(ppst[i].x) * 1.000001f)
+#else
+#define PNORM_OF(i) (aux0[i])
+#endif
 #ifndef RECHECK_BATCH
 #define RECHECK_BATCH 4
 #endif
@@ -1198,6 +1209,10 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool fu
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(full ? 16 : 0)
                : "memory");
 }
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
@@ -1221,7 +1236,13 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
   // bounds (pruning only loosens by < 2^-7 = 0.78%), half the largest shared array
   __shared__ __nv_bfloat16 st_lb[kTileWarps][kTileStack][32];
   __shared__ __align__(16) float stage_all[kTileWarps][32 * RS];
+#if P2_EXP
+  // staged points' (|p~|^2, |p~_B|^2); |p| <= sqrt(|p~|^2) (1 + 1e-6)
+  __shared__ float2 pp_all[kTileWarps][32];
+  float2* ppst = pp_all[threadIdx.x >> 5];
+#else
   __shared__ float aux_all[kTileWarps][32];  // staged points' |p|
+#endif
   __shared__ int2 cmeta_all[kTileWarps][kTileMaxB];
   __shared__ __align__(16) float box_all[kTileWarps][kTileMaxB][2 * kBoxDims];
   __shared__ int32_t pid_all[kTileWarps][32];
@@ -1235,7 +1256,9 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
   int2* sm_ = st_meta[warp];
   __nv_bfloat16(*slb)[32] = st_lb[warp];
   float* stage = stage_all[warp];
+#if !P2_EXP
   float* aux0 = aux_all[warp];
+#endif
   int2* cmeta = cmeta_all[warp];
   float(*boxs)[2 * kBoxDims] = box_all[warp];
   int32_t* pid = pid_all[warp];
@@ -1319,6 +1342,26 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
       qn2 += v0 * v0 + v1 * v1;
     }
     const float qn = __double2float_ru(sqrt(qn2) * (1.0 + 1e-12));
+#if P2_EXP
+    // |q~_B|^2 of the fp32 query (B = the second half of the dims), and the
+    // rigorous bound of the expanded form's rounding: |fl(qq + pp - 2 q.p) -
+    // |q~ - p~|^2| <= (n + 4) 2^-24 (qq + pp + 2 |q.p|) <= (n + 4) 2^-24 (|q| + |p|)^2
+    // for n = the dims in expanded form (x1.5 margin for the rounded norms)
+    float qqx;
+    {
+      double t = 0.0;
+#pragma unroll
+      for (int j = DP / 4; j < DP / 2; ++j) {
+        t += (double)q2[j].x * (double)q2[j].x;
+        t += (double)q2[j].y * (double)q2[j].y;
+      }
+      qqx = (float)t;
+    }
+    const float exp_slack = 1.5f * (float)(DP / 2 + 4) * 5.9604645e-8f *
+                            (qn + a.pnorm_max) * (qn + a.pnorm_max);
+#else
+    constexpr float exp_slack = 0.f;
+#endif
     // box margin: >= |float(q_j) - q_j| + the rounding of (-q_j -/+ margin)
     const float qdelta2 = 2.4e-7f * qn;
     // invalid lanes hold best = -1: every bound (>= 0) prunes them
@@ -1390,8 +1433,12 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
             // registers; dims >= d are zero-filled (src-size 0)
 #pragma unroll
             for (int k = 0; k < DP / 4; ++k) cp_async16(dst + k, col + (int64_t)k * N, 4 * k < d);
-            cp_async4(aux0 + lane, a.pnorm32 + pos);
             cp_async4(pid + lane, a.perm + pos);
+#if P2_EXP
+            cp_async8(ppst + lane, a.pp32 + pos);
+#else
+            cp_async4(aux0 + lane, a.pnorm32 + pos);
+#endif
           }
           asm volatile("cp.async.wait_all;" ::: "memory");
           __syncwarp();
@@ -1399,8 +1446,8 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
           // thr >= s for every point that can pass the precise test below
           // (eps is increasing in s and |p| <= pnorm_max)
           float best_up = bestf;
-          float thr = best_up * (1.f + 1e-4f) +
-                      1.01e-6f * (qn + a.pnorm_max) * (sqrtf(2.f * best_up + 1.f) + 1e-3f) + 1e-30f;
+          float thr = (best_up + exp_slack) * (1.f + 1e-4f) +
+                      1.01e-6f * (qn + a.pnorm_max) * (sqrtf(2.f * (best_up + exp_slack) + 1.f) + 1e-3f) + 1e-30f;
           // phase 1, branch-free over the batch: the P1_DIMS leading (highest
           // variance) PCA dims of every staged point against the batch-start
           // threshold; rounded sums of non-negative terms only grow, so a
@@ -1442,6 +1489,18 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
             // dims: rounded sums of non-negative terms only grow, so a partial
             // sum above thr already rules the point out for this lane
             if (!__any_sync(0xffffffffu, (sa.x + sa.y) + (sb.x + sb.y) <= thr)) continue;
+#if P2_EXP
+            // second half in expanded form: |q~_B|^2 + |p~_B|^2 - 2 q~_B.p~_B
+            float2 ta = make_float2(0.f, 0.f), tb = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int k = DP / 8; k < DP / 4; ++k) {
+              const float4 p = pr[k];
+              ta = __ffma2_rn(q2[2 * k], make_float2(p.x, p.y), ta);
+              tb = __ffma2_rn(q2[2 * k + 1], make_float2(p.z, p.w), tb);
+            }
+            const float s = ((sa.x + sa.y) + (sb.x + sb.y)) +
+                            fmaf(2.f, (ta.x + ta.y) + (tb.x + tb.y), qqx + ppst[i].y);
+#else
 #pragma unroll
             for (int k = DP / 8; k < DP / 4; ++k) {
               const float4 p = pr[k];
@@ -1451,10 +1510,12 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
               sb = __ffma2_rn(u1, u1, sb);
             }
             const float s = (sa.x + sa.y) + (sb.x + sb.y);
+#endif
             bool surv = s <= thr;
             if (surv) {
-              const float eps = 2.5e-7f * (float)(d + 4) * s +
-                                1.0e-6f * (qn + aux0[i]) * (sqrtf(s) + 1e-3f) + 1e-30f;
+              const float sp = fmaxf(s, 0.f);
+              const float eps = 2.5e-7f * (float)(d + 4) * sp +
+                                1.0e-6f * (qn + PNORM_OF(i)) * (sqrtf(sp) + 1e-3f) + 1e-30f + exp_slack;
               surv = s - eps <= best_up;
             }
             if (__any_sync(0xffffffffu, surv)) {
@@ -1468,8 +1529,8 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
                   best_id = id;
                   best_up = infl(best);
                   bestf = best_up;
-                  thr = best_up * (1.f + 1e-4f) +
-                        1.01e-6f * (qn + a.pnorm_max) * (sqrtf(2.f * best_up + 1.f) + 1e-3f) + 1e-30f;
+                  thr = (best_up + exp_slack) * (1.f + 1e-4f) +
+                        1.01e-6f * (qn + a.pnorm_max) * (sqrtf(2.f * (best_up + exp_slack) + 1.f) + 1e-3f) + 1e-30f;
                 } else if (id != best_id) {
                   push(d2, id);
                 }
@@ -1863,27 +1924,35 @@ void launch_scatter_i64(psg_ctx* ctx, const int64_t* src, const int32_t* order, 
 }
 
 // fp32 filter copies in leaf order: q4[j/4][pos][j%4] = (float) soa[j][pos], |p| rounded up.
+// pp: (|p~|^2, |p~_B|^2) of the fp32 point p~ (B = dims >= dp / 2), rounded
+// to nearest from exact fp64 sums of the fp32 squares.
 __global__ void make_fp32_copies_kernel(const double* __restrict__ soa, int64_t N, int d, int dp,
-                                        float* __restrict__ q4, float* __restrict__ pn) {
+                                        float* __restrict__ q4, float* __restrict__ pn,
+                                        float2* __restrict__ pp) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
        i += (int64_t)gridDim.x * blockDim.x) {
-    double n2 = 0.0;
+    double n2 = 0.0, f2 = 0.0, h2 = 0.0;
     for (int j = 0; j < dp; ++j) {
       const double v = j < d ? soa[(int64_t)j * N + i] : 0.0;
-      q4[((int64_t)(j / 4) * N + i) * 4 + (j % 4)] = (float)v;
+      const float vf = (float)v;
+      q4[((int64_t)(j / 4) * N + i) * 4 + (j % 4)] = vf;
       n2 += v * v;
+      const double vv = (double)vf * (double)vf;
+      f2 += vv;
+      if (j >= dp / 2) h2 += vv;
     }
     pn[i] = __double2float_ru(sqrt(n2) * (1.0 + 1e-12));
+    if (pp) pp[i] = make_float2((float)f2, (float)h2);
   }
 }
 
 void launch_make_fp32_copies(psg_ctx* ctx, const double* soa, int64_t N, int d, int dp,
-                             float* aos32, float* pn) {
+                             float* aos32, float* pn, float2* pp) {
   ProfScope _prof(ctx, K_BUILD);
   if (N <= 0) return;
   int64_t blocks = (N + 255) / 256;
   if (blocks > (int64_t)ctx->num_sms * 32) blocks = (int64_t)ctx->num_sms * 32;
-  make_fp32_copies_kernel<<<(int)blocks, 256, 0, ctx->stream>>>(soa, N, d, dp, aos32, pn);
+  make_fp32_copies_kernel<<<(int)blocks, 256, 0, ctx->stream>>>(soa, N, d, dp, aos32, pn, pp);
   PSG_LAUNCHED(ctx);
 }
 

@@ -95,6 +95,7 @@ struct Index {
   float* proj32_q4 = nullptr;  // [dp/4][N] float4 groups, leaf order, fp32 filter copy
   int dp = 32;
   float* pnorm32 = nullptr;    // [N] leaf order, |p| rounded up
+  float2* pp32 = nullptr;      // [N] leaf order, (|p~|^2, |p~_B|^2) of the fp32 point
   float pnorm_max = 0.f;
   int32_t* perm = nullptr;     // leaf order -> id
   DevTree tree;
@@ -359,6 +360,7 @@ struct SearchArgs {
   const double* proj_soa;   // [d][N] leaf order
   const float* proj32_q4;   // [dp/4][N] float4 groups, leaf order (fp32 filter)
   const float* pnorm32;     // [N] leaf order
+  const float2* pp32 = nullptr;  // [N] leaf order (|p~|^2, |p~_B|^2) (expanded-form filter)
   float pnorm_max;          // max of pnorm32 (rounded up)
   const int32_t* perm;
   int64_t N;
@@ -421,7 +423,7 @@ void launch_scatter_f64(psg_ctx* ctx, const double* src, const int32_t* order, i
 void launch_scatter_i64(psg_ctx* ctx, const int64_t* src, const int32_t* order, int64_t n,
                         int64_t* dst);
 void launch_make_fp32_copies(psg_ctx* ctx, const double* soa, int64_t N, int d, int dp,
-                             float* aos32, float* pn);
+                             float* aos32, float* pn, float2* pp);
 // Full-D distance between query windows and assigned candidates (optimizer.cpp:117-124).
 void launch_rescore_windows(psg_ctx* ctx, const float* mirror, int img_w, int C, int w,
                             AnchorSet anchors, const Index& ix, const int32_t* idx, double* dist,
