@@ -732,8 +732,10 @@ __global__ void __launch_bounds__(32 * kSearchWarps) search_kernel(SearchArgs a)
   double* sk = st_key[warp];
   const int d = a.d;
 
-  for (int64_t q = (int64_t)blockIdx.x * kSearchWarps + warp; q < a.nq;
-       q += (int64_t)gridDim.x * kSearchWarps) {
+  const int64_t nlist = a.ovf_list ? (int64_t)*a.ovf_count : a.nq;
+  for (int64_t i = (int64_t)blockIdx.x * kSearchWarps + warp; i < nlist;
+       i += (int64_t)gridDim.x * kSearchWarps) {
+    const int64_t q = a.ovf_list ? (int64_t)a.ovf_list[i] : i;  // list mode: the pool overflows
     for (int j = lane; j < d; j += 32) qs[j] = a.q[q * d + j];
     __syncwarp();
     double best = DBL_MAX * 2;
@@ -897,6 +899,165 @@ __global__ void __launch_bounds__(32 * kSearchWarps) search_kernel(SearchArgs a)
       a.out_idx[q] = best_id;
       a.out_d2[q] = best;
       if (a.out_scanned) a.out_scanned[q] = scanned;
+    }
+    __syncwarp();
+  }
+}
+
+// ----------------------------------------------------------------------------
+// backtrack(m) with one warp per query (km_tree.cpp:232-250), m > 2: the
+// best-first frontier is an unsorted pool in shared memory holding (key,
+// node, tie id, node meta); a pop is one warp-wide lexicographic min over
+// (key, tie) carrying the slot, and the popped entry already holds the node's
+// children range or leaf range (no dependent metadata load).  An expansion
+// stages the children's centroid rows (contiguous in the breadth-first
+// layout), metas and tie ids with one round of independent coalesced loads;
+// lane c forms child c's key dist^2(q, centroid) with the reference's
+// j-ascending fp64 chain from shared memory.  A leaf stages its points
+// (leaf-ordered [d][N] columns) the same way and lane i scans point i
+// (lexicographic (dist^2, id) minimum, km_tree.cpp:128-139).
+constexpr int kBtWarps = 4, kBtCap = 192;
+
+template <int DP>
+__global__ void __launch_bounds__(32 * kBtWarps) search_backtrack_kernel(SearchArgs a) {
+  constexpr int CH = 8;  // rows staged per round (children or leaf points)
+  __shared__ double qs_all[kBtWarps][DP];
+  __shared__ double pk_all[kBtWarps][kBtCap];
+  __shared__ int4 pn_all[kBtWarps][kBtCap];  // (node, tie id, meta.x, meta.y)
+  // rows padded to an odd number of doubles: lane r reading row r, dim j is
+  // free of bank conflicts (a DP-double stride put 16 lanes on one bank)
+  constexpr int RP = DP + 1;
+  __shared__ double cs_all[kBtWarps][CH][RP];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* qs = qs_all[warp];
+  double* pk = pk_all[warp];
+  int4* pn = pn_all[warp];
+  double(*cs)[RP] = cs_all[warp];
+  const int d = a.d;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  const int2 root = a.tree.meta[0];
+  const int32_t root_tie = a.tree.tie ? a.tree.tie[0] : 0;
+  // dims d..DP-1 are zero on both sides: their terms add an exact +0.0 to a
+  // non-negative accumulator, so the full DP-step chain equals the d-step one
+  auto chain = [&](const double* r) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < DP; ++j) {
+      const double t = dsub(qs[j], r[j]);
+      acc = dadd(acc, dmul(t, t));
+    }
+    return acc;
+  };
+  for (int64_t q = (int64_t)blockIdx.x * kBtWarps + warp; q < a.nq;
+       q += (int64_t)gridDim.x * kBtWarps) {
+    for (int j = lane; j < DP; j += 32) qs[j] = j < d ? a.q[q * d + j] : 0.0;
+    if (lane == 0) {
+      pk[0] = 0.0;
+      pn[0] = make_int4(0, root_tie, root.x, root.y);
+    }
+    __syncwarp();
+    double best = kInf;
+    int32_t best_id = 0x7fffffff;
+    int64_t scanned = 0;
+    int32_t visited = 0;
+    int size = 1, leaves = 0;
+    bool overflow = false;
+    while (size > 0 && leaves < a.max_leaves) {
+      // pop the lexicographic minimum (key, tie)
+      double bk = kInf;
+      int32_t bt = 0x7fffffff, bs = -1;
+      for (int s0 = lane; s0 < size; s0 += 32) {
+        const double k = pk[s0];
+        const int32_t t = pn[s0].y;
+        if (k < bk || (k == bk && t < bt)) {
+          bk = k;
+          bt = t;
+          bs = s0;
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const double ok = __shfl_xor_sync(0xffffffffu, bk, off);
+        const int32_t ot = __shfl_xor_sync(0xffffffffu, bt, off);
+        const int32_t os = __shfl_xor_sync(0xffffffffu, bs, off);
+        if (ok < bk || (ok == bk && ot < bt)) {
+          bk = ok;
+          bt = ot;
+          bs = os;
+        }
+      }
+      const int4 e = pn[bs];
+      __syncwarp();
+      if (lane == 0) {
+        pk[bs] = pk[size - 1];
+        pn[bs] = pn[size - 1];
+      }
+      --size;
+      ++visited;
+      __syncwarp();
+      if (e.w >= 0) {  // leaf: points [e.z, e.z + e.w) of the leaf order
+        for (int base = 0; base < e.w; base += CH) {
+          const int cn = min(CH, e.w - base);
+          const int64_t p0 = (int64_t)e.z + base;
+          // the leaf's rows are contiguous in the leaf-ordered row copy
+          const double* src = a.proj_leaf + p0 * d;
+          for (int f = lane; f < cn * DP; f += 32) {
+            const int i = f / DP, j = f - i * DP;
+            cs[i][j] = j < d ? __ldg(src + (int64_t)i * d + j) : 0.0;
+          }
+          const int32_t id = lane < cn ? __ldg(a.perm + p0 + lane) : 0x7fffffff;
+          __syncwarp();
+          const double d2 = lane < cn ? chain(cs[lane]) : kInf;
+          const WarpLexMin m = warp_lexmin(d2, id);
+          if (lex_less(m.d2, m.id, best, best_id)) {
+            best = m.d2;
+            best_id = m.id;
+          }
+          __syncwarp();
+        }
+        scanned += e.w;
+        ++leaves;
+        continue;
+      }
+      const int nc = -e.w, fc = e.z;
+      if (size + nc > kBtCap) {  // frontier too wide for the pool: the query
+        overflow = true;         // is re-run by the deep-stack warp kernel
+        break;
+      }
+      for (int cb = 0; cb < nc; cb += CH) {
+        const int cn = min(CH, nc - cb);
+        // children's centroid rows are contiguous: coalesced staging
+        const double* src = a.tree.centroid + (int64_t)(fc + cb) * d;
+        for (int f = lane; f < cn * DP; f += 32) {
+          const int c = f / DP, j = f - c * DP;
+          cs[c][j] = j < d ? __ldg(src + (int64_t)c * d + j) : 0.0;
+        }
+        int2 cm = make_int2(0, 0);
+        int32_t ct = 0;
+        if (lane < cn) {
+          const int child = fc + cb + lane;
+          cm = __ldg(a.tree.meta + child);
+          ct = a.tree.tie ? __ldg(a.tree.tie + child) : child;
+        }
+        __syncwarp();
+        if (lane < cn) {
+          pk[size + lane] = chain(cs[lane]);
+          pn[size + lane] = make_int4(fc + cb + lane, ct, cm.x, cm.y);
+        }
+        size += cn;
+        __syncwarp();
+      }
+    }
+    if (lane == 0) {
+      if (overflow) {
+        a.ovf_list[atomicAdd(a.ovf_count, 1)] = (int32_t)q;
+      } else {
+        a.out_idx[q] = best_id;
+        a.out_d2[q] = best;
+        if (a.out_scanned) a.out_scanned[q] = scanned;
+        if (a.out_exact) a.out_exact[q] = scanned;
+        if (a.out_visited) a.out_visited[q] = visited;
+      }
     }
     __syncwarp();
   }
@@ -1749,6 +1910,27 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
       search_budget_kernel<32><<<(int)blocks, 128, 0, ctx->stream>>>(a);
     else
       search_budget_kernel<64><<<(int)blocks, 128, 0, ctx->stream>>>(a);
+    PSG_LAUNCHED(ctx);
+    return;
+  }
+  if (a.mode == PSG_BACKTRACK && a.d <= 64 && !ctx->knobs.legacy_search) {
+    // queries whose frontier outgrows the shared-memory pool are listed and
+    // re-run by the deep-stack warp kernel below (same answers)
+    DBuf<int32_t> ovf((size_t)a.nq);
+    DBuf<int> ovf_n(1);
+    PSG_CUDA(cudaMemsetAsync(ovf_n.p, 0, sizeof(int), ctx->stream));
+    SearchArgs b = a;
+    b.ovf_list = ovf.p;
+    b.ovf_count = ovf_n.p;
+    int64_t blocks = (a.nq + kBtWarps - 1) / kBtWarps;
+    const int64_t cap = (int64_t)ctx->num_sms * 16;
+    if (blocks > cap) blocks = cap;
+    if (a.d <= 32)
+      search_backtrack_kernel<32><<<(int)blocks, 32 * kBtWarps, 0, ctx->stream>>>(b);
+    else
+      search_backtrack_kernel<64><<<(int)blocks, 32 * kBtWarps, 0, ctx->stream>>>(b);
+    PSG_LAUNCHED(ctx);
+    search_kernel<<<ctx->num_sms, 32 * kSearchWarps, 0, ctx->stream>>>(b);
     PSG_LAUNCHED(ctx);
     return;
   }

@@ -92,6 +92,7 @@ struct Index {
   double* basis = nullptr;     // [d][D]
   double* proj = nullptr;      // [N][d] original order
   double* proj_soa = nullptr;  // [d][N] leaf order
+  double* proj_leaf = nullptr; // [N][d] leaf order (budget searches: a leaf's rows are contiguous)
   float* proj32_q4 = nullptr;  // [dp/4][N] float4 groups, leaf order, fp32 filter copy
   int dp = 32;
   float* pnorm32 = nullptr;    // [N] leaf order, |p| rounded up
@@ -358,6 +359,7 @@ struct SearchArgs {
   const int32_t* seed_idx;  // optional initial candidate per query (upper bound)
   const double* proj;       // [N][d] original order (seed distances)
   const double* proj_soa;   // [d][N] leaf order
+  const double* proj_leaf = nullptr;  // [N][d] leaf order
   const float* proj32_q4;   // [dp/4][N] float4 groups, leaf order (fp32 filter)
   const float* pnorm32;     // [N] leaf order
   const float2* pp32 = nullptr;  // [N] leaf order (|p~|^2, |p~_B|^2) (expanded-form filter)
@@ -389,6 +391,8 @@ struct SearchArgs {
   int* amb_count = nullptr;     // device counter (zeroed by the caller)
   const int* nq_dev = nullptr;  // optional: query count read on the device
   const int32_t* out_map = nullptr;  // optional (warp kernel): query -> output slot, counters add
+  int32_t* ovf_list = nullptr;       // backtrack: queries whose frontier outgrew the pool (re-run)
+  int* ovf_count = nullptr;
 };
 // Tile permutation for the next exact search of the same anchors: descending
 // previous per-tile work (order: [image_tile_count(nq, qnx)]).

@@ -172,7 +172,7 @@ double pow_cr_host(double x, double y) { return pow_cr(x, y); }
 Index::~Index() {
   // stream-ordered frees (the allocations come from the context's pool)
   cudaStream_t st = ctx ? ctx->stream : nullptr;
-  for (void* p : {(void*)ex_mirror, (void*)ex_mirror8, (void*)vectors, (void*)mean, (void*)basis, (void*)proj, (void*)proj_soa, (void*)perm, (void*)tree.centroid, (void*)tree.radius, (void*)tree.first_child, (void*)tree.n_children, (void*)tree.leaf_start, (void*)tree.leaf_count, (void*)tree.centroid32, (void*)tree.radius32, (void*)tree.cnorm32, (void*)proj32_q4, (void*)tree.centroid32T, (void*)tree.boxlo, (void*)tree.boxhi, (void*)tree.meta, (void*)tree.tie, (void*)pnorm32, (void*)ex_hist, (void*)brute_op, (void*)brute_n2, (void*)brute_nup, (void*)brute_mu, (void*)brute_tmax, (void*)tc_b, (void*)tc_bmu, (void*)pp32})
+  for (void* p : {(void*)ex_mirror, (void*)ex_mirror8, (void*)vectors, (void*)mean, (void*)basis, (void*)proj, (void*)proj_soa, (void*)perm, (void*)tree.centroid, (void*)tree.radius, (void*)tree.first_child, (void*)tree.n_children, (void*)tree.leaf_start, (void*)tree.leaf_count, (void*)tree.centroid32, (void*)tree.radius32, (void*)tree.cnorm32, (void*)proj32_q4, (void*)tree.centroid32T, (void*)tree.boxlo, (void*)tree.boxhi, (void*)tree.meta, (void*)tree.tie, (void*)pnorm32, (void*)ex_hist, (void*)brute_op, (void*)brute_n2, (void*)brute_nup, (void*)brute_mu, (void*)brute_tmax, (void*)tc_b, (void*)tc_bmu, (void*)pp32, (void*)proj_leaf})
     if (p) cudaFreeAsync(p, st);
 }
 
@@ -191,7 +191,7 @@ void free_tree(Index& ix) {
                   (void*)T.leaf_start, (void*)T.leaf_count, (void*)T.centroid32,
                   (void*)T.centroid32T, (void*)T.radius32, (void*)T.cnorm32, (void*)T.boxlo,
                   (void*)T.boxhi, (void*)T.meta, (void*)T.tie, (void*)ix.perm, (void*)ix.proj_soa,
-                  (void*)ix.proj32_q4, (void*)ix.pnorm32, (void*)ix.pp32})
+                  (void*)ix.proj32_q4, (void*)ix.pnorm32, (void*)ix.pp32, (void*)ix.proj_leaf})
     if (p) cudaFreeAsync(p, ctx_stream);
   T = DevTree{};
   ix.perm = nullptr;
@@ -199,6 +199,7 @@ void free_tree(Index& ix) {
   ix.proj32_q4 = nullptr;
   ix.pnorm32 = nullptr;
   ix.pp32 = nullptr;
+  ix.proj_leaf = nullptr;
 }
 
 void upload_tree(psg_ctx* ctx, Index& ix) {
@@ -230,6 +231,8 @@ void upload_tree(psg_ctx* ctx, Index& ix) {
   up(ix.perm, t.perm);
   ix.proj_soa = dalloc<double>((size_t)ix.N * (d > 0 ? d : 1));
   launch_gather_soa(ctx, ix.proj, ix.N, d, ix.perm, ix.proj_soa);
+  ix.proj_leaf = dalloc<double>((size_t)ix.N * (d > 0 ? d : 1));
+  if (d > 0) launch_gather_rows_f64(ctx, ix.proj, ix.perm, ix.N, d, ix.proj_leaf);
   // fp32 bound/filter copies (conservative rounding, see search_exact_kernel)
   ix.dp = d <= 32 ? 32 : (d <= 64 ? 64 : kMaxDP);
   ix.proj32_q4 = dalloc<float>((size_t)ix.N * ix.dp);
@@ -700,6 +703,7 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
   a.seed_idx = L.cfg.budget.mode == PSG_EXACT ? seed : nullptr;
   a.proj = ix.proj;
   a.proj_soa = ix.proj_soa;
+  a.proj_leaf = ix.proj_leaf;
   a.proj32_q4 = ix.proj32_q4;
   a.pnorm32 = ix.pnorm32;
   a.pp32 = ix.pp32;
@@ -1481,6 +1485,7 @@ psg_status psg_index_query(psg_ctx* ctx, const psg_index* index, const float* Q,
     a.d = ix.d;
     a.proj = ix.proj;
     a.proj_soa = ix.proj_soa;
+    a.proj_leaf = ix.proj_leaf;
     a.proj32_q4 = ix.proj32_q4;
     a.pnorm32 = ix.pnorm32;
     a.pp32 = ix.pp32;
