@@ -30,6 +30,9 @@
 // leading PCA dims of the branch-free first filter phase (measured on the
 // bench stage: 4 -> 1.41 ms, 8 -> 1.50, 12 -> 1.75)
 #define P1_DIMS 4
+// image query tiles: kTW x kTH anchors per warp (lane = query).  Measured on
+// the bench stage: 8 x 4 1.39 ms, 4 x 8 1.40, 16 x 2 1.46.
+constexpr int kTW = 8, kTH = 32 / kTW;
 // phase 2: the second half of the dims in expanded form |q~|^2 + |p~|^2 -
 // 2 q~.p~ (one FFMA2 per two dims; rounding covered by exp_slack).  Measured:
 // 1.41 -> 1.39 ms; all dims expanded (no half-way early exit) 1.52.
@@ -1439,8 +1442,8 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
   // image queries: 8 x 4 anchor tiles (overlapping windows share candidates);
   // vector queries: 32 consecutive rows
   const int qny = a.qxs ? (int)(nq / a.qnx) : 0;
-  const int tnx = a.qxs ? (a.qnx + 7) / 8 : 0;
-  const int64_t n_tiles = a.qxs ? (int64_t)tnx * ((qny + 3) / 4) : (nq + 31) / 32;
+  const int tnx = a.qxs ? (a.qnx + kTW - 1) / kTW : 0;
+  const int64_t n_tiles = a.qxs ? (int64_t)tnx * ((qny + kTH - 1) / kTH) : (nq + 31) / 32;
 
   // persistent warps fetch tiles from a global ticket: tile costs vary ~4x,
   // and a fast warp must not idle until its CTA's slowest warp finishes
@@ -1454,7 +1457,7 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
     bool valid;
     if (a.qxs) {
       const int tx = (int)(t % tnx), ty = (int)(t / tnx);
-      const int ix = tx * 8 + (lane & 7), iy = ty * 4 + (lane >> 3);
+      const int ix = tx * kTW + (lane % kTW), iy = ty * kTH + (lane / kTW);
       valid = ix < a.qnx && iy < qny;
       q = valid ? (int64_t)iy * a.qnx + ix : 0;
     } else {
@@ -2018,7 +2021,7 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(const int64_t* __restr
   __syncthreads();
   for (int64_t t = threadIdx.x; t < n_tiles; t += blockDim.x) {
     const int tx = (int)(t % tnx), ty = (int)(t / tnx);
-    atomicAdd(&cnt[tile_cost_bucket(scanned[(int64_t)ty * 4 * qnx + tx * 8])], 1);
+    atomicAdd(&cnt[tile_cost_bucket(scanned[(int64_t)ty * kTH * qnx + tx * kTW])], 1);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -2031,14 +2034,14 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(const int64_t* __restr
   __syncthreads();
   for (int64_t t = threadIdx.x; t < n_tiles; t += blockDim.x) {
     const int tx = (int)(t % tnx), ty = (int)(t / tnx);
-    const int b = tile_cost_bucket(scanned[(int64_t)ty * 4 * qnx + tx * 8]);
+    const int b = tile_cost_bucket(scanned[(int64_t)ty * kTH * qnx + tx * kTW]);
     order[atomicAdd(&pos[b], 1)] = (int32_t)t;
   }
 }
 
 int64_t image_tile_count(int64_t nq, int qnx) {
   const int qny = (int)(nq / qnx);
-  return (int64_t)((qnx + 7) / 8) * ((qny + 3) / 4);
+  return (int64_t)((qnx + kTW - 1) / kTW) * ((qny + kTH - 1) / kTH);
 }
 
 void launch_tile_order(psg_ctx* ctx, const int64_t* prev_scanned, int64_t nq, int qnx,
@@ -2046,7 +2049,7 @@ void launch_tile_order(psg_ctx* ctx, const int64_t* prev_scanned, int64_t nq, in
   ProfScope _prof(ctx, K_SCHED);
   const int64_t nt = image_tile_count(nq, qnx);
   if (nt <= 0) return;
-  tile_order_kernel<<<1, 1024, 0, ctx->stream>>>(prev_scanned, qnx, (qnx + 7) / 8, nt, order);
+  tile_order_kernel<<<1, 1024, 0, ctx->stream>>>(prev_scanned, qnx, (qnx + kTW - 1) / kTW, nt, order);
   PSG_LAUNCHED(ctx);
 }
 
