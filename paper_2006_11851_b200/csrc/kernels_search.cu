@@ -33,11 +33,16 @@
 // image query tiles: kTW x kTH anchors per warp (lane = query).  Measured on
 // the bench stage: 8 x 4 1.39 ms, 4 x 8 1.40, 16 x 2 1.46.
 constexpr int kTW = 8, kTH = 32 / kTW;
-// phase 2: the second half of the dims in expanded form |q~|^2 + |p~|^2 -
-// 2 q~.p~ (one FFMA2 per two dims; rounding covered by exp_slack).  Measured:
-// 1.41 -> 1.39 ms; all dims expanded (no half-way early exit) 1.52.
+// phase 2: the dims after the first DP / P2_SPLIT_DEN (difference form, then
+// an early exit) in expanded form |q~|^2 + |p~|^2 - 2 q~.p~ (one FFMA2 per two
+// dims; rounding covered by exp_slack).  Measured on the bench stage: all
+// difference form 1.41 ms; split 16 | 16 1.39; 8 | 24 1.38; 4 | 28 1.58;
+// all expanded (no early exit) 1.52.
 #ifndef P2_EXP
 #define P2_EXP 1
+#endif
+#ifndef P2_SPLIT_DEN
+#define P2_SPLIT_DEN 4
 #endif
 #if P2_EXP
 #define PNORM_OF(i) (sqrtf(ppst[i].x) * 1.000001f)
@@ -1507,7 +1512,7 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
     }
     const float qn = __double2float_ru(sqrt(qn2) * (1.0 + 1e-12));
 #if P2_EXP
-    // |q~_B|^2 of the fp32 query (B = the second half of the dims), and the
+    // |q~_B|^2 of the fp32 query (B = the dims after the first DP / P2_SPLIT_DEN), and the
     // rigorous bound of the expanded form's rounding: |fl(qq + pp - 2 q.p) -
     // |q~ - p~|^2| <= (n + 4) 2^-24 (qq + pp + 2 |q.p|) <= (n + 4) 2^-24 (|q| + |p|)^2
     // for n = the dims in expanded form (x1.5 margin for the rounded norms)
@@ -1515,13 +1520,13 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
     {
       double t = 0.0;
 #pragma unroll
-      for (int j = DP / 4; j < DP / 2; ++j) {
+      for (int j = DP / 2 / P2_SPLIT_DEN; j < DP / 2; ++j) {
         t += (double)q2[j].x * (double)q2[j].x;
         t += (double)q2[j].y * (double)q2[j].y;
       }
       qqx = (float)t;
     }
-    const float exp_slack = 1.5f * (float)(DP / 2 + 4) * 5.9604645e-8f *
+    const float exp_slack = 1.5f * (float)(DP - DP / P2_SPLIT_DEN + 4) * 5.9604645e-8f *
                             (qn + a.pnorm_max) * (qn + a.pnorm_max);
 #else
     constexpr float exp_slack = 0.f;
@@ -1642,22 +1647,22 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
             // bound covers it
             float2 sa = make_float2(0.f, 0.f), sb = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int k = 0; k < DP / 8; ++k) {
+            for (int k = 0; k < DP / 4 / P2_SPLIT_DEN; ++k) {
               const float4 p = pr[k];
               const float2 u0 = __fadd2_rn(q2[2 * k], make_float2(p.x, p.y));
               const float2 u1 = __fadd2_rn(q2[2 * k + 1], make_float2(p.z, p.w));
               sa = __ffma2_rn(u0, u0, sa);
               sb = __ffma2_rn(u1, u1, sb);
             }
-            // early exit after the leading (highest-variance) half of the PCA
-            // dims: rounded sums of non-negative terms only grow, so a partial
-            // sum above thr already rules the point out for this lane
+            // early exit after the leading (highest-variance) PCA dims: rounded
+            // sums of non-negative terms only grow, so a partial sum above thr
+            // already rules the point out for this lane
             if (!__any_sync(0xffffffffu, (sa.x + sa.y) + (sb.x + sb.y) <= thr)) continue;
 #if P2_EXP
-            // second half in expanded form: |q~_B|^2 + |p~_B|^2 - 2 q~_B.p~_B
+            // the remaining dims B in expanded form: |q~_B|^2 + |p~_B|^2 - 2 q~_B.p~_B
             float2 ta = make_float2(0.f, 0.f), tb = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int k = DP / 8; k < DP / 4; ++k) {
+            for (int k = DP / 4 / P2_SPLIT_DEN; k < DP / 4; ++k) {
               const float4 p = pr[k];
               ta = __ffma2_rn(q2[2 * k], make_float2(p.x, p.y), ta);
               tb = __ffma2_rn(q2[2 * k + 1], make_float2(p.z, p.w), tb);
@@ -2109,7 +2114,7 @@ void launch_scatter_i64(psg_ctx* ctx, const int64_t* src, const int32_t* order, 
 }
 
 // fp32 filter copies in leaf order: q4[j/4][pos][j%4] = (float) soa[j][pos], |p| rounded up.
-// pp: (|p~|^2, |p~_B|^2) of the fp32 point p~ (B = dims >= dp / 2), rounded
+// pp: (|p~|^2, |p~_B|^2) of the fp32 point p~ (B = dims >= dp / P2_SPLIT_DEN), rounded
 // to nearest from exact fp64 sums of the fp32 squares.
 __global__ void make_fp32_copies_kernel(const double* __restrict__ soa, int64_t N, int d, int dp,
                                         float* __restrict__ q4, float* __restrict__ pn,
@@ -2124,7 +2129,7 @@ __global__ void make_fp32_copies_kernel(const double* __restrict__ soa, int64_t 
       n2 += v * v;
       const double vv = (double)vf * (double)vf;
       f2 += vv;
-      if (j >= dp / 2) h2 += vv;
+      if (j >= dp / P2_SPLIT_DEN) h2 += vv;
     }
     pn[i] = __double2float_ru(sqrt(n2) * (1.0 + 1e-12));
     if (pp) pp[i] = make_float2((float)f2, (float)h2);

@@ -96,7 +96,7 @@ struct Index {
   float* proj32_q4 = nullptr;  // [dp/4][N] float4 groups, leaf order, fp32 filter copy
   int dp = 32;
   float* pnorm32 = nullptr;    // [N] leaf order, |p| rounded up
-  float2* pp32 = nullptr;      // [N] leaf order, (|p~|^2, |p~_B|^2) of the fp32 point
+  float2* pp32 = nullptr;      // [N] leaf order, (|p~|^2, |p~_B|^2) of the fp32 point (B: kernels_search.cu P2_SPLIT_DEN)
   float pnorm_max = 0.f;
   int32_t* perm = nullptr;     // leaf order -> id
   DevTree tree;
