@@ -35,6 +35,9 @@
 // 128 anchors = one contiguous 2 KB block).  Persistent, warp-specialised:
 // warp 0 stages, warp 1 issues the UMMAs, warps 2-9 drain TMEM.  Basis rows
 // go in blocks of 32 (TMEM holds 416 accumulator columns per block).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
@@ -152,11 +155,24 @@ struct TcArgs {
   int d, kb;
   double* out;          // [nx * ny][d]
   float* delta_out;     // [nx * ny]
+  int tma_sp = 0;       // > 0: anchor spacing of the tensor map (strided tiles by TMA)
 };
 
 // A work item = (tile of <= 128 consecutive anchors of one anchor row, basis block).
+// 5-D TMA of one K group of 128 anchors at a uniform anchor spacing sp:
+// dims (16 bytes, sp / 2 pixel pairs, anchor column, row, digit slice)
+__device__ __forceinline__ void tma_group(void* dst, const CUtensorMap* map, int c1, int c2, int c3,
+                                          int c4, uint64_t* mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4, %5, %6}], [%7];" ::"r"(mma::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+      "r"(mma::smem_u32(mbar))
+      : "memory");
+}
+
 template <bool kStrip>
-__global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(TcArgs a) {
+__global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(TcArgs a, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int S = kStrip ? kStripStages : kStages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (kStrip ? kStripBarOff : kBarOff));
@@ -272,13 +288,28 @@ __global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(TcArgs a) {
       // the anchors step by 2 pixels (16-byte aligned: even pixel index)
       const bool contig = a.xs[ix0 + nt - 1] - x0 == 2 * (nt - 1) && (x0 & 1) == 0 &&
                           (a.img_w & 1) == 0;
+      // uniform spacing sp > 2: one 5-D TMA per (slice, K group) gathers the
+      // 128 anchors' 16-byte chunks (anchor column stride sp pixels)
+      const bool tma = !contig && a.tma_sp > 0 && (x0 & 1) == 0 &&
+                       a.xs[ix0 + nt - 1] - x0 == a.tma_sp * (nt - 1);
       const int8_t* bsrc = a.bop + (int64_t)kblk * n_groups * kNP * 16;
       for (int c = 0; c < n_chunks; ++c) {
         mma::mbar_wait(&empty[stage], ph ^ 1u);
         uint8_t* A = smem + stage * kStageBytes;
         uint8_t* B = A + kSA * kASlice;
         const int g0 = c * kGC, ng = min(kGC, n_groups - g0);
-        if (contig) {
+        if (tma) {
+          if (lane == 0) {
+            mma::mbar_expect_tx(&full[stage], (uint32_t)(ng * (kSA * kAGroup + kNP * 16)));
+            mma::bulk_g2s(B, bsrc + (int64_t)g0 * kNP * 16, ng * kNP * 16, &full[stage]);
+            for (int g = 0; g < ng; ++g) {
+              const int gg = g0 + g, dy = gg / gpr, dx = (gg - dy * gpr) * 2;
+              const int X = x0 + dx, c2 = X / a.tma_sp, c1 = (X - c2 * a.tma_sp) >> 1;
+              for (int s = 0; s < kSA; ++s)
+                tma_group(A + s * kASlice + g * kAGroup, &tmap, c1, c2, ay + dy, s, &full[stage]);
+            }
+          }
+        } else if (contig) {
           if (lane == 0) {
             mma::mbar_expect_tx(&full[stage], (uint32_t)(ng * (kSA * nt * 16 + kNP * 16)));
             mma::bulk_g2s(B, bsrc + (int64_t)g0 * kNP * 16, ng * kNP * 16, &full[stage]);
@@ -612,7 +643,7 @@ bool tc_prepare(psg_ctx* ctx, Index& ix) {
 
 void launch_project_windows_tc(psg_ctx* ctx, const uint8_t* q8, int64_t slice_bytes, int img_w,
                                const int* bad, AnchorSet anchors, bool stride2, const Index& ix,
-                               double* out, float* delta) {
+                               double* out, float* delta, int sp) {
   ProfScope _prof(ctx, K_PROJECT);
   if (anchors.count <= 0) return;
   if (!ix.tc) fail(PSG_E_LOGIC, "tensor-core projection without a prepared basis");
@@ -647,10 +678,34 @@ void launch_project_windows_tc(psg_ctx* ctx, const uint8_t* q8, int64_t slice_by
   const int blocks = (int)std::min<int64_t>(items, ctx->num_sms);
   const bool strip = stride2 && nkb == 1 && a.w % 4 == 0 && a.w <= 8 && (img_w & 1) == 0 &&
                      (uint32_t)(a.kb / 16) * kNP * 16 <= kBresBytes;
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof tmap);
+  if (!strip && sp > 2 && (sp & 1) == 0 && (img_w & 1) == 0 && img_w >= sp) {
+    // digit mirror slice s, row y, anchor column c, pixel pair p, byte e at
+    // s * slice_bytes + y * img_w * 8 + c * sp * 8 + p * 16 + e
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult qr;
+      void* fn = nullptr;
+      PSG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
+      if (qr != cudaDriverEntryPointSuccess || !fn) fail(PSG_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const int64_t rows = slice_bytes / ((int64_t)img_w * 8);
+    const cuuint64_t dims[5] = {16, (cuuint64_t)(sp / 2), (cuuint64_t)(img_w / sp), (cuuint64_t)rows,
+                                (cuuint64_t)kSA};
+    const cuuint64_t strides[4] = {16, (cuuint64_t)sp * 8, (cuuint64_t)img_w * 8, (cuuint64_t)slice_bytes};
+    const cuuint32_t box[5] = {16, 1, (cuuint32_t)kTM, 1, 1};
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    const CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<uint8_t*>(q8), dims, strides,
+                              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS) a.tma_sp = sp;
+  }
   if (strip)
-    project_tc_kernel<true><<<blocks, kTcThreads, kStripSmemBytes, ctx->stream>>>(a);
+    project_tc_kernel<true><<<blocks, kTcThreads, kStripSmemBytes, ctx->stream>>>(a, tmap);
   else
-    project_tc_kernel<false><<<blocks, kTcThreads, kSmemBytes, ctx->stream>>>(a);
+    project_tc_kernel<false><<<blocks, kTcThreads, kSmemBytes, ctx->stream>>>(a, tmap);
   PSG_LAUNCHED(ctx);
 }
 

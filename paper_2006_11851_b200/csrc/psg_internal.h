@@ -320,7 +320,7 @@ bool tc_prepare(psg_ctx* ctx, Index& ix);
 // (spacing 2, W - w even): the strip-mode kernel applies.
 void launch_project_windows_tc(psg_ctx* ctx, const uint8_t* q8, int64_t slice_bytes, int img_w,
                                const int* bad, AnchorSet anchors, bool stride2, const Index& ix,
-                               double* out, float* delta);
+                               double* out, float* delta, int sp = 0);
 // Exact fallback for the ambiguous queries of an approximate search (count
 // read on the device): the reference's projection chain of each listed
 // window, then either the exact lexicographic min over its two band

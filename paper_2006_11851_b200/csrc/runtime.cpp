@@ -692,7 +692,7 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
     PSG_CUDA(cudaMemsetAsync(L.full_n.p, 0, sizeof(int), ctx->stream));
     launch_make_digits(ctx, L.mirror.p, L.C, L.W, L.Hl, L.q8.p, q8_slice, L.q8_bad.p);
     launch_project_windows_tc(ctx, L.q8.p, q8_slice, L.W, L.q8_bad.p, as, L.stride2, ix,
-                              L.qproj.p, L.qdelta.p);
+                              L.qproj.p, L.qdelta.p, L.cfg.spacing);
   } else if (ix.d > 0) {
     launch_project_windows(ctx, L.mirror.p, L.W, L.C, L.w, as, ix.mean, ix.basis, ix.d, L.qproj.p);
   }
@@ -2189,7 +2189,7 @@ extern "C" psg_status psg_debug_projection(psg_ctx* ctx, const psg_index* index,
     const AnchorSet as{xs.p, ys.p, (int)hx.size(), A};
     bool stride2 = hx[0] % 2 == 0;
     for (size_t i = 1; i < hx.size(); ++i) stride2 = stride2 && hx[i] - hx[i - 1] == 2;
-    launch_project_windows_tc(ctx, q8.p, P * 8, W, bad.p, as, stride2, ix, qt.p, dl.p);
+    launch_project_windows_tc(ctx, q8.p, P * 8, W, bad.p, as, stride2, ix, qt.p, dl.p, spacing);
     launch_project_windows(ctx, mir.p, W, ix.C, ix.w, as, ix.mean, ix.basis, ix.d, qe.p);
     if (q_tc) qt.download(ctx, q_tc, qt.n);
     if (delta) dl.download(ctx, delta, dl.n);
