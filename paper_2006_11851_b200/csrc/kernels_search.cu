@@ -1850,9 +1850,16 @@ static int tile_resident_ctas(psg_ctx* ctx) {
   return per_sm * ctx->num_sms;
 }
 
-bool search_uses_tiles(psg_ctx* ctx, const DevTree& tree, int d, bool exact) {
+// Image searches with few queries leave most of the GPU idle on 32-query
+// tiles (one warp per tile): below ~6 tiles per SM the warp-per-query kernel
+// wins (measured: cfg3 finest w = 32, 15,625 anchors: tiles 4.06 ms vs
+// 2.79 ms; w = 16, 64,009 anchors: 2.54 vs 7.07).
+static bool enough_tiles(psg_ctx* ctx, int64_t nq) { return nq >= (int64_t)32 * 6 * ctx->num_sms; }
+
+bool search_uses_tiles(psg_ctx* ctx, const DevTree& tree, int d, bool exact, int64_t nq) {
   return exact && d <= 64 && tree.centroid32 && !ctx->knobs.legacy_search &&
-         tree.max_children <= kTileMaxB && 1 + tree.max_depth * (tree.max_children - 1) <= kTileStack;
+         tree.max_children <= kTileMaxB && 1 + tree.max_depth * (tree.max_children - 1) <= kTileStack &&
+         (nq < 0 || enough_tiles(ctx, nq));
 }
 
 void launch_search(psg_ctx* ctx, const SearchArgs& a) {
@@ -1876,7 +1883,8 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
   }
   if (a.d > kMaxD) fail(PSG_E_DOMAIN, "retained PCA dimension > 128 is not supported");
   const bool tile_ok = a.d <= 64 && a.tree.max_children <= kTileMaxB &&
-                       1 + a.tree.max_depth * (a.tree.max_children - 1) <= kTileStack;
+                       1 + a.tree.max_depth * (a.tree.max_children - 1) <= kTileStack &&
+                       (!a.qxs || a.qdelta || enough_tiles(ctx, a.nq));
   if (a.mode == PSG_EXACT && a.proj32_q4 && a.tree.centroid32 && tile_ok && !ctx->knobs.legacy_search) {
     if (!a.sched) fail(PSG_E_LOGIC, "tile search launched without its scheduler counters");
     const int64_t tiles = (a.nq + 31) / 32;

@@ -409,7 +409,8 @@ void launch_brute_search(psg_ctx* ctx, const Index& ix, const RowSrc& qsrc, int6
                          int64_t* out_scanned, int64_t* out_exact);
 void launch_search(psg_ctx* ctx, const SearchArgs& a);
 // true when an exact search of this tree runs on the tile kernel
-bool search_uses_tiles(psg_ctx* ctx, const DevTree& tree, int d, bool exact);
+// nq >= 0: an image search of nq anchors (few anchors -> warp-per-query kernel)
+bool search_uses_tiles(psg_ctx* ctx, const DevTree& tree, int d, bool exact, int64_t nq = -1);
 // tcgen05 (UMMA) tile search; returns false when the tree shape is unsupported.
 // Tile search with the leaf filter on mma.sync (bf16 split); false if unsupported.
 // Locality ordering of unstructured queries (search-only workloads).

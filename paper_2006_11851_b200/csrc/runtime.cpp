@@ -671,7 +671,7 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
   // exact budget on the tile kernel: tensor-core projection with an error
   // band + exact fallback for the ambiguous queries (kernels_project_tc.cu)
   const bool tc = ix.tc && ix.d > 0 && L.cfg.budget.mode == PSG_EXACT &&
-                  !ctx->knobs.exact_projection && search_uses_tiles(ctx, ix.tree, ix.d, true);
+                  !ctx->knobs.exact_projection && search_uses_tiles(ctx, ix.tree, ix.d, true, L.Ao);
   const int64_t q8_slice = (int64_t)L.W * L.Hl * 8;
   if (tc) {
     if (!L.q8.p) {

@@ -36,8 +36,8 @@ def main():
             "optimize_s": sum(s["optimize_millis"] for s in rep["stages"]) / 1e3,
             "final_energy": rep["final_energy"], "total_nn_calls": rep["total_nn_calls"],
             "image_range": [float(out.min()), float(out.max())],
-            "stages": [{k: (round(v, 2) if isinstance(v, float) else v) for k, v in s.items()}
-                       for s in rep["stages"]]}
+            "stages": [{k: (round(v, 2) if isinstance(v, float) else v) for k, v in s.items()
+                        if isinstance(v, (int, float, str))} for s in rep["stages"]]}
     print(json.dumps(line))
 
 
