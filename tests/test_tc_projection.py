@@ -22,7 +22,12 @@ api = pytest.importorskip("paper_2006_11851_b200.api")
 @pytest.mark.parametrize("G,w,d,out,ex_size", [(1, 8, 16, 96, 48), (2, 8, 32, 256, 64),
                                                (2, 16, 32, 128, 64), (1, 4, 12, 64, 32),
                                                (2, 8, 48, 160, 64), (1, 8, 64, 96, 48),
-                                               (2, 32, 24, 160, 64)])
+                                               (2, 32, 24, 160, 64),
+                                               # spacing 4 / 8: the 5-D TMA tensor-map staging,
+                                               # with a clamped (non-uniform) last anchor and
+                                               # with several 128-anchor tiles per row
+                                               (2, 16, 32, 134, 64), (1, 32, 24, 170, 64),
+                                               (1, 16, 32, 600, 64)])
 def test_projection_error_within_bound(gpu_ctx, port, G, w, d, out, ex_size):
     ex = wl.rgbs_planes(wl.sinusoid_exemplar(ex_size, 16, 2.0, d), G)
     init = wl.init_output(ex, out, out, G, w)
