@@ -2193,6 +2193,36 @@ __device__ __forceinline__ double window_dist2_any(const float* __restrict__ mir
                                                    const float* __restrict__ ex8, int ew, int ex,
                                                    int ey);
 
+// Same chain, with a whole window row's loads (w = 8: 8 candidate pixels and
+// 8 x NC state values) issued before the row's adds: one memory round trip per
+// row instead of one per pixel pair, for the latency-bound few-anchor case.
+template <int NC>
+__device__ __forceinline__ double window_dist2_pad_rows8(const float* __restrict__ mirror, int img_w,
+                                                         int ax, int ay, const float* __restrict__ ex8,
+                                                         int ew, int ex, int ey) {
+  double acc = 0.0;
+  for (int dy = 0; dy < 8; ++dy) {
+    const float* v = mirror + ((int64_t)(ay + dy) * img_w + ax) * NC;
+    const float* z8 = ex8 + ((int64_t)(ey + dy) * ew + ex) * 8;
+    float4 z0[8], z1[8];
+    float vc[8 * NC];
+#pragma unroll
+    for (int dx = 0; dx < 8; ++dx) ldg256(z8 + 8 * dx, z0[dx], z1[dx]);
+#pragma unroll
+    for (int k = 0; k < 8 * NC; ++k) vc[k] = __ldg(v + k);
+#pragma unroll
+    for (int dx = 0; dx < 8; ++dx) {
+      const float zc[8] = {z0[dx].x, z0[dx].y, z0[dx].z, z0[dx].w, z1[dx].x, z1[dx].y, z1[dx].z, z1[dx].w};
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const double t = dsub((double)vc[dx * NC + c], (double)zc[c]);
+        acc = dadd(acc, dmul(t, t));
+      }
+    }
+  }
+  return acc;
+}
+
 __device__ __forceinline__ double window_dist2(const float* __restrict__ mirror, int img_w, int C,
                                                int w, int ax, int ay,
                                                const float* __restrict__ ex_mirror, int ew,
@@ -2253,9 +2283,9 @@ __global__ void rescore_windows_kernel(const float* __restrict__ mirror, int img
 // whose assignment did not change has the distance prev_dist already (the
 // lsq-after diagnostic computed it: same window, same candidate, same chain),
 // so only the changed anchors (~5% once EM settles) are recomputed: they are
-// listed (warp-aggregated), then a warp per listed anchor forms its D squared
-// differences in parallel (coalesced window and candidate rows) and one lane
-// adds them in the reference's order j = (dy, dx, c) ascending.
+// listed (warp-aggregated) and a thread per listed anchor runs the reference's
+// chain (a warp per anchor with one lane adding the staged squares measured
+// ~3x slower: the 320-step fp64 chain is the latency, not the loads).
 constexpr int kRescoreBlock = 256;
 __global__ void __launch_bounds__(kRescoreBlock) rescore_mark_kernel(
     int64_t n, const int32_t* __restrict__ idx, const int32_t* __restrict__ prev_idx,
@@ -2279,57 +2309,27 @@ __global__ void __launch_bounds__(kRescoreBlock) rescore_mark_kernel(
   }
 }
 
-constexpr int kRescoreChunk = 256;  // squared terms staged per warp round
-__global__ void __launch_bounds__(256) rescore_list_kernel(
+// One thread per listed (changed) anchor: all lanes run a chain (the listed
+// anchors are compacted globally, so warps are full even when few anchors
+// changed).
+__global__ void __launch_bounds__(128) rescore_list_kernel(
     const float* __restrict__ mirror, int img_w, int C, int w, const int32_t* __restrict__ xs,
     const int32_t* __restrict__ ys, int nx, const float* __restrict__ ex_mirror,
     const float* __restrict__ ex8, int ew, int nxe, const int32_t* __restrict__ idx,
     const int32_t* __restrict__ list, const int* __restrict__ count, double* __restrict__ dist) {
-  __shared__ double sq_all[8][kRescoreChunk];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* sq = sq_all[warp];
   const int n = *count;
-  const int D = w * w * C, row = w * C;
-  for (int i = blockIdx.x * 8 + warp; i < n; i += gridDim.x * 8) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int64_t b = list[i];
     const int32_t id = idx[b];
-    const int ax = xs[b % nx], ay = ys[b / nx];
-    const int ex = id % nxe, ey = id / nxe;
-    double acc = 0.0;
-    for (int j0 = 0; j0 < D; j0 += kRescoreChunk) {
-#pragma unroll
-      for (int u = 0; u < kRescoreChunk / 32; ++u) {
-        const int j = j0 + u * 32 + lane;
-        if (j < D) {
-          const int dy = j / row, r = j - dy * row;  // r = dx * C + c
-          const float v = __ldg(mirror + ((int64_t)(ay + dy) * img_w + ax) * C + r);
-          float z;
-          if (ex8) {
-            const int dx = r / C, c = r - dx * C;
-            z = __ldg(ex8 + ((int64_t)(ey + dy) * ew + ex + dx) * 8 + c);
-          } else {
-            z = __ldg(ex_mirror + ((int64_t)(ey + dy) * ew + ex) * C + r);
-          }
-          const double t = dsub((double)v, (double)z);
-          sq[u * 32 + lane] = dmul(t, t);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) {
-        const int m = min(kRescoreChunk, D - j0);
-        int k = 0;
-        for (; k + 8 <= m; k += 8) {
-          double s8[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) s8[u] = sq[k + u];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) acc = dadd(acc, s8[u]);
-        }
-        for (; k < m; ++k) acc = dadd(acc, sq[k]);
-      }
-      __syncwarp();
-    }
-    if (lane == 0) dist[b] = sqrt(acc);
+    const int ax = xs[b % nx], ay = ys[b / nx], ex = id % nxe, ey = id / nxe;
+    double d2;
+    if (ex8 && w == 8 && C == 5)
+      d2 = window_dist2_pad_rows8<5>(mirror, img_w, ax, ay, ex8, ew, ex, ey);
+    else if (ex8 && w == 8 && C == 4)
+      d2 = window_dist2_pad_rows8<4>(mirror, img_w, ax, ay, ex8, ew, ex, ey);
+    else
+      d2 = window_dist2_any(mirror, img_w, C, w, ax, ay, ex_mirror, ex8, ew, ex, ey);
+    dist[b] = sqrt(d2);
   }
 }
 
@@ -2348,7 +2348,7 @@ void launch_rescore_windows(psg_ctx* ctx, const float* mirror, int img_w, int C,
     rescore_mark_kernel<<<(unsigned)blocks, kRescoreBlock, 0, ctx->stream>>>(anchors.count, idx, prev_idx,
                                                                             prev_dist, dist, list, count);
     PSG_LAUNCHED(ctx);
-    rescore_list_kernel<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(
+    rescore_list_kernel<<<ctx->num_sms * 8, 128, 0, ctx->stream>>>(
         mirror, img_w, C, w, anchors.xs, anchors.ys, anchors.nx, ix.ex_mirror, ex8, ix.ew, ix.nxe, idx,
         list, count, dist);
     PSG_LAUNCHED(ctx);
