@@ -1932,12 +1932,18 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
   if (a.mode == PSG_BACKTRACK && a.d <= 64 && !ctx->knobs.legacy_search) {
     // queries whose frontier outgrows the shared-memory pool are listed and
     // re-run by the deep-stack warp kernel below (same answers)
-    DBuf<int32_t> ovf((size_t)a.nq);
-    DBuf<int> ovf_n(1);
-    PSG_CUDA(cudaMemsetAsync(ovf_n.p, 0, sizeof(int), ctx->stream));
+    // (the caller may provide the list buffers: levels allocate them once,
+    // outside any captured iteration)
+    DBuf<int32_t> ovf;
+    DBuf<int> ovf_n;
     SearchArgs b = a;
-    b.ovf_list = ovf.p;
-    b.ovf_count = ovf_n.p;
+    if (!b.ovf_list || !b.ovf_count) {
+      ovf.alloc((size_t)a.nq);
+      ovf_n.alloc(1);
+      b.ovf_list = ovf.p;
+      b.ovf_count = ovf_n.p;
+    }
+    PSG_CUDA(cudaMemsetAsync(b.ovf_count, 0, sizeof(int), ctx->stream));
     int64_t blocks = (a.nq + kBtWarps - 1) / kBtWarps;
     const int64_t cap = (int64_t)ctx->num_sms * 16;
     if (blocks > cap) blocks = cap;
