@@ -1959,7 +1959,10 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
   int64_t blocks = (a.nq + kSearchWarps - 1) / kSearchWarps;
   const int64_t cap = (int64_t)ctx->num_sms * 16;
   if (blocks > cap) blocks = cap;
-  search_kernel<<<(int)blocks, 32 * kSearchWarps, 0, ctx->stream>>>(a);
+  SearchArgs c = a;  // all queries (not the overflow-list mode)
+  c.ovf_list = nullptr;
+  c.ovf_count = nullptr;
+  search_kernel<<<(int)blocks, 32 * kSearchWarps, 0, ctx->stream>>>(c);
   PSG_LAUNCHED(ctx);
 }
 
