@@ -1685,7 +1685,9 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
               const float sp = fmaxf(s, 0.f);
               const float eps = 2.5e-7f * (float)(d + 4) * sp +
                                 1.0e-6f * (qn + PNORM_OF(i)) * (sqrtf(sp) + 1e-3f) + 1e-30f + exp_slack;
-              surv = s - eps <= best_up;
+              // the current best (usually the seed, met again in its leaf) is
+              // exact already: re-evaluating it cannot change anything
+              surv = s - eps <= best_up && pid[i] != best_id;
             }
             if (__any_sync(0xffffffffu, surv)) {
               if (surv) {
