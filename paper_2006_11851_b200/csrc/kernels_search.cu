@@ -1222,13 +1222,15 @@ __global__ void __launch_bounds__(256) search_exact_kernel(SearchArgs a) {
             const float pn = a.pnorm32[pos];
             eps = 2.5e-7f * (float)(d + 4) * s + 1.0e-6f * (qn + pn) * (sqrtf(s) + 1e-3f) + 1e-30f;
           }
-          const bool surv = pos >= 0 && (double)s - (double)eps <= best;
+          // (the current best is exact already: never re-evaluated)
+          const int32_t pid = pos >= 0 ? a.perm[pos] : -1;
+          const bool surv = pos >= 0 && (double)s - (double)eps <= best && pid != best_id;
           const unsigned smask = __ballot_sync(0xffffffffu, surv);
           if (!smask) continue;
           double d2 = kInf;
           int32_t id = 0x7fffffff;
           if (surv) {
-            id = a.perm[pos];
+            id = pid;
             const double* col = a.proj_soa + pos;
             double acc = 0.0;
 #pragma unroll
