@@ -1719,15 +1719,14 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
       const int nc = -node.y;
       const int fc = node.x;
       __syncwarp();
-      if (lane < nc) cmeta[lane] = a.tree.meta[fc + lane];
-#pragma unroll
-      for (int f = lane; f < kTileMaxB * kBoxDims; f += 32) {  // dims >= d hold [0, 0]
-        const int c = f % kTileMaxB, j = f / kTileMaxB;
-        if (c < nc) {  // stored (lo, -hi): one FADD2 per dim below
-          boxs[c][2 * j] = __ldg(a.tree.boxlo + (int64_t)j * nn + fc + c);
-          boxs[c][2 * j + 1] = -__ldg(a.tree.boxhi + (int64_t)j * nn + fc + c);
-        }
-      }
+      // the children's metas and (lo, -hi) boxes (64 contiguous bytes per
+      // child in the tree's box2 layout; dims >= d hold [0, 0]) copied
+      // global -> shared asynchronously
+      if (lane < nc) cp_async8(cmeta + lane, a.tree.meta + fc + lane);
+      for (int f = lane; f < nc * (kBoxDims / 2); f += 32)
+        cp_async16(reinterpret_cast<float4*>(&boxs[0][0]) + f,
+                   reinterpret_cast<const float4*>(a.tree.box2) + (int64_t)fc * (kBoxDims / 2) + f, true);
+      asm volatile("cp.async.wait_all;" ::: "memory");
       __syncwarp();
       // phase 1: box bound of every child (8 leading dims):
       // gap_j = max(lo_j - q_j - m, q_j - hi_j - m, 0) as one FADD2 + FMNMX3.

@@ -60,6 +60,7 @@ struct DevTree {
   float* cnorm32 = nullptr;     // |centroid|
   float* boxlo = nullptr;       // [kBoxDims][n_nodes] per-dim minimum over the subtree
   float* boxhi = nullptr;       // [kBoxDims][n_nodes]
+  float* box2 = nullptr;        // [n_nodes][kBoxDims][2]: (lo_j, -hi_j) per node, 64 contiguous bytes
   int2* meta = nullptr;         // {first_child, -n_children} or {leaf_start, leaf_count}
   int32_t* tie = nullptr;       // optional backtrack tie-break id per node (null = node index)
 };

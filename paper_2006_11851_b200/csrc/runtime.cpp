@@ -172,7 +172,7 @@ double pow_cr_host(double x, double y) { return pow_cr(x, y); }
 Index::~Index() {
   // stream-ordered frees (the allocations come from the context's pool)
   cudaStream_t st = ctx ? ctx->stream : nullptr;
-  for (void* p : {(void*)ex_mirror, (void*)ex_mirror8, (void*)vectors, (void*)mean, (void*)basis, (void*)proj, (void*)proj_soa, (void*)perm, (void*)tree.centroid, (void*)tree.radius, (void*)tree.first_child, (void*)tree.n_children, (void*)tree.leaf_start, (void*)tree.leaf_count, (void*)tree.centroid32, (void*)tree.radius32, (void*)tree.cnorm32, (void*)proj32_q4, (void*)tree.centroid32T, (void*)tree.boxlo, (void*)tree.boxhi, (void*)tree.meta, (void*)tree.tie, (void*)pnorm32, (void*)ex_hist, (void*)brute_op, (void*)brute_n2, (void*)brute_nup, (void*)brute_mu, (void*)brute_tmax, (void*)tc_b, (void*)tc_bmu, (void*)pp32, (void*)proj_leaf})
+  for (void* p : {(void*)ex_mirror, (void*)ex_mirror8, (void*)vectors, (void*)mean, (void*)basis, (void*)proj, (void*)proj_soa, (void*)perm, (void*)tree.centroid, (void*)tree.radius, (void*)tree.first_child, (void*)tree.n_children, (void*)tree.leaf_start, (void*)tree.leaf_count, (void*)tree.centroid32, (void*)tree.radius32, (void*)tree.cnorm32, (void*)proj32_q4, (void*)tree.centroid32T, (void*)tree.boxlo, (void*)tree.boxhi, (void*)tree.box2, (void*)tree.meta, (void*)tree.tie, (void*)pnorm32, (void*)ex_hist, (void*)brute_op, (void*)brute_n2, (void*)brute_nup, (void*)brute_mu, (void*)brute_tmax, (void*)tc_b, (void*)tc_bmu, (void*)pp32, (void*)proj_leaf})
     if (p) cudaFreeAsync(p, st);
 }
 
@@ -190,7 +190,7 @@ void free_tree(Index& ix) {
   for (void* p : {(void*)T.centroid, (void*)T.radius, (void*)T.first_child, (void*)T.n_children,
                   (void*)T.leaf_start, (void*)T.leaf_count, (void*)T.centroid32,
                   (void*)T.centroid32T, (void*)T.radius32, (void*)T.cnorm32, (void*)T.boxlo,
-                  (void*)T.boxhi, (void*)T.meta, (void*)T.tie, (void*)ix.perm, (void*)ix.proj_soa,
+                  (void*)T.boxhi, (void*)T.box2, (void*)T.meta, (void*)T.tie, (void*)ix.perm, (void*)ix.proj_soa,
                   (void*)ix.proj32_q4, (void*)ix.pnorm32, (void*)ix.pp32, (void*)ix.proj_leaf})
     if (p) cudaFreeAsync(p, ctx_stream);
   T = DevTree{};
@@ -261,6 +261,14 @@ void upload_tree(psg_ctx* ctx, Index& ix) {
         blo[(size_t)j * nn + i] = std::nextafter((float)t.boxlo[(size_t)i * kBoxDims + j], -INFINITY);
         bhi[(size_t)j * nn + i] = std::nextafter((float)t.boxhi[(size_t)i * kBoxDims + j], INFINITY);
       }
+    std::vector<float> box2((size_t)nn * 2 * kBoxDims);
+    for (int i = 0; i < nn; ++i)
+      for (int j = 0; j < kBoxDims; ++j) {
+        box2[((size_t)i * kBoxDims + j) * 2] = blo[(size_t)j * nn + i];
+        box2[((size_t)i * kBoxDims + j) * 2 + 1] = -bhi[(size_t)j * nn + i];
+      }
+    ix.tree.box2 = dalloc<float>(box2.size());
+    up(ix.tree.box2, box2);
     ix.tree.centroid32T = dalloc<float>(c32t.empty() ? 1 : c32t.size());
     ix.tree.boxlo = dalloc<float>(blo.size());
     ix.tree.boxhi = dalloc<float>(bhi.size());
