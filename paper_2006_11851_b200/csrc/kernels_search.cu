@@ -1624,19 +1624,24 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
           // threshold; rounded sums of non-negative terms only grow, so a
           // partial sum above thr already rules the point out for this lane
           uint32_t pass = 0;
+          // in chunks of 8 staged points (a batch holds cn <= 32 of them)
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float4* pr = reinterpret_cast<const float4*>(stage + i * RS);
-            float2 sa = make_float2(0.f, 0.f);
+          for (int i0 = 0; i0 < 32; i0 += 8) {
+            if (i0 >= cn) break;
 #pragma unroll
-            for (int k = 0; k < P1_DIMS / 4; ++k) {
-              const float4 p = pr[k];
-              const float2 u0 = __fadd2_rn(q2[2 * k], make_float2(p.x, p.y));
-              const float2 u1 = __fadd2_rn(q2[2 * k + 1], make_float2(p.z, p.w));
-              sa = __ffma2_rn(u0, u0, sa);
-              sa = __ffma2_rn(u1, u1, sa);
+            for (int i = i0; i < i0 + 8; ++i) {
+              const float4* pr = reinterpret_cast<const float4*>(stage + i * RS);
+              float2 sa = make_float2(0.f, 0.f);
+#pragma unroll
+              for (int k = 0; k < P1_DIMS / 4; ++k) {
+                const float4 p = pr[k];
+                const float2 u0 = __fadd2_rn(q2[2 * k], make_float2(p.x, p.y));
+                const float2 u1 = __fadd2_rn(q2[2 * k + 1], make_float2(p.z, p.w));
+                sa = __ffma2_rn(u0, u0, sa);
+                sa = __ffma2_rn(u1, u1, sa);
+              }
+              if (sa.x + sa.y <= thr) pass |= 1u << i;
             }
-            if (sa.x + sa.y <= thr) pass |= 1u << i;
           }
           if (cn < 32) pass &= (1u << cn) - 1u;
           uint32_t todo = __reduce_or_sync(0xffffffffu, pass);
