@@ -30,6 +30,9 @@
 // leading PCA dims of the branch-free first filter phase (measured on the
 // bench stage: 4 -> 1.41 ms, 8 -> 1.50, 12 -> 1.75)
 #define P1_DIMS 4
+// phase-1 chunk: 8 staged points (4: same speed, 16: 3% slower, 32 = the
+// whole staging buffer: 6% slower -- short batches filtered stale rows)
+#define P1_CHUNK 8
 // image query tiles: kTW x kTH anchors per warp (lane = query).  Measured on
 // the bench stage: 8 x 4 1.39 ms, 4 x 8 1.40, 16 x 2 1.46.
 constexpr int kTW = 8, kTH = 32 / kTW;
@@ -1624,12 +1627,12 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
           // threshold; rounded sums of non-negative terms only grow, so a
           // partial sum above thr already rules the point out for this lane
           uint32_t pass = 0;
-          // in chunks of 8 staged points (a batch holds cn <= 32 of them)
+          // in chunks of P1_CHUNK staged points (a batch holds cn <= 32 of them)
 #pragma unroll
-          for (int i0 = 0; i0 < 32; i0 += 8) {
+          for (int i0 = 0; i0 < 32; i0 += P1_CHUNK) {
             if (i0 >= cn) break;
 #pragma unroll
-            for (int i = i0; i < i0 + 8; ++i) {
+            for (int i = i0; i < i0 + P1_CHUNK; ++i) {
               const float4* pr = reinterpret_cast<const float4*>(stage + i * RS);
               float2 sa = make_float2(0.f, 0.f);
 #pragma unroll
