@@ -2226,10 +2226,17 @@ __device__ __forceinline__ double window_dist2_pad_rows8(const float* __restrict
     const float* z8 = ex8 + ((int64_t)(ey + dy) * ew + ex) * 8;
     float4 z0[8], z1[8];
     float vc[8 * NC];
+    // volatile loads: issued in this order, all before the row's chain (the
+    // compiler otherwise sinks each load next to its use, one round trip per
+    // pixel)
 #pragma unroll
-    for (int dx = 0; dx < 8; ++dx) ldg256(z8 + 8 * dx, z0[dx], z1[dx]);
+    for (int dx = 0; dx < 8; ++dx)
+      asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                   : "=f"(z0[dx].x), "=f"(z0[dx].y), "=f"(z0[dx].z), "=f"(z0[dx].w), "=f"(z1[dx].x),
+                     "=f"(z1[dx].y), "=f"(z1[dx].z), "=f"(z1[dx].w)
+                   : "l"(z8 + 8 * dx));
 #pragma unroll
-    for (int k = 0; k < 8 * NC; ++k) vc[k] = __ldg(v + k);
+    for (int k = 0; k < 8 * NC; ++k) asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(vc[k]) : "l"(v + k));
 #pragma unroll
     for (int dx = 0; dx < 8; ++dx) {
       const float zc[8] = {z0[dx].x, z0[dx].y, z0[dx].z, z0[dx].w, z1[dx].x, z1[dx].y, z1[dx].z, z1[dx].w};
@@ -2332,7 +2339,7 @@ __global__ void __launch_bounds__(kRescoreBlock) rescore_mark_kernel(
 // One thread per listed (changed) anchor: all lanes run a chain (the listed
 // anchors are compacted globally, so warps are full even when few anchors
 // changed).
-__global__ void __launch_bounds__(128) rescore_list_kernel(
+__global__ void __maxnreg__(168) rescore_list_kernel(
     const float* __restrict__ mirror, int img_w, int C, int w, const int32_t* __restrict__ xs,
     const int32_t* __restrict__ ys, int nx, const float* __restrict__ ex_mirror,
     const float* __restrict__ ex8, int ew, int nxe, const int32_t* __restrict__ idx,
