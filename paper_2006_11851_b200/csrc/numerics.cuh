@@ -99,16 +99,19 @@ PSG_HD dd dd_exp(dd x) {
   // scale down by 2^-10 then Taylor (degree 11), then square 10 times
   r.hi = ldexp(r.hi, -10);
   r.lo = ldexp(r.lo, -10);
+  // 1/n as double-doubles (|error| < 2^-106 relative): the Taylor terms are
+  // scaled by multiplication instead of two fp64 divisions per term
+  const double inv_hi[12] = {0, 0, 0x1p-1, 0x1.5555555555555p-2, 0x1p-2, 0x1.999999999999ap-3,
+                             0x1.5555555555555p-3, 0x1.2492492492492p-3, 0x1p-3, 0x1.c71c71c71c71cp-4,
+                             0x1.999999999999ap-4, 0x1.745d1745d1746p-4};
+  const double inv_lo[12] = {0, 0, 0, 0x1.5555555555555p-56, 0, -0x1.999999999999ap-57,
+                             0x1.5555555555555p-57, 0x1.2492492492492p-57, 0, 0x1.c71c71c71c71cp-58,
+                             -0x1.999999999999ap-58, -0x1.745d1745d1746p-59};
   dd term = r;
   dd sum = r;  // expm1 accumulation
+#pragma unroll
   for (int n = 2; n <= 11; ++n) {
-    term = dd_mul(term, r);
-    // divide by n: term = term / n (exact enough: compute in dd by two-step)
-    const double qh = term.hi / n;
-    const dd back = two_prod(qh, (double)n);
-    const double ql = dsub(dsub(term.hi, back.hi), back.lo);
-    const double ql2 = dadd(ql, term.lo) / n;
-    term = quick_two_sum(qh, ql2);
+    term = dd_mul(dd_mul(term, r), dd{inv_hi[n], inv_lo[n]});
     sum = dd_add(sum, term);
   }
   // (1 + s)^2 - 1 = 2s + s^2 keeps the small quantity exact-ish
