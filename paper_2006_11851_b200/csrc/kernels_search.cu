@@ -41,16 +41,8 @@ constexpr int kTW = 8, kTH = 32 / kTW;
 // dims; rounding covered by exp_slack).  Measured on the bench stage: all
 // difference form 1.41 ms; split 16 | 16 1.39; 8 | 24 1.38; 4 | 28 1.58;
 // all expanded (no early exit) 1.52.
-#ifndef P2_EXP
-#define P2_EXP 1
-#endif
 #ifndef P2_SPLIT_DEN
 #define P2_SPLIT_DEN 4
-#endif
-#if P2_EXP
-#define PNORM_OF(i) (sqrtf(ppst[i].x) * 1.000001f)
-#else
-#define PNORM_OF(i) (aux0[i])
 #endif
 #ifndef RECHECK_BATCH
 #define RECHECK_BATCH 4
@@ -1410,13 +1402,9 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
   // bounds (pruning only loosens by < 2^-7 = 0.78%), half the largest shared array
   __shared__ __nv_bfloat16 st_lb[kTileWarps][kTileStack][32];
   __shared__ __align__(16) float stage_all[kTileWarps][32 * RS];
-#if P2_EXP
   // staged points' (|p~|^2, |p~_B|^2); |p| <= sqrt(|p~|^2) (1 + 1e-6)
   __shared__ float2 pp_all[kTileWarps][32];
   float2* ppst = pp_all[threadIdx.x >> 5];
-#else
-  __shared__ float aux_all[kTileWarps][32];  // staged points' |p|
-#endif
   __shared__ int2 cmeta_all[kTileWarps][kTileMaxB];
   __shared__ __align__(16) float box_all[kTileWarps][kTileMaxB][2 * kBoxDims];
   __shared__ int32_t pid_all[kTileWarps][32];
@@ -1430,9 +1418,6 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
   int2* sm_ = st_meta[warp];
   __nv_bfloat16(*slb)[32] = st_lb[warp];
   float* stage = stage_all[warp];
-#if !P2_EXP
-  float* aux0 = aux_all[warp];
-#endif
   int2* cmeta = cmeta_all[warp];
   float(*boxs)[2 * kBoxDims] = box_all[warp];
   int32_t* pid = pid_all[warp];
@@ -1516,7 +1501,6 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
       qn2 += v0 * v0 + v1 * v1;
     }
     const float qn = __double2float_ru(sqrt(qn2) * (1.0 + 1e-12));
-#if P2_EXP
     // |q~_B|^2 of the fp32 query (B = the dims after the first DP / P2_SPLIT_DEN), and the
     // rigorous bound of the expanded form's rounding: |fl(qq + pp - 2 q.p) -
     // |q~ - p~|^2| <= (n + 4) 2^-24 (qq + pp + 2 |q.p|) <= (n + 4) 2^-24 (|q| + |p|)^2
@@ -1533,9 +1517,6 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
     }
     const float exp_slack = 1.5f * (float)(DP - DP / P2_SPLIT_DEN + 4) * 5.9604645e-8f *
                             (qn + a.pnorm_max) * (qn + a.pnorm_max);
-#else
-    constexpr float exp_slack = 0.f;
-#endif
     // box margin: >= |float(q_j) - q_j| + the rounding of (-q_j -/+ margin)
     const float qdelta2 = 2.4e-7f * qn;
     // invalid lanes hold best = -1: every bound (>= 0) prunes them
@@ -1608,11 +1589,7 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
 #pragma unroll
             for (int k = 0; k < DP / 4; ++k) cp_async16(dst + k, col + (int64_t)k * N, 4 * k < d);
             cp_async4(pid + lane, a.perm + pos);
-#if P2_EXP
             cp_async8(ppst + lane, a.pp32 + pos);
-#else
-            cp_async4(aux0 + lane, a.pnorm32 + pos);
-#endif
           }
           asm volatile("cp.async.wait_all;" ::: "memory");
           __syncwarp();
@@ -1668,7 +1645,6 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
             // sums of non-negative terms only grow, so a partial sum above thr
             // already rules the point out for this lane
             if (!__any_sync(0xffffffffu, (sa.x + sa.y) + (sb.x + sb.y) <= thr)) continue;
-#if P2_EXP
             // the remaining dims B in expanded form: |q~_B|^2 + |p~_B|^2 - 2 q~_B.p~_B
             float2 ta = make_float2(0.f, 0.f), tb = make_float2(0.f, 0.f);
 #pragma unroll
@@ -1679,22 +1655,11 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
             }
             const float s = ((sa.x + sa.y) + (sb.x + sb.y)) +
                             fmaf(2.f, (ta.x + ta.y) + (tb.x + tb.y), qqx + ppst[i].y);
-#else
-#pragma unroll
-            for (int k = DP / 8; k < DP / 4; ++k) {
-              const float4 p = pr[k];
-              const float2 u0 = __fadd2_rn(q2[2 * k], make_float2(p.x, p.y));
-              const float2 u1 = __fadd2_rn(q2[2 * k + 1], make_float2(p.z, p.w));
-              sa = __ffma2_rn(u0, u0, sa);
-              sb = __ffma2_rn(u1, u1, sb);
-            }
-            const float s = (sa.x + sa.y) + (sb.x + sb.y);
-#endif
             bool surv = s <= thr;
             if (surv) {
               const float sp = fmaxf(s, 0.f);
               const float eps = 2.5e-7f * (float)(d + 4) * sp +
-                                1.0e-6f * (qn + PNORM_OF(i)) * (sqrtf(sp) + 1e-3f) + 1e-30f + exp_slack;
+                                1.0e-6f * (qn + (sqrtf(ppst[i].x) * 1.000001f)) * (sqrtf(sp) + 1e-3f) + 1e-30f + exp_slack;
               // the current best (usually the seed, met again in its leaf) is
               // exact already: re-evaluating it cannot change anything
               surv = s - eps <= best_up && pid[i] != best_id;
