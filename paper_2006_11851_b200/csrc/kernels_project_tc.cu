@@ -683,13 +683,19 @@ void launch_project_windows_tc(psg_ctx* ctx, const uint8_t* q8, int64_t slice_by
   if (!strip && sp > 2 && (sp & 1) == 0 && (img_w & 1) == 0 && img_w >= sp) {
     // digit mirror slice s, row y, anchor column c, pixel pair p, byte e at
     // s * slice_bytes + y * img_w * 8 + c * sp * 8 + p * 16 + e
+    // (a driver without the tensor-map entry point keeps the register-copy
+    // staging of strided tiles: same results, slower)
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-    if (!encode) {
+    static bool probed = false;
+    if (!probed) {
+      probed = true;
       cudaDriverEntryPointQueryResult qr;
       void* fn = nullptr;
-      PSG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
-      if (qr != cudaDriverEntryPointSuccess || !fn) fail(PSG_E_CUDA, "cuTensorMapEncodeTiled unavailable");
-      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) == cudaSuccess &&
+          qr == cudaDriverEntryPointSuccess && fn)
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+      else
+        (void)cudaGetLastError();
     }
     const int64_t rows = slice_bytes / ((int64_t)img_w * 8);
     const cuuint64_t dims[5] = {16, (cuuint64_t)(sp / 2), (cuuint64_t)(img_w / sp), (cuuint64_t)rows,
@@ -697,7 +703,7 @@ void launch_project_windows_tc(psg_ctx* ctx, const uint8_t* q8, int64_t slice_by
     const cuuint64_t strides[4] = {16, (cuuint64_t)sp * 8, (cuuint64_t)img_w * 8, (cuuint64_t)slice_bytes};
     const cuuint32_t box[5] = {16, 1, (cuuint32_t)kTM, 1, 1};
     const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-    const CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<uint8_t*>(q8), dims, strides,
+    const CUresult r = !encode ? CUDA_ERROR_NOT_SUPPORTED : encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<uint8_t*>(q8), dims, strides,
                               box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r == CUDA_SUCCESS) a.tma_sp = sp;
