@@ -156,6 +156,8 @@ struct TcArgs {
   double* out;          // [nx * ny][d]
   float* delta_out;     // [nx * ny]
   int tma_sp = 0;       // > 0: anchor spacing of the tensor map (strided tiles by TMA)
+  int kb_first = 0;     // first basis block of this launch
+  int nkb_run = 0;      // basis blocks of this launch (0: all)
 };
 
 // A work item = (tile of <= 128 consecutive anchors of one anchor row, basis block).
@@ -204,7 +206,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(TcArgs a, con
   const uint32_t tmem = *tmem_slot;
 
   const int tpr = (a.nx + kTM - 1) / kTM;  // tiles per anchor row
-  const int nkb = (a.d + kNB - 1) / kNB;   // basis blocks
+  const int nkb = a.nkb_run > 0 ? a.nkb_run : (a.d + kNB - 1) / kNB;  // basis blocks (this launch)
   const int64_t n_items = (int64_t)tpr * a.ny * nkb;
   const int gpr = a.w >> 1;                // 16-byte groups per window row
   const int n_groups = a.kb >> 4;          // per slice
@@ -214,7 +216,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(TcArgs a, con
     // ---- producer (strip mode): the basis once, then one window row per stage --------
     if (lane == 0) {
       mma::mbar_expect_tx(bfull, (uint32_t)(n_groups * kNP * 16));
-      mma::bulk_g2s(smem, a.bop, n_groups * kNP * 16, bfull);
+      mma::bulk_g2s(smem, a.bop + (int64_t)a.kb_first * n_groups * kNP * 16, n_groups * kNP * 16, bfull);
       int stage = 0;
       uint32_t ph = 0;
       for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(TcArgs a, con
     uint32_t ph = 0;
     for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int64_t t = it / nkb;
-      const int kblk = (int)(it - t * nkb);
+      const int kblk = a.kb_first + (int)(it - t * nkb);
       const int iy = (int)(t / tpr), ix0 = (int)(t - (int64_t)iy * tpr) * kTM;
       const int nt = min(kTM, a.nx - ix0);
       const int ay = a.ys[iy];
@@ -394,7 +396,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) project_tc_kernel(TcArgs a, con
     uint32_t tph = 0;
     for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int64_t t = it / nkb;
-      const int kblk = (int)(it - t * nkb);
+      const int kblk = a.kb_first + (int)(it - t * nkb);
       mma::mbar_wait(tfull, tph);
       tph ^= 1u;
       mma::fence_after();
@@ -676,7 +678,9 @@ void launch_project_windows_tc(psg_ctx* ctx, const uint8_t* q8, int64_t slice_by
   const int nkb = (a.d + kNB - 1) / kNB;
   const int64_t items = (int64_t)((a.nx + kTM - 1) / kTM) * a.ny * nkb;
   const int blocks = (int)std::min<int64_t>(items, ctx->num_sms);
-  const bool strip = stride2 && nkb == 1 && a.w % 4 == 0 && a.w <= 8 && (img_w & 1) == 0 &&
+  // strip mode keeps one basis block resident: d > 32 runs one strip launch
+  // per block (the window rows are streamed once per block)
+  const bool strip = stride2 && a.w % 4 == 0 && a.w <= 8 && (img_w & 1) == 0 &&
                      (uint32_t)(a.kb / 16) * kNP * 16 <= kBresBytes;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof tmap);
@@ -708,9 +712,16 @@ void launch_project_windows_tc(psg_ctx* ctx, const uint8_t* q8, int64_t slice_by
                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r == CUDA_SUCCESS) a.tma_sp = sp;
   }
-  if (strip)
-    project_tc_kernel<true><<<blocks, kTcThreads, kStripSmemBytes, ctx->stream>>>(a, tmap);
-  else
+  if (strip) {
+    const int blocks1 = (int)std::min<int64_t>(items / nkb, ctx->num_sms);
+    for (int b = 0; b < nkb; ++b) {
+      TcArgs ab = a;
+      ab.kb_first = b;
+      ab.nkb_run = 1;
+      project_tc_kernel<true><<<blocks1, kTcThreads, kStripSmemBytes, ctx->stream>>>(ab, tmap);
+      if (b + 1 < nkb) PSG_LAUNCHED(ctx);
+    }
+  } else
     project_tc_kernel<false><<<blocks, kTcThreads, kSmemBytes, ctx->stream>>>(a, tmap);
   PSG_LAUNCHED(ctx);
 }
