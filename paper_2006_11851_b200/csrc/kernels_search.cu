@@ -1866,11 +1866,18 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
     const int64_t tiles = (a.nq + 31) / 32;
     const int wpb = a.d <= 32 ? 4 : 2;  // static smem <= 48 KB per CTA
     int64_t blocks = (tiles + wpb - 1) / wpb;
-    const int64_t cap = a.d <= 32 ? tile_resident_ctas<32, 4>(ctx) : tile_resident_ctas<64, 2>(ctx);
+    // the instantiation's DP must equal the index's fp32 layout width (ix.dp:
+    // the per-point half norms are split at DP / P2_SPLIT_DEN)
+    const int64_t cap = a.d <= 32   ? tile_resident_ctas<32, 4>(ctx)
+                        : a.d <= 48 ? tile_resident_ctas<48, 2>(ctx)
+                                    : tile_resident_ctas<64, 2>(ctx);
     if (blocks > cap) blocks = cap;
     if (a.d <= 32)
       (a.qdelta ? search_tile_kernel<32, 4, true> : search_tile_kernel<32, 4, false>)
           <<<(int)blocks, 32 * 4, 0, ctx->stream>>>(a);
+    else if (a.d <= 48)
+      (a.qdelta ? search_tile_kernel<48, 2, true> : search_tile_kernel<48, 2, false>)
+          <<<(int)blocks, 32 * 2, 0, ctx->stream>>>(a);
     else
       (a.qdelta ? search_tile_kernel<64, 2, true> : search_tile_kernel<64, 2, false>)
           <<<(int)blocks, 32 * 2, 0, ctx->stream>>>(a);
