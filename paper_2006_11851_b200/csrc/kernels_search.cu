@@ -44,6 +44,9 @@ constexpr int kTW = 8, kTH = 32 / kTW;
 #ifndef P2_SPLIT_DEN
 #define P2_SPLIT_DEN 4
 #endif
+// dims in difference form: DP / P2_SPLIT_DEN rounded down to whole float4
+// groups (the per-point half norms pp32.y use the same split)
+__host__ __device__ constexpr int p2_split(int dp) { return (dp / P2_SPLIT_DEN) & ~3; }
 #ifndef RECHECK_BATCH
 #define RECHECK_BATCH 4
 #endif
@@ -1509,13 +1512,13 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
     {
       double t = 0.0;
 #pragma unroll
-      for (int j = DP / 2 / P2_SPLIT_DEN; j < DP / 2; ++j) {
+      for (int j = p2_split(DP) / 2; j < DP / 2; ++j) {
         t += (double)q2[j].x * (double)q2[j].x;
         t += (double)q2[j].y * (double)q2[j].y;
       }
       qqx = (float)t;
     }
-    const float exp_slack = 1.5f * (float)(DP - DP / P2_SPLIT_DEN + 4) * 5.9604645e-8f *
+    const float exp_slack = 1.5f * (float)(DP - p2_split(DP) + 4) * 5.9604645e-8f *
                             (qn + a.pnorm_max) * (qn + a.pnorm_max);
     // box margin: >= |float(q_j) - q_j| + the rounding of (-q_j -/+ margin)
     const float qdelta2 = 2.4e-7f * qn;
@@ -1634,7 +1637,7 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
             // bound covers it
             float2 sa = make_float2(0.f, 0.f), sb = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int k = 0; k < DP / 4 / P2_SPLIT_DEN; ++k) {
+            for (int k = 0; k < p2_split(DP) / 4; ++k) {
               const float4 p = pr[k];
               const float2 u0 = __fadd2_rn(q2[2 * k], make_float2(p.x, p.y));
               const float2 u1 = __fadd2_rn(q2[2 * k + 1], make_float2(p.z, p.w));
@@ -1648,7 +1651,7 @@ __global__ void __launch_bounds__(32 * kTileWarps, DP <= 32 ? TILE_MIN_CTAS : TI
             // the remaining dims B in expanded form: |q~_B|^2 + |p~_B|^2 - 2 q~_B.p~_B
             float2 ta = make_float2(0.f, 0.f), tb = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int k = DP / 4 / P2_SPLIT_DEN; k < DP / 4; ++k) {
+            for (int k = p2_split(DP) / 4; k < DP / 4; ++k) {
               const float4 p = pr[k];
               ta = __ffma2_rn(q2[2 * k], make_float2(p.x, p.y), ta);
               tb = __ffma2_rn(q2[2 * k + 1], make_float2(p.z, p.w), tb);
@@ -1868,11 +1871,15 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
     int64_t blocks = (tiles + wpb - 1) / wpb;
     // the instantiation's DP must equal the index's fp32 layout width (ix.dp:
     // the per-point half norms are split at DP / P2_SPLIT_DEN)
-    const int64_t cap = a.d <= 32   ? tile_resident_ctas<32, 4>(ctx)
+    const int64_t cap = a.d <= 24   ? tile_resident_ctas<24, 4>(ctx)
+                        : a.d <= 32 ? tile_resident_ctas<32, 4>(ctx)
                         : a.d <= 48 ? tile_resident_ctas<48, 2>(ctx)
                                     : tile_resident_ctas<64, 2>(ctx);
     if (blocks > cap) blocks = cap;
-    if (a.d <= 32)
+    if (a.d <= 24)
+      (a.qdelta ? search_tile_kernel<24, 4, true> : search_tile_kernel<24, 4, false>)
+          <<<(int)blocks, 32 * 4, 0, ctx->stream>>>(a);
+    else if (a.d <= 32)
       (a.qdelta ? search_tile_kernel<32, 4, true> : search_tile_kernel<32, 4, false>)
           <<<(int)blocks, 32 * 4, 0, ctx->stream>>>(a);
     else if (a.d <= 48)
@@ -2129,7 +2136,7 @@ __global__ void make_fp32_copies_kernel(const double* __restrict__ soa, int64_t 
       n2 += v * v;
       const double vv = (double)vf * (double)vf;
       f2 += vv;
-      if (j >= dp / P2_SPLIT_DEN) h2 += vv;
+      if (j >= p2_split(dp)) h2 += vv;
     }
     pn[i] = __double2float_ru(sqrt(n2) * (1.0 + 1e-12));
     if (pp) pp[i] = make_float2((float)f2, (float)h2);

@@ -234,8 +234,8 @@ void upload_tree(psg_ctx* ctx, Index& ix) {
   ix.proj_leaf = dalloc<double>((size_t)ix.N * (d > 0 ? d : 1));
   if (d > 0) launch_gather_rows_f64(ctx, ix.proj, ix.perm, ix.N, d, ix.proj_leaf);
   // fp32 bound/filter copies (conservative rounding, see search_exact_kernel)
-  // fp32 layout width = the tile kernel's DP (32, 48, 64; kMaxDP above)
-  ix.dp = d <= 32 ? 32 : (d <= 48 ? 48 : (d <= 64 ? 64 : kMaxDP));
+  // fp32 layout width = the tile kernel's DP (24, 32, 48, 64; kMaxDP above)
+  ix.dp = d <= 24 ? 24 : (d <= 32 ? 32 : (d <= 48 ? 48 : (d <= 64 ? 64 : kMaxDP)));
   ix.proj32_q4 = dalloc<float>((size_t)ix.N * ix.dp);
   ix.pnorm32 = dalloc<float>(ix.N);
   ix.pp32 = dalloc<float2>(ix.N);
