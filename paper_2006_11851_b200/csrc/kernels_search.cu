@@ -1070,6 +1070,215 @@ __global__ void __launch_bounds__(32 * kBtWarps) search_backtrack_kernel(SearchA
 }
 
 // ----------------------------------------------------------------------------
+// backtrack(m), m > 2, with a GROUP of G lanes per query (G = 8 or 16 >= the
+// tree's branching; 32 / G queries per warp).  The warp-per-query kernel above
+// is issue-bound with 8 of its 32 lanes forming keys; here lane c of a group
+// forms child c's key (or scans leaf point c) and every lane is busy.
+//
+//  * rows come straight from global memory into registers: the children of a
+//    node (contiguous in the breadth-first layout) and the points of a leaf
+//    are stored PAIR-INTERLEAVED per block -- element (row i, dim j) of a
+//    block of n rows starting at row s sits at s*dE + (j/2)*(2n) + 2i + (j&1)
+//    (dE = d rounded up to even) -- so the G lanes' 16-byte loads of one dim
+//    pair are one contiguous segment: no shared-memory staging, no barrier
+//    between the loads and the chains;
+//  * the frontier is the same unsorted pool of (key, tie id, node meta) in
+//    shared memory, CAP entries per query; a pop is a group-wide lexicographic
+//    min; a query whose frontier would outgrow the pool is listed and re-run
+//    by the deep-stack kernel (same answers);
+//  * the loop body is the same for leaves and inner nodes (evaluate <= G rows,
+//    then either fold into the best or append to the pool), so the groups of
+//    a warp stay converged; every shuffle uses the full-warp mask with xor
+//    offsets < G.
+// Keys and leaf distances are the reference's fp64 j-ascending chains
+// (km_tree.cpp:15-22, 128-139, 232-250); dims d..DP-1 add an exact +0.0.
+#ifndef PSG_BG_CAP
+#define PSG_BG_CAP 64
+#endif
+constexpr int kBgWarps = 4, kBgCap = PSG_BG_CAP;
+
+template <int DP, int G, int CAP>
+__global__ void __launch_bounds__(32 * kBgWarps) search_backtrack_group_kernel(SearchArgs a) {
+  constexpr int QPW = 32 / G, QPC = kBgWarps * QPW;
+  constexpr int QS = DP + 4;  // q rows 32 bytes apart modulo the banks: the groups' 16-byte reads spread
+  __shared__ __align__(16) double qs_all[QPC][QS];
+  __shared__ double pk_all[QPC][CAP];
+  __shared__ int32_t pt_all[QPC][CAP];
+  __shared__ int2 pm_all[QPC][CAP];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int l = lane % G, slot = warp * QPW + lane / G;
+  double* qs = qs_all[slot];
+  double* pk = pk_all[slot];
+  int32_t* pt = pt_all[slot];
+  int2* pm = pm_all[slot];
+  const int d = a.d, dE = (d + 1) & ~1;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  const int2 root = a.tree.meta[0];
+  const int32_t root_tie = a.tree.tie ? a.tree.tie[0] : 0;
+  const unsigned kFull = 0xffffffffu;
+  for (int64_t q0 = (int64_t)blockIdx.x * QPC; q0 < a.nq; q0 += (int64_t)gridDim.x * QPC) {
+    const int64_t q = q0 + slot;
+    const bool live = q < a.nq;
+    for (int j = l; j < DP; j += G) qs[j] = (live && j < d) ? a.q[q * d + j] : 0.0;
+    if (l == 0) {
+      pk[0] = 0.0;
+      pt[0] = root_tie;
+      pm[0] = root;
+    }
+    __syncwarp();
+    double best = kInf;
+    int32_t best_id = 0x7fffffff;
+    int32_t scanned = 0, visited = 0;
+    int size = live ? 1 : 0, leaves = 0;
+    bool overflow = false;
+    for (;;) {
+      const bool act = size > 0 && leaves < a.max_leaves && !overflow;
+      if (!__any_sync(kFull, act)) break;
+      // ---- pop the lexicographic minimum (key, tie) of the group's pool ----
+      double bk = kInf;
+      int32_t bt = 0x7fffffff, bs = 0;
+      const int n = act ? size : 0;
+      for (int s = l; s < n; s += G) {
+        const double k = pk[s];
+        const int32_t t = pt[s];
+        if (k < bk || (k == bk && t < bt)) {
+          bk = k;
+          bt = t;
+          bs = s;
+        }
+      }
+#pragma unroll
+      for (int off = G / 2; off > 0; off >>= 1) {
+        const double ok = __shfl_xor_sync(kFull, bk, off);
+        const int32_t ot = __shfl_xor_sync(kFull, bt, off);
+        const int32_t os = __shfl_xor_sync(kFull, bs, off);
+        if (ok < bk || (ok == bk && ot < bt)) {
+          bk = ok;
+          bt = ot;
+          bs = os;
+        }
+      }
+      const int2 e = pm[bs];
+      __syncwarp();
+      if (act) {
+        if (l == 0) {
+          pk[bs] = pk[size - 1];
+          pt[bs] = pt[size - 1];
+          pm[bs] = pm[size - 1];
+        }
+        --size;
+        ++visited;
+      }
+      __syncwarp();
+      // ---- the popped node's rows: leaf points or children's centroids ----
+      const bool leaf = e.y >= 0;
+      int cnt = act ? (leaf ? e.y : -e.y) : 0;
+      if (act && !leaf && size + cnt > CAP) {
+        overflow = true;  // re-run by the deep-stack kernel
+        cnt = 0;
+      }
+      const double* blk = (leaf ? a.proj_leaf_il : a.tree.centroid_il) + (int64_t)e.x * dE;
+      for (int base = 0; __any_sync(kFull, base < cnt); base += G) {
+        const int i = base + l;
+        const bool on = i < cnt;
+        double2 r[DP / 2];
+#pragma unroll
+        for (int jp = 0; jp < DP / 2; ++jp) {
+          r[jp] = make_double2(0.0, 0.0);
+          if (on && 2 * jp < dE)
+            r[jp] = __ldg(reinterpret_cast<const double2*>(blk + (int64_t)jp * 2 * cnt + 2 * i));
+        }
+        int2 cm = make_int2(0, 0);
+        int32_t ct = 0x7fffffff;
+        if (on) {
+          if (leaf) {
+            ct = __ldg(a.perm + e.x + i);
+          } else {
+            cm = __ldg(a.tree.meta + e.x + i);
+            ct = a.tree.tie ? __ldg(a.tree.tie + e.x + i) : e.x + i;
+          }
+        }
+        double acc = 0.0;
+#pragma unroll
+        for (int jp = 0; jp < DP / 2; ++jp) {
+          const double2 qq = *reinterpret_cast<const double2*>(qs + 2 * jp);
+          const double t0 = dsub(qq.x, r[jp].x);
+          acc = dadd(acc, dmul(t0, t0));
+          const double t1 = dsub(qq.y, r[jp].y);
+          acc = dadd(acc, dmul(t1, t1));
+        }
+        if (on && !leaf) {
+          pk[size + i] = acc;
+          pt[size + i] = ct;
+          pm[size + i] = cm;
+        }
+        // leaf rows: group-wide lexicographic (dist^2, id) minimum (inner-node
+        // groups and idle lanes carry +inf and change nothing)
+        double md = (on && leaf) ? acc : kInf;
+        int32_t mi = (on && leaf) ? ct : 0x7fffffff;
+#pragma unroll
+        for (int off = G / 2; off > 0; off >>= 1) {
+          const double od = __shfl_xor_sync(kFull, md, off);
+          const int32_t oi = __shfl_xor_sync(kFull, mi, off);
+          if (lex_less(od, oi, md, mi)) {
+            md = od;
+            mi = oi;
+          }
+        }
+        if (lex_less(md, mi, best, best_id)) {
+          best = md;
+          best_id = mi;
+        }
+      }
+      if (act && !overflow) {
+        if (leaf) {
+          scanned += cnt;
+          ++leaves;
+        } else {
+          size += cnt;
+        }
+      }
+      __syncwarp();
+    }
+    if (live && l == 0) {
+      if (overflow) {
+        a.ovf_list[atomicAdd(a.ovf_count, 1)] = (int32_t)q;
+      } else {
+        a.out_idx[q] = best_id;
+        a.out_d2[q] = best;
+        if (a.out_scanned) a.out_scanned[q] = scanned;
+        if (a.out_exact) a.out_exact[q] = scanned;
+        if (a.out_visited) a.out_visited[q] = visited;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Pair-interleaved copy of row blocks (see search_backtrack_group_kernel): one
+// warp per tree node; inner nodes interleave their children's centroid rows,
+// leaves their points' rows (leaf order).  `out` is zeroed by the caller (the
+// pad dim of an odd d).
+__global__ void interleave_blocks_kernel(const double* __restrict__ rows,
+                                         const int2* __restrict__ meta, int n_nodes, int d,
+                                         int want_leaves, double* __restrict__ out) {
+  const int dE = (d + 1) & ~1;
+  const int lane = threadIdx.x & 31;
+  for (int64_t node = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; node < n_nodes;
+       node += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int2 m = meta[node];
+    const bool leaf = m.y >= 0;
+    if (leaf != (want_leaves != 0)) continue;
+    const int cnt = leaf ? m.y : -m.y;
+    const int64_t s = m.x;
+    for (int f = lane; f < cnt * d; f += 32) {
+      const int i = f / d, j = f - i * d;
+      out[s * dE + (int64_t)(j >> 1) * 2 * cnt + 2 * i + (j & 1)] = rows[(s + i) * d + j];
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
 // Exact search (the bit-parity mode, km_tree.cpp:251-278 semantics: the
 // lexicographic minimum of (fp64 dist^2, id) over ALL database points).
 //
@@ -1934,13 +2143,34 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
       b.ovf_count = ovf_n.p;
     }
     PSG_CUDA(cudaMemsetAsync(b.ovf_count, 0, sizeof(int), ctx->stream));
-    int64_t blocks = (a.nq + kBtWarps - 1) / kBtWarps;
-    const int64_t cap = (int64_t)ctx->num_sms * 16;
-    if (blocks > cap) blocks = cap;
-    if (a.d <= 32)
-      search_backtrack_kernel<32><<<(int)blocks, 32 * kBtWarps, 0, ctx->stream>>>(b);
-    else
-      search_backtrack_kernel<64><<<(int)blocks, 32 * kBtWarps, 0, ctx->stream>>>(b);
+    const int mc = a.tree.max_children;
+    if (b.proj_leaf_il && a.tree.centroid_il && mc <= 16 && !ctx->knobs.bt_warp) {
+      // a group of 8 (16) lanes per query: 16 (8) queries per CTA
+      const int qpc = kBgWarps * (mc <= 8 ? 4 : 2);
+      int64_t blocks = (a.nq + qpc - 1) / qpc;
+      const int64_t cap = (int64_t)ctx->num_sms * 16;
+      if (blocks > cap) blocks = cap;
+      const dim3 blk(32 * kBgWarps);
+      if (mc <= 8) {
+        if (a.d <= 32)
+          search_backtrack_group_kernel<32, 8, kBgCap><<<(int)blocks, blk, 0, ctx->stream>>>(b);
+        else
+          search_backtrack_group_kernel<64, 8, kBgCap><<<(int)blocks, blk, 0, ctx->stream>>>(b);
+      } else {
+        if (a.d <= 32)
+          search_backtrack_group_kernel<32, 16, kBgCap><<<(int)blocks, blk, 0, ctx->stream>>>(b);
+        else
+          search_backtrack_group_kernel<64, 16, kBgCap><<<(int)blocks, blk, 0, ctx->stream>>>(b);
+      }
+    } else {
+      int64_t blocks = (a.nq + kBtWarps - 1) / kBtWarps;
+      const int64_t cap = (int64_t)ctx->num_sms * 16;
+      if (blocks > cap) blocks = cap;
+      if (a.d <= 32)
+        search_backtrack_kernel<32><<<(int)blocks, 32 * kBtWarps, 0, ctx->stream>>>(b);
+      else
+        search_backtrack_kernel<64><<<(int)blocks, 32 * kBtWarps, 0, ctx->stream>>>(b);
+    }
     PSG_LAUNCHED(ctx);
     search_kernel<<<ctx->num_sms, 32 * kSearchWarps, 0, ctx->stream>>>(b);
     PSG_LAUNCHED(ctx);
@@ -2085,6 +2315,18 @@ void launch_greedy_keys(psg_ctx* ctx, const double* q, int64_t nq, int d, const 
   int64_t blocks = (nq + 255) / 256;
   if (blocks > (int64_t)ctx->num_sms * 32) blocks = (int64_t)ctx->num_sms * 32;
   greedy_leaf_key_kernel<<<(int)blocks, 256, 0, ctx->stream>>>(q, nq, d, tree, keys, order);
+  PSG_LAUNCHED(ctx);
+}
+
+void launch_interleave_blocks(psg_ctx* ctx, const double* rows, const int2* meta, int n_nodes,
+                              int d, bool leaves, int64_t n_rows, double* out) {
+  const int dE = (d + 1) & ~1;
+  PSG_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * (size_t)n_rows * dE, ctx->stream));
+  int64_t blocks = ((int64_t)n_nodes * 32 + 255) / 256;
+  if (blocks > (int64_t)ctx->num_sms * 32) blocks = (int64_t)ctx->num_sms * 32;
+  if (blocks < 1) blocks = 1;
+  interleave_blocks_kernel<<<(int)blocks, 256, 0, ctx->stream>>>(rows, meta, n_nodes, d,
+                                                                 leaves ? 1 : 0, out);
   PSG_LAUNCHED(ctx);
 }
 

@@ -63,6 +63,8 @@ struct DevTree {
   float* box2 = nullptr;        // [n_nodes][kBoxDims][2]: (lo_j, -hi_j) per node, 64 contiguous bytes
   int2* meta = nullptr;         // {first_child, -n_children} or {leaf_start, leaf_count}
   int32_t* tie = nullptr;       // optional backtrack tie-break id per node (null = node index)
+  // fp64 centroid rows, pair-interleaved per sibling block (search_backtrack_group_kernel)
+  double* centroid_il = nullptr;
 };
 #ifndef PSG_BOX_DIMS
 #define PSG_BOX_DIMS 8
@@ -94,6 +96,7 @@ struct Index {
   double* proj = nullptr;      // [N][d] original order
   double* proj_soa = nullptr;  // [d][N] leaf order
   double* proj_leaf = nullptr; // [N][d] leaf order (budget searches: a leaf's rows are contiguous)
+  double* proj_leaf_il = nullptr;  // the same rows pair-interleaved per leaf (search_backtrack_group_kernel)
   float* proj32_q4 = nullptr;  // [dp/4][N] float4 groups, leaf order, fp32 filter copy
   int dp = 32;
   float* pnorm32 = nullptr;    // [N] leaf order, |p| rounded up
@@ -197,6 +200,7 @@ struct psg_ctx {
     bool no_carry = false;            // PERSYN_NO_CARRY: stages do not seed from the previous
     bool eig_direct = false;          // PERSYN_EIG: dense eigensolver instead of subspace iteration
     bool exact_projection = false;    // PERSYN_EXACT_PROJECTION: fp64 SIMT projection of every query
+    bool bt_warp = false;             // PERSYN_BT_WARP: backtrack(m > 2) warp per query (not lane groups)
   } knobs;
 };
 
@@ -361,6 +365,7 @@ struct SearchArgs {
   const double* proj;       // [N][d] original order (seed distances)
   const double* proj_soa;   // [d][N] leaf order
   const double* proj_leaf = nullptr;  // [N][d] leaf order
+  const double* proj_leaf_il = nullptr;  // pair-interleaved per leaf (lane-group backtrack)
   const float* proj32_q4;   // [dp/4][N] float4 groups, leaf order (fp32 filter)
   const float* pnorm32;     // [N] leaf order
   const float2* pp32 = nullptr;  // [N] leaf order (|p~|^2, |p~_B|^2) (expanded-form filter)
@@ -420,6 +425,8 @@ void launch_greedy_keys(psg_ctx* ctx, const double* q, int64_t nq, int d, const 
 size_t sort_pairs_temp_bytes(int64_t n);
 void sort_pairs_u32(psg_ctx* ctx, const uint32_t* kin, uint32_t* kout, const int32_t* vin,
                     int32_t* vout, int64_t n, void* temp, size_t temp_bytes);
+void launch_interleave_blocks(psg_ctx* ctx, const double* rows, const int2* meta, int n_nodes,
+                              int d, bool leaves, int64_t n_rows, double* out);
 void launch_gather_rows_f64(psg_ctx* ctx, const double* src, const int32_t* order, int64_t n,
                             int width, double* dst);
 void launch_scatter_i32(psg_ctx* ctx, const int32_t* src, const int32_t* order, int64_t n,

@@ -172,7 +172,7 @@ double pow_cr_host(double x, double y) { return pow_cr(x, y); }
 Index::~Index() {
   // stream-ordered frees (the allocations come from the context's pool)
   cudaStream_t st = ctx ? ctx->stream : nullptr;
-  for (void* p : {(void*)ex_mirror, (void*)ex_mirror8, (void*)vectors, (void*)mean, (void*)basis, (void*)proj, (void*)proj_soa, (void*)perm, (void*)tree.centroid, (void*)tree.radius, (void*)tree.first_child, (void*)tree.n_children, (void*)tree.leaf_start, (void*)tree.leaf_count, (void*)tree.centroid32, (void*)tree.radius32, (void*)tree.cnorm32, (void*)proj32_q4, (void*)tree.centroid32T, (void*)tree.boxlo, (void*)tree.boxhi, (void*)tree.box2, (void*)tree.meta, (void*)tree.tie, (void*)pnorm32, (void*)ex_hist, (void*)brute_op, (void*)brute_n2, (void*)brute_nup, (void*)brute_mu, (void*)brute_tmax, (void*)tc_b, (void*)tc_bmu, (void*)pp32, (void*)proj_leaf})
+  for (void* p : {(void*)ex_mirror, (void*)ex_mirror8, (void*)vectors, (void*)mean, (void*)basis, (void*)proj, (void*)proj_soa, (void*)perm, (void*)tree.centroid, (void*)tree.radius, (void*)tree.first_child, (void*)tree.n_children, (void*)tree.leaf_start, (void*)tree.leaf_count, (void*)tree.centroid32, (void*)tree.radius32, (void*)tree.cnorm32, (void*)proj32_q4, (void*)tree.centroid32T, (void*)tree.boxlo, (void*)tree.boxhi, (void*)tree.box2, (void*)tree.meta, (void*)tree.tie, (void*)pnorm32, (void*)ex_hist, (void*)brute_op, (void*)brute_n2, (void*)brute_nup, (void*)brute_mu, (void*)brute_tmax, (void*)tc_b, (void*)tc_bmu, (void*)pp32, (void*)proj_leaf, (void*)proj_leaf_il, (void*)tree.centroid_il})
     if (p) cudaFreeAsync(p, st);
 }
 
@@ -191,7 +191,8 @@ void free_tree(Index& ix) {
                   (void*)T.leaf_start, (void*)T.leaf_count, (void*)T.centroid32,
                   (void*)T.centroid32T, (void*)T.radius32, (void*)T.cnorm32, (void*)T.boxlo,
                   (void*)T.boxhi, (void*)T.box2, (void*)T.meta, (void*)T.tie, (void*)ix.perm, (void*)ix.proj_soa,
-                  (void*)ix.proj32_q4, (void*)ix.pnorm32, (void*)ix.pp32, (void*)ix.proj_leaf})
+                  (void*)ix.proj32_q4, (void*)ix.pnorm32, (void*)ix.pp32, (void*)ix.proj_leaf,
+                  (void*)ix.proj_leaf_il, (void*)T.centroid_il})
     if (p) cudaFreeAsync(p, ctx_stream);
   T = DevTree{};
   ix.perm = nullptr;
@@ -200,6 +201,7 @@ void free_tree(Index& ix) {
   ix.pnorm32 = nullptr;
   ix.pp32 = nullptr;
   ix.proj_leaf = nullptr;
+  ix.proj_leaf_il = nullptr;
 }
 
 void upload_tree(psg_ctx* ctx, Index& ix) {
@@ -298,6 +300,15 @@ void upload_tree(psg_ctx* ctx, Index& ix) {
   if (!t.tie.empty()) {
     ix.tree.tie = dalloc<int32_t>(nn);
     up(ix.tree.tie, t.tie);
+  }
+  // pair-interleaved row blocks of the lane-group backtrack kernel
+  if (d > 0 && ix.tree.max_children <= 16) {
+    const int dE = (d + 1) & ~1;
+    ix.tree.centroid_il = dalloc<double>((size_t)nn * dE);
+    launch_interleave_blocks(ctx, ix.tree.centroid, ix.tree.meta, nn, d, false, nn,
+                             ix.tree.centroid_il);
+    ix.proj_leaf_il = dalloc<double>((size_t)ix.N * dE);
+    launch_interleave_blocks(ctx, ix.proj_leaf, ix.tree.meta, nn, d, true, ix.N, ix.proj_leaf_il);
   }
   PSG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
@@ -719,6 +730,7 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
   a.proj = ix.proj;
   a.proj_soa = ix.proj_soa;
   a.proj_leaf = ix.proj_leaf;
+  a.proj_leaf_il = ix.proj_leaf_il;
   a.proj32_q4 = ix.proj32_q4;
   a.pnorm32 = ix.pnorm32;
   a.pp32 = ix.pp32;
@@ -1239,6 +1251,7 @@ psg_status psg_ctx_create(int device, void* stream, psg_ctx** out) {
       kn.no_carry = on("PERSYN_NO_CARRY");
       kn.eig_direct = on("PERSYN_EIG");
       kn.exact_projection = on("PERSYN_EXACT_PROJECTION");
+      kn.bt_warp = on("PERSYN_BT_WARP");
     }
     if (stream) {
       c->stream = static_cast<cudaStream_t>(stream);
@@ -1503,6 +1516,7 @@ psg_status psg_index_query(psg_ctx* ctx, const psg_index* index, const float* Q,
     a.proj = ix.proj;
     a.proj_soa = ix.proj_soa;
     a.proj_leaf = ix.proj_leaf;
+    a.proj_leaf_il = ix.proj_leaf_il;
     a.proj32_q4 = ix.proj32_q4;
     a.pnorm32 = ix.pnorm32;
     a.pp32 = ix.pp32;
