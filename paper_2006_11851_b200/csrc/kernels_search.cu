@@ -1078,10 +1078,11 @@ __global__ void __launch_bounds__(32 * kBtWarps) search_backtrack_kernel(SearchA
 //  * rows come straight from global memory into registers: the children of a
 //    node (contiguous in the breadth-first layout) and the points of a leaf
 //    are stored PAIR-INTERLEAVED per block -- element (row i, dim j) of a
-//    block of n rows starting at row s sits at s*dE + (j/2)*(2n) + 2i + (j&1)
-//    (dE = d rounded up to even) -- so the G lanes' 16-byte loads of one dim
-//    pair are one contiguous segment: no shared-memory staging, no barrier
-//    between the loads and the chains;
+//    block of n rows starting at row s sits at s*DP + (j/2)*(2n) + 2i + (j&1)
+//    (DP = the fp32 layouts' width class of d, pad dims zero) -- so the G
+//    lanes' 16-byte loads of one dim pair are one contiguous segment: no
+//    shared-memory staging, no barrier between the loads and the chains, and
+//    the loads are unpredicated (idle lanes re-read a valid row);
 //  * the frontier is the same unsorted pool of (key, tie id, node meta) in
 //    shared memory, CAP entries per query; a pop is a group-wide lexicographic
 //    min; a query whose frontier would outgrow the pool is listed and re-run
@@ -1093,12 +1094,16 @@ __global__ void __launch_bounds__(32 * kBtWarps) search_backtrack_kernel(SearchA
 // Keys and leaf distances are the reference's fp64 j-ascending chains
 // (km_tree.cpp:15-22, 128-139, 232-250); dims d..DP-1 add an exact +0.0.
 #ifndef PSG_BG_CAP
-#define PSG_BG_CAP 64
+#define PSG_BG_CAP 96
+#endif
+#ifndef PSG_BG_MINB
+#define PSG_BG_MINB 4
 #endif
 constexpr int kBgWarps = 4, kBgCap = PSG_BG_CAP;
 
 template <int DP, int G, int CAP>
-__global__ void __launch_bounds__(32 * kBgWarps) search_backtrack_group_kernel(SearchArgs a) {
+__global__ void __launch_bounds__(32 * kBgWarps, (DP <= 32 ? PSG_BG_MINB : 2))
+search_backtrack_group_kernel(SearchArgs a) {
   constexpr int QPW = 32 / G, QPC = kBgWarps * QPW;
   constexpr int QS = DP + 4;  // q rows 32 bytes apart modulo the banks: the groups' 16-byte reads spread
   __shared__ __align__(16) double qs_all[QPC][QS];
@@ -1111,7 +1116,7 @@ __global__ void __launch_bounds__(32 * kBgWarps) search_backtrack_group_kernel(S
   double* pk = pk_all[slot];
   int32_t* pt = pt_all[slot];
   int2* pm = pm_all[slot];
-  const int d = a.d, dE = (d + 1) & ~1;
+  const int d = a.d;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
   const int2 root = a.tree.meta[0];
   const int32_t root_tie = a.tree.tie ? a.tree.tie[0] : 0;
@@ -1177,16 +1182,18 @@ __global__ void __launch_bounds__(32 * kBgWarps) search_backtrack_group_kernel(S
         overflow = true;  // re-run by the deep-stack kernel
         cnt = 0;
       }
-      const double* blk = (leaf ? a.proj_leaf_il : a.tree.centroid_il) + (int64_t)e.x * dE;
+      // idle groups / lanes read row 0 of a one-row block (always valid)
+      const int cl = cnt > 0 ? cnt : 1;
+      const double* blk = cnt > 0 ? (leaf ? a.proj_leaf_il : a.tree.centroid_il) + (int64_t)e.x * DP
+                                  : a.tree.centroid_il;
       for (int base = 0; __any_sync(kFull, base < cnt); base += G) {
         const int i = base + l;
         const bool on = i < cnt;
         double2 r[DP / 2];
+        {
+          const double2* p = reinterpret_cast<const double2*>(blk) + (on ? i : 0);
 #pragma unroll
-        for (int jp = 0; jp < DP / 2; ++jp) {
-          r[jp] = make_double2(0.0, 0.0);
-          if (on && 2 * jp < dE)
-            r[jp] = __ldg(reinterpret_cast<const double2*>(blk + (int64_t)jp * 2 * cnt + 2 * i));
+          for (int jp = 0; jp < DP / 2; ++jp) r[jp] = __ldg(p + (int64_t)jp * cl);
         }
         int2 cm = make_int2(0, 0);
         int32_t ct = 0x7fffffff;
@@ -1214,20 +1221,22 @@ __global__ void __launch_bounds__(32 * kBgWarps) search_backtrack_group_kernel(S
         }
         // leaf rows: group-wide lexicographic (dist^2, id) minimum (inner-node
         // groups and idle lanes carry +inf and change nothing)
-        double md = (on && leaf) ? acc : kInf;
-        int32_t mi = (on && leaf) ? ct : 0x7fffffff;
+        if (__any_sync(kFull, on && leaf)) {
+          double md = (on && leaf) ? acc : kInf;
+          int32_t mi = (on && leaf) ? ct : 0x7fffffff;
 #pragma unroll
-        for (int off = G / 2; off > 0; off >>= 1) {
-          const double od = __shfl_xor_sync(kFull, md, off);
-          const int32_t oi = __shfl_xor_sync(kFull, mi, off);
-          if (lex_less(od, oi, md, mi)) {
-            md = od;
-            mi = oi;
+          for (int off = G / 2; off > 0; off >>= 1) {
+            const double od = __shfl_xor_sync(kFull, md, off);
+            const int32_t oi = __shfl_xor_sync(kFull, mi, off);
+            if (lex_less(od, oi, md, mi)) {
+              md = od;
+              mi = oi;
+            }
           }
-        }
-        if (lex_less(md, mi, best, best_id)) {
-          best = md;
-          best_id = mi;
+          if (lex_less(md, mi, best, best_id)) {
+            best = md;
+            best_id = mi;
+          }
         }
       }
       if (act && !overflow) {
@@ -1257,12 +1266,11 @@ __global__ void __launch_bounds__(32 * kBgWarps) search_backtrack_group_kernel(S
 
 // Pair-interleaved copy of row blocks (see search_backtrack_group_kernel): one
 // warp per tree node; inner nodes interleave their children's centroid rows,
-// leaves their points' rows (leaf order).  `out` is zeroed by the caller (the
-// pad dim of an odd d).
+// leaves their points' rows (leaf order); dE = the padded block width.  `out`
+// is zeroed by the caller (the pad dims).
 __global__ void interleave_blocks_kernel(const double* __restrict__ rows,
                                          const int2* __restrict__ meta, int n_nodes, int d,
-                                         int want_leaves, double* __restrict__ out) {
-  const int dE = (d + 1) & ~1;
+                                         int dE, int want_leaves, double* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   for (int64_t node = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; node < n_nodes;
        node += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -2144,24 +2152,26 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
     }
     PSG_CUDA(cudaMemsetAsync(b.ovf_count, 0, sizeof(int), ctx->stream));
     const int mc = a.tree.max_children;
-    if (b.proj_leaf_il && a.tree.centroid_il && mc <= 16 && !ctx->knobs.bt_warp) {
+    if (b.proj_leaf_il && a.tree.centroid_il && mc <= 16 && a.d <= 64 && !ctx->knobs.bt_warp) {
       // a group of 8 (16) lanes per query: 16 (8) queries per CTA
       const int qpc = kBgWarps * (mc <= 8 ? 4 : 2);
       int64_t blocks = (a.nq + qpc - 1) / qpc;
       const int64_t cap = (int64_t)ctx->num_sms * 16;
       if (blocks > cap) blocks = cap;
       const dim3 blk(32 * kBgWarps);
-      if (mc <= 8) {
-        if (a.d <= 32)
-          search_backtrack_group_kernel<32, 8, kBgCap><<<(int)blocks, blk, 0, ctx->stream>>>(b);
-        else
-          search_backtrack_group_kernel<64, 8, kBgCap><<<(int)blocks, blk, 0, ctx->stream>>>(b);
-      } else {
-        if (a.d <= 32)
-          search_backtrack_group_kernel<32, 16, kBgCap><<<(int)blocks, blk, 0, ctx->stream>>>(b);
-        else
-          search_backtrack_group_kernel<64, 16, kBgCap><<<(int)blocks, blk, 0, ctx->stream>>>(b);
-      }
+#define PSG_BG_LAUNCH(DPV)                                                                      \
+  do {                                                                                          \
+    if (mc <= 8)                                                                                \
+      search_backtrack_group_kernel<DPV, 8, kBgCap><<<(int)blocks, blk, 0, ctx->stream>>>(b);   \
+    else                                                                                        \
+      search_backtrack_group_kernel<DPV, 16, kBgCap><<<(int)blocks, blk, 0, ctx->stream>>>(b);  \
+  } while (0)
+      // the blocks' width = the index's fp32 layout class (upload_tree)
+      if (a.d <= 24) PSG_BG_LAUNCH(24);
+      else if (a.d <= 32) PSG_BG_LAUNCH(32);
+      else if (a.d <= 48) PSG_BG_LAUNCH(48);
+      else PSG_BG_LAUNCH(64);
+#undef PSG_BG_LAUNCH
     } else {
       int64_t blocks = (a.nq + kBtWarps - 1) / kBtWarps;
       const int64_t cap = (int64_t)ctx->num_sms * 16;
@@ -2319,13 +2329,12 @@ void launch_greedy_keys(psg_ctx* ctx, const double* q, int64_t nq, int d, const 
 }
 
 void launch_interleave_blocks(psg_ctx* ctx, const double* rows, const int2* meta, int n_nodes,
-                              int d, bool leaves, int64_t n_rows, double* out) {
-  const int dE = (d + 1) & ~1;
+                              int d, int dE, bool leaves, int64_t n_rows, double* out) {
   PSG_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * (size_t)n_rows * dE, ctx->stream));
   int64_t blocks = ((int64_t)n_nodes * 32 + 255) / 256;
   if (blocks > (int64_t)ctx->num_sms * 32) blocks = (int64_t)ctx->num_sms * 32;
   if (blocks < 1) blocks = 1;
-  interleave_blocks_kernel<<<(int)blocks, 256, 0, ctx->stream>>>(rows, meta, n_nodes, d,
+  interleave_blocks_kernel<<<(int)blocks, 256, 0, ctx->stream>>>(rows, meta, n_nodes, d, dE,
                                                                  leaves ? 1 : 0, out);
   PSG_LAUNCHED(ctx);
 }

@@ -426,7 +426,7 @@ size_t sort_pairs_temp_bytes(int64_t n);
 void sort_pairs_u32(psg_ctx* ctx, const uint32_t* kin, uint32_t* kout, const int32_t* vin,
                     int32_t* vout, int64_t n, void* temp, size_t temp_bytes);
 void launch_interleave_blocks(psg_ctx* ctx, const double* rows, const int2* meta, int n_nodes,
-                              int d, bool leaves, int64_t n_rows, double* out);
+                              int d, int dE, bool leaves, int64_t n_rows, double* out);
 void launch_gather_rows_f64(psg_ctx* ctx, const double* src, const int32_t* order, int64_t n,
                             int width, double* dst);
 void launch_scatter_i32(psg_ctx* ctx, const int32_t* src, const int32_t* order, int64_t n,

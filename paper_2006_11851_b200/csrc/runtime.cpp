@@ -302,13 +302,14 @@ void upload_tree(psg_ctx* ctx, Index& ix) {
     up(ix.tree.tie, t.tie);
   }
   // pair-interleaved row blocks of the lane-group backtrack kernel
-  if (d > 0 && ix.tree.max_children <= 16) {
-    const int dE = (d + 1) & ~1;
+  if (d > 0 && d <= 64 && ix.tree.max_children <= 16) {
+    const int dE = ix.dp;  // blocks padded to the fp32 layouts' width class
     ix.tree.centroid_il = dalloc<double>((size_t)nn * dE);
-    launch_interleave_blocks(ctx, ix.tree.centroid, ix.tree.meta, nn, d, false, nn,
+    launch_interleave_blocks(ctx, ix.tree.centroid, ix.tree.meta, nn, d, dE, false, nn,
                              ix.tree.centroid_il);
     ix.proj_leaf_il = dalloc<double>((size_t)ix.N * dE);
-    launch_interleave_blocks(ctx, ix.proj_leaf, ix.tree.meta, nn, d, true, ix.N, ix.proj_leaf_il);
+    launch_interleave_blocks(ctx, ix.proj_leaf, ix.tree.meta, nn, d, dE, true, ix.N,
+                             ix.proj_leaf_il);
   }
   PSG_CUDA(cudaStreamSynchronize(ctx->stream));
 }

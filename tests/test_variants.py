@@ -71,6 +71,29 @@ def test_budget_kernels_agree(gpu_ctx, port, monkeypatch, m):
     assert res[0][3] == res[1][3]  # points scanned
 
 
+@pytest.mark.parametrize("d,b,m,depth", [(12, 4, 4, 2), (32, 8, 4, 4), (40, 8, 16, 4),
+                                         (56, 16, 6, 3), (32, 8, 40, 4), (24, 2, 30, 9)])
+def test_backtrack_lane_group_kernel_equals_warp_kernel(gpu_ctx, port, monkeypatch, d, b, m,
+                                                        depth):
+    """backtrack(m > 2): the lane-group kernel (8 / 16 lanes per query, rows from
+    the pair-interleaved blocks; every width class, leaves larger than a group,
+    frontiers that outgrow the pool and are re-run) and the warp-per-query
+    kernel (PERSYN_BT_WARP) return identical answers and scan counts."""
+    ex, init = _stage()
+    cand = port.extract_all(ex, 8, 1)
+    mean, basis, _ = fit_pca(cand, d_fixed=d)
+    monkeypatch.setenv("PERSYN_BT_WARP", "1")
+    warp_ctx = api.Context(0)
+    monkeypatch.delenv("PERSYN_BT_WARP", raising=False)
+    res = []
+    for ctx in (gpu_ctx, warp_ctx):
+        ix = api.make_pca_tree_index(ex, 8, mean=mean, basis=basis, branching=b,
+                                     max_depth=depth, seed=3, ctx=ctx)
+        res.append(api.search_step(init, ix, 2, 2, api.QueryBudget.backtrack(m)))
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    assert res[0][3] == res[1][3]  # points scanned
+
+
 def test_eigensolver_paths_agree(gpu_ctx, monkeypatch):
     """Top-d PCA pairs by subspace iteration vs the direct DSYEVDX solver."""
     ex, _ = _stage(size=48, G=2)
