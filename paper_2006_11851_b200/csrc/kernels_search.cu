@@ -902,9 +902,11 @@ __global__ void __launch_bounds__(32 * kSearchWarps) search_kernel(SearchArgs a)
       }
     }
     if (lane == 0) {
-      a.out_idx[q] = best_id;
-      a.out_d2[q] = best;
-      if (a.out_scanned) a.out_scanned[q] = scanned;
+      // a listed query of a mapped re-run: results go to its output slot
+      const int64_t o = (a.ovf_list && a.out_map) ? (int64_t)a.out_map[q] : q;
+      a.out_idx[o] = best_id;
+      if (a.out_d2) a.out_d2[o] = best;
+      if (a.out_scanned) a.out_scanned[o] = scanned;
     }
     __syncwarp();
   }
@@ -1101,7 +1103,19 @@ __global__ void __launch_bounds__(32 * kBtWarps) search_backtrack_kernel(SearchA
 #endif
 constexpr int kBgWarps = 4, kBgCap = PSG_BG_CAP;
 
-template <int DP, int G, int CAP>
+//
+// Approximate queries (AP, tensor-core projection): a.q holds q^ with
+// |q^ - q|_2 <= delta = a.qdelta[query] (q = the reference's fp64 projection).
+// For any row p, |sqrt(D^(p)) - sqrt(D(p))| <= delta (D = real dist^2), and a
+// chain's rounding is <= (d + 3) 2^-53 relative.  A decision "key a is the
+// strict minimum" made on the q^ keys is the reference's decision whenever
+// every other key exceeds T(a) = (sqrt(K^_a) + 2 delta)^2 inflated by 1e-11
+// (which dominates both chains' rounding): the kernel tracks the second
+// smallest key of every pop and of all scanned points, and a query with any
+// decision inside its band (or whose frontier outgrows the pool) is listed in
+// a.amb_list and re-run with its exact projection (AP = false, device-counted
+// list, results written through a.out_map).
+template <int DP, int G, int CAP, bool AP>
 __global__ void __launch_bounds__(32 * kBgWarps, (DP <= 32 ? PSG_BG_MINB : 2))
 search_backtrack_group_kernel(SearchArgs a) {
   constexpr int QPW = 32 / G, QPC = kBgWarps * QPW;
@@ -1121,9 +1135,15 @@ search_backtrack_group_kernel(SearchArgs a) {
   const int2 root = a.tree.meta[0];
   const int32_t root_tie = a.tree.tie ? a.tree.tie[0] : 0;
   const unsigned kFull = 0xffffffffu;
-  for (int64_t q0 = (int64_t)blockIdx.x * QPC; q0 < a.nq; q0 += (int64_t)gridDim.x * QPC) {
+  const int64_t nq = a.nq_dev ? (int64_t)*a.nq_dev : a.nq;
+  // smallest key another entry must exceed for `k` to be the robust minimum
+  auto band_top = [](double k, double dl2) {
+    const double s = (double)__fsqrt_ru(__double2float_ru(k));
+    return (k + dl2 * (2.0 * s + dl2)) * (1.0 + 1e-11);
+  };
+  for (int64_t q0 = (int64_t)blockIdx.x * QPC; q0 < nq; q0 += (int64_t)gridDim.x * QPC) {
     const int64_t q = q0 + slot;
-    const bool live = q < a.nq;
+    const bool live = q < nq;
     for (int j = l; j < DP; j += G) qs[j] = (live && j < d) ? a.q[q * d + j] : 0.0;
     if (l == 0) {
       pk[0] = 0.0;
@@ -1131,25 +1151,34 @@ search_backtrack_group_kernel(SearchArgs a) {
       pm[0] = root;
     }
     __syncwarp();
-    double best = kInf;
+    double best = kInf, second = kInf;
     int32_t best_id = 0x7fffffff;
     int32_t scanned = 0, visited = 0;
     int size = live ? 1 : 0, leaves = 0;
-    bool overflow = false;
+    bool overflow = false;  // AP: also "a decision fell inside the band"
+    double dl2 = 0.0;       // 2 delta (slightly inflated)
+    if (AP && live) {
+      const float dl = a.qdelta[q];
+      if (!(dl < 3.0e38f)) overflow = true;  // no bound for this query: exact re-run
+      dl2 = 2.0 * (double)dl * (1.0 + 1e-6);
+    }
     for (;;) {
       const bool act = size > 0 && leaves < a.max_leaves && !overflow;
       if (!__any_sync(kFull, act)) break;
       // ---- pop the lexicographic minimum (key, tie) of the group's pool ----
-      double bk = kInf;
+      double bk = kInf, k2 = kInf;
       int32_t bt = 0x7fffffff, bs = 0;
       const int n = act ? size : 0;
       for (int s = l; s < n; s += G) {
         const double k = pk[s];
         const int32_t t = pt[s];
         if (k < bk || (k == bk && t < bt)) {
+          if (AP) k2 = bk;
           bk = k;
           bt = t;
           bs = s;
+        } else if (AP) {
+          k2 = fmin(k2, k);
         }
       }
 #pragma unroll
@@ -1157,6 +1186,10 @@ search_backtrack_group_kernel(SearchArgs a) {
         const double ok = __shfl_xor_sync(kFull, bk, off);
         const int32_t ot = __shfl_xor_sync(kFull, bt, off);
         const int32_t os = __shfl_xor_sync(kFull, bs, off);
+        if (AP) {
+          const double o2 = __shfl_xor_sync(kFull, k2, off);
+          k2 = fmin(fmin(k2, o2), fmax(bk, ok));
+        }
         if (ok < bk || (ok == bk && ot < bt)) {
           bk = ok;
           bt = ot;
@@ -1180,6 +1213,10 @@ search_backtrack_group_kernel(SearchArgs a) {
       int cnt = act ? (leaf ? e.y : -e.y) : 0;
       if (act && !leaf && size + cnt > CAP) {
         overflow = true;  // re-run by the deep-stack kernel
+        cnt = 0;
+      }
+      if (AP && act && !(k2 > band_top(bk, dl2))) {
+        overflow = true;  // the pop order is not certain: exact re-run
         cnt = 0;
       }
       // idle groups / lanes read row 0 of a one-row block (always valid)
@@ -1222,17 +1259,22 @@ search_backtrack_group_kernel(SearchArgs a) {
         // leaf rows: group-wide lexicographic (dist^2, id) minimum (inner-node
         // groups and idle lanes carry +inf and change nothing)
         if (__any_sync(kFull, on && leaf)) {
-          double md = (on && leaf) ? acc : kInf;
+          double md = (on && leaf) ? acc : kInf, m2 = kInf;
           int32_t mi = (on && leaf) ? ct : 0x7fffffff;
 #pragma unroll
           for (int off = G / 2; off > 0; off >>= 1) {
             const double od = __shfl_xor_sync(kFull, md, off);
             const int32_t oi = __shfl_xor_sync(kFull, mi, off);
+            if (AP) {
+              const double o2 = __shfl_xor_sync(kFull, m2, off);
+              m2 = fmin(fmin(m2, o2), fmax(md, od));
+            }
             if (lex_less(od, oi, md, mi)) {
               md = od;
               mi = oi;
             }
           }
+          if (AP) second = fmin(fmin(second, m2), fmax(best, md));
           if (lex_less(md, mi, best, best_id)) {
             best = md;
             best_id = mi;
@@ -1249,15 +1291,24 @@ search_backtrack_group_kernel(SearchArgs a) {
       }
       __syncwarp();
     }
+    if (AP && live && !overflow && !(second > band_top(best, dl2))) overflow = true;
     if (live && l == 0) {
       if (overflow) {
-        a.ovf_list[atomicAdd(a.ovf_count, 1)] = (int32_t)q;
+        if (AP) {
+          const int s = atomicAdd(a.amb_count, 1);
+          a.amb_list[s] = (int32_t)q;
+          a.amb_c0[s] = 0;
+          a.amb_c1[s] = -1;  // resolve: exact projection only, then the re-run
+        } else {
+          a.ovf_list[atomicAdd(a.ovf_count, 1)] = (int32_t)q;
+        }
       } else {
-        a.out_idx[q] = best_id;
-        a.out_d2[q] = best;
-        if (a.out_scanned) a.out_scanned[q] = scanned;
-        if (a.out_exact) a.out_exact[q] = scanned;
-        if (a.out_visited) a.out_visited[q] = visited;
+        const int64_t o = a.out_map ? (int64_t)a.out_map[q] : q;
+        a.out_idx[o] = best_id;
+        if (a.out_d2) a.out_d2[o] = best;
+        if (a.out_scanned) a.out_scanned[o] = scanned;
+        if (a.out_exact) a.out_exact[o] = scanned;
+        if (a.out_visited) a.out_visited[o] = visited;
       }
     }
     __syncwarp();
@@ -2058,6 +2109,79 @@ bool search_uses_tiles(psg_ctx* ctx, const DevTree& tree, int d, bool exact, int
          (nq < 0 || enough_tiles(ctx, nq));
 }
 
+bool search_uses_groups(psg_ctx* ctx, const Index& ix, const psg_budget& budget) {
+  return budget.mode == PSG_BACKTRACK && budget.max_leaves > 2 && ix.d > 0 && ix.d <= 64 &&
+         ix.proj_leaf_il && ix.tree.centroid_il && ix.tree.max_children <= 16 &&
+         !ctx->knobs.legacy_search && !ctx->knobs.bt_warp;
+}
+
+// backtrack(m > 2), d <= 64: the lane-group kernel (or the warp-per-query
+// kernel for wide trees / PERSYN_BT_WARP), then the deep-stack kernel for the
+// queries whose frontier outgrew the pool.  a.qdelta set: approximate queries
+// (see search_backtrack_group_kernel; uncertain queries go to a.amb_list and
+// nothing overflows).  a.nq_dev set: a device-counted list of exact queries
+// whose results go through a.out_map.
+static void launch_backtrack(psg_ctx* ctx, const SearchArgs& a) {
+  DBuf<int32_t> ovf;
+  DBuf<int> ovf_n;
+  SearchArgs b = a;
+  // (the caller may provide the list buffers: levels allocate them once,
+  // outside any captured iteration)
+  if (!b.ovf_list || !b.ovf_count) {
+    ovf.alloc((size_t)a.nq);
+    ovf_n.alloc(1);
+    b.ovf_list = ovf.p;
+    b.ovf_count = ovf_n.p;
+  }
+  PSG_CUDA(cudaMemsetAsync(b.ovf_count, 0, sizeof(int), ctx->stream));
+  const int mc = a.tree.max_children;
+  const bool groups = b.proj_leaf_il && a.tree.centroid_il && mc <= 16 && !ctx->knobs.bt_warp;
+  if (!groups && (a.qdelta || a.nq_dev || a.out_map))
+    fail(PSG_E_LOGIC, "approximate / listed backtrack queries need the lane-group kernel");
+  if (groups) {
+    // a group of 8 (16) lanes per query: 16 (8) queries per CTA
+    const int qpc = kBgWarps * (mc <= 8 ? 4 : 2);
+    int64_t blocks = (a.nq + qpc - 1) / qpc;
+    const int64_t cap = a.nq_dev ? (int64_t)ctx->num_sms : (int64_t)ctx->num_sms * 16;
+    if (blocks > cap) blocks = cap;
+    const dim3 blk(32 * kBgWarps);
+#define PSG_BG_LAUNCH2(DPV, GV)                                                                  \
+  do {                                                                                           \
+    if (a.qdelta)                                                                                \
+      search_backtrack_group_kernel<DPV, GV, kBgCap, true>                                       \
+          <<<(int)blocks, blk, 0, ctx->stream>>>(b);                                             \
+    else                                                                                         \
+      search_backtrack_group_kernel<DPV, GV, kBgCap, false>                                      \
+          <<<(int)blocks, blk, 0, ctx->stream>>>(b);                                             \
+  } while (0)
+#define PSG_BG_LAUNCH(DPV)                \
+  do {                                    \
+    if (mc <= 8) PSG_BG_LAUNCH2(DPV, 8);  \
+    else PSG_BG_LAUNCH2(DPV, 16);         \
+  } while (0)
+    // the blocks' width = the index's fp32 layout class (upload_tree)
+    if (a.d <= 24) PSG_BG_LAUNCH(24);
+    else if (a.d <= 32) PSG_BG_LAUNCH(32);
+    else if (a.d <= 48) PSG_BG_LAUNCH(48);
+    else PSG_BG_LAUNCH(64);
+#undef PSG_BG_LAUNCH
+#undef PSG_BG_LAUNCH2
+  } else {
+    int64_t blocks = (a.nq + kBtWarps - 1) / kBtWarps;
+    const int64_t cap = (int64_t)ctx->num_sms * 16;
+    if (blocks > cap) blocks = cap;
+    if (a.d <= 32)
+      search_backtrack_kernel<32><<<(int)blocks, 32 * kBtWarps, 0, ctx->stream>>>(b);
+    else
+      search_backtrack_kernel<64><<<(int)blocks, 32 * kBtWarps, 0, ctx->stream>>>(b);
+  }
+  PSG_LAUNCHED(ctx);
+  if (a.qdelta) return;  // uncertain / overflowing queries are on the caller's list
+  b.nq_dev = nullptr;
+  search_kernel<<<ctx->num_sms, 32 * kSearchWarps, 0, ctx->stream>>>(b);
+  PSG_LAUNCHED(ctx);
+}
+
 void launch_search(psg_ctx* ctx, const SearchArgs& a) {
   ProfScope _prof(ctx, a.nq_dev ? K_FALLBACK : K_SEARCH);
   if (a.nq <= 0) return;
@@ -2065,6 +2189,10 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
     // a device-counted list of unrelated queries (the exact fallback of the
     // tensor-core projection): one warp per query -- tiles of 32 unrelated
     // queries would traverse the union of their candidate sets
+    if (a.mode == PSG_BACKTRACK) {  // uncertain queries of an approximate backtrack search
+      launch_backtrack(ctx, a);
+      return;
+    }
     if (a.mode != PSG_EXACT || !a.proj32_q4 || !a.tree.centroid32T)
       fail(PSG_E_LOGIC, "device-counted search needs the exact warp kernel");
     const int64_t blocks = 32;  // re-searches are rare: a few hundred warps
@@ -2137,53 +2265,7 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
     return;
   }
   if (a.mode == PSG_BACKTRACK && a.d <= 64 && !ctx->knobs.legacy_search) {
-    // queries whose frontier outgrows the shared-memory pool are listed and
-    // re-run by the deep-stack warp kernel below (same answers)
-    // (the caller may provide the list buffers: levels allocate them once,
-    // outside any captured iteration)
-    DBuf<int32_t> ovf;
-    DBuf<int> ovf_n;
-    SearchArgs b = a;
-    if (!b.ovf_list || !b.ovf_count) {
-      ovf.alloc((size_t)a.nq);
-      ovf_n.alloc(1);
-      b.ovf_list = ovf.p;
-      b.ovf_count = ovf_n.p;
-    }
-    PSG_CUDA(cudaMemsetAsync(b.ovf_count, 0, sizeof(int), ctx->stream));
-    const int mc = a.tree.max_children;
-    if (b.proj_leaf_il && a.tree.centroid_il && mc <= 16 && a.d <= 64 && !ctx->knobs.bt_warp) {
-      // a group of 8 (16) lanes per query: 16 (8) queries per CTA
-      const int qpc = kBgWarps * (mc <= 8 ? 4 : 2);
-      int64_t blocks = (a.nq + qpc - 1) / qpc;
-      const int64_t cap = (int64_t)ctx->num_sms * 16;
-      if (blocks > cap) blocks = cap;
-      const dim3 blk(32 * kBgWarps);
-#define PSG_BG_LAUNCH(DPV)                                                                      \
-  do {                                                                                          \
-    if (mc <= 8)                                                                                \
-      search_backtrack_group_kernel<DPV, 8, kBgCap><<<(int)blocks, blk, 0, ctx->stream>>>(b);   \
-    else                                                                                        \
-      search_backtrack_group_kernel<DPV, 16, kBgCap><<<(int)blocks, blk, 0, ctx->stream>>>(b);  \
-  } while (0)
-      // the blocks' width = the index's fp32 layout class (upload_tree)
-      if (a.d <= 24) PSG_BG_LAUNCH(24);
-      else if (a.d <= 32) PSG_BG_LAUNCH(32);
-      else if (a.d <= 48) PSG_BG_LAUNCH(48);
-      else PSG_BG_LAUNCH(64);
-#undef PSG_BG_LAUNCH
-    } else {
-      int64_t blocks = (a.nq + kBtWarps - 1) / kBtWarps;
-      const int64_t cap = (int64_t)ctx->num_sms * 16;
-      if (blocks > cap) blocks = cap;
-      if (a.d <= 32)
-        search_backtrack_kernel<32><<<(int)blocks, 32 * kBtWarps, 0, ctx->stream>>>(b);
-      else
-        search_backtrack_kernel<64><<<(int)blocks, 32 * kBtWarps, 0, ctx->stream>>>(b);
-    }
-    PSG_LAUNCHED(ctx);
-    search_kernel<<<ctx->num_sms, 32 * kSearchWarps, 0, ctx->stream>>>(b);
-    PSG_LAUNCHED(ctx);
+    launch_backtrack(ctx, a);
     return;
   }
   int64_t blocks = (a.nq + kSearchWarps - 1) / kSearchWarps;

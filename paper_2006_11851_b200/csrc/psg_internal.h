@@ -201,6 +201,7 @@ struct psg_ctx {
     bool eig_direct = false;          // PERSYN_EIG: dense eigensolver instead of subspace iteration
     bool exact_projection = false;    // PERSYN_EXACT_PROJECTION: fp64 SIMT projection of every query
     bool bt_warp = false;             // PERSYN_BT_WARP: backtrack(m > 2) warp per query (not lane groups)
+    bool bt_exact_projection = false; // PERSYN_BT_EXACT_PROJECTION: fp64 projection for backtrack(m > 2)
   } knobs;
 };
 
@@ -417,6 +418,9 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a);
 // true when an exact search of this tree runs on the tile kernel
 // nq >= 0: an image search of nq anchors (few anchors -> warp-per-query kernel)
 bool search_uses_tiles(psg_ctx* ctx, const DevTree& tree, int d, bool exact, int64_t nq = -1);
+// true when a backtrack(m) search of this index runs on the lane-group kernel
+// (which also takes tensor-core-projected queries with an error band)
+bool search_uses_groups(psg_ctx* ctx, const Index& ix, const psg_budget& budget);
 // tcgen05 (UMMA) tile search; returns false when the tree shape is unsupported.
 // Tile search with the leaf filter on mma.sync (bf16 split); false if unsupported.
 // Locality ordering of unstructured queries (search-only workloads).

@@ -697,8 +697,12 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
   }
   // exact budget on the tile kernel: tensor-core projection with an error
   // band + exact fallback for the ambiguous queries (kernels_project_tc.cu)
-  const bool tc = ix.tc && ix.d > 0 && L.cfg.budget.mode == PSG_EXACT &&
-                  !ctx->knobs.exact_projection && search_uses_tiles(ctx, ix.tree, ix.d, true, L.Ao);
+  // (backtrack(m > 2) on the lane-group kernel takes the same projection: every
+  // pop and the final winner are checked against the band)
+  const bool tc = ix.tc && ix.d > 0 && !ctx->knobs.exact_projection &&
+                  ((L.cfg.budget.mode == PSG_EXACT &&
+                    search_uses_tiles(ctx, ix.tree, ix.d, true, L.Ao)) ||
+                   (search_uses_groups(ctx, ix, L.cfg.budget) && !ctx->knobs.bt_exact_projection));
   const int64_t q8_slice = (int64_t)L.W * L.Hl * 8;
   if (tc) {
     if (!L.q8.p) {
@@ -827,7 +831,7 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
     f.nq_dev = L.full_n.p;
     f.qxs = nullptr;
     f.qys = nullptr;
-    f.seed_idx = L.seed_c.p;
+    f.seed_idx = a.mode == PSG_EXACT ? L.seed_c.p : nullptr;
     f.out_map = L.full_anchor.p;  // results straight to the anchors
     f.out_idx = out_idx + L.off;
     f.out_d2 = nullptr;
@@ -1253,6 +1257,7 @@ psg_status psg_ctx_create(int device, void* stream, psg_ctx** out) {
       kn.eig_direct = on("PERSYN_EIG");
       kn.exact_projection = on("PERSYN_EXACT_PROJECTION");
       kn.bt_warp = on("PERSYN_BT_WARP");
+      kn.bt_exact_projection = on("PERSYN_BT_EXACT_PROJECTION");
     }
     if (stream) {
       c->stream = static_cast<cudaStream_t>(stream);

@@ -94,6 +94,35 @@ def test_backtrack_lane_group_kernel_equals_warp_kernel(gpu_ctx, port, monkeypat
     assert res[0][3] == res[1][3]  # points scanned
 
 
+@pytest.mark.parametrize("kind", ["sinusoid", "periodic"])
+@pytest.mark.parametrize("d,b,m", [(16, 8, 4), (32, 4, 8), (40, 16, 4)])
+def test_backtrack_tensor_core_projection_equals_exact_projection(gpu_ctx, port, monkeypatch, kind,
+                                                                  d, b, m):
+    """backtrack(m > 2) with the tensor-core projection (every pop and the final
+    winner checked against the projection's error band, uncertain queries re-run
+    with the exact fp64 projection) returns what the all-exact path returns --
+    also on a periodic exemplar whose duplicate windows tie EVERY decision."""
+    if kind == "sinusoid":
+        ex, init = _stage()
+    else:
+        rng = np.random.default_rng(5)
+        cell = rng.integers(0, 256, (3, 8, 8)).astype(np.float64) / 255.0
+        ex = np.concatenate([np.tile(cell, (1, 5, 5)), np.full((1, 40, 40), 0.5)], 0)
+        init = np.concatenate([rng.random((3, 56, 56)), np.full((1, 56, 56), 0.5)], 0)
+    cand = port.extract_all(ex, 8, 1)
+    mean, basis, _ = fit_pca(cand, d_fixed=d)
+    monkeypatch.setenv("PERSYN_BT_EXACT_PROJECTION", "1")
+    exact_ctx = api.Context(0)
+    monkeypatch.delenv("PERSYN_BT_EXACT_PROJECTION", raising=False)
+    res = []
+    for ctx in (gpu_ctx, exact_ctx):
+        ix = api.make_pca_tree_index(ex, 8, mean=mean, basis=basis, branching=b, max_depth=4,
+                                     seed=3, ctx=ctx)
+        res.append(api.search_step(init, ix, 2, 2, api.QueryBudget.backtrack(m)))
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    assert res[0][3] == res[1][3]  # points scanned
+
+
 def test_eigensolver_paths_agree(gpu_ctx, monkeypatch):
     """Top-d PCA pairs by subspace iteration vs the direct DSYEVDX solver."""
     ex, _ = _stage(size=48, G=2)
