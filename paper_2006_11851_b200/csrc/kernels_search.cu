@@ -1111,7 +1111,9 @@ constexpr int kBgWarps = 4, kBgCap = PSG_BG_CAP;
 // strict minimum" made on the q^ keys is the reference's decision whenever
 // every other key exceeds T(a) = (sqrt(K^_a) + 2 delta)^2 inflated by 1e-11
 // (which dominates both chains' rounding): the kernel tracks the second
-// smallest key of every pop and of all scanned points, and a query with any
+// smallest key of every pop and of all scanned points -- as the HIGH WORD of
+// the non-negative double (an ordered integer; hi(k2) > hi(T) implies k2 > T,
+// one 32-bit min / shuffle instead of fp64 ones) -- and a query with any
 // decision inside its band (or whose frontier outgrows the pool) is listed in
 // a.amb_list and re-run with its exact projection (AP = false, device-counted
 // list, results written through a.out_map).
@@ -1151,7 +1153,8 @@ search_backtrack_group_kernel(SearchArgs a) {
       pm[0] = root;
     }
     __syncwarp();
-    double best = kInf, second = kInf;
+    double best = kInf;
+    int32_t second = 0x7ff00000;  // high word of the second smallest scanned key
     int32_t best_id = 0x7fffffff;
     int32_t scanned = 0, visited = 0;
     int size = live ? 1 : 0, leaves = 0;
@@ -1166,19 +1169,20 @@ search_backtrack_group_kernel(SearchArgs a) {
       const bool act = size > 0 && leaves < a.max_leaves && !overflow;
       if (!__any_sync(kFull, act)) break;
       // ---- pop the lexicographic minimum (key, tie) of the group's pool ----
-      double bk = kInf, k2 = kInf;
+      double bk = kInf;
+      int32_t k2 = 0x7ff00000;  // high word of the second smallest key
       int32_t bt = 0x7fffffff, bs = 0;
       const int n = act ? size : 0;
       for (int s = l; s < n; s += G) {
         const double k = pk[s];
         const int32_t t = pt[s];
         if (k < bk || (k == bk && t < bt)) {
-          if (AP) k2 = bk;
+          if (AP) k2 = __double2hiint(bk);
           bk = k;
           bt = t;
           bs = s;
         } else if (AP) {
-          k2 = fmin(k2, k);
+          k2 = min(k2, __double2hiint(k));
         }
       }
 #pragma unroll
@@ -1187,8 +1191,8 @@ search_backtrack_group_kernel(SearchArgs a) {
         const int32_t ot = __shfl_xor_sync(kFull, bt, off);
         const int32_t os = __shfl_xor_sync(kFull, bs, off);
         if (AP) {
-          const double o2 = __shfl_xor_sync(kFull, k2, off);
-          k2 = fmin(fmin(k2, o2), fmax(bk, ok));
+          const int32_t o2 = __shfl_xor_sync(kFull, k2, off);
+          k2 = min(min(k2, o2), max(__double2hiint(bk), __double2hiint(ok)));
         }
         if (ok < bk || (ok == bk && ot < bt)) {
           bk = ok;
@@ -1215,7 +1219,7 @@ search_backtrack_group_kernel(SearchArgs a) {
         overflow = true;  // re-run by the deep-stack kernel
         cnt = 0;
       }
-      if (AP && act && !(k2 > band_top(bk, dl2))) {
+      if (AP && act && !(k2 > __double2hiint(band_top(bk, dl2)))) {
         overflow = true;  // the pop order is not certain: exact re-run
         cnt = 0;
       }
@@ -1259,22 +1263,23 @@ search_backtrack_group_kernel(SearchArgs a) {
         // leaf rows: group-wide lexicographic (dist^2, id) minimum (inner-node
         // groups and idle lanes carry +inf and change nothing)
         if (__any_sync(kFull, on && leaf)) {
-          double md = (on && leaf) ? acc : kInf, m2 = kInf;
+          double md = (on && leaf) ? acc : kInf;
+          int32_t m2 = 0x7ff00000;
           int32_t mi = (on && leaf) ? ct : 0x7fffffff;
 #pragma unroll
           for (int off = G / 2; off > 0; off >>= 1) {
             const double od = __shfl_xor_sync(kFull, md, off);
             const int32_t oi = __shfl_xor_sync(kFull, mi, off);
             if (AP) {
-              const double o2 = __shfl_xor_sync(kFull, m2, off);
-              m2 = fmin(fmin(m2, o2), fmax(md, od));
+              const int32_t o2 = __shfl_xor_sync(kFull, m2, off);
+              m2 = min(min(m2, o2), max(__double2hiint(md), __double2hiint(od)));
             }
             if (lex_less(od, oi, md, mi)) {
               md = od;
               mi = oi;
             }
           }
-          if (AP) second = fmin(fmin(second, m2), fmax(best, md));
+          if (AP) second = min(min(second, m2), max(__double2hiint(best), __double2hiint(md)));
           if (lex_less(md, mi, best, best_id)) {
             best = md;
             best_id = mi;
@@ -1291,7 +1296,7 @@ search_backtrack_group_kernel(SearchArgs a) {
       }
       __syncwarp();
     }
-    if (AP && live && !overflow && !(second > band_top(best, dl2))) overflow = true;
+    if (AP && live && !overflow && !(second > __double2hiint(band_top(best, dl2)))) overflow = true;
     if (live && l == 0) {
       if (overflow) {
         if (AP) {
