@@ -1138,6 +1138,10 @@ search_backtrack_group_kernel(SearchArgs a) {
   const int32_t root_tie = a.tree.tie ? a.tree.tie[0] : 0;
   const unsigned kFull = 0xffffffffu;
   const int64_t nq = a.nq_dev ? (int64_t)*a.nq_dev : a.nq;
+  // greedy (km_tree.cpp:213-229): the frontier holds the current node's children
+  // only, ties go to the first child, one leaf
+  const bool greedy = a.mode == PSG_GREEDY;
+  const int max_leaves = greedy ? 1 : a.max_leaves;
   // smallest key another entry must exceed for `k` to be the robust minimum
   auto band_top = [](double k, double dl2) {
     const double s = (double)__fsqrt_ru(__double2float_ru(k));
@@ -1166,7 +1170,7 @@ search_backtrack_group_kernel(SearchArgs a) {
       dl2 = 2.0 * (double)dl * (1.0 + 1e-6);
     }
     for (;;) {
-      const bool act = size > 0 && leaves < a.max_leaves && !overflow;
+      const bool act = size > 0 && leaves < max_leaves && !overflow;
       if (!__any_sync(kFull, act)) break;
       // ---- pop the lexicographic minimum (key, tie) of the group's pool ----
       double bk = kInf;
@@ -1209,6 +1213,7 @@ search_backtrack_group_kernel(SearchArgs a) {
           pm[bs] = pm[size - 1];
         }
         --size;
+        if (greedy) size = 0;  // the siblings are dropped
         ++visited;
       }
       __syncwarp();
@@ -1243,7 +1248,7 @@ search_backtrack_group_kernel(SearchArgs a) {
             ct = __ldg(a.perm + e.x + i);
           } else {
             cm = __ldg(a.tree.meta + e.x + i);
-            ct = a.tree.tie ? __ldg(a.tree.tie + e.x + i) : e.x + i;
+            ct = (a.tree.tie && !greedy) ? __ldg(a.tree.tie + e.x + i) : e.x + i;
           }
         }
         double acc = 0.0;
@@ -2115,13 +2120,14 @@ bool search_uses_tiles(psg_ctx* ctx, const DevTree& tree, int d, bool exact, int
 }
 
 bool search_uses_groups(psg_ctx* ctx, const Index& ix, const psg_budget& budget) {
-  return budget.mode == PSG_BACKTRACK && budget.max_leaves > 2 && ix.d > 0 && ix.d <= 64 &&
-         ix.proj_leaf_il && ix.tree.centroid_il && ix.tree.max_children <= 16 &&
-         !ctx->knobs.legacy_search && !ctx->knobs.bt_warp;
+  const bool small = budget.mode == PSG_GREEDY || budget.max_leaves <= 2;
+  return budget.mode != PSG_EXACT && ix.d > 0 && ix.d <= 64 && ix.proj_leaf_il &&
+         ix.tree.centroid_il && ix.tree.max_children <= 16 && !ctx->knobs.legacy_search &&
+         !ctx->knobs.bt_warp && !(ctx->knobs.bt_thread && small);
 }
 
-// backtrack(m > 2), d <= 64: the lane-group kernel (or the warp-per-query
-// kernel for wide trees / PERSYN_BT_WARP), then the deep-stack kernel for the
+// greedy / backtrack(m), d <= 64: the lane-group kernel (or, for m > 2 on wide
+// trees / PERSYN_BT_WARP, the warp-per-query kernel), then the deep-stack kernel for the
 // queries whose frontier outgrew the pool.  a.qdelta set: approximate queries
 // (see search_backtrack_group_kernel; uncertain queries go to a.amb_list and
 // nothing overflows).  a.nq_dev set: a device-counted list of exact queries
@@ -2194,7 +2200,7 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
     // a device-counted list of unrelated queries (the exact fallback of the
     // tensor-core projection): one warp per query -- tiles of 32 unrelated
     // queries would traverse the union of their candidate sets
-    if (a.mode == PSG_BACKTRACK) {  // uncertain queries of an approximate backtrack search
+    if (a.mode != PSG_EXACT) {  // uncertain queries of an approximate greedy / backtrack search
       launch_backtrack(ctx, a);
       return;
     }
@@ -2257,6 +2263,13 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
   // thread-per-query kernel for greedy and short backtracks; longer frontiers
   // (m > 2) spill the per-thread heap and run faster warp-per-query (as does
   // d > 64: the per-thread query would not fit the register file)
+  // greedy / backtrack(m) on the lane-group kernel whenever the tree fits it
+  if (a.mode != PSG_EXACT && !ctx->knobs.legacy_search && a.d <= 64 && a.proj_leaf_il &&
+      a.tree.centroid_il && a.tree.max_children <= 16 && !ctx->knobs.bt_warp &&
+      !(ctx->knobs.bt_thread && (a.mode == PSG_GREEDY || a.max_leaves <= 2))) {
+    launch_backtrack(ctx, a);
+    return;
+  }
   if (a.mode != PSG_EXACT && !ctx->knobs.legacy_search && a.d <= 64 &&
       (a.mode == PSG_GREEDY || a.max_leaves <= 2)) {
     int64_t blocks = (a.nq + 127) / 128;

@@ -201,7 +201,8 @@ struct psg_ctx {
     bool eig_direct = false;          // PERSYN_EIG: dense eigensolver instead of subspace iteration
     bool exact_projection = false;    // PERSYN_EXACT_PROJECTION: fp64 SIMT projection of every query
     bool bt_warp = false;             // PERSYN_BT_WARP: backtrack(m > 2) warp per query (not lane groups)
-    bool bt_exact_projection = false; // PERSYN_BT_EXACT_PROJECTION: fp64 projection for backtrack(m > 2)
+    bool bt_thread = false;           // PERSYN_BT_THREAD: greedy / backtrack(m <= 2) thread per query
+    bool bt_exact_projection = false; // PERSYN_BT_EXACT_PROJECTION: fp64 projection for greedy / backtrack
   } knobs;
 };
 

@@ -1257,6 +1257,7 @@ psg_status psg_ctx_create(int device, void* stream, psg_ctx** out) {
       kn.eig_direct = on("PERSYN_EIG");
       kn.exact_projection = on("PERSYN_EXACT_PROJECTION");
       kn.bt_warp = on("PERSYN_BT_WARP");
+      kn.bt_thread = on("PERSYN_BT_THREAD");
       kn.bt_exact_projection = on("PERSYN_BT_EXACT_PROJECTION");
     }
     if (stream) {

@@ -123,6 +123,30 @@ def test_backtrack_tensor_core_projection_equals_exact_projection(gpu_ctx, port,
     assert res[0][3] == res[1][3]  # points scanned
 
 
+@pytest.mark.parametrize("budget", ["greedy", "bt1", "bt2"])
+@pytest.mark.parametrize("d,b", [(12, 4), (32, 8), (40, 16)])
+def test_small_budgets_lane_group_kernel_equals_thread_kernel(gpu_ctx, port, monkeypatch, budget,
+                                                              d, b):
+    """greedy / backtrack(1) / backtrack(2): the lane-group kernel fed by the
+    tensor-core projection and the thread-per-query kernel with the fp64
+    projection (PERSYN_BT_THREAD) return identical answers and scan counts."""
+    ex, init = _stage()
+    cand = port.extract_all(ex, 8, 1)
+    mean, basis, _ = fit_pca(cand, d_fixed=d)
+    monkeypatch.setenv("PERSYN_BT_THREAD", "1")
+    thread_ctx = api.Context(0)
+    monkeypatch.delenv("PERSYN_BT_THREAD", raising=False)
+    bud = {"greedy": api.QueryBudget.greedy(), "bt1": api.QueryBudget.backtrack(1),
+           "bt2": api.QueryBudget.backtrack(2)}[budget]
+    res = []
+    for ctx in (gpu_ctx, thread_ctx):
+        ix = api.make_pca_tree_index(ex, 8, mean=mean, basis=basis, branching=b, max_depth=4,
+                                     seed=3, ctx=ctx)
+        res.append(api.search_step(init, ix, 2, 2, bud))
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    assert res[0][3] == res[1][3]  # points scanned
+
+
 def test_eigensolver_paths_agree(gpu_ctx, monkeypatch):
     """Top-d PCA pairs by subspace iteration vs the direct DSYEVDX solver."""
     ex, _ = _stage(size=48, G=2)
