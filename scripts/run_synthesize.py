@@ -1,6 +1,7 @@
 """Full coarse-to-fine synthesis of a BASELINE config through psg_synthesize.
 
-usage: python scripts/run_synthesize.py <cfg id> [iterations] [budget]
+usage: python scripts/run_synthesize.py <cfg id> [iterations] [budget] [tree]
+  budget: exact (default) | greedy | backtrack:<m>      tree: device (default) | reference
 Prints per-stage timings (index build / optimize) and the totals as JSON.
 """
 import json
@@ -21,16 +22,22 @@ def main():
     iters = int(sys.argv[2]) if len(sys.argv) > 2 else cfg.iterations
     rgb = wl.sinusoid_exemplar(cfg.ex_size, cfg.n_sin, cfg.ramp, cfg.seed, cfg.lum_gain)
     ex = wl.rgbs_planes(rgb, cfg.G)
+    bname = sys.argv[3] if len(sys.argv) > 3 else "exact"
+    budget = (api.QueryBudget.exact() if bname == "exact" else api.QueryBudget.greedy()
+              if bname == "greedy" else api.QueryBudget.backtrack(int(bname.split(":")[1])))
+    tree = sys.argv[4] if len(sys.argv) > 4 else "device"
     ocfg = api.OptimizerConfig(max_iterations=iters, min_iterations=iters,
-                               convergence_fraction=1e-9, budget=api.QueryBudget.exact())
+                               convergence_fraction=1e-9, budget=budget)
     ctx = api.Context(0)
     t = time.perf_counter()
     out, rep = api.synthesize(ex, cfg.out, cfg.out, cfg.levels, cfg.sizes, ocfg,
                               variance_target=0.95, d_cap=cfg.d_cap, d_fixed=cfg.d_fixed,
-                              branching=cfg.branching, max_depth=cfg.depth, seed=cfg.seed, ctx=ctx)
+                              branching=cfg.branching, seed=cfg.seed, ctx=ctx,
+                              max_depth=0 if tree == "reference" else cfg.depth,
+                              tree_kind=api.TREE_REFERENCE if tree == "reference" else api.TREE_DEVICE)
     wall = time.perf_counter() - t
     n_it = sum(s["iterations"] for s in rep["stages"])
-    line = {"config": cfg.name, "out": cfg.out, "levels": cfg.levels, "sizes": list(cfg.sizes),
+    line = {"config": cfg.name, "budget": bname, "tree": tree, "out": cfg.out, "levels": cfg.levels, "sizes": list(cfg.sizes),
             "wall_s": wall, "em_iterations": n_it,
             "index_build_s": sum(s["index_millis"] for s in rep["stages"]) / 1e3,
             "optimize_s": sum(s["optimize_millis"] for s in rep["stages"]) / 1e3,
