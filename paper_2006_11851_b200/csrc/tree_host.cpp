@@ -21,6 +21,9 @@
 #include <random>
 #include <vector>
 
+#include <thread>
+
+#include "kmeans_host.h"
 #include "psg_internal.h"
 
 namespace psg {
@@ -33,97 +36,6 @@ inline double dist2(const double* a, const double* b, int d) {
     acc += t * t;
   }
   return acc;
-}
-
-// Clusterer::run (km_tree.cpp:34-119) over ascending ids: k-means++ seeding
-// (first centre uniform_int(0, n-1); then D^2 sampling with
-// uniform_real(0, total) and the subtract-until-<=0 scan), a strict-<
-// reassign (lowest centre wins ties), <= 20 Lloyd sweeps with ordered sums
-// (empty clusters keep their centre) stopping when the largest move < 1e-6,
-// then the non-empty clusters, each in ascending id order.
-std::vector<std::vector<int32_t>> kmeans_reference(const double* P, int d,
-                                                   const std::vector<int32_t>& ids, int k,
-                                                   std::mt19937_64& rng) {
-  const size_t n = ids.size();
-  auto pt = [&](size_t i) { return P + (size_t)ids[i] * d; };
-  std::vector<double> ctr;
-  ctr.reserve((size_t)k * d);
-  std::uniform_int_distribution<std::size_t> first(0, n - 1);
-  {
-    const double* c0 = pt(first(rng));
-    ctr.insert(ctr.end(), c0, c0 + d);
-  }
-  std::vector<double> d2(n);
-  for (size_t i = 0; i < n; ++i) d2[i] = dist2(pt(i), ctr.data(), d);
-  int nc = 1;
-  while (nc < k) {
-    double total = 0.0;
-    for (double v : d2) total += v;
-    if (total <= 0.0) break;
-    std::uniform_real_distribution<double> pick(0.0, total);
-    double r = pick(rng);
-    size_t chosen = n - 1;
-    for (size_t i = 0; i < n; ++i) {
-      r -= d2[i];
-      if (r <= 0.0) {
-        chosen = i;
-        break;
-      }
-    }
-    const double* c = pt(chosen);
-    ctr.insert(ctr.end(), c, c + d);
-    const double* cn = ctr.data() + (size_t)nc * d;
-    ++nc;
-    for (size_t i = 0; i < n; ++i) d2[i] = std::min(d2[i], dist2(pt(i), cn, d));
-  }
-  std::vector<int> assign(n);
-  auto reassign = [&] {
-    for (size_t i = 0; i < n; ++i) {
-      int best = 0;
-      double bd = dist2(pt(i), ctr.data(), d);
-      for (int c = 1; c < nc; ++c) {
-        const double v = dist2(pt(i), ctr.data() + (size_t)c * d, d);
-        if (v < bd) {
-          bd = v;
-          best = c;
-        }
-      }
-      assign[i] = best;
-    }
-  };
-  reassign();
-  std::vector<double> sums((size_t)nc * d);
-  std::vector<size_t> sizes((size_t)nc);
-  for (int sweep = 0; sweep < 20; ++sweep) {
-    std::fill(sums.begin(), sums.end(), 0.0);
-    std::fill(sizes.begin(), sizes.end(), 0);
-    for (size_t i = 0; i < n; ++i) {
-      const double* p = pt(i);
-      double* s = sums.data() + (size_t)assign[i] * d;
-      for (int j = 0; j < d; ++j) s[j] += p[j];
-      ++sizes[(size_t)assign[i]];
-    }
-    double movement = 0.0;
-    for (int c = 0; c < nc; ++c) {
-      if (sizes[(size_t)c] == 0) continue;
-      double move = 0.0;
-      for (int j = 0; j < d; ++j) {
-        const double v = sums[(size_t)c * d + j] / sizes[(size_t)c];
-        const double t = v - ctr[(size_t)c * d + j];
-        move += t * t;
-        ctr[(size_t)c * d + j] = v;
-      }
-      movement = std::max(movement, std::sqrt(move));
-    }
-    if (movement < 1e-6) break;
-    reassign();
-  }
-  std::vector<std::vector<int32_t>> out((size_t)nc);
-  for (size_t i = 0; i < n; ++i) out[(size_t)assign[i]].push_back(ids[i]);
-  out.erase(std::remove_if(out.begin(), out.end(),
-                           [](const std::vector<int32_t>& v) { return v.empty(); }),
-            out.end());
-  return out;
 }
 
 }  // namespace
@@ -140,6 +52,10 @@ HostTree build_reference_tree_host(const double* P, int64_t N, int d, int branch
   if (branching < 2) fail(PSG_E_DOMAIN, "tree branching must be >= 2");
   if (leaf_threshold <= 0) leaf_threshold = branching;
   std::mt19937_64 rng(seed);
+  // the k-means of large nodes runs on a few host threads (kmeans_host.cpp);
+  // the walk itself and every RNG draw stay sequential
+  const unsigned hw = std::thread::hardware_concurrency();
+  HostPool pool(N >= 4096 ? (int)std::min(16u, std::max(1u, hw)) : 1);
   std::vector<int32_t> n_children, leaf_sizes, leaf_ids;
   leaf_ids.reserve((size_t)N);
   std::vector<std::vector<int32_t>> todo(1);
@@ -150,7 +66,7 @@ HostTree build_reference_tree_host(const double* P, int64_t N, int d, int branch
     todo.pop_back();
     if ((int64_t)ids.size() >= leaf_threshold && d > 0) {
       const int k = (int)std::min<size_t>((size_t)branching, ids.size());
-      auto cl = kmeans_reference(P, d, ids, k, rng);
+      auto cl = kmeans_reference(P, d, ids, k, rng, &pool);
       if (cl.size() >= 2) {
         n_children.push_back((int32_t)cl.size());
         for (size_t c = cl.size(); c-- > 0;) todo.push_back(std::move(cl[c]));
