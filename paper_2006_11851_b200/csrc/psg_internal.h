@@ -156,6 +156,7 @@ extern const char* const kKernelNames[K_COUNT];
 }  // namespace psg
 
 struct psg_ctx {
+  psg_ctx* builder = nullptr;  // second context of psg_synthesize's index build-ahead thread (owned)
   // per-kernel event timing (psg_ctx_profile)
   bool profile = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -202,6 +203,7 @@ struct psg_ctx {
     bool exact_projection = false;    // PERSYN_EXACT_PROJECTION: fp64 SIMT projection of every query
     bool bt_warp = false;             // PERSYN_BT_WARP: backtrack(m > 2) warp per query (not lane groups)
     bool bt_thread = false;           // PERSYN_BT_THREAD: greedy / backtrack(m <= 2) thread per query
+    bool no_build_ahead = false;      // PERSYN_NO_BUILD_AHEAD: synthesize builds each index inline
     bool bt_exact_projection = false; // PERSYN_BT_EXACT_PROJECTION: fp64 projection for greedy / backtrack
   } knobs;
 };

@@ -18,7 +18,12 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
+#include <exception>
+#include <functional>
 #include <memory>
+#include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -1258,6 +1263,7 @@ psg_status psg_ctx_create(int device, void* stream, psg_ctx** out) {
       kn.exact_projection = on("PERSYN_EXACT_PROJECTION");
       kn.bt_warp = on("PERSYN_BT_WARP");
       kn.bt_thread = on("PERSYN_BT_THREAD");
+      kn.no_build_ahead = on("PERSYN_NO_BUILD_AHEAD");
       kn.bt_exact_projection = on("PERSYN_BT_EXACT_PROJECTION");
     }
     if (stream) {
@@ -1286,6 +1292,7 @@ psg_status psg_ctx_create(int device, void* stream, psg_ctx** out) {
 
 void psg_ctx_destroy(psg_ctx* ctx) {
   if (!ctx) return;
+  if (ctx->builder) psg_ctx_destroy(ctx->builder);
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (auto& p : ctx->pending) {
@@ -1877,6 +1884,107 @@ double psg_hist_mass(int64_t count, int64_t pixels) {
 // (level x neighbourhood size) per the BASELINE configs.
 // ===========================================================================
 
+namespace psg {
+namespace {
+
+// The stages' indexes built ONE STAGE AHEAD of the EM loop: an index depends
+// only on the exemplar level and the stage's configuration, never on the
+// output, so stage k + 1's PCA fit / projection / tree build (many small
+// kernels and host synchronisations, or the host replica of KmTree::build)
+// runs in a worker thread on a second context (own stream, own cuBLAS /
+// cuSOLVER handles) while stage k's EM iterations saturate the GPU from the
+// caller's stream.  Results do not depend on the overlap; PERSYN_NO_BUILD_AHEAD
+// builds each index inline on the caller's context.
+class IndexAhead {
+ public:
+  using Build = std::function<std::unique_ptr<psg_index>(psg_ctx*)>;
+  IndexAhead(psg_ctx* main, std::vector<Build> jobs) : main_(main), jobs_(std::move(jobs)) {
+    done_.resize(jobs_.size());
+    if (main_->knobs.no_build_ahead || jobs_.size() < 2) return;
+    if (!main_->builder) {
+      psg_ctx* b = nullptr;
+      if (psg_ctx_create(main_->device, nullptr, &b) != PSG_OK)
+        fail(PSG_E_CUDA, "cannot create the index builder context: " + g_last_error);
+      main_->builder = b;
+    }
+    worker_ = std::thread([this] { run(); });
+  }
+  ~IndexAhead() {
+    if (worker_.joinable()) {
+      {
+        std::lock_guard<std::mutex> lk(m_);
+        stop_ = true;
+      }
+      cv_.notify_all();
+      worker_.join();
+    }
+  }
+  // index of stage k (stages are taken in order); ms = its build time
+  std::unique_ptr<psg_index> take(size_t k, double* ms) {
+    if (!worker_.joinable()) {
+      const double t = now_ms();
+      auto ix = jobs_[k](main_);
+      *ms = now_ms() - t;
+      return ix;
+    }
+    std::unique_lock<std::mutex> lk(m_);
+    taken_ = k + 1;
+    cv_.notify_all();
+    cv_.wait(lk, [&] { return done_[k].ready; });
+    if (done_[k].err) std::rethrow_exception(done_[k].err);
+    *ms = done_[k].ms;
+    return std::move(done_[k].index);
+  }
+
+ private:
+  struct Slot {
+    std::unique_ptr<psg_index> index;
+    double ms = 0.0;
+    std::exception_ptr err;
+    bool ready = false;
+  };
+  void run() {
+    cudaSetDevice(main_->device);
+    psg_ctx* b = main_->builder;
+    StreamScope ss(b->stream);
+    for (size_t k = 0; k < jobs_.size(); ++k) {
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return stop_ || k <= taken_; });  // at most one stage ahead
+        if (stop_) return;
+      }
+      Slot s;
+      const double t = now_ms();
+      try {
+        s.index = jobs_[k](b);
+        cudaStreamSynchronize(b->stream);  // ready for the caller's stream
+      } catch (...) {
+        s.err = std::current_exception();
+      }
+      s.ms = now_ms() - t;
+      s.ready = true;
+      const bool failed = (bool)s.err;
+      {
+        std::lock_guard<std::mutex> lk(m_);
+        done_[k] = std::move(s);
+      }
+      cv_.notify_all();
+      if (failed) return;
+    }
+  }
+  psg_ctx* main_;
+  std::vector<Build> jobs_;
+  std::vector<Slot> done_;
+  std::thread worker_;
+  std::mutex m_;
+  std::condition_variable cv_;
+  size_t taken_ = 0;
+  bool stop_ = false;
+};
+
+}  // namespace
+}  // namespace psg
+
 extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, double* out_planes,
                                      psg_report* report) {
   return guarded([&] {
@@ -1953,6 +2061,47 @@ extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, doubl
     ex_lv[0].download(ctx, hex.data(), hex.size());
     og_lv[0].download(ctx, hog.data(), hog.size());
     PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    // the stages in schedule order and their index builds (IndexAhead: one
+    // stage ahead of the EM loop; the exemplar levels are complete here)
+    struct StageJob {
+      int l, si, w;
+    };
+    std::vector<StageJob> stage_jobs;
+    std::vector<IndexAhead::Build> builds;
+    for (int l = 0; l < L; ++l)
+      for (int si = 0; si < req->stages.n_sizes; ++si) {
+        const int w = req->stages.sizes[si];
+        if (w < 2 || w % 2) fail(PSG_E_DOMAIN, "neighbourhood sizes must be even and >= 2");
+        if (ow[l] < w || oh[l] < w || ew[l] < w || eh[l] < w) continue;
+        if ((int64_t)(ew[l] - w + 1) * (eh[l] - w + 1) < 2) continue;  // fit_pca needs n >= 2
+        psg_index_cfg icfg = req->index;
+        // level_seed (pipeline.cpp:54-56); several sizes per level (the
+        // BASELINE configs' stages) also mix in the window width
+        icfg.seed = (req->seed ^ (0x9E3779B97F4A7C15ull * (uint64_t)(l + 1))) ^
+                    (req->stages.n_sizes > 1 ? (uint64_t)w : 0ull);
+        if (req->cfg.histogram_matching) {
+          icfg.hist_bins = req->cfg.histogram_bins;
+          icfg.hist_include_scale = req->cfg.histogram_include_scale;
+        }
+        const int s_id = l * req->stages.n_sizes + si;
+        const double* s_mean = req->stage_mean ? req->stage_mean[s_id] : nullptr;
+        const double* s_basis = req->stage_basis ? req->stage_basis[s_id] : nullptr;
+        const int s_d = (s_basis && req->stage_d) ? req->stage_d[s_id] : 0;
+        if ((s_mean == nullptr) != (s_basis == nullptr))
+          fail(PSG_E_DOMAIN, "stage PCA injection needs both mean and basis");
+        const double* exl = ex_lv[l].p;
+        const int ewl = ew[l], ehl = eh[l];
+        const bool brute = req->index_kind == PSG_INDEX_BRUTE_FORCE;
+        stage_jobs.push_back({l, si, w});
+        builds.push_back([=](psg_ctx* bctx) {
+          return brute ? create_brute_from_device_planes(bctx, exl, C, ewl, ehl, w, icfg.hist_bins,
+                                                         icfg.hist_include_scale)
+                       : create_index_from_device_planes(bctx, exl, C, ewl, ehl, w, s_mean,
+                                                         s_basis, s_d, icfg);
+        });
+      }
+    IndexAhead ahead(ctx, std::move(builds));
+    size_t stage_no = 0;
     const size_t op0 = (size_t)ow[0] * oh[0];
     std::vector<double> init((size_t)C * op0);
     {
@@ -1996,27 +2145,11 @@ extern "C" psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, doubl
         if ((int64_t)(ew[l] - w + 1) * (eh[l] - w + 1) < 2) continue;  // fit_pca needs n >= 2
         const double ti = now_ms();
         {  // stage scope: index and level are released before the next stage
-        psg_index_cfg icfg = req->index;
-        // level_seed (pipeline.cpp:54-56); several sizes per level (the
-        // BASELINE configs' stages) also mix in the window width
-        icfg.seed = (req->seed ^ (0x9E3779B97F4A7C15ull * (uint64_t)(l + 1))) ^
-                    (req->stages.n_sizes > 1 ? (uint64_t)w : 0ull);
-        if (req->cfg.histogram_matching) {
-          icfg.hist_bins = req->cfg.histogram_bins;
-          icfg.hist_include_scale = req->cfg.histogram_include_scale;
-        }
-        const int s_id = l * req->stages.n_sizes + si;
-        const double* s_mean = req->stage_mean ? req->stage_mean[s_id] : nullptr;
-        const double* s_basis = req->stage_basis ? req->stage_basis[s_id] : nullptr;
-        const int s_d = (s_basis && req->stage_d) ? req->stage_d[s_id] : 0;
-        if ((s_mean == nullptr) != (s_basis == nullptr))
-          fail(PSG_E_DOMAIN, "stage PCA injection needs both mean and basis");
-        auto index = req->index_kind == PSG_INDEX_BRUTE_FORCE
-                         ? create_brute_from_device_planes(ctx, ex_lv[l].p, C, ew[l], eh[l], w,
-                                                           icfg.hist_bins, icfg.hist_include_scale)
-                         : create_index_from_device_planes(ctx, ex_lv[l].p, C, ew[l], eh[l], w,
-                                                           s_mean, s_basis, s_d, icfg);
-        const double index_ms = now_ms() - ti;
+        if (stage_no >= stage_jobs.size() || stage_jobs[stage_no].l != l ||
+            stage_jobs[stage_no].si != si)
+          fail(PSG_E_LOGIC, "stage schedule mismatch");
+        double index_ms = 0.0;
+        auto index = ahead.take(stage_no++, &index_ms);
         psg_opt_cfg cfg = req->cfg;
         cfg.spacing = std::max(1, w / 4);
         cfg.patch_width = std::min(std::max(1, cfg.patch_width), cfg.spacing);

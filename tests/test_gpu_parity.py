@@ -258,6 +258,32 @@ def test_synthesize_carried_seed_is_result_neutral(gpu_ctx, monkeypatch):
     assert r1["total_nn_calls"] == r2["total_nn_calls"]
 
 
+@pytest.mark.parametrize("budget,tree", [("exact", "device"), ("bt4", "reference")])
+def test_synthesize_index_build_ahead_is_result_neutral(monkeypatch, budget, tree):
+    """psg_synthesize builds stage k + 1's index in a worker thread on a second
+    context while stage k iterates; the overlap never changes a result (inline
+    builds: PERSYN_NO_BUILD_AHEAD).  The same context serves repeated calls."""
+    ex = wl.rgbs_planes(wl.sinusoid_exemplar(64, 16, 2.0, 3), 2)
+    bud = api.QueryBudget.exact() if budget == "exact" else api.QueryBudget.backtrack(4)
+    cfg = api.OptimizerConfig(max_iterations=3, min_iterations=3, convergence_fraction=1e-9,
+                              budget=bud)
+    kw = dict(variance_target=0.95, d_cap=32, branching=8, seed=1,
+              max_depth=3 if tree == "device" else 0,
+              tree_kind=api.TREE_DEVICE if tree == "device" else api.TREE_REFERENCE)
+    ahead = api.Context(0)
+    monkeypatch.setenv("PERSYN_NO_BUILD_AHEAD", "1")
+    inline = api.Context(0)
+    monkeypatch.delenv("PERSYN_NO_BUILD_AHEAD", raising=False)
+    o1, r1 = api.synthesize(ex, 128, 128, 3, (16, 8), cfg, ctx=ahead, **kw)
+    o2, r2 = api.synthesize(ex, 128, 128, 3, (16, 8), cfg, ctx=inline, **kw)
+    o3, r3 = api.synthesize(ex, 128, 128, 3, (16, 8), cfg, ctx=ahead, **kw)
+    assert np.array_equal(o1, o2) and np.array_equal(o1, o3)
+    assert len(r1["stages"]) == len(r2["stages"]) == len(r3["stages"]) == 5  # 16^2, w = 16 is skipped
+    for a, b, c in zip(r1["stages"], r2["stages"], r3["stages"]):
+        assert a["final_energy"] == b["final_energy"] == c["final_energy"]
+    assert r1["total_nn_calls"] == r2["total_nn_calls"] == r3["total_nn_calls"]
+
+
 @pytest.mark.parametrize("size,out,G,d,b,depth", [(128, 256, 2, 32, 8, 4), (256, 1024, 2, 32, 8, 4),
                                                   (96, 192, 1, 48, 16, 3)])
 def test_exact_search_full_size_sampled(gpu_ctx, port, size, out, G, d, b, depth):
