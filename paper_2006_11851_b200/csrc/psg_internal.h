@@ -156,7 +156,7 @@ extern const char* const kKernelNames[K_COUNT];
 }  // namespace psg
 
 struct psg_ctx {
-  psg_ctx* builder = nullptr;  // second context of psg_synthesize's index build-ahead thread (owned)
+  std::vector<psg_ctx*> builders;  // contexts of psg_synthesize's index build-ahead threads (owned)
   // per-kernel event timing (psg_ctx_profile)
   bool profile = false;
   std::vector<cudaEvent_t> ev_pool;

@@ -1292,7 +1292,7 @@ psg_status psg_ctx_create(int device, void* stream, psg_ctx** out) {
 
 void psg_ctx_destroy(psg_ctx* ctx) {
   if (!ctx) return;
-  if (ctx->builder) psg_ctx_destroy(ctx->builder);
+  for (psg_ctx* b : ctx->builders) psg_ctx_destroy(b);
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (auto& p : ctx->pending) {
@@ -1887,41 +1887,41 @@ double psg_hist_mass(int64_t count, int64_t pixels) {
 namespace psg {
 namespace {
 
-// The stages' indexes built ONE STAGE AHEAD of the EM loop: an index depends
-// only on the exemplar level and the stage's configuration, never on the
-// output, so stage k + 1's PCA fit / projection / tree build (many small
-// kernels and host synchronisations, or the host replica of KmTree::build)
-// runs in a worker thread on a second context (own stream, own cuBLAS /
-// cuSOLVER handles) while stage k's EM iterations saturate the GPU from the
-// caller's stream.  Results do not depend on the overlap; PERSYN_NO_BUILD_AHEAD
+// The stages' indexes built AHEAD of the EM loop: an index depends only on
+// the exemplar level and the stage's configuration, never on the output, so
+// the next stages' PCA fits / projections / tree builds (many small kernels
+// and host synchronisations, or the host replica of KmTree::build) run in up
+// to three worker threads, each on its own context (own stream, own cuBLAS /
+// cuSOLVER handles), while the current stage's EM iterations saturate the GPU
+// from the caller's stream.  Results do not depend on the overlap; PERSYN_NO_BUILD_AHEAD
 // builds each index inline on the caller's context.
 class IndexAhead {
  public:
   using Build = std::function<std::unique_ptr<psg_index>(psg_ctx*)>;
+  static constexpr int kWorkers = 3;  // stages in flight ahead of the EM loop
   IndexAhead(psg_ctx* main, std::vector<Build> jobs) : main_(main), jobs_(std::move(jobs)) {
     done_.resize(jobs_.size());
     if (main_->knobs.no_build_ahead || jobs_.size() < 2) return;
-    if (!main_->builder) {
+    const int nw = (int)std::min<size_t>(kWorkers, jobs_.size());
+    while ((int)main_->builders.size() < nw) {
       psg_ctx* b = nullptr;
       if (psg_ctx_create(main_->device, nullptr, &b) != PSG_OK)
-        fail(PSG_E_CUDA, "cannot create the index builder context: " + g_last_error);
-      main_->builder = b;
+        fail(PSG_E_CUDA, "cannot create an index builder context: " + g_last_error);
+      main_->builders.push_back(b);
     }
-    worker_ = std::thread([this] { run(); });
+    for (int i = 0; i < nw; ++i) workers_.emplace_back([this, i, nw] { run(i, nw); });
   }
   ~IndexAhead() {
-    if (worker_.joinable()) {
-      {
-        std::lock_guard<std::mutex> lk(m_);
-        stop_ = true;
-      }
-      cv_.notify_all();
-      worker_.join();
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      stop_ = true;
     }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
   }
   // index of stage k (stages are taken in order); ms = its build time
   std::unique_ptr<psg_index> take(size_t k, double* ms) {
-    if (!worker_.joinable()) {
+    if (workers_.empty()) {
       const double t = now_ms();
       auto ix = jobs_[k](main_);
       *ms = now_ms() - t;
@@ -1943,14 +1943,16 @@ class IndexAhead {
     std::exception_ptr err;
     bool ready = false;
   };
-  void run() {
+  // worker i builds stages i, i + nw, ... on its own context, never more than
+  // nw stages ahead of the stage the EM loop has taken
+  void run(int i, int nw) {
     cudaSetDevice(main_->device);
-    psg_ctx* b = main_->builder;
+    psg_ctx* b = main_->builders[(size_t)i];
     StreamScope ss(b->stream);
-    for (size_t k = 0; k < jobs_.size(); ++k) {
+    for (size_t k = (size_t)i; k < jobs_.size(); k += (size_t)nw) {
       {
         std::unique_lock<std::mutex> lk(m_);
-        cv_.wait(lk, [&] { return stop_ || k <= taken_; });  // at most one stage ahead
+        cv_.wait(lk, [&] { return stop_ || k < taken_ + (size_t)nw; });
         if (stop_) return;
       }
       Slot s;
@@ -1975,7 +1977,7 @@ class IndexAhead {
   psg_ctx* main_;
   std::vector<Build> jobs_;
   std::vector<Slot> done_;
-  std::thread worker_;
+  std::vector<std::thread> workers_;
   std::mutex m_;
   std::condition_variable cv_;
   size_t taken_ = 0;
