@@ -381,7 +381,12 @@ typedef struct {
  * Part 1 is the reference's initialize_output (below) with the guidance row
  * ramp (plane 3) as the normalised scale map (bounds [0, 1]); each level l > 0
  * starts from upsample_bilinear(x2) + fit_to of the previous level's RGB with
- * the level's guidance re-imposed (pipeline.cpp:269-274). */
+ * the level's guidance re-imposed (pipeline.cpp:269-274).
+ * Threads: the stages' indexes are built ahead of the EM loop by up to three
+ * worker threads of this call, each on a context owned by `ctx` (created on
+ * first use, destroyed with it); they are joined before the call returns.
+ * index_millis is a stage's own build time (stages overlap, so the sum may
+ * exceed the wall time).  Results do not depend on the overlap. */
 psg_status psg_synthesize(psg_ctx* ctx, const psg_request* req, double* out_planes,
                           psg_report* report);
 
