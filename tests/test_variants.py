@@ -72,7 +72,8 @@ def test_budget_kernels_agree(gpu_ctx, port, monkeypatch, m):
 
 
 @pytest.mark.parametrize("d,b,m,depth", [(12, 4, 4, 2), (32, 8, 4, 4), (40, 8, 16, 4),
-                                         (56, 16, 6, 3), (32, 8, 40, 4), (24, 2, 30, 9)])
+                                         (56, 16, 6, 3), (32, 8, 40, 4), (24, 2, 30, 9),
+                                         (13, 3, 5, 5), (64, 8, 4, 4), (25, 5, 7, 4), (1, 4, 4, 3)])
 def test_backtrack_lane_group_kernel_equals_warp_kernel(gpu_ctx, port, monkeypatch, d, b, m,
                                                         depth):
     """backtrack(m > 2): the lane-group kernel (8 / 16 lanes per query, rows from
