@@ -46,6 +46,23 @@ def test_loopback_bands_equal_single_device(gpu_ctx, port, world, hist):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("world,budget", [(2, "bt4"), (3, "greedy"), (3, "bt4")])
+def test_loopback_bands_budget_searches_equal_single_device(gpu_ctx, port, world, budget):
+    """Row bands with the reference's default budget: the bands' lane-group
+    searches (tensor-core projection + band checks, per band) reproduce the
+    single-device assignments bit for bit."""
+    ex, init, mean, basis, cfg = _case(port)
+    cfg.budget = api.QueryBudget.backtrack(4) if budget == "bt4" else api.QueryBudget.greedy()
+    ix = api.make_pca_tree_index(ex, 8, mean=mean, basis=basis, branching=8, seed=5,
+                                 tree_kind=api.TREE_REFERENCE, hist_bins=16, ctx=gpu_ctx)
+    ref, st_ref = api.optimize_level(init, ix, cfg)
+    out, st = api.optimize_level_loopback(init, ix, cfg, world)
+    assert np.array_equal(out, ref)
+    assert [s.changed for s in st] == [s.changed for s in st_ref]
+    assert [s.nn_calls for s in st] == [s.nn_calls for s in st_ref]
+
+
+@pytest.mark.gpu
 def test_nccl_world1_band_equals_single_device(gpu_ctx, port):
     """A real NCCL communicator (world 1: the exchanges degenerate, the
     collectives still run) through psg_optimize_level_sharded and the
