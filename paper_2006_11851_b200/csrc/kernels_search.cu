@@ -482,7 +482,10 @@ void launch_project_vectors(psg_ctx* ctx, const float* X, int64_t n, int D, cons
 // ----------------------------------------------------------------------------
 // Tree search: one warp per query (persistent grid-stride over queries).
 constexpr int kSearchWarps = 4;
-constexpr int kStack = 512;   // warp-per-query kernel (deep imported trees, backtrack frontier)
+#ifndef PSG_KSTACK
+#define PSG_KSTACK 512
+#endif
+constexpr int kStack = PSG_KSTACK;  // warp-per-query kernel (deep imported trees, backtrack frontier; spills to global scratch)
 constexpr int kStackX = 256;  // search_exact_kernel
 constexpr int kMaxD = kMaxDP;  // the warp kernels; the tile kernel takes d <= 64
 
@@ -838,7 +841,9 @@ __global__ void __launch_bounds__(32 * kSearchWarps) search_kernel(SearchArgs a)
       // node id); frontier kept as an unsorted pool, min found by the warp.
       // The node id of the tie-break is the tree's tie id (the reference's
       // post-order id for an imported tree, km_tree.cpp:159,187-188).
-      int size = 1;
+      int size = 1, cap = kStack;
+      sn = st_node[warp];  // (a previous query may have moved its frontier to the global scratch)
+      sk = st_key[warp];
       if (lane == 0) {
         sn[0] = 0;
         sk[0] = 0.0;
@@ -885,9 +890,26 @@ __global__ void __launch_bounds__(32 * kSearchWarps) search_kernel(SearchArgs a)
           ++leaves;
         } else {
           const int fc = a.tree.first_child[node];
-          if (size + nc > kStack) {
-            if (lane == 0) atomicOr(a.flags, FLAG_STACK_OVERFLOW);
-            break;
+          if (size + nc > cap) {
+            // frontier past the shared-memory pool: move it to this warp's
+            // global scratch (the reference's priority queue is unbounded,
+            // km_tree.cpp:206-208) and go on there
+            if (cap == kStack && a.deep_key && size + nc <= a.deep_cap) {
+              const int64_t w0 = ((int64_t)blockIdx.x * kSearchWarps + warp) * a.deep_cap;
+              double* gk = a.deep_key + w0;
+              int32_t* gn = a.deep_node + w0;
+              for (int s = lane; s < size; s += 32) {
+                gk[s] = sk[s];
+                gn[s] = sn[s];
+              }
+              __syncwarp();
+              sk = gk;
+              sn = gn;
+              cap = a.deep_cap;
+            } else {
+              if (lane == 0) atomicOr(a.flags, FLAG_STACK_OVERFLOW);
+              break;
+            }
           }
           for (int cb = 0; cb < nc; cb += 32) {
             const int c = cb + lane;
@@ -1102,6 +1124,8 @@ __global__ void __launch_bounds__(32 * kBtWarps) search_backtrack_kernel(SearchA
 #define PSG_BG_MINB 4
 #endif
 constexpr int kBgWarps = 4, kBgCap = PSG_BG_CAP;
+// 16-lane groups (branching 9..16): a frontier grows by up to 15 per expansion
+constexpr int kBgCap16 = 224;
 
 //
 // Approximate queries (AP, tensor-core projection): a.q holds q^ with
@@ -2132,6 +2156,20 @@ bool search_uses_groups(psg_ctx* ctx, const Index& ix, const psg_budget& budget)
 // (see search_backtrack_group_kernel; uncertain queries go to a.amb_list and
 // nothing overflows).  a.nq_dev set: a device-counted list of exact queries
 // whose results go through a.out_map.
+// Global scratch of the deep-stack kernel's frontiers (one region per warp of
+// its num_sms x kSearchWarps grid), allocated once per context on first use.
+constexpr int kDeepCap = 16384;
+static void deep_scratch(psg_ctx* ctx, SearchArgs& b) {
+  const size_t warps = (size_t)ctx->num_sms * kSearchWarps;
+  if (!ctx->deep_key) {
+    PSG_CUDA(cudaMalloc(&ctx->deep_key, sizeof(double) * warps * kDeepCap));
+    PSG_CUDA(cudaMalloc(&ctx->deep_node, sizeof(int32_t) * warps * kDeepCap));
+  }
+  b.deep_key = ctx->deep_key;
+  b.deep_node = ctx->deep_node;
+  b.deep_cap = kDeepCap;
+}
+
 static void launch_backtrack(psg_ctx* ctx, const SearchArgs& a) {
   DBuf<int32_t> ovf;
   DBuf<int> ovf_n;
@@ -2159,10 +2197,10 @@ static void launch_backtrack(psg_ctx* ctx, const SearchArgs& a) {
 #define PSG_BG_LAUNCH2(DPV, GV)                                                                  \
   do {                                                                                           \
     if (a.qdelta)                                                                                \
-      search_backtrack_group_kernel<DPV, GV, kBgCap, true>                                       \
+      search_backtrack_group_kernel<DPV, GV, (GV == 8 ? kBgCap : kBgCap16), true>                \
           <<<(int)blocks, blk, 0, ctx->stream>>>(b);                                             \
     else                                                                                         \
-      search_backtrack_group_kernel<DPV, GV, kBgCap, false>                                      \
+      search_backtrack_group_kernel<DPV, GV, (GV == 8 ? kBgCap : kBgCap16), false>               \
           <<<(int)blocks, blk, 0, ctx->stream>>>(b);                                             \
   } while (0)
 #define PSG_BG_LAUNCH(DPV)                \
@@ -2189,6 +2227,7 @@ static void launch_backtrack(psg_ctx* ctx, const SearchArgs& a) {
   PSG_LAUNCHED(ctx);
   if (a.qdelta) return;  // uncertain / overflowing queries are on the caller's list
   b.nq_dev = nullptr;
+  deep_scratch(ctx, b);
   search_kernel<<<ctx->num_sms, 32 * kSearchWarps, 0, ctx->stream>>>(b);
   PSG_LAUNCHED(ctx);
 }
@@ -2292,6 +2331,10 @@ void launch_search(psg_ctx* ctx, const SearchArgs& a) {
   SearchArgs c = a;  // all queries (not the overflow-list mode)
   c.ovf_list = nullptr;
   c.ovf_count = nullptr;
+  if (c.mode == PSG_BACKTRACK) {  // frontiers may outgrow shared memory: one scratch region per warp
+    if (blocks > ctx->num_sms) blocks = ctx->num_sms;
+    deep_scratch(ctx, c);
+  }
   search_kernel<<<(int)blocks, 32 * kSearchWarps, 0, ctx->stream>>>(c);
   PSG_LAUNCHED(ctx);
 }

@@ -156,6 +156,8 @@ extern const char* const kKernelNames[K_COUNT];
 }  // namespace psg
 
 struct psg_ctx {
+  double* deep_key = nullptr;   // frontier scratch of the deep-stack backtrack kernel (lazy)
+  int32_t* deep_node = nullptr;
   std::vector<psg_ctx*> builders;  // contexts of psg_synthesize's index build-ahead threads (owned)
   // per-kernel event timing (psg_ctx_profile)
   bool profile = false;
@@ -402,6 +404,9 @@ struct SearchArgs {
   const int* nq_dev = nullptr;  // optional: query count read on the device
   const int32_t* out_map = nullptr;  // optional (warp kernel): query -> output slot, counters add
   int32_t* ovf_list = nullptr;       // backtrack: queries whose frontier outgrew the pool (re-run)
+  double* deep_key = nullptr;        // deep-stack kernel: per-warp global frontier scratch
+  int32_t* deep_node = nullptr;
+  int deep_cap = 0;
   int* ovf_count = nullptr;
 };
 // Tile permutation for the next exact search of the same anchors: descending

@@ -1309,6 +1309,8 @@ void psg_ctx_destroy(psg_ctx* ctx) {
   if (ctx->cublas) cublasDestroy(static_cast<cublasHandle_t>(ctx->cublas));
   if (ctx->cusolver) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(ctx->cusolver));
   cudaFree(ctx->d_flags);
+  if (ctx->deep_key) cudaFree(ctx->deep_key);
+  if (ctx->deep_node) cudaFree(ctx->deep_node);
   cudaFree(ctx->d_sched);
   for (void* b : ctx->pinned_blocks) cudaFreeHost(b);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -1933,6 +1935,10 @@ class IndexAhead {
     cv_.wait(lk, [&] { return done_[k].ready; });
     if (done_[k].err) std::rethrow_exception(done_[k].err);
     *ms = done_[k].ms;
+    // the builder's stream is idle for this index: from here on it belongs to
+    // the caller's context, whose stream orders its (stream-ordered) frees
+    // after every kernel that reads it -- also when an exception unwinds
+    done_[k].index->impl.ctx = main_;
     return std::move(done_[k].index);
   }
 

@@ -155,6 +155,33 @@ def test_reference_tree_kind_equals_reference_tree(gpu_ctx, port, ref, b, seed, 
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("b,m", [(16, 400), (8, 250)])
+def test_wide_frontiers_spill_past_shared_memory(gpu_ctx, port, ref, b, m):
+    """backtrack(m) with hundreds of leaves on a wide tree: the frontier (one
+    entry per child of every expanded node) outgrows the lane-group pool AND the
+    deep-stack kernel's shared-memory pool (512 entries), and continues in the
+    warp's global scratch -- the reference's priority queue is unbounded
+    (km_tree.cpp:206-208).  Same answers and scan counts as KmTree::query."""
+    ex = wl.rgbs_planes(wl.sinusoid_exemplar(72, 8, 2.0, 9), 1)
+    init = wl.init_output(ex, 40, 40, 1, 9)
+    cand = port.extract_all(ex, 8, 1)
+    mean, basis, _ = fit_pca(cand, d_fixed=10)
+    h, sj, leaves = _ref_tree(ref, ex, 8, mean, basis, b, 5)
+    assert len(leaves) > m  # the budget, not the tree, ends the walk
+    ix = api.make_pca_tree_index(ex, 8, mean=mean, basis=basis, branching=b, seed=5,
+                                 tree_kind=api.TREE_REFERENCE, ctx=gpu_ctx)
+    rng = np.random.default_rng(b)
+    Q = port.extract_all(init, 8, 1)[rng.choice(33 * 33, 40, replace=False)]
+    idx, dist, _, scanned = ix.nearest(Q, api.QueryBudget.backtrack(m))
+    for i in range(Q.shape[0]):
+        ri, rd, rs = h.nearest(Q[i], mode="backtrack", max_leaves=m)
+        assert (idx[i], dist[i], scanned[i]) == (ri, rd, rs), i
+    i2, d2, _, _ = api.search_step(init, ix, 2, 2, api.QueryBudget.backtrack(m))
+    i_r, d_r, _, _ = h.search_step(init, 8, 2, 2, mode="backtrack", max_leaves=m)
+    assert np.array_equal(i2, i_r) and np.array_equal(d2, d_r)
+
+
+@pytest.mark.gpu
 def test_reference_tree_kind_rejects_depth_cap(gpu_ctx, port):
     ex, _ = _stage(size=24)
     cand = port.extract_all(ex, 8, 1)
