@@ -1141,10 +1141,10 @@ constexpr int kBgCap16 = 224;
 // decision inside its band (or whose frontier outgrows the pool) is listed in
 // a.amb_list and re-run with its exact projection (AP = false, device-counted
 // list, results written through a.out_map).
-template <int DP, int G, int CAP, bool AP>
-__global__ void __launch_bounds__(32 * kBgWarps, (DP <= 32 ? PSG_BG_MINB : 2))
+template <int DP, int G, int CAP, bool AP, int WARPS>
+__global__ void __launch_bounds__(32 * WARPS, (DP <= 32 && WARPS == kBgWarps ? PSG_BG_MINB : 2))
 search_backtrack_group_kernel(SearchArgs a) {
-  constexpr int QPW = 32 / G, QPC = kBgWarps * QPW;
+  constexpr int QPW = 32 / G, QPC = WARPS * QPW;
   constexpr int QS = DP + 4;  // q rows 32 bytes apart modulo the banks: the groups' 16-byte reads spread
   __shared__ __align__(16) double qs_all[QPC][QS];
   __shared__ double pk_all[QPC][CAP];
@@ -1172,8 +1172,9 @@ search_backtrack_group_kernel(SearchArgs a) {
     return (k + dl2 * (2.0 * s + dl2)) * (1.0 + 1e-11);
   };
   for (int64_t q0 = (int64_t)blockIdx.x * QPC; q0 < nq; q0 += (int64_t)gridDim.x * QPC) {
-    const int64_t q = q0 + slot;
-    const bool live = q < nq;
+    const bool live = q0 + slot < nq;
+    // listed queries (the pool overflows of a previous pass): item -> query id
+    const int64_t q = !live ? 0 : (a.q_list ? (int64_t)a.q_list[q0 + slot] : q0 + slot);
     for (int j = l; j < DP; j += G) qs[j] = (live && j < d) ? a.q[q * d + j] : 0.0;
     if (l == 0) {
       pk[0] = 0.0;
@@ -1186,15 +1187,16 @@ search_backtrack_group_kernel(SearchArgs a) {
     int32_t best_id = 0x7fffffff;
     int32_t scanned = 0, visited = 0;
     int size = live ? 1 : 0, leaves = 0;
-    bool overflow = false;  // AP: also "a decision fell inside the band"
+    bool overflow = false;  // the frontier outgrew the pool
+    bool ambig = false;     // AP: a decision fell inside the band
     double dl2 = 0.0;       // 2 delta (slightly inflated)
     if (AP && live) {
       const float dl = a.qdelta[q];
-      if (!(dl < 3.0e38f)) overflow = true;  // no bound for this query: exact re-run
+      if (!(dl < 3.0e38f)) ambig = true;  // no bound for this query: exact re-run
       dl2 = 2.0 * (double)dl * (1.0 + 1e-6);
     }
     for (;;) {
-      const bool act = size > 0 && leaves < max_leaves && !overflow;
+      const bool act = size > 0 && leaves < max_leaves && !overflow && !ambig;
       if (!__any_sync(kFull, act)) break;
       // ---- pop the lexicographic minimum (key, tie) of the group's pool ----
       double bk = kInf;
@@ -1249,7 +1251,7 @@ search_backtrack_group_kernel(SearchArgs a) {
         cnt = 0;
       }
       if (AP && act && !(k2 > __double2hiint(band_top(bk, dl2)))) {
-        overflow = true;  // the pop order is not certain: exact re-run
+        ambig = true;  // the pop order is not certain: exact re-run
         cnt = 0;
       }
       // idle groups / lanes read row 0 of a one-row block (always valid)
@@ -1315,7 +1317,7 @@ search_backtrack_group_kernel(SearchArgs a) {
           }
         }
       }
-      if (act && !overflow) {
+      if (act && !overflow && !ambig) {
         if (leaf) {
           scanned += cnt;
           ++leaves;
@@ -1325,16 +1327,19 @@ search_backtrack_group_kernel(SearchArgs a) {
       }
       __syncwarp();
     }
-    if (AP && live && !overflow && !(second > __double2hiint(band_top(best, dl2)))) overflow = true;
+    if (AP && live && !overflow && !ambig && !(second > __double2hiint(band_top(best, dl2))))
+      ambig = true;
     if (live && l == 0) {
-      if (overflow) {
+      if (overflow && a.ovf_list) {  // next pass: the larger pool, then the deep stack
+        a.ovf_list[atomicAdd(a.ovf_count, 1)] = (int32_t)q;
+      } else if (overflow || ambig) {
         if (AP) {
           const int s = atomicAdd(a.amb_count, 1);
           a.amb_list[s] = (int32_t)q;
           a.amb_c0[s] = 0;
           a.amb_c1[s] = -1;  // resolve: exact projection only, then the re-run
         } else {
-          a.ovf_list[atomicAdd(a.ovf_count, 1)] = (int32_t)q;
+          atomicOr(a.flags, FLAG_STACK_OVERFLOW);  // no list to hand the query to
         }
       } else {
         const int64_t o = a.out_map ? (int64_t)a.out_map[q] : q;
@@ -2187,34 +2192,66 @@ static void launch_backtrack(psg_ctx* ctx, const SearchArgs& a) {
   const bool groups = b.proj_leaf_il && a.tree.centroid_il && mc <= 16 && !ctx->knobs.bt_warp;
   if (!groups && (a.qdelta || a.nq_dev || a.out_map))
     fail(PSG_E_LOGIC, "approximate / listed backtrack queries need the lane-group kernel");
+  DBuf<int32_t> ovf2;
+  DBuf<int> ovf2_n;
   if (groups) {
-    // a group of 8 (16) lanes per query: 16 (8) queries per CTA
+    // a group of 8 (16) lanes per query: 16 (8) queries per 4-warp CTA with a
+    // pool of 96 (224) entries.  8-lane groups whose frontier outgrows the 96
+    // (budgets past ~8 leaves, deep trees) are listed and re-run by a second
+    // pass with the 224-entry pool in 2-warp CTAs (static shared memory stays
+    // below 48 KB); what outgrows that goes to the deep-stack kernel.
+    const dim3 blk(32 * kBgWarps), blk2(64);
+#define PSG_BG_LAUNCH3(DPV, GV, CAPV, WV, GRID, BLK, ARGS)                                       \
+  do {                                                                                           \
+    if ((ARGS).qdelta)                                                                           \
+      search_backtrack_group_kernel<DPV, GV, CAPV, true, WV>                                     \
+          <<<(int)(GRID), BLK, 0, ctx->stream>>>(ARGS);                                          \
+    else                                                                                         \
+      search_backtrack_group_kernel<DPV, GV, CAPV, false, WV>                                    \
+          <<<(int)(GRID), BLK, 0, ctx->stream>>>(ARGS);                                          \
+  } while (0)
+#define PSG_BG_LAUNCH(DPV)                                                          \
+  do {                                                                              \
+    if (mc > 8) {                                                                   \
+      PSG_BG_LAUNCH3(DPV, 16, kBgCap16, kBgWarps, blocks, blk, b);                  \
+    } else {                                                                        \
+      PSG_BG_LAUNCH3(DPV, 8, kBgCap, kBgWarps, blocks, blk, b);                     \
+      PSG_LAUNCHED(ctx);                                                            \
+      PSG_BG_LAUNCH3(DPV, 8, kBgCap16, 2, blocks2, blk2, b2);                       \
+    }                                                                               \
+  } while (0)
     const int qpc = kBgWarps * (mc <= 8 ? 4 : 2);
     int64_t blocks = (a.nq + qpc - 1) / qpc;
     const int64_t cap = a.nq_dev ? (int64_t)ctx->num_sms : (int64_t)ctx->num_sms * 16;
     if (blocks > cap) blocks = cap;
-    const dim3 blk(32 * kBgWarps);
-#define PSG_BG_LAUNCH2(DPV, GV)                                                                  \
-  do {                                                                                           \
-    if (a.qdelta)                                                                                \
-      search_backtrack_group_kernel<DPV, GV, (GV == 8 ? kBgCap : kBgCap16), true>                \
-          <<<(int)blocks, blk, 0, ctx->stream>>>(b);                                             \
-    else                                                                                         \
-      search_backtrack_group_kernel<DPV, GV, (GV == 8 ? kBgCap : kBgCap16), false>               \
-          <<<(int)blocks, blk, 0, ctx->stream>>>(b);                                             \
-  } while (0)
-#define PSG_BG_LAUNCH(DPV)                \
-  do {                                    \
-    if (mc <= 8) PSG_BG_LAUNCH2(DPV, 8);  \
-    else PSG_BG_LAUNCH2(DPV, 16);         \
-  } while (0)
+    // second pass over the first pass's overflow list (device-counted)
+    SearchArgs b2 = b;
+    int64_t blocks2 = std::min<int64_t>((a.nq + 7) / 8, a.nq_dev ? ctx->num_sms : ctx->num_sms * 8);
+    if (mc <= 8) {
+      ovf2.alloc((size_t)a.nq);
+      ovf2_n.alloc(1);
+      PSG_CUDA(cudaMemsetAsync(ovf2_n.p, 0, sizeof(int), ctx->stream));
+      b2.q_list = b.ovf_list;
+      b2.nq_dev = b.ovf_count;
+      // approximate queries: what outgrows the large pool too joins the
+      // uncertain queries' list (exact re-run); exact ones go to the deep stack
+      b2.ovf_list = a.qdelta ? nullptr : ovf2.p;
+      b2.ovf_count = a.qdelta ? nullptr : ovf2_n.p;
+    } else if (a.qdelta) {
+      b.ovf_list = nullptr;  // 16-lane groups, approximate: overflows join the uncertain list
+      b.ovf_count = nullptr;
+    }
     // the blocks' width = the index's fp32 layout class (upload_tree)
     if (a.d <= 24) PSG_BG_LAUNCH(24);
     else if (a.d <= 32) PSG_BG_LAUNCH(32);
     else if (a.d <= 48) PSG_BG_LAUNCH(48);
     else PSG_BG_LAUNCH(64);
 #undef PSG_BG_LAUNCH
-#undef PSG_BG_LAUNCH2
+#undef PSG_BG_LAUNCH3
+    if (mc <= 8 && !a.qdelta) {  // the deep-stack kernel takes the second pass's list
+      b.ovf_list = ovf2.p;
+      b.ovf_count = ovf2_n.p;
+    }
   } else {
     int64_t blocks = (a.nq + kBtWarps - 1) / kBtWarps;
     const int64_t cap = (int64_t)ctx->num_sms * 16;

@@ -404,6 +404,7 @@ struct SearchArgs {
   const int* nq_dev = nullptr;  // optional: query count read on the device
   const int32_t* out_map = nullptr;  // optional (warp kernel): query -> output slot, counters add
   int32_t* ovf_list = nullptr;       // backtrack: queries whose frontier outgrew the pool (re-run)
+  const int32_t* q_list = nullptr;   // lane-group kernel: work item -> query id (a listed pass)
   double* deep_key = nullptr;        // deep-stack kernel: per-warp global frontier scratch
   int32_t* deep_node = nullptr;
   int deep_cap = 0;
