@@ -2164,12 +2164,15 @@ bool search_uses_groups(psg_ctx* ctx, const Index& ix, const psg_budget& budget)
 // Global scratch of the deep-stack kernel's frontiers (one region per warp of
 // its num_sms x kSearchWarps grid), allocated once per context on first use.
 constexpr int kDeepCap = 16384;
-static void deep_scratch(psg_ctx* ctx, SearchArgs& b) {
+void ensure_deep_scratch(psg_ctx* ctx) {
   const size_t warps = (size_t)ctx->num_sms * kSearchWarps;
   if (!ctx->deep_key) {
     PSG_CUDA(cudaMalloc(&ctx->deep_key, sizeof(double) * warps * kDeepCap));
     PSG_CUDA(cudaMalloc(&ctx->deep_node, sizeof(int32_t) * warps * kDeepCap));
   }
+}
+static void deep_scratch(psg_ctx* ctx, SearchArgs& b) {
+  ensure_deep_scratch(ctx);
   b.deep_key = ctx->deep_key;
   b.deep_node = ctx->deep_node;
   b.deep_cap = kDeepCap;
@@ -2227,16 +2230,24 @@ static void launch_backtrack(psg_ctx* ctx, const SearchArgs& a) {
     // second pass over the first pass's overflow list (device-counted)
     SearchArgs b2 = b;
     int64_t blocks2 = std::min<int64_t>((a.nq + 7) / 8, a.nq_dev ? ctx->num_sms : ctx->num_sms * 8);
+    int32_t* l2 = a.ovf2_list;
+    int* n2 = a.ovf2_count;
     if (mc <= 8) {
-      ovf2.alloc((size_t)a.nq);
-      ovf2_n.alloc(1);
-      PSG_CUDA(cudaMemsetAsync(ovf2_n.p, 0, sizeof(int), ctx->stream));
+      if (!a.qdelta) {
+        if (!l2 || !n2) {  // (levels provide these buffers)
+          ovf2.alloc((size_t)a.nq);
+          ovf2_n.alloc(1);
+          l2 = ovf2.p;
+          n2 = ovf2_n.p;
+        }
+        PSG_CUDA(cudaMemsetAsync(n2, 0, sizeof(int), ctx->stream));
+      }
       b2.q_list = b.ovf_list;
       b2.nq_dev = b.ovf_count;
       // approximate queries: what outgrows the large pool too joins the
       // uncertain queries' list (exact re-run); exact ones go to the deep stack
-      b2.ovf_list = a.qdelta ? nullptr : ovf2.p;
-      b2.ovf_count = a.qdelta ? nullptr : ovf2_n.p;
+      b2.ovf_list = a.qdelta ? nullptr : l2;
+      b2.ovf_count = a.qdelta ? nullptr : n2;
     } else if (a.qdelta) {
       b.ovf_list = nullptr;  // 16-lane groups, approximate: overflows join the uncertain list
       b.ovf_count = nullptr;
@@ -2249,8 +2260,8 @@ static void launch_backtrack(psg_ctx* ctx, const SearchArgs& a) {
 #undef PSG_BG_LAUNCH
 #undef PSG_BG_LAUNCH3
     if (mc <= 8 && !a.qdelta) {  // the deep-stack kernel takes the second pass's list
-      b.ovf_list = ovf2.p;
-      b.ovf_count = ovf2_n.p;
+      b.ovf_list = l2;
+      b.ovf_count = n2;
     }
   } else {
     int64_t blocks = (a.nq + kBtWarps - 1) / kBtWarps;

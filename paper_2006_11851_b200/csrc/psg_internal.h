@@ -404,6 +404,8 @@ struct SearchArgs {
   const int* nq_dev = nullptr;  // optional: query count read on the device
   const int32_t* out_map = nullptr;  // optional (warp kernel): query -> output slot, counters add
   int32_t* ovf_list = nullptr;       // backtrack: queries whose frontier outgrew the pool (re-run)
+  int32_t* ovf2_list = nullptr;      // optional: the second (large-pool) pass's overflow list
+  int* ovf2_count = nullptr;
   const int32_t* q_list = nullptr;   // lane-group kernel: work item -> query id (a listed pass)
   double* deep_key = nullptr;        // deep-stack kernel: per-warp global frontier scratch
   int32_t* deep_node = nullptr;
@@ -424,6 +426,8 @@ void launch_brute_search(psg_ctx* ctx, const Index& ix, const RowSrc& qsrc, int6
                          const int32_t* seed, int32_t* out_idx, double* out_d2,
                          int64_t* out_scanned, int64_t* out_exact);
 void launch_search(psg_ctx* ctx, const SearchArgs& a);
+// allocates the deep-stack backtrack kernel's global frontier scratch (once per context)
+void ensure_deep_scratch(psg_ctx* ctx);
 // true when an exact search of this tree runs on the tile kernel
 // nq >= 0: an image search of nq anchors (few anchors -> warp-per-query kernel)
 bool search_uses_tiles(psg_ctx* ctx, const DevTree& tree, int d, bool exact, int64_t nq = -1);

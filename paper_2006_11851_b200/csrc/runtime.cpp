@@ -474,6 +474,8 @@ struct psg_level {
   psg::DBuf<int> resc_n;
   psg::DBuf<int32_t> ovf_list;   // backtrack(m > 2): queries re-run by the deep-stack kernel
   psg::DBuf<int> ovf_n;
+  psg::DBuf<int32_t> ovf2_list;  // ... and the second (large-pool) pass's overflows
+  psg::DBuf<int> ovf2_n;
   // tensor-core projection (kernels_project_tc.cu): digit mirror, per-query
   // error bands, ambiguous-query list and the exact fallback's compact buffers
   psg::DBuf<uint8_t> q8;
@@ -621,9 +623,14 @@ void level_setup_band(psg_level& L, psg_ctx* ctx, const Index& ix, const psg_ban
   L.visited.alloc(L.Ao);
   L.resc_list.alloc(L.Ao);
   L.resc_n.alloc(1);
-  if (cfg.budget.mode == PSG_BACKTRACK) {
+  if (cfg.budget.mode != PSG_EXACT) {
+    // the budget searches' escalation lists and the deep-stack scratch are
+    // set up here, never inside a (possibly captured) iteration
     L.ovf_list.alloc(L.Ao);
     L.ovf_n.alloc(1);
+    L.ovf2_list.alloc(L.Ao);
+    L.ovf2_n.alloc(1);
+    ensure_deep_scratch(ctx);
   }
   L.stats_dev.alloc(8 + 6 * 296);
   L.tile_order.alloc((size_t)image_tile_count(L.Ao, L.nx));
@@ -764,6 +771,8 @@ void level_search(psg_level& L, const int32_t* seed, int32_t* out_idx, double* o
   a.sched = ctx->d_sched;
   a.ovf_list = L.ovf_list.p;
   a.ovf_count = L.ovf_n.p;
+  a.ovf2_list = L.ovf2_list.p;
+  a.ovf2_count = L.ovf2_n.p;
   // unseeded exact search (the priming search of an unconverged image): a
   // greedy descent (one leaf per query) supplies the seeds, whose exact
   // distances start every query's bound (~4% faster priming search on the
