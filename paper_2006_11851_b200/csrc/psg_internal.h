@@ -181,6 +181,7 @@ struct psg_ctx {
   std::vector<double*> pinned_free;
   // side stream for kernels that overlap the critical path (fork / join by events)
   cudaStream_t side = nullptr;
+  cudaStream_t copy = nullptr;  // early download of the final image (psg_optimize_level)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_tile = nullptr;
   int* d_flags = nullptr;
   int64_t* d_sched = nullptr;  // [0..1] search tile scheduler, [2] stats fold ticket
@@ -206,6 +207,7 @@ struct psg_ctx {
     bool bt_warp = false;             // PERSYN_BT_WARP: backtrack(m > 2) warp per query (not lane groups)
     bool bt_thread = false;           // PERSYN_BT_THREAD: greedy / backtrack(m <= 2) thread per query
     bool no_build_ahead = false;      // PERSYN_NO_BUILD_AHEAD: synthesize builds each index inline
+    bool no_early_download = false;   // PERSYN_NO_EARLY_DOWNLOAD: optimize_level downloads the image at the end
     bool bt_exact_projection = false; // PERSYN_BT_EXACT_PROJECTION: fp64 projection for greedy / backtrack
   } knobs;
 };

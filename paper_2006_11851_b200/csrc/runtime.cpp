@@ -498,7 +498,15 @@ struct psg_level {
   double pending_ms = 0.0;
   int64_t unique_queries = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // psg_optimize_level with a pinned result buffer: the image is final after
+  // the LAST iteration's M-step, so its download starts there, on the copy
+  // stream, under that iteration's E-step
+  double* early_host = nullptr;
+  cudaEvent_t ev_early = nullptr;
+  bool early_done = false;
   ~psg_level() {
+    if (early_done && ctx) cudaStreamSynchronize(ctx->copy);  // the copy reads `planes`
+    if (ev_early) cudaEventDestroy(ev_early);
     for (auto& g : graph)
       if (g) cudaGraphExecDestroy(g);
     if (stats_host && ctx) ctx->pinned_free.push_back(stats_host);
@@ -1104,6 +1112,14 @@ void step_body(psg_level& L, bool conc, bool mark) {
   phase_weights(L, conc, mark);
   phase_penalty(L, L.counts.p, conc ? ctx->ev_join : nullptr);
   phase_update(L);
+  if (mark && L.early_host && !L.early_done && L.iter + 1 >= L.cfg.max_iterations) {
+    if (!L.ev_early) PSG_CUDA(cudaEventCreateWithFlags(&L.ev_early, cudaEventDisableTiming));
+    PSG_CUDA(cudaEventRecord(L.ev_early, ctx->stream));
+    PSG_CUDA(cudaStreamWaitEvent(ctx->copy, L.ev_early, 0));
+    PSG_CUDA(cudaMemcpyAsync(L.early_host, L.planes.p, sizeof(double) * (size_t)L.P * L.C,
+                             cudaMemcpyDeviceToHost, ctx->copy));
+    L.early_done = true;
+  }
   phase_search_enqueue(L);
   L.stats_dev.download(ctx, L.stats_host, 6);
   PSG_CUDA(cudaMemcpyAsync(reinterpret_cast<int*>(L.stats_host + 7), ctx->d_flags, sizeof(int),
@@ -1273,6 +1289,7 @@ psg_status psg_ctx_create(int device, void* stream, psg_ctx** out) {
       kn.bt_warp = on("PERSYN_BT_WARP");
       kn.bt_thread = on("PERSYN_BT_THREAD");
       kn.no_build_ahead = on("PERSYN_NO_BUILD_AHEAD");
+      kn.no_early_download = on("PERSYN_NO_EARLY_DOWNLOAD");
       kn.bt_exact_projection = on("PERSYN_BT_EXACT_PROJECTION");
     }
     if (stream) {
@@ -1288,6 +1305,7 @@ psg_status psg_ctx_create(int device, void* stream, psg_ctx** out) {
       PSG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     }
     PSG_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    PSG_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
     for (cudaEvent_t* e : {&c->ev_fork, &c->ev_join, &c->ev_tile})
       PSG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     PSG_CUDA(cudaMalloc(&c->d_flags, sizeof(int)));
@@ -1312,6 +1330,10 @@ void psg_ctx_destroy(psg_ctx* ctx) {
   if (ctx->side) {
     cudaStreamSynchronize(ctx->side);
     cudaStreamDestroy(ctx->side);
+  }
+  if (ctx->copy) {
+    cudaStreamSynchronize(ctx->copy);
+    cudaStreamDestroy(ctx->copy);
   }
   for (cudaEvent_t e : {ctx->ev_fork, ctx->ev_join, ctx->ev_tile})
     if (e) cudaEventDestroy(e);
@@ -1861,10 +1883,22 @@ psg_status psg_optimize_level(psg_ctx* ctx, const psg_index* index, const double
   psg_status s = psg_level_create(ctx, index, init, W, H, cfg, ex_hist, &L);
   if (s != PSG_OK) return s;
   std::unique_ptr<psg_level> hold(L);
+  {  // a pinned (page-locked) result buffer can take the image early, asynchronously
+    cudaPointerAttributes at{};
+    if (out_planes && cudaPointerGetAttributes(&at, out_planes) == cudaSuccess &&
+        at.type == cudaMemoryTypeHost && !ctx->knobs.graph && !ctx->knobs.no_early_download)
+      L->early_host = out_planes;
+    cudaGetLastError();  // (unregistered memory may leave an error state on old drivers)
+  }
   int done = 0;
   s = psg_level_iterate(L, cfg->max_iterations, 1, stats, &done);
   if (s != PSG_OK) return s;
   if (n_iters) *n_iters = done;
+  if (L->early_done)  // the final image is already on its way
+    return guarded([&] {
+      PSG_CUDA(cudaStreamSynchronize(ctx->copy));
+      PSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
   return psg_level_download(L, out_planes, nullptr, nullptr);
 }
 

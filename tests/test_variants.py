@@ -197,3 +197,44 @@ def test_em_scheduling_variants_bit_identical(gpu_ctx, monkeypatch, env):
     for a, b in zip(ref[:3], got[:3]):
         assert np.array_equal(a, b)
     assert ref[3] == got[3]
+
+
+@pytest.mark.parametrize("budget,early_stop", [("exact", False), ("bt4", False), ("exact", True)])
+def test_optimize_level_pinned_result_early_download(gpu_ctx, port, budget, early_stop):
+    """psg_optimize_level with a page-locked result buffer starts the image's
+    download after the last iteration's M-step (copy stream, under that
+    iteration's E-step): same image and statistics as with a pageable buffer --
+    also when convergence ends the loop before the last possible iteration."""
+    import ctypes as ct
+
+    import torch
+
+    from paper_2006_11851_b200 import native as N
+    ex, init = _stage()
+    cand = port.extract_all(ex, 8, 1)
+    mean, basis, _ = fit_pca(cand, d_fixed=16)
+    ix = api.make_pca_tree_index(ex, 8, mean=mean, basis=basis, branching=8, seed=3, hist_bins=16,
+                                 tree_kind=api.TREE_REFERENCE, ctx=gpu_ctx)
+    bud = api.QueryBudget.exact() if budget == "exact" else api.QueryBudget.backtrack(4)
+    n_it = 30 if early_stop else 4
+    cfg = api.OptimizerConfig(max_iterations=n_it, min_iterations=1 if early_stop else n_it,
+                              convergence_fraction=0.05 if early_stop else 1e-9, nbhd_width=8,
+                              spacing=2, patch_width=2, budget=bud)
+    ref_out, ref_st = api.optimize_level(init, ix, cfg)  # pageable result buffer
+    if early_stop:
+        assert len(ref_st) < n_it
+    pin_in = torch.empty(init.shape, dtype=torch.float64, pin_memory=True)
+    pin_in.numpy()[...] = init
+    pin_out = torch.zeros(init.shape, dtype=torch.float64, pin_memory=True)
+    c = cfg.c()
+    st = (N.psg_iter_stats * n_it)()
+    n = ct.c_int()
+    H, W = init.shape[1], init.shape[2]
+    for _ in range(2):  # the context and its copy stream are reused
+        pin_out.zero_()
+        N.check(N.lib.psg_optimize_level(gpu_ctx.h, ix.h, ct.c_void_p(pin_in.data_ptr()), W, H,
+                                         ct.byref(c), None, ct.c_void_p(pin_out.data_ptr()),
+                                         ct.cast(st, ct.c_void_p), ct.byref(n)))
+        assert n.value == len(ref_st)
+        assert np.array_equal(pin_out.numpy(), ref_out)
+        assert [st[i].changed for i in range(n.value)] == [s.changed for s in ref_st]
