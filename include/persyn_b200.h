@@ -195,6 +195,17 @@ typedef struct {
   const int32_t* leaf_ids;
 } psg_tree_import;
 psg_status psg_index_import_tree(psg_ctx* ctx, psg_index* index, const psg_tree_import* tree);
+
+/* The library's replica of KmTree::build (km_tree.cpp:141-195: one
+ * std::mt19937_64 consumed in the recursion's order) over N projected points
+ * proj[N][d], on the HOST (no device needed) -- what tree_kind =
+ * PSG_TREE_REFERENCE builds inside psg_index_create.  Outputs in
+ * psg_tree_import's form: n_children (pre-order, capacity 2N), leaf_sizes
+ * (capacity N), leaf_ids (N).  leaf_threshold <= 0: the branching. */
+psg_status psg_reference_tree_host(const double* proj, int64_t N, int d, int branching,
+                                   int leaf_threshold, uint64_t seed, int32_t* n_children,
+                                   int64_t* n_nodes, int32_t* leaf_sizes, int64_t* n_leaves,
+                                   int32_t* leaf_ids);
 /* Exemplar histogram [slots][bins] (pipeline.cpp:286-292). */
 psg_status psg_index_histograms(const psg_index* index, double* mass);
 /*

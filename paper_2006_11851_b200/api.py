@@ -299,6 +299,22 @@ def make_brute_force_vector_index(X: np.ndarray, *, ctx: Optional[Context] = Non
     return SearchIndex(ctx, h, None)
 
 
+def reference_tree_host(proj: np.ndarray, branching: int, seed: int = 0, leaf_threshold: int = 0):
+    """The library's host replica of KmTree::build (km_tree.cpp:141-195) over
+    projected points [N][d] -- no device needed.  Returns (pre-order child
+    counts, list of the leaves' id arrays in DFS order): psg_tree_import's form."""
+    P = _c(proj, np.float64)
+    n, d = P.shape
+    nc = np.zeros(2 * n, np.int32)
+    ls = np.zeros(n, np.int32)
+    li = np.zeros(n, np.int32)
+    nn, nl = ct.c_int64(), ct.c_int64()
+    N.check(N.lib.psg_reference_tree_host(_p(P), n, d, branching, leaf_threshold, seed, _p(nc),
+                                          ct.byref(nn), _p(ls), ct.byref(nl), _p(li)))
+    sizes = ls[: nl.value]
+    return nc[: nn.value].copy(), np.split(li, np.cumsum(sizes)[:-1])
+
+
 def make_vector_index(X: np.ndarray, variance_target: float = 0.95, branching: int = 8,
                       seed: int = 0, *, mean=None, basis=None, d_fixed: int = 0,
                       max_depth: int = 0, tree_kind: int = TREE_DEVICE,

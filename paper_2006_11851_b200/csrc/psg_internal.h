@@ -570,6 +570,10 @@ void launch_fit_to(psg_ctx* ctx, const double* in, int W, int H, int ow, int oh,
 // ---- host pieces --------------------------------------------------------------
 // KmTree::build replica (tree_kind = PSG_TREE_REFERENCE): the reference's own
 // tree, bit for bit (host, the shared sequential engine; tree_host.cpp).
+// the walk alone: pre-order child counts and the leaves' id lists in DFS order
+void reference_tree_walk(const double* proj, int64_t N, int d, int branching, int leaf_threshold,
+                         uint64_t seed, std::vector<int32_t>& n_children,
+                         std::vector<int32_t>& leaf_sizes, std::vector<int32_t>& leaf_ids);
 HostTree build_reference_tree_host(const double* proj, int64_t N, int d, int branching,
                                    int leaf_threshold, uint64_t seed);
 // Same construction on the device (level-synchronous, deterministic); P is

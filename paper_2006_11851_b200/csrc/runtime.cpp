@@ -1509,6 +1509,23 @@ psg_status psg_index_leaves(const psg_index* index, int32_t* ids, int32_t* sizes
   });
 }
 
+psg_status psg_reference_tree_host(const double* proj, int64_t N, int d, int branching,
+                                   int leaf_threshold, uint64_t seed, int32_t* n_children,
+                                   int64_t* n_nodes, int32_t* leaf_sizes, int64_t* n_leaves,
+                                   int32_t* leaf_ids) {
+  return guarded([&] {
+    if (!proj || !n_children || !n_nodes || !leaf_sizes || !n_leaves || !leaf_ids)
+      fail(PSG_E_DOMAIN, "null argument");
+    std::vector<int32_t> nc, ls, li;
+    psg::reference_tree_walk(proj, N, d, branching, leaf_threshold, seed, nc, ls, li);
+    std::copy(nc.begin(), nc.end(), n_children);
+    std::copy(ls.begin(), ls.end(), leaf_sizes);
+    std::copy(li.begin(), li.end(), leaf_ids);
+    *n_nodes = (int64_t)nc.size();
+    *n_leaves = (int64_t)ls.size();
+  });
+}
+
 psg_status psg_index_import_tree(psg_ctx* ctx, psg_index* index, const psg_tree_import* tree) {
   return guarded([&] {
     psg::StreamScope _ss(ctx ? ctx->stream : nullptr);

@@ -46,8 +46,9 @@ inline double dist2(const double* a, const double* b, int d) {
 // split when >= 2 clusters are non-empty; its children are then built one
 // subtree at a time in cluster order -- the recursion's order, hence the
 // order in which the shared engine is consumed.
-HostTree build_reference_tree_host(const double* P, int64_t N, int d, int branching,
-                                   int leaf_threshold, uint64_t seed) {
+void reference_tree_walk(const double* P, int64_t N, int d, int branching, int leaf_threshold,
+                         uint64_t seed, std::vector<int32_t>& n_children,
+                         std::vector<int32_t>& leaf_sizes, std::vector<int32_t>& leaf_ids) {
   if (N < 1) fail(PSG_E_DOMAIN, "cannot build a tree over zero points");
   if (branching < 2) fail(PSG_E_DOMAIN, "tree branching must be >= 2");
   if (leaf_threshold <= 0) leaf_threshold = branching;
@@ -56,7 +57,9 @@ HostTree build_reference_tree_host(const double* P, int64_t N, int d, int branch
   // the walk itself and every RNG draw stay sequential
   const unsigned hw = std::thread::hardware_concurrency();
   HostPool pool(N >= 4096 ? (int)std::min(16u, std::max(1u, hw)) : 1);
-  std::vector<int32_t> n_children, leaf_sizes, leaf_ids;
+  n_children.clear();
+  leaf_sizes.clear();
+  leaf_ids.clear();
   leaf_ids.reserve((size_t)N);
   std::vector<std::vector<int32_t>> todo(1);
   todo[0].resize((size_t)N);
@@ -77,6 +80,12 @@ HostTree build_reference_tree_host(const double* P, int64_t N, int d, int branch
     leaf_sizes.push_back((int32_t)ids.size());
     leaf_ids.insert(leaf_ids.end(), ids.begin(), ids.end());
   }
+}
+
+HostTree build_reference_tree_host(const double* P, int64_t N, int d, int branching,
+                                   int leaf_threshold, uint64_t seed) {
+  std::vector<int32_t> n_children, leaf_sizes, leaf_ids;
+  reference_tree_walk(P, N, d, branching, leaf_threshold, seed, n_children, leaf_sizes, leaf_ids);
   return import_tree_host(P, N, d, n_children.data(), (int64_t)n_children.size(),
                           leaf_sizes.data(), (int64_t)leaf_sizes.size(), leaf_ids.data());
 }

@@ -117,6 +117,7 @@ _SIGS = {
     "psg_index_leaves": (I, [VP, VP, VP, VP]),
     "psg_index_histograms": (I, [VP, VP]),
     "psg_index_import_tree": (I, [VP, VP, VP]),
+    "psg_reference_tree_host": (I, [VP, I64, I, I, I, ct.c_uint64, VP, VP, VP, VP, VP]),
     "psg_index_create_brute": (I, [VP, VP, I, I, I, I, I, I, PP]),
     "psg_index_create_brute_vectors": (I, [VP, VP, I64, I, PP]),
     "psg_index_query": (I, [VP, VP, VP, I64, psg_budget, VP, VP, VP, VP]),

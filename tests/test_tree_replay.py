@@ -122,6 +122,24 @@ def test_replayed_tree_optimize_level_backtrack4(gpu_ctx, port, ref, hist):
         assert s.points_scanned == r[6]
 
 
+# ---- the host replica of KmTree::build, on the CPU ------------------------------------
+@pytest.mark.parametrize("size,b,seed,d", [(32, 4, 7, 12), (40, 8, 3, 16), (40, 16, 11, 8),
+                                           (80, 8, 5, 24)])
+def test_host_tree_replica_equals_reference_tree_cpu(port, ref, size, b, seed, d):
+    """psg_reference_tree_host (vectorised, threaded k-means; the RNG walk
+    sequential) builds the reference's own KmTree: same pre-order structure,
+    same leaves in the same order.  (80^2 exemplar: 5,329 points -- the thread
+    pool and every vector clone's code path run.)"""
+    ex = wl.rgbs_planes(wl.sinusoid_exemplar(size, 8, 2.0, seed), 1)
+    cand = port.extract_all(ex, 8, 1)
+    mean, basis, _ = fit_pca(cand, d_fixed=d)
+    h, sj, leaves = _ref_tree(ref, ex, 8, mean, basis, b, seed)
+    nc, lv = api.reference_tree_host(port.project_all(cand, mean, basis), b, seed)
+    assert len(lv) == len(leaves)
+    assert all(np.array_equal(a, np.asarray(r)) for a, r in zip(lv, leaves))
+    assert np.array_equal(nc, api.preorder_child_counts(sj))
+
+
 # ---- the library's own replica of KmTree::build (no import) -----------------------------
 @pytest.mark.gpu
 @pytest.mark.parametrize("b,seed,d", [(4, 7, 12), (8, 3, 16), (16, 11, 8)])
